@@ -1,0 +1,401 @@
+"""CPU oracle for the GraphMat superstep path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` /
+``--impl reference`` legs import this package, and only as the checker.  The
+product (``paper_1503_07241_b200``) never imports it.
+
+Two checkers live here:
+
+* ``liboracle.so`` -- our C restatement of the reference algorithms
+  (graphmat_oracle.c; every function cites the reference file:line it follows).
+* ``_ref/libsemigraph_ref.so`` -- the reference's own header-only engine
+  (/root/reference/proj/include/semigraph), compiled by oracle/Makefile from the
+  sources where they lie and driven by ref_driver.cpp.  It pins the restatement.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+_REF = None
+
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+
+
+class Stats(C.Structure):
+    """Mirrors semigraph::IterationStats (include/semigraph/engine.hpp:32-39)."""
+
+    _fields_ = [
+        ("iteration", C.c_int64),
+        ("active_before", C.c_int64),
+        ("messages_generated", C.c_int64),
+        ("vertices_updated", C.c_int64),
+        ("spmv_seconds", C.c_double),
+        ("total_seconds", C.c_double),
+    ]
+
+
+def stats_tuples(arr, count):
+    return [
+        (s.iteration, s.active_before, s.messages_generated, s.vertices_updated)
+        for s in arr[:count]
+    ]
+
+
+def build():
+    """Compile liboracle.so (and oracle/_ref when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def lib():
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = os.path.join(HERE, "liboracle.so")
+    if not os.path.exists(path):
+        build()
+    L = C.CDLL(path)
+    L.or_mix64.restype = C.c_uint64
+    L.or_mix64.argtypes = [C.c_uint64]
+    L.or_permute.restype = C.c_uint32
+    L.or_permute.argtypes = [C.c_uint32, C.c_uint, C.c_uint64]
+    L.or_rmat_generate.restype = C.c_int64
+    L.or_rmat_generate.argtypes = [C.c_uint, C.c_uint, C.c_double, C.c_double, C.c_double,
+                                   C.c_uint64, C.c_int, u32p, u32p]
+    L.or_edge_weights.restype = None
+    L.or_edge_weights.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, u8p]
+    L.or_ratings.restype = None
+    L.or_ratings.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, u8p]
+    L.or_bipartite_generate.restype = C.c_int64
+    L.or_bipartite_generate.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,
+                                        C.c_uint64, C.c_void_p, C.c_void_p]
+    L.or_pick_source.restype = C.c_uint32
+    L.or_pick_source.argtypes = [C.c_uint64, C.c_uint64, u32p]
+    L.or_preprocess.restype = C.c_int64
+    L.or_preprocess.argtypes = [C.c_int64, u32p, u32p, C.c_void_p, C.c_int]
+    L.or_csr_build.restype = None
+    L.or_csr_build.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, C.c_void_p, u64p, u32p,
+                               C.c_void_p]
+    L.or_bfs.restype = C.c_int64
+    L.or_bfs.argtypes = [C.c_uint64, u64p, u32p, C.c_uint32, C.c_int64, i32p,
+                         C.POINTER(Stats), C.c_int64]
+    L.or_sssp.restype = C.c_int64
+    L.or_sssp.argtypes = [C.c_uint64, u64p, u32p, u32p, C.c_uint32, C.c_int64, u32p,
+                          C.POINTER(Stats), C.c_int64]
+    L.or_sssp_f64.restype = C.c_int64
+    L.or_sssp_f64.argtypes = [C.c_uint64, u64p, u32p, f64p, C.c_uint32, C.c_int64, f64p,
+                              C.POINTER(Stats), C.c_int64]
+    L.or_pagerank_norm.restype = None
+    L.or_pagerank_norm.argtypes = [C.c_uint64, u64p, u32p, u32p, C.c_double, C.c_int64,
+                                   f64p, C.POINTER(Stats)]
+    L.or_pagerank_ref.restype = C.c_int64
+    L.or_pagerank_ref.argtypes = [C.c_uint64, u64p, u32p, u32p, C.c_double, C.c_int64, f64p,
+                                  C.POINTER(Stats)]
+    L.or_cf_gd.restype = None
+    L.or_cf_gd.argtypes = [C.c_uint64, u64p, u32p, f64p, u64p, u32p, f64p, C.c_int64,
+                           C.c_double, C.c_double, C.c_int64, f64p, f64p, f64p]
+    L.or_cf_gd_f32.restype = None
+    L.or_cf_gd_f32.argtypes = [C.c_uint64, u64p, u32p, f64p, u64p, u32p, f64p, C.c_int64,
+                               C.c_float, C.c_float, C.c_int64, f32p, f64p]
+    L.or_semiring_spmv.restype = None
+    L.or_semiring_spmv.argtypes = [C.c_uint64, u64p, u32p, i64p, i64p, u8p, i64p, u8p]
+    _LIB = L
+    return L
+
+
+def ref_lib():
+    """The compiled reference engine, or None when oracle/_ref was never built."""
+    global _REF
+    if _REF is not None:
+        return _REF
+    path = os.path.join(HERE, "_ref", "libsemigraph_ref.so")
+    if not os.path.exists(path):
+        return None
+    R = C.CDLL(path)
+    R.ref_last_error.restype = C.c_char_p
+    R.ref_hardware_threads.restype = C.c_int
+    common = [C.c_uint64, C.c_int64, u32p, u32p]
+    sp = [C.POINTER(Stats), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+    R.ref_bfs.argtypes = common + [C.c_uint64, C.c_int64, C.c_uint, f64p] + sp
+    R.ref_sssp.argtypes = common + [f64p, C.c_uint64, C.c_int64, C.c_uint, f64p] + sp
+    R.ref_pagerank.argtypes = common + [C.c_double, C.c_int64, C.c_uint, f64p] + sp
+    R.ref_pagerank_norm.argtypes = common + [C.c_double, C.c_int64, C.c_uint, f64p] + sp
+    R.ref_cf.argtypes = common + [f64p, C.c_int64, C.c_double, C.c_double, C.c_int64,
+                                  C.c_uint, C.c_int, f64p, C.c_void_p, C.c_void_p,
+                                  C.POINTER(C.c_double)]
+    R.ref_semiring_spmv.argtypes = common + [i64p, i64p, u8p, C.c_uint, C.c_uint, i64p, u8p]
+    for f in (R.ref_bfs, R.ref_sssp, R.ref_pagerank, R.ref_pagerank_norm, R.ref_cf,
+              R.ref_semiring_spmv):
+        f.restype = C.c_int
+    _REF = R
+    return R
+
+
+# ---------------------------------------------------------------- helpers
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, permute=True):
+    m = edge_factor << scale
+    src = np.empty(m, np.uint32)
+    dst = np.empty(m, np.uint32)
+    lib().or_rmat_generate(scale, edge_factor, a, b, c, seed, 1 if permute else 0, src, dst)
+    return src, dst
+
+
+def bipartite(users, items, c_numerator, cap, seed):
+    L = lib()
+    m = L.or_bipartite_generate(users, items, c_numerator, cap, seed, None, None)
+    src = np.empty(m, np.uint32)
+    dst = np.empty(m, np.uint32)
+    L.or_bipartite_generate(users, items, c_numerator, cap, seed, src.ctypes.data,
+                            dst.ctypes.data)
+    return src, dst
+
+
+def edge_weights(seed, src, dst):
+    src, dst = _u32(src), _u32(dst)
+    w = np.empty(len(src), np.uint8)
+    lib().or_edge_weights(seed, len(src), src, dst, w)
+    return w
+
+
+def ratings(seed, src, dst):
+    src, dst = _u32(src), _u32(dst)
+    r = np.empty(len(src), np.uint8)
+    lib().or_ratings(seed, len(src), src, dst, r)
+    return r
+
+
+def pick_source(seed, degree):
+    degree = _u32(degree)
+    return int(lib().or_pick_source(seed, len(degree), degree))
+
+
+def preprocess(src, dst, vals=None, symmetrize=False):
+    """src/io.cpp:184-222 -- returns new (src, dst, vals) sorted by (src, dst)."""
+    m = len(src)
+    cap = 2 * m if symmetrize else m
+    s = np.zeros(max(cap, 1), np.uint32)
+    d = np.zeros(max(cap, 1), np.uint32)
+    s[:m] = src
+    d[:m] = dst
+    v = None
+    if vals is not None:
+        v = np.zeros(max(cap, 1), np.float64)
+        v[:m] = vals
+    m2 = lib().or_preprocess(m, s, d, v.ctypes.data if v is not None else None,
+                             1 if symmetrize else 0)
+    return s[:m2].copy(), d[:m2].copy(), (v[:m2].copy() if v is not None else None)
+
+
+def csr(n, row, col, vals=None):
+    row, col = _u32(row), _u32(col)
+    m = len(row)
+    ptr = np.empty(n + 1, np.uint64)
+    idx = np.empty(max(m, 1), np.uint32)
+    ov = None
+    vv = None
+    if vals is not None:
+        vv = np.ascontiguousarray(vals, dtype=np.float64)
+        ov = np.empty(max(m, 1), np.float64)
+    lib().or_csr_build(n, m, row, col, vv.ctypes.data if vv is not None else None, ptr, idx,
+                       ov.ctypes.data if ov is not None else None)
+    return ptr, idx[:m], (ov[:m] if ov is not None else None)
+
+
+def _sorted_by(primary, secondary, *rest):
+    order = np.lexsort((secondary, primary))
+    return [np.ascontiguousarray(a[order]) if a is not None else None
+            for a in (primary, secondary) + rest]
+
+
+def bfs(n, src, dst, root, max_iters=None):
+    """BSP BFS levels (int32, -1 unreached) + per-superstep stats tuples."""
+    s, d = _sorted_by(_u32(src), _u32(dst))
+    ptr, idx, _ = csr(n, s, d)
+    lvl = np.empty(n, np.int32)
+    cap = n + 2
+    st = (Stats * cap)()
+    k = lib().or_bfs(n, ptr, idx, root, max_iters if max_iters is not None else n + 1, lvl,
+                     st, cap)
+    return lvl, stats_tuples(st, k)
+
+
+def sssp(n, src, dst, w, root, max_iters=None):
+    s, d, ww = _sorted_by(_u32(src), _u32(dst), np.asarray(w))
+    ptr, idx, wv = csr(n, s, d, ww.astype(np.float64))
+    dist = np.empty(n, np.uint32)
+    cap = n + 2
+    st = (Stats * cap)()
+    k = lib().or_sssp(n, ptr, idx, np.ascontiguousarray(wv.astype(np.uint32)), root,
+                      max_iters if max_iters is not None else n + 1, dist, st, cap)
+    return dist, stats_tuples(st, k)
+
+
+def sssp_f64(n, src, dst, w, root, max_iters=None):
+    s, d, ww = _sorted_by(_u32(src), _u32(dst), np.asarray(w, np.float64))
+    ptr, idx, wv = csr(n, s, d, ww)
+    dist = np.empty(n, np.float64)
+    cap = n + 2
+    st = (Stats * cap)()
+    k = lib().or_sssp_f64(n, ptr, idx, np.ascontiguousarray(wv), root,
+                          max_iters if max_iters is not None else n + 1, dist, st, cap)
+    return dist, stats_tuples(st, k)
+
+
+def in_csr(n, src, dst, vals=None):
+    """CSR(G^T): rows = destinations, entries = sources ascending."""
+    d, s, v = _sorted_by(_u32(dst), _u32(src), vals)
+    return csr(n, d, s, v)
+
+
+def out_csr(n, src, dst, vals=None):
+    s, d, v = _sorted_by(_u32(src), _u32(dst), vals)
+    return csr(n, s, d, v)
+
+
+def pagerank_norm(n, src, dst, damping=0.85, iters=20):
+    ptr, idx, _ = in_csr(n, src, dst)
+    outdeg = np.bincount(_u32(src), minlength=n).astype(np.uint32)
+    rank = np.empty(n, np.float64)
+    st = (Stats * max(iters, 1))()
+    lib().or_pagerank_norm(n, ptr, idx, outdeg, damping, iters, rank, st)
+    return rank, stats_tuples(st, iters)
+
+
+def pagerank_ref(n, src, dst, r=0.15, iters=20):
+    ptr, idx, _ = in_csr(n, src, dst)
+    outdeg = np.bincount(_u32(src), minlength=n).astype(np.uint32)
+    rank = np.empty(n, np.float64)
+    st = (Stats * max(iters, 1))()
+    k = lib().or_pagerank_ref(n, ptr, idx, outdeg, r, iters, rank, st)
+    return rank, stats_tuples(st, k)
+
+
+def cf_gd(n, src, dst, rating, factors, gamma, lam, iters, fp32=False):
+    """Returns (factors, objective_trace or None, rmse_trace)."""
+    rating = np.asarray(rating, np.float64)
+    tptr, tidx, tval = in_csr(n, src, dst, rating)
+    fptr, fidx, fval = out_csr(n, src, dst, rating)
+    k = factors.shape[1]
+    rm = np.zeros(iters, np.float64)
+    if fp32:
+        f = np.ascontiguousarray(factors, np.float32).copy()
+        lib().or_cf_gd_f32(n, tptr, tidx, tval, fptr, fidx, fval, k, gamma, lam, iters, f, rm)
+        return f, None, rm
+    f = np.ascontiguousarray(factors, np.float64).copy()
+    obj = np.zeros(iters, np.float64)
+    lib().or_cf_gd(n, tptr, tidx, tval, fptr, fidx, fval, k, gamma, lam, iters, f, obj, rm)
+    return f, obj, rm
+
+
+def semiring_spmv(n, src, dst, vals, x, xvalid):
+    ptr, idx, _ = in_csr(n, src, dst)
+    d, s, v = _sorted_by(_u32(dst), _u32(src), np.asarray(vals, np.int64))
+    y = np.empty(n, np.int64)
+    yv = np.empty(n, np.uint8)
+    lib().or_semiring_spmv(n, ptr, idx, np.ascontiguousarray(v, np.int64),
+                           np.ascontiguousarray(x, np.int64),
+                           np.ascontiguousarray(xvalid, np.uint8), y, yv)
+    return y, yv.astype(bool)
+
+
+# ------------------------------------------------- reference (oracle/_ref)
+
+class RefError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def _ref_call(fn, *args):
+    R = ref_lib()
+    rc = fn(*args)
+    if rc != 0:
+        raise RefError(rc, R.ref_last_error().decode())
+
+
+def ref_bfs(n, src, dst, root, threads=0, max_iters=None):
+    R = ref_lib()
+    out = np.empty(n, np.float64)
+    cap = n + 2
+    st = (Stats * cap)()
+    k = C.c_int64()
+    t = C.c_double()
+    _ref_call(R.ref_bfs, n, len(src), _u32(src), _u32(dst), root,
+              max_iters if max_iters is not None else n + 1, threads, out, st, cap,
+              C.byref(k), C.byref(t))
+    return out, stats_tuples(st, k.value), t.value
+
+
+def ref_sssp(n, src, dst, w, root, threads=0, max_iters=None):
+    R = ref_lib()
+    out = np.empty(n, np.float64)
+    cap = n + 2
+    st = (Stats * cap)()
+    k = C.c_int64()
+    t = C.c_double()
+    _ref_call(R.ref_sssp, n, len(src), _u32(src), _u32(dst),
+              np.ascontiguousarray(w, np.float64), root,
+              max_iters if max_iters is not None else n + 1, threads, out, st, cap,
+              C.byref(k), C.byref(t))
+    return out, stats_tuples(st, k.value), t.value
+
+
+def ref_pagerank(n, src, dst, r=0.15, iters=20, threads=0):
+    R = ref_lib()
+    out = np.empty(n, np.float64)
+    st = (Stats * max(iters, 1))()
+    k = C.c_int64()
+    t = C.c_double()
+    _ref_call(R.ref_pagerank, n, len(src), _u32(src), _u32(dst), r, iters, threads, out, st,
+              max(iters, 1), C.byref(k), C.byref(t))
+    return out, stats_tuples(st, k.value), t.value
+
+
+def ref_pagerank_norm(n, src, dst, damping=0.85, iters=20, threads=0):
+    R = ref_lib()
+    out = np.empty(n, np.float64)
+    st = (Stats * max(iters, 1))()
+    k = C.c_int64()
+    t = C.c_double()
+    _ref_call(R.ref_pagerank_norm, n, len(src), _u32(src), _u32(dst), damping, iters, threads,
+              out, st, max(iters, 1), C.byref(k), C.byref(t))
+    return out, stats_tuples(st, k.value), t.value
+
+
+def ref_cf(n, src, dst, rating, factors, gamma, lam, iters, threads=0, per_iteration=True):
+    R = ref_lib()
+    f = np.ascontiguousarray(factors, np.float64).copy()
+    obj = np.zeros(max(iters, 1), np.float64)
+    rm = np.zeros(max(iters, 1), np.float64)
+    t = C.c_double()
+    _ref_call(R.ref_cf, n, len(src), _u32(src), _u32(dst),
+              np.ascontiguousarray(rating, np.float64), f.shape[1], gamma, lam, iters,
+              threads, 1 if per_iteration else 0, f, obj.ctypes.data,
+              rm.ctypes.data if per_iteration else None, C.byref(t))
+    return f, obj[:iters], (rm[:iters] if per_iteration else None), t.value
+
+
+def ref_semiring_spmv(n, src, dst, vals, x, xvalid, threads=1, parts=1):
+    R = ref_lib()
+    y = np.empty(n, np.int64)
+    yv = np.empty(n, np.uint8)
+    _ref_call(R.ref_semiring_spmv, n, len(src), _u32(src), _u32(dst),
+              np.ascontiguousarray(vals, np.int64), np.ascontiguousarray(x, np.int64),
+              np.ascontiguousarray(xvalid, np.uint8), threads, parts, y, yv)
+    return y, yv.astype(bool)

@@ -1,0 +1,340 @@
+// ref_driver.cpp -- C entry points that run the UNMODIFIED reference engine.
+//
+// TEST INFRASTRUCTURE ONLY.  This file is ours; the engine it drives is the
+// reference's header-only library, included from where it lies
+// (/root/reference/proj/include/semigraph, never copied).  oracle/Makefile
+// compiles it into oracle/_ref/libsemigraph_ref.so, which tests use to pin the
+// C restatement (graphmat_oracle.c) and bench.py uses as the CPU baseline
+// (cpu_baseline.kind = "reference", bench.py --impl reference).
+//
+// Everything below calls the reference's own public API:
+//   build_graph               include/semigraph/dcsc.hpp:243-274
+//   Engine phases / run loop  include/semigraph/engine.hpp:76-213
+//   algo::bfs / algo::sssp    include/semigraph/algorithms/traversal.hpp:119-133
+//   algo::pagerank            include/semigraph/algorithms/pagerank.hpp:73-110
+//   collaborative_filtering_gd include/semigraph/algorithms/collaborative_filtering.hpp:134-211
+// The one new program is the BASELINE-normalised PageRank, which
+// BASELINE configs[0] needs and the reference does not ship; it is driven
+// through the reference engine phases exactly like the CF driver does.
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "semigraph/algorithms/collaborative_filtering.hpp"
+#include "semigraph/algorithms/pagerank.hpp"
+#include "semigraph/algorithms/traversal.hpp"
+#include "semigraph/engine.hpp"
+
+using namespace semigraph;
+
+extern "C" {
+typedef struct {
+  int64_t iteration, active_before, messages_generated, vertices_updated;
+  double spmv_seconds, total_seconds;
+} ref_stats;
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+unsigned resolve_threads(unsigned t) {
+  if (t == 0) t = std::thread::hardware_concurrency();
+  return t == 0 ? 1 : t;
+}
+
+std::vector<EdgeTriple<double>> triples(int64_t m, const uint32_t* src, const uint32_t* dst,
+                                        const double* vals) {
+  std::vector<EdgeTriple<double>> e(static_cast<std::size_t>(m));
+  for (int64_t i = 0; i < m; ++i) e[i] = {src[i], dst[i], vals ? vals[i] : 1.0};
+  return e;
+}
+
+void copy_stats(const std::vector<IterationStats>& s, ref_stats* out, int64_t cap,
+                int64_t* n_out) {
+  if (n_out) *n_out = static_cast<int64_t>(s.size());
+  if (!out) return;
+  for (std::size_t i = 0; i < s.size() && static_cast<int64_t>(i) < cap; ++i) {
+    out[i] = {static_cast<int64_t>(s[i].iteration), static_cast<int64_t>(s[i].active_before),
+              static_cast<int64_t>(s[i].messages_generated),
+              static_cast<int64_t>(s[i].vertices_updated), s[i].spmv_seconds,
+              s[i].total_seconds};
+  }
+}
+
+// Status codes mirror the reference CLI (tools/sgraph.cpp:24): 2 input, 3 engine.
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const InputError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+// BASELINE configs[0] PageRank as a VertexProgram on the reference concept
+// (core.hpp:239-253); shape follows PageRankProgram (pagerank.hpp:36-63).
+struct NormalizedPageRank {
+  using vertex_t = algo::PageRankState;
+  using edge_t = double;
+  using message_t = double;
+  using reduced_t = double;
+  double damping = 0.85;
+  double base = 0.0;
+  ScatterDirection direction() const { return ScatterDirection::OUT; }
+  std::optional<message_t> send_message(const vertex_t& v, VertexId) const {
+    if (v.out_degree == 0) return std::nullopt;
+    return v.rank / static_cast<double>(v.out_degree);
+  }
+  reduced_t process_message(const message_t& m, const edge_t&, const vertex_t&) const {
+    return m;
+  }
+  reduced_t reduce(const reduced_t& a, const reduced_t& b) const { return a + b; }
+  reduced_t reduce_identity() const { return 0.0; }
+  vertex_t apply(const reduced_t& sum, const vertex_t& old) const {
+    return {base + damping * sum, old.out_degree};
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_hardware_threads(void) { return static_cast<int>(resolve_threads(0)); }
+
+int ref_bfs(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst, uint64_t root,
+            int64_t max_iters, unsigned threads, double* out_dist, ref_stats* st, int64_t cap,
+            int64_t* n_stats, double* algo_seconds) {
+  return guarded([&] {
+    threads = resolve_threads(threads);
+    auto e = triples(m, src, dst, nullptr);
+    auto g = build_graph<algo::DistanceState>(e, n, std::size_t(threads) * 8);
+    EngineConfig cfg;
+    cfg.thread_count = threads;
+    cfg.max_iterations = static_cast<std::size_t>(max_iters);
+    Engine eng(cfg);
+    std::vector<IterationStats> stats;
+    const double t0 = now_s();
+    auto d = algo::bfs(g, eng, root, &stats);
+    if (algo_seconds) *algo_seconds = now_s() - t0;
+    std::memcpy(out_dist, d.data(), sizeof(double) * n);
+    copy_stats(stats, st, cap, n_stats);
+  });
+}
+
+int ref_sssp(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst, const double* w,
+             uint64_t root, int64_t max_iters, unsigned threads, double* out_dist,
+             ref_stats* st, int64_t cap, int64_t* n_stats, double* algo_seconds) {
+  return guarded([&] {
+    threads = resolve_threads(threads);
+    auto e = triples(m, src, dst, w);
+    auto g = build_graph<algo::DistanceState>(e, n, std::size_t(threads) * 8);
+    EngineConfig cfg;
+    cfg.thread_count = threads;
+    cfg.max_iterations = static_cast<std::size_t>(max_iters);
+    Engine eng(cfg);
+    std::vector<IterationStats> stats;
+    const double t0 = now_s();
+    auto d = algo::sssp(g, eng, root, &stats);
+    if (algo_seconds) *algo_seconds = now_s() - t0;
+    std::memcpy(out_dist, d.data(), sizeof(double) * n);
+    copy_stats(stats, st, cap, n_stats);
+  });
+}
+
+int ref_pagerank(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst, double r,
+                 int64_t iters, unsigned threads, double* out_rank, ref_stats* st,
+                 int64_t cap, int64_t* n_stats, double* algo_seconds) {
+  return guarded([&] {
+    threads = resolve_threads(threads);
+    auto e = triples(m, src, dst, nullptr);
+    auto g = build_graph<algo::PageRankState>(e, n, std::size_t(threads) * 8);
+    EngineConfig cfg;
+    cfg.thread_count = threads;
+    Engine eng(cfg);
+    algo::PageRankConfig pc;
+    pc.r = r;
+    pc.max_iterations = static_cast<std::size_t>(iters);
+    std::vector<IterationStats> stats;
+    const double t0 = now_s();
+    auto rk = algo::pagerank(g, eng, pc, &stats);
+    if (algo_seconds) *algo_seconds = now_s() - t0;
+    std::memcpy(out_rank, rk.data(), sizeof(double) * n);
+    copy_stats(stats, st, cap, n_stats);
+  });
+}
+
+int ref_pagerank_norm(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
+                      double damping, int64_t iters, unsigned threads, double* out_rank,
+                      ref_stats* st, int64_t cap, int64_t* n_stats, double* algo_seconds) {
+  return guarded([&] {
+    threads = resolve_threads(threads);
+    auto e = triples(m, src, dst, nullptr);
+    auto g = build_graph<algo::PageRankState>(e, n, std::size_t(threads) * 8);
+    EngineConfig cfg;
+    cfg.thread_count = threads;
+    Engine eng(cfg);
+    const auto deg = degree_vector(eng, g, DegreeKind::OUT);
+    auto& props = g.properties();
+    const double nd = static_cast<double>(n);
+    for (VertexId v = 0; v < n; ++v) props[v] = {1.0 / nd, deg[v]};
+    std::vector<IterationStats> stats;
+    const double t0 = now_s();
+    for (int64_t it = 1; it <= iters; ++it) {
+      IterationStats s;
+      const double ts = now_s();
+      double dangling = 0.0;
+      for (VertexId v = 0; v < n; ++v)
+        if (props[v].out_degree == 0) dangling += props[v].rank;
+      NormalizedPageRank prog;
+      prog.damping = damping;
+      prog.base = (1.0 - damping) / nd + damping * dangling / nd;
+      props.set_all_active(true);
+      s.active_before = n;
+      auto x = eng.generate_messages(g, prog);
+      s.messages_generated = x.count_valid();
+      const double t1 = now_s();
+      auto y = eng.generalized_spmv(g, x, prog);
+      s.spmv_seconds = now_s() - t1;
+      s.vertices_updated = eng.apply_and_activate(g, y, prog);
+      for (VertexId v = 0; v < n; ++v)
+        if (!y.valid(v)) props[v] = prog.apply(0.0, props[v]);
+      s.total_seconds = now_s() - ts;
+      s.iteration = static_cast<std::size_t>(it);
+      stats.push_back(s);
+    }
+    if (algo_seconds) *algo_seconds = now_s() - t0;
+    for (VertexId v = 0; v < n; ++v) out_rank[v] = props[v].rank;
+    copy_stats(stats, st, cap, n_stats);
+  });
+}
+
+// factors: n*k doubles (in: injected start, out: final). Sides follow the
+// reference inference (users = rating sources). per_iteration != 0 runs the
+// driver one iteration at a time (state carries over in the graph) so the
+// RMSE after every iteration can be read; algo time then covers those calls.
+int ref_cf(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
+           const double* ratings, int64_t k, double gamma, double lambda, int64_t iters,
+           unsigned threads, int per_iteration, double* factors, double* objective_trace,
+           double* rmse_trace, double* algo_seconds) {
+  return guarded([&] {
+    threads = resolve_threads(threads);
+    auto e = triples(m, src, dst, ratings);
+    auto g = build_graph<algo::LatentVector>(e, n, std::size_t(threads) * 8);
+    EngineConfig cfg;
+    cfg.thread_count = threads;
+    Engine eng(cfg);
+    auto& props = g.properties();
+    for (VertexId v = 0; v < n; ++v)
+      props[v].p.assign(factors + v * k, factors + (v + 1) * k);
+    algo::CfConfig cc;
+    cc.k = static_cast<std::size_t>(k);
+    cc.gamma = gamma;
+    cc.lambda = lambda;
+    auto rmse_now = [&]() {
+      double sq = 0.0;
+      for (const auto& t : e) {
+        double dot = 0.0;
+        for (int64_t d = 0; d < k; ++d) dot += props[t.src].p[d] * props[t.dst].p[d];
+        const double err = t.value - dot;
+        sq += err * err;
+      }
+      return m ? std::sqrt(sq / static_cast<double>(m)) : 0.0;
+    };
+    double algo = 0.0;
+    if (per_iteration) {
+      cc.iterations = 1;
+      for (int64_t it = 0; it < iters; ++it) {
+        const double t0 = now_s();
+        auto res = algo::collaborative_filtering_gd(g, eng, cc);
+        algo += now_s() - t0;
+        if (objective_trace) objective_trace[it] = res.objective_trace.back();
+        if (rmse_trace) rmse_trace[it] = rmse_now();
+      }
+    } else {
+      cc.iterations = static_cast<std::size_t>(iters);
+      const double t0 = now_s();
+      auto res = algo::collaborative_filtering_gd(g, eng, cc);
+      algo = now_s() - t0;
+      if (objective_trace)
+        for (std::size_t i = 0; i < res.objective_trace.size(); ++i)
+          objective_trace[i] = res.objective_trace[i];
+    }
+    if (algo_seconds) *algo_seconds = algo;
+    for (VertexId v = 0; v < n; ++v)
+      std::memcpy(factors + v * k, props[v].p.data(), sizeof(double) * k);
+  });
+}
+
+// Semiring (+, x) over int64 like tests/acceptance.cpp:97-116: x valid where
+// xvalid[j]; y written where valid.
+int ref_semiring_spmv(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
+                      const int64_t* vals, const int64_t* x, const uint8_t* xvalid,
+                      unsigned threads, unsigned parts, int64_t* y, uint8_t* yvalid) {
+  return guarded([&] {
+    struct Cell {
+      long long x = 0, y = 0;
+      bool has_x = false, has_y = false;
+      bool operator==(const Cell& o) const {
+        return x == o.x && y == o.y && has_x == o.has_x && has_y == o.has_y;
+      }
+    };
+    struct Prog {
+      using vertex_t = Cell;
+      using edge_t = long long;
+      using message_t = long long;
+      using reduced_t = long long;
+      ScatterDirection direction() const { return ScatterDirection::OUT; }
+      std::optional<message_t> send_message(const vertex_t& v, VertexId) const {
+        if (!v.has_x) return std::nullopt;
+        return v.x;
+      }
+      reduced_t process_message(const message_t& mm, const edge_t& ee, const vertex_t&) const {
+        return mm * ee;
+      }
+      reduced_t reduce(const reduced_t& a, const reduced_t& b) const { return a + b; }
+      reduced_t reduce_identity() const { return 0; }
+      vertex_t apply(const reduced_t& s, const vertex_t& o) const { return {o.x, s, o.has_x, true}; }
+    };
+    threads = resolve_threads(threads);
+    std::vector<EdgeTriple<long long>> e(static_cast<std::size_t>(m));
+    for (int64_t i = 0; i < m; ++i) e[i] = {src[i], dst[i], vals[i]};
+    auto g = build_graph<Cell, long long>(e, n, parts ? parts : 1);
+    EngineConfig cfg;
+    cfg.thread_count = threads;
+    Engine eng(cfg);
+    auto& props = g.properties();
+    for (VertexId j = 0; j < n; ++j) {
+      if (!xvalid[j]) continue;
+      props[j].x = x[j];
+      props[j].has_x = true;
+      props.set_active(j, true);
+    }
+    Prog prog;
+    auto xs = eng.generate_messages(g, prog);
+    auto ys = eng.generalized_spmv(g, xs, prog);
+    for (VertexId k2 = 0; k2 < n; ++k2) {
+      yvalid[k2] = ys.valid(k2) ? 1 : 0;
+      y[k2] = ys.valid(k2) ? ys.value(k2) : 0;
+    }
+  });
+}
+
+}  // extern "C"

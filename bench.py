@@ -1,0 +1,557 @@
+#!/usr/bin/env python
+"""bench.py -- GraphMat superstep hot path on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE configs[1], BFS on the symmetrised R-MAT
+scale-23 graph (edge factor 16, a/b/c = .57/.19/.19, seed 1, permuted ids),
+push/pull direction switch at 5% of edges.  One step = one full BFS from the
+seed-chosen root (all supersteps).  Other configs: --workload pagerank (configs[0],
+scale 20), pagerank23 (the scale-23 pull-SpMV roofline target), sssp (configs[2]),
+cf (configs[3]).
+
+value  = whole-job GTEPS, inputs resident in HBM, device time (CUDA events on the
+         library stream), max over ranks.  BFS uses the Graph500 convention:
+         undirected edges inside the reached component / BFS time.
+e2e    = the same metric through the public API (paper_1503_07241_b200.bfs) with a
+         pinned host output buffer: H2D of the step's input (root id) and D2H of the
+         step's result (the level vector) are inside the timed region.
+--impl reference: the reference engine (oracle/_ref, compiled from
+         /root/reference/proj/include) on the host cores, same workload/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS (edges/s) per superstep & end-to-end; % of HBM roofline; 1/2/4/8 B200"
+RMAT = dict(a=0.57, b=0.19, c=0.19)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- dist
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Dist:
+    def __init__(self, world, rank, local, backend="nccl"):
+        self.world, self.rank, self.local = world, rank, local
+        self.pg = None
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            import torch
+            t = torch.zeros(1, device="cuda")
+            self.pg.all_reduce(t)
+            torch.cuda.synchronize()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ------------------------------------------------------------- workloads
+
+class Workload:
+    name = ""
+    dtype = ""
+
+    def __init__(self, args):
+        self.args = args
+
+    def roofline(self, stats, peak, peak_kind):
+        return None
+
+
+class BfsWorkload(Workload):
+    name = "bfs"
+    dtype = "int32"
+
+    def build(self, gm):
+        a = self.args
+        t0 = time.perf_counter()
+        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, symmetrize=True, relabel=True, **RMAT)
+        self.ingest_s = time.perf_counter() - t0
+        self.n = 1 << a.scale
+        self.root = self.g.pick_source(a.seed)
+        import torch
+        self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
+        self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
+        lvl, st = gm.bfs(self.g, self.root)
+        deg = self.g.degree_vector("out")
+        # Graph500 TEPS: undirected edges inside the reached component.
+        self.edges = int(deg[lvl >= 0].sum()) // 2
+        self.levels = lvl
+        self.stats = st
+        self.config = {"workload": "bfs_rmat23_sym" if a.scale == 23 else f"bfs_rmat{a.scale}_sym",
+                       "scale": a.scale, "edge_factor": 16, "n": self.n,
+                       "m_directed": self.g.num_edges, "root": self.root,
+                       "teps_edges": self.edges, "switch": "pull when frontier edges > 5% of m",
+                       "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB)"
+                       % (self.g.info().device_bytes / 1e9)}
+
+    def run_device(self, gm):
+        gm.bfs(self.g, self.root, with_stats=False, out_device_ptr=self.dev_out.data_ptr())
+
+    def run_e2e(self, gm):
+        out = self.host_out.numpy()
+        gm.bfs(self.g, self.root, with_stats=False, out=out)
+        return out
+
+    def e2e_bytes(self):
+        return 8, self.n * 4
+
+    def per_superstep(self, gm):
+        _, st = gm.bfs(self.g, self.root)
+        return st
+
+    def roofline(self, st, peak, peak_kind):
+        pulls = [s for s in st if s.direction == "pull"] or st
+        top = max(pulls, key=lambda s: s.spmv_seconds)
+        gbs = top.bytes_algorithmic / top.spmv_seconds / 1e9
+        return {"bound": "hbm", "kernel": "k_bfs_pull" if top.direction == "pull" else "k_bfs_push",
+                "superstep": top.iteration, "achieved": round(gbs, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
+                "bytes_per_launch": top.bytes_algorithmic,
+                "launch_us": round(top.spmv_seconds * 1e6, 2), "traffic": None}
+
+    def cpu_baseline(self, orc):
+        s, d, _ = self.g.edges()
+        R = orc.ref_lib()
+        kind = "reference" if R is not None else "port"
+        if R is not None:
+            b, _, secs = orc.ref_bfs(self.n, s, d, self.root, threads=0)
+            cores = int(R.ref_hardware_threads())
+        else:
+            t0 = time.perf_counter()
+            orc.bfs(self.n, s, d, self.root, presorted=True)
+            secs = time.perf_counter() - t0
+            cores = 1
+        return {"value": round(self.edges / secs / 1e9, 6), "unit": "GTEPS", "cores": cores,
+                "kind": kind, "seconds": round(secs, 4),
+                "sample": "one BFS from the same root on the full graph (graph build excluded)"}
+
+
+class PageRankWorkload(Workload):
+    name = "pagerank"
+    dtype = "f32"
+
+    def build(self, gm):
+        a = self.args
+        t0 = time.perf_counter()
+        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, relabel=True, **RMAT)
+        self.ingest_s = time.perf_counter() - t0
+        self.n = 1 << a.scale
+        self.iters = 20
+        import torch
+        self.dev_out = torch.empty(self.n, dtype=torch.float32, device="cuda")
+        self.host_out = torch.empty(self.n, dtype=torch.float32).pin_memory()
+        self.m = self.g.num_edges
+        self.edges = self.m * self.iters
+        self.config = {"workload": f"pagerank_rmat{a.scale}", "scale": a.scale, "edge_factor": 16,
+                       "n": self.n, "m": self.m, "iterations": self.iters, "damping": 0.85,
+                       "l2": "inputs larger than L2" if self.m * 4 > 126e6
+                       else "working set L2-resident (HBM fraction may exceed 1)"}
+
+    def run_device(self, gm):
+        gm.pagerank(self.g, 0.85, self.iters, with_stats=False,
+                    out_device_ptr=self.dev_out.data_ptr())
+
+    def run_e2e(self, gm):
+        out = self.host_out.numpy()
+        gm.pagerank(self.g, 0.85, self.iters, with_stats=False, out=out)
+        return out
+
+    def e2e_bytes(self):
+        return 16, self.n * 4
+
+    def per_superstep(self, gm):
+        _, st = gm.pagerank(self.g, 0.85, self.iters)
+        return st
+
+    def roofline(self, st, peak, peak_kind):
+        t = statistics.median([s.spmv_seconds for s in st])
+        b = st[0].bytes_algorithmic
+        gbs = b / t / 1e9
+        return {"bound": "hbm", "kernel": "k_pr_rows+k_pr_long_rows", "achieved": round(gbs, 1),
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
+                "bytes_per_launch": b, "launch_us": round(t * 1e6, 2), "traffic": None}
+
+    def cpu_baseline(self, orc):
+        s, d, _ = self.g.edges()
+        R = orc.ref_lib()
+        if R is not None:
+            _, _, secs = orc.ref_pagerank_norm(self.n, s, d, 0.85, self.iters, threads=0)
+            cores, kind = int(R.ref_hardware_threads()), "reference"
+        else:
+            t0 = time.perf_counter()
+            orc.pagerank_norm(self.n, s, d, 0.85, self.iters)
+            secs, cores, kind = time.perf_counter() - t0, 1, "port"
+        return {"value": round(self.edges / secs / 1e9, 6), "unit": "GTEPS", "cores": cores,
+                "kind": kind, "seconds": round(secs, 4),
+                "sample": f"{self.iters} supersteps on the full graph (graph build excluded)"}
+
+
+class SsspWorkload(Workload):
+    name = "sssp"
+    dtype = "uint32"
+
+    def build(self, gm):
+        a = self.args
+        t0 = time.perf_counter()
+        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, relabel=True, weights=True, **RMAT)
+        self.g.ensure_forward()
+        self.ingest_s = time.perf_counter() - t0
+        self.n = 1 << a.scale
+        self.root = self.g.pick_source(a.seed)
+        import torch
+        self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
+        self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
+        _, st = gm.sssp(self.g, self.root)
+        self.edges = int(sum(s.edges_processed for s in st))
+        self.config = {"workload": f"sssp_rmat{a.scale}", "scale": a.scale, "edge_factor": 16,
+                       "n": self.n, "m": self.g.num_edges, "root": self.root,
+                       "weights": "uint8 in [1,255] from the seed",
+                       "teps_edges": self.edges, "teps": "edges relaxed over all supersteps"}
+
+    def run_device(self, gm):
+        gm.sssp(self.g, self.root, with_stats=False, out_device_ptr=self.dev_out.data_ptr())
+
+    def run_e2e(self, gm):
+        out = self.host_out.numpy().view(np.uint32)
+        gm.sssp(self.g, self.root, with_stats=False, out=out)
+        return out
+
+    def e2e_bytes(self):
+        return 8, self.n * 4
+
+    def per_superstep(self, gm):
+        _, st = gm.sssp(self.g, self.root)
+        return st
+
+    def roofline(self, st, peak, peak_kind):
+        top = max(st, key=lambda s: s.spmv_seconds)
+        gbs = top.bytes_algorithmic / top.spmv_seconds / 1e9
+        return {"bound": "hbm", "kernel": "k_sssp_push", "superstep": top.iteration,
+                "achieved": round(gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(gbs / peak, 4), "bytes_per_launch": top.bytes_algorithmic,
+                "launch_us": round(top.spmv_seconds * 1e6, 2), "traffic": None}
+
+    def cpu_baseline(self, orc):
+        s, d, w = self.g.edges()
+        R = orc.ref_lib()
+        _, _, secs = orc.ref_sssp(self.n, s, d, w.astype(np.float64), self.root, threads=0)
+        return {"value": round(self.edges / secs / 1e9, 6), "unit": "GTEPS",
+                "cores": int(R.ref_hardware_threads()), "kind": "reference",
+                "seconds": round(secs, 4),
+                "sample": "one SSSP from the same source on the full graph (build excluded)"}
+
+
+class CfWorkload(Workload):
+    name = "cf"
+    dtype = "f32"
+
+    def build(self, gm):
+        t0 = time.perf_counter()
+        self.g = gm.Graph.bipartite(480189, 17770, 20081304.0, 17770, seed=self.args.seed)
+        self.ingest_s = time.perf_counter() - t0
+        self.n = self.g.num_vertices
+        self.k, self.iters = 20, 10
+        rng = np.random.default_rng(self.args.seed)
+        self.init = rng.uniform(0, 0.1, (self.n, self.k)).astype(np.float32)
+        self.m = self.g.num_edges
+        self.edges = 2 * self.m * self.iters
+        self.config = {"workload": "cf_zipf_480189x17770", "users": 480189, "items": 17770,
+                       "ratings": self.m, "k": 20, "lr": 0.001, "lambda": 0.05,
+                       "iterations": 10}
+
+    def run_device(self, gm):
+        gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters, init=self.init)
+
+    def run_e2e(self, gm):
+        return gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters,
+                                             init=self.init)[0]
+
+    def e2e_bytes(self):
+        return self.n * self.k * 4, self.n * self.k * 4
+
+    def per_superstep(self, gm):
+        return gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters,
+                                             init=self.init)[2]
+
+    def cpu_baseline(self, orc):
+        return None
+
+
+WORKLOADS = {"bfs": (BfsWorkload, 23), "pagerank": (PageRankWorkload, 20),
+             "pagerank23": (PageRankWorkload, 23), "sssp": (SsspWorkload, 23),
+             "cf": (CfWorkload, 0)}
+
+
+# ----------------------------------------------------------------- arms
+
+def run_ours(args, d: Dist):
+    import torch
+
+    import paper_1503_07241_b200 as gm
+
+    torch.cuda.set_device(d.local)
+    cls, default_scale = WORKLOADS[args.workload]
+    if args.scale is None:
+        args.scale = default_scale
+    w = cls(args)
+    w.build(gm)
+    stream = torch.cuda.ExternalStream(w.g.stream)
+    peak, peak_kind = measured_peaks()
+
+    for _ in range(args.warmup):
+        w.run_device(gm)
+    torch.cuda.synchronize()
+
+    # timed region: K steps, inputs resident in HBM
+    d.barrier()
+    torch.cuda.synchronize()
+    launches0 = gm.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(d.local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            w.run_device(gm)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        # keep the GPU busy ~0.5 s more so the clock sampler sees load
+        t_end = time.perf_counter() + 0.5
+        while time.perf_counter() < t_end:
+            w.run_device(gm)
+        torch.cuda.synchronize()
+    launches = gm.kernel_launches() - launches0
+    d.barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    t_ms = d.max(t_ms)
+    value = w.edges * args.steps * d.world / (t_ms * 1e-3) / 1e9
+
+    # end-to-end through the public API with pinned host buffers
+    torch.cuda.synchronize()
+    d.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        w.run_e2e(gm)
+    e2e_s = d.max(time.perf_counter() - t0)
+    e2e = w.edges * args.steps * d.world / e2e_s / 1e9
+    h2d, d2h = w.e2e_bytes()
+
+    st = w.per_superstep(gm)
+    per = [{"it": s.iteration, "dir": s.direction, "active": s.active_before,
+            "updated": s.vertices_updated, "edges": s.edges_processed,
+            "us": round(s.spmv_seconds * 1e6, 2),
+            "gteps": round(s.edges_processed / s.spmv_seconds / 1e9, 3) if s.spmv_seconds else None}
+           for s in st]
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": d.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": w.dtype,
+        "data": "synthetic: seeded counter-based R-MAT/Zipf generators (DESIGN.md), no datasets",
+        "config": dict(w.config, parallelism=("replicas%d" % d.world) if d.world > 1 else "single"),
+        "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_s * 1e3 / args.steps, 4)},
+        "roofline": w.roofline(st, peak, peak_kind),
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "ingest_seconds": round(w.ingest_s, 3),
+        "per_superstep": per,
+    }
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+        import oracle
+        line["cpu_baseline"] = w.cpu_baseline(oracle)
+    if d.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_reference(args, d: Dist):
+    """The reference engine (oracle/_ref) on the host cores, same workload/metric."""
+    if d.rank != 0:
+        return
+    import oracle
+
+    R = oracle.ref_lib()
+    cls, default_scale = WORKLOADS[args.workload]
+    scale = args.scale if args.scale is not None else default_scale
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    cores = int(R.ref_hardware_threads())
+    n = 1 << scale
+    t0 = time.perf_counter()
+    s, dd = oracle.rmat(scale, 16, seed=args.seed, **RMAT)
+    if args.workload == "bfs":
+        s, dd, _ = oracle.preprocess(s, dd, symmetrize=True)
+        deg = np.bincount(s, minlength=n).astype(np.uint32)
+        root = oracle.pick_source(args.seed, deg)
+        gen_s = time.perf_counter() - t0
+        lvl, _ = oracle.bfs(n, s, dd, root, presorted=True)
+        edges = int(deg[lvl >= 0].sum()) // 2
+
+        def step():
+            return oracle.ref_bfs(n, s, dd, root, threads=0)[2]
+        config = {"workload": f"bfs_rmat{scale}_sym", "scale": scale, "edge_factor": 16,
+                  "n": n, "m_directed": len(s), "root": root, "teps_edges": edges}
+    elif args.workload in ("pagerank", "pagerank23"):
+        s, dd, _ = oracle.preprocess(s, dd)
+        gen_s = time.perf_counter() - t0
+        edges = len(s) * 20
+
+        def step():
+            return oracle.ref_pagerank_norm(n, s, dd, 0.85, 20, threads=0)[2]
+        config = {"workload": f"pagerank_rmat{scale}", "scale": scale, "n": n, "m": len(s),
+                  "iterations": 20}
+    else:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"--impl reference not wired for workload {args.workload}"}))
+        return
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    value = edges * args.steps / total / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GTEPS",
+        "n_gpus": d.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total * 1e3 / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config,
+        "cpu_baseline": {"value": round(value, 6), "unit": "GTEPS", "cores": cores,
+                         "kind": "reference",
+                         "sample": "each step = one full run on the full graph; the reference "
+                                   "engine's algorithm time (graph build excluded, as "
+                                   "tools/sgraph.cpp:101-103)"},
+        "e2e": {"value": round(value, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "setup_seconds": round(gen_s, 2),
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bfs", choices=sorted(WORKLOADS))
+    ap.add_argument("--scale", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        run_reference(args, Dist(1, 0, local))
+        return
+    d = Dist(world, rank, local)
+    try:
+        run_ours(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * graphmat_b200.h -- C ABI of the B200-native GraphMat superstep backend.
+ *
+ * The reference (semigraph, /root/reference/proj) exposes its superstep path as
+ * C++20 templates only (no C ABI, no FFI).  Each entry point below replaces one
+ * reference interface; the citation is the reference file:line it stands in for
+ * (paths relative to /root/reference/proj).  All pointers are plain host pointers
+ * unless the matching *_on_device flag is set.  The library copies its inputs,
+ * owns every device allocation and never retains caller pointers.
+ *
+ * Errors: every call returns a gm_status; gm_last_error() returns the message
+ * of the last failure on the calling thread.  Codes mirror the reference CLI's
+ * exit codes (tools/sgraph.cpp:24): usage 1, InputError 2, EngineError 3.
+ *
+ * Threading: one handle is driven by one host thread at a time (the reference
+ * Engine is not re-entrant either, include/semigraph/engine.hpp:55-57).
+ */
+#ifndef GRAPHMAT_B200_H
+#define GRAPHMAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define GM_API __attribute__((visibility("default")))
+#else
+#define GM_API
+#endif
+
+typedef enum {
+  GM_OK = 0,
+  GM_EUSAGE = 1,  /* bad arguments / API misuse            (sgraph.cpp:24 usage)       */
+  GM_EINPUT = 2,  /* semigraph::InputError                  (core.hpp:44-50)            */
+  GM_EENGINE = 3, /* semigraph::EngineError                 (core.hpp:52-57)            */
+  GM_ECUDA = 4,   /* CUDA runtime failure                                              */
+  GM_ENCCL = 5    /* NCCL failure (multi-GPU sharding)                                 */
+} gm_status;
+
+typedef struct gm_graph* gm_graph_t;
+
+typedef enum { GM_ID_U32 = 0, GM_ID_U64 = 1 } gm_id_type;
+
+/* Edge value storage types.  The reference stores EdgeTriple<E>::value
+ * (core.hpp:35-42); the device stores the narrowest type the program needs. */
+typedef enum {
+  GM_VAL_NONE = 0,
+  GM_VAL_F64 = 1,
+  GM_VAL_F32 = 2,
+  GM_VAL_U8 = 3,
+  GM_VAL_I64 = 4,
+  GM_VAL_U32 = 5
+} gm_value_type;
+
+/* Structure-of-arrays edge list; replaces std::span<const EdgeTriple<E>>
+ * (dcsc.hpp:243-245).  Ids are 0-based like the library side of the reference. */
+typedef struct {
+  const void* src;
+  const void* dst;
+  const void* values; /* may be NULL (every edge gets value 1, like unweighted loads) */
+  int64_t count;
+  int32_t id_type;    /* gm_id_type */
+  int32_t value_type; /* gm_value_type of `values` as passed */
+  int32_t on_device;  /* 1: src/dst/values are device pointers */
+  int32_t reserved;
+} gm_edge_list;
+
+enum {
+  GM_PREPROCESS = 1u,   /* io::preprocess cleanup: drop self loops, dedup keep-first (io.cpp:184-196) */
+  GM_SYMMETRIZE = 2u,   /* PreprocessMode::SYMMETRIZE (io.cpp:198-204); implies GM_PREPROCESS      */
+  GM_RELABEL = 4u,      /* internal degree-ordered vertex ids (results stay in caller ids)          */
+  GM_NEED_FORWARD = 8u  /* build CSR(G) eagerly (Graph::ensure_forward, dcsc.hpp:201-215)           */
+};
+
+/* Mirrors semigraph::IterationStats (engine.hpp:32-39) plus device counters. */
+typedef struct {
+  int64_t iteration;
+  int64_t active_before;
+  int64_t messages_generated;
+  int64_t vertices_updated;
+  double spmv_seconds;
+  double total_seconds;
+  int64_t edges_processed;   /* adjacency entries read by the SpMV / SpMSpV        */
+  int64_t bytes_algorithmic; /* DESIGN.md formula for the kernel that ran          */
+  int32_t direction;         /* 0 = pull SpMV over G^T, 1 = push SpMSpV over G     */
+  int32_t reserved;
+} gm_iteration_stats;
+
+typedef struct {
+  uint64_t num_vertices;
+  uint64_t num_edges;
+  uint32_t flags;
+  int32_t value_type;
+  int32_t forward_built;
+  int32_t device;
+  uint64_t device_bytes;
+  uint64_t nonzero_out_degree;
+} gm_graph_info;
+
+GM_API const char* gm_last_error(void);
+GM_API const char* gm_version(void);
+/* Process-wide count of this library's kernel launches (benchmark evidence). */
+GM_API uint64_t gm_kernel_launches(void);
+
+/* ---- graph construction: replaces build_graph (dcsc.hpp:243-274) and, with
+ *      GM_PREPROCESS / GM_SYMMETRIZE, io::preprocess (io.cpp:184-222). ----------
+ * Rejects out-of-range endpoints and, without GM_PREPROCESS, duplicate edges
+ * with the reference's messages (dcsc.hpp:252-256, 148-150).  value_storage
+ * selects the device value type (GM_VAL_NONE drops values). */
+GM_API gm_status gm_graph_create(const gm_edge_list* edges, uint64_t num_vertices,
+                                 uint32_t flags, int32_t value_storage, gm_graph_t* out);
+/* Seeded R-MAT (semantics of io::rmat_generate,
+ * io.cpp:224-255, made counter-based + permuted) generated and ingested on the
+ * GPU.  weights = GM_VAL_U8 attaches seeded integer weights in [1,255]. */
+GM_API gm_status gm_graph_generate_rmat(uint32_t scale, uint32_t edge_factor, double a,
+                                        double b, double c, uint64_t seed, int32_t permute,
+                                        uint32_t flags, int32_t weights, gm_graph_t* out);
+/* Seeded Zipf bipartite rating graph (stands in for io::bipartite_generate,
+ * io.cpp:257-288): users [0,U), items [U,U+I), uint8 ratings in 1..5. */
+GM_API gm_status gm_graph_generate_bipartite(uint32_t users, uint32_t items,
+                                             double c_numerator, uint32_t cap, uint64_t seed,
+                                             uint32_t flags, gm_graph_t* out);
+GM_API gm_status gm_graph_destroy(gm_graph_t g);
+GM_API gm_status gm_graph_get_info(gm_graph_t g, gm_graph_info* info);
+/* Graph::ensure_forward (dcsc.hpp:201-215). */
+GM_API gm_status gm_graph_ensure_forward(gm_graph_t g);
+/* The stored edge list in caller ids, sorted by (src, dst): the same list
+ * io::preprocess returns (io.cpp:184-222).  values typed by the storage type. */
+GM_API gm_status gm_graph_export_edges(gm_graph_t g, uint32_t* src, uint32_t* dst,
+                                       void* values);
+/* degree_vector (engine.hpp:295-312); kind 0 = IN, 1 = OUT. */
+GM_API gm_status gm_degree_vector(gm_graph_t g, int32_t kind, uint64_t* out);
+/* Seed-chosen vertex with nonzero out-degree (BASELINE configs[1..2]). */
+GM_API gm_status gm_pick_source(gm_graph_t g, uint64_t seed, uint64_t* out);
+/* The cudaStream_t every call on this handle is issued on (for event timing). */
+GM_API void* gm_graph_stream(gm_graph_t g);
+
+/* ---- fast programs (specialised kernels) --------------------------------- */
+typedef struct {
+  double damping;     /* BASELINE: 0.85                          */
+  int64_t iterations; /* fixed supersteps, all vertices active   */
+} gm_pagerank_config;
+
+/* Normalised PageRank (BASELINE configs[0]); the reference program shape is
+ * PageRankProgram (algorithms/pagerank.hpp:36-63) driven like the CF driver
+ * (algorithms/collaborative_filtering.hpp:181-193). out_rank: n floats. */
+GM_API gm_status gm_pagerank(gm_graph_t g, const gm_pagerank_config* cfg, float* out_rank,
+                             int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                             int64_t* n_stats);
+/* algo::bfs (algorithms/traversal.hpp:119-123): int32 level, -1 unreached.
+ * Direction-optimising push/pull; pull when frontier edges > alpha * m. */
+GM_API gm_status gm_bfs(gm_graph_t g, uint64_t root, int64_t max_iters, int32_t* out_level,
+                        int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                        int64_t* n_stats);
+/* algo::sssp (algorithms/traversal.hpp:125-133) on integer weights:
+ * uint32 distance, UINT32_MAX unreached. */
+GM_API gm_status gm_sssp(gm_graph_t g, uint64_t source, int64_t max_iters, uint32_t* out_dist,
+                         int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                         int64_t* n_stats);
+
+typedef struct {
+  int64_t k;
+  float gamma;
+  float lambda;
+  int64_t iterations;
+} gm_cf_config;
+/* collaborative_filtering_gd (algorithms/collaborative_filtering.hpp:134-211)
+ * in fp32.  init_factors / out_factors: n*k floats (row-major, caller ids).
+ * rmse_trace[it] = RMSE over ratings after iteration it. */
+GM_API gm_status gm_cf(gm_graph_t g, const gm_cf_config* cfg, const float* init_factors,
+                       float* out_factors, double* rmse_trace, gm_iteration_stats* stats,
+                       int64_t cap, int64_t* n_stats);
+
+/* ---- generic engine: any VertexProgram, exact reference semantics -------- */
+/* Built-in instantiations of the device-side VertexProgram template (see
+ * paper_1503_07241_b200/csrc/engine.cuh).  Fold order per row is ascending
+ * internal source id, which equals the reference order (engine.hpp:59-66) on
+ * graphs built without GM_RELABEL. */
+typedef enum {
+  GM_PROG_PAGERANK_REF = 1,    /* PageRankProgram, pagerank.hpp:36-63 (fp64)          */
+  GM_PROG_BFS_REF = 2,         /* BfsProgram, traversal.hpp:39-63 (fp64)              */
+  GM_PROG_SSSP_REF = 3,        /* SsspProgram, traversal.hpp:67-91 (fp64 weights)     */
+  GM_PROG_SEMIRING_I64 = 4,    /* tests/acceptance.cpp:94-116                          */
+  GM_PROG_ADD_PROBE = 5,       /* tests/test_engine.cpp:31-43                          */
+  GM_PROG_IN_ADD_PROBE = 6,    /* tests/test_engine.cpp:206-223                        */
+  GM_PROG_SELECTIVE_PROBE = 7, /* tests/test_engine.cpp:172-184 (vertex 0 declines)    */
+  GM_PROG_THROWING_APPLY = 8,  /* tests/test_engine.cpp:67-80                          */
+  GM_PROG_BOTH_ORDER_PROBE = 9,/* tests/test_engine.cpp:45-65                          */
+  GM_PROG_FIXED_PROBE = 10,    /* tests/test_engine.cpp:133-143                        */
+  GM_PROG_NORM_PAGERANK = 11   /* BASELINE PageRank as a generic fp64 program          */
+} gm_program_id;
+
+/* sizeof(vertex_t), sizeof(message_t), sizeof(reduced_t) of a program. */
+GM_API gm_status gm_program_sizes(int32_t program, size_t* vertex_bytes, size_t* message_bytes,
+                                  size_t* reduced_bytes);
+/* Engine::run_graph_program (engine.hpp:193-213).  props (n * vertex_bytes) and
+ * active (n bytes, 0/1) are the caller's VertexPropertyStore (core.hpp:179-222),
+ * read on entry and written back on return.  params: program scalar (double*)
+ * or NULL. */
+GM_API gm_status gm_run_graph_program(gm_graph_t g, int32_t program, const double* params,
+                                      void* props, uint8_t* active, int64_t max_iters,
+                                      gm_iteration_stats* stats, int64_t cap, int64_t* n_stats);
+/* Phase-level access: Engine::generate_messages (engine.hpp:76-98) and, when
+ * run_spmv != 0, Engine::generalized_spmv (engine.hpp:104-134).  x (n *
+ * message_bytes) / y (n * reduced_bytes) values are written where valid. */
+GM_API gm_status gm_superstep_phases(gm_graph_t g, int32_t program, const double* params,
+                                     const void* props, const uint8_t* active, void* x,
+                                     uint8_t* x_valid, int32_t run_spmv, void* y,
+                                     uint8_t* y_valid);
+
+/* ---- multi-GPU sharding (1-D row blocks of G^T, one process per GPU) ----- */
+/* Row-block boundaries balanced by stored entries, like
+ * detail::balanced_row_boundaries (dcsc.hpp:81-105).  row_nnz: n counts;
+ * bounds: parts+1 entries. */
+GM_API gm_status gm_balanced_row_boundaries(const uint64_t* row_nnz, uint64_t n, uint64_t parts,
+                                            uint64_t* bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAPHMAT_B200_H */

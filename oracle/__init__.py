@@ -73,6 +73,8 @@ def lib():
     L.or_rmat_generate.restype = C.c_int64
     L.or_rmat_generate.argtypes = [C.c_uint, C.c_uint, C.c_double, C.c_double, C.c_double,
                                    C.c_uint64, C.c_int, u32p, u32p]
+    L.or_edge_weight.restype = C.c_uint8
+    L.or_edge_weight.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32]
     L.or_edge_weights.restype = None
     L.or_edge_weights.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, u8p]
     L.or_ratings.restype = None
@@ -223,9 +225,10 @@ def _sorted_by(primary, secondary, *rest):
             for a in (primary, secondary) + rest]
 
 
-def bfs(n, src, dst, root, max_iters=None):
-    """BSP BFS levels (int32, -1 unreached) + per-superstep stats tuples."""
-    s, d = _sorted_by(_u32(src), _u32(dst))
+def bfs(n, src, dst, root, max_iters=None, presorted=False):
+    """BSP BFS levels (int32, -1 unreached) + per-superstep stats tuples.
+    presorted: edges already sorted by (src, dst) (skips the host sort)."""
+    s, d = (_u32(src), _u32(dst)) if presorted else _sorted_by(_u32(src), _u32(dst))
     ptr, idx, _ = csr(n, s, d)
     lvl = np.empty(n, np.int32)
     cap = n + 2
@@ -235,13 +238,16 @@ def bfs(n, src, dst, root, max_iters=None):
     return lvl, stats_tuples(st, k)
 
 
-def sssp(n, src, dst, w, root, max_iters=None):
-    s, d, ww = _sorted_by(_u32(src), _u32(dst), np.asarray(w))
-    ptr, idx, wv = csr(n, s, d, ww.astype(np.float64))
+def sssp(n, src, dst, w, root, max_iters=None, presorted=False):
+    if presorted:
+        s, d, ww = _u32(src), _u32(dst), np.asarray(w)
+    else:
+        s, d, ww = _sorted_by(_u32(src), _u32(dst), np.asarray(w))
+    ptr, idx, _ = csr(n, s, d)
     dist = np.empty(n, np.uint32)
     cap = n + 2
     st = (Stats * cap)()
-    k = lib().or_sssp(n, ptr, idx, np.ascontiguousarray(wv.astype(np.uint32)), root,
+    k = lib().or_sssp(n, ptr, idx, np.ascontiguousarray(ww, dtype=np.uint32), root,
                       max_iters if max_iters is not None else n + 1, dist, st, cap)
     return dist, stats_tuples(st, k)
 

@@ -5,10 +5,12 @@
  * -ffp-contract=off so fp64 folds round exactly like the reference build
  * (FMA contraction breaks bitwise parity).
  */
-#define _POSIX_C_SOURCE 199309L
+#define _POSIX_C_SOURCE 200809L
 #include "graphmat_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
+#include <unistd.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
@@ -93,27 +95,31 @@ static uint64_t prob_threshold(double p) {
   return (uint64_t)(p * 4294967296.0);
 }
 
-int64_t or_rmat_generate(unsigned scale, unsigned edge_factor, double a, double b, double c,
-                         uint64_t seed, int permute, uint32_t* src, uint32_t* dst) {
-  const uint64_t count = (uint64_t)edge_factor << scale;
-  const uint64_t ta = prob_threshold(a), tab = prob_threshold(a + b),
-                 tabc = prob_threshold(a + b + c);
-  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-  perm_keys pk;
-  perm_init(&pk, scale, seed);
-  for (uint64_t t = 0; t < count; ++t) {
+typedef struct {
+  unsigned scale;
+  uint64_t ta, tab, tabc, lo, hi;
+  uint32_t key[2];
+  int permute;
+  const perm_keys* pk;
+  uint32_t *src, *dst;
+} rmat_job;
+
+static void* rmat_worker(void* arg) {
+  const rmat_job* j = (const rmat_job*)arg;
+  const unsigned scale = j->scale;
+  for (uint64_t t = j->lo; t < j->hi; ++t) {
     uint32_t s = 0, d = 0;
     for (unsigned l = 0; l < scale; l += 4) {
       const uint32_t ctr[4] = {(uint32_t)t, (uint32_t)(t >> 32), l >> 2, 0x524D4154u};
       uint32_t out[4];
-      or_philox4x32_10(ctr, key, out);
+      or_philox4x32_10(ctr, j->key, out);
       for (unsigned q = 0; q < 4 && l + q < scale; ++q) {
         const uint64_t r = out[q];
         const uint32_t bit = 1u << (scale - 1 - (l + q));
-        if (r < ta) {
-        } else if (r < tab) {
+        if (r < j->ta) {
+        } else if (r < j->tab) {
           d |= bit;
-        } else if (r < tabc) {
+        } else if (r < j->tabc) {
           s |= bit;
         } else {
           s |= bit;
@@ -121,13 +127,49 @@ int64_t or_rmat_generate(unsigned scale, unsigned edge_factor, double a, double 
         }
       }
     }
-    if (permute) {
-      s = perm_apply(&pk, s);
-      d = perm_apply(&pk, d);
+    if (j->permute) {
+      s = perm_apply(j->pk, s);
+      d = perm_apply(j->pk, d);
     }
-    src[t] = s;
-    dst[t] = d;
+    j->src[t] = s;
+    j->dst[t] = d;
   }
+  return NULL;
+}
+
+/* Each tuple t is a pure function of (seed, t): the work is split across host
+ * threads without changing the output. */
+int64_t or_rmat_generate(unsigned scale, unsigned edge_factor, double a, double b, double c,
+                         uint64_t seed, int permute, uint32_t* src, uint32_t* dst) {
+  const uint64_t count = (uint64_t)edge_factor << scale;
+  perm_keys pk;
+  perm_init(&pk, scale, seed);
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  if (nt < 1) nt = 1;
+  if (nt > 64) nt = 64;
+  if (count < (1u << 16)) nt = 1;
+  rmat_job jobs[64];
+  pthread_t th[64];
+  for (long i = 0; i < nt; ++i) {
+    rmat_job* j = &jobs[i];
+    j->scale = scale;
+    j->ta = prob_threshold(a);
+    j->tab = prob_threshold(a + b);
+    j->tabc = prob_threshold(a + b + c);
+    j->lo = count * (uint64_t)i / (uint64_t)nt;
+    j->hi = count * (uint64_t)(i + 1) / (uint64_t)nt;
+    j->key[0] = (uint32_t)seed;
+    j->key[1] = (uint32_t)(seed >> 32);
+    j->permute = permute;
+    j->pk = &pk;
+    j->src = src;
+    j->dst = dst;
+    if (nt > 1) pthread_create(&th[i], NULL, rmat_worker, j);
+  }
+  if (nt == 1)
+    rmat_worker(&jobs[0]);
+  else
+    for (long i = 0; i < nt; ++i) pthread_join(th[i], NULL);
   return (int64_t)count;
 }
 

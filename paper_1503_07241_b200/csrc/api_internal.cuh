@@ -1,0 +1,31 @@
+// api_internal.cuh -- C++ entry points behind the C ABI (capi.cu).
+#pragma once
+
+#include <vector>
+
+#include "graph.cuh"
+
+namespace gm {
+
+// generic_programs.cu
+void program_sizes(int prog, size_t* v, size_t* m, size_t* r);
+std::vector<gm_iteration_stats> run_program(Graph& g, int prog, const double* params, void* props,
+                                            uint8_t* active, int64_t max_iters);
+void superstep_phases(Graph& g, int prog, const double* params, const void* props,
+                      const uint8_t* active, void* x, uint8_t* x_valid, int run_spmv, void* y,
+                      uint8_t* y_valid);
+
+// pagerank.cu
+std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters, float* out,
+                                         bool out_on_device, bool collect_stats);
+// traversal.cu
+std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, int32_t* out,
+                                    bool out_on_device, bool collect_stats);
+std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters, uint32_t* out,
+                                     bool out_on_device, bool collect_stats);
+// cf.cu
+std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
+                                   const float* init, float* out, double* rmse_trace);
+
+
+}  // namespace gm

@@ -1,0 +1,227 @@
+// capi.cu -- the C ABI (include/graphmat_b200.h).  Every entry point catches
+// the library's exceptions and turns them into a gm_status plus a thread-local
+// message, the way the reference CLI maps InputError/EngineError to exit codes
+// (tools/sgraph.cpp:24, 293-354).
+#include <string>
+#include <vector>
+
+#include "api_internal.cuh"
+
+namespace gm {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace gm
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+gm_status guarded(F&& f) {
+  try {
+    f();
+    return GM_OK;
+  } catch (const gm::Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return GM_ECUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return GM_EENGINE;
+  }
+}
+
+gm::Graph* handle(gm_graph_t g) {
+  if (!g) gm::fail(GM_EUSAGE, "null graph handle");
+  return reinterpret_cast<gm::Graph*>(g);
+}
+
+void copy_stats(const std::vector<gm_iteration_stats>& st, gm_iteration_stats* out, int64_t cap,
+                int64_t* n_out) {
+  if (n_out) *n_out = int64_t(st.size());
+  if (!out) return;
+  for (size_t i = 0; i < st.size() && int64_t(i) < cap; ++i) out[i] = st[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+GM_API const char* gm_last_error(void) { return g_last_error.c_str(); }
+
+GM_API const char* gm_version(void) { return "graphmat_b200 0.1 (sm_100a)"; }
+
+GM_API uint64_t gm_kernel_launches(void) { return gm::g_launches.load(); }
+
+GM_API gm_status gm_graph_create(const gm_edge_list* edges, uint64_t num_vertices, uint32_t flags,
+                                 int32_t value_storage, gm_graph_t* out) {
+  return guarded([&] {
+    if (!edges || !out) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_graph_t>(gm::graph_create(*edges, num_vertices, flags, value_storage));
+  });
+}
+
+GM_API gm_status gm_graph_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b,
+                                        double c, uint64_t seed, int32_t permute, uint32_t flags,
+                                        int32_t weights, gm_graph_t* out) {
+  return guarded([&] {
+    if (!out) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_graph_t>(
+        gm::graph_generate_rmat(scale, edge_factor, a, b, c, seed, permute, flags, weights));
+  });
+}
+
+GM_API gm_status gm_graph_generate_bipartite(uint32_t users, uint32_t items, double c_numerator,
+                                             uint32_t cap, uint64_t seed, uint32_t flags,
+                                             gm_graph_t* out) {
+  return guarded([&] {
+    if (!out) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_graph_t>(
+        gm::graph_generate_bipartite(users, items, c_numerator, cap, seed, flags));
+  });
+}
+
+GM_API gm_status gm_graph_destroy(gm_graph_t g) {
+  return guarded([&] { gm::graph_destroy(reinterpret_cast<gm::Graph*>(g)); });
+}
+
+GM_API gm_status gm_graph_get_info(gm_graph_t g, gm_graph_info* info) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (!info) gm::fail(GM_EUSAGE, "null info");
+    info->num_vertices = h->n;
+    info->num_edges = h->m;
+    info->flags = h->flags;
+    info->value_type = h->value_type;
+    info->forward_built = h->out_built ? 1 : 0;
+    info->device = h->device;
+    info->device_bytes = h->device_bytes();
+    info->nonzero_out_degree = h->nonzero_outdeg;
+  });
+}
+
+GM_API gm_status gm_graph_ensure_forward(gm_graph_t g) {
+  return guarded([&] { gm::ensure_forward(*handle(g)); });
+}
+
+GM_API gm_status gm_graph_export_edges(gm_graph_t g, uint32_t* src, uint32_t* dst, void* values) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if ((!src || !dst) && h->m) gm::fail(GM_EUSAGE, "null output arrays");
+    gm::export_edges(*h, src, dst, values);
+  });
+}
+
+GM_API gm_status gm_degree_vector(gm_graph_t g, int32_t kind, uint64_t* out) {
+  return guarded([&] {
+    if (kind != 0 && kind != 1) gm::fail(GM_EUSAGE, "degree kind must be 0 (IN) or 1 (OUT)");
+    gm::degree_vector(*handle(g), kind, out);
+  });
+}
+
+GM_API gm_status gm_pick_source(gm_graph_t g, uint64_t seed, uint64_t* out) {
+  return guarded([&] { *out = gm::pick_source(*handle(g), seed); });
+}
+
+GM_API void* gm_graph_stream(gm_graph_t g) {
+  return g ? reinterpret_cast<void*>(reinterpret_cast<gm::Graph*>(g)->stream) : nullptr;
+}
+
+GM_API gm_status gm_pagerank(gm_graph_t g, const gm_pagerank_config* cfg, float* out_rank,
+                             int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                             int64_t* n_stats) {
+  return guarded([&] {
+    if (!cfg) gm::fail(GM_EUSAGE, "null config");
+    auto st = gm::pagerank(*handle(g), cfg->damping, cfg->iterations, out_rank, out_on_device != 0,
+                           stats != nullptr || n_stats != nullptr);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
+GM_API gm_status gm_bfs(gm_graph_t g, uint64_t root, int64_t max_iters, int32_t* out_level,
+                        int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                        int64_t* n_stats) {
+  return guarded([&] {
+    auto st = gm::bfs(*handle(g), root, max_iters, out_level, out_on_device != 0,
+                      stats != nullptr || n_stats != nullptr);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
+GM_API gm_status gm_sssp(gm_graph_t g, uint64_t source, int64_t max_iters, uint32_t* out_dist,
+                         int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                         int64_t* n_stats) {
+  return guarded([&] {
+    auto st = gm::sssp(*handle(g), source, max_iters, out_dist, out_on_device != 0,
+                       stats != nullptr || n_stats != nullptr);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
+GM_API gm_status gm_cf(gm_graph_t g, const gm_cf_config* cfg, const float* init_factors,
+                       float* out_factors, double* rmse_trace, gm_iteration_stats* stats,
+                       int64_t cap, int64_t* n_stats) {
+  return guarded([&] {
+    if (!cfg) gm::fail(GM_EUSAGE, "null config");
+    auto st = gm::cf(*handle(g), cfg->k, cfg->gamma, cfg->lambda, cfg->iterations, init_factors,
+                     out_factors, rmse_trace);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
+GM_API gm_status gm_program_sizes(int32_t program, size_t* vertex_bytes, size_t* message_bytes,
+                                  size_t* reduced_bytes) {
+  return guarded([&] { gm::program_sizes(program, vertex_bytes, message_bytes, reduced_bytes); });
+}
+
+GM_API gm_status gm_run_graph_program(gm_graph_t g, int32_t program, const double* params,
+                                      void* props, uint8_t* active, int64_t max_iters,
+                                      gm_iteration_stats* stats, int64_t cap, int64_t* n_stats) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (h->n && (!props || !active)) gm::fail(GM_EUSAGE, "null property / activity arrays");
+    auto st = gm::run_program(*h, program, params, props, active, max_iters);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
+GM_API gm_status gm_superstep_phases(gm_graph_t g, int32_t program, const double* params,
+                                     const void* props, const uint8_t* active, void* x,
+                                     uint8_t* x_valid, int32_t run_spmv, void* y,
+                                     uint8_t* y_valid) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (h->n && (!props || !active)) gm::fail(GM_EUSAGE, "null property / activity arrays");
+    gm::superstep_phases(*h, program, params, props, active, x, x_valid, run_spmv, y, y_valid);
+  });
+}
+
+// detail::balanced_row_boundaries (dcsc.hpp:81-105): boundary p is the smallest
+// row i with cum(i) * parts >= p * total.
+GM_API gm_status gm_balanced_row_boundaries(const uint64_t* row_nnz, uint64_t n, uint64_t parts,
+                                            uint64_t* bounds) {
+  return guarded([&] {
+    if (parts == 0) gm::fail(GM_EUSAGE, "parts must be positive");
+    std::vector<uint64_t> cum(n + 1, 0);
+    for (uint64_t i = 0; i < n; ++i) cum[i + 1] = cum[i] + row_nnz[i];
+    const uint64_t total = cum[n];
+    bounds[0] = 0;
+    bounds[parts] = n;
+    for (uint64_t p = 1; p < parts; ++p) {
+      const unsigned __int128 target = (unsigned __int128)p * total;
+      uint64_t lo = bounds[p - 1], hi = n;
+      while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if ((unsigned __int128)cum[mid] * parts >= target)
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      bounds[p] = lo;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,355 @@
+// cf.cu -- collaborative filtering (gradient descent) superstep in fp32.
+//
+// Reference: CfGdProgram (include/semigraph/algorithms/collaborative_filtering.hpp:51-90)
+// driven by collaborative_filtering_gd (:134-211): every vertex sends its
+// latent vector both ways (ScatterDirection::BOTH); a receiver turns each
+// incoming q into e*q with e = rating - p.q, sums, and applies
+// p' = p + gamma*(sum - lambda*p); vertices with no ratings take the empty
+// sum.  BOTH = SpMV over G^T (items receive from users) and over G (users
+// receive from items), merged out-route first (engine.hpp:113-126).
+//
+// Device layout: factors f[N][K] f32 row-major, double-buffered (bulk-
+// synchronous reads, S3).  Each CSR is cut into work items of <= kChunk
+// entries of one row; a warp owns an item, each lane owns whole ratings: it
+// gathers the source vector (K floats as float4s), dots it with the row's
+// vector (held in registers), and accumulates e*q.  Warp shuffle trees reduce
+// per item; k_cf_apply folds a vertex's item partials in fixed order (out-route
+// items first) -- deterministic, no float atomics.
+#include <cmath>
+#include <vector>
+
+#include "api_internal.cuh"
+
+namespace gm {
+
+constexpr uint32_t kChunk = 1024;
+
+struct CfCache {
+  int64_t k = 0;
+  DevBuf<uint32_t> items_t, items_f;        // (row) per item
+  DevBuf<uint64_t> ibeg_t, ibeg_f;          // item edge ranges: begin (end = next or row end)
+  DevBuf<uint64_t> iend_t, iend_f;
+  DevBuf<uint32_t> rowitem_t, rowitem_f;    // n+1: first item of each row
+  uint64_t nit_t = 0, nit_f = 0;
+  DevBuf<float> part_t, part_f;             // nitems * k
+  DevBuf<float> sq;                         // per item of the forward pass
+  DevBuf<float> f0, f1;
+  DevBuf<double> scal;
+  DevBuf<unsigned long long> ctr;
+};
+
+namespace {
+
+void build_items(const Csr& c, uint64_t n, DevBuf<uint32_t>& rows, DevBuf<uint64_t>& beg,
+                 DevBuf<uint64_t>& end, DevBuf<uint32_t>& rowitem, uint64_t& nit, cudaStream_t s) {
+  std::vector<uint64_t> ptr(n + 1);
+  GM_CUDA(cudaMemcpyAsync(ptr.data(), c.ptr.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint32_t> r, ri(n + 1);
+  std::vector<uint64_t> b, e;
+  for (uint64_t v = 0; v < n; ++v) {
+    ri[v] = uint32_t(r.size());
+    for (uint64_t p = ptr[v]; p < ptr[v + 1]; p += kChunk) {
+      r.push_back(uint32_t(v));
+      b.push_back(p);
+      e.push_back(std::min<uint64_t>(ptr[v + 1], p + kChunk));
+    }
+  }
+  ri[n] = uint32_t(r.size());
+  nit = r.size();
+  rows.alloc(nit + 1, s);
+  beg.alloc(nit + 1, s);
+  end.alloc(nit + 1, s);
+  rowitem.alloc(n + 1, s);
+  if (nit) {
+    GM_CUDA(cudaMemcpyAsync(rows.get(), r.data(), nit * 4, cudaMemcpyHostToDevice, s));
+    GM_CUDA(cudaMemcpyAsync(beg.get(), b.data(), nit * 8, cudaMemcpyHostToDevice, s));
+    GM_CUDA(cudaMemcpyAsync(end.get(), e.data(), nit * 8, cudaMemcpyHostToDevice, s));
+  }
+  GM_CUDA(cudaMemcpyAsync(rowitem.get(), ri.data(), (n + 1) * 4, cudaMemcpyHostToDevice, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename RT>
+__device__ __forceinline__ float rating_at(const uint8_t* val, uint64_t e) {
+  return float(reinterpret_cast<const RT*>(val)[e]);
+}
+
+// K > 0: compile-time latent dimension (vectorised); K == 0: runtime k <= 64.
+template <int K, typename RT>
+__global__ void __launch_bounds__(256) k_cf_items(const uint32_t* __restrict__ rows,
+                                                  const uint64_t* __restrict__ ibeg,
+                                                  const uint64_t* __restrict__ iend, uint64_t nit,
+                                                  const uint32_t* __restrict__ idx,
+                                                  const uint8_t* __restrict__ val,
+                                                  const float* __restrict__ f, int kr,
+                                                  float* __restrict__ part, float* __restrict__ sq) {
+  constexpr int KM = K > 0 ? K : 64;
+  const int k = K > 0 ? K : kr;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  for (uint64_t it = warp; it < nit; it += nwarps) {
+    const uint32_t row = rows[it];
+    const uint64_t b = ibeg[it], e1 = iend[it];
+    float p[KM], acc[KM];
+    const float* pr = f + uint64_t(row) * k;
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      if (K == 0 && i >= k) break;
+      p[i] = pr[i];
+      acc[i] = 0.0f;
+    }
+    float s2 = 0.0f;
+    for (uint64_t e = b + lane; e < e1; e += 32) {
+      const float* q = f + uint64_t(idx[e]) * k;
+      float qv[KM];
+      if constexpr (K > 0 && (K % 4) == 0) {
+#pragma unroll
+        for (int i = 0; i < K; i += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(q + i);
+          qv[i] = t.x;
+          qv[i + 1] = t.y;
+          qv[i + 2] = t.z;
+          qv[i + 3] = t.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < KM; ++i) {
+          if (K == 0 && i >= k) break;
+          qv[i] = q[i];
+        }
+      }
+      float dot = 0.0f;
+#pragma unroll
+      for (int i = 0; i < KM; ++i) {
+        if (K == 0 && i >= k) break;
+        dot += p[i] * qv[i];
+      }
+      const float err = rating_at<RT>(val, e) - dot;
+      s2 += err * err;
+#pragma unroll
+      for (int i = 0; i < KM; ++i) {
+        if (K == 0 && i >= k) break;
+        acc[i] += err * qv[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      if (K == 0 && i >= k) break;
+      float a = acc[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) part[it * uint64_t(k) + i] = a;
+    }
+    if (sq) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (lane == 0) sq[it] = s2;
+    }
+  }
+}
+
+// p' = p + gamma * (sum - lambda * p); sum = out-route items then in-route items.
+__global__ void k_cf_apply(uint64_t n, int k, const uint32_t* rit, const uint32_t* rif,
+                           const float* part_t, const float* part_f, const float* f, float* fn,
+                           float gamma, float lambda, unsigned long long* changed) {
+  unsigned long long ch = 0;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n * uint64_t(k);
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t v = t / k;
+    const int i = int(t % k);
+    float s = 0.0f;
+    const uint32_t a0 = rit[v], a1 = rit[v + 1], b0 = rif[v], b1 = rif[v + 1];
+    bool any = false;
+    for (uint32_t j = a0; j < a1; ++j) {
+      s = any ? s + part_t[uint64_t(j) * k + i] : part_t[uint64_t(j) * k + i];
+      any = true;
+    }
+    float si = 0.0f;
+    bool anyi = false;
+    for (uint32_t j = b0; j < b1; ++j) {
+      si = anyi ? si + part_f[uint64_t(j) * k + i] : part_f[uint64_t(j) * k + i];
+      anyi = true;
+    }
+    if (anyi) s = any ? s + si : si;
+    const float p = f[t];
+    const float np = p + gamma * (s - lambda * p);
+    fn[t] = np;
+    ch += (__float_as_uint(np) != __float_as_uint(p)) && (any || anyi);
+  }
+  warp_add_u64(changed, ch);
+}
+
+__global__ void k_sum_sq(const float* sq, uint64_t nit, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (uint64_t i = threadIdx.x; i < nit; i += blockDim.x) s += sq[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+__global__ void k_bipartite_check(const uint32_t* outdeg, const uint32_t* indeg, uint64_t n,
+                                  const uint32_t* iperm, unsigned long long* bad) {
+  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
+       v += uint64_t(gridDim.x) * blockDim.x)
+    if (outdeg[v] && indeg[v]) atomicMin(bad, (unsigned long long)(iperm ? iperm[v] : v));
+}
+
+__global__ void k_cf_random_init(uint64_t total, float hi, float* f) {
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t o[4];
+    philox4x32_10(uint32_t(t), uint32_t(t >> 32), 0, 0x43464E49u, 1u, 0u, o);
+    f[t] = hi * (float(o[0] >> 8) * (1.0f / 16777216.0f));
+  }
+}
+
+template <int K, typename RT>
+void launch_items(const CfCache& c, const Csr& csr, bool fwd, const float* f, int k, cudaStream_t s,
+                  float* sq) {
+  const uint64_t nit = fwd ? c.nit_f : c.nit_t;
+  if (!nit) return;
+  const unsigned grid = grid_for(nit * 32, 256);
+  k_cf_items<K, RT><<<grid, 256, 0, s>>>(fwd ? c.items_f.get() : c.items_t.get(),
+                                         fwd ? c.ibeg_f.get() : c.ibeg_t.get(),
+                                         fwd ? c.iend_f.get() : c.iend_t.get(), nit, csr.idx.get(),
+                                         csr.val.get(), f, k,
+                                         fwd ? c.part_f.get() : c.part_t.get(), sq);
+  GM_LAUNCH_CHECK();
+}
+
+template <typename RT>
+void pass(const CfCache& c, Graph& g, bool fwd, const float* f, int k, float* sq) {
+  const Csr& csr = fwd ? g.fwd() : g.in;
+  if (k == 20)
+    launch_items<20, RT>(c, csr, fwd, f, k, g.stream, sq);
+  else
+    launch_items<0, RT>(c, csr, fwd, f, k, g.stream, sq);
+}
+
+}  // namespace
+
+std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
+                                   const float* init, float* out, double* rmse_trace) {
+  if (k <= 0) fail(GM_EINPUT, "cf: k must be positive");
+  if (k > 64) fail(GM_EUSAGE, "cf: k above 64 is not supported");
+  if (!(gamma > 0.0f)) fail(GM_EINPUT, "cf: gamma must be positive");
+  if (!(lambda >= 0.0f)) fail(GM_EINPUT, "cf: lambda must be non-negative");
+  if (g.value_type != GM_VAL_U8 && g.value_type != GM_VAL_F32 && g.value_type != GM_VAL_F64)
+    fail(GM_EUSAGE, "cf: ratings must be stored as u8, f32 or f64");
+  const uint64_t n = g.n;
+  cudaStream_t s = g.stream;
+  std::vector<gm_iteration_stats> stats;
+  ensure_forward(g);
+  {
+    DevBuf<unsigned long long> bad(1, s);
+    GM_CUDA(cudaMemsetAsync(bad.get(), 0xFF, 8, s));
+    if (n)
+      k_bipartite_check<<<grid_for(n, 256), 256, 0, s>>>(g.outdeg.get(), g.indeg.get(), n,
+                                                         g.relabeled ? g.iperm.get() : nullptr,
+                                                         bad.get());
+    GM_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    GM_CUDA(cudaMemcpyAsync(&h, bad.get(), 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    if (h != ~0ull)
+      fail(GM_EINPUT, "cf: vertex " + std::to_string(h + 1) +
+                          " (1-based) has both outgoing and incoming ratings; graph is not bipartite");
+  }
+  if (!g.cf || g.cf->k != k) {
+    g.cf = std::unique_ptr<CfCache, void (*)(CfCache*)>(new CfCache(), [](CfCache* p) { delete p; });
+    CfCache& c = *g.cf;
+    c.k = k;
+    build_items(g.in, n, c.items_t, c.ibeg_t, c.iend_t, c.rowitem_t, c.nit_t, s);
+    build_items(g.fwd(), n, c.items_f, c.ibeg_f, c.iend_f, c.rowitem_f, c.nit_f, s);
+    c.part_t.alloc((c.nit_t + 1) * k, s);
+    c.part_f.alloc((c.nit_f + 1) * k, s);
+    c.sq.alloc(c.nit_f + 1, s);
+    c.f0.alloc(n * k + 4, s);
+    c.f1.alloc(n * k + 4, s);
+    c.scal.alloc(2, s);
+    c.ctr.alloc(2, s);
+  }
+  CfCache& c = *g.cf;
+  const uint64_t total = n * uint64_t(k);
+  if (init) {
+    DevBuf<float> tmp(total, s);
+    GM_CUDA(cudaMemcpyAsync(tmp.get(), init, total * 4, cudaMemcpyHostToDevice, s));
+    to_internal(g, tmp.get(), c.f0.get(), size_t(k) * 4);
+  } else if (total) {
+    k_cf_random_init<<<grid_for(total, 256), 256, 0, s>>>(total, 1.0f / std::sqrt(float(k)), c.f0.get());
+    GM_LAUNCH_CHECK();
+  }
+  float* f = c.f0.get();
+  float* fn = c.f1.get();
+  const uint64_t m = g.in.nnz;
+  auto run_pass = [&](bool fwd, const float* fac, float* sq) {
+    switch (g.value_type) {
+      case GM_VAL_U8: pass<uint8_t>(c, g, fwd, fac, int(k), sq); break;
+      case GM_VAL_F32: pass<float>(c, g, fwd, fac, int(k), sq); break;
+      default: pass<double>(c, g, fwd, fac, int(k), sq); break;
+    }
+  };
+  auto read_rmse = [&]() {
+    k_sum_sq<<<1, 256, 0, s>>>(c.sq.get(), c.nit_f, c.scal.get());
+    GM_LAUNCH_CHECK();
+    double h = 0;
+    GM_CUDA(cudaMemcpyAsync(&h, c.scal.get(), 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    return m ? std::sqrt(h / double(m)) : 0.0;
+  };
+  cudaEvent_t e0, e1;
+  GM_CUDA(cudaEventCreate(&e0));
+  GM_CUDA(cudaEventCreate(&e1));
+  for (int64_t it = 1; it <= iters; ++it) {
+    GM_CUDA(cudaEventRecord(e0, s));
+    c.ctr.zero(s);
+    run_pass(false, f, nullptr);  // items receive from users (G^T)
+    run_pass(true, f, c.sq.get());  // users receive from items (G); squared errors
+    if (total)
+      k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
+                                                      c.part_t.get(), c.part_f.get(), f, fn, gamma,
+                                                      lambda, c.ctr.get());
+    GM_LAUNCH_CHECK();
+    GM_CUDA(cudaEventRecord(e1, s));
+    if (rmse_trace && it > 1) rmse_trace[it - 2] = read_rmse();  // post-update RMSE of it-1
+    unsigned long long ch = 0;
+    GM_CUDA(cudaMemcpyAsync(&ch, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    GM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    gm_iteration_stats st{};
+    st.iteration = it;
+    st.active_before = int64_t(n);
+    st.messages_generated = int64_t(n);
+    st.vertices_updated = int64_t(ch);
+    st.spmv_seconds = ms * 1e-3;
+    st.total_seconds = ms * 1e-3;
+    st.edges_processed = int64_t(2 * m);
+    st.bytes_algorithmic = int64_t(2 * 5 * m + 2 * 8 * (n + 2) + 3 * 4 * uint64_t(k) * n);
+    st.direction = 0;
+    stats.push_back(st);
+    std::swap(f, fn);
+  }
+  if (rmse_trace && iters > 0) {
+    run_pass(true, f, c.sq.get());
+    rmse_trace[iters - 1] = read_rmse();
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (out && total) {
+    DevBuf<float> ext(total, s);
+    to_external(g, f, ext.get(), size_t(k) * 4);
+    GM_CUDA(cudaMemcpyAsync(out, ext.get(), total * 4, cudaMemcpyDeviceToHost, s));
+  }
+  GM_CUDA(cudaStreamSynchronize(s));
+  return stats;
+}
+
+}  // namespace gm

@@ -1,0 +1,422 @@
+// engine.cuh -- device-side VertexProgram engine (generic path, exact semantics).
+//
+// Mirrors semigraph::Engine (include/semigraph/engine.hpp:67-264) for ANY
+// program: user functors are __device__ members of a program struct compiled
+// into the kernels below as template parameters.  The device program contract
+// restates the VertexProgram concept (include/semigraph/core.hpp:239-253):
+//
+//   using vertex_t, message_t, reduced_t, edge_t;   // edge_t = gm::NoEdge to ignore values
+//   static constexpr gm_value_type kEdgeType;        // storage the program reads
+//   __host__ __device__ Direction direction() const;
+//   __device__ bool send_message(const vertex_t&, uint64_t v, message_t* out) const;  // false = nullopt
+//   __device__ reduced_t process_message(const message_t&, const edge_t&, const vertex_t& dst) const;
+//   __device__ reduced_t reduce(const reduced_t&, const reduced_t&) const;
+//   __device__ reduced_t reduce_identity() const;
+//   __device__ vertex_t apply(const reduced_t&, const vertex_t&) const;
+//   __device__ bool equal(const vertex_t&, const vertex_t&) const;                      // operator==
+//
+// Programs that can fail set `static constexpr bool kCanFail = true` and take a
+// trailing `int& err` in send/process/apply (the device analogue of a throwing
+// callback); the engine attaches the vertex / (column, row) context exactly like
+// engine.hpp:90-94, 158-162, 251-257.
+//
+// Semantics (SURVEY.md 8b rules S1-S9): bulk-synchronous reads, y valid iff one
+// contribution landed, first fold reduce(identity, r), per-row fold order =
+// ascending internal source id (caller order on graphs built without
+// GM_RELABEL), BOTH merges out-route first, apply clears all flags and
+// re-activates changed vertices only, zero budget is a no-op.
+//
+// Layout: properties / messages / reduced values are AoS device arrays in
+// internal order; validity and activity are 32-bit-word bitmaps built with
+// __ballot_sync (one word per warp, no atomics on the flags).  The pull SpMV is
+// one thread per destination row so the fold order is the reference's; the
+// specialised kernels (pagerank.cu, traversal.cu, cf.cu) trade that order for
+// throughput where the program's reduce is exact or tolerance-checked.
+#pragma once
+
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "graph.cuh"
+
+namespace gm {
+
+enum class Direction : int { OUT = 0, IN = 1, BOTH = 2 };
+
+struct NoEdge {};
+
+template <typename P, typename = void>
+struct can_fail : std::false_type {};
+template <typename P>
+struct can_fail<P, std::void_t<decltype(P::kCanFail)>> : std::bool_constant<P::kCanFail> {};
+
+enum Phase : int { kPhaseNone = 0, kPhaseSend = 1, kPhaseSpmv = 2, kPhaseApply = 3 };
+
+struct DevError {
+  int code;
+  int phase;
+  uint64_t vertex, col, row;
+};
+
+__device__ __forceinline__ void record_error(DevError* e, int code, int phase, uint64_t v,
+                                             uint64_t col, uint64_t row) {
+  if (atomicCAS(&e->code, 0, code) == 0) {
+    e->phase = phase;
+    e->vertex = v;
+    e->col = col;
+    e->row = row;
+  }
+}
+
+template <typename E>
+__device__ __forceinline__ E load_edge(const uint8_t* val, uint64_t e) {
+  if constexpr (std::is_same_v<E, NoEdge>) {
+    return E{};
+  } else {
+    return reinterpret_cast<const E*>(val)[e];
+  }
+}
+
+__device__ __forceinline__ uint64_t ext_id(const uint32_t* iperm, uint64_t v) {
+  return iperm ? uint64_t(iperm[v]) : v;
+}
+
+// ---------------------------------------------------------------- kernels
+// Phase 1, engine.hpp:76-98: x[v] = send(prop[v]) for active v.
+template <typename P>
+__global__ void k_send(P p, uint64_t n, const typename P::vertex_t* props, const uint32_t* active,
+                       const uint32_t* iperm, typename P::message_t* x, uint32_t* xbits,
+                       unsigned long long* ctr, DevError* err) {
+  const uint64_t words = (n + 31) / 32;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = warp; w < words; w += nwarps) {
+    const uint64_t v = w * 32 + lane_id();
+    const bool act = v < n && bit_test(active, uint32_t(v));
+    bool ok = false;
+    if (act) {
+      typename P::message_t m;
+      if constexpr (can_fail<P>::value) {
+        int ec = 0;
+        ok = p.send_message(props[v], ext_id(iperm, v), &m, ec);
+        if (ec) {
+          record_error(err, ec, kPhaseSend, ext_id(iperm, v), 0, 0);
+          ok = false;
+        }
+      } else {
+        ok = p.send_message(props[v], ext_id(iperm, v), &m);
+      }
+      if (ok) x[v] = m;
+    }
+    const unsigned ab = __ballot_sync(0xffffffffu, act);
+    const unsigned ob = __ballot_sync(0xffffffffu, ok);
+    if (lane_id() == 0) {
+      xbits[w] = ob;
+      if (ab) atomicAdd(&ctr[0], (unsigned long long)__popc(ab));
+      if (ob) atomicAdd(&ctr[1], (unsigned long long)__popc(ob));
+    }
+  }
+}
+
+// Phase 2, engine.hpp:224-260: one thread per destination row, entries in
+// ascending source order, first contribution folded as reduce(identity, r).
+template <typename P>
+__global__ void k_pull(P p, uint64_t n, const uint64_t* ptr, const uint32_t* idx,
+                       const uint8_t* val, const typename P::message_t* x, const uint32_t* xbits,
+                       const typename P::vertex_t* props, const uint32_t* iperm,
+                       typename P::reduced_t* y, uint32_t* ybits, DevError* err) {
+  using R = typename P::reduced_t;
+  const uint64_t words = (n + 31) / 32;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = warp; w < words; w += nwarps) {
+    const uint64_t k = w * 32 + lane_id();
+    bool any = false;
+    if (k < n) {
+      R acc = p.reduce_identity();
+      const uint64_t e1 = ptr[k + 1];
+      for (uint64_t e = ptr[k]; e < e1; ++e) {
+        const uint32_t j = idx[e];
+        if (!bit_test(xbits, j)) continue;
+        R r;
+        if constexpr (can_fail<P>::value) {
+          int ec = 0;
+          r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k], ec);
+          if (ec) {
+            record_error(err, ec, kPhaseSpmv, 0, ext_id(iperm, j), ext_id(iperm, k));
+            break;
+          }
+        } else {
+          r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k]);
+        }
+        acc = any ? p.reduce(acc, r) : p.reduce(p.reduce_identity(), r);
+        any = true;
+      }
+      if (any) y[k] = acc;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, any);
+    if (lane_id() == 0) ybits[w] = b;
+  }
+}
+
+// BOTH merge, engine.hpp:113-126: y_in folded into y_out, out-route first.
+template <typename P>
+__global__ void k_merge(P p, uint64_t n, typename P::reduced_t* y, uint32_t* ybits,
+                        const typename P::reduced_t* y2, const uint32_t* y2bits) {
+  const uint64_t words = (n + 31) / 32;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = warp; w < words; w += nwarps) {
+    const uint64_t v = w * 32 + lane_id();
+    if (v < n) {
+      const bool o = bit_test(ybits, uint32_t(v)), i = bit_test(y2bits, uint32_t(v));
+      if (o && i)
+        y[v] = p.reduce(y[v], y2[v]);
+      else if (i)
+        y[v] = y2[v];
+    }
+    __syncwarp();
+    if (lane_id() == 0) ybits[w] |= y2bits[w];
+  }
+}
+
+// Phase 3, engine.hpp:139-172: clear every flag, apply where y is valid,
+// re-activate iff the state changed.
+template <typename P>
+__global__ void k_apply(P p, uint64_t n, const typename P::reduced_t* y, const uint32_t* ybits,
+                        typename P::vertex_t* props, uint32_t* active, const uint32_t* iperm,
+                        unsigned long long* ctr, DevError* err) {
+  const uint64_t words = (n + 31) / 32;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = warp; w < words; w += nwarps) {
+    const uint64_t v = w * 32 + lane_id();
+    bool upd = false;
+    if (v < n && bit_test(ybits, uint32_t(v))) {
+      const typename P::vertex_t old = props[v];
+      typename P::vertex_t fresh;
+      bool okv = true;
+      if constexpr (can_fail<P>::value) {
+        int ec = 0;
+        fresh = p.apply(y[v], old, ec);
+        if (ec) {
+          record_error(err, ec, kPhaseApply, ext_id(iperm, v), 0, 0);
+          okv = false;
+        }
+      } else {
+        fresh = p.apply(y[v], old);
+      }
+      if (okv && !p.equal(fresh, old)) {
+        props[v] = fresh;
+        upd = true;
+      }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, upd);
+    if (lane_id() == 0) {
+      active[w] = b;
+      if (b) atomicAdd(&ctr[2], (unsigned long long)__popc(b));
+    }
+  }
+}
+
+__global__ void k_bytes_to_bits(const uint8_t* bytes, uint64_t n, uint32_t* bits);
+__global__ void k_bits_to_bytes(const uint32_t* bits, uint64_t n, uint8_t* bytes);
+
+// ------------------------------------------------------------------ host side
+template <typename P>
+class Engine {
+ public:
+  using V = typename P::vertex_t;
+  using M = typename P::message_t;
+  using R = typename P::reduced_t;
+
+  Engine(Graph& g, const P& p) : g_(g), p_(p), s_(g.stream) {
+    if constexpr (!std::is_same_v<typename P::edge_t, NoEdge>) {
+      if (g.value_type != P::kEdgeType)
+        fail(GM_EUSAGE, std::string("program reads ") + value_name(P::kEdgeType) +
+                            " edge values but the graph stores " + value_name(g.value_type));
+    }
+    const Direction d = p_.direction();
+    if (d != Direction::OUT) ensure_forward(g_);  // engine.hpp:107, 195
+    const uint64_t n = g_.n, words = (n + 31) / 32;
+    props_.alloc(n, s_);
+    active_.alloc(words + 1, s_);
+    active_.zero(s_);
+    x_.alloc(n, s_);
+    xbits_.alloc(words + 1, s_);
+    y_.alloc(n, s_);
+    ybits_.alloc(words + 1, s_);
+    if (d == Direction::BOTH) {
+      y2_.alloc(n, s_);
+      y2bits_.alloc(words + 1, s_);
+    }
+    ctr_.alloc(3, s_);
+    err_.alloc(1, s_);
+    GM_CUDA(cudaEventCreate(&e0_));
+    GM_CUDA(cudaEventCreate(&e1_));
+    GM_CUDA(cudaEventCreate(&e2_));
+    GM_CUDA(cudaEventCreate(&e3_));
+  }
+  ~Engine() {
+    cudaEventDestroy(e0_);
+    cudaEventDestroy(e1_);
+    cudaEventDestroy(e2_);
+    cudaEventDestroy(e3_);
+  }
+
+  // Caller-order host arrays -> internal device state.
+  void load(const void* props_host, const uint8_t* active_host) {
+    const uint64_t n = g_.n;
+    if (!n) return;
+    DevBuf<V> tmp(n, s_);
+    GM_CUDA(cudaMemcpyAsync(tmp.get(), props_host, n * sizeof(V), cudaMemcpyHostToDevice, s_));
+    to_internal(g_, tmp.get(), props_.get(), sizeof(V));
+    DevBuf<uint8_t> a(n, s_), ai(n, s_);
+    GM_CUDA(cudaMemcpyAsync(a.get(), active_host, n, cudaMemcpyHostToDevice, s_));
+    to_internal(g_, a.get(), ai.get(), 1);
+    k_bytes_to_bits<<<grid_for((n + 31) / 32, 256), 256, 0, s_>>>(ai.get(), n, active_.get());
+    GM_LAUNCH_CHECK();
+    GM_CUDA(cudaStreamSynchronize(s_));
+  }
+
+  void store(void* props_host, uint8_t* active_host) {
+    const uint64_t n = g_.n;
+    if (!n) return;
+    DevBuf<V> tmp(n, s_);
+    to_external(g_, props_.get(), tmp.get(), sizeof(V));
+    GM_CUDA(cudaMemcpyAsync(props_host, tmp.get(), n * sizeof(V), cudaMemcpyDeviceToHost, s_));
+    bits_out(active_.get(), active_host);
+  }
+
+  void bits_out(const uint32_t* bits, uint8_t* host) {
+    const uint64_t n = g_.n;
+    DevBuf<uint8_t> b(n, s_), be(n, s_);
+    k_bits_to_bytes<<<grid_for(n, 256), 256, 0, s_>>>(bits, n, b.get());
+    GM_LAUNCH_CHECK();
+    to_external(g_, b.get(), be.get(), 1);
+    GM_CUDA(cudaMemcpyAsync(host, be.get(), n, cudaMemcpyDeviceToHost, s_));
+    GM_CUDA(cudaStreamSynchronize(s_));
+  }
+
+  void send() {
+    const uint64_t n = g_.n;
+    const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
+    k_send<P><<<grid, 256, 0, s_>>>(p_, n, props_.get(), active_.get(), iperm(), x_.get(),
+                                     xbits_.get(), ctr_.get(), err_.get());
+    GM_LAUNCH_CHECK();
+  }
+
+  void spmv() {
+    const uint64_t n = g_.n;
+    const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
+    const Direction d = p_.direction();
+    const Csr& first = d == Direction::IN ? g_.fwd() : g_.in;
+    k_pull<P><<<grid, 256, 0, s_>>>(p_, n, first.ptr.get(), first.idx.get(), first.val.get(),
+                                     x_.get(), xbits_.get(), props_.get(), iperm(), y_.get(),
+                                     ybits_.get(), err_.get());
+    GM_LAUNCH_CHECK();
+    if (d == Direction::BOTH) {
+      const Csr& f = g_.fwd();
+      k_pull<P><<<grid, 256, 0, s_>>>(p_, n, f.ptr.get(), f.idx.get(), f.val.get(), x_.get(),
+                                       xbits_.get(), props_.get(), iperm(), y2_.get(),
+                                       y2bits_.get(), err_.get());
+      GM_LAUNCH_CHECK();
+      k_merge<P><<<grid, 256, 0, s_>>>(p_, n, y_.get(), ybits_.get(), y2_.get(), y2bits_.get());
+      GM_LAUNCH_CHECK();
+    }
+  }
+
+  void apply() {
+    const uint64_t n = g_.n;
+    const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
+    k_apply<P><<<grid, 256, 0, s_>>>(p_, n, y_.get(), ybits_.get(), props_.get(), active_.get(),
+                                      iperm(), ctr_.get(), err_.get());
+    GM_LAUNCH_CHECK();
+  }
+
+  // Engine::step (engine.hpp:176-189).
+  gm_iteration_stats step() {
+    gm_iteration_stats st{};
+    if (g_.n == 0) return st;
+    ctr_.zero(s_);
+    err_.zero(s_);
+    GM_CUDA(cudaEventRecord(e0_, s_));
+    send();
+    GM_CUDA(cudaEventRecord(e1_, s_));
+    spmv();
+    GM_CUDA(cudaEventRecord(e2_, s_));
+    check_error();  // a failed SpMV aborts before apply (engine.hpp:251-257)
+    apply();
+    GM_CUDA(cudaEventRecord(e3_, s_));
+    unsigned long long c[3];
+    GM_CUDA(cudaMemcpyAsync(c, ctr_.get(), sizeof(c), cudaMemcpyDeviceToHost, s_));
+    GM_CUDA(cudaStreamSynchronize(s_));
+    check_error();
+    float spmv_ms = 0, total_ms = 0;
+    GM_CUDA(cudaEventElapsedTime(&spmv_ms, e1_, e2_));
+    GM_CUDA(cudaEventElapsedTime(&total_ms, e0_, e3_));
+    st.active_before = int64_t(c[0]);
+    st.messages_generated = int64_t(c[1]);
+    st.vertices_updated = int64_t(c[2]);
+    st.spmv_seconds = spmv_ms * 1e-3;
+    st.total_seconds = total_ms * 1e-3;
+    const Direction d = p_.direction();
+    st.edges_processed = int64_t(d == Direction::BOTH ? 2 * g_.m : g_.m);
+    st.direction = 0;
+    return st;
+  }
+
+  // Engine::run_graph_program (engine.hpp:193-213).
+  std::vector<gm_iteration_stats> run(int64_t max_iters) {
+    std::vector<gm_iteration_stats> out;
+    for (int64_t it = 1; it <= max_iters; ++it) {
+      gm_iteration_stats st = step();
+      st.iteration = it;
+      out.push_back(st);
+      if (st.vertices_updated == 0) break;
+    }
+    return out;
+  }
+
+  void check_error() {
+    DevError h{};
+    GM_CUDA(cudaMemcpyAsync(&h, err_.get(), sizeof(h), cudaMemcpyDeviceToHost, s_));
+    GM_CUDA(cudaStreamSynchronize(s_));
+    if (!h.code) return;
+    const std::string what = P::error_message(h.code);
+    switch (h.phase) {
+      case kPhaseSend:
+        fail(GM_EENGINE, "send_message failed at vertex " + std::to_string(h.vertex) + ": " + what);
+      case kPhaseApply:
+        fail(GM_EENGINE, "apply failed at vertex " + std::to_string(h.vertex) + ": " + what);
+      default:
+        fail(GM_EENGINE, "vertex program callback failed at (column " + std::to_string(h.col) +
+                             ", row " + std::to_string(h.row) + "): " + what);
+    }
+  }
+
+  const uint32_t* iperm() const { return g_.relabeled ? g_.iperm.get() : nullptr; }
+  Graph& graph() { return g_; }
+  DevBuf<M>& x() { return x_; }
+  DevBuf<R>& y() { return y_; }
+  DevBuf<uint32_t>& xbits() { return xbits_; }
+  DevBuf<uint32_t>& ybits() { return ybits_; }
+  cudaStream_t stream() const { return s_; }
+
+ private:
+  Graph& g_;
+  P p_;
+  cudaStream_t s_;
+  DevBuf<V> props_;
+  DevBuf<uint32_t> active_;
+  DevBuf<M> x_;
+  DevBuf<uint32_t> xbits_;
+  DevBuf<R> y_, y2_;
+  DevBuf<uint32_t> ybits_, y2bits_;
+  DevBuf<unsigned long long> ctr_;
+  DevBuf<DevError> err_;
+  cudaEvent_t e0_{}, e1_{}, e2_{}, e3_{};
+};
+
+}  // namespace gm

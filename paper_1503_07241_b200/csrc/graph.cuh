@@ -1,0 +1,75 @@
+// graph.cuh -- device-resident graph: CSR(G^T) (+ lazily CSR(G)) over internal ids.
+//
+// Replaces semigraph::Graph (include/semigraph/dcsc.hpp:183-238).  The reference
+// keeps G^T as nnz-balanced DCSC row partitions (dcsc.hpp:43-65); here the whole
+// transpose is one CSR with int64 offsets and int32 column ids (4 B/entry instead
+// of the reference's 16 B), rows = destination, entries = sources ascending.
+// Optional relabeling (GM_RELABEL) orders internal ids by out-degree, descending,
+// so hot sources are contiguous (gather locality) -- results are always mapped
+// back to caller ids.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gm {
+
+struct Csr {
+  uint64_t n = 0, nnz = 0;
+  DevBuf<uint64_t> ptr;  // n + 1
+  DevBuf<uint32_t> idx;  // nnz
+  DevBuf<uint8_t> val;   // nnz * value_size(value_type)
+};
+
+struct PrCache;    // pagerank.cu
+struct TravCache;  // traversal.cu
+struct CfCache;    // cf.cu
+
+struct Graph {
+  uint64_t n = 0, m = 0;
+  uint32_t flags = 0;
+  int value_type = GM_VAL_NONE;
+  int device = 0;
+  bool symmetric = false;
+  bool relabeled = false;
+  unsigned nb = 1;  // bits per vertex id
+  cudaStream_t stream = nullptr;
+
+  DevBuf<uint32_t> perm;   // caller id -> internal id (empty when identity)
+  DevBuf<uint32_t> iperm;  // internal id -> caller id
+  DevBuf<uint32_t> outdeg; // internal order
+  DevBuf<uint32_t> indeg;  // internal order
+  uint64_t nonzero_outdeg = 0;
+
+  Csr in;    // CSR(G^T): row k lists sources j of edges j -> k
+  Csr out;   // CSR(G):   row j lists destinations k of edges j -> k
+  bool out_built = false;
+  bool out_alias = false;  // symmetric and value-less: CSR(G) == CSR(G^T)
+
+  std::unique_ptr<PrCache, void (*)(PrCache*)> pr{nullptr, nullptr};
+  std::unique_ptr<TravCache, void (*)(TravCache*)> trav{nullptr, nullptr};
+  std::unique_ptr<CfCache, void (*)(CfCache*)> cf{nullptr, nullptr};
+
+  const Csr& fwd() const { return out_alias ? in : out; }
+  uint64_t device_bytes() const;
+};
+
+// ingest.cu
+Graph* graph_create(const gm_edge_list& e, uint64_t n, uint32_t flags, int storage);
+Graph* graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c,
+                           uint64_t seed, int permute, uint32_t flags, int weights);
+Graph* graph_generate_bipartite(uint32_t users, uint32_t items, double c_num, uint32_t cap,
+                                uint64_t seed, uint32_t flags);
+void graph_destroy(Graph* g);
+void ensure_forward(Graph& g);
+void export_edges(Graph& g, uint32_t* src, uint32_t* dst, void* values);
+void degree_vector(Graph& g, int kind, uint64_t* out);
+uint64_t pick_source(Graph& g, uint64_t seed);
+
+// Gather/scatter between caller order and internal order (elem_bytes wide).
+void to_internal(Graph& g, const void* ext_dev, void* int_dev, size_t elem_bytes);
+void to_external(Graph& g, const void* int_dev, void* ext_dev, size_t elem_bytes);
+
+}  // namespace gm

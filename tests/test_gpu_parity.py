@@ -1,0 +1,312 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bars (BASELINE.json north_star): bit-exact BFS levels and integer SSSP
+distances (+ identical per-superstep IterationStats), PageRank fp32 within
+1e-5 relative L1 of the fp64 oracle, CF RMSE within 1e-4 while finite; the
+generic engine bit-exact with the reference on fp64 programs.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+INF32 = 2**32 - 1
+
+
+def rel_l1(got, want):
+    want = np.asarray(want, np.float64)
+    return float(np.abs(np.asarray(got, np.float64) - want).sum() / np.abs(want).sum())
+
+
+def _bits(a):
+    return np.asarray(a, np.float64).view(np.uint64)
+
+
+def _stats_key(st):
+    return [s.key() for s in st]
+
+
+# ------------------------------------------------------------ generators
+
+@pytest.mark.parametrize("relabel", [False, True])
+@pytest.mark.parametrize("sym", [False, True])
+def test_rmat_ingest_bitexact(gm, orc, relabel, sym):
+    g = gm.Graph.rmat(12, 16, seed=11, symmetrize=sym, relabel=relabel)
+    s, d, _ = g.edges()
+    os_, od = orc.rmat(12, 16, seed=11)
+    ws, wd, _ = orc.preprocess(os_, od, symmetrize=sym)
+    assert np.array_equal(s, ws) and np.array_equal(d, wd)
+    assert g.num_edges == len(ws)
+
+
+def test_rmat_weights_bitexact(gm, orc):
+    g = gm.Graph.rmat(11, 16, seed=5, weights=True, relabel=True)
+    s, d, w = g.edges()
+    assert np.array_equal(w, orc.edge_weights(5, s, d))
+
+
+def test_bipartite_bitexact(gm, orc):
+    g = gm.Graph.bipartite(3000, 400, 30000.0, 400, seed=9)
+    s, d, r = g.edges()
+    os_, od = orc.bipartite(3000, 400, 30000.0, 400, 9)
+    ws, wd, _ = orc.preprocess(os_, od)
+    assert np.array_equal(s, ws) and np.array_equal(d, wd)
+    assert np.array_equal(r, orc.ratings(9, s, d))
+
+
+def test_degree_vector_and_forward(gm):
+    # tests/test_engine.cpp:238-253
+    g = gm.Graph.from_edges([0, 0, 1], [1, 2, 2], 3)
+    assert not g.forward_built()
+    assert list(g.degree_vector("out")) == [2, 1, 0]
+    assert not g.forward_built()
+    assert list(g.degree_vector("in")) == [0, 1, 2]
+    g.ensure_forward()
+    assert g.forward_built()
+    assert list(g.degree_vector("out")) == [2, 1, 0]
+
+
+# --------------------------------------------------- reference goldens
+
+@pytest.mark.parametrize("relabel", [False, True])
+def test_golden_traversals(gm, golden, relabel):
+    for key in golden["cases"]:
+        key = str(key)
+        n = int(golden[f"{key}_n"][0])
+        s, d = golden[f"{key}_src"], golden[f"{key}_dst"]
+        root = int(golden[f"{key}_root"][0])
+        # BFS on the symmetrised graph (preprocessed on the GPU from the raw list)
+        g = gm.Graph.from_edges(s, d, n, symmetrize=True, relabel=relabel)
+        lvl, st = gm.bfs(g, root)
+        want = golden[f"{key}_bfs"]
+        assert np.array_equal(lvl, np.where(np.isinf(want), -1, want).astype(np.int32)), key
+        assert np.array_equal(np.array(_stats_key(st)), golden[f"{key}_bfs_stats"]), key
+        # integer SSSP
+        g = gm.Graph.from_edges(s, d, n, golden[f"{key}_wint"].astype(np.uint8), relabel=relabel)
+        dist, st = gm.sssp(g, root)
+        want = golden[f"{key}_sssp_int"]
+        assert np.array_equal(dist, np.where(np.isinf(want), INF32, want).astype(np.uint32)), key
+        assert np.array_equal(np.array(_stats_key(st)), golden[f"{key}_sssp_int_stats"]), key
+
+
+def test_golden_generic_programs_bitexact(gm, golden):
+    """Generic engine vs the reference engine, bit for bit (no relabel)."""
+    for key in golden["cases"]:
+        key = str(key)
+        n = int(golden[f"{key}_n"][0])
+        s, d = golden[f"{key}_src"], golden[f"{key}_dst"]
+        root = int(golden[f"{key}_root"][0])
+        # reference PageRankProgram (activity gated, fp64)
+        g = gm.Graph.from_edges(s, d, n)
+        props = np.zeros(n, gm.PAGERANK_STATE)
+        props["rank"] = 1.0
+        props["out_degree"] = g.degree_vector("out")
+        act = np.ones(n, np.uint8)
+        st = gm.run_graph_program(g, gm.PROG_PAGERANK_REF, props, act, 20, params=[0.15])
+        assert np.array_equal(_bits(props["rank"]), _bits(golden[f"{key}_prref"])), key
+        assert np.array_equal(np.array(_stats_key(st)), golden[f"{key}_prref_stats"]), key
+        # reference SsspProgram on real weights
+        g = gm.Graph.from_edges(s, d, n, golden[f"{key}_wreal"])
+        dist = np.full(n, np.inf)
+        dist[root] = 0.0
+        act = np.zeros(n, np.uint8)
+        act[root] = 1
+        st = gm.run_graph_program(g, gm.PROG_SSSP_REF, dist, act, n + 1)
+        assert np.array_equal(_bits(dist), _bits(golden[f"{key}_sssp_real"])), key
+        assert np.array_equal(np.array(_stats_key(st)), golden[f"{key}_sssp_real_stats"]), key
+        # semiring (+, x) over int64, one SpMV (tests/acceptance.cpp:119-192)
+        g = gm.Graph.from_edges(s, d, n, golden[f"{key}_semi_vals"])
+        cell = np.zeros(n, gm.SEMIRING_CELL)
+        xv = golden[f"{key}_semi_xv"]
+        cell["x"] = np.where(xv, golden[f"{key}_semi_x"], 0)
+        cell["has_x"] = xv
+        _, _, y, yv = gm.superstep_phases(g, gm.PROG_SEMIRING_I64, cell, xv.astype(np.uint8))
+        assert np.array_equal(yv, golden[f"{key}_semi_yv"].astype(bool)), key
+        assert np.array_equal(y[yv], golden[f"{key}_semi_y"][yv]), key
+
+
+@pytest.mark.parametrize("relabel", [False, True])
+def test_golden_pagerank_norm(gm, golden, relabel):
+    for key in golden["cases"]:
+        key = str(key)
+        n = int(golden[f"{key}_n"][0])
+        g = gm.Graph.from_edges(golden[f"{key}_src"], golden[f"{key}_dst"], n, relabel=relabel)
+        r, st = gm.pagerank(g, 0.85, 20)
+        assert rel_l1(r, golden[f"{key}_prnorm"]) <= 1e-5, key
+        want = golden[f"{key}_prnorm_stats"]
+        assert [x.active_before for x in st] == list(want[:, 1])
+        assert [x.messages_generated for x in st] == list(want[:, 2])
+
+
+def test_golden_cf(gm, golden):
+    for t in range(4):
+        key = f"cf{t}"
+        n, k = (int(x) for x in golden[f"{key}_n"])
+        g = gm.Graph.from_edges(golden[f"{key}_src"], golden[f"{key}_dst"], n,
+                                golden[f"{key}_rating"].astype(np.float32))
+        f, rm, st = gm.collaborative_filtering_gd(g, k, 1e-3, 0.05, 10,
+                                                  init=golden[f"{key}_init"])
+        np.testing.assert_allclose(rm, golden[f"{key}_rmse"], atol=1e-4)
+        np.testing.assert_allclose(f, golden[f"{key}_factors"], rtol=1e-4, atol=1e-6)
+        assert len(st) == 10
+
+
+# ------------------------------------------------------- engine semantics
+# Ports of tests/test_engine.cpp (cited per test).
+
+def chain():
+    return [0, 1], [1, 2], np.array([1.0, 10.0, 100.0])
+
+
+def test_bulk_synchronous_reads(gm):
+    # test_engine.cpp:104-122
+    s, d, v = chain()
+    g = gm.Graph.from_edges(s, d, 3)
+    props = v.copy()
+    act = np.ones(3, np.uint8)
+    st = gm.run_graph_program(g, gm.PROG_ADD_PROBE, props, act, 1)
+    assert st[0].key() == (1, 3, 3, 2)
+    assert list(props) == [1.0, 11.0, 110.0]
+    assert list(act) == [0, 1, 1]
+
+
+def test_zero_budget_noop(gm):
+    # test_engine.cpp:124-131
+    s, d, v = chain()
+    g = gm.Graph.from_edges(s, d, 3)
+    props = v.copy()
+    act = np.ones(3, np.uint8)
+    assert gm.run_graph_program(g, gm.PROG_ADD_PROBE, props, act, 0) == []
+    assert props[1] == 10.0 and act.sum() == 3
+
+
+def test_fixpoint_terminates(gm):
+    # test_engine.cpp:133-143
+    s, d, v = chain()
+    g = gm.Graph.from_edges(s, d, 3)
+    st = gm.run_graph_program(g, gm.PROG_FIXED_PROBE, v.copy(), np.ones(3, np.uint8), 50)
+    assert len(st) == 1 and st[0].vertices_updated == 0
+
+
+def test_active_without_out_edges(gm):
+    # test_engine.cpp:145-157
+    g = gm.Graph.from_edges([0], [1], 3)
+    props = np.array([0.0, 0.0, 5.0])
+    act = np.array([0, 0, 1], np.uint8)
+    st = gm.run_graph_program(g, gm.PROG_ADD_PROBE, props, act, 100)
+    assert len(st) == 1 and st[0].key() == (1, 1, 1, 0)
+
+
+def test_generate_messages_and_decline(gm):
+    # test_engine.cpp:159-184
+    s, d, v = chain()
+    g = gm.Graph.from_edges(s, d, 3)
+    x, xv, _, _ = gm.superstep_phases(g, gm.PROG_ADD_PROBE, v, np.array([0, 1, 0], np.uint8),
+                                      run_spmv=False)
+    assert list(xv) == [False, True, False] and x[1] == 10.0
+    x, xv, _, _ = gm.superstep_phases(g, gm.PROG_SELECTIVE_PROBE, v, np.ones(3, np.uint8),
+                                      run_spmv=False)
+    assert xv.sum() == 2 and not xv[0]
+
+
+def test_both_merge_order(gm):
+    # test_engine.cpp:186-204
+    g = gm.Graph.from_edges([0, 1], [1, 0], 2, np.array([7.0, 9.0]))
+    _, _, y, yv = gm.superstep_phases(g, gm.PROG_BOTH_ORDER_PROBE, np.array([1.0, 2.0]),
+                                      np.ones(2, np.uint8))
+    assert yv.all()
+    assert list(y[0]["v"][: y[0]["n"]]) == [209.0, 207.0]
+    assert list(y[1]["v"][: y[1]["n"]]) == [107.0, 109.0]
+
+
+def test_in_scatter(gm):
+    # test_engine.cpp:206-223
+    g = gm.Graph.from_edges([0], [1], 2, np.array([3.0]))
+    _, _, y, yv = gm.superstep_phases(g, gm.PROG_IN_ADD_PROBE, np.array([1.0, 2.0]),
+                                      np.ones(2, np.uint8))
+    assert list(yv) == [True, False] and y[0] == 2.0
+
+
+def test_callback_failure_context(gm):
+    # test_engine.cpp:225-236
+    s, d, v = chain()
+    g = gm.Graph.from_edges(s, d, 3)
+    with pytest.raises(gm.EngineError) as e:
+        gm.run_graph_program(g, gm.PROG_THROWING_APPLY, v.copy(), np.ones(3, np.uint8), 1)
+    assert "apply failed at vertex" in str(e.value) and "boom" in str(e.value)
+
+
+def test_relabel_invariance_generic(gm, orc):
+    # test_engine.cpp:255-277 analogue: identical results whatever the layout
+    rng = np.random.default_rng(424242)
+    n = 150
+    s = rng.integers(0, n, 900)
+    d = rng.integers(0, n, 900)
+    w = rng.uniform(0.5, 9.5, 900)
+    outs = []
+    for relabel in (False, True):
+        g = gm.Graph.from_edges(s, d, n, w, preprocess=True, relabel=relabel)
+        dist = np.full(n, np.inf)
+        dist[0] = 0
+        act = np.zeros(n, np.uint8)
+        act[0] = 1
+        gm.run_graph_program(g, gm.PROG_SSSP_REF, dist, act, n)
+        outs.append(dist)
+    assert np.array_equal(_bits(outs[0]), _bits(outs[1]))
+
+
+# ------------------------------------------------------------------ errors
+
+def test_input_errors(gm):
+    with pytest.raises(gm.InputError, match=r"edge 1 -> 6 \(1-based\) exceeds vertex count 3"):
+        gm.Graph.from_edges([0], [5], 3)
+    with pytest.raises(gm.InputError, match=r"duplicate edge 1 -> 2 \(1-based\)"):
+        gm.Graph.from_edges([0, 0], [1, 1], 3)
+    g = gm.Graph.from_edges([0], [1], 3)
+    with pytest.raises(gm.InputError, match=r"source vertex 10 \(1-based\) exceeds vertex count 3"):
+        gm.bfs(g, 9)
+    with pytest.raises(gm.InputError):
+        gm.run_graph_program(g, gm.PROG_PAGERANK_REF, np.zeros(3, gm.PAGERANK_STATE),
+                             np.ones(3, np.uint8), 1, params=[1.01])
+    g = gm.Graph.from_edges([0, 1], [1, 2], 3, np.array([3.0, 4.0], np.float32))
+    with pytest.raises(gm.InputError, match="not bipartite"):
+        gm.collaborative_filtering_gd(g, 2, 1e-3, 0.05, 1, init=np.zeros((3, 2), np.float32))
+
+
+def test_empty_and_isolated(gm):
+    g = gm.Graph.from_edges([], [], 4)
+    lvl, st = gm.bfs(g, 0)
+    assert list(lvl) == [0, -1, -1, -1] and len(st) == 1
+    r, _ = gm.pagerank(g, 0.85, 3)
+    np.testing.assert_allclose(r, 0.25, rtol=1e-6)
+
+
+# ------------------------------------------------------- medium R-MAT
+
+@pytest.mark.parametrize("scale", [14, 16])
+def test_rmat_traversals_vs_oracle(gm, orc, scale):
+    g = gm.Graph.rmat(scale, 16, seed=scale, symmetrize=True, relabel=True)
+    s, d, _ = g.edges()
+    n = 1 << scale
+    root = g.pick_source(scale)
+    assert root == orc.pick_source(scale, np.bincount(s, minlength=n).astype(np.uint32))
+    lvl, st = gm.bfs(g, root)
+    wl, wst = orc.bfs(n, s, d, root, presorted=True)
+    assert np.array_equal(lvl, wl)
+    assert _stats_key(st) == wst
+    assert any(x.direction == "pull" for x in st)  # the switch fired
+    g = gm.Graph.rmat(scale, 16, seed=scale, weights=True, relabel=True)
+    s, d, w = g.edges()
+    dist, st = gm.sssp(g, root)
+    wd, wst = orc.sssp(n, s, d, w, root, presorted=True)
+    assert np.array_equal(dist, wd)
+    assert _stats_key(st) == wst
+
+
+def test_rmat_pagerank_vs_oracle(gm, orc):
+    g = gm.Graph.rmat(16, 16, seed=3, relabel=True)
+    s, d, _ = g.edges()
+    r, st = gm.pagerank(g, 0.85, 20)
+    want, _ = orc.pagerank_norm(1 << 16, s, d)
+    assert rel_l1(r, want) <= 1e-5
+    assert abs(float(np.sum(r, dtype=np.float64)) - 1.0) < 1e-4

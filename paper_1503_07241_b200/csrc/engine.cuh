@@ -252,7 +252,9 @@ class Engine {
       y2bits_.alloc(words + 1, s_);
     }
     ctr_.alloc(3, s_);
+    ctr_.zero(s_);
     err_.alloc(1, s_);
+    err_.zero(s_);
     GM_CUDA(cudaEventCreate(&e0_));
     GM_CUDA(cudaEventCreate(&e1_));
     GM_CUDA(cudaEventCreate(&e2_));

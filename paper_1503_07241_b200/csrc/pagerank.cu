@@ -9,38 +9,52 @@
 //
 // Device layout per superstep (internal ids, relabeled by out-degree so
 // dangling vertices form the tail [nonzero_outdeg, n)):
-//   x_cur[N]  f32  message vector (rank * inv_outdeg; 0 for dangling)   read by gather
+//   x_cur[N]  f32  message vector (rank * inv_outdeg; 0 for dangling)   gathered
 //   in.ptr    u64  CSR(G^T) offsets                                      streamed
-//   in.idx    u32  CSR(G^T) sources                                      streamed (128-bit)
+//   in.idx    u32  CSR(G^T) sources                                      streamed
 //   inv[N]    f32  1/outdeg                                              streamed
 //   rank[N]   f32  written in place (only the row owner touches it)
-//   x_next[N] f32  written (the next superstep's message vector: the send
-//                  phase is fused into this superstep's apply epilogue)
+//   x_next[N] f32  written: the next superstep's message vector (the send phase
+//                  is fused into this superstep's apply epilogue)
 // Algorithmic bytes/superstep = 4·nnz + 8·(N+1) + 16·N.
 //
-// Kernels: rows with in-degree <= kLongRow go to k_pr_rows (8-lane groups, one
-// row per group, shuffle tree reduce); longer rows get a CTA each
-// (k_pr_long_rows).  Both reductions are fixed trees -> bitwise reproducible.
+// SpMV = merge-path over row-aligned tiles (Merrill & Garland's CSR merge
+// SpMV, specialised): the row sequence is cut once (cached per graph) into
+// tiles of at most kTile path items (rows + nonzeros).  A 256-thread CTA
+// stages the tile's row ends and the gathered x[col] values in shared memory
+// (every gather of the tile in flight at once), each thread takes exactly
+// kIPT path items found by a merge-path search in shared memory, and a block
+// segmented scan hands partial row sums across threads.  Load balance is
+// perfect whatever the degree mix (54% empty rows, hubs of 10^5 entries), and
+// every reduction is a fixed tree, so results are bitwise reproducible.
+// Rows longer than a tile get a CTA each (k_pr_long_rows).
 // The dangling mass for the NEXT superstep is reduced deterministically by
-// k_dangling (fixed grid, per-block partials, single-block final), which also
-// computes base on device, so 20 supersteps run without a host round trip.
+// k_dangling (fixed grid, per-block partials, last-block final), which also
+// computes base on device, so the supersteps run without a host round trip.
 #include <vector>
 
 #include "api_internal.cuh"
 
 namespace gm {
 
-constexpr uint32_t kLongRow = 1024;
+constexpr int kPrThreads = 256;
+constexpr int kIPT = 8;
+constexpr int kTile = kPrThreads * kIPT;  // path items per tile
 constexpr unsigned kDangBlocks = 296;
 
 struct PrCache {
   uint64_t n = 0;
   DevBuf<float> inv, rank, x0, x1;
-  DevBuf<uint32_t> long_rows;
-  uint64_t n_long = 0;
+  DevBuf<uint32_t> tile_b, tile_e, long_rows;
+  uint64_t ntiles = 0, n_long = 0;
   DevBuf<float> scalars;       // [0] = base for the current superstep
   DevBuf<float> dang_partial;  // kDangBlocks
   DevBuf<unsigned long long> ctr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ~PrCache() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  }
 };
 
 namespace {
@@ -54,17 +68,6 @@ __global__ void k_pr_init(uint64_t n, const uint32_t* outdeg, float* inv, float*
     inv[v] = iv;
     rank[v] = r0;
     x[v] = r0 * iv;
-  }
-}
-
-__global__ void k_long_rows(const uint64_t* ptr, uint64_t n, uint32_t thresh, uint32_t* list,
-                            unsigned long long* cnt) {
-  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
-       v += uint64_t(gridDim.x) * blockDim.x) {
-    if (ptr[v + 1] - ptr[v] > thresh) {
-      const unsigned long long at = atomicAdd(cnt, 1ull);
-      list[at] = uint32_t(v);
-    }
   }
 }
 
@@ -90,7 +93,6 @@ __global__ void k_dangling(uint64_t lo, uint64_t n, const float* rank, const flo
   }
   __syncthreads();
   if (!last) return;
-  // Final fixed-order reduction by the last block to arrive.
   float t = 0.0f;
   for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) t += ((volatile float*)partial)[i];
   red[threadIdx.x] = t;
@@ -108,33 +110,116 @@ __global__ void k_dangling(uint64_t lo, uint64_t n, const float* rank, const flo
 }
 
 template <bool kCount>
-__global__ void __launch_bounds__(256) k_pr_rows(uint64_t n, const uint64_t* __restrict__ ptr,
-                                                 const uint32_t* __restrict__ idx,
-                                                 const float* __restrict__ x_cur,
-                                                 const float* __restrict__ inv, float* rank,
-                                                 float* __restrict__ x_next,
-                                                 const float* __restrict__ scalars, float damping,
-                                                 unsigned long long* ctr) {
-  const unsigned lane8 = threadIdx.x & 7u;
-  const unsigned gmask = 0xFFu << (threadIdx.x & 24u);
-  const uint64_t group = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 3;
-  const uint64_t ngroups = (uint64_t(gridDim.x) * blockDim.x) >> 3;
+__device__ __forceinline__ void pr_write(uint64_t row, float sum, float base, float damping,
+                                         const float* __restrict__ inv, float* rank,
+                                         float* __restrict__ x_next, bool nonempty,
+                                         unsigned long long& changed) {
+  const float r = base + damping * sum;
+  if (kCount) changed += nonempty && (__float_as_uint(r) != __float_as_uint(rank[row]));
+  rank[row] = r;
+  x_next[row] = r * inv[row];
+}
+
+template <bool kCount>
+__global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
+    const uint32_t* __restrict__ tile_b, const uint32_t* __restrict__ tile_e,
+    const uint64_t* __restrict__ ptr, const uint32_t* __restrict__ idx,
+    const float* __restrict__ x_cur, const float* __restrict__ inv, float* rank,
+    float* __restrict__ x_next, const float* __restrict__ scalars, float damping,
+    unsigned long long* ctr) {
+  __shared__ uint32_t s_end[kTile + 1];
+  __shared__ float s_val[kTile];
+  __shared__ uint32_t s_wk[kPrThreads / 32];
+  __shared__ float s_wv[kPrThreads / 32];
+  const unsigned tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+  const uint32_t r0 = tile_b[blockIdx.x], r1 = tile_e[blockIdx.x];
+  const uint64_t j0 = ptr[r0];
+  const uint32_t nrows = r1 - r0;
+  const uint32_t nnz = uint32_t(ptr[r1] - j0);
+  const uint32_t items = nrows + nnz;
   const float base = scalars[0];
+  // Stage row ends and gathered messages; all gathers of the tile in flight.
+  for (uint32_t k = tid; k < nrows; k += kPrThreads) s_end[k] = uint32_t(ptr[r0 + k + 1] - j0);
+  if (tid == 0) s_end[nrows] = 0xFFFFFFFFu;
+#pragma unroll
+  for (int u = 0; u < kIPT; ++u) {
+    const uint32_t k = tid + u * kPrThreads;
+    if (k < nnz) s_val[k] = __ldg(&x_cur[__ldg(&idx[j0 + k])]);
+  }
+  __syncthreads();
+  // Merge-path search for this thread's diagonal.
+  const uint32_t d0 = min(tid * kIPT, items), d1 = min(d0 + kIPT, items);
+  uint32_t lo = d0 > nnz ? d0 - nnz : 0, hi = min(d0, nrows);
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s_end[mid] <= d0 - mid - 1)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  uint32_t ti = lo, tj = d0 - lo;
+  const uint32_t start_row = ti;
+  float run = 0.0f, first_val = 0.0f;
+  bool has_first = false;
   unsigned long long changed = 0;
-  for (uint64_t row = group; row < n; row += ngroups) {
-    const uint64_t beg = ptr[row], end = ptr[row + 1];
-    if (end - beg > kLongRow) continue;
-    float s = 0.0f;
-    for (uint64_t e = beg + lane8; e < end; e += 8) s += __ldg(&x_cur[__ldg(&idx[e])]);
-    s += __shfl_xor_sync(gmask, s, 4, 8);
-    s += __shfl_xor_sync(gmask, s, 2, 8);
-    s += __shfl_xor_sync(gmask, s, 1, 8);
-    if (lane8 == 0) {
-      const float r = base + damping * s;
-      if (kCount) changed += (end > beg) && (__float_as_uint(r) != __float_as_uint(rank[row]));
-      rank[row] = r;
-      x_next[row] = r * inv[row];
+  for (uint32_t k = d0; k < d1; ++k) {
+    if (tj < s_end[ti]) {
+      run += s_val[tj];
+      ++tj;
+    } else {
+      if (!has_first) {
+        has_first = true;
+        first_val = run;
+      } else {
+        const uint32_t row_len = s_end[ti] - (ti ? s_end[ti - 1] : 0);
+        pr_write<kCount>(r0 + ti, run, base, damping, inv, rank, x_next, row_len != 0, changed);
+      }
+      run = 0.0f;
+      ++ti;
     }
+  }
+  // Block segmented inclusive scan of the carries (key = open row, val = partial).
+  uint32_t key = ti;
+  float val = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t k2 = __shfl_up_sync(0xffffffffu, key, o);
+    const float v2 = __shfl_up_sync(0xffffffffu, val, o);
+    if (lane >= unsigned(o) && k2 == key) val += v2;
+  }
+  if (lane == 31) {
+    s_wk[wid] = key;
+    s_wv[wid] = val;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t wk = lane < kPrThreads / 32 ? s_wk[lane] : 0xFFFFFFFFu;
+    float wv = lane < kPrThreads / 32 ? s_wv[lane] : 0.0f;
+#pragma unroll
+    for (int o = 1; o < kPrThreads / 32; o <<= 1) {
+      const uint32_t k2 = __shfl_up_sync(0xffffffffu, wk, o);
+      const float v2 = __shfl_up_sync(0xffffffffu, wv, o);
+      if (lane >= unsigned(o) && k2 == wk) wv += v2;
+    }
+    if (lane < kPrThreads / 32) {
+      s_wk[lane] = wk;
+      s_wv[lane] = wv;
+    }
+  }
+  __syncthreads();
+  if (wid > 0 && s_wk[wid - 1] == key) val += s_wv[wid - 1];
+  // carry-in of this thread = inclusive carry of the previous thread
+  uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+  float pv = __shfl_up_sync(0xffffffffu, val, 1);
+  if (lane == 0) {
+    pk = wid > 0 ? s_wk[wid - 1] : 0xFFFFFFFFu;
+    pv = wid > 0 ? s_wv[wid - 1] : 0.0f;
+  }
+  if (has_first) {
+    const float carry = (tid > 0 && pk == start_row) ? pv : 0.0f;
+    const uint32_t row_len = s_end[start_row] - (start_row ? s_end[start_row - 1] : 0);
+    pr_write<kCount>(r0 + start_row, carry + first_val, base, damping, inv, rank, x_next,
+                     row_len != 0, changed);
   }
   if (kCount) warp_add_u64(ctr, changed);
 }
@@ -149,9 +234,16 @@ __global__ void __launch_bounds__(256) k_pr_long_rows(const uint32_t* rows, cons
   __shared__ float red[256];
   const uint32_t row = rows[blockIdx.x];
   const uint64_t beg = ptr[row], end = ptr[row + 1];
-  float s = 0.0f;
-  for (uint64_t e = beg + threadIdx.x; e < end; e += blockDim.x) s += __ldg(&x_cur[__ldg(&idx[e])]);
-  red[threadIdx.x] = s;
+  float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+  uint64_t e = beg + threadIdx.x;
+  for (; e + 3 * 256 < end; e += 4 * 256) {
+    a0 += __ldg(&x_cur[__ldg(&idx[e])]);
+    a1 += __ldg(&x_cur[__ldg(&idx[e + 256])]);
+    a2 += __ldg(&x_cur[__ldg(&idx[e + 512])]);
+    a3 += __ldg(&x_cur[__ldg(&idx[e + 768])]);
+  }
+  for (; e < end; e += 256) a0 += __ldg(&x_cur[__ldg(&idx[e])]);
+  red[threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
@@ -163,6 +255,47 @@ __global__ void __launch_bounds__(256) k_pr_long_rows(const uint32_t* rows, cons
     rank[row] = r;
     x_next[row] = r * inv[row];
   }
+}
+
+// Row-aligned tiles of <= kTile path items; rows needing more than a tile go
+// to the long-row list.  One-time host pass over the offsets (cached).
+void build_tiles(Graph& g, PrCache& c, cudaStream_t s) {
+  const uint64_t n = g.n;
+  std::vector<uint64_t> ptr(n + 1);
+  GM_CUDA(cudaMemcpyAsync(ptr.data(), g.in.ptr.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint32_t> tb, te, lr;
+  uint64_t r = 0;
+  while (r < n) {
+    const uint64_t deg = ptr[r + 1] - ptr[r];
+    if (deg + 1 > uint64_t(kTile)) {
+      lr.push_back(uint32_t(r));
+      ++r;
+      continue;
+    }
+    const uint64_t start = r;
+    uint64_t items = 0;
+    while (r < n) {
+      const uint64_t d = ptr[r + 1] - ptr[r];
+      if (d + 1 > uint64_t(kTile) || items + d + 1 > uint64_t(kTile)) break;
+      items += d + 1;
+      ++r;
+    }
+    tb.push_back(uint32_t(start));
+    te.push_back(uint32_t(r));
+  }
+  c.ntiles = tb.size();
+  c.n_long = lr.size();
+  c.tile_b.alloc(c.ntiles + 1, s);
+  c.tile_e.alloc(c.ntiles + 1, s);
+  c.long_rows.alloc(c.n_long + 1, s);
+  if (c.ntiles) {
+    GM_CUDA(cudaMemcpyAsync(c.tile_b.get(), tb.data(), c.ntiles * 4, cudaMemcpyHostToDevice, s));
+    GM_CUDA(cudaMemcpyAsync(c.tile_e.get(), te.data(), c.ntiles * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (c.n_long)
+    GM_CUDA(cudaMemcpyAsync(c.long_rows.get(), lr.data(), c.n_long * 4, cudaMemcpyHostToDevice, s));
+  GM_CUDA(cudaStreamSynchronize(s));
 }
 
 PrCache& cache(Graph& g) {
@@ -180,18 +313,9 @@ PrCache& cache(Graph& g) {
     c.dang_partial.alloc(kDangBlocks + 1, s);
     c.ctr.alloc(4, s);
     c.ctr.zero(s);
-    // long-row list
-    DevBuf<unsigned long long> cnt(1, s);
-    cnt.zero(s);
-    c.long_rows.alloc(n ? n : 1, s);
-    if (n)
-      k_long_rows<<<grid_for(n, 256), 256, 0, s>>>(g.in.ptr.get(), n, kLongRow, c.long_rows.get(),
-                                                   cnt.get());
-    GM_LAUNCH_CHECK();
-    unsigned long long h = 0;
-    GM_CUDA(cudaMemcpyAsync(&h, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
-    GM_CUDA(cudaStreamSynchronize(s));
-    c.n_long = h;
+    GM_CUDA(cudaEventCreate(&c.e0));
+    GM_CUDA(cudaEventCreate(&c.e1));
+    build_tiles(g, c, s);
   }
   return *g.pr;
 }
@@ -207,7 +331,6 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   if (n == 0) return stats;
   PrCache& c = cache(g);
   cudaStream_t s = g.stream;
-  const unsigned grid_rows = 148 * 8;
   const uint64_t dang_lo = g.relabeled ? g.nonzero_outdeg : 0;
   k_pr_init<<<grid_for(n, 256), 256, 0, s>>>(n, g.outdeg.get(), c.inv.get(), c.rank.get(), c.x0.get());
   GM_LAUNCH_CHECK();
@@ -216,23 +339,23 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   float* xc = c.x0.get();
   float* xn = c.x1.get();
   const float d = float(damping);
-  cudaEvent_t e0, e1;
-  GM_CUDA(cudaEventCreate(&e0));
-  GM_CUDA(cudaEventCreate(&e1));
   for (int64_t it = 1; it <= iters; ++it) {
-    if (collect) GM_CUDA(cudaEventRecord(e0, s));
+    if (collect) GM_CUDA(cudaEventRecord(c.e0, s));
     k_dangling<<<kDangBlocks, 256, 0, s>>>(dang_lo, n, c.rank.get(), c.inv.get(),
                                            c.dang_partial.get(), c.scalars.get(), damping, ticket);
     GM_LAUNCH_CHECK();
-    if (collect) {
-      GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
-      k_pr_rows<true><<<grid_rows, 256, 0, s>>>(n, g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
-                                                c.rank.get(), xn, c.scalars.get(), d, c.ctr.get());
-    } else {
-      k_pr_rows<false><<<grid_rows, 256, 0, s>>>(n, g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
-                                                 c.rank.get(), xn, c.scalars.get(), d, c.ctr.get());
+    if (collect) GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
+    if (c.ntiles) {
+      if (collect)
+        k_pr_tiles<true><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
+            c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
+            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get());
+      else
+        k_pr_tiles<false><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
+            c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
+            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get());
+      GM_LAUNCH_CHECK();
     }
-    GM_LAUNCH_CHECK();
     if (c.n_long) {
       if (collect)
         k_pr_long_rows<true><<<unsigned(c.n_long), 256, 0, s>>>(
@@ -246,12 +369,12 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
     }
     std::swap(xc, xn);
     if (!collect) continue;
-    GM_CUDA(cudaEventRecord(e1, s));
+    GM_CUDA(cudaEventRecord(c.e1, s));
     unsigned long long upd = 0;
     GM_CUDA(cudaMemcpyAsync(&upd, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
     GM_CUDA(cudaStreamSynchronize(s));
     float ms = 0;
-    GM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    GM_CUDA(cudaEventElapsedTime(&ms, c.e0, c.e1));
     gm_iteration_stats st{};
     st.iteration = it;
     st.active_before = int64_t(n);
@@ -264,8 +387,6 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
     st.direction = 0;
     stats.push_back(st);
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   if (out) {
     if (out_on_device) {
       to_external(g, c.rank.get(), out, 4);

@@ -109,15 +109,52 @@ __global__ void k_dangling(uint64_t lo, uint64_t n, const float* rank, const flo
   }
 }
 
+// Next superstep's base from the per-CTA dangling partials, summed in a fixed
+// order (one CTA): base = (1-d)/N + d*D/N.
+__global__ void __launch_bounds__(1024) k_pr_base(const float* partial, uint32_t np, uint64_t n,
+                                                  double damping, float* scalars) {
+  __shared__ float red[1024];
+  float s = 0.0f;
+  for (uint32_t i = threadIdx.x; i < np; i += 1024) s += partial[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const float nf = float(n), d = float(damping);
+    scalars[0] = (1.0f - d) / nf + d * red[0] / nf;
+  }
+}
+
+// Block-wide fixed-tree sum (all threads call; result valid in thread 0).
+template <int kThreadsT>
+__device__ __forceinline__ float block_sum(float v, float* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31u) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.0f;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < kThreadsT / 32 ? scratch[threadIdx.x] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;
+}
+
 template <bool kCount>
 __device__ __forceinline__ void pr_write(uint64_t row, float sum, float base, float damping,
                                          const float* __restrict__ inv, float* rank,
                                          float* __restrict__ x_next, bool nonempty,
-                                         unsigned long long& changed) {
+                                         unsigned long long& changed, float& dangling) {
   const float r = base + damping * sum;
   if (kCount) changed += nonempty && (__float_as_uint(r) != __float_as_uint(rank[row]));
   rank[row] = r;
-  x_next[row] = r * inv[row];
+  const float iv = inv[row];
+  x_next[row] = r * iv;
+  if (iv == 0.0f) dangling += r;
 }
 
 template <bool kCount>
@@ -126,8 +163,10 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
     const uint64_t* __restrict__ ptr, const uint32_t* __restrict__ idx,
     const float* __restrict__ x_cur, const float* __restrict__ inv, float* rank,
     float* __restrict__ x_next, const float* __restrict__ scalars, float damping,
-    unsigned long long* ctr) {
+    unsigned long long* ctr, float* __restrict__ dang_partial) {
   __shared__ uint32_t s_end[kTile + 1];
+  __shared__ float s_red[kPrThreads / 32];
+  float dangling = 0.0f;
   __shared__ float s_val[kTile];
   __shared__ uint32_t s_wk[kPrThreads / 32];
   __shared__ float s_wv[kPrThreads / 32];
@@ -172,7 +211,8 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
         first_val = run;
       } else {
         const uint32_t row_len = s_end[ti] - (ti ? s_end[ti - 1] : 0);
-        pr_write<kCount>(r0 + ti, run, base, damping, inv, rank, x_next, row_len != 0, changed);
+        pr_write<kCount>(r0 + ti, run, base, damping, inv, rank, x_next, row_len != 0, changed,
+                         dangling);
       }
       run = 0.0f;
       ++ti;
@@ -219,9 +259,12 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
     const float carry = (tid > 0 && pk == start_row) ? pv : 0.0f;
     const uint32_t row_len = s_end[start_row] - (start_row ? s_end[start_row - 1] : 0);
     pr_write<kCount>(r0 + start_row, carry + first_val, base, damping, inv, rank, x_next,
-                     row_len != 0, changed);
+                     row_len != 0, changed, dangling);
   }
   if (kCount) warp_add_u64(ctr, changed);
+  // Dangling mass of this tile's rows, for the next superstep's base.
+  const float dsum = block_sum<kPrThreads>(dangling, s_red);
+  if (tid == 0) dang_partial[blockIdx.x] = dsum;
 }
 
 template <bool kCount>
@@ -230,7 +273,8 @@ __global__ void __launch_bounds__(256) k_pr_long_rows(const uint32_t* rows, cons
                                                       const float* __restrict__ x_cur,
                                                       const float* inv, float* rank, float* x_next,
                                                       const float* scalars, float damping,
-                                                      unsigned long long* ctr) {
+                                                      unsigned long long* ctr,
+                                                      float* dang_partial) {
   __shared__ float red[256];
   const uint32_t row = rows[blockIdx.x];
   const uint64_t beg = ptr[row], end = ptr[row + 1];
@@ -253,7 +297,9 @@ __global__ void __launch_bounds__(256) k_pr_long_rows(const uint32_t* rows, cons
     const float r = scalars[0] + damping * red[0];
     if (kCount && __float_as_uint(r) != __float_as_uint(rank[row])) atomicAdd(ctr, 1ull);
     rank[row] = r;
-    x_next[row] = r * inv[row];
+    const float iv = inv[row];
+    x_next[row] = r * iv;
+    dang_partial[blockIdx.x] = iv == 0.0f ? r : 0.0f;
   }
 }
 
@@ -310,12 +356,12 @@ PrCache& cache(Graph& g) {
     c.x0.alloc(n, s);
     c.x1.alloc(n, s);
     c.scalars.alloc(4, s);
-    c.dang_partial.alloc(kDangBlocks + 1, s);
     c.ctr.alloc(4, s);
     c.ctr.zero(s);
     GM_CUDA(cudaEventCreate(&c.e0));
     GM_CUDA(cudaEventCreate(&c.e1));
     build_tiles(g, c, s);
+    c.dang_partial.alloc(std::max<uint64_t>(kDangBlocks, c.ntiles + c.n_long) + 1, s);
   }
   return *g.pr;
 }
@@ -339,34 +385,39 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   float* xc = c.x0.get();
   float* xn = c.x1.get();
   const float d = float(damping);
+  // Base of the first superstep (initial ranks); later bases come from the
+  // dangling partials the SpMV kernels emit (k_pr_base).
+  k_dangling<<<kDangBlocks, 256, 0, s>>>(dang_lo, n, c.rank.get(), c.inv.get(),
+                                         c.dang_partial.get(), c.scalars.get(), damping, ticket);
+  GM_LAUNCH_CHECK();
+  float* part = c.dang_partial.get();
   for (int64_t it = 1; it <= iters; ++it) {
     if (collect) GM_CUDA(cudaEventRecord(c.e0, s));
-    k_dangling<<<kDangBlocks, 256, 0, s>>>(dang_lo, n, c.rank.get(), c.inv.get(),
-                                           c.dang_partial.get(), c.scalars.get(), damping, ticket);
-    GM_LAUNCH_CHECK();
     if (collect) GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
     if (c.ntiles) {
       if (collect)
         k_pr_tiles<true><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
             c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
-            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get());
+            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get(), part);
       else
         k_pr_tiles<false><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
             c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
-            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get());
+            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get(), part);
       GM_LAUNCH_CHECK();
     }
     if (c.n_long) {
       if (collect)
         k_pr_long_rows<true><<<unsigned(c.n_long), 256, 0, s>>>(
             c.long_rows.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(), c.rank.get(), xn,
-            c.scalars.get(), d, c.ctr.get());
+            c.scalars.get(), d, c.ctr.get(), part + c.ntiles);
       else
         k_pr_long_rows<false><<<unsigned(c.n_long), 256, 0, s>>>(
             c.long_rows.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(), c.rank.get(), xn,
-            c.scalars.get(), d, c.ctr.get());
+            c.scalars.get(), d, c.ctr.get(), part + c.ntiles);
       GM_LAUNCH_CHECK();
     }
+    k_pr_base<<<1, 1024, 0, s>>>(part, uint32_t(c.ntiles + c.n_long), n, damping, c.scalars.get());
+    GM_LAUNCH_CHECK();
     std::swap(xc, xn);
     if (!collect) continue;
     GM_CUDA(cudaEventRecord(c.e1, s));

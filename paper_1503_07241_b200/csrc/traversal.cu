@@ -22,7 +22,8 @@
 //        offsets, so one hub and a million leaves cost the same per edge.
 //        A vertex is claimed once through the visited bitmap (atomicOr).
 //   pull (SpMV over CSR(G^T), unvisited rows only): pass 1 probes at most
-//        kPullProbes in-neighbours per row (thread per row); rows still open
+//        kHead in-neighbours per row (thread per row, one 16-byte head load);
+//        rows still open
 //        are deferred to pass 2, edge-balanced over their remaining in-edges.
 //        The hot prefix of the frontier bitmap is staged in shared memory
 //        (with GM_RELABEL low ids are the hubs every adjacency list starts
@@ -34,6 +35,10 @@
 // balanced push, carrying the frontier's superstep-start distances (the
 // message snapshot, rule S3); atomicMin into dist; a vertex whose distance
 // dropped is claimed once through a changed-bitmap and forms the next frontier.
+#include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "api_internal.cuh"
@@ -45,9 +50,8 @@ namespace {
 constexpr int kMaxRecorded = 4096;  // per-superstep records kept on device
 constexpr int kBatch = 4;           // supersteps enqueued per host check
 constexpr int kEPT = 4;             // edges per thread, edge-balanced passes
-constexpr int kPullProbes = 8;      // pull pass 1 probes at most this many in-neighbours
 constexpr uint32_t kSmemFbWords = 24 * 1024;  // 96 KB of frontier bitmap per CTA
-constexpr unsigned kGrid = 148 * 2;           // persistent grid (2 CTAs of 1024 per SM)
+constexpr unsigned kGrid = 148 * 2;           // persistent grid for the SSSP kernels
 constexpr unsigned kThreads = 1024;
 constexpr int kCountShift = 36;  // packed counter: count << 36 | edges
 constexpr unsigned long long kEdgeMask = (1ull << kCountShift) - 1;
@@ -56,6 +60,7 @@ enum Dir : int32_t { kPush = 1, kPull = 0 };
 
 struct StepRec {
   int64_t active, updated, edges, examined;
+  int64_t deferred, deferred_edges;  // pull pass 2 work
   int32_t dir, pad;
 };
 
@@ -63,10 +68,16 @@ struct StepRec {
 struct Ctl {
   unsigned long long qpack;     // next queue (count << 36 | edges)
   unsigned long long dpack;     // deferred rows (count << 36 | remaining edges)
+  unsigned long long bpack;     // bitmap -> queue conversion counter
+  unsigned long long upack;     // next unvisited-row list length
   unsigned long long found_n, found_e, examined;
   unsigned long long nf, mf;    // current frontier: vertices, edges
-  int32_t it, dir, prev_pull, cur_is_queue, done, max_it;
+  unsigned long long ucur;      // current unvisited-row list length
+  int32_t it, dir, prev_pull, cur_is_queue, done, max_it, u_implicit, usel;
   uint64_t n_total, m_total, nv;
+  uint64_t t_start[kMaxRecorded];  // %globaltimer per superstep (cooperative kernel)
+  uint64_t t_mid[kMaxRecorded];    // after the first phase (bitmap->queue / pull pass 1)
+  uint64_t t_end[kMaxRecorded];
   StepRec rec[kMaxRecorded];
 };
 
@@ -80,6 +91,11 @@ struct TravCache {
   DevBuf<uint64_t> offs[2];     // exclusive edge offsets, parallel to q (+1 total)
   DevBuf<uint32_t> dq[2];       // SSSP message snapshots parallel to q
   DevBuf<uint32_t> defq;        // pull: deferred rows
+  DevBuf<uint32_t> ul[2];       // pull: unvisited-row lists
+  DevBuf<uint4> head;           // pull: first kHead in-neighbours per row
+  DevBuf<uint64_t> qe[2];       // start-edge pointers parallel to q
+  DevBuf<uint64_t> defe;        // pull: deferred rows' next unprobed edge
+  unsigned coop_grid = 0;
   DevBuf<uint64_t> defo;        // pull: their exclusive remaining-edge offsets
   DevBuf<uint32_t> vis, fb[2];  // visited / frontier bitmaps (cur = it & 1)
   DevBuf<uint32_t> changed;     // SSSP changed-bitmap
@@ -109,6 +125,11 @@ TravCache& cache(Graph& g) {
       c.fb[i].alloc(words, s);
     }
     c.defq.alloc(n + 1, s);
+    c.defe.alloc(n + 1, s);
+    c.qe[0].alloc(n + 1, s);
+    c.qe[1].alloc(n + 1, s);
+    c.ul[0].alloc(n + 1, s);
+    c.ul[1].alloc(n + 1, s);
     c.defo.alloc(n + 2, s);
     c.vis.alloc(words, s);
     c.ctl.alloc(1, s);
@@ -152,22 +173,51 @@ __device__ __forceinline__ void warp_enqueue(bool want, uint32_t v, uint32_t edg
     const unsigned long long ex = base + incl - mine;
     const uint32_t pos = uint32_t(ex >> kCountShift);
     q[pos] = v;
-    offs[pos] = ex & kEdgeMask;
+    if (offs) offs[pos] = ex & kEdgeMask;
   }
 }
 
-__device__ __forceinline__ bool fb_probe(const uint32_t* s_fb, uint32_t s_words,
-                                         const uint32_t* __restrict__ fb, uint32_t u) {
-  const uint32_t w = u >> 5;
-  const uint32_t word = w < s_words ? s_fb[w] : __ldg(&fb[w]);
-  return (word >> (u & 31u)) & 1u;
+// Warp-aggregated append of up to kMaxPer entries per lane: (vertex, edge
+// count, start-edge pointer) -> q / offs / qe with one packed atomicAdd.
+template <int kMaxPer>
+__device__ __forceinline__ void warp_enqueue_multi(unsigned mask, const uint32_t* v,
+                                                   const uint32_t* edges, const uint64_t* estart,
+                                                   unsigned long long* pack, uint32_t* q,
+                                                   uint64_t* offs, uint64_t* qe) {
+  const unsigned lane = lane_id();
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int k = 0; k < kMaxPer; ++k)
+    if ((mask >> k) & 1u) mine += (1ull << kCountShift) | edges[k];
+  unsigned long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= unsigned(o)) incl += t;
+  }
+  const unsigned long long total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(pack, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  unsigned long long ex = base + incl - mine;
+#pragma unroll
+  for (int k = 0; k < kMaxPer; ++k) {
+    if ((mask >> k) & 1u) {
+      const uint32_t pos = uint32_t(ex >> kCountShift);
+      q[pos] = v[k];
+      offs[pos] = ex & kEdgeMask;
+      qe[pos] = estart[k];
+      ex += (1ull << kCountShift) | edges[k];
+    }
+  }
 }
 
 // ------------------------------------------------------------- control
 __global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t root_ext,
-                           const uint32_t* perm, uint32_t* q1, uint64_t* offs1,
-                           const uint32_t* deg, int32_t* level, uint64_t n, uint64_t m,
-                           uint64_t nv, int32_t max_it) {
+                           const uint32_t* perm, uint32_t* q1, uint64_t* offs1, uint64_t* qe1,
+                           const uint64_t* out_ptr, const uint32_t* deg, int32_t* level,
+                           uint64_t n, uint64_t m, uint64_t nv, int32_t max_it) {
   const uint32_t root = perm ? perm[root_ext] : uint32_t(root_ext);
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words;
        i += uint64_t(gridDim.x) * blockDim.x)
@@ -176,6 +226,7 @@ __global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t roo
     q1[0] = root;
     offs1[0] = 0;
     offs1[1] = deg[root];
+    qe1[0] = out_ptr[root];
     level[root] = 0;
     ctl->nf = 1;
     ctl->mf = deg[root];
@@ -187,24 +238,10 @@ __global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t roo
     ctl->n_total = n;
     ctl->m_total = m;
     ctl->nv = nv;
+    ctl->u_implicit = 1;  // first pull scans every row; later pulls the unvisited list
+    ctl->usel = 0;
+    ctl->ucur = 0;
   }
-}
-
-// Superstep prologue: direction choice and counter reset (one thread).
-__global__ void k_decide(Ctl* ctl, uint64_t* offs_cur) {
-  if (ctl->done) return;
-  const int32_t it = ++ctl->it;
-  const uint64_t nf = ctl->nf, mf = ctl->mf;
-  int32_t pull;
-  if (it == 1)
-    pull = 0;
-  else if (ctl->prev_pull)
-    pull = nf * 24 >= ctl->n_total;
-  else
-    pull = double(mf) > 0.05 * double(ctl->m_total);
-  ctl->dir = pull ? kPull : kPush;
-  ctl->qpack = ctl->dpack = ctl->found_n = ctl->found_e = ctl->examined = 0;
-  if (!pull && ctl->cur_is_queue) offs_cur[nf] = mf;
 }
 
 // Superstep epilogue (one thread): next frontier, stats record, termination.
@@ -236,190 +273,6 @@ __global__ void k_finish(Ctl* ctl, uint64_t* offs_next) {
 }
 
 // ------------------------------------------------------------------- BFS
-// bitmap -> queue (+ offsets) when a push follows a pull.
-__global__ void __launch_bounds__(kThreads) k_bfs_b2q(const Ctl* ctl, const uint32_t* fb,
-                                                      uint64_t words, const uint32_t* deg,
-                                                      uint32_t* q, uint64_t* offs,
-                                                      unsigned long long* pack) {
-  if (ctl->done || ctl->dir != kPush || ctl->cur_is_queue) return;
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t w = warp; w < words; w += nwarps) {
-    const uint32_t word = fb[w];
-    if (!word) continue;  // warp-uniform
-    const uint32_t v = uint32_t(w * 32 + lane_id());
-    const bool set = (word >> lane_id()) & 1u;
-    warp_enqueue(set, v, set ? deg[v] : 0, pack, q, offs);
-  }
-}
-
-// Edge-balanced push.  pack_cur holds the b2q counter (count of the current
-// queue when it came from a bitmap); the frontier size is ctl->nf either way.
-__global__ void __launch_bounds__(kThreads) k_bfs_push(Ctl* ctl, const uint32_t* __restrict__ q,
-                                                       const uint64_t* __restrict__ offs,
-                                                       const uint64_t* __restrict__ ptr,
-                                                       const uint32_t* __restrict__ idx,
-                                                       const uint32_t* __restrict__ deg,
-                                                       int32_t* level, uint32_t* vis,
-                                                       uint32_t* fb_next, uint32_t* qn,
-                                                       uint64_t* offs_n) {
-  if (ctl->done || ctl->dir != kPush) return;
-  const uint32_t nq = uint32_t(ctl->nf);
-  const uint64_t total = ctl->mf;
-  const int32_t next_level = ctl->it;
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned lane = lane_id();
-  for (uint64_t wb = warp * 32 * kEPT; wb < total; wb += nwarps * 32 * kEPT) {
-    const uint64_t t0 = wb + uint64_t(lane) * kEPT;
-    uint32_t i = 0;
-    uint64_t e = 0, rem = 0;
-    if (t0 < total) {
-      i = find_source(offs, nq, t0);
-      e = ptr[q[i]] + (t0 - offs[i]);
-      rem = (i + 1 < nq ? offs[i + 1] : total) - t0;
-    }
-#pragma unroll
-    for (int k = 0; k < kEPT; ++k) {
-      const uint64_t t = t0 + k;
-      bool won = false;
-      uint32_t v = 0;
-      if (t < total) {
-        while (rem == 0) {  // next queue entry with edges
-          ++i;
-          e = ptr[q[i]];
-          rem = (i + 1 < nq ? offs[i + 1] : total) - offs[i];
-        }
-        v = idx[e];
-        ++e;
-        --rem;
-        const uint32_t bit = 1u << (v & 31u);
-        if (!(vis[v >> 5] & bit)) won = !(atomicOr(&vis[v >> 5], bit) & bit);
-        if (won) {
-          level[v] = next_level;
-          atomicOr(&fb_next[v >> 5], bit);
-        }
-      }
-      warp_enqueue(won, v, won ? deg[v] : 0, &ctl->qpack, qn, offs_n);
-    }
-  }
-}
-
-// Pull pass 1: thread per unvisited row, at most kPullProbes probes.
-__global__ void __launch_bounds__(kThreads, 2) k_bfs_pull1(
-    Ctl* ctl, const uint64_t* __restrict__ ptr, const uint32_t* __restrict__ idx,
-    const uint32_t* __restrict__ fb, uint32_t s_words, uint32_t* vis, uint32_t* nbm,
-    int32_t* level, const uint32_t* __restrict__ outdeg, uint32_t* defq, uint64_t* defo) {
-  if (ctl->done || ctl->dir != kPull) return;
-  extern __shared__ uint32_t s_fb[];
-  for (uint32_t i = threadIdx.x; i < s_words; i += blockDim.x) s_fb[i] = fb[i];
-  __syncthreads();
-  const uint64_t nv = ctl->nv;
-  const int32_t next_level = ctl->it;
-  const uint64_t words = (nv + 31) / 32;
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned lane = lane_id();
-  unsigned long long found_n = 0, found_e = 0, examined = 0;
-  for (uint64_t w = warp; w < words; w += nwarps) {
-    const uint32_t vw = vis[w];
-    if (vw == 0xFFFFFFFFu) {  // warp-uniform: all 32 rows already visited
-      if (lane == 0) nbm[w] = 0u;
-      continue;
-    }
-    const uint64_t v = w * 32 + lane;
-    bool found = false, defer = false;
-    uint32_t rest = 0;
-    if (v < nv && !((vw >> lane) & 1u)) {
-      const uint64_t beg = ptr[v], end = ptr[v + 1];
-      const uint64_t d = end - beg;
-      const uint32_t lim = d < kPullProbes ? uint32_t(d) : kPullProbes;
-      for (uint32_t p = 0; p < lim && !found; p += 4) {
-        uint32_t u[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) u[k] = p + k < lim ? __ldg(&idx[beg + p + k]) : 0xFFFFFFFFu;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (!found && u[k] != 0xFFFFFFFFu) {
-            ++examined;
-            found = fb_probe(s_fb, s_words, fb, u[k]);
-          }
-        }
-      }
-      if (found) {
-        level[v] = next_level;
-        found_e += outdeg[v];
-      } else if (d > kPullProbes) {
-        defer = true;
-        rest = uint32_t(d - kPullProbes);
-      }
-    }
-    const unsigned b = __ballot_sync(0xffffffffu, found);
-    if (lane == 0) {
-      nbm[w] = b;
-      if (b) vis[w] = vw | b;
-    }
-    found_n += found;
-    if (__any_sync(0xffffffffu, defer)) warp_enqueue(defer, uint32_t(v), rest, &ctl->dpack, defq, defo);
-  }
-  warp_add_u64(&ctl->found_n, found_n);
-  warp_add_u64(&ctl->found_e, found_e);
-  warp_add_u64(&ctl->examined, examined);
-}
-
-// Pull pass 2: edge-balanced over the deferred rows' remaining in-edges; a row
-// is claimed once through its next-frontier bit.
-__global__ void __launch_bounds__(kThreads, 2) k_bfs_pull2(
-    Ctl* ctl, const uint32_t* __restrict__ defq, const uint64_t* __restrict__ defo,
-    const uint64_t* __restrict__ ptr, const uint32_t* __restrict__ idx,
-    const uint32_t* __restrict__ fb, uint32_t s_words, uint32_t* vis, uint32_t* nbm,
-    int32_t* level, const uint32_t* __restrict__ outdeg) {
-  if (ctl->done || ctl->dir != kPull) return;
-  const unsigned long long dp = ctl->dpack;
-  const uint32_t ndef = uint32_t(dp >> kCountShift);
-  const uint64_t total = dp & kEdgeMask;
-  if (ndef == 0) return;
-  extern __shared__ uint32_t s_fb[];
-  for (uint32_t i = threadIdx.x; i < s_words; i += blockDim.x) s_fb[i] = fb[i];
-  __syncthreads();
-  const int32_t next_level = ctl->it;
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned lane = lane_id();
-  unsigned long long found_n = 0, found_e = 0, examined = 0;
-  for (uint64_t wb = warp * 32 * kEPT; wb < total; wb += nwarps * 32 * kEPT) {
-    const uint64_t t0 = wb + uint64_t(lane) * kEPT;
-    if (t0 >= total) continue;
-    uint32_t i = find_source(defo, ndef, t0);
-    uint32_t v = defq[i];
-    uint64_t e = ptr[v] + kPullProbes + (t0 - defo[i]);
-    uint64_t rem = (i + 1 < ndef ? defo[i + 1] : total) - t0;
-    for (int k = 0; k < kEPT && t0 + k < total; ++k) {
-      while (rem == 0) {
-        ++i;
-        v = defq[i];
-        e = ptr[v] + kPullProbes;
-        rem = (i + 1 < ndef ? defo[i + 1] : total) - defo[i];
-      }
-      const uint32_t bit = 1u << (v & 31u);
-      if (!(nbm[v >> 5] & bit)) {
-        ++examined;
-        if (fb_probe(s_fb, s_words, fb, __ldg(&idx[e])) && !(atomicOr(&nbm[v >> 5], bit) & bit)) {
-          level[v] = next_level;
-          atomicOr(&vis[v >> 5], bit);
-          ++found_n;
-          found_e += outdeg[v];
-        }
-      }
-      ++e;
-      --rem;
-    }
-  }
-  warp_add_u64(&ctl->found_n, found_n);
-  warp_add_u64(&ctl->found_e, found_e);
-  warp_add_u64(&ctl->examined, examined);
-}
-
 // Caller-order output: out[v] = visited(p) ? level[p] : -1, p = perm[v].
 __global__ void k_bfs_output(uint64_t n, const uint32_t* perm, const uint32_t* vis,
                              const int32_t* level, int32_t* out) {
@@ -427,6 +280,514 @@ __global__ void k_bfs_output(uint64_t n, const uint32_t* perm, const uint32_t* v
        v += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t p = perm ? perm[v] : uint32_t(v);
     out[v] = bit_test(vis, p) ? level[p] : -1;
+  }
+}
+
+// ------------------------------------------------ cooperative BFS (all supersteps)
+// One persistent cooperative launch runs every superstep: phases are separated
+// by grid-wide barriers, the direction is decided identically by every block
+// from the device counters, and nothing returns to the host until the BFS is
+// done.  Data another block wrote in an earlier phase is read with ld.global.cg
+// (L2) so no SM sees a stale L1 line.
+constexpr unsigned kCoopThreads = 512;
+
+struct CoopArgs {
+  Ctl* ctl;
+  const uint64_t* in_ptr;
+  const uint32_t* in_idx;   // CSR(G^T): pull
+  const uint64_t* out_ptr;
+  const uint32_t* out_idx;  // CSR(G): push
+  const uint32_t* deg;      // out-degree
+  const uint32_t* indeg;    // in-degree (pull row length)
+  const uint4* head;        // first kHead in-neighbours of each pull row
+  int32_t* level;
+  uint32_t* vis;
+  uint32_t* fb[2];
+  uint32_t* q[2];
+  uint64_t* offs[2];
+  uint64_t* qe[2];          // start-edge pointer of each queued vertex
+  uint32_t* ul[2];          // unvisited-row lists
+  uint32_t* defq;
+  uint64_t* defo;
+  uint64_t* defe;           // deferred rows: first edge not probed in pass 1
+  uint64_t n, nv, m, words_all;
+  uint32_t s_words;
+  int32_t use_ulist;        // later pulls walk the unvisited-row list (else every row)
+};
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t find_source_cg(const uint64_t* offs, uint32_t nq, uint64_t t) {
+  uint32_t lo = 0, hi = nq;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldcg(&offs[mid]) <= t)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Warp-cooperative source lookup for edge t (t >= warp chunk start wb): lane 0
+// binary-searches the chunk start once; every lane then gallops from there
+// (its entry is a few slots away, in lines the warp already touched).
+__device__ __forceinline__ uint32_t warp_find_source(const uint64_t* offs, uint32_t nq, uint64_t wb,
+                                                     uint64_t t) {
+  uint32_t i0 = 0;
+  if (lane_id() == 0) i0 = find_source_cg(offs, nq, wb);
+  i0 = __shfl_sync(0xffffffffu, i0, 0);
+  uint32_t lo = i0, hi = nq, step = 1;
+  for (;;) {
+    const uint32_t p = lo + step;
+    if (p >= nq) break;
+    if (__ldcg(&offs[p]) > t) {
+      hi = p;
+      break;
+    }
+    lo = p;
+    step <<= 1;
+  }
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldcg(&offs[mid]) <= t)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// 32-way warp search: last i in [lo, hi) with offs[i] <= t, given offs[lo] <= t.
+// Each round is one batch of 32 independent loads (log32 rounds).
+__device__ __forceinline__ uint32_t warp_kary(const uint64_t* offs, uint32_t lo, uint32_t hi,
+                                              uint64_t t) {
+  const unsigned lane = lane_id();
+  while (hi - lo > 1) {
+    const uint32_t st = (hi - lo + 31) / 32;
+    const uint64_t p = uint64_t(lo) + uint64_t(lane + 1) * st;
+    const bool ok = p < hi && __ldcg(&offs[p]) <= t;
+    const unsigned b = __ballot_sync(0xffffffffu, ok);
+    lo += uint32_t(__popc(b)) * st;
+    hi = min(hi, lo + st);
+  }
+  return lo;
+}
+
+// Forward 32-way gallop from a known position (offs[lo] <= t): one round when
+// the answer is within 32 entries, which is the common case between chunks.
+__device__ __forceinline__ uint32_t warp_forward(const uint64_t* offs, uint32_t nq, uint32_t lo,
+                                                 uint64_t t) {
+  const unsigned lane = lane_id();
+  uint64_t step = 1;
+  for (;;) {
+    const uint64_t p = uint64_t(lo) + uint64_t(lane + 1) * step;
+    const bool ok = p < nq && __ldcg(&offs[p]) <= t;
+    const unsigned b = __ballot_sync(0xffffffffu, ok);
+    if (b != 0xffffffffu) {
+      const uint32_t base = lo + uint32_t(__popc(b) * step);
+      return step == 1 ? base
+                       : warp_kary(offs, base,
+                                   uint32_t(uint64_t(nq) < base + step ? uint64_t(nq) : base + step),
+                                   t);
+    }
+    lo += uint32_t(32 * step);
+    step *= 32;
+  }
+}
+
+// Per-lane gallop from the warp's chunk start (entries a few slots away).
+__device__ __forceinline__ uint32_t lane_gallop(const uint64_t* offs, uint32_t nq, uint32_t lo,
+                                                uint64_t t) {
+  uint32_t hi = nq, step = 1;
+  for (;;) {
+    const uint32_t p = lo + step;
+    if (p >= nq) break;
+    if (__ldcg(&offs[p]) > t) {
+      hi = p;
+      break;
+    }
+    lo = p;
+    step <<= 1;
+  }
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldcg(&offs[mid]) <= t)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// First kHead in-neighbours of every pull row as two 16-byte words loaded in
+// one round (0xFFFFFFFF pads short rows).  Built once per graph.
+constexpr int kHead = 8;
+
+__global__ void k_build_head(const uint64_t* ptr, const uint32_t* idx, uint64_t nv, uint4* head) {
+  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nv;
+       v += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t b = ptr[v], e = ptr[v + 1];
+    uint32_t h[kHead];
+#pragma unroll
+    for (int k = 0; k < kHead; ++k) h[k] = b + k < e ? idx[b + k] : 0xFFFFFFFFu;
+    head[2 * v] = make_uint4(h[0], h[1], h[2], h[3]);
+    head[2 * v + 1] = make_uint4(h[4], h[5], h[6], h[7]);
+  }
+}
+
+__device__ __forceinline__ void coop_push(const CoopArgs& a, int cur, uint64_t nf, uint64_t total,
+                                          int32_t next_level, uint64_t gwarp, uint64_t nwarps) {
+  const uint64_t* offs = a.offs[cur];
+  const uint64_t* qe = a.qe[cur];
+  uint32_t* qn = a.q[cur ^ 1];
+  uint64_t* on = a.offs[cur ^ 1];
+  uint64_t* qen = a.qe[cur ^ 1];
+  uint32_t* fbn = a.fb[cur ^ 1];
+  const uint32_t nq = uint32_t(nf);
+  const unsigned lane = lane_id();
+  // Each warp owns a contiguous edge range: one warp search for its first
+  // chunk, a forward gallop for the next ones.
+  const uint64_t e_lo = total * gwarp / nwarps, e_hi = total * (gwarp + 1) / nwarps;
+  uint32_t ib0 = 0;
+  bool first = true;
+  for (uint64_t wb = e_lo; wb < e_hi; wb += 32 * kEPT) {
+    const uint64_t t0 = wb + uint64_t(lane) * kEPT;
+    ib0 = first ? warp_kary(offs, 0, nq, wb) : warp_forward(offs, nq, ib0, wb);
+    first = false;
+    uint32_t i = lane_gallop(offs, nq, ib0, t0 < e_hi ? t0 : wb);
+    // 1) resolve this lane's kEPT edge slots (offsets / start pointers only)
+    uint64_t re[kEPT];
+    int nk = 0;
+    if (t0 < e_hi) {
+      uint64_t ib = __ldcg(&offs[i]);
+      uint64_t inx = i + 1 < nq ? __ldcg(&offs[i + 1]) : total;
+      uint64_t es = __ldcg(&qe[i]);
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k) {
+        const uint64_t t = t0 + k;
+        if (t < e_hi) {
+          while (t >= inx) {
+            ++i;
+            ib = inx;
+            inx = i + 1 < nq ? __ldcg(&offs[i + 1]) : total;
+            es = __ldcg(&qe[i]);
+          }
+          re[k] = es + (t - ib);
+          nk = k + 1;
+        }
+      }
+    }
+    // 2) all column loads in flight, then all visited probes
+    uint32_t vk[kEPT], visw[kEPT];
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) vk[k] = k < nk ? __ldg(&a.out_idx[re[k]]) : 0u;
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) visw[k] = k < nk ? __ldcg(&a.vis[vk[k] >> 5]) : 0xFFFFFFFFu;
+    // 3) claim, then one warp-aggregated append for all winners
+    uint32_t we[kEPT];
+    uint64_t ws[kEPT];
+    unsigned won = 0;
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) {
+      we[k] = 0;
+      ws[k] = 0;
+      if (k < nk) {
+        const uint32_t v = vk[k], bit = 1u << (v & 31u);
+        if (!(visw[k] & bit) && !(atomicOr(&a.vis[v >> 5], bit) & bit)) {
+          a.level[v] = next_level;
+          atomicOr(&fbn[v >> 5], bit);
+          won |= 1u << k;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) {
+      if ((won >> k) & 1u) {
+        const uint64_t ps = __ldg(&a.out_ptr[vk[k]]), pe = __ldg(&a.out_ptr[vk[k] + 1]);
+        we[k] = uint32_t(pe - ps);
+        ws[k] = ps;
+      }
+    }
+    warp_enqueue_multi<kEPT>(won, vk, we, ws, &a.ctl->qpack, qn, on, qen);
+  }
+}
+
+// Probe the kHead first in-neighbours of row v (two 16-byte loads in one
+// round); returns found, sets defer/rest for rows with more in-edges.
+__device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t* s_fb,
+                                               const uint32_t* fbc, uint64_t v, bool& defer,
+                                               uint32_t& rest, unsigned long long& examined) {
+  const uint4 h0 = __ldg(&a.head[2 * v]);
+  const uint4 h1 = __ldg(&a.head[2 * v + 1]);
+  const uint32_t d = __ldg(&a.indeg[v]);
+  const uint32_t u[kHead] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  bool found = false;
+#pragma unroll
+  for (int k = 0; k < kHead; ++k) {
+    if (!found && u[k] != 0xFFFFFFFFu) {
+      ++examined;
+      const uint32_t w = u[k] >> 5;
+      const uint32_t word = w < a.s_words ? s_fb[w] : __ldcg(&fbc[w]);
+      found = (word >> (u[k] & 31u)) & 1u;
+    }
+  }
+  defer = !found && d > kHead;
+  rest = defer ? d - kHead : 0u;
+  return found;
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint32_t s_fb[];
+  volatile Ctl* vc = a.ctl;
+  const uint64_t gtid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+  const unsigned lane = lane_id();
+  for (;;) {
+    grid.sync();
+    if (vc->done) break;
+    const int32_t it = vc->it + 1;
+    const int cur = it & 1;
+    const uint64_t nf = vc->nf, mf = vc->mf;
+    const bool pull = it == 1 ? false
+                              : (vc->prev_pull ? nf * 24 >= a.n : double(mf) > 0.05 * double(a.m));
+    if (gtid == 0 && it <= kMaxRecorded) {
+      a.ctl->t_start[it - 1] = globaltimer();
+      a.ctl->t_mid[it - 1] = 0;
+    }
+    uint32_t* fbc = a.fb[cur];
+    uint32_t* fbn = a.fb[cur ^ 1];
+    if (!pull) {
+      if (!vc->cur_is_queue) {  // frontier bitmap -> queue with edge offsets
+        const uint64_t words = (a.n + 31) / 32;
+        // lanes load 32 consecutive words at once; the warp then walks the
+        // nonzero ones, a lane per bit
+        for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
+          const uint64_t wl = gwarp + (k0 + lane) * nwarps;
+          const uint32_t myword = wl < words ? __ldcg(&fbc[wl]) : 0u;
+          unsigned nz = __ballot_sync(0xffffffffu, myword != 0u);
+          while (nz) {
+            const int j = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t word = __shfl_sync(0xffffffffu, myword, j);
+            const uint32_t v = uint32_t((gwarp + (k0 + j) * nwarps) * 32 + lane);
+            const bool set = (word >> lane) & 1u;
+            uint32_t ed = 0;
+            uint64_t ps = 0;
+            if (set) {
+              ps = __ldg(&a.out_ptr[v]);
+              ed = uint32_t(__ldg(&a.out_ptr[v + 1]) - ps);
+            }
+            warp_enqueue_multi<1>(set ? 1u : 0u, &v, &ed, &ps, &a.ctl->bpack, a.q[cur], a.offs[cur],
+                                  a.qe[cur]);
+          }
+        }
+        grid.sync();
+        if (gtid == 0 && it <= kMaxRecorded) a.ctl->t_mid[it - 1] = globaltimer();
+      }
+      coop_push(a, cur, nf, mf, it, gwarp, nwarps);
+    } else {
+      for (uint32_t i = threadIdx.x; i < a.s_words; i += blockDim.x) s_fb[i] = __ldcg(&fbc[i]);
+      __syncthreads();
+      unsigned long long found_n = 0, found_e = 0, examined = 0;
+      const int us = vc->usel;
+      uint32_t* unext = a.ul[us ^ 1];
+      // A large frontier leaves few rows unvisited: only then is the list of
+      // the remaining rows worth building for the next pull.
+      const bool build_list = a.use_ulist && nf * 16 >= a.n;
+      if (vc->u_implicit) {
+        const uint64_t words = (a.nv + 31) / 32;
+        // Words are dealt round-robin (warp g owns g, g + nwarps, ...) so every
+        // warp gets a statistically equal share; lanes prefetch the visited
+        // words of the warp's next 32 assignments in one load.
+        for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
+         const uint64_t wl = gwarp + (k0 + lane) * nwarps;
+         const uint32_t myvis = wl < words ? __ldcg(&a.vis[wl]) : 0xFFFFFFFFu;
+         unsigned open_words = __ballot_sync(0xffffffffu, myvis != 0xFFFFFFFFu);
+         while (open_words) {
+          const int j = __ffs(open_words) - 1;
+          open_words &= open_words - 1;
+          const uint64_t w = gwarp + (k0 + j) * nwarps;
+          const uint32_t vw = __shfl_sync(0xffffffffu, myvis, j);
+          const uint64_t v = w * 32 + lane;
+          bool found = false, defer = false;
+          uint32_t rest = 0;
+          const bool open = v < a.nv && !((vw >> lane) & 1u);
+          if (open) {
+            found = coop_probe_row(a, s_fb, fbc, v, defer, rest, examined);
+            if (found) {
+              a.level[v] = it;
+              found_e += __ldg(&a.deg[v]);
+            }
+          }
+          const unsigned b = __ballot_sync(0xffffffffu, found);
+          if (lane == 0 && b) {
+            fbn[w] = b;  // word exclusively owned in this pass
+            a.vis[w] = vw | b;
+          }
+          found_n += found;
+          if (__any_sync(0xffffffffu, defer)) {
+            const uint32_t vv = uint32_t(v);
+            const uint64_t es = defer ? __ldg(&a.in_ptr[v]) + kHead : 0;
+            warp_enqueue_multi<1>(defer ? 1u : 0u, &vv, &rest, &es, &a.ctl->dpack, a.defq, a.defo,
+                                  a.defe);
+          }
+          const bool keep = open && !found;
+          if (build_list && __any_sync(0xffffffffu, keep))
+            warp_enqueue(keep, uint32_t(v), 0, &a.ctl->upack, unext, nullptr);
+         }
+        }
+      } else {
+        const uint64_t cnt = vc->ucur;
+        const uint32_t* ucur = a.ul[us];
+        for (uint64_t base = gwarp * 32; base < cnt; base += nwarps * 32) {
+          const uint64_t i = base + lane;
+          bool found = false, defer = false, open = false;
+          uint32_t rest = 0, v = 0;
+          if (i < cnt) {
+            v = __ldcg(&ucur[i]);
+            open = !((__ldcg(&a.vis[v >> 5]) >> (v & 31u)) & 1u);
+            if (open) {
+              found = coop_probe_row(a, s_fb, fbc, v, defer, rest, examined);
+              if (found) {
+                const uint32_t bit = 1u << (v & 31u);
+                a.level[v] = it;
+                atomicOr(&fbn[v >> 5], bit);
+                atomicOr(&a.vis[v >> 5], bit);
+                found_e += __ldg(&a.deg[v]);
+              }
+            }
+          }
+          found_n += found;
+          if (__any_sync(0xffffffffu, defer)) {
+            const uint64_t es = defer ? __ldg(&a.in_ptr[v]) + kHead : 0;
+            warp_enqueue_multi<1>(defer ? 1u : 0u, &v, &rest, &es, &a.ctl->dpack, a.defq, a.defo,
+                                  a.defe);
+          }
+          const bool keep = open && !found;
+          if (build_list && __any_sync(0xffffffffu, keep))
+            warp_enqueue(keep, v, 0, &a.ctl->upack, unext, nullptr);
+        }
+      }
+      grid.sync();
+      if (gtid == 0 && it <= kMaxRecorded) a.ctl->t_mid[it - 1] = globaltimer();
+      // pass 2: edge-balanced over the deferred rows' remaining in-edges:
+      // resolve the slots, put every column load in flight, then probe.
+      const unsigned long long dp = vc->dpack;
+      const uint32_t ndef = uint32_t(dp >> kCountShift);
+      const uint64_t total = dp & kEdgeMask;
+      const uint64_t e_lo = total * gwarp / nwarps, e_hi = total * (gwarp + 1) / nwarps;
+      uint32_t ib0 = 0;
+      bool first = true;
+      for (uint64_t wb = e_lo; wb < e_hi; wb += 32 * kEPT) {
+        const uint64_t t0 = wb + uint64_t(lane) * kEPT;
+        ib0 = first ? warp_kary(a.defo, 0, ndef, wb) : warp_forward(a.defo, ndef, ib0, wb);
+        first = false;
+        uint32_t i = lane_gallop(a.defo, ndef, ib0, t0 < e_hi ? t0 : wb);
+        uint32_t rv[kEPT];
+        uint64_t re[kEPT];
+        int nk = 0;
+        if (t0 < e_hi) {
+          uint64_t ib = __ldcg(&a.defo[i]);
+          uint64_t inx = i + 1 < ndef ? __ldcg(&a.defo[i + 1]) : total;
+          uint64_t es = __ldcg(&a.defe[i]);
+          uint32_t v = __ldcg(&a.defq[i]);
+#pragma unroll
+          for (int k = 0; k < kEPT; ++k) {
+            const uint64_t t = t0 + k;
+            rv[k] = v;
+            re[k] = 0;
+            if (t < e_hi) {
+              while (t >= inx) {
+                ++i;
+                ib = inx;
+                inx = i + 1 < ndef ? __ldcg(&a.defo[i + 1]) : total;
+                es = __ldcg(&a.defe[i]);
+                v = __ldcg(&a.defq[i]);
+              }
+              rv[k] = v;
+              re[k] = es + (t - ib);
+              nk = k + 1;
+            }
+          }
+        }
+        uint32_t u[kEPT];
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) u[k] = k < nk ? __ldg(&a.in_idx[re[k]]) : 0xFFFFFFFFu;
+        // rows already found (by an earlier chunk) skip their probe; this load
+        // is issued alongside the column loads, off the critical path
+        uint32_t done_w[kEPT];
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) done_w[k] = k < nk ? __ldcg(&fbn[rv[k] >> 5]) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < kEPT; ++k) {
+          const uint32_t bit = 1u << (rv[k] & 31u);
+          if (k < nk && !(done_w[k] & bit)) {
+            ++examined;
+            const uint32_t w = u[k] >> 5;
+            const uint32_t word = w < a.s_words ? s_fb[w] : __ldcg(&fbc[w]);
+            if ((word >> (u[k] & 31u)) & 1u) {
+              const uint32_t v = rv[k];
+              if (!(atomicOr(&fbn[v >> 5], bit) & bit)) {
+                a.level[v] = it;
+                atomicOr(&a.vis[v >> 5], bit);
+                ++found_n;
+                found_e += __ldg(&a.deg[v]);
+              }
+            }
+          }
+        }
+      }
+      warp_add_u64(&a.ctl->found_n, found_n);
+      warp_add_u64(&a.ctl->found_e, found_e);
+      warp_add_u64(&a.ctl->examined, examined);
+    }
+    grid.sync();
+    // finish: the consumed frontier bitmap becomes the next step's output buffer
+    for (uint64_t w = gtid; w < a.words_all; w += gthreads) fbc[w] = 0u;
+    if (gtid == 0) {
+      Ctl* c = a.ctl;
+      uint64_t nn, mn;
+      if (!pull) {
+        nn = c->qpack >> kCountShift;
+        mn = c->qpack & kEdgeMask;
+        a.offs[cur ^ 1][nn] = mn;
+      } else {
+        nn = c->found_n;
+        mn = c->found_e;
+        c->ucur = c->upack >> kCountShift;
+        const bool built = a.use_ulist && nf * 16 >= a.n;
+        c->u_implicit = built ? 0 : 1;
+        c->usel ^= 1;
+      }
+      if (it <= kMaxRecorded) {
+        StepRec& r = c->rec[it - 1];
+        r.active = int64_t(nf);
+        r.updated = int64_t(nn);
+        r.edges = int64_t(pull ? c->examined : mf);
+        r.examined = int64_t(c->examined);
+        r.deferred = int64_t(c->dpack >> kCountShift);
+        r.deferred_edges = int64_t(c->dpack & kEdgeMask);
+        r.dir = pull ? kPull : kPush;
+        c->t_end[it - 1] = globaltimer();
+      }
+      c->prev_pull = pull;
+      c->cur_is_queue = !pull;
+      c->nf = nn;
+      c->mf = mn;
+      c->it = it;
+      c->qpack = c->dpack = c->bpack = c->upack = 0;
+      c->found_n = c->found_e = c->examined = 0;
+      if (nn == 0 || it >= c->max_it) c->done = 1;
+      __threadfence();
+    }
   }
 }
 
@@ -615,56 +976,114 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
     fail(GM_EUSAGE, "bfs: graphs above 2^28 vertices are not supported by the packed queue");
   TravCache& c = cache(g);
   cudaStream_t s = g.stream;
-  if (!c.level) c.level.alloc(n, s);
-  if (!c.attrs) {
-    GM_CUDA(cudaFuncSetAttribute(k_bfs_pull1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kSmemFbWords * 4)));
-    GM_CUDA(cudaFuncSetAttribute(k_bfs_pull2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kSmemFbWords * 4)));
-    c.attrs = true;
-  }
-  ensure_forward(g);
-  const Csr& fw = g.fwd();
   const uint64_t words = (n + 31) / 32;
   // Pull rows: on a relabeled symmetric graph only the nonzero-degree prefix
   // can ever be reached.
   const uint64_t nv = (g.relabeled && g.symmetric) ? g.nonzero_outdeg : n;
   const uint32_t s_words = uint32_t(std::min<uint64_t>(kSmemFbWords, (nv + 31) / 32));
-  const size_t smem = size_t(s_words) * 4;
+  const size_t smem = size_t(kSmemFbWords) * 4;
+  if (!c.level) {
+    c.level.alloc(n, s);
+    c.head.alloc(2 * nv + 2, s);
+    if (nv) {
+      k_build_head<<<grid_for(nv, 256), 256, 0, s>>>(g.in.ptr.get(), g.in.idx.get(), nv, c.head.get());
+      GM_LAUNCH_CHECK();
+    }
+    GM_CUDA(cudaFuncSetAttribute(k_bfs_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0, dev = 0, sms = 0;
+    GM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_coop, kCoopThreads, smem));
+    GM_CUDA(cudaGetDevice(&dev));
+    GM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (per_sm < 1) fail(GM_ECUDA, "bfs: cooperative kernel does not fit on an SM");
+    c.coop_grid = unsigned(std::min(per_sm, 2) * sms);
+  }
+  ensure_forward(g);
+  const Csr& fw = g.fwd();
   const uint32_t* perm = g.relabeled ? g.perm.get() : nullptr;
   const int32_t max_it = int32_t(std::min<int64_t>(max_iters, 0x7FFFFFFF));
   Ctl* ctl = c.ctl.get();
+  GM_CUDA(cudaMemsetAsync(ctl, 0, offsetof(Ctl, t_start), s));
+  GM_CUDA(cudaMemsetAsync(c.fb[0].get(), 0, (words + 1) * 4, s));
+  GM_CUDA(cudaMemsetAsync(c.fb[1].get(), 0, (words + 1) * 4, s));
   k_bfs_init<<<grid_for(words + 1, 256), 256, 0, s>>>(ctl, c.vis.get(), words + 1, root, perm,
-                                                      c.q[1].get(), c.offs[1].get(),
-                                                      g.outdeg.get(), c.level.get(), n, g.m, nv,
-                                                      max_it);
+                                                      c.q[1].get(), c.offs[1].get(), c.qe[1].get(),
+                                                      fw.ptr.get(), g.outdeg.get(), c.level.get(), n,
+                                                      g.m, nv, max_it);
   GM_LAUNCH_CHECK();
-  const int64_t enq = run_batches(c, s, max_iters, collect, [&](int64_t it) {
-    const int cur = int(it & 1), nxt = cur ^ 1;
-    GM_CUDA(cudaMemsetAsync(c.fb[nxt].get(), 0, (words + 1) * 4, s));
-    k_decide<<<1, 1, 0, s>>>(ctl, c.offs[cur].get());
-    GM_LAUNCH_CHECK();
-    // push path (kernels exit at once when the device chose pull)
-    k_bfs_b2q<<<kGrid, kThreads, 0, s>>>(ctl, c.fb[cur].get(), words, g.outdeg.get(), c.q[cur].get(),
-                                          c.offs[cur].get(), &ctl->dpack);
-    GM_LAUNCH_CHECK();
-    k_bfs_push<<<kGrid, kThreads, 0, s>>>(ctl, c.q[cur].get(), c.offs[cur].get(), fw.ptr.get(),
-                                           fw.idx.get(), g.outdeg.get(), c.level.get(), c.vis.get(),
-                                           c.fb[nxt].get(), c.q[nxt].get(), c.offs[nxt].get());
-    GM_LAUNCH_CHECK();
-    // pull path
-    k_bfs_pull1<<<kGrid, kThreads, smem, s>>>(ctl, g.in.ptr.get(), g.in.idx.get(), c.fb[cur].get(),
-                                              s_words, c.vis.get(), c.fb[nxt].get(), c.level.get(),
-                                              g.outdeg.get(), c.defq.get(), c.defo.get());
-    GM_LAUNCH_CHECK();
-    k_bfs_pull2<<<kGrid, kThreads, smem, s>>>(ctl, c.defq.get(), c.defo.get(), g.in.ptr.get(),
-                                              g.in.idx.get(), c.fb[cur].get(), s_words, c.vis.get(),
-                                              c.fb[nxt].get(), c.level.get(), g.outdeg.get());
-    GM_LAUNCH_CHECK();
-    k_finish<<<1, 1, 0, s>>>(ctl, c.offs[nxt].get());
-    GM_LAUNCH_CHECK();
-  });
-  std::vector<gm_iteration_stats> stats = read_records(c, s, enq, n, nv, collect);
+  CoopArgs a{};
+  a.ctl = ctl;
+  a.in_ptr = g.in.ptr.get();
+  a.in_idx = g.in.idx.get();
+  a.out_ptr = fw.ptr.get();
+  a.out_idx = fw.idx.get();
+  a.deg = g.outdeg.get();
+  a.indeg = g.indeg.get();
+  a.head = c.head.get();
+  a.level = c.level.get();
+  a.vis = c.vis.get();
+  for (int i = 0; i < 2; ++i) {
+    a.fb[i] = c.fb[i].get();
+    a.q[i] = c.q[i].get();
+    a.offs[i] = c.offs[i].get();
+    a.qe[i] = c.qe[i].get();
+    a.ul[i] = c.ul[i].get();
+  }
+  a.defq = c.defq.get();
+  a.defo = c.defo.get();
+  a.defe = c.defe.get();
+  a.n = n;
+  a.nv = nv;
+  a.m = g.m;
+  a.words_all = words + 1;
+  a.s_words = s_words;
+  {
+    const char* e = getenv("GM_BFS_ULIST");
+    a.use_ulist = e ? atoi(e) : 1;
+  }
+  void* args[] = {&a};
+  GM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs_coop), dim3(c.coop_grid),
+                                      dim3(kCoopThreads), args, smem, s));
+  ::gm::count_launch();
+  std::vector<gm_iteration_stats> stats;
+  if (collect) {
+    int32_t it = 0;
+    GM_CUDA(cudaMemcpyAsync(&it, &ctl->it, 4, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    const int64_t nrec = std::min<int64_t>(it, kMaxRecorded);
+    std::vector<StepRec> rec(size_t(nrec > 0 ? nrec : 1));
+    std::vector<uint64_t> t0(rec.size()), t1(rec.size());
+    if (nrec > 0) {
+      GM_CUDA(cudaMemcpyAsync(rec.data(), ctl->rec, nrec * sizeof(StepRec), cudaMemcpyDeviceToHost, s));
+      GM_CUDA(cudaMemcpyAsync(t0.data(), ctl->t_start, nrec * 8, cudaMemcpyDeviceToHost, s));
+      GM_CUDA(cudaMemcpyAsync(t1.data(), ctl->t_end, nrec * 8, cudaMemcpyDeviceToHost, s));
+    }
+    GM_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint64_t> tm(rec.size());
+    if (nrec > 0 && getenv("GM_BFS_PHASES")) {
+      GM_CUDA(cudaMemcpy(tm.data(), ctl->t_mid, nrec * 8, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < nrec; ++i)
+        fprintf(stderr, "bfs step %lld dir=%d phase1=%.1fus total=%.1fus examined=%lld deferred=%lld/%lld\n",
+                (long long)(i + 1), rec[i].dir, tm[i] ? double(tm[i] - t0[i]) * 1e-3 : 0.0,
+                double(t1[i] - t0[i]) * 1e-3, (long long)rec[i].examined, (long long)rec[i].deferred,
+                (long long)rec[i].deferred_edges);
+    }
+    for (int64_t i = 0; i < nrec; ++i) {
+      const StepRec& r = rec[i];
+      gm_iteration_stats st{};
+      st.iteration = i + 1;
+      st.active_before = r.active;
+      st.messages_generated = r.active;
+      st.vertices_updated = r.updated;
+      st.spmv_seconds = double(t1[i] - t0[i]) * 1e-9;
+      st.total_seconds = st.spmv_seconds;
+      st.edges_processed = r.edges;
+      st.direction = r.dir == kPush ? 1 : 0;
+      st.bytes_algorithmic = r.dir == kPush
+                                 ? int64_t(24 * r.active + 4 * r.edges + 16 * r.updated + n / 8)
+                                 : int64_t(16 * nv + 4 * r.examined + 4 * r.updated + 2 * n / 8);
+      stats.push_back(st);
+    }
+  }
   if (out) {
     int32_t* dst = out;
     if (!out_on_device) {

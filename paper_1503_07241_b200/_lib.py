@@ -67,6 +67,7 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("GM_LIB", path)  # alternative build of the same ABI (experiments)
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -426,17 +426,23 @@ __device__ __forceinline__ uint32_t lane_gallop(const uint64_t* offs, uint32_t n
 
 // First kHead in-neighbours of every pull row as two 16-byte words loaded in
 // one round (0xFFFFFFFF pads short rows).  Built once per graph.
-constexpr int kHead = 8;
+#ifndef GM_BFS_HEAD
+#define GM_BFS_HEAD 16
+#endif
+constexpr int kHead = GM_BFS_HEAD;  // multiple of 4
+constexpr int kHeadVec = kHead / 4;
 
 __global__ void k_build_head(const uint64_t* ptr, const uint32_t* idx, uint64_t nv, uint4* head) {
   for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nv;
        v += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t b = ptr[v], e = ptr[v + 1];
-    uint32_t h[kHead];
 #pragma unroll
-    for (int k = 0; k < kHead; ++k) h[k] = b + k < e ? idx[b + k] : 0xFFFFFFFFu;
-    head[2 * v] = make_uint4(h[0], h[1], h[2], h[3]);
-    head[2 * v + 1] = make_uint4(h[4], h[5], h[6], h[7]);
+    for (int j = 0; j < kHeadVec; ++j) {
+      uint32_t h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = b + 4 * j + k < e ? idx[b + 4 * j + k] : 0xFFFFFFFFu;
+      head[kHeadVec * v + j] = make_uint4(h[0], h[1], h[2], h[3]);
+    }
   }
 }
 
@@ -517,15 +523,25 @@ __device__ __forceinline__ void coop_push(const CoopArgs& a, int cur, uint64_t n
   }
 }
 
-// Probe the kHead first in-neighbours of row v (two 16-byte loads in one
-// round); returns found, sets defer/rest for rows with more in-edges.
+// Probe the first 4*hv in-neighbours of row v (hv 16-byte head loads, all in
+// one round); returns found, sets defer/rest for rows with more in-edges.
+// hv shrinks when the frontier is large: the first probe then almost always
+// hits and the rest of the head would be wasted bandwidth.
 __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t* s_fb,
-                                               const uint32_t* fbc, uint64_t v, bool& defer,
-                                               uint32_t& rest, unsigned long long& examined) {
-  const uint4 h0 = __ldg(&a.head[2 * v]);
-  const uint4 h1 = __ldg(&a.head[2 * v + 1]);
+                                               const uint32_t* fbc, uint64_t v, int hv,
+                                               bool& defer, uint32_t& rest,
+                                               unsigned long long& examined) {
+  uint32_t u[kHead];
+#pragma unroll
+  for (int j = 0; j < kHeadVec; ++j) {
+    uint4 h = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (j < hv) h = __ldg(&a.head[kHeadVec * v + j]);
+    u[4 * j] = h.x;
+    u[4 * j + 1] = h.y;
+    u[4 * j + 2] = h.z;
+    u[4 * j + 3] = h.w;
+  }
   const uint32_t d = __ldg(&a.indeg[v]);
-  const uint32_t u[kHead] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
   bool found = false;
 #pragma unroll
   for (int k = 0; k < kHead; ++k) {
@@ -536,8 +552,9 @@ __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t
       found = (word >> (u[k] & 31u)) & 1u;
     }
   }
-  defer = !found && d > kHead;
-  rest = defer ? d - kHead : 0u;
+  const uint32_t probed = 4u * uint32_t(hv);
+  defer = !found && d > probed;
+  rest = defer ? d - probed : 0u;
   return found;
 }
 
@@ -602,6 +619,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
       // A large frontier leaves few rows unvisited: only then is the list of
       // the remaining rows worth building for the next pull.
       const bool build_list = a.use_ulist && nf * 16 >= a.n;
+      const int hv = nf * 32 >= a.n ? 1 : kHeadVec;
       if (vc->u_implicit) {
         const uint64_t words = (a.nv + 31) / 32;
         // Words are dealt round-robin (warp g owns g, g + nwarps, ...) so every
@@ -621,7 +639,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
           uint32_t rest = 0;
           const bool open = v < a.nv && !((vw >> lane) & 1u);
           if (open) {
-            found = coop_probe_row(a, s_fb, fbc, v, defer, rest, examined);
+            found = coop_probe_row(a, s_fb, fbc, v, hv, defer, rest, examined);
             if (found) {
               a.level[v] = it;
               found_e += __ldg(&a.deg[v]);
@@ -635,7 +653,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
           found_n += found;
           if (__any_sync(0xffffffffu, defer)) {
             const uint32_t vv = uint32_t(v);
-            const uint64_t es = defer ? __ldg(&a.in_ptr[v]) + kHead : 0;
+            const uint64_t es = defer ? __ldg(&a.in_ptr[v]) + 4u * hv : 0;
             warp_enqueue_multi<1>(defer ? 1u : 0u, &vv, &rest, &es, &a.ctl->dpack, a.defq, a.defo,
                                   a.defe);
           }
@@ -655,7 +673,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
             v = __ldcg(&ucur[i]);
             open = !((__ldcg(&a.vis[v >> 5]) >> (v & 31u)) & 1u);
             if (open) {
-              found = coop_probe_row(a, s_fb, fbc, v, defer, rest, examined);
+              found = coop_probe_row(a, s_fb, fbc, v, hv, defer, rest, examined);
               if (found) {
                 const uint32_t bit = 1u << (v & 31u);
                 a.level[v] = it;
@@ -667,7 +685,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
           }
           found_n += found;
           if (__any_sync(0xffffffffu, defer)) {
-            const uint64_t es = defer ? __ldg(&a.in_ptr[v]) + kHead : 0;
+            const uint64_t es = defer ? __ldg(&a.in_ptr[v]) + 4u * hv : 0;
             warp_enqueue_multi<1>(defer ? 1u : 0u, &v, &rest, &es, &a.ctl->dpack, a.defq, a.defo,
                                   a.defe);
           }
@@ -984,7 +1002,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   const size_t smem = size_t(kSmemFbWords) * 4;
   if (!c.level) {
     c.level.alloc(n, s);
-    c.head.alloc(2 * nv + 2, s);
+    c.head.alloc(size_t(kHeadVec) * (nv + 1), s);
     if (nv) {
       k_build_head<<<grid_for(nv, 256), 256, 0, s>>>(g.in.ptr.get(), g.in.idx.get(), nv, c.head.get());
       GM_LAUNCH_CHECK();

@@ -216,7 +216,9 @@ class BfsWorkload(Workload):
         R = orc.ref_lib()
         kind = "reference" if R is not None else "port"
         if R is not None:
-            b, _, secs = orc.ref_bfs(self.n, s, d, self.root, threads=0)
+            rg = orc.RefGraph("dist", self.n, s, d, threads=0)
+            _, _, secs = rg.run_dist("bfs", self.root)
+            rg.close()
             cores = int(R.ref_hardware_threads())
         else:
             t0 = time.perf_counter()
@@ -277,7 +279,9 @@ class PageRankWorkload(Workload):
         s, d, _ = self.g.edges()
         R = orc.ref_lib()
         if R is not None:
-            _, _, secs = orc.ref_pagerank_norm(self.n, s, d, 0.85, self.iters, threads=0)
+            rg = orc.RefGraph("pr", self.n, s, d, threads=0)
+            _, secs = rg.run_pagerank(0.85, self.iters)
+            rg.close()
             cores, kind = int(R.ref_hardware_threads()), "reference"
         else:
             t0 = time.perf_counter()
@@ -303,12 +307,16 @@ class SsspWorkload(Workload):
         import torch
         self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
         self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
-        _, st = gm.sssp(self.g, self.root)
-        self.edges = int(sum(s.edges_processed for s in st))
+        dist, st = gm.sssp(self.g, self.root)
+        deg = self.g.degree_vector("out")
+        # Graph500 convention: out-edges of every reached source
+        self.edges = int(deg[dist != 0xFFFFFFFF].sum())
+        self.relaxed = int(sum(s.edges_processed for s in st))
         self.config = {"workload": f"sssp_rmat{a.scale}", "scale": a.scale, "edge_factor": 16,
                        "n": self.n, "m": self.g.num_edges, "root": self.root,
                        "weights": "uint8 in [1,255] from the seed",
-                       "teps_edges": self.edges, "teps": "edges relaxed over all supersteps"}
+                       "teps_edges": self.edges, "edges_relaxed": self.relaxed,
+                       "teps": "edges whose source is reached / time (Graph500)"}
 
     def run_device(self, gm):
         gm.sssp(self.g, self.root, with_stats=False, out_device_ptr=self.dev_out.data_ptr())
@@ -336,7 +344,9 @@ class SsspWorkload(Workload):
     def cpu_baseline(self, orc):
         s, d, w = self.g.edges()
         R = orc.ref_lib()
-        _, _, secs = orc.ref_sssp(self.n, s, d, w.astype(np.float64), self.root, threads=0)
+        rg = orc.RefGraph("dist", self.n, s, d, w.astype(np.float64), threads=0)
+        _, _, secs = rg.run_dist("sssp", self.root)
+        rg.close()
         return {"value": round(self.edges / secs / 1e9, 6), "unit": "GTEPS",
                 "cores": int(R.ref_hardware_threads()), "kind": "reference",
                 "seconds": round(secs, 4),
@@ -480,25 +490,37 @@ def run_reference(args, d: Dist):
     n = 1 << scale
     t0 = time.perf_counter()
     s, dd = oracle.rmat(scale, 16, seed=args.seed, **RMAT)
-    if args.workload == "bfs":
-        s, dd, _ = oracle.preprocess(s, dd, symmetrize=True)
+    if args.workload in ("bfs", "sssp"):
+        sym = args.workload == "bfs"
+        s, dd, _ = oracle.preprocess(s, dd, symmetrize=sym)
         deg = np.bincount(s, minlength=n).astype(np.uint32)
         root = oracle.pick_source(args.seed, deg)
+        w = None if sym else oracle.edge_weights(args.seed, s, dd).astype(np.float64)
+        rg = oracle.RefGraph("dist", n, s, dd, w, threads=0)
         gen_s = time.perf_counter() - t0
-        lvl, _ = oracle.bfs(n, s, dd, root, presorted=True)
-        edges = int(deg[lvl >= 0].sum()) // 2
+        _, st, _ = rg.run_dist(args.workload, root)
+        # Graph500 convention: edges inside the reached component (undirected
+        # edges for the symmetrised BFS graph, out-edges of reached sources for SSSP)
+        if sym:
+            lvl, _ = oracle.bfs(n, s, dd, root, presorted=True)
+            edges = int(deg[lvl >= 0].sum()) // 2
+        else:
+            dist, _ = oracle.sssp(n, s, dd, w.astype(np.uint8), root, presorted=True)
+            edges = int(deg[dist != 0xFFFFFFFF].sum())
 
         def step():
-            return oracle.ref_bfs(n, s, dd, root, threads=0)[2]
-        config = {"workload": f"bfs_rmat{scale}_sym", "scale": scale, "edge_factor": 16,
-                  "n": n, "m_directed": len(s), "root": root, "teps_edges": edges}
+            return rg.run_dist(args.workload, root)[2]
+        config = {"workload": f"{args.workload}_rmat{scale}{'_sym' if sym else ''}",
+                  "scale": scale, "edge_factor": 16, "n": n, "m_directed": len(s), "root": root,
+                  "teps_edges": edges}
     elif args.workload in ("pagerank", "pagerank23"):
         s, dd, _ = oracle.preprocess(s, dd)
+        rg = oracle.RefGraph("pr", n, s, dd, threads=0)
         gen_s = time.perf_counter() - t0
         edges = len(s) * 20
 
         def step():
-            return oracle.ref_pagerank_norm(n, s, dd, 0.85, 20, threads=0)[2]
+            return rg.run_pagerank(0.85, 20)[1]
         config = {"workload": f"pagerank_rmat{scale}", "scale": scale, "n": n, "m": len(s),
                   "iterations": 20}
     else:

@@ -405,3 +405,71 @@ def ref_semiring_spmv(n, src, dst, vals, x, xvalid, threads=1, parts=1):
               np.ascontiguousarray(vals, np.int64), np.ascontiguousarray(x, np.int64),
               np.ascontiguousarray(xvalid, np.uint8), threads, parts, y, yv)
     return y, yv.astype(bool)
+
+
+class RefGraph:
+    """Reference graph built once, run many times (oracle/_ref handle API).
+
+    kind "dist": algo::bfs / algo::sssp; kind "pr": BASELINE PageRank driver.
+    Only the algorithm time is reported, like tools/sgraph.cpp:101-103."""
+
+    def __init__(self, kind, n, src, dst, weights=None, threads=0):
+        R = ref_lib()
+        if R is None:
+            raise RuntimeError("oracle/_ref not built")
+        self.R, self.kind, self.n = R, kind, n
+        R.ref_dist_graph_new.restype = C.c_void_p
+        R.ref_dist_graph_new.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, C.c_void_p, C.c_uint]
+        R.ref_pr_graph_new.restype = C.c_void_p
+        R.ref_pr_graph_new.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, C.c_uint]
+        R.ref_dist_graph_free.argtypes = [C.c_void_p]
+        R.ref_pr_graph_free.argtypes = [C.c_void_p]
+        R.ref_dist_run.restype = C.c_int
+        R.ref_dist_run.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int64, C.c_void_p,
+                                   C.POINTER(Stats), C.c_int64, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_double)]
+        R.ref_pr_norm_run.restype = C.c_int
+        R.ref_pr_norm_run.argtypes = [C.c_void_p, C.c_double, C.c_int64, C.c_void_p,
+                                      C.POINTER(C.c_double)]
+        src, dst = _u32(src), _u32(dst)
+        if kind == "dist":
+            w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+            self.h = R.ref_dist_graph_new(n, len(src), src, dst,
+                                          w.ctypes.data if w is not None else None, threads)
+            self._free = R.ref_dist_graph_free
+        else:
+            self.h = R.ref_pr_graph_new(n, len(src), src, dst, threads)
+            self._free = R.ref_pr_graph_free
+        if not self.h:
+            raise RefError(2, R.ref_last_error().decode())
+
+    def run_dist(self, kind, root, max_iters=None, want_output=False):
+        out = np.empty(self.n, np.float64) if want_output else None
+        cap = 4096
+        st = (Stats * cap)()
+        k = C.c_int64()
+        t = C.c_double()
+        rc = self.R.ref_dist_run(self.h, 0 if kind == "bfs" else 1, root,
+                                 max_iters if max_iters is not None else self.n + 1,
+                                 out.ctypes.data if out is not None else None, st, cap,
+                                 C.byref(k), C.byref(t))
+        if rc:
+            raise RefError(rc, self.R.ref_last_error().decode())
+        return out, stats_tuples(st, min(k.value, cap)), t.value
+
+    def run_pagerank(self, damping=0.85, iters=20, want_output=False):
+        out = np.empty(self.n, np.float64) if want_output else None
+        t = C.c_double()
+        rc = self.R.ref_pr_norm_run(self.h, damping, iters,
+                                    out.ctypes.data if out is not None else None, C.byref(t))
+        if rc:
+            raise RefError(rc, self.R.ref_last_error().decode())
+        return out, t.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

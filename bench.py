@@ -37,6 +37,18 @@ METRIC = "GTEPS (edges/s) per superstep & end-to-end; % of HBM roofline; 1/2/4/8
 RMAT = dict(a=0.57, b=0.19, c=0.19)
 
 
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary, or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        with open(f) as fh:
+            d = json.load(fh)
+        if kernel in d:
+            return d[kernel]["dram_bytes_per_launch"], d[kernel]["source"]
+    return None, None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -202,14 +214,16 @@ class BfsWorkload(Workload):
         return st
 
     def roofline(self, st, peak, peak_kind):
-        pulls = [s for s in st if s.direction == "pull"] or st
-        top = max(pulls, key=lambda s: s.spmv_seconds)
-        gbs = top.bytes_algorithmic / top.spmv_seconds / 1e9
-        return {"bound": "hbm", "kernel": "k_bfs_pull" if top.direction == "pull" else "k_bfs_push",
-                "superstep": top.iteration, "achieved": round(gbs, 1), "peak": peak,
+        # The whole BFS is one cooperative launch (k_bfs_coop); its duration is
+        # the sum of the per-superstep %globaltimer spans measured inside it.
+        b = sum(s.bytes_algorithmic for s in st)
+        t = sum(s.spmv_seconds for s in st)
+        gbs = b / t / 1e9
+        traffic, src = ncu_traffic("k_bfs_coop")
+        return {"bound": "hbm", "kernel": "k_bfs_coop", "achieved": round(gbs, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
-                "bytes_per_launch": top.bytes_algorithmic,
-                "launch_us": round(top.spmv_seconds * 1e6, 2), "traffic": None}
+                "bytes_per_launch": b, "launch_us": round(t * 1e6, 2), "traffic": traffic,
+                "traffic_source": src}
 
     def cpu_baseline(self, orc):
         s, d, _ = self.g.edges()
@@ -271,9 +285,11 @@ class PageRankWorkload(Workload):
         t = statistics.median([s.spmv_seconds for s in st])
         b = st[0].bytes_algorithmic
         gbs = b / t / 1e9
-        return {"bound": "hbm", "kernel": "k_pr_rows+k_pr_long_rows", "achieved": round(gbs, 1),
-                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
-                "bytes_per_launch": b, "launch_us": round(t * 1e6, 2), "traffic": None}
+        traffic, src = ncu_traffic("k_pr_tiles")
+        return {"bound": "hbm", "kernel": "pr superstep (k_pr_tiles + k_pr_long_rows + k_pr_base)",
+                "achieved": round(gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(gbs / peak, 4), "bytes_per_launch": b, "launch_us": round(t * 1e6, 2),
+                "traffic": traffic, "traffic_kernel": "k_pr_tiles only", "traffic_source": src}
 
     def cpu_baseline(self, orc):
         s, d, _ = self.g.edges()
@@ -336,10 +352,12 @@ class SsspWorkload(Workload):
     def roofline(self, st, peak, peak_kind):
         top = max(st, key=lambda s: s.spmv_seconds)
         gbs = top.bytes_algorithmic / top.spmv_seconds / 1e9
+        traffic, src = ncu_traffic("k_sssp_push")
         return {"bound": "hbm", "kernel": "k_sssp_push", "superstep": top.iteration,
                 "achieved": round(gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": round(gbs / peak, 4), "bytes_per_launch": top.bytes_algorithmic,
-                "launch_us": round(top.spmv_seconds * 1e6, 2), "traffic": None}
+                "launch_us": round(top.spmv_seconds * 1e6, 2), "traffic": traffic,
+                "traffic_source": src}
 
     def cpu_baseline(self, orc):
         s, d, w = self.g.edges()

@@ -321,47 +321,6 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__device__ __forceinline__ uint32_t find_source_cg(const uint64_t* offs, uint32_t nq, uint64_t t) {
-  uint32_t lo = 0, hi = nq;
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldcg(&offs[mid]) <= t)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-// Warp-cooperative source lookup for edge t (t >= warp chunk start wb): lane 0
-// binary-searches the chunk start once; every lane then gallops from there
-// (its entry is a few slots away, in lines the warp already touched).
-__device__ __forceinline__ uint32_t warp_find_source(const uint64_t* offs, uint32_t nq, uint64_t wb,
-                                                     uint64_t t) {
-  uint32_t i0 = 0;
-  if (lane_id() == 0) i0 = find_source_cg(offs, nq, wb);
-  i0 = __shfl_sync(0xffffffffu, i0, 0);
-  uint32_t lo = i0, hi = nq, step = 1;
-  for (;;) {
-    const uint32_t p = lo + step;
-    if (p >= nq) break;
-    if (__ldcg(&offs[p]) > t) {
-      hi = p;
-      break;
-    }
-    lo = p;
-    step <<= 1;
-  }
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldcg(&offs[mid]) <= t)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
 // 32-way warp search: last i in [lo, hi) with offs[i] <= t, given offs[lo] <= t.
 // Each round is one batch of 32 independent loads (log32 rounds).
 __device__ __forceinline__ uint32_t warp_kary(const uint64_t* offs, uint32_t lo, uint32_t hi,

@@ -163,9 +163,12 @@ class Dist:
 class Workload:
     name = ""
     dtype = ""
+    scaling = "weak"          # N>1: independent replicas unless a workload shards
+    parallelism = "replicas"
 
-    def __init__(self, args):
+    def __init__(self, args, dist=None):
         self.args = args
+        self.dist = dist
 
     def roofline(self, stats, peak, peak_kind):
         return None
@@ -250,11 +253,22 @@ class PageRankWorkload(Workload):
 
     def build(self, gm):
         a = self.args
+        d = self.dist
         t0 = time.perf_counter()
-        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, relabel=True, **RMAT)
+        shards = d.world if d is not None and d.world > 1 else 1
+        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, relabel=True, shards=shards, **RMAT)
         self.ingest_s = time.perf_counter() - t0
         self.n = 1 << a.scale
         self.iters = 20
+        self.sharded = shards > 1
+        if self.sharded:
+            # 1-D row sharding of G^T across the ranks (strong scaling: one graph)
+            from paper_1503_07241_b200.sharded import GpuShardBackend, TorchExchange, row_block
+            lo, hi = row_block(self.n, d.world, d.rank)
+            self.backend = GpuShardBackend(self.g, lo, hi)
+            self.exchange = TorchExchange()
+            self.scaling = "strong"
+            self.parallelism = f"rows{d.world}"
         import torch
         self.dev_out = torch.empty(self.n, dtype=torch.float32, device="cuda")
         self.host_out = torch.empty(self.n, dtype=torch.float32).pin_memory()
@@ -266,10 +280,15 @@ class PageRankWorkload(Workload):
                        else "working set L2-resident (HBM fraction may exceed 1)"}
 
     def run_device(self, gm):
+        if self.sharded:
+            from paper_1503_07241_b200.sharded import sharded_pagerank
+            return sharded_pagerank(self.backend, self.exchange, self.n, 0.85, self.iters)
         gm.pagerank(self.g, 0.85, self.iters, with_stats=False,
                     out_device_ptr=self.dev_out.data_ptr())
 
     def run_e2e(self, gm):
+        if self.sharded:  # this rank's block comes back to the host
+            return self.run_device(gm)
         out = self.host_out.numpy()
         gm.pagerank(self.g, 0.85, self.iters, with_stats=False, out=out)
         return out
@@ -278,10 +297,14 @@ class PageRankWorkload(Workload):
         return 16, self.n * 4
 
     def per_superstep(self, gm):
+        if self.sharded:
+            return []
         _, st = gm.pagerank(self.g, 0.85, self.iters)
         return st
 
     def roofline(self, st, peak, peak_kind):
+        if not st:
+            return None
         t = statistics.median([s.spmv_seconds for s in st])
         b = st[0].bytes_algorithmic
         gbs = b / t / 1e9
@@ -423,9 +446,12 @@ def run_ours(args, d: Dist):
     cls, default_scale = WORKLOADS[args.workload]
     if args.scale is None:
         args.scale = default_scale
-    w = cls(args)
+    w = cls(args, d)
     w.build(gm)
-    stream = torch.cuda.ExternalStream(w.g.stream)
+    # sharded workloads interleave library kernels with collectives on torch's
+    # stream (host-sequenced per superstep): time on that stream
+    stream = (torch.cuda.current_stream() if getattr(w, "sharded", False)
+              else torch.cuda.ExternalStream(w.g.stream))
     peak, peak_kind = measured_peaks()
 
     for _ in range(args.warmup):
@@ -453,7 +479,8 @@ def run_ours(args, d: Dist):
     d.barrier()
     t_ms = ev0.elapsed_time(ev1)
     t_ms = d.max(t_ms)
-    value = w.edges * args.steps * d.world / (t_ms * 1e-3) / 1e9
+    replicas = d.world if w.scaling == "weak" else 1
+    value = w.edges * args.steps * replicas / (t_ms * 1e-3) / 1e9
 
     # end-to-end through the public API with pinned host buffers
     torch.cuda.synchronize()
@@ -462,7 +489,7 @@ def run_ours(args, d: Dist):
     for _ in range(args.steps):
         w.run_e2e(gm)
     e2e_s = d.max(time.perf_counter() - t0)
-    e2e = w.edges * args.steps * d.world / e2e_s / 1e9
+    e2e = w.edges * args.steps * replicas / e2e_s / 1e9
     h2d, d2h = w.e2e_bytes()
 
     st = w.per_superstep(gm)
@@ -474,9 +501,10 @@ def run_ours(args, d: Dist):
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": d.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": w.dtype,
+        "higher_is_better": True, "scaling": w.scaling, "vs_baseline": None, "dtype": w.dtype,
         "data": "synthetic: seeded counter-based R-MAT/Zipf generators (DESIGN.md), no datasets",
-        "config": dict(w.config, parallelism=("replicas%d" % d.world) if d.world > 1 else "single"),
+        "config": dict(w.config, parallelism=(f"{w.parallelism}{d.world}" if w.parallelism == "replicas"
+                                            else w.parallelism) if d.world > 1 else "single"),
         "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_s * 1e3 / args.steps, 4)},
         "roofline": w.roofline(st, peak, peak_kind),

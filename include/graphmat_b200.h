@@ -74,6 +74,11 @@ enum {
   GM_RELABEL = 4u,      /* internal degree-ordered vertex ids (results stay in caller ids)          */
   GM_NEED_FORWARD = 8u  /* build CSR(G) eagerly (Graph::ensure_forward, dcsc.hpp:201-215)           */
 };
+/* With GM_RELABEL, GM_SHARDS(P) deals the degree-ordered vertices round-robin
+ * over P equal contiguous row blocks (internal id = (k % P) * N/P + k / P for
+ * degree rank k), so block r = [r*N/P, (r+1)*N/P) of G^T carries ~1/P of the
+ * nonzeros: the 1-D row partition of dcsc.hpp:77-105 for P GPUs.  N % P == 0. */
+#define GM_SHARDS(p) ((uint32_t)(p) << 16)
 
 /* Mirrors semigraph::IterationStats (engine.hpp:32-39) plus device counters. */
 typedef struct {
@@ -212,6 +217,20 @@ GM_API gm_status gm_superstep_phases(gm_graph_t g, int32_t program, const double
                                      uint8_t* y_valid);
 
 /* ---- multi-GPU sharding (1-D row blocks of G^T, one process per GPU) ----- */
+/* caller id -> internal id (n entries, host); identity without GM_RELABEL. */
+GM_API gm_status gm_graph_permutation(gm_graph_t g, uint32_t* caller_to_internal);
+/* PageRank over the rows [row_begin, row_end) of G^T this rank owns (internal
+ * ids; with GM_SHARDS(P) rank r owns [r*N/P, (r+1)*N/P)).  x_block_dev receives
+ * the block of the message vector; the caller all-gathers the blocks of every
+ * rank into x_full_dev (n floats, internal order) and sums the dangling masses
+ * into base = (1-d)/N + d*D/N for the next superstep. */
+GM_API gm_status gm_pagerank_shard_init(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                        float* x_block_dev, double* dangling_block);
+GM_API gm_status gm_pagerank_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                        const float* x_full_dev, double base, double damping,
+                                        float* x_block_dev, double* dangling_block);
+GM_API gm_status gm_pagerank_shard_ranks(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                         float* ranks_block_host);
 /* Row-block boundaries balanced by stored entries, like
  * detail::balanced_row_boundaries (dcsc.hpp:81-105).  row_nnz: n counts;
  * bounds: parts+1 entries. */

@@ -24,7 +24,8 @@ EXPORTED = [
     "gm_graph_ensure_forward", "gm_graph_export_edges", "gm_degree_vector", "gm_pick_source",
     "gm_graph_stream", "gm_pagerank", "gm_bfs", "gm_sssp", "gm_cf", "gm_program_sizes",
     "gm_run_graph_program", "gm_superstep_phases", "gm_balanced_row_boundaries",
-    "gm_kernel_launches",
+    "gm_kernel_launches", "gm_graph_permutation", "gm_pagerank_shard_init",
+    "gm_pagerank_shard_step", "gm_pagerank_shard_ranks",
 ]
 
 
@@ -100,6 +101,10 @@ def load(path: str = LIB_PATH):
         "gm_superstep_phases": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, i32, vp, vp]),
         "gm_balanced_row_boundaries": (C.c_int, [vp, u64, u64, vp]),
         "gm_kernel_launches": (C.c_uint64, []),
+        "gm_graph_permutation": (C.c_int, [vp, vp]),
+        "gm_pagerank_shard_init": (C.c_int, [vp, u64, u64, vp, C.POINTER(dp)]),
+        "gm_pagerank_shard_step": (C.c_int, [vp, u64, u64, vp, dp, dp, vp, C.POINTER(dp)]),
+        "gm_pagerank_shard_ranks": (C.c_int, [vp, u64, u64, vp]),
     }
     for name, (res, args) in proto.items():
         f = getattr(L, name)

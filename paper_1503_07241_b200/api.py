@@ -148,11 +148,13 @@ class Graph:
 
     @classmethod
     def rmat(cls, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, *, permute=True,
-             symmetrize=False, relabel=True, weights=False, need_forward=False):
+             symmetrize=False, relabel=True, weights=False, need_forward=False, shards=1):
         """Seeded R-MAT generated + ingested on the GPU (io::rmat_generate
-        semantics, io.cpp:224-255; dedup + loop removal always on)."""
+        semantics, io.cpp:224-255; dedup + loop removal always on).  shards=P
+        lays internal ids out as P nnz-balanced row blocks (GM_SHARDS)."""
         flags = (L.GM_PREPROCESS | (L.GM_SYMMETRIZE if symmetrize else 0)
-                 | (L.GM_RELABEL if relabel else 0) | (L.GM_NEED_FORWARD if need_forward else 0))
+                 | (L.GM_RELABEL if relabel else 0) | (L.GM_NEED_FORWARD if need_forward else 0)
+                 | ((int(shards) & 0xFF) << 16 if shards > 1 else 0))
         h = C.c_void_p()
         _check(L.load().gm_graph_generate_rmat(scale, edge_factor, a, b, c, seed,
                                                1 if permute else 0, flags,
@@ -227,6 +229,12 @@ class Graph:
         n = self.num_vertices
         out = np.empty(n, np.uint64)
         _check(L.load().gm_degree_vector(self._h, 0 if kind in ("in", 0) else 1, out.ctypes.data))
+        return out
+
+    def permutation(self):
+        """caller id -> internal id (identity without relabeling)."""
+        out = np.empty(self.num_vertices, np.uint32)
+        _check(L.load().gm_graph_permutation(self._h, out.ctypes.data))
         return out
 
     def pick_source(self, seed) -> int:

@@ -198,6 +198,41 @@ GM_API gm_status gm_superstep_phases(gm_graph_t g, int32_t program, const double
   });
 }
 
+GM_API gm_status gm_graph_permutation(gm_graph_t g, uint32_t* caller_to_internal) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (!caller_to_internal && h->n) gm::fail(GM_EUSAGE, "null output");
+    if (h->relabeled) {
+      GM_CUDA(cudaMemcpy(caller_to_internal, h->perm.get(), h->n * 4, cudaMemcpyDeviceToHost));
+    } else {
+      for (uint64_t v = 0; v < h->n; ++v) caller_to_internal[v] = uint32_t(v);
+    }
+  });
+}
+
+GM_API gm_status gm_pagerank_shard_init(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                        float* x_block_dev, double* dangling_block) {
+  return guarded([&] {
+    const double d = gm::pagerank_shard_init(*handle(g), row_begin, row_end, x_block_dev);
+    if (dangling_block) *dangling_block = d;
+  });
+}
+
+GM_API gm_status gm_pagerank_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                        const float* x_full_dev, double base, double damping,
+                                        float* x_block_dev, double* dangling_block) {
+  return guarded([&] {
+    const double d = gm::pagerank_shard_step(*handle(g), row_begin, row_end, x_full_dev, base,
+                                             damping, x_block_dev);
+    if (dangling_block) *dangling_block = d;
+  });
+}
+
+GM_API gm_status gm_pagerank_shard_ranks(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                         float* ranks_block_host) {
+  return guarded([&] { gm::pagerank_shard_ranks(*handle(g), row_begin, row_end, ranks_block_host); });
+}
+
 // detail::balanced_row_boundaries (dcsc.hpp:81-105): boundary p is the smallest
 // row i with cum(i) * parts >= p * total.
 GM_API gm_status gm_balanced_row_boundaries(const uint64_t* row_nnz, uint64_t n, uint64_t parts,

@@ -30,6 +30,7 @@ struct CfCache;    // cf.cu
 struct Graph {
   uint64_t n = 0, m = 0;
   uint32_t flags = 0;
+  uint32_t shards = 1;  // GM_SHARDS(P): row blocks of n / shards internal ids
   int value_type = GM_VAL_NONE;
   int device = 0;
   bool symmetric = false;

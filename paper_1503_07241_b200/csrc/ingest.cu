@@ -136,11 +136,15 @@ __global__ void k_relabel_keys(const uint32_t* outdeg, uint64_t n, uint64_t* key
     keys[v] = (uint64_t(0xFFFFFFFFu - outdeg[v]) << 32) | v;
 }
 
-__global__ void k_perm_from_keys(const uint64_t* keys, uint64_t n, uint32_t* perm,
+// Degree rank k -> internal id; with P shards the ranks are dealt round-robin
+// over P contiguous blocks of n/P ids (each block hub-first, nnz-balanced).
+__global__ void k_perm_from_keys(const uint64_t* keys, uint64_t n, uint32_t shards, uint32_t* perm,
                                  uint32_t* iperm) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t v = uint32_t(keys[i]);
+  const uint64_t block = n / shards;
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = uint32_t(keys[k]);
+    const uint64_t i = (k % shards) * block + k / shards;
     iperm[i] = v;
     perm[v] = uint32_t(i);
   }
@@ -482,8 +486,9 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
     sort_keys(rk, int64_t(n), 64, s);
     g.perm.alloc(n, s);
     g.iperm.alloc(n, s);
+    const uint32_t shards = g.shards;
     launch(n, s, [&](unsigned gr, unsigned b) {
-      k_perm_from_keys<<<gr, b, 0, s>>>(rk.get(), n, g.perm.get(), g.iperm.get());
+      k_perm_from_keys<<<gr, b, 0, s>>>(rk.get(), n, shards, g.perm.get(), g.iperm.get());
     });
     g.outdeg.alloc(n, s);
     g.indeg.alloc(n, s);
@@ -529,7 +534,14 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
 
 Graph* new_graph(uint64_t n, uint32_t flags, int storage) {
   if (n > 0xFFFFFFFFull) fail(GM_EUSAGE, "graphs above 2^32-1 vertices are not supported");
+  uint32_t shards = (flags >> 16) & 0xFFu;
+  if (shards == 0) shards = 1;
+  if (shards > 1 && !(flags & GM_RELABEL)) fail(GM_EUSAGE, "GM_SHARDS needs GM_RELABEL");
+  if (shards > 1 && n % shards != 0)
+    fail(GM_EUSAGE, "GM_SHARDS(" + std::to_string(shards) + "): vertex count " + std::to_string(n) +
+                        " is not a multiple of the shard count");
   auto* g = new Graph();
+  g->shards = shards;
   GM_CUDA(cudaGetDevice(&g->device));
   GM_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
   g->n = n;

@@ -44,6 +44,7 @@ constexpr unsigned kDangBlocks = 296;
 
 struct PrCache {
   uint64_t n = 0;
+  uint64_t row_lo = 0, row_hi = 0;  // rows of G^T this process computes
   DevBuf<float> inv, rank, x0, x1;
   DevBuf<uint32_t> tile_b, tile_e, long_rows;
   uint64_t ntiles = 0, n_long = 0;
@@ -305,13 +306,12 @@ __global__ void __launch_bounds__(256) k_pr_long_rows(const uint32_t* rows, cons
 
 // Row-aligned tiles of <= kTile path items; rows needing more than a tile go
 // to the long-row list.  One-time host pass over the offsets (cached).
-void build_tiles(Graph& g, PrCache& c, cudaStream_t s) {
-  const uint64_t n = g.n;
-  std::vector<uint64_t> ptr(n + 1);
-  GM_CUDA(cudaMemcpyAsync(ptr.data(), g.in.ptr.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+void build_tiles(Graph& g, PrCache& c, cudaStream_t s, uint64_t lo, uint64_t n) {
+  std::vector<uint64_t> ptr(g.n + 1);
+  GM_CUDA(cudaMemcpyAsync(ptr.data(), g.in.ptr.get(), (g.n + 1) * 8, cudaMemcpyDeviceToHost, s));
   GM_CUDA(cudaStreamSynchronize(s));
   std::vector<uint32_t> tb, te, lr;
-  uint64_t r = 0;
+  uint64_t r = lo;
   while (r < n) {
     const uint64_t deg = ptr[r + 1] - ptr[r];
     if (deg + 1 > uint64_t(kTile)) {
@@ -344,13 +344,17 @@ void build_tiles(Graph& g, PrCache& c, cudaStream_t s) {
   GM_CUDA(cudaStreamSynchronize(s));
 }
 
-PrCache& cache(Graph& g) {
-  if (!g.pr) {
+// Per-graph state for the rows [lo, hi) this process computes (all rows on
+// one GPU; one row block of G^T per rank when sharded).
+PrCache& cache(Graph& g, uint64_t lo, uint64_t hi) {
+  if (!g.pr || g.pr->row_lo != lo || g.pr->row_hi != hi) {
     g.pr = std::unique_ptr<PrCache, void (*)(PrCache*)>(new PrCache(), [](PrCache* p) { delete p; });
     PrCache& c = *g.pr;
     cudaStream_t s = g.stream;
     const uint64_t n = g.n;
     c.n = n;
+    c.row_lo = lo;
+    c.row_hi = hi;
     c.inv.alloc(n, s);
     c.rank.alloc(n, s);
     c.x0.alloc(n, s);
@@ -360,11 +364,17 @@ PrCache& cache(Graph& g) {
     c.ctr.zero(s);
     GM_CUDA(cudaEventCreate(&c.e0));
     GM_CUDA(cudaEventCreate(&c.e1));
-    build_tiles(g, c, s);
+    build_tiles(g, c, s, lo, hi);
     c.dang_partial.alloc(std::max<uint64_t>(kDangBlocks, c.ntiles + c.n_long) + 1, s);
+    k_pr_init<<<grid_for(n, 256), 256, 0, s>>>(n, g.outdeg.get(), c.inv.get(), c.rank.get(),
+                                               c.x0.get());
+    GM_LAUNCH_CHECK();
+    GM_CUDA(cudaStreamSynchronize(s));
   }
   return *g.pr;
 }
+
+PrCache& cache(Graph& g) { return cache(g, 0, g.n); }
 
 }  // namespace
 
@@ -377,7 +387,7 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   if (n == 0) return stats;
   PrCache& c = cache(g);
   cudaStream_t s = g.stream;
-  const uint64_t dang_lo = g.relabeled ? g.nonzero_outdeg : 0;
+  const uint64_t dang_lo = (g.relabeled && g.shards == 1) ? g.nonzero_outdeg : 0;
   k_pr_init<<<grid_for(n, 256), 256, 0, s>>>(n, g.outdeg.get(), c.inv.get(), c.rank.get(), c.x0.get());
   GM_LAUNCH_CHECK();
   unsigned* ticket = reinterpret_cast<unsigned*>(c.ctr.get() + 3);
@@ -449,6 +459,103 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   }
   GM_CUDA(cudaStreamSynchronize(s));
   return stats;
+}
+
+// ---- 1-D row sharding: this process owns rows [lo, hi) of G^T --------------
+// (the reference's row partitions, dcsc.hpp:77-105, one per GPU).  The caller
+// all-gathers the message blocks of every rank into x_full between supersteps
+// and all-reduces the dangling masses into the next base.
+
+namespace {
+
+__global__ void k_count_dangling(const float* inv, uint64_t lo, uint64_t hi,
+                                 unsigned long long* cnt) {
+  unsigned long long c = 0;
+  for (uint64_t v = lo + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < hi;
+       v += uint64_t(gridDim.x) * blockDim.x)
+    c += inv[v] == 0.0f;
+  warp_add_u64(cnt, c);
+}
+
+// Fixed-order sum of the per-tile dangling partials (one CTA) into a double.
+__global__ void __launch_bounds__(1024) k_sum_partials(const float* partial, uint32_t np,
+                                                       double* out) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (uint32_t i = threadIdx.x; i < np; i += 1024) s += partial[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+void check_block(Graph& g, uint64_t lo, uint64_t hi) {
+  if (lo > hi || hi > g.n) fail(GM_EUSAGE, "pagerank shard: bad row block");
+}
+
+}  // namespace
+
+double pagerank_shard_init(Graph& g, uint64_t lo, uint64_t hi, float* x_block) {
+  check_block(g, lo, hi);
+  PrCache& c = cache(g, lo, hi);
+  cudaStream_t s = g.stream;
+  k_pr_init<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, g.outdeg.get(), c.inv.get(), c.rank.get(),
+                                               c.x0.get());
+  GM_LAUNCH_CHECK();
+  if (hi > lo)
+    GM_CUDA(cudaMemcpyAsync(x_block, c.x0.get() + lo, (hi - lo) * 4, cudaMemcpyDeviceToDevice, s));
+  GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
+  if (hi > lo) {
+    k_count_dangling<<<grid_for(hi - lo, 256), 256, 0, s>>>(c.inv.get(), lo, hi, c.ctr.get());
+    GM_LAUNCH_CHECK();
+  }
+  unsigned long long cnt = 0;
+  GM_CUDA(cudaMemcpyAsync(&cnt, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  return double(cnt) / double(g.n);
+}
+
+double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_full, double base,
+                           double damping, float* x_block) {
+  check_block(g, lo, hi);
+  PrCache& c = cache(g, lo, hi);
+  cudaStream_t s = g.stream;
+  const float b = float(base);
+  const float d = float(damping);
+  GM_CUDA(cudaMemcpyAsync(c.scalars.get(), &b, 4, cudaMemcpyHostToDevice, s));
+  float* part = c.dang_partial.get();
+  float* xn = x_block - lo;  // the kernels write x_next[row] for rows in [lo, hi)
+  if (c.ntiles) {
+    k_pr_tiles<false><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
+        c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), x_full, c.inv.get(),
+        c.rank.get(), xn, c.scalars.get(), d, c.ctr.get(), part);
+    GM_LAUNCH_CHECK();
+  }
+  if (c.n_long) {
+    k_pr_long_rows<false><<<unsigned(c.n_long), 256, 0, s>>>(
+        c.long_rows.get(), g.in.ptr.get(), g.in.idx.get(), x_full, c.inv.get(), c.rank.get(), xn,
+        c.scalars.get(), d, c.ctr.get(), part + c.ntiles);
+    GM_LAUNCH_CHECK();
+  }
+  double* dsum = reinterpret_cast<double*>(c.ctr.get() + 2);
+  k_sum_partials<<<1, 1024, 0, s>>>(part, uint32_t(c.ntiles + c.n_long), dsum);
+  GM_LAUNCH_CHECK();
+  double h = 0.0;
+  GM_CUDA(cudaMemcpyAsync(&h, dsum, 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+void pagerank_shard_ranks(Graph& g, uint64_t lo, uint64_t hi, float* out_host) {
+  check_block(g, lo, hi);
+  PrCache& c = cache(g, lo, hi);
+  if (hi > lo)
+    GM_CUDA(cudaMemcpyAsync(out_host, c.rank.get() + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost,
+                            g.stream));
+  GM_CUDA(cudaStreamSynchronize(g.stream));
 }
 
 }  // namespace gm

@@ -956,7 +956,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   const uint64_t words = (n + 31) / 32;
   // Pull rows: on a relabeled symmetric graph only the nonzero-degree prefix
   // can ever be reached.
-  const uint64_t nv = (g.relabeled && g.symmetric) ? g.nonzero_outdeg : n;
+  const uint64_t nv = (g.relabeled && g.symmetric && g.shards == 1) ? g.nonzero_outdeg : n;
   const uint32_t s_words = uint32_t(std::min<uint64_t>(kSmemFbWords, (nv + 31) / 32));
   const size_t smem = size_t(kSmemFbWords) * 4;
   if (!c.level) {

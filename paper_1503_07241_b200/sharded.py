@@ -1,0 +1,106 @@
+"""Multi-GPU PageRank: 1-D row sharding of G^T, one process per GPU.
+
+The reference partitions G^T into row blocks that own disjoint destination
+rows (include/semigraph/dcsc.hpp:77-105) and every partition reads the whole
+message vector (engine.hpp:59-66, 220-223).  Across GPUs that becomes: rank r
+owns the internal rows [r*N/P, (r+1)*N/P) (GM_SHARDS(P) relabeling makes those
+blocks nnz-balanced), computes its rows' ranks and next messages with the
+fused superstep kernels, and per superstep the ranks all-gather the message
+blocks into the full vector and all-reduce the dangling mass for the next base.
+There is no reduce-scatter: row ownership is disjoint.
+
+The driver is backend-agnostic so its orchestration (blocks, exchange order,
+base arithmetic) is tested on CPU with gloo; the GPU backend calls the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from .api import _check
+
+
+def row_block(n: int, world: int, rank: int):
+    """Rows [lo, hi) of G^T owned by `rank` (equal blocks; n % world == 0)."""
+    if n % world:
+        raise ValueError(f"vertex count {n} is not a multiple of {world} ranks")
+    b = n // world
+    return rank * b, (rank + 1) * b
+
+
+class TorchExchange:
+    """all_gather / all_reduce over a torch.distributed process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def allgather_into(self, full, block):
+        try:
+            self.dist.all_gather_into_tensor(full, block, group=self.group)
+        except (RuntimeError, NotImplementedError, AttributeError):
+            # backends without the fused collective (gloo): list form, in place
+            world = self.dist.get_world_size(self.group)
+            b = block.numel()
+            self.dist.all_gather([full[r * b:(r + 1) * b] for r in range(world)], block,
+                                 group=self.group)
+
+    def allreduce_sum(self, value: float, like):
+        import torch
+        t = torch.tensor([value], dtype=torch.float64, device=like.device)
+        self.dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+
+class GpuShardBackend:
+    """The CUDA kernels on this rank's row block (C ABI gm_pagerank_shard_*)."""
+
+    def __init__(self, g, lo, hi):
+        import torch
+        self.g, self.lo, self.hi = g, lo, hi
+        self.block = torch.empty(max(hi - lo, 1), dtype=torch.float32, device="cuda")[: hi - lo]
+        self.full = torch.empty(g.num_vertices, dtype=torch.float32, device="cuda")
+        self._stream = None
+
+    def init(self):
+        d = C.c_double()
+        _check(L.load().gm_pagerank_shard_init(self.g._h, self.lo, self.hi, self.block.data_ptr(),
+                                               C.byref(d)))
+        return d.value
+
+    def step(self, base, damping):
+        import torch
+        # the exchange wrote `full` on torch's stream; the kernels run on the graph's
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        d = C.c_double()
+        _check(L.load().gm_pagerank_shard_step(self.g._h, self.lo, self.hi, self.full.data_ptr(),
+                                               base, damping, self.block.data_ptr(), C.byref(d)))
+        return d.value
+
+    def ranks(self):
+        out = np.empty(self.hi - self.lo, np.float32)
+        _check(L.load().gm_pagerank_shard_ranks(self.g._h, self.lo, self.hi, out.ctypes.data))
+        return out
+
+
+def sharded_pagerank(backend, exchange, n: int, damping=0.85, iterations=20, sync=None):
+    """Run the BASELINE PageRank on this rank's rows; returns this block's ranks
+    (internal order).  base_t = (1-d)/N + d*D_t/N with D_t the global dangling
+    mass after superstep t (pagerank.hpp program shape, CF-driver loop)."""
+    dangling = exchange.allreduce_sum(backend.init(), backend.block)
+    exchange.allgather_into(backend.full, backend.block)
+    for _ in range(iterations):
+        base = (1.0 - damping) / n + damping * dangling / n
+        local = backend.step(base, damping)
+        if sync is not None:
+            sync()
+        dangling = exchange.allreduce_sum(local, backend.block)
+        exchange.allgather_into(backend.full, backend.block)
+    return backend.ranks()

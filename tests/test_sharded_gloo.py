@@ -1,0 +1,85 @@
+"""CPU, world_size 2 over gloo: the multi-GPU PageRank orchestration
+(paper_1503_07241_b200.sharded) -- row blocks, all-gather order, dangling
+all-reduce, base arithmetic -- with a numpy stand-in for the per-rank kernels,
+against the single-process oracle (oracle/graphmat_oracle.c)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class NumpyShardBackend:
+    """Test stand-in for GpuShardBackend: the same block contract in fp64."""
+
+    def __init__(self, n, src, dst, lo, hi):
+        self.n, self.lo, self.hi = n, lo, hi
+        outdeg = np.bincount(src, minlength=n)
+        self.inv = np.where(outdeg > 0, 1.0 / np.maximum(outdeg, 1), 0.0)
+        self.dangling = outdeg == 0
+        order = np.lexsort((src, dst))
+        s, d = src[order], dst[order]
+        keep = (d >= lo) & (d < hi)
+        self.rows, self.cols = d[keep] - lo, s[keep]
+        self.block = torch.zeros(hi - lo, dtype=torch.float64)
+        self.full = torch.zeros(n, dtype=torch.float64)
+        self.rank = np.zeros(hi - lo)
+
+    def init(self):
+        self.rank[:] = 1.0 / self.n
+        self.block.copy_(torch.from_numpy(self.rank * self.inv[self.lo:self.hi]))
+        return float(self.rank[self.dangling[self.lo:self.hi]].sum())
+
+    def step(self, base, damping):
+        x = self.full.numpy()
+        sums = np.zeros(self.hi - self.lo)
+        np.add.at(sums, self.rows, x[self.cols])
+        self.rank = base + damping * sums
+        self.block.copy_(torch.from_numpy(self.rank * self.inv[self.lo:self.hi]))
+        return float(self.rank[self.dangling[self.lo:self.hi]].sum())
+
+    def ranks(self):
+        return self.rank.copy()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, src, dst, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1503_07241_b200.sharded import TorchExchange, row_block, sharded_pagerank
+    lo, hi = row_block(n, world, rank)
+    backend = NumpyShardBackend(n, src, dst, lo, hi)
+    block = sharded_pagerank(backend, TorchExchange(), n, 0.85, 20)
+    full = torch.zeros(n, dtype=torch.float64)
+    TorchExchange().allgather_into(full, torch.from_numpy(block))
+    if rank == 0:
+        out[:] = full
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_pagerank_matches_oracle(orc, world):
+    n = 512
+    src, dst = orc.rmat(9, 8, seed=3)
+    src, dst, _ = orc.preprocess(src, dst)
+    want, _ = orc.pagerank_norm(n, src, dst, 0.85, 20)
+    out = torch.zeros(n, dtype=torch.float64).share_memory_()
+    mp.spawn(_worker, args=(world, _free_port(), n, src.astype(np.int64), dst.astype(np.int64), out),
+             nprocs=world, join=True)
+    np.testing.assert_allclose(out.numpy(), want, rtol=1e-12, atol=0)
+
+
+def test_row_blocks():
+    from paper_1503_07241_b200.sharded import row_block
+    assert [row_block(16, 4, r) for r in range(4)] == [(0, 4), (4, 8), (8, 12), (12, 16)]
+    with pytest.raises(ValueError):
+        row_block(10, 4, 0)

@@ -9,28 +9,35 @@
 //
 // Device layout per superstep (internal ids, relabeled by out-degree so
 // dangling vertices form the tail [nonzero_outdeg, n)):
-//   x_cur[N]  f32  message vector (rank * inv_outdeg; 0 for dangling)   gathered
-//   in.ptr    u64  CSR(G^T) offsets                                      streamed
-//   in.idx    u32  CSR(G^T) sources                                      streamed
-//   inv[N]    f32  1/outdeg                                              streamed
-//   rank[N]   f32  written in place (only the row owner touches it)
-//   x_next[N] f32  written: the next superstep's message vector (the send phase
-//                  is fused into this superstep's apply epilogue)
+//   x_cur[N]   f32  message vector (rank * inv_outdeg; 0 for dangling)   gathered
+//   in.ptr     u64  CSR(G^T) offsets                                      streamed
+//   in.idx     u32  CSR(G^T) sources                                      streamed
+//   inv[N]     f32  1/outdeg                                              streamed
+//   rank_n[N]  f32  written (double-buffered: the previous superstep's ranks stay
+//                   readable for the stats pass, the SpMV never reads ranks)
+//   x_next[N]  f32  written: the next superstep's message vector (the send phase
+//                   is fused into this superstep's apply epilogue)
 // Algorithmic bytes/superstep = 4·nnz + 8·(N+1) + 16·N.
 //
 // SpMV = merge-path over row-aligned tiles (Merrill & Garland's CSR merge
 // SpMV, specialised): the row sequence is cut once (cached per graph) into
 // tiles of at most kTile path items (rows + nonzeros).  A 256-thread CTA
-// stages the tile's row ends and the gathered x[col] values in shared memory
-// (every gather of the tile in flight at once), each thread takes exactly
-// kIPT path items found by a merge-path search in shared memory, and a block
-// segmented scan hands partial row sums across threads.  Load balance is
-// perfect whatever the degree mix (54% empty rows, hubs of 10^5 entries), and
-// every reduction is a fixed tree, so results are bitwise reproducible.
-// Rows longer than a tile get a CTA each (k_pr_long_rows).
-// The dangling mass for the NEXT superstep is reduced deterministically by
-// k_dangling (fixed grid, per-block partials, last-block final), which also
-// computes base on device, so the supersteps run without a host round trip.
+// stages the tile's row ends (16-bit, tile-local) and the gathered x[col]
+// values in shared memory (every gather of the tile in flight at once), each
+// thread takes exactly kIPT path items found by a merge-path search in shared
+// memory, and a block segmented scan hands partial row sums across threads.
+// Rows longer than a tile are cut into tile-sized chunks, one CTA each, in the
+// same launch; the last chunk of a row to finish folds the chunk sums in order.
+// Every reduction is a fixed tree, so results are bitwise reproducible.
+//
+// Shared memory is kept small on purpose (12.3 KB per CTA): the L1 that the
+// carveout leaves is what caches the hub entries of x (relabeling puts them at
+// the low ids), and the kernel time tracks that hit rate.
+//
+// The dangling mass for the NEXT superstep's base is reduced from per-CTA
+// partials in a fixed order by k_pr_base, on device: the supersteps run without
+// a host round trip.  The updated-vertex count of a stats superstep is a
+// separate streaming pass over the two rank buffers (k_pr_count).
 #include <vector>
 
 #include "api_internal.cuh"
@@ -40,18 +47,25 @@ namespace gm {
 constexpr int kPrThreads = 256;
 constexpr int kIPT = 8;
 constexpr int kTile = kPrThreads * kIPT;  // path items per tile
+static_assert(kTile < 0xFFFF, "tile-local row ends are 16-bit");
 constexpr unsigned kDangBlocks = 296;
 
 struct PrCache {
   uint64_t n = 0;
   uint64_t row_lo = 0, row_hi = 0;  // rows of G^T this process computes
-  DevBuf<float> inv, rank, x0, x1;
-  DevBuf<uint32_t> tile_b, tile_e, long_rows;
-  uint64_t ntiles = 0, n_long = 0;
+  DevBuf<float> inv, rank0, rank1, x0, x1;
+  int cur = 0;  // rank buffer holding the latest ranks
+  DevBuf<uint32_t> tile_b, tile_e;
+  DevBuf<uint32_t> chunk_row, chunk_slot, slot_first;  // long rows, kTile nnz per chunk
+  DevBuf<float> chunk_sum;
+  DevBuf<unsigned> slot_ticket;
+  uint64_t ntiles = 0, n_long = 0, nchunks = 0;
   DevBuf<float> scalars;       // [0] = base for the current superstep
-  DevBuf<float> dang_partial;  // kDangBlocks
+  DevBuf<float> dang_partial;  // per SpMV CTA (and kDangBlocks for the first base)
   DevBuf<unsigned long long> ctr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  float* rank() { return cur ? rank1.get() : rank0.get(); }
+  float* rank_other() { return cur ? rank0.get() : rank1.get(); }
   ~PrCache() {
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
@@ -129,6 +143,18 @@ __global__ void __launch_bounds__(1024) k_pr_base(const float* partial, uint32_t
   }
 }
 
+// vertices_updated of a stats superstep (rule S7): rows with at least one
+// in-edge (a valid y) whose rank changed bitwise.  Streams ptr and both rank
+// buffers once; one atomic per warp.
+__global__ void k_pr_count(uint64_t lo, uint64_t hi, const uint64_t* ptr, const float* old_rank,
+                           const float* new_rank, unsigned long long* ctr) {
+  unsigned long long c = 0;
+  for (uint64_t v = lo + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < hi;
+       v += uint64_t(gridDim.x) * blockDim.x)
+    c += ptr[v + 1] != ptr[v] && __float_as_uint(old_rank[v]) != __float_as_uint(new_rank[v]);
+  warp_add_u64(ctr, c);
+}
+
 // Block-wide fixed-tree sum (all threads call; result valid in thread 0).
 template <int kThreadsT>
 __device__ __forceinline__ float block_sum(float v, float* scratch) {
@@ -145,46 +171,104 @@ __device__ __forceinline__ float block_sum(float v, float* scratch) {
   return t;
 }
 
-template <bool kCount>
+// Apply + send for one row: stores only, plus the inv read.
 __device__ __forceinline__ void pr_write(uint64_t row, float sum, float base, float damping,
-                                         const float* __restrict__ inv, float* rank,
-                                         float* __restrict__ x_next, bool nonempty,
-                                         unsigned long long& changed, float& dangling) {
+                                         const float* __restrict__ inv, float* __restrict__ rank,
+                                         float* __restrict__ x_next, float& dangling) {
   const float r = base + damping * sum;
-  if (kCount) changed += nonempty && (__float_as_uint(r) != __float_as_uint(rank[row]));
   rank[row] = r;
-  const float iv = inv[row];
+  const float iv = __ldg(&inv[row]);
   x_next[row] = r * iv;
   if (iv == 0.0f) dangling += r;
 }
 
-template <bool kCount>
-__global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
-    const uint32_t* __restrict__ tile_b, const uint32_t* __restrict__ tile_e,
-    const uint64_t* __restrict__ ptr, const uint32_t* __restrict__ idx,
-    const float* __restrict__ x_cur, const float* __restrict__ inv, float* rank,
-    float* __restrict__ x_next, const float* __restrict__ scalars, float damping,
-    unsigned long long* ctr, float* __restrict__ dang_partial) {
-  __shared__ uint32_t s_end[kTile + 1];
-  __shared__ float s_red[kPrThreads / 32];
+// One superstep's SpMV launch: blocks [0, nchunks) take one kTile-nnz chunk of
+// a long row each (the heaviest work first), blocks [nchunks, nchunks+ntiles)
+// one merge-path tile each.  Dangling partials: tiles at [0, ntiles), long row
+// `slot` at ntiles + slot.
+struct PrArgs {
+  const uint32_t* tile_b;
+  const uint32_t* tile_e;
+  const uint64_t* ptr;
+  const uint32_t* idx;
+  const float* x_cur;
+  const float* inv;
+  float* rank;  // this superstep's output buffer
+  float* x_next;
+  const float* scalars;
+  float damping;
+  uint32_t ntiles, nchunks;
+  const uint32_t* chunk_row;   // [nchunks] row of G^T
+  const uint32_t* chunk_slot;  // [nchunks] long-row slot
+  const uint32_t* slot_first;  // [n_long + 1] first chunk of each long row
+  float* chunk_sum;            // [nchunks]
+  unsigned* slot_ticket;       // [n_long] arrivals this superstep (reset by the last)
+  float* dang_partial;
+};
+
+// A long row is cut into chunks of kTile nonzeros, one CTA each (all gathers
+// in flight, fixed-tree block sum).  The CTA that completes a row last (ticket)
+// folds the row's chunk sums in chunk order, so the result does not depend on
+// which CTA finishes last, and runs the apply + send epilogue.
+__device__ __forceinline__ void pr_chunk(const PrArgs& a, float* s_red) {
+  const unsigned tid = threadIdx.x;
+  const uint32_t ci = blockIdx.x;
+  const uint32_t row = a.chunk_row[ci], slot = a.chunk_slot[ci];
+  const uint32_t f = a.slot_first[slot], nch = a.slot_first[slot + 1] - f;
+  const uint64_t re = a.ptr[row + 1];
+  const uint64_t beg = a.ptr[row] + uint64_t(ci - f) * kTile;
+  const uint32_t len = uint32_t(min(uint64_t(kTile), re - beg));
+  float v[kIPT];
+#pragma unroll
+  for (int u = 0; u < kIPT; ++u) {
+    const uint32_t k = tid + u * kPrThreads;
+    v[u] = k < len ? __ldg(&a.x_cur[__ldg(&a.idx[beg + k])]) : 0.0f;
+  }
+  float acc = 0.0f;
+#pragma unroll
+  for (int u = 0; u < kIPT; ++u) acc += v[u];
+  acc = block_sum<kPrThreads>(acc, s_red);
+  if (tid != 0) return;
+  a.chunk_sum[ci] = acc;
+  __threadfence();
+  if (atomicAdd(&a.slot_ticket[slot], 1u) != nch - 1) return;
+  __threadfence();
+  float sum = 0.0f;
+  for (uint32_t i = 0; i < nch; ++i) sum += __ldcg(&a.chunk_sum[f + i]);
+  a.slot_ticket[slot] = 0;
   float dangling = 0.0f;
-  __shared__ float s_val[kTile];
+  pr_write(row, sum, a.scalars[0], a.damping, a.inv, a.rank, a.x_next, dangling);
+  a.dang_partial[a.ntiles + slot] = dangling;
+}
+
+__global__ void __launch_bounds__(kPrThreads) k_pr_spmv(const PrArgs a) {
+  __shared__ uint16_t s_end[kTile + 1];  // tile-local row ends (exclusive nnz offsets)
+  __shared__ float s_val[kTile];         // gathered x[col] of the tile's nonzeros
+  __shared__ float s_red[kPrThreads / 32];
   __shared__ uint32_t s_wk[kPrThreads / 32];
   __shared__ float s_wv[kPrThreads / 32];
+  if (blockIdx.x < a.nchunks) {
+    pr_chunk(a, s_red);
+    return;
+  }
+  const uint64_t* __restrict__ ptr = a.ptr;
+  const float damping = a.damping;
+  const uint32_t tile = blockIdx.x - a.nchunks;
+  float dangling = 0.0f;
   const unsigned tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
-  const uint32_t r0 = tile_b[blockIdx.x], r1 = tile_e[blockIdx.x];
+  const uint32_t r0 = a.tile_b[tile], r1 = a.tile_e[tile];
   const uint64_t j0 = ptr[r0];
   const uint32_t nrows = r1 - r0;
   const uint32_t nnz = uint32_t(ptr[r1] - j0);
   const uint32_t items = nrows + nnz;
-  const float base = scalars[0];
+  const float base = a.scalars[0];
   // Stage row ends and gathered messages; all gathers of the tile in flight.
-  for (uint32_t k = tid; k < nrows; k += kPrThreads) s_end[k] = uint32_t(ptr[r0 + k + 1] - j0);
-  if (tid == 0) s_end[nrows] = 0xFFFFFFFFu;
+  for (uint32_t k = tid; k < nrows; k += kPrThreads) s_end[k] = uint16_t(ptr[r0 + k + 1] - j0);
+  if (tid == 0) s_end[nrows] = 0xFFFFu;
 #pragma unroll
   for (int u = 0; u < kIPT; ++u) {
     const uint32_t k = tid + u * kPrThreads;
-    if (k < nnz) s_val[k] = __ldg(&x_cur[__ldg(&idx[j0 + k])]);
+    if (k < nnz) s_val[k] = __ldg(&a.x_cur[__ldg(&a.idx[j0 + k])]);
   }
   __syncthreads();
   // Merge-path search for this thread's diagonal.
@@ -201,7 +285,6 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
   const uint32_t start_row = ti;
   float run = 0.0f, first_val = 0.0f;
   bool has_first = false;
-  unsigned long long changed = 0;
   for (uint32_t k = d0; k < d1; ++k) {
     if (tj < s_end[ti]) {
       run += s_val[tj];
@@ -211,9 +294,7 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
         has_first = true;
         first_val = run;
       } else {
-        const uint32_t row_len = s_end[ti] - (ti ? s_end[ti - 1] : 0);
-        pr_write<kCount>(r0 + ti, run, base, damping, inv, rank, x_next, row_len != 0, changed,
-                         dangling);
+        pr_write(r0 + ti, run, base, damping, a.inv, a.rank, a.x_next, dangling);
       }
       run = 0.0f;
       ++ti;
@@ -258,64 +339,30 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_tiles(
   }
   if (has_first) {
     const float carry = (tid > 0 && pk == start_row) ? pv : 0.0f;
-    const uint32_t row_len = s_end[start_row] - (start_row ? s_end[start_row - 1] : 0);
-    pr_write<kCount>(r0 + start_row, carry + first_val, base, damping, inv, rank, x_next,
-                     row_len != 0, changed, dangling);
+    pr_write(r0 + start_row, carry + first_val, base, damping, a.inv, a.rank, a.x_next, dangling);
   }
-  if (kCount) warp_add_u64(ctr, changed);
   // Dangling mass of this tile's rows, for the next superstep's base.
   const float dsum = block_sum<kPrThreads>(dangling, s_red);
-  if (tid == 0) dang_partial[blockIdx.x] = dsum;
+  if (tid == 0) a.dang_partial[tile] = dsum;
 }
 
-template <bool kCount>
-__global__ void __launch_bounds__(256) k_pr_long_rows(const uint32_t* rows, const uint64_t* ptr,
-                                                      const uint32_t* __restrict__ idx,
-                                                      const float* __restrict__ x_cur,
-                                                      const float* inv, float* rank, float* x_next,
-                                                      const float* scalars, float damping,
-                                                      unsigned long long* ctr,
-                                                      float* dang_partial) {
-  __shared__ float red[256];
-  const uint32_t row = rows[blockIdx.x];
-  const uint64_t beg = ptr[row], end = ptr[row + 1];
-  float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-  uint64_t e = beg + threadIdx.x;
-  for (; e + 3 * 256 < end; e += 4 * 256) {
-    a0 += __ldg(&x_cur[__ldg(&idx[e])]);
-    a1 += __ldg(&x_cur[__ldg(&idx[e + 256])]);
-    a2 += __ldg(&x_cur[__ldg(&idx[e + 512])]);
-    a3 += __ldg(&x_cur[__ldg(&idx[e + 768])]);
-  }
-  for (; e < end; e += 256) a0 += __ldg(&x_cur[__ldg(&idx[e])]);
-  red[threadIdx.x] = (a0 + a1) + (a2 + a3);
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const float r = scalars[0] + damping * red[0];
-    if (kCount && __float_as_uint(r) != __float_as_uint(rank[row])) atomicAdd(ctr, 1ull);
-    rank[row] = r;
-    const float iv = inv[row];
-    x_next[row] = r * iv;
-    dang_partial[blockIdx.x] = iv == 0.0f ? r : 0.0f;
-  }
-}
-
-// Row-aligned tiles of <= kTile path items; rows needing more than a tile go
-// to the long-row list.  One-time host pass over the offsets (cached).
+// Row-aligned tiles of <= kTile path items; rows needing more than a tile are
+// long rows, cut into chunks of kTile nonzeros.  One-time host pass over the
+// offsets (cached with the graph).
 void build_tiles(Graph& g, PrCache& c, cudaStream_t s, uint64_t lo, uint64_t n) {
   std::vector<uint64_t> ptr(g.n + 1);
   GM_CUDA(cudaMemcpyAsync(ptr.data(), g.in.ptr.get(), (g.n + 1) * 8, cudaMemcpyDeviceToHost, s));
   GM_CUDA(cudaStreamSynchronize(s));
-  std::vector<uint32_t> tb, te, lr;
+  std::vector<uint32_t> tb, te, crow, cslot, sfirst;
   uint64_t r = lo;
   while (r < n) {
     const uint64_t deg = ptr[r + 1] - ptr[r];
     if (deg + 1 > uint64_t(kTile)) {
-      lr.push_back(uint32_t(r));
+      sfirst.push_back(uint32_t(crow.size()));
+      for (uint64_t k = 0; k < deg; k += kTile) {
+        crow.push_back(uint32_t(r));
+        cslot.push_back(uint32_t(sfirst.size() - 1));
+      }
       ++r;
       continue;
     }
@@ -331,17 +378,54 @@ void build_tiles(Graph& g, PrCache& c, cudaStream_t s, uint64_t lo, uint64_t n) 
     te.push_back(uint32_t(r));
   }
   c.ntiles = tb.size();
-  c.n_long = lr.size();
-  c.tile_b.alloc(c.ntiles + 1, s);
-  c.tile_e.alloc(c.ntiles + 1, s);
-  c.long_rows.alloc(c.n_long + 1, s);
-  if (c.ntiles) {
-    GM_CUDA(cudaMemcpyAsync(c.tile_b.get(), tb.data(), c.ntiles * 4, cudaMemcpyHostToDevice, s));
-    GM_CUDA(cudaMemcpyAsync(c.tile_e.get(), te.data(), c.ntiles * 4, cudaMemcpyHostToDevice, s));
-  }
-  if (c.n_long)
-    GM_CUDA(cudaMemcpyAsync(c.long_rows.get(), lr.data(), c.n_long * 4, cudaMemcpyHostToDevice, s));
+  c.n_long = sfirst.size();
+  c.nchunks = crow.size();
+  sfirst.push_back(uint32_t(crow.size()));
+  if (c.ntiles + c.nchunks > 0x7FFFFFFFull) fail(GM_EENGINE, "pagerank: graph too large for one grid");
+  auto up = [&](DevBuf<uint32_t>& d, const std::vector<uint32_t>& h) {
+    d.alloc(h.size() + 1, s);
+    if (!h.empty())
+      GM_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * 4, cudaMemcpyHostToDevice, s));
+  };
+  up(c.tile_b, tb);
+  up(c.tile_e, te);
+  up(c.chunk_row, crow);
+  up(c.chunk_slot, cslot);
+  up(c.slot_first, sfirst);
+  c.chunk_sum.alloc(c.nchunks + 1, s);
+  c.slot_ticket.alloc(c.n_long + 1, s);
+  c.slot_ticket.zero(s);
   GM_CUDA(cudaStreamSynchronize(s));
+}
+
+// Run one superstep's SpMV: reads x_cur, writes the other rank buffer and x_next.
+void launch_spmv(Graph& g, PrCache& c, const float* x_cur, float* x_next, float damping,
+                 cudaStream_t s) {
+  PrArgs a;
+  a.tile_b = c.tile_b.get();
+  a.tile_e = c.tile_e.get();
+  a.ptr = g.in.ptr.get();
+  a.idx = g.in.idx.get();
+  a.x_cur = x_cur;
+  a.inv = c.inv.get();
+  a.rank = c.rank_other();
+  a.x_next = x_next;
+  a.scalars = c.scalars.get();
+  a.damping = damping;
+  a.ntiles = uint32_t(c.ntiles);
+  a.nchunks = uint32_t(c.nchunks);
+  a.chunk_row = c.chunk_row.get();
+  a.chunk_slot = c.chunk_slot.get();
+  a.slot_first = c.slot_first.get();
+  a.chunk_sum = c.chunk_sum.get();
+  a.slot_ticket = c.slot_ticket.get();
+  a.dang_partial = c.dang_partial.get();
+  const unsigned grid = a.ntiles + a.nchunks;
+  if (grid) {
+    k_pr_spmv<<<grid, kPrThreads, 0, s>>>(a);
+    GM_LAUNCH_CHECK();
+  }
+  c.cur ^= 1;
 }
 
 // Per-graph state for the rows [lo, hi) this process computes (all rows on
@@ -356,7 +440,8 @@ PrCache& cache(Graph& g, uint64_t lo, uint64_t hi) {
     c.row_lo = lo;
     c.row_hi = hi;
     c.inv.alloc(n, s);
-    c.rank.alloc(n, s);
+    c.rank0.alloc(n, s);
+    c.rank1.alloc(n, s);
     c.x0.alloc(n, s);
     c.x1.alloc(n, s);
     c.scalars.alloc(4, s);
@@ -366,15 +451,20 @@ PrCache& cache(Graph& g, uint64_t lo, uint64_t hi) {
     GM_CUDA(cudaEventCreate(&c.e1));
     build_tiles(g, c, s, lo, hi);
     c.dang_partial.alloc(std::max<uint64_t>(kDangBlocks, c.ntiles + c.n_long) + 1, s);
-    k_pr_init<<<grid_for(n, 256), 256, 0, s>>>(n, g.outdeg.get(), c.inv.get(), c.rank.get(),
-                                               c.x0.get());
-    GM_LAUNCH_CHECK();
     GM_CUDA(cudaStreamSynchronize(s));
   }
   return *g.pr;
 }
 
 PrCache& cache(Graph& g) { return cache(g, 0, g.n); }
+
+// Initial state: ranks 1/N in buffer 0, x = rank * inv.
+void init_state(Graph& g, PrCache& c) {
+  c.cur = 0;
+  k_pr_init<<<grid_for(g.n, 256), 256, 0, g.stream>>>(g.n, g.outdeg.get(), c.inv.get(),
+                                                       c.rank0.get(), c.x0.get());
+  GM_LAUNCH_CHECK();
+}
 
 }  // namespace
 
@@ -388,49 +478,30 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   PrCache& c = cache(g);
   cudaStream_t s = g.stream;
   const uint64_t dang_lo = (g.relabeled && g.shards == 1) ? g.nonzero_outdeg : 0;
-  k_pr_init<<<grid_for(n, 256), 256, 0, s>>>(n, g.outdeg.get(), c.inv.get(), c.rank.get(), c.x0.get());
-  GM_LAUNCH_CHECK();
+  init_state(g, c);
   unsigned* ticket = reinterpret_cast<unsigned*>(c.ctr.get() + 3);
   GM_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
   float* xc = c.x0.get();
   float* xn = c.x1.get();
   const float d = float(damping);
   // Base of the first superstep (initial ranks); later bases come from the
-  // dangling partials the SpMV kernels emit (k_pr_base).
-  k_dangling<<<kDangBlocks, 256, 0, s>>>(dang_lo, n, c.rank.get(), c.inv.get(),
-                                         c.dang_partial.get(), c.scalars.get(), damping, ticket);
+  // dangling partials the SpMV kernel emits (k_pr_base).
+  k_dangling<<<kDangBlocks, 256, 0, s>>>(dang_lo, n, c.rank(), c.inv.get(), c.dang_partial.get(),
+                                         c.scalars.get(), damping, ticket);
   GM_LAUNCH_CHECK();
-  float* part = c.dang_partial.get();
   for (int64_t it = 1; it <= iters; ++it) {
     if (collect) GM_CUDA(cudaEventRecord(c.e0, s));
-    if (collect) GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
-    if (c.ntiles) {
-      if (collect)
-        k_pr_tiles<true><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
-            c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
-            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get(), part);
-      else
-        k_pr_tiles<false><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
-            c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(),
-            c.rank.get(), xn, c.scalars.get(), d, c.ctr.get(), part);
-      GM_LAUNCH_CHECK();
-    }
-    if (c.n_long) {
-      if (collect)
-        k_pr_long_rows<true><<<unsigned(c.n_long), 256, 0, s>>>(
-            c.long_rows.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(), c.rank.get(), xn,
-            c.scalars.get(), d, c.ctr.get(), part + c.ntiles);
-      else
-        k_pr_long_rows<false><<<unsigned(c.n_long), 256, 0, s>>>(
-            c.long_rows.get(), g.in.ptr.get(), g.in.idx.get(), xc, c.inv.get(), c.rank.get(), xn,
-            c.scalars.get(), d, c.ctr.get(), part + c.ntiles);
-      GM_LAUNCH_CHECK();
-    }
-    k_pr_base<<<1, 1024, 0, s>>>(part, uint32_t(c.ntiles + c.n_long), n, damping, c.scalars.get());
+    launch_spmv(g, c, xc, xn, d, s);
+    k_pr_base<<<1, 1024, 0, s>>>(c.dang_partial.get(), uint32_t(c.ntiles + c.n_long), n, damping,
+                                 c.scalars.get());
     GM_LAUNCH_CHECK();
     std::swap(xc, xn);
     if (!collect) continue;
     GM_CUDA(cudaEventRecord(c.e1, s));
+    GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
+    k_pr_count<<<grid_for(n, 256), 256, 0, s>>>(0, n, g.in.ptr.get(), c.rank_other(), c.rank(),
+                                                c.ctr.get());
+    GM_LAUNCH_CHECK();
     unsigned long long upd = 0;
     GM_CUDA(cudaMemcpyAsync(&upd, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
     GM_CUDA(cudaStreamSynchronize(s));
@@ -450,10 +521,10 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   }
   if (out) {
     if (out_on_device) {
-      to_external(g, c.rank.get(), out, 4);
+      to_external(g, c.rank(), out, 4);
     } else {
       DevBuf<float> ext(n, s);
-      to_external(g, c.rank.get(), ext.get(), 4);
+      to_external(g, c.rank(), ext.get(), 4);
       GM_CUDA(cudaMemcpyAsync(out, ext.get(), n * 4, cudaMemcpyDeviceToHost, s));
     }
   }
@@ -502,9 +573,7 @@ double pagerank_shard_init(Graph& g, uint64_t lo, uint64_t hi, float* x_block) {
   check_block(g, lo, hi);
   PrCache& c = cache(g, lo, hi);
   cudaStream_t s = g.stream;
-  k_pr_init<<<grid_for(g.n, 256), 256, 0, s>>>(g.n, g.outdeg.get(), c.inv.get(), c.rank.get(),
-                                               c.x0.get());
-  GM_LAUNCH_CHECK();
+  init_state(g, c);
   if (hi > lo)
     GM_CUDA(cudaMemcpyAsync(x_block, c.x0.get() + lo, (hi - lo) * 4, cudaMemcpyDeviceToDevice, s));
   GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
@@ -524,24 +593,11 @@ double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_fu
   PrCache& c = cache(g, lo, hi);
   cudaStream_t s = g.stream;
   const float b = float(base);
-  const float d = float(damping);
   GM_CUDA(cudaMemcpyAsync(c.scalars.get(), &b, 4, cudaMemcpyHostToDevice, s));
-  float* part = c.dang_partial.get();
-  float* xn = x_block - lo;  // the kernels write x_next[row] for rows in [lo, hi)
-  if (c.ntiles) {
-    k_pr_tiles<false><<<unsigned(c.ntiles), kPrThreads, 0, s>>>(
-        c.tile_b.get(), c.tile_e.get(), g.in.ptr.get(), g.in.idx.get(), x_full, c.inv.get(),
-        c.rank.get(), xn, c.scalars.get(), d, c.ctr.get(), part);
-    GM_LAUNCH_CHECK();
-  }
-  if (c.n_long) {
-    k_pr_long_rows<false><<<unsigned(c.n_long), 256, 0, s>>>(
-        c.long_rows.get(), g.in.ptr.get(), g.in.idx.get(), x_full, c.inv.get(), c.rank.get(), xn,
-        c.scalars.get(), d, c.ctr.get(), part + c.ntiles);
-    GM_LAUNCH_CHECK();
-  }
+  // the kernel writes x_next[row] for rows in [lo, hi) only
+  launch_spmv(g, c, x_full, x_block - lo, float(damping), s);
   double* dsum = reinterpret_cast<double*>(c.ctr.get() + 2);
-  k_sum_partials<<<1, 1024, 0, s>>>(part, uint32_t(c.ntiles + c.n_long), dsum);
+  k_sum_partials<<<1, 1024, 0, s>>>(c.dang_partial.get(), uint32_t(c.ntiles + c.n_long), dsum);
   GM_LAUNCH_CHECK();
   double h = 0.0;
   GM_CUDA(cudaMemcpyAsync(&h, dsum, 8, cudaMemcpyDeviceToHost, s));
@@ -553,7 +609,7 @@ void pagerank_shard_ranks(Graph& g, uint64_t lo, uint64_t hi, float* out_host) {
   check_block(g, lo, hi);
   PrCache& c = cache(g, lo, hi);
   if (hi > lo)
-    GM_CUDA(cudaMemcpyAsync(out_host, c.rank.get() + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost,
+    GM_CUDA(cudaMemcpyAsync(out_host, c.rank() + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost,
                             g.stream));
   GM_CUDA(cudaStreamSynchronize(g.stream));
 }

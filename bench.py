@@ -438,7 +438,11 @@ class CfWorkload(Workload):
 
 WORKLOADS = {"bfs": (BfsWorkload, 23), "pagerank": (PageRankWorkload, 20),
              "pagerank23": (PageRankWorkload, 23), "sssp": (SsspWorkload, 23),
-             "cf": (CfWorkload, 0)}
+             "cf": (CfWorkload, 0),
+             # BASELINE configs[4] (scale 28) on one GPU / sharded over N
+             "bfs28": (BfsWorkload, 28), "pagerank28": (PageRankWorkload, 28)}
+# The reference engine cannot hold scale >= 26 in host memory.
+CPU_MAX_SCALE = 25
 
 
 # ----------------------------------------------------------------- arms
@@ -534,8 +538,13 @@ def run_ours(args, d: Dist):
         "per_superstep": per,
     }
     if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
-        import oracle
-        line["cpu_baseline"] = w.cpu_baseline(oracle)
+        if getattr(args, "scale", 0) and args.scale > CPU_MAX_SCALE:
+            line["cpu_baseline"] = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
+                                    "sample": f"none: the reference engine needs >100 GB of host "
+                                              f"memory at scale {args.scale} (SURVEY.md 8d)"}
+        else:
+            import oracle
+            line["cpu_baseline"] = w.cpu_baseline(oracle)
     if d.rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -551,6 +560,10 @@ def run_reference(args, d: Dist):
     scale = args.scale if args.scale is not None else default_scale
     if R is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    if args.workload != "cf" and scale > CPU_MAX_SCALE:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"scale {scale}: the reference engine needs >100 GB of host memory"}))
         return
     cores = int(R.ref_hardware_threads())
     n = 1 << scale

@@ -216,6 +216,14 @@ GM_API gm_status gm_superstep_phases(gm_graph_t g, int32_t program, const double
                                      uint8_t* x_valid, int32_t run_spmv, void* y,
                                      uint8_t* y_valid);
 
+/* Zero-copy view of the device CSR in internal ids: which 0 = CSR(G^T) (rows =
+ * destinations, the matrix the reference stores, dcsc.hpp:243-274), 1 = CSR(G)
+ * (built on demand like ensure_forward, dcsc.hpp:201-215).  The pointers stay
+ * valid until gm_graph_destroy and must not be written.  For validation
+ * harnesses and callers that run their own kernels on the graph. */
+GM_API gm_status gm_graph_csr(gm_graph_t g, int32_t which, const uint64_t** ptr_dev,
+                              const uint32_t** idx_dev, uint64_t* rows, uint64_t* nnz);
+
 /* ---- multi-GPU sharding (1-D row blocks of G^T, one process per GPU) ----- */
 /* caller id -> internal id (n entries, host); identity without GM_RELABEL. */
 GM_API gm_status gm_graph_permutation(gm_graph_t g, uint32_t* caller_to_internal);

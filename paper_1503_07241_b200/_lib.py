@@ -25,7 +25,7 @@ EXPORTED = [
     "gm_graph_stream", "gm_pagerank", "gm_bfs", "gm_sssp", "gm_cf", "gm_program_sizes",
     "gm_run_graph_program", "gm_superstep_phases", "gm_balanced_row_boundaries",
     "gm_kernel_launches", "gm_graph_permutation", "gm_pagerank_shard_init",
-    "gm_pagerank_shard_step", "gm_pagerank_shard_ranks",
+    "gm_pagerank_shard_step", "gm_pagerank_shard_ranks", "gm_graph_csr",
 ]
 
 
@@ -102,6 +102,8 @@ def load(path: str = LIB_PATH):
         "gm_balanced_row_boundaries": (C.c_int, [vp, u64, u64, vp]),
         "gm_kernel_launches": (C.c_uint64, []),
         "gm_graph_permutation": (C.c_int, [vp, vp]),
+        "gm_graph_csr": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64),
+                                   C.POINTER(u64)]),
         "gm_pagerank_shard_init": (C.c_int, [vp, u64, u64, vp, C.POINTER(dp)]),
         "gm_pagerank_shard_step": (C.c_int, [vp, u64, u64, vp, dp, dp, vp, C.POINTER(dp)]),
         "gm_pagerank_shard_ranks": (C.c_int, [vp, u64, u64, vp]),

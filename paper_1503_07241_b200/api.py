@@ -237,6 +237,16 @@ class Graph:
         _check(L.load().gm_graph_permutation(self._h, out.ctypes.data))
         return out
 
+    def csr(self, which: str = "in"):
+        """Device CSR in internal ids (gm_graph_csr): ``(ptr, idx, rows, nnz)`` with
+        ``ptr``/``idx`` raw device addresses of u64[rows+1] / u32[nnz] arrays.
+        ``which`` = "in" (G^T, rows = destinations) or "out" (G)."""
+        p, i = C.c_void_p(), C.c_void_p()
+        rows, nnz = C.c_uint64(), C.c_uint64()
+        _check(L.load().gm_graph_csr(self._h, 1 if which == "out" else 0, C.byref(p), C.byref(i),
+                                     C.byref(rows), C.byref(nnz)))
+        return int(p.value or 0), int(i.value or 0), int(rows.value), int(nnz.value)
+
     def pick_source(self, seed) -> int:
         v = C.c_uint64()
         _check(L.load().gm_pick_source(self._h, seed, C.byref(v)))

@@ -210,6 +210,21 @@ GM_API gm_status gm_graph_permutation(gm_graph_t g, uint32_t* caller_to_internal
   });
 }
 
+GM_API gm_status gm_graph_csr(gm_graph_t g, int32_t which, const uint64_t** ptr_dev,
+                              const uint32_t** idx_dev, uint64_t* rows, uint64_t* nnz) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (which != 0 && which != 1) gm::fail(GM_EUSAGE, "csr: which must be 0 (G^T) or 1 (G)");
+    if (!ptr_dev || !idx_dev || !rows || !nnz) gm::fail(GM_EUSAGE, "null argument");
+    if (which == 1) gm::ensure_forward(*h);
+    const gm::Csr& c = which == 1 ? h->fwd() : h->in;
+    *ptr_dev = c.ptr.get();
+    *idx_dev = c.idx.get();
+    *rows = h->n;
+    *nnz = c.nnz;
+  });
+}
+
 GM_API gm_status gm_pagerank_shard_init(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                         float* x_block_dev, double* dangling_block) {
   return guarded([&] {

@@ -53,19 +53,19 @@ void sort_keys(DevBuf<uint64_t>& keys, int64_t m, int end_bit, cudaStream_t s) {
   if (dk.Current() != keys.get()) keys.swap(k2);
 }
 
+// In-place stable compaction (no second m-sized buffer: at scale 28 the key
+// array alone is 34-69 GB).
 template <typename T>
 int64_t select_flagged(DevBuf<T>& data, const uint8_t* flags, int64_t m, cudaStream_t s) {
   if (m == 0) return 0;
-  DevBuf<T> out(m, s);
   DevBuf<int64_t> cnt(1, s);
   size_t tmp = 0;
-  GM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, data.get(), flags, out.get(), cnt.get(), m, s));
+  GM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, data.get(), flags, cnt.get(), m, s));
   DevBuf<uint8_t> t(tmp, s);
-  GM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, data.get(), flags, out.get(), cnt.get(), m, s));
+  GM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, data.get(), flags, cnt.get(), m, s));
   int64_t h = 0;
   GM_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
   GM_CUDA(cudaStreamSynchronize(s));
-  data.swap(out);
   return h;
 }
 
@@ -95,7 +95,7 @@ __global__ void k_make_keys(const uint32_t* s, const uint32_t* d, int64_t m, uns
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
        e += int64_t(gridDim.x) * blockDim.x) {
     keys[e] = (uint64_t(s[e]) << nb) | d[e];
-    idx[e] = uint32_t(e);
+    if (idx) idx[e] = uint32_t(e);
     keep[e] = drop_loops ? (s[e] != d[e]) : 1;
   }
 }
@@ -116,7 +116,7 @@ __global__ void k_append_reverse(uint64_t* keys, uint32_t* idx, int64_t m, unsig
        i += int64_t(gridDim.x) * blockDim.x) {
     const uint64_t k = keys[i];
     keys[m + i] = ((k & mask) << nb) | (k >> nb);
-    idx[m + i] = idx[i];
+    if (idx) idx[m + i] = idx[i];
   }
 }
 
@@ -341,14 +341,24 @@ __global__ void k_count_nonzero(const uint32_t* deg, uint64_t n, unsigned long l
   warp_add_u64(cnt, c);
 }
 
+__global__ void k_widen(const uint32_t* in, uint64_t n, uint64_t* out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
 void exclusive_scan_to_ptr(const uint32_t* counts, uint64_t* ptr, uint64_t n, cudaStream_t s) {
-  // ptr[0] = 0, ptr[i+1] = sum counts[0..i]
+  // ptr[0] = 0, ptr[i+1] = sum counts[0..i].  The counts are widened to u64
+  // first: CUB accumulates in the input type, and above 2^32 stored entries
+  // (scale-28 R-MAT) a u32 running sum wraps.
   GM_CUDA(cudaMemsetAsync(ptr, 0, sizeof(uint64_t), s));
   if (n == 0) return;
+  k_widen<<<grid_for(n, 256), 256, 0, s>>>(counts, n, ptr + 1);
+  GM_LAUNCH_CHECK();
   size_t tmp = 0;
-  GM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, counts, ptr + 1, int64_t(n), s));
+  GM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, ptr + 1, ptr + 1, int64_t(n), s));
   DevBuf<uint8_t> t(tmp, s);
-  GM_CUDA(cub::DeviceScan::InclusiveSum(t.get(), tmp, counts, ptr + 1, int64_t(n), s));
+  GM_CUDA(cub::DeviceScan::InclusiveSum(t.get(), tmp, ptr + 1, ptr + 1, int64_t(n), s));
 }
 
 template <typename F>
@@ -408,27 +418,35 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
   const int end_bit = int(2 * nb);
   const bool pre = (g.flags & (GM_PREPROCESS | GM_SYMMETRIZE)) != 0;
   const size_t vs = value_size(g.value_type);
+  // The payload (input position of each edge, to carry its value through the
+  // sorts) exists only when there are values: value-less graphs sort bare keys,
+  // which is what lets scale-28 R-MAT (4.3e9 raw, 8.6e9 symmetrised) fit.
+  const bool payload = vs && values;
 
   DevBuf<uint64_t> keys(m, s);
-  DevBuf<uint32_t> idx(m, s);
+  DevBuf<uint32_t> idx(payload ? m : 0, s);
   {
     DevBuf<uint8_t> keep(m, s);
     launch(m, s, [&](unsigned gr, unsigned b) {
-      k_make_keys<<<gr, b, 0, s>>>(s32.get(), d32.get(), m, nb, keys.get(), idx.get(), keep.get(),
-                                   pre ? 1 : 0);
+      k_make_keys<<<gr, b, 0, s>>>(s32.get(), d32.get(), m, nb, keys.get(),
+                                   payload ? idx.get() : nullptr, keep.get(), pre ? 1 : 0);
     });
     s32.reset();
     d32.reset();
     if (pre) {
-      DevBuf<uint8_t> keep2(m, s);
-      GM_CUDA(cudaMemcpyAsync(keep2.get(), keep.get(), m, cudaMemcpyDeviceToDevice, s));
-      select_flagged(keys, keep.get(), m, s);
-      m = select_flagged(idx, keep2.get(), m, s);
+      if (payload) select_flagged(idx, keep.get(), m, s);
+      m = select_flagged(keys, keep.get(), m, s);
     }
   }
+  auto sort = [&]() {
+    if (payload)
+      sort_pairs(keys, idx, m, end_bit, s);
+    else
+      sort_keys(keys, m, end_bit, s);
+  };
   auto dedup = [&](bool allow_dups) {
-    sort_pairs(keys, idx, m, end_bit, s);
-    DevBuf<uint8_t> flag(m, s), flag2(m, s);
+    sort();
+    DevBuf<uint8_t> flag(m, s);
     DevBuf<unsigned long long> dup(1, s);
     GM_CUDA(cudaMemsetAsync(dup.get(), 0xFF, sizeof(unsigned long long), s));
     launch(m, s, [&](unsigned gr, unsigned b) {
@@ -444,21 +462,22 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
                             std::to_string((k & mask) + 1) +
                             " (1-based); deduplicate before building");
       }
-      GM_CUDA(cudaMemcpyAsync(flag2.get(), flag.get(), m, cudaMemcpyDeviceToDevice, s));
-      select_flagged(keys, flag.get(), m, s);
-      m = select_flagged(idx, flag2.get(), m, s);
+      if (payload) select_flagged(idx, flag.get(), m, s);
+      m = select_flagged(keys, flag.get(), m, s);
     }
   };
   dedup(pre);
   if (g.flags & GM_SYMMETRIZE) {
     DevBuf<uint64_t> k2(2 * m, s);
-    DevBuf<uint32_t> i2(2 * m, s);
+    DevBuf<uint32_t> i2(payload ? 2 * m : 0, s);
     if (m) {
       GM_CUDA(cudaMemcpyAsync(k2.get(), keys.get(), m * 8, cudaMemcpyDeviceToDevice, s));
-      GM_CUDA(cudaMemcpyAsync(i2.get(), idx.get(), m * 4, cudaMemcpyDeviceToDevice, s));
+      if (payload) GM_CUDA(cudaMemcpyAsync(i2.get(), idx.get(), m * 4, cudaMemcpyDeviceToDevice, s));
     }
+    keys.reset();
+    idx.reset();
     launch(m, s, [&](unsigned gr, unsigned b) {
-      k_append_reverse<<<gr, b, 0, s>>>(k2.get(), i2.get(), m, nb);
+      k_append_reverse<<<gr, b, 0, s>>>(k2.get(), payload ? i2.get() : nullptr, m, nb);
     });
     keys.swap(k2);
     idx.swap(i2);
@@ -511,7 +530,7 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
   launch(m, s, [&](unsigned gr, unsigned b) {
     k_transpose_keys<<<gr, b, 0, s>>>(keys.get(), m, nb, g.relabeled ? g.perm.get() : nullptr);
   });
-  sort_pairs(keys, idx, m, end_bit, s);
+  sort();
   g.in.n = n;
   g.in.nnz = uint64_t(m);
   g.in.ptr.alloc(n + 1, s);
@@ -521,7 +540,7 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
     k_low_bits<<<gr, b, 0, s>>>(keys.get(), m, (uint64_t(1) << nb) - 1, g.in.idx.get());
   });
   keys.reset();
-  if (vs && values) {
+  if (payload) {
     g.in.val.alloc(size_t(m) * vs, s);
     gather_values(values.get(), idx.get(), m, vs, g.in.val.get(), s);
   }
@@ -648,7 +667,8 @@ Graph* graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b, doub
   if (!(a >= 0.0 && b >= 0.0 && c >= 0.0 && a + b + c <= 1.0))
     fail(GM_EINPUT, "rmat: quadrant probabilities must be non-negative and sum to at most 1");
   const uint64_t count = uint64_t(ef) << scale;
-  if (count >= 0xFFFFFFFFull) fail(GM_EUSAGE, "rmat: more than 2^32-2 raw edges");
+  // no payload (weights are derived from ids after the build): 2^36 raw edges
+  if (count > (uint64_t(1) << 36)) fail(GM_EUSAGE, "rmat: more than 2^36 raw edges");
   if (weights != GM_VAL_NONE && weights != GM_VAL_U8) fail(GM_EUSAGE, "rmat: weights must be none or u8");
   const uint64_t n = uint64_t(1) << scale;
   std::unique_ptr<Graph> g(new_graph(n, flags, weights));

@@ -949,7 +949,8 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   if (root >= n)
     fail(GM_EINPUT, "source vertex " + std::to_string(root + 1) + " (1-based) exceeds vertex count " +
                         std::to_string(n));
-  if (n >= (1ull << (64 - kCountShift)))
+  // a packed count holds a vertex count <= n - 1 (the source never re-enters)
+  if (n > (1ull << (64 - kCountShift)))
     fail(GM_EUSAGE, "bfs: graphs above 2^28 vertices are not supported by the packed queue");
   TravCache& c = cache(g);
   cudaStream_t s = g.stream;
@@ -1084,7 +1085,8 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
   if (g.value_type != GM_VAL_U8 && g.value_type != GM_VAL_U32)
     fail(GM_EUSAGE, std::string("sssp: needs u8 or u32 edge weights, graph stores ") +
                         value_name(g.value_type) + " (use GM_PROG_SSSP_REF for real weights)");
-  if (n >= (1ull << (64 - kCountShift)))
+  // a packed count holds a vertex count <= n - 1 (the source never re-enters)
+  if (n > (1ull << (64 - kCountShift)))
     fail(GM_EUSAGE, "sssp: graphs above 2^28 vertices are not supported by the packed queue");
   TravCache& c = cache(g);
   cudaStream_t s = g.stream;

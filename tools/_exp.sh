@@ -1,7 +1,8 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -q -x -k "pagerank or shard or smoke" 2>&1 | tail -5 > gpurun_out/t.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_pr -c 20 --csv --log-file gpurun_out/z.csv python tools/pr_once.py 23 > /dev/null 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_pr -c 20 --csv --log-file gpurun_out/z_stats.csv python tools/pr_once.py 23 stats > /dev/null 2>&1
-python bench.py --workload pagerank23 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b_pr23.json 2>&1
-python bench.py --workload pagerank --steps 5 --warmup 3 > gpurun_out/b_pr20.json 2>&1
-cat gpurun_out/t.log
+timeout 900 python tools/diag28.py 28 2>&1 | grep -v Assertion | head -20 > gpurun_out/diag28.txt
+SECONDS=0
+timeout 1500 python -m pytest tests/test_gpu_scale28.py -x -q > gpurun_out/t28.log 2>&1
+echo "rc=$? secs=$SECONDS" >> gpurun_out/t28.log
+timeout 600 python bench.py --workload bfs28 --steps 5 --warmup 3 > gpurun_out/b_bfs28.json 2> gpurun_out/b_bfs28.err
+timeout 600 python bench.py --workload pagerank28 --steps 2 --warmup 3 > gpurun_out/b_pr28.json 2> gpurun_out/b_pr28.err
+cat gpurun_out/diag28.txt; tail -4 gpurun_out/t28.log

@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1503_07241_b200 as gm  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("workload", choices=["pagerank", "bfs", "sssp"])
+ap.add_argument("workload", choices=["pagerank", "bfs", "sssp", "cf"])
 ap.add_argument("--scale", type=int, default=23)
 ap.add_argument("--reps", type=int, default=2)
 a = ap.parse_args()
@@ -20,6 +20,12 @@ elif a.workload == "bfs":
     r = g.pick_source(1)
     for _ in range(a.reps):
         gm.bfs(g, r, with_stats=False)
+elif a.workload == "cf":
+    import numpy as np
+    g = gm.Graph.bipartite(480189, 17770, 20081304.0, 17770, seed=1)
+    init = np.random.default_rng(1).uniform(0, 0.1, (g.num_vertices, 20)).astype(np.float32)
+    for _ in range(a.reps):
+        gm.collaborative_filtering_gd(g, 20, 1e-3, 0.05, 3, init=init)
 else:
     g = gm.Graph.rmat(a.scale, 16, seed=1, relabel=True, weights=True)
     r = g.pick_source(1)

@@ -86,6 +86,12 @@ def lib():
     L.or_pick_source.argtypes = [C.c_uint64, C.c_uint64, u32p]
     L.or_preprocess.restype = C.c_int64
     L.or_preprocess.argtypes = [C.c_int64, u32p, u32p, C.c_void_p, C.c_int]
+    L.or_preprocess_checked.restype = C.c_int64
+    L.or_preprocess_checked.argtypes = [C.c_int64, u32p, u32p, C.c_void_p, C.c_int,
+                                        C.POINTER(C.c_int64)]
+    L.or_triangle_count.restype = C.c_int64
+    L.or_triangle_count.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, C.c_void_p,
+                                    C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
     L.or_csr_build.restype = None
     L.or_csr_build.argtypes = [C.c_uint64, C.c_int64, u32p, u32p, C.c_void_p, u64p, u32p,
                                C.c_void_p]
@@ -137,8 +143,12 @@ def ref_lib():
                                   C.c_uint, C.c_int, f64p, C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_double)]
     R.ref_semiring_spmv.argtypes = common + [i64p, i64p, u8p, C.c_uint, C.c_uint, i64p, u8p]
+    R.ref_triangle_count.argtypes = common + [C.c_uint, C.c_uint, C.POINTER(C.c_uint64),
+                                              C.c_void_p, C.POINTER(C.c_double)]
+    R.ref_preprocess.argtypes = [C.c_int64, u32p, u32p, C.c_void_p, C.c_int]
+    R.ref_preprocess.restype = C.c_int64
     for f in (R.ref_bfs, R.ref_sssp, R.ref_pagerank, R.ref_pagerank_norm, R.ref_cf,
-              R.ref_semiring_spmv):
+              R.ref_semiring_spmv, R.ref_triangle_count):
         f.restype = C.c_int
     _REF = R
     return R
@@ -187,10 +197,21 @@ def pick_source(seed, degree):
     return int(lib().or_pick_source(seed, len(degree), degree))
 
 
-def preprocess(src, dst, vals=None, symmetrize=False):
-    """src/io.cpp:184-222 -- returns new (src, dst, vals) sorted by (src, dst)."""
+PREPROCESS_MODES = {"none": 0, "symmetrize": 1, "dagify": 2, "bipartite_check": 3}
+
+
+class OracleInputError(ValueError):
+    """The restated reference raised InputError."""
+
+
+def preprocess(src, dst, vals=None, symmetrize=False, mode=None):
+    """src/io.cpp:184-222 -- returns new (src, dst, vals) sorted by (src, dst).
+    mode: "none" | "symmetrize" | "dagify" | "bipartite_check" (default from
+    `symmetrize`).  BIPARTITE_CHECK failures raise OracleInputError with the
+    reference's message."""
+    mode = PREPROCESS_MODES[mode] if mode is not None else (1 if symmetrize else 0)
     m = len(src)
-    cap = 2 * m if symmetrize else m
+    cap = 2 * m if mode in (1, 2) else m
     s = np.zeros(max(cap, 1), np.uint32)
     d = np.zeros(max(cap, 1), np.uint32)
     s[:m] = src
@@ -199,9 +220,27 @@ def preprocess(src, dst, vals=None, symmetrize=False):
     if vals is not None:
         v = np.zeros(max(cap, 1), np.float64)
         v[:m] = vals
-    m2 = lib().or_preprocess(m, s, d, v.ctypes.data if v is not None else None,
-                             1 if symmetrize else 0)
+    bad = C.c_int64(-1)
+    m2 = lib().or_preprocess_checked(m, s, d, v.ctypes.data if v is not None else None, mode,
+                                     C.byref(bad))
+    if m2 < 0:
+        # cleanup ran in place: s/d hold the sorted unique edges
+        e = bad.value
+        raise OracleInputError(f"not bipartite: edge {int(s[e]) + 1} -> {int(d[e]) + 1} "
+                               "(1-based) mixes the user and item sides")
     return s[:m2].copy(), d[:m2].copy(), (v[:m2].copy() if v is not None else None)
+
+
+def triangle_count(n, src, dst):
+    """algorithms/triangle_count.hpp:115-134 -> (total, local counts uint64[n])."""
+    src, dst = _u32(src), _u32(dst)
+    local = np.zeros(max(n, 1), np.uint64)
+    bs, bd = C.c_uint32(), C.c_uint32()
+    t = lib().or_triangle_count(n, len(src), src, dst, local.ctypes.data, C.byref(bs), C.byref(bd))
+    if t < 0:
+        raise OracleInputError(f"triangle_count: edge {bs.value + 1} -> {bd.value + 1} (1-based) "
+                               "violates src < dst; run DAGIFY preprocessing first")
+    return int(t), local[:n]
 
 
 def csr(n, row, col, vals=None):
@@ -405,6 +444,34 @@ def ref_semiring_spmv(n, src, dst, vals, x, xvalid, threads=1, parts=1):
               np.ascontiguousarray(vals, np.int64), np.ascontiguousarray(x, np.int64),
               np.ascontiguousarray(xvalid, np.uint8), threads, parts, y, yv)
     return y, yv.astype(bool)
+
+
+def ref_triangle_count(n, src, dst, threads=1, parts=1):
+    """algo::triangle_count of the compiled reference -> (total, local uint64[n])."""
+    R = ref_lib()
+    tot = C.c_uint64()
+    local = np.zeros(max(n, 1), np.uint64)
+    _ref_call(R.ref_triangle_count, n, len(src), _u32(src), _u32(dst), threads, parts,
+              C.byref(tot), local.ctypes.data, None)
+    return int(tot.value), local[:n]
+
+
+def ref_preprocess(src, dst, vals=None, mode="none"):
+    """io::preprocess of the compiled reference (src/io.cpp:184-222)."""
+    R = ref_lib()
+    m = len(src)
+    cap = max(2 * m, 1)
+    s = np.zeros(cap, np.uint32)
+    d = np.zeros(cap, np.uint32)
+    s[:m], d[:m] = src, dst
+    v = None
+    if vals is not None:
+        v = np.zeros(cap, np.float64)
+        v[:m] = vals
+    k = R.ref_preprocess(m, s, d, v.ctypes.data if v is not None else None, PREPROCESS_MODES[mode])
+    if k < 0:
+        raise OracleInputError(R.ref_last_error().decode())
+    return s[:k].copy(), d[:k].copy(), (v[:k].copy() if v is not None else None)
 
 
 class RefGraph:

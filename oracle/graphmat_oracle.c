@@ -341,17 +341,119 @@ static int64_t cleanup(int64_t m, uint32_t* src, uint32_t* dst, double* vals) {
   return out;
 }
 
-int64_t or_preprocess(int64_t m, uint32_t* src, uint32_t* dst, double* vals, int symmetrize) {
+/* io::preprocess (src/io.cpp:184-222): cleanup, then SYMMETRIZE / DAGIFY append
+ * the reversed edges after the originals and clean up again (stable: an
+ * original (a, b) keeps its value over the reverse of (b, a)); DAGIFY then
+ * drops src >= dst; BIPARTITE_CHECK rejects an edge whose source is some
+ * edge's destination or whose destination is some edge's source. */
+int64_t or_preprocess_checked(int64_t m, uint32_t* src, uint32_t* dst, double* vals, int mode,
+                              int64_t* bad) {
   m = cleanup(m, src, dst, vals);
-  if (symmetrize) {
+  if (mode == 1 || mode == 2) {
     for (int64_t e = 0; e < m; ++e) {
       src[m + e] = dst[e];
       dst[m + e] = src[e];
       if (vals) vals[m + e] = vals[e];
     }
     m = cleanup(2 * m, src, dst, vals);
+    if (mode == 2) {
+      int64_t w = 0;
+      for (int64_t e = 0; e < m; ++e) {
+        if (src[e] >= dst[e]) continue;
+        src[w] = src[e];
+        dst[w] = dst[e];
+        if (vals) vals[w] = vals[e];
+        ++w;
+      }
+      m = w;
+    }
+  } else if (mode == 3) {
+    uint32_t mx = 0;
+    for (int64_t e = 0; e < m; ++e) {
+      if (src[e] > mx) mx = src[e];
+      if (dst[e] > mx) mx = dst[e];
+    }
+    uint8_t* role = (uint8_t*)calloc((size_t)mx + 1, 1); /* bit 0 source, bit 1 destination */
+    for (int64_t e = 0; e < m; ++e) {
+      role[src[e]] |= 1;
+      role[dst[e]] |= 2;
+    }
+    for (int64_t e = 0; e < m; ++e)
+      if ((role[src[e]] & 2) || (role[dst[e]] & 1)) {
+        if (bad) *bad = e;
+        free(role);
+        return -1;
+      }
+    free(role);
   }
   return m;
+}
+
+int64_t or_preprocess(int64_t m, uint32_t* src, uint32_t* dst, double* vals, int mode) {
+  return or_preprocess_checked(m, src, dst, vals, mode, NULL);
+}
+
+/* triangle_count (algorithms/triangle_count.hpp:115-134): phase 1 gives every
+ * vertex its ascending in-neighbour list (NeighborGatherProgram), phase 2 sends
+ * each list along the out-edges and the receiver counts the ids shared with its
+ * own list (ListIntersectProgram, a linear merge). */
+int64_t or_triangle_count(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
+                          uint64_t* local, uint32_t* bad_src, uint32_t* bad_dst) {
+  int found = 0;
+  uint32_t bs = 0, bd = 0;
+  for (int64_t e = 0; e < m; ++e)
+    if (src[e] >= dst[e] &&
+        (!found || src[e] < bs || (src[e] == bs && dst[e] < bd))) {
+      found = 1;
+      bs = src[e];
+      bd = dst[e];
+    }
+  if (found) {
+    if (bad_src) *bad_src = bs;
+    if (bad_dst) *bad_dst = bd;
+    return -1;
+  }
+  uint64_t* ptr = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n + 1));
+  uint32_t* idx = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(m ? m : 1));
+  or_csr_build(n, m, dst, src, NULL, ptr, idx, NULL); /* rows = destinations */
+  /* counting-sort CSR keeps input order: sort each list ascending */
+  for (uint64_t v = 0; v < n; ++v) {
+    uint32_t* a = idx + ptr[v];
+    const uint64_t len = ptr[v + 1] - ptr[v];
+    for (uint64_t i = 1; i < len; ++i) { /* insertion sort; lists are short in tests */
+      const uint32_t x = a[i];
+      uint64_t j = i;
+      while (j > 0 && a[j - 1] > x) {
+        a[j] = a[j - 1];
+        --j;
+      }
+      a[j] = x;
+    }
+  }
+  int64_t total = 0;
+  for (uint64_t w = 0; w < n; ++w) {
+    uint64_t cnt = 0;
+    for (uint64_t k = ptr[w]; k < ptr[w + 1]; ++k) {
+      const uint32_t v = idx[k];
+      uint64_t a = ptr[v], ae = ptr[v + 1], b = ptr[w], be = ptr[w + 1];
+      while (a < ae && b < be) {
+        if (idx[a] < idx[b])
+          ++a;
+        else if (idx[b] < idx[a])
+          ++b;
+        else {
+          ++cnt;
+          ++a;
+          ++b;
+        }
+      }
+    }
+    if (local) local[w] = cnt;
+    total += (int64_t)cnt;
+  }
+  free(ptr);
+  free(idx);
+  return total;
 }
 
 void or_csr_build(uint64_t n, int64_t m, const uint32_t* row, const uint32_t* col,

@@ -16,7 +16,10 @@
  *                          (algorithms/collaborative_filtering.hpp:181-193)
  *   or_cf_gd               algorithms/collaborative_filtering.hpp:51-211
  *   or_semiring_spmv       tests/support/oracles.cpp:33-50 (dense_spmv) over stored entries
- *   or_preprocess          src/io.cpp:184-222 (self loops, stable dedup keep-first, SYMMETRIZE)
+ *   or_preprocess          src/io.cpp:184-222 (self loops, stable dedup keep-first,
+ *                          SYMMETRIZE, DAGIFY, BIPARTITE_CHECK)
+ *   or_triangle_count      include/semigraph/algorithms/triangle_count.hpp:35-134 (gather the
+ *                          ascending in-neighbour lists, intersect along every stored edge)
  * The generators (R-MAT with Philox counters + seeded bijection, Zipf bipartite) are the
  * seeded generators this repo defines for the BASELINE configs (the reference's mt19937
  * stream, src/io.cpp:224-288, is sequential and has no permutation); the CUDA ingest
@@ -61,7 +64,19 @@ uint32_t or_pick_source(uint64_t seed, uint64_t n, const uint32_t* degree);
 /* In place. Removes self loops, stable-sorts by (src,dst), keeps the first of each
  * duplicate; symmetrize appends reverses and cleans again (src/io.cpp:184-206).
  * Arrays must have room for 2*m entries when symmetrize != 0. vals may be NULL. */
-int64_t or_preprocess(int64_t m, uint32_t* src, uint32_t* dst, double* vals, int symmetrize);
+/* mode 0 NONE, 1 SYMMETRIZE, 2 DAGIFY (symmetrize, keep src < dst), 3 BIPARTITE_CHECK.
+ * src/dst/vals need room for 2m entries for modes 1-2.  Returns the new count,
+ * or -1 for BIPARTITE_CHECK failure with *bad = index (in the returned sorted
+ * order) of the first edge whose source is also a destination or vice versa. */
+int64_t or_preprocess(int64_t m, uint32_t* src, uint32_t* dst, double* vals, int mode);
+int64_t or_preprocess_checked(int64_t m, uint32_t* src, uint32_t* dst, double* vals, int mode,
+                              int64_t* bad);
+/* Triangles of a DAG-form graph (every edge src < dst).  local[w] = sum over
+ * stored v -> w of |N_in(v) & N_in(w)| (TriangleState::local_count).  Returns
+ * the total, or -1 with *bad_src, *bad_dst = the first edge (by (src, dst))
+ * violating src < dst. */
+int64_t or_triangle_count(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
+                          uint64_t* local, uint32_t* bad_src, uint32_t* bad_dst);
 /* Counting-sort CSR keyed by row[], entries keep input order (stable). */
 void or_csr_build(uint64_t n, int64_t m, const uint32_t* row, const uint32_t* col,
                   const double* vals, uint64_t* ptr, uint32_t* idx, double* out_vals);

@@ -13,6 +13,8 @@
 //   algo::bfs / algo::sssp    include/semigraph/algorithms/traversal.hpp:119-133
 //   algo::pagerank            include/semigraph/algorithms/pagerank.hpp:73-110
 //   collaborative_filtering_gd include/semigraph/algorithms/collaborative_filtering.hpp:134-211
+//   algo::triangle_count      include/semigraph/algorithms/triangle_count.hpp:115-134
+//   io::preprocess            src/io.cpp:184-222 (compiled from the reference tree with it)
 // The one new program is the BASELINE-normalised PageRank, which
 // BASELINE configs[0] needs and the reference does not ship; it is driven
 // through the reference engine phases exactly like the CF driver does.
@@ -28,7 +30,9 @@
 #include "semigraph/algorithms/collaborative_filtering.hpp"
 #include "semigraph/algorithms/pagerank.hpp"
 #include "semigraph/algorithms/traversal.hpp"
+#include "semigraph/algorithms/triangle_count.hpp"
 #include "semigraph/engine.hpp"
+#include "semigraph/io.hpp"
 
 using namespace semigraph;
 
@@ -423,6 +427,48 @@ int ref_semiring_spmv(uint64_t n, int64_t m, const uint32_t* src, const uint32_t
     for (VertexId k2 = 0; k2 < n; ++k2) {
       yvalid[k2] = ys.valid(k2) ? 1 : 0;
       y[k2] = ys.valid(k2) ? ys.value(k2) : 0;
+    }
+  });
+}
+
+// io::preprocess(mode 0..3); returns the new count (arrays need 2m room) or -1
+// (InputError, message in ref_last_error).
+int64_t ref_preprocess(int64_t m, uint32_t* src, uint32_t* dst, double* vals, int mode) {
+  int64_t out = -1;
+  const int rc = guarded([&] {
+    auto e = triples(m, src, dst, vals);
+    const io::PreprocessMode md = mode == 1   ? io::PreprocessMode::SYMMETRIZE
+                                  : mode == 2 ? io::PreprocessMode::DAGIFY
+                                  : mode == 3 ? io::PreprocessMode::BIPARTITE_CHECK
+                                              : io::PreprocessMode::NONE;
+    auto r = io::preprocess(std::move(e), md);
+    for (std::size_t i = 0; i < r.size(); ++i) {
+      src[i] = static_cast<uint32_t>(r[i].src);
+      dst[i] = static_cast<uint32_t>(r[i].dst);
+      if (vals) vals[i] = r[i].value;
+    }
+    out = static_cast<int64_t>(r.size());
+  });
+  return rc == 0 ? out : -1;
+}
+
+// algo::triangle_count on a DAG-form edge list; local = TriangleState::local_count.
+int ref_triangle_count(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
+                       unsigned threads, unsigned parts, uint64_t* total, uint64_t* local,
+                       double* algo_seconds) {
+  return guarded([&] {
+    auto e = triples(m, src, dst, nullptr);
+    auto g = build_graph<algo::TriangleState, double>(e, n, parts ? parts : 1);
+    EngineConfig cfg;
+    cfg.thread_count = resolve_threads(threads);
+    cfg.max_iterations = 4;
+    Engine eng(cfg);
+    const double t0 = now_s();
+    *total = algo::triangle_count(g, eng);
+    if (algo_seconds) *algo_seconds = now_s() - t0;
+    if (local) {
+      auto& props = g.properties();
+      for (VertexId v = 0; v < n; ++v) local[v] = props[v].local_count;
     }
   });
 }

@@ -9,6 +9,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "reference_golden.npz")
+GOLDEN_F = os.path.join(ROOT, "tests", "golden", "reference_golden_f.npz")
 
 
 def pytest_configure(config):
@@ -19,6 +20,11 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden():
     return np.load(GOLDEN)
+
+
+@pytest.fixture(scope="session")
+def golden_f():
+    return np.load(GOLDEN_F)
 
 
 @pytest.fixture(scope="session")

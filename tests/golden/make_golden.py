@@ -3,7 +3,9 @@
 
     python tests/golden/make_golden.py
 
-Writes tests/golden/reference_golden.npz.  The fixtures are outputs of the
+Writes tests/golden/reference_golden.npz (the superstep programs) and
+tests/golden/reference_golden_f.npz (SURVEY 8f rows: io::preprocess modes,
+triangle counting).  The fixtures are outputs of the
 reference itself on seeded inputs; the CPU tests pin the C restatement
 (oracle/graphmat_oracle.c) to them and the GPU tests pin the CUDA path.
 """
@@ -16,6 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import oracle  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_golden.npz")
+OUT_F = os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_golden_f.npz")
 
 
 def rand_graph(rng, n, m):
@@ -83,5 +86,46 @@ def main():
     print("wrote", OUT, os.path.getsize(OUT), "bytes")
 
 
+def main_f():
+    """io::preprocess (all four modes, values kept) and algo::triangle_count."""
+    rng = np.random.default_rng(20261019)
+    out = {}
+    cases = []
+    for t in range(16):
+        n = int(rng.integers(3, 500))
+        m = int(rng.integers(0, 5 * n))
+        s = rng.integers(0, n, m).astype(np.uint32)
+        d = rng.integers(0, n, m).astype(np.uint32)
+        v = rng.uniform(-4.0, 4.0, m)
+        key = f"p{t}"
+        out[f"{key}_n"] = np.array([n])
+        out[f"{key}_src"], out[f"{key}_dst"], out[f"{key}_val"] = s, d, v
+        for mode in ("none", "symmetrize", "dagify"):
+            ps, pd, pv = oracle.ref_preprocess(s, d, v, mode=mode)
+            out[f"{key}_{mode}_src"], out[f"{key}_{mode}_dst"], out[f"{key}_{mode}_val"] = ps, pd, pv
+        ds, dd = out[f"{key}_dagify_src"], out[f"{key}_dagify_dst"]
+        tot, local = oracle.ref_triangle_count(n, ds, dd, threads=2, parts=3)
+        out[f"{key}_tc_total"], out[f"{key}_tc_local"] = np.array([tot], np.uint64), local
+        cases.append(key)
+    # bipartite check: one passing, one failing instance (message pinned)
+    users, items = 30, 12
+    s = rng.integers(0, users, 90).astype(np.uint32)
+    d = (users + rng.integers(0, items, 90)).astype(np.uint32)
+    out["bip_ok_src"], out["bip_ok_dst"] = s, d
+    bs = np.concatenate([s, [users + 3]]).astype(np.uint32)
+    bd = np.concatenate([d, [5]]).astype(np.uint32)
+    out["bip_bad_src"], out["bip_bad_dst"] = bs, bd
+    try:
+        oracle.ref_preprocess(bs, bd, mode="bipartite_check")
+        raise AssertionError("expected rejection")
+    except oracle.OracleInputError as e:
+        out["bip_bad_msg"] = np.array([str(e)])
+    out["cases"] = np.array(cases)
+    np.savez_compressed(OUT_F, **out)
+    print("wrote", OUT_F, os.path.getsize(OUT_F), "bytes")
+
+
 if __name__ == "__main__":
-    main()
+    if "--f-only" not in sys.argv:
+        main()
+    main_f()

@@ -72,7 +72,10 @@ enum {
   GM_PREPROCESS = 1u,   /* io::preprocess cleanup: drop self loops, dedup keep-first (io.cpp:184-196) */
   GM_SYMMETRIZE = 2u,   /* PreprocessMode::SYMMETRIZE (io.cpp:198-204); implies GM_PREPROCESS      */
   GM_RELABEL = 4u,      /* internal degree-ordered vertex ids (results stay in caller ids)          */
-  GM_NEED_FORWARD = 8u  /* build CSR(G) eagerly (Graph::ensure_forward, dcsc.hpp:201-215)           */
+  GM_NEED_FORWARD = 8u, /* build CSR(G) eagerly (Graph::ensure_forward, dcsc.hpp:201-215)           */
+  GM_DAGIFY = 16u,      /* PreprocessMode::DAGIFY (io.cpp:198-207): symmetrize, keep src < dst      */
+  GM_BIPARTITE_CHECK = 32u /* PreprocessMode::BIPARTITE_CHECK (io.cpp:208-219): reject an edge whose
+                              source is a destination or destination a source; GM_EINPUT          */
 };
 /* With GM_RELABEL, GM_SHARDS(P) deals the degree-ordered vertices round-robin
  * over P equal contiguous row blocks (internal id = (k % P) * N/P + k / P for
@@ -178,6 +181,14 @@ typedef struct {
 GM_API gm_status gm_cf(gm_graph_t g, const gm_cf_config* cfg, const float* init_factors,
                        float* out_factors, double* rmse_trace, gm_iteration_stats* stats,
                        int64_t cap, int64_t* n_stats);
+
+/* algo::triangle_count (algorithms/triangle_count.hpp:115-134) on a DAG-form
+ * graph (every stored edge src < dst in caller ids; build with GM_DAGIFY):
+ * total triangles, and optionally TriangleState::local_count per vertex
+ * (host array of n, caller order): local[w] = sum over stored v -> w of
+ * |N_in(v) & N_in(w)|.  A stored edge with src >= dst is GM_EINPUT with the
+ * reference's message ("... violates src < dst; run DAGIFY preprocessing first"). */
+GM_API gm_status gm_triangle_count(gm_graph_t g, uint64_t* total, uint64_t* local_counts);
 
 /* ---- generic engine: any VertexProgram, exact reference semantics -------- */
 /* Built-in instantiations of the device-side VertexProgram template (see

@@ -17,6 +17,7 @@ GM_OK, GM_EUSAGE, GM_EINPUT, GM_EENGINE, GM_ECUDA, GM_ENCCL = range(6)
 GM_ID_U32, GM_ID_U64 = 0, 1
 GM_VAL_NONE, GM_VAL_F64, GM_VAL_F32, GM_VAL_U8, GM_VAL_I64, GM_VAL_U32 = range(6)
 GM_PREPROCESS, GM_SYMMETRIZE, GM_RELABEL, GM_NEED_FORWARD = 1, 2, 4, 8
+GM_DAGIFY, GM_BIPARTITE_CHECK = 16, 32
 
 EXPORTED = [
     "gm_last_error", "gm_version", "gm_graph_create", "gm_graph_generate_rmat",
@@ -26,6 +27,7 @@ EXPORTED = [
     "gm_run_graph_program", "gm_superstep_phases", "gm_balanced_row_boundaries",
     "gm_kernel_launches", "gm_graph_permutation", "gm_pagerank_shard_init",
     "gm_pagerank_shard_step", "gm_pagerank_shard_ranks", "gm_graph_csr",
+    "gm_triangle_count",
 ]
 
 
@@ -102,6 +104,7 @@ def load(path: str = LIB_PATH):
         "gm_balanced_row_boundaries": (C.c_int, [vp, u64, u64, vp]),
         "gm_kernel_launches": (C.c_uint64, []),
         "gm_graph_permutation": (C.c_int, [vp, vp]),
+        "gm_triangle_count": (C.c_int, [vp, C.POINTER(u64), vp]),
         "gm_graph_csr": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64),
                                    C.POINTER(u64)]),
         "gm_pagerank_shard_init": (C.c_int, [vp, u64, u64, vp, C.POINTER(dp)]),

@@ -4,7 +4,9 @@ Names, argument meaning and error behaviour follow semigraph (paths relative to
 /root/reference/proj):
 
 * ``Graph`` / ``build_graph``           include/semigraph/dcsc.hpp:183-274
-* ``preprocess`` flags                  src/io.cpp:184-222 (PREPROCESS / SYMMETRIZE)
+* ``preprocess`` flags / ``mode``       src/io.cpp:184-222 (PREPROCESS, SYMMETRIZE, DAGIFY,
+                                        BIPARTITE_CHECK)
+* ``triangle_count``                    include/semigraph/algorithms/triangle_count.hpp:115-134
 * ``run_graph_program``, phases         include/semigraph/engine.hpp:76-213
 * ``degree_vector``                     include/semigraph/engine.hpp:295-312
 * ``pagerank`` / ``bfs`` / ``sssp`` / ``collaborative_filtering_gd``
@@ -96,6 +98,10 @@ _CODE_OF_NP = {np.dtype(np.float64): L.GM_VAL_F64, np.dtype(np.float32): L.GM_VA
                np.dtype(np.uint32): L.GM_VAL_U32}
 
 
+_MODE_FLAGS = {"none": 0, "symmetrize": L.GM_SYMMETRIZE, "dagify": L.GM_DAGIFY,
+               "bipartite_check": L.GM_BIPARTITE_CHECK}
+
+
 class Graph:
     """A device-resident graph: CSR(G^T) (+ CSR(G) on demand) over internal ids."""
 
@@ -105,10 +111,13 @@ class Graph:
     # -- construction ------------------------------------------------------
     @classmethod
     def from_edges(cls, src, dst, num_vertices, values=None, *, value_type=None,
-                   preprocess=False, symmetrize=False, relabel=False, need_forward=False):
+                   preprocess=False, symmetrize=False, relabel=False, need_forward=False,
+                   mode=None):
         """build_graph (dcsc.hpp:243-274); with preprocess/symmetrize also
-        io::preprocess (io.cpp:184-222).  value_type: storage ('f64', 'f32',
-        'u8', 'i64', 'u32' or None to drop values)."""
+        io::preprocess (io.cpp:184-222).  mode: io::PreprocessMode by name --
+        "none", "symmetrize", "dagify", "bipartite_check" (implies preprocess).
+        value_type: storage ('f64', 'f32', 'u8', 'i64', 'u32' or None to drop
+        values)."""
         src = np.asarray(src)
         dst = np.asarray(dst)
         if src.shape != dst.shape:
@@ -141,20 +150,22 @@ class Graph:
                         vals_arr.ctypes.data if vals_arr is not None and vals_arr.size else None,
                         src.size, id_type, vt_in, 0, 0)
         flags = ((L.GM_PREPROCESS if preprocess else 0) | (L.GM_SYMMETRIZE if symmetrize else 0)
-                 | (L.GM_RELABEL if relabel else 0) | (L.GM_NEED_FORWARD if need_forward else 0))
+                 | (L.GM_RELABEL if relabel else 0) | (L.GM_NEED_FORWARD if need_forward else 0)
+                 | _MODE_FLAGS[mode or "none"])
         h = C.c_void_p()
         _check(L.load().gm_graph_create(C.byref(el), int(num_vertices), flags, storage, C.byref(h)))
         return cls(h.value)
 
     @classmethod
     def rmat(cls, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, *, permute=True,
-             symmetrize=False, relabel=True, weights=False, need_forward=False, shards=1):
+             symmetrize=False, relabel=True, weights=False, need_forward=False, shards=1,
+             mode=None):
         """Seeded R-MAT generated + ingested on the GPU (io::rmat_generate
         semantics, io.cpp:224-255; dedup + loop removal always on).  shards=P
         lays internal ids out as P nnz-balanced row blocks (GM_SHARDS)."""
         flags = (L.GM_PREPROCESS | (L.GM_SYMMETRIZE if symmetrize else 0)
                  | (L.GM_RELABEL if relabel else 0) | (L.GM_NEED_FORWARD if need_forward else 0)
-                 | ((int(shards) & 0xFF) << 16 if shards > 1 else 0))
+                 | ((int(shards) & 0xFF) << 16 if shards > 1 else 0) | _MODE_FLAGS[mode or "none"])
         h = C.c_void_p()
         _check(L.load().gm_graph_generate_rmat(scale, edge_factor, a, b, c, seed,
                                                1 if permute else 0, flags,
@@ -319,6 +330,17 @@ def sssp(g: Graph, source: int, max_iterations=None, *, with_stats=True, out=Non
     _check(L.load().gm_sssp(g._h, source, cap, ptr, on_dev, st if with_stats else None,
                             min(cap, 1 << 16), C.byref(k) if with_stats else None))
     return out, _stats(st, k.value) if with_stats else []
+
+
+def triangle_count(g: Graph, local=False):
+    """algo::triangle_count (triangle_count.hpp:115-134) on a DAG-form graph
+    (build with mode="dagify").  Returns the total, or (total, local_count
+    uint64[n] in caller order) with local=True."""
+    tot = C.c_uint64()
+    out = np.empty(g.num_vertices, np.uint64) if local else None
+    _check(L.load().gm_triangle_count(g._h, C.byref(tot),
+                                      out.ctypes.data if out is not None and out.size else None))
+    return (int(tot.value), out) if local else int(tot.value)
 
 
 def collaborative_filtering_gd(g: Graph, k=20, gamma=1e-3, lam=0.05, iterations=10, init=None):

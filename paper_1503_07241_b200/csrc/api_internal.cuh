@@ -28,6 +28,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
 std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters, uint32_t* out,
                                      bool out_on_device, bool collect_stats);
 // cf.cu
+uint64_t triangle_count(Graph& g, uint64_t* local_host);
 std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
                                    const float* init, float* out, double* rmse_trace);
 

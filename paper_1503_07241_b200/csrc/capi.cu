@@ -171,6 +171,13 @@ GM_API gm_status gm_cf(gm_graph_t g, const gm_cf_config* cfg, const float* init_
   });
 }
 
+GM_API gm_status gm_triangle_count(gm_graph_t g, uint64_t* total, uint64_t* local_counts) {
+  return guarded([&] {
+    if (!total) gm::fail(GM_EUSAGE, "null argument");
+    *total = gm::triangle_count(*handle(g), local_counts);
+  });
+}
+
 GM_API gm_status gm_program_sizes(int32_t program, size_t* vertex_bytes, size_t* message_bytes,
                                   size_t* reduced_bytes) {
   return guarded([&] { gm::program_sizes(program, vertex_bytes, message_bytes, reduced_bytes); });

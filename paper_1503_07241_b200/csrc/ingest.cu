@@ -120,6 +120,25 @@ __global__ void k_append_reverse(uint64_t* keys, uint32_t* idx, int64_t m, unsig
   }
 }
 
+// DAGIFY (io.cpp:206): keep src < dst.
+__global__ void k_dag_flags(const uint64_t* keys, int64_t m, unsigned nb, uint8_t* keep) {
+  const uint64_t mask = (uint64_t(1) << nb) - 1;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+       i += int64_t(gridDim.x) * blockDim.x)
+    keep[i] = (keys[i] >> nb) < (keys[i] & mask);
+}
+
+// BIPARTITE_CHECK (io.cpp:208-219): the first edge (sorted order) whose source
+// is some edge's destination or whose destination is some edge's source.
+__global__ void k_bipartite_first(const uint64_t* keys, int64_t m, unsigned nb,
+                                  const uint32_t* outdeg, const uint32_t* indeg,
+                                  unsigned long long* first) {
+  const uint64_t mask = (uint64_t(1) << nb) - 1;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (indeg[keys[i] >> nb] || outdeg[keys[i] & mask]) atomicMin(first, (unsigned long long)i);
+}
+
 __global__ void k_degrees(const uint64_t* keys, int64_t m, unsigned nb, uint32_t* outdeg,
                           uint32_t* indeg) {
   const uint64_t mask = (uint64_t(1) << nb) - 1;
@@ -416,7 +435,7 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
   cudaStream_t s = g.stream;
   const unsigned nb = g.nb;
   const int end_bit = int(2 * nb);
-  const bool pre = (g.flags & (GM_PREPROCESS | GM_SYMMETRIZE)) != 0;
+  const bool pre = (g.flags & (GM_PREPROCESS | GM_SYMMETRIZE | GM_DAGIFY | GM_BIPARTITE_CHECK)) != 0;
   const size_t vs = value_size(g.value_type);
   // The payload (input position of each edge, to carry its value through the
   // sorts) exists only when there are values: value-less graphs sort bare keys,
@@ -467,7 +486,7 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
     }
   };
   dedup(pre);
-  if (g.flags & GM_SYMMETRIZE) {
+  if (g.flags & (GM_SYMMETRIZE | GM_DAGIFY)) {
     DevBuf<uint64_t> k2(2 * m, s);
     DevBuf<uint32_t> i2(payload ? 2 * m : 0, s);
     if (m) {
@@ -485,6 +504,12 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
     i2.reset();
     m *= 2;
     dedup(true);
+    if (g.flags & GM_DAGIFY) {
+      DevBuf<uint8_t> keep(m, s);
+      launch(m, s, [&](unsigned gr, unsigned b) { k_dag_flags<<<gr, b, 0, s>>>(keys.get(), m, nb, keep.get()); });
+      if (payload) select_flagged(idx, keep.get(), m, s);
+      m = select_flagged(keys, keep.get(), m, s);
+    }
   }
   g.m = uint64_t(m);
 
@@ -496,6 +521,21 @@ void build(Graph& g, DevBuf<uint32_t>& s32, DevBuf<uint32_t>& d32, int64_t m,
   launch(m, s, [&](unsigned gr, unsigned b) {
     k_degrees<<<gr, b, 0, s>>>(keys.get(), m, nb, outdeg.get(), indeg.get());
   });
+  if (g.flags & GM_BIPARTITE_CHECK) {
+    DevBuf<unsigned long long> first(1, s);
+    GM_CUDA(cudaMemsetAsync(first.get(), 0xFF, sizeof(unsigned long long), s));
+    launch(m, s, [&](unsigned gr, unsigned b) {
+      k_bipartite_first<<<gr, b, 0, s>>>(keys.get(), m, nb, outdeg.get(), indeg.get(), first.get());
+    });
+    const uint64_t e = read_u64(first.get(), s);
+    if (e != ~0ull) {
+      uint64_t k = 0;
+      GM_CUDA(cudaMemcpy(&k, keys.get() + e, sizeof(k), cudaMemcpyDeviceToHost));
+      const uint64_t mask = (uint64_t(1) << nb) - 1;
+      fail(GM_EINPUT, "not bipartite: edge " + std::to_string((k >> nb) + 1) + " -> " +
+                          std::to_string((k & mask) + 1) + " (1-based) mixes the user and item sides");
+    }
+  }
 
   // Relabel: internal id = rank by (out-degree desc, caller id asc).
   if (g.flags & GM_RELABEL) {
@@ -559,13 +599,17 @@ Graph* new_graph(uint64_t n, uint32_t flags, int storage) {
   if (shards > 1 && n % shards != 0)
     fail(GM_EUSAGE, "GM_SHARDS(" + std::to_string(shards) + "): vertex count " + std::to_string(n) +
                         " is not a multiple of the shard count");
+  if ((flags & GM_SYMMETRIZE) && (flags & (GM_DAGIFY | GM_BIPARTITE_CHECK)))
+    fail(GM_EUSAGE, "SYMMETRIZE, DAGIFY and BIPARTITE_CHECK are exclusive preprocessing modes");
+  if ((flags & GM_DAGIFY) && (flags & GM_BIPARTITE_CHECK))
+    fail(GM_EUSAGE, "SYMMETRIZE, DAGIFY and BIPARTITE_CHECK are exclusive preprocessing modes");
   auto* g = new Graph();
   g->shards = shards;
   GM_CUDA(cudaGetDevice(&g->device));
   GM_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
   g->n = n;
   g->flags = flags;
-  if (flags & GM_SYMMETRIZE) g->flags |= GM_PREPROCESS;
+  if (flags & (GM_SYMMETRIZE | GM_DAGIFY | GM_BIPARTITE_CHECK)) g->flags |= GM_PREPROCESS;
   g->symmetric = (flags & GM_SYMMETRIZE) != 0;
   g->value_type = storage;
   g->nb = bits_for(n);

@@ -400,6 +400,53 @@ class SsspWorkload(Workload):
                 "sample": "one SSSP from the same source on the full graph (build excluded)"}
 
 
+class TcWorkload(Workload):
+    """triangle counting on the DAGIFY'd R-MAT graph (not a
+    BASELINE config; measured like one).  One step = one full count."""
+    name = "tc"
+    dtype = "uint64"
+
+    def build(self, gm):
+        a = self.args
+        t0 = time.perf_counter()
+        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, relabel=False, mode="dagify", **RMAT)
+        self.ingest_s = time.perf_counter() - t0
+        self.n = 1 << a.scale
+        self.m = self.g.num_edges
+        self.edges = self.m
+        self.total = gm.triangle_count(self.g)
+        self.config = {"workload": f"tc_rmat{a.scale}_dag", "scale": a.scale, "edge_factor": 16,
+                       "n": self.n, "m": self.m, "triangles": self.total,
+                       "teps": "stored DAG edges / count time",
+                       "l2": "inputs larger than L2" if not self.flush_l2()
+                       else "L2 flushed between steps (256 MB write, outside the events)"}
+
+    def run_device(self, gm):
+        gm.triangle_count(self.g)
+
+    def run_e2e(self, gm):
+        return gm.triangle_count(self.g)
+
+    def e2e_bytes(self):
+        return 0, 8
+
+    def per_superstep(self, gm):
+        return []
+
+    def cpu_baseline(self, orc):
+        s, d, _ = self.g.edges()
+        R = orc.ref_lib()
+        t0 = time.perf_counter()
+        tot, _ = orc.ref_triangle_count(self.n, s, d, threads=0, parts=8 * int(R.ref_hardware_threads()))
+        secs = time.perf_counter() - t0
+        assert tot == self.total, (tot, self.total)
+        return {"value": round(self.edges / secs / 1e9, 6), "unit": "GTEPS",
+                "cores": int(R.ref_hardware_threads()), "kind": "reference",
+                "seconds": round(secs, 4),
+                "sample": "one full count on the same DAG graph (build included: the reference "
+                          "API builds inside triangle_count's caller)"}
+
+
 class CfWorkload(Workload):
     name = "cf"
     dtype = "f32"
@@ -440,7 +487,9 @@ WORKLOADS = {"bfs": (BfsWorkload, 23), "pagerank": (PageRankWorkload, 20),
              "pagerank23": (PageRankWorkload, 23), "sssp": (SsspWorkload, 23),
              "cf": (CfWorkload, 0),
              # BASELINE configs[4] (scale 28) on one GPU / sharded over N
-             "bfs28": (BfsWorkload, 28), "pagerank28": (PageRankWorkload, 28)}
+             "bfs28": (BfsWorkload, 28), "pagerank28": (PageRankWorkload, 28),
+             # SURVEY 8f row 2 (not a BASELINE config)
+             "tc": (TcWorkload, 20)}
 # The reference engine cannot hold scale >= 26 in host memory.
 CPU_MAX_SCALE = 25
 
@@ -602,6 +651,16 @@ def run_reference(args, d: Dist):
             return rg.run_pagerank(0.85, 20)[1]
         config = {"workload": f"pagerank_rmat{scale}", "scale": scale, "n": n, "m": len(s),
                   "iterations": 20}
+    elif args.workload == "tc":
+        s, dd, _ = oracle.preprocess(s, dd, mode="dagify")
+        gen_s = time.perf_counter() - t0
+        edges = len(s)
+
+        def step():
+            t = time.perf_counter()
+            oracle.ref_triangle_count(n, s, dd, threads=0, parts=8 * cores)
+            return time.perf_counter() - t
+        config = {"workload": f"tc_rmat{scale}_dag", "scale": scale, "n": n, "m": len(s)}
     else:
         print(json.dumps({"impl": "reference", "unavailable":
                           f"--impl reference not wired for workload {args.workload}"}))

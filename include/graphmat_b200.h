@@ -190,6 +190,53 @@ GM_API gm_status gm_cf(gm_graph_t g, const gm_cf_config* cfg, const float* init_
  * reference's message ("... violates src < dst; run DAGIFY preprocessing first"). */
 GM_API gm_status gm_triangle_count(gm_graph_t g, uint64_t* total, uint64_t* local_counts);
 
+/* ---- files: the reference's formats (src/io.cpp, src/report.cpp) --------- */
+/* Host-side edge buffer: caller ids (0-based) as u64, values as f64 (1.0 for
+ * unweighted inputs), num_vertices as the reference's EdgeList reports it. */
+typedef struct gm_edges_s* gm_edges_t;
+/* io::load_edge_list (io.cpp:85-110): "src dst [weight]" lines, 1-based ids,
+ * '#'/'%' comments; InputError messages carry path:line. */
+GM_API gm_status gm_edges_load_text(const char* path, int32_t weighted, gm_edges_t* out);
+/* io::load_matrix_market (io.cpp:112-182): coordinate real|pattern|integer,
+ * general|symmetric (symmetric entries expanded, diagonal once). */
+GM_API gm_status gm_edges_load_matrix_market(const char* path, gm_edges_t* out);
+/* io::read_binary (io.cpp:317-362): "GMB1", n, m, then (src, dst, value) u64/u64/f64 LE. */
+GM_API gm_status gm_edges_read_binary(const char* path, gm_edges_t* out);
+/* Borrowed views into the buffer (valid until gm_edges_free). */
+GM_API gm_status gm_edges_view(gm_edges_t e, uint64_t* num_vertices, uint64_t* num_edges,
+                               const uint64_t** src, const uint64_t** dst, const double** values);
+GM_API gm_status gm_edges_free(gm_edges_t e);
+/* io::write_binary (io.cpp:290-315); values may be null (1.0). */
+GM_API gm_status gm_edges_write_binary(const char* path, const uint64_t* src, const uint64_t* dst,
+                                       const double* values, uint64_t num_edges,
+                                       uint64_t num_vertices);
+/* io::write_edge_list (io.cpp:364-373): 1-based "src dst %.17g" lines. */
+GM_API gm_status gm_edges_write_text(const char* path, const uint64_t* src, const uint64_t* dst,
+                                     const double* values, uint64_t num_edges);
+/* bench::write_results / write_vector_results (report.cpp:53-75): one
+ * "v<TAB>x[<TAB>x...]" line per vertex, 1-based, %.17g. rows: n*k row-major. */
+GM_API gm_status gm_write_results(const char* path, const double* values, uint64_t n);
+GM_API gm_status gm_write_vector_results(const char* path, const double* rows, uint64_t n,
+                                         uint64_t k);
+/* bench::RunReport (report.hpp:13-24) and write_report (report.cpp:77-102). */
+typedef struct {
+  const char* algorithm;
+  const char* graph;
+  uint32_t threads;
+  uint64_t partitions;
+  const double* iteration_seconds; /* IterationStats::total_seconds per superstep */
+  uint64_t n_iterations;
+  double total_seconds;
+  uint64_t checksum;               /* FNV-1a 64 of the results file */
+  const char* const* extra_keys;
+  const char* const* extra_values;
+  uint64_t n_extras;
+} gm_run_report;
+GM_API gm_status gm_write_report(const char* path, const gm_run_report* report);
+/* bench::fnv1a64 / fnv1a64_file (report.cpp:27-51). */
+GM_API uint64_t gm_fnv1a64(const void* data, uint64_t size);
+GM_API gm_status gm_fnv1a64_file(const char* path, uint64_t* out);
+
 /* ---- generic engine: any VertexProgram, exact reference semantics -------- */
 /* Built-in instantiations of the device-side VertexProgram template (see
  * paper_1503_07241_b200/csrc/engine.cuh).  Fold order per row is ascending

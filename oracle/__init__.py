@@ -147,8 +147,18 @@ def ref_lib():
                                               C.c_void_p, C.POINTER(C.c_double)]
     R.ref_preprocess.argtypes = [C.c_int64, u32p, u32p, C.c_void_p, C.c_int]
     R.ref_preprocess.restype = C.c_int64
+    cp = C.c_char_p
+    R.ref_io_load_to_binary.argtypes = [C.c_int, cp, cp]
+    R.ref_io_write_edge_list.argtypes = [cp, cp]
+    R.ref_io_write_results.argtypes = [cp, f64p, C.c_uint64]
+    R.ref_io_write_vector_results.argtypes = [cp, f64p, C.c_uint64, C.c_uint64]
+    R.ref_io_write_report.argtypes = [cp, cp, cp, C.c_uint, C.c_uint64, C.c_void_p, C.c_uint64,
+                                      C.c_double, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]
+    R.ref_io_fnv1a64_file.argtypes = [cp, C.POINTER(C.c_uint64)]
     for f in (R.ref_bfs, R.ref_sssp, R.ref_pagerank, R.ref_pagerank_norm, R.ref_cf,
-              R.ref_semiring_spmv, R.ref_triangle_count):
+              R.ref_semiring_spmv, R.ref_triangle_count, R.ref_io_load_to_binary,
+              R.ref_io_write_edge_list, R.ref_io_write_results, R.ref_io_write_vector_results,
+              R.ref_io_write_report, R.ref_io_fnv1a64_file):
         f.restype = C.c_int
     _REF = R
     return R
@@ -472,6 +482,68 @@ def ref_preprocess(src, dst, vals=None, mode="none"):
     if k < 0:
         raise OracleInputError(R.ref_last_error().decode())
     return s[:k].copy(), d[:k].copy(), (v[:k].copy() if v is not None else None)
+
+
+# ---- files (src/io.cpp, src/report.cpp) through the compiled reference ----
+
+def gmb1_parse(path):
+    """Independent numpy reader of the GMB1 layout (io.hpp: magic, n, m, then
+    little-endian u64 src, u64 dst, f64 value per edge)."""
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"GMB1"
+    n, m = np.frombuffer(raw[4:20], "<u8")
+    rec = np.frombuffer(raw[20:], dtype=[("s", "<u8"), ("d", "<u8"), ("v", "<f8")])
+    assert len(rec) == m
+    return rec["s"].copy(), rec["d"].copy(), rec["v"].copy(), int(n)
+
+
+def gmb1_write(path, src, dst, vals, n):
+    rec = np.empty(len(src), dtype=[("s", "<u8"), ("d", "<u8"), ("v", "<f8")])
+    rec["s"], rec["d"], rec["v"] = src, dst, vals
+    with open(path, "wb") as f:
+        f.write(b"GMB1" + np.array([n, len(src)], "<u8").tobytes() + rec.tobytes())
+
+
+def ref_io_load(kind, path, tmp_out):
+    """The reference loader (kind: text | text-weighted | mm | binary) -> (src,
+    dst, values, num_vertices); OracleInputError carries its message."""
+    R = ref_lib()
+    k = {"text": 0, "text-weighted": 1, "mm": 2, "binary": 3}[kind]
+    if R.ref_io_load_to_binary(k, os.fsencode(path), os.fsencode(tmp_out)) != 0:
+        raise OracleInputError(R.ref_last_error().decode())
+    return gmb1_parse(tmp_out)
+
+
+def ref_io_write_edge_list(src, dst, vals, n, tmp_gmb1, out_path):
+    gmb1_write(tmp_gmb1, src, dst, vals, n)
+    _ref_call(ref_lib().ref_io_write_edge_list, os.fsencode(tmp_gmb1), os.fsencode(out_path))
+
+
+def ref_io_write_results(path, values):
+    v = np.ascontiguousarray(values, np.float64)
+    _ref_call(ref_lib().ref_io_write_results, os.fsencode(path), v, len(v))
+
+
+def ref_io_write_vector_results(path, rows):
+    r = np.ascontiguousarray(rows, np.float64)
+    _ref_call(ref_lib().ref_io_write_vector_results, os.fsencode(path), r.reshape(-1),
+              r.shape[0], r.shape[1])
+
+
+def ref_io_write_report(path, algorithm, graph, threads, partitions, iteration_seconds,
+                        total_seconds, checksum, extras):
+    it = np.ascontiguousarray(iteration_seconds, np.float64)
+    keys = (C.c_char_p * max(len(extras), 1))(*[k.encode() for k, _ in extras])
+    vals = (C.c_char_p * max(len(extras), 1))(*[str(v).encode() for _, v in extras])
+    _ref_call(ref_lib().ref_io_write_report, os.fsencode(path), algorithm.encode(), graph.encode(),
+              threads, partitions, it.ctypes.data, len(it), total_seconds, checksum, keys, vals,
+              len(extras))
+
+
+def ref_io_fnv1a64_file(path):
+    out = C.c_uint64()
+    _ref_call(ref_lib().ref_io_fnv1a64_file, os.fsencode(path), C.byref(out))
+    return int(out.value)
 
 
 class RefGraph:

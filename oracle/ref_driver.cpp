@@ -15,6 +15,7 @@
 //   collaborative_filtering_gd include/semigraph/algorithms/collaborative_filtering.hpp:134-211
 //   algo::triangle_count      include/semigraph/algorithms/triangle_count.hpp:115-134
 //   io::preprocess            src/io.cpp:184-222 (compiled from the reference tree with it)
+//   io loaders / writers      src/io.cpp:85-373, bench:: report writers src/report.cpp
 // The one new program is the BASELINE-normalised PageRank, which
 // BASELINE configs[0] needs and the reference does not ship; it is driven
 // through the reference engine phases exactly like the CF driver does.
@@ -33,6 +34,7 @@
 #include "semigraph/algorithms/triangle_count.hpp"
 #include "semigraph/engine.hpp"
 #include "semigraph/io.hpp"
+#include "semigraph/report.hpp"
 
 using namespace semigraph;
 
@@ -471,6 +473,59 @@ int ref_triangle_count(uint64_t n, int64_t m, const uint32_t* src, const uint32_
       for (VertexId v = 0; v < n; ++v) local[v] = props[v].local_count;
     }
   });
+}
+
+// ---- files: run the reference's loader (kind 0 text, 1 text weighted,
+// 2 Matrix Market, 3 GMB1) and re-emit what it parsed as GMB1 with the
+// reference's own writer, so tests compare parsed edge lists exactly.
+int ref_io_load_to_binary(int kind, const char* path, const char* out_gmb1) {
+  return guarded([&] {
+    io::EdgeList e = kind == 0   ? io::load_edge_list(path, false)
+                     : kind == 1 ? io::load_edge_list(path, true)
+                     : kind == 2 ? io::load_matrix_market(path)
+                                 : io::read_binary(path);
+    io::write_binary(out_gmb1, e.edges, e.num_vertices);
+  });
+}
+
+// io::write_edge_list of a GMB1 file's edges.
+int ref_io_write_edge_list(const char* in_gmb1, const char* out_path) {
+  return guarded([&] { io::write_edge_list(out_path, io::read_binary(in_gmb1).edges); });
+}
+
+int ref_io_write_results(const char* path, const double* values, uint64_t n) {
+  return guarded([&] { bench::write_results(path, std::vector<double>(values, values + n)); });
+}
+
+int ref_io_write_vector_results(const char* path, const double* rows, uint64_t n, uint64_t k) {
+  return guarded([&] {
+    std::vector<std::vector<double>> r(n);
+    for (uint64_t v = 0; v < n; ++v) r[v].assign(rows + v * k, rows + (v + 1) * k);
+    bench::write_vector_results(path, r);
+  });
+}
+
+int ref_io_write_report(const char* path, const char* algorithm, const char* graph,
+                        unsigned threads, uint64_t partitions, const double* iter_seconds,
+                        uint64_t n_iter, double total_seconds, uint64_t checksum,
+                        const char* const* keys, const char* const* values, uint64_t n_extras) {
+  return guarded([&] {
+    bench::RunReport r;
+    r.algorithm = algorithm;
+    r.graph = graph;
+    r.threads = threads;
+    r.partitions = partitions;
+    r.iterations.resize(n_iter);
+    for (uint64_t i = 0; i < n_iter; ++i) r.iterations[i].total_seconds = iter_seconds[i];
+    r.total_seconds = total_seconds;
+    r.checksum = checksum;
+    for (uint64_t i = 0; i < n_extras; ++i) r.extras.emplace_back(keys[i], values[i]);
+    bench::write_report(path, r);
+  });
+}
+
+int ref_io_fnv1a64_file(const char* path, uint64_t* out) {
+  return guarded([&] { *out = bench::fnv1a64_file(path); });
 }
 
 }  // extern "C"

@@ -27,7 +27,10 @@ EXPORTED = [
     "gm_run_graph_program", "gm_superstep_phases", "gm_balanced_row_boundaries",
     "gm_kernel_launches", "gm_graph_permutation", "gm_pagerank_shard_init",
     "gm_pagerank_shard_step", "gm_pagerank_shard_ranks", "gm_graph_csr",
-    "gm_triangle_count",
+    "gm_triangle_count", "gm_edges_load_text", "gm_edges_load_matrix_market",
+    "gm_edges_read_binary", "gm_edges_view", "gm_edges_free", "gm_edges_write_binary",
+    "gm_edges_write_text", "gm_write_results", "gm_write_vector_results", "gm_write_report",
+    "gm_fnv1a64", "gm_fnv1a64_file",
 ]
 
 
@@ -51,6 +54,16 @@ class GraphInfo(C.Structure):
     _fields_ = [("num_vertices", C.c_uint64), ("num_edges", C.c_uint64), ("flags", C.c_uint32),
                 ("value_type", C.c_int32), ("forward_built", C.c_int32), ("device", C.c_int32),
                 ("device_bytes", C.c_uint64), ("nonzero_out_degree", C.c_uint64)]
+
+
+class RunReportC(C.Structure):
+    """gm_run_report: bench::RunReport (report.hpp:13-24)."""
+
+    _fields_ = [("algorithm", C.c_char_p), ("graph", C.c_char_p), ("threads", C.c_uint32),
+                ("partitions", C.c_uint64), ("iteration_seconds", C.POINTER(C.c_double)),
+                ("n_iterations", C.c_uint64), ("total_seconds", C.c_double),
+                ("checksum", C.c_uint64), ("extra_keys", C.POINTER(C.c_char_p)),
+                ("extra_values", C.POINTER(C.c_char_p)), ("n_extras", C.c_uint64)]
 
 
 class PageRankConfig(C.Structure):
@@ -105,6 +118,19 @@ def load(path: str = LIB_PATH):
         "gm_kernel_launches": (C.c_uint64, []),
         "gm_graph_permutation": (C.c_int, [vp, vp]),
         "gm_triangle_count": (C.c_int, [vp, C.POINTER(u64), vp]),
+        "gm_edges_load_text": (C.c_int, [C.c_char_p, i32, C.POINTER(vp)]),
+        "gm_edges_load_matrix_market": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+        "gm_edges_read_binary": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+        "gm_edges_view": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(vp),
+                                    C.POINTER(vp), C.POINTER(vp)]),
+        "gm_edges_free": (C.c_int, [vp]),
+        "gm_edges_write_binary": (C.c_int, [C.c_char_p, vp, vp, vp, u64, u64]),
+        "gm_edges_write_text": (C.c_int, [C.c_char_p, vp, vp, vp, u64]),
+        "gm_write_results": (C.c_int, [C.c_char_p, vp, u64]),
+        "gm_write_vector_results": (C.c_int, [C.c_char_p, vp, u64, u64]),
+        "gm_write_report": (C.c_int, [C.c_char_p, C.POINTER(RunReportC)]),
+        "gm_fnv1a64": (u64, [vp, u64]),
+        "gm_fnv1a64_file": (C.c_int, [C.c_char_p, C.POINTER(u64)]),
         "gm_graph_csr": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64),
                                    C.POINTER(u64)]),
         "gm_pagerank_shard_init": (C.c_int, [vp, u64, u64, vp, C.POINTER(dp)]),

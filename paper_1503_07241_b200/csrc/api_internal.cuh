@@ -29,6 +29,27 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
                                      bool out_on_device, bool collect_stats);
 // cf.cu
 uint64_t triangle_count(Graph& g, uint64_t* local_host);
+
+// Files (gmio.cu): the reference's formats, host side.
+struct EdgeBuffer {
+  std::vector<uint64_t> src, dst;
+  std::vector<double> val;
+  uint64_t num_vertices = 0;
+};
+namespace io {
+EdgeBuffer load_edge_list(const std::string& path, bool weighted);
+EdgeBuffer load_matrix_market(const std::string& path);
+EdgeBuffer read_binary(const std::string& path);
+void write_binary(const std::string& path, const uint64_t* src, const uint64_t* dst,
+                  const double* val, uint64_t m, uint64_t n);
+void write_edge_list(const std::string& path, const uint64_t* src, const uint64_t* dst,
+                     const double* val, uint64_t m);
+void write_results(const std::string& path, const double* values, uint64_t n);
+void write_vector_results(const std::string& path, const double* rows, uint64_t n, uint64_t k);
+void write_report(const std::string& path, const gm_run_report& r);
+uint64_t fnv1a64(const void* data, uint64_t size);
+uint64_t fnv1a64_file(const std::string& path);
+}  // namespace io
 std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
                                    const float* init, float* out, double* rmse_trace);
 

@@ -178,6 +178,97 @@ GM_API gm_status gm_triangle_count(gm_graph_t g, uint64_t* total, uint64_t* loca
   });
 }
 
+GM_API gm_status gm_edges_load_text(const char* path, int32_t weighted, gm_edges_t* out) {
+  return guarded([&] {
+    if (!path || !out) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_edges_t>(new gm::EdgeBuffer(gm::io::load_edge_list(path, weighted != 0)));
+  });
+}
+
+GM_API gm_status gm_edges_load_matrix_market(const char* path, gm_edges_t* out) {
+  return guarded([&] {
+    if (!path || !out) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_edges_t>(new gm::EdgeBuffer(gm::io::load_matrix_market(path)));
+  });
+}
+
+GM_API gm_status gm_edges_read_binary(const char* path, gm_edges_t* out) {
+  return guarded([&] {
+    if (!path || !out) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_edges_t>(new gm::EdgeBuffer(gm::io::read_binary(path)));
+  });
+}
+
+GM_API gm_status gm_edges_view(gm_edges_t e, uint64_t* num_vertices, uint64_t* num_edges,
+                               const uint64_t** src, const uint64_t** dst, const double** values) {
+  return guarded([&] {
+    if (!e) gm::fail(GM_EUSAGE, "null edge buffer");
+    const auto* b = reinterpret_cast<const gm::EdgeBuffer*>(e);
+    if (num_vertices) *num_vertices = b->num_vertices;
+    if (num_edges) *num_edges = b->src.size();
+    if (src) *src = b->src.data();
+    if (dst) *dst = b->dst.data();
+    if (values) *values = b->val.data();
+  });
+}
+
+GM_API gm_status gm_edges_free(gm_edges_t e) {
+  return guarded([&] { delete reinterpret_cast<gm::EdgeBuffer*>(e); });
+}
+
+GM_API gm_status gm_edges_write_binary(const char* path, const uint64_t* src, const uint64_t* dst,
+                                       const double* values, uint64_t num_edges,
+                                       uint64_t num_vertices) {
+  return guarded([&] {
+    if (!path || (num_edges && (!src || !dst))) gm::fail(GM_EUSAGE, "null argument");
+    gm::io::write_binary(path, src, dst, values, num_edges, num_vertices);
+  });
+}
+
+GM_API gm_status gm_edges_write_text(const char* path, const uint64_t* src, const uint64_t* dst,
+                                     const double* values, uint64_t num_edges) {
+  return guarded([&] {
+    if (!path || (num_edges && (!src || !dst))) gm::fail(GM_EUSAGE, "null argument");
+    gm::io::write_edge_list(path, src, dst, values, num_edges);
+  });
+}
+
+GM_API gm_status gm_write_results(const char* path, const double* values, uint64_t n) {
+  return guarded([&] {
+    if (!path || (n && !values)) gm::fail(GM_EUSAGE, "null argument");
+    gm::io::write_results(path, values, n);
+  });
+}
+
+GM_API gm_status gm_write_vector_results(const char* path, const double* rows, uint64_t n,
+                                         uint64_t k) {
+  return guarded([&] {
+    if (!path || (n && k && !rows)) gm::fail(GM_EUSAGE, "null argument");
+    gm::io::write_vector_results(path, rows, n, k);
+  });
+}
+
+GM_API gm_status gm_write_report(const char* path, const gm_run_report* report) {
+  return guarded([&] {
+    if (!path || !report) gm::fail(GM_EUSAGE, "null argument");
+    if ((report->n_iterations && !report->iteration_seconds) ||
+        (report->n_extras && (!report->extra_keys || !report->extra_values)))
+      gm::fail(GM_EUSAGE, "null report arrays");
+    gm::io::write_report(path, *report);
+  });
+}
+
+GM_API uint64_t gm_fnv1a64(const void* data, uint64_t size) {
+  return gm::io::fnv1a64(data, data ? size : 0);
+}
+
+GM_API gm_status gm_fnv1a64_file(const char* path, uint64_t* out) {
+  return guarded([&] {
+    if (!path || !out) gm::fail(GM_EUSAGE, "null argument");
+    *out = gm::io::fnv1a64_file(path);
+  });
+}
+
 GM_API gm_status gm_program_sizes(int32_t program, size_t* vertex_bytes, size_t* message_bytes,
                                   size_t* reduced_bytes) {
   return guarded([&] { gm::program_sizes(program, vertex_bytes, message_bytes, reduced_bytes); });

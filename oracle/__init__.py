@@ -155,6 +155,9 @@ def ref_lib():
     R.ref_io_write_report.argtypes = [cp, cp, cp, C.c_uint, C.c_uint64, C.c_void_p, C.c_uint64,
                                       C.c_double, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]
     R.ref_io_fnv1a64_file.argtypes = [cp, C.POINTER(C.c_uint64)]
+    R.ref_run_one.argtypes = [cp, cp, cp, C.c_int, C.c_uint64, C.c_int64, C.c_double, C.c_uint,
+                              cp, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+    R.ref_run_one.restype = C.c_int
     for f in (R.ref_bfs, R.ref_sssp, R.ref_pagerank, R.ref_pagerank_norm, R.ref_cf,
               R.ref_semiring_spmv, R.ref_triangle_count, R.ref_io_load_to_binary,
               R.ref_io_write_edge_list, R.ref_io_write_results, R.ref_io_write_vector_results,
@@ -538,6 +541,19 @@ def ref_io_write_report(path, algorithm, graph, threads, partitions, iteration_s
     _ref_call(ref_lib().ref_io_write_report, os.fsencode(path), algorithm.encode(), graph.encode(),
               threads, partitions, it.ctypes.data, len(it), total_seconds, checksum, keys, vals,
               len(extras))
+
+
+def ref_run_one(algorithm, graph_path, out_path, fmt="edgelist", weighted=False, source=1,
+                max_iters=-1, damping=0.15, threads=0):
+    """The reference CLI's run composition (tools/sgraph.cpp:104-183) through the
+    reference library; returns the results file's FNV-1a checksum."""
+    R = ref_lib()
+    ck = C.c_uint64()
+    tot = C.c_double()
+    _ref_call(R.ref_run_one, algorithm.encode(), os.fsencode(graph_path), fmt.encode(),
+              1 if weighted else 0, source, max_iters, damping, threads, os.fsencode(out_path),
+              C.byref(ck), C.byref(tot))
+    return int(ck.value)
 
 
 def ref_io_fnv1a64_file(path):

@@ -528,4 +528,54 @@ int ref_io_fnv1a64_file(const char* path, uint64_t* out) {
   return guarded([&] { *out = bench::fnv1a64_file(path); });
 }
 
+// The reference CLI's "run" composition (tools/sgraph.cpp:104-183) over the
+// reference library API -- the CLI binary itself needs the absent CLI11.  Writes
+// the results file and returns its FNV-1a checksum (report.checksum).
+int ref_run_one(const char* algorithm, const char* graph_path, const char* format, int weighted,
+                uint64_t source, int64_t max_iters, double damping, unsigned threads,
+                const char* out_path, uint64_t* checksum, double* total_out) {
+  return guarded([&] {
+    const std::string algo_name = algorithm, fmt = format;
+    io::EdgeList input = fmt == "mtx"   ? io::load_matrix_market(graph_path)
+                         : fmt == "bin" ? io::read_binary(graph_path)
+                                        : io::load_edge_list(graph_path, weighted != 0);
+    const io::PreprocessMode mode = algo_name == "bfs"  ? io::PreprocessMode::SYMMETRIZE
+                                    : algo_name == "tc" ? io::PreprocessMode::DAGIFY
+                                                        : io::PreprocessMode::NONE;
+    auto edges = io::preprocess(std::move(input.edges), mode);
+    const std::size_t n = input.num_vertices;
+    threads = resolve_threads(threads);
+    const std::size_t parts = std::size_t(threads) * 8;
+    EngineConfig ec;
+    ec.thread_count = threads;
+    if (algo_name == "pagerank") {
+      auto g = build_graph<algo::PageRankState, double>(edges, n, parts);
+      Engine eng(ec);
+      algo::PageRankConfig pc;
+      pc.r = damping;
+      pc.max_iterations = max_iters < 0 ? 100 : std::size_t(max_iters);
+      bench::write_results(out_path, algo::pagerank(g, eng, pc));
+    } else if (algo_name == "bfs" || algo_name == "sssp") {
+      auto g = build_graph<algo::DistanceState, double>(edges, n, parts);
+      const std::size_t budget = max_iters < 0 ? std::max<std::size_t>(n, 1) : std::size_t(max_iters);
+      ec.max_iterations = budget == 0 ? 1 : budget;
+      Engine eng(ec);
+      const VertexId root = source - 1;
+      bench::write_results(out_path, algo_name == "bfs" ? algo::bfs(g, eng, root)
+                                                        : algo::sssp(g, eng, root));
+    } else if (algo_name == "tc") {
+      auto g = build_graph<algo::TriangleState, double>(edges, n, parts);
+      Engine eng(ec);
+      const std::uint64_t total = algo::triangle_count(g, eng);
+      std::vector<double> per(n);
+      for (VertexId v = 0; v < n; ++v) per[v] = static_cast<double>(g.properties()[v].local_count);
+      bench::write_results(out_path, per);
+      if (total_out) *total_out = static_cast<double>(total);
+    } else {
+      throw InputError("ref_run_one: unsupported algorithm " + algo_name);
+    }
+    *checksum = bench::fnv1a64_file(out_path);
+  });
+}
+
 }  // extern "C"

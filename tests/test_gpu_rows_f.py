@@ -106,3 +106,32 @@ def test_triangle_rmat(gm, orc):
     tot, local = gm.triangle_count(g, local=True)
     assert tot == want and want > 0
     assert np.array_equal(local, wl)
+
+
+# ---- the CLI "run" pipeline: result files and checksums vs the reference ----
+
+@pytest.mark.parametrize("algorithm", ["bfs", "sssp", "pagerank", "tc"])
+def test_run_pipeline_results_byte_identical(gm, orc, tmp_path, algorithm):
+    if orc.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    from paper_1503_07241_b200 import files as F
+    from paper_1503_07241_b200.run import run_one
+    rng = np.random.default_rng(11)
+    n, m = 3000, 24000
+    s = rng.integers(0, n, m).astype(np.uint64)
+    d = rng.integers(0, n, m).astype(np.uint64)
+    w = rng.integers(1, 100, m).astype(np.float64) / 4.0
+    graph = str(tmp_path / "g.txt")
+    weighted = algorithm == "sssp"
+    F.write_edge_list(graph, s, d, w if weighted else None)
+    if not weighted:  # unweighted file: two columns
+        with open(graph, "w") as f:
+            f.write("".join(f"{a + 1} {b + 1}\n" for a, b in zip(s, d)))
+    ours, theirs = str(tmp_path / "ours.tsv"), str(tmp_path / "ref.tsv")
+    rep = str(tmp_path / "report.txt")
+    kw = dict(weighted=weighted, source=7, max_iters=30 if algorithm == "pagerank" else -1)
+    run_one(algorithm, graph, ours, rep, **kw)
+    ck = orc.ref_run_one(algorithm, graph, theirs, weighted=weighted, source=7,
+                         max_iters=kw["max_iters"])
+    assert open(ours, "rb").read() == open(theirs, "rb").read()
+    assert f"checksum={ck:016x}\n" in open(rep).read()

@@ -466,7 +466,14 @@ class CfWorkload(Workload):
                        "iterations": 10}
 
     def run_device(self, gm):
-        gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters, init=self.init)
+        # factors resident in HBM (caller order), as every other workload's inputs
+        if not hasattr(self, "dev_init"):
+            import torch
+            self.dev_init = torch.from_numpy(self.init).cuda()
+            self.dev_out = torch.empty_like(self.dev_init)
+        gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters,
+                                      init_device_ptr=self.dev_init.data_ptr(),
+                                      out_device_ptr=self.dev_out.data_ptr())
 
     def run_e2e(self, gm):
         return gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters,
@@ -479,8 +486,47 @@ class CfWorkload(Workload):
         return gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters,
                                              init=self.init)[2]
 
+    def roofline(self, st, peak, peak_kind):
+        """CF sits near the FP32 ridge -> report max(bytes/BW, flops/FP32)."""
+        if not st:
+            return None
+        import paper_1503_07241_b200 as gm
+        t = statistics.median([s.spmv_seconds for s in st])
+        b = st[0].bytes_algorithmic
+        flops = 160 * self.m
+        fp32 = gm.measure_fp32_fma()
+        gbs, tfl = b / t / 1e9, flops / t / 1e12
+        f_mem, f_fp = gbs / peak, tfl / fp32
+        bound = "hbm" if f_mem >= f_fp else "fp32"
+        traffic, src = ncu_traffic("k_cf_items", self.config["workload"])
+        return {"bound": bound, "kernel": "cf superstep (k_cf_items x2 + k_cf_apply)",
+                "achieved": round(gbs if bound == "hbm" else tfl, 2), "unit": "GB/s" if bound == "hbm"
+                else "TFLOP/s", "peak": peak if bound == "hbm" else round(fp32, 2),
+                "peak_kind": peak_kind if bound == "hbm" else "measured (FMA probe, this run)",
+                "frac": round(max(f_mem, f_fp), 4), "frac_hbm": round(f_mem, 4),
+                "frac_fp32": round(f_fp, 4), "achieved_gbs": round(gbs, 1),
+                "achieved_tflops": round(tfl, 3), "fp32_peak_tflops": round(fp32, 2),
+                "bytes_per_launch": b, "flops_per_launch": flops,
+                "launch_us": round(t * 1e6, 2), "traffic": traffic, "traffic_source": src}
+
     def cpu_baseline(self, orc):
-        return None
+        """Bounded sample: one superstep of the reference CF on the ratings of the
+        first 1/8 of the users (the CF reduced-size parity case)."""
+        s, d, r = self.g.edges()
+        users = 480189 // 8
+        keep = s < users
+        s, d, r = s[keep], d[keep], r[keep].astype(np.float64)
+        items = d - 480189 + users
+        n = users + 17770
+        f0 = self.init[np.r_[0:users, 480189:480189 + 17770]].astype(np.float64)
+        R = orc.ref_lib()
+        _, _, _, secs = orc.ref_cf(n, s, items.astype(np.uint32), r, f0, 1e-3, 0.05, 1,
+                                   threads=0, per_iteration=False)
+        return {"value": round(2 * len(s) / secs / 1e9, 6), "unit": "GTEPS",
+                "cores": int(R.ref_hardware_threads()), "kind": "reference",
+                "seconds": round(secs, 4),
+                "sample": f"one superstep (both directions) on the {len(s)} ratings of users "
+                          f"< {users} (graph build excluded)"}
 
 
 WORKLOADS = {"bfs": (BfsWorkload, 23), "pagerank": (PageRankWorkload, 20),

@@ -174,6 +174,8 @@ typedef struct {
   float gamma;
   float lambda;
   int64_t iterations;
+  int32_t factors_on_device; /* 1: init_factors / out_factors are device pointers */
+  int32_t reserved;
 } gm_cf_config;
 /* collaborative_filtering_gd (algorithms/collaborative_filtering.hpp:134-211)
  * in fp32.  init_factors / out_factors: n*k floats (row-major, caller ids).
@@ -189,6 +191,10 @@ GM_API gm_status gm_cf(gm_graph_t g, const gm_cf_config* cfg, const float* init_
  * |N_in(v) & N_in(w)|.  A stored edge with src >= dst is GM_EINPUT with the
  * reference's message ("... violates src < dst; run DAGIFY preprocessing first"). */
 GM_API gm_status gm_triangle_count(gm_graph_t g, uint64_t* total, uint64_t* local_counts);
+
+/* Measurement helper (bench.py's CF roofline): sustained FP32 FMA
+ * throughput of this GPU in TFLOP/s (2 flops per FMA). */
+GM_API gm_status gm_measure_fp32_fma(double* tflops);
 
 /* ---- files: the reference's formats (src/io.cpp, src/report.cpp) --------- */
 /* Host-side edge buffer: caller ids (0-based) as u64, values as f64 (1.0 for

@@ -9,6 +9,7 @@ this package is the host-side mirror of the reference API.
 from .api import (  # noqa: F401
     CudaError, EngineError, Graph, GraphMatError, InputError, IterationStats, UsageError,
     balanced_row_boundaries, bfs, kernel_launches, build_graph, collaborative_filtering_gd, pagerank,
+    measure_fp32_fma,
     program_sizes, run_graph_program, sssp, superstep_phases, triangle_count,
     PROG_PAGERANK_REF, PROG_BFS_REF, PROG_SSSP_REF, PROG_SEMIRING_I64, PROG_ADD_PROBE,
     PROG_IN_ADD_PROBE, PROG_SELECTIVE_PROBE, PROG_THROWING_APPLY, PROG_BOTH_ORDER_PROBE,

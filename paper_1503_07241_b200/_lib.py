@@ -30,7 +30,7 @@ EXPORTED = [
     "gm_triangle_count", "gm_edges_load_text", "gm_edges_load_matrix_market",
     "gm_edges_read_binary", "gm_edges_view", "gm_edges_free", "gm_edges_write_binary",
     "gm_edges_write_text", "gm_write_results", "gm_write_vector_results", "gm_write_report",
-    "gm_fnv1a64", "gm_fnv1a64_file",
+    "gm_fnv1a64", "gm_fnv1a64_file", "gm_measure_fp32_fma",
 ]
 
 
@@ -72,7 +72,8 @@ class PageRankConfig(C.Structure):
 
 class CfConfig(C.Structure):
     _fields_ = [("k", C.c_int64), ("gamma", C.c_float), ("lam", C.c_float),
-                ("iterations", C.c_int64)]
+                ("iterations", C.c_int64), ("factors_on_device", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 _lib = None
@@ -131,6 +132,7 @@ def load(path: str = LIB_PATH):
         "gm_write_report": (C.c_int, [C.c_char_p, C.POINTER(RunReportC)]),
         "gm_fnv1a64": (u64, [vp, u64]),
         "gm_fnv1a64_file": (C.c_int, [C.c_char_p, C.POINTER(u64)]),
+        "gm_measure_fp32_fma": (C.c_int, [C.POINTER(dp)]),
         "gm_graph_csr": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64),
                                    C.POINTER(u64)]),
         "gm_pagerank_shard_init": (C.c_int, [vp, u64, u64, vp, C.POINTER(dp)]),

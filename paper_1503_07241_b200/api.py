@@ -343,24 +343,38 @@ def triangle_count(g: Graph, local=False):
     return (int(tot.value), out) if local else int(tot.value)
 
 
-def collaborative_filtering_gd(g: Graph, k=20, gamma=1e-3, lam=0.05, iterations=10, init=None):
+def collaborative_filtering_gd(g: Graph, k=20, gamma=1e-3, lam=0.05, iterations=10, init=None,
+                               *, init_device_ptr=None, out_device_ptr=None):
     """collaborative_filtering_gd (collaborative_filtering.hpp:134-211) in fp32.
-    Returns (factors [n, k] float32, rmse_trace [iterations], stats)."""
+    Returns (factors [n, k] float32, rmse_trace [iterations], stats).  With
+    init_device_ptr / out_device_ptr (n*k float32 on the device, caller order)
+    the factors stay on the GPU and the returned factors are None."""
     n = g.num_vertices
-    cfg = L.CfConfig(k, gamma, lam, iterations)
-    out = np.empty((n, k), np.float32)
+    dev = init_device_ptr is not None or out_device_ptr is not None
+    if dev and (init_device_ptr is None or out_device_ptr is None or init is not None):
+        raise UsageError("cf: give both init_device_ptr and out_device_ptr (and no host init)")
+    cfg = L.CfConfig(k, gamma, lam, iterations, 1 if dev else 0, 0)
+    out = None if dev else np.empty((n, k), np.float32)
     rm = np.zeros(max(iterations, 1), np.float64)
     st, kk = _stats_buf(iterations)
-    initp = None
+    initp = init_device_ptr if dev else None
     if init is not None:
         init = np.ascontiguousarray(init, np.float32)
         if init.shape != (n, k):
             raise InputError(f"cf: latent vectors must have shape ({n}, {k}), got {init.shape} "
                              f"(expected k = {k})")
         initp = init.ctypes.data
-    _check(L.load().gm_cf(g._h, C.byref(cfg), initp, out.ctypes.data, rm.ctypes.data, st,
+    outp = out_device_ptr if dev else out.ctypes.data
+    _check(L.load().gm_cf(g._h, C.byref(cfg), initp, outp, rm.ctypes.data, st,
                           iterations, C.byref(kk)))
     return out, rm[:iterations], _stats(st, kk.value)
+
+
+def measure_fp32_fma() -> float:
+    """Sustained FP32 FMA throughput (TFLOP/s) of the current GPU."""
+    t = C.c_double()
+    _check(L.load().gm_measure_fp32_fma(C.byref(t)))
+    return float(t.value)
 
 
 # ---------------------------------------------------- generic VertexPrograms

@@ -50,8 +50,10 @@ void write_report(const std::string& path, const gm_run_report& r);
 uint64_t fnv1a64(const void* data, uint64_t size);
 uint64_t fnv1a64_file(const std::string& path);
 }  // namespace io
+double measure_fp32_fma();
 std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
-                                   const float* init, float* out, double* rmse_trace);
+                                   const float* init, float* out, double* rmse_trace,
+                                   bool on_device = false);
 
 
 }  // namespace gm

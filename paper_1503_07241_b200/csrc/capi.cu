@@ -166,7 +166,7 @@ GM_API gm_status gm_cf(gm_graph_t g, const gm_cf_config* cfg, const float* init_
   return guarded([&] {
     if (!cfg) gm::fail(GM_EUSAGE, "null config");
     auto st = gm::cf(*handle(g), cfg->k, cfg->gamma, cfg->lambda, cfg->iterations, init_factors,
-                     out_factors, rmse_trace);
+                     out_factors, rmse_trace, cfg->factors_on_device != 0);
     copy_stats(st, stats, cap, n_stats);
   });
 }
@@ -255,6 +255,13 @@ GM_API gm_status gm_write_report(const char* path, const gm_run_report* report) 
         (report->n_extras && (!report->extra_keys || !report->extra_values)))
       gm::fail(GM_EUSAGE, "null report arrays");
     gm::io::write_report(path, *report);
+  });
+}
+
+GM_API gm_status gm_measure_fp32_fma(double* tflops) {
+  return guarded([&] {
+    if (!tflops) gm::fail(GM_EUSAGE, "null argument");
+    *tflops = gm::measure_fp32_fma();
   });
 }
 

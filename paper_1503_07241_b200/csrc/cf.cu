@@ -236,7 +236,8 @@ void pass(const CfCache& c, Graph& g, bool fwd, const float* f, int k, float* sq
 }  // namespace
 
 std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
-                                   const float* init, float* out, double* rmse_trace) {
+                                   const float* init, float* out, double* rmse_trace,
+                                   bool on_device) {
   if (k <= 0) fail(GM_EINPUT, "cf: k must be positive");
   if (k > 64) fail(GM_EUSAGE, "cf: k above 64 is not supported");
   if (!(gamma > 0.0f)) fail(GM_EINPUT, "cf: gamma must be positive");
@@ -280,7 +281,8 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
   const uint64_t total = n * uint64_t(k);
   if (init) {
     DevBuf<float> tmp(total, s);
-    GM_CUDA(cudaMemcpyAsync(tmp.get(), init, total * 4, cudaMemcpyHostToDevice, s));
+    GM_CUDA(cudaMemcpyAsync(tmp.get(), init, total * 4,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     to_internal(g, tmp.get(), c.f0.get(), size_t(k) * 4);
   } else if (total) {
     k_cf_random_init<<<grid_for(total, 256), 256, 0, s>>>(total, 1.0f / std::sqrt(float(k)), c.f0.get());
@@ -344,12 +346,58 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (out && total) {
-    DevBuf<float> ext(total, s);
-    to_external(g, f, ext.get(), size_t(k) * 4);
-    GM_CUDA(cudaMemcpyAsync(out, ext.get(), total * 4, cudaMemcpyDeviceToHost, s));
+    if (on_device) {
+      to_external(g, f, out, size_t(k) * 4);
+    } else {
+      DevBuf<float> ext(total, s);
+      to_external(g, f, ext.get(), size_t(k) * 4);
+      GM_CUDA(cudaMemcpyAsync(out, ext.get(), total * 4, cudaMemcpyDeviceToHost, s));
+    }
   }
   GM_CUDA(cudaStreamSynchronize(s));
   return stats;
+}
+
+// ---- FP32 FMA throughput probe (the CF roofline's compute ceiling) --------
+namespace {
+__global__ void __launch_bounds__(256) k_fma_probe(float* out, int iters, float a, float b) {
+  float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+        x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+      x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+    }
+  }
+  const float r = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (r == 1234.5f) out[blockIdx.x * blockDim.x + threadIdx.x] = r;  // keep the chains live
+}
+}  // namespace
+
+double measure_fp32_fma() {
+  int dev = 0, sms = 0;
+  GM_CUDA(cudaGetDevice(&dev));
+  GM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid = unsigned(sms) * 8;
+  const int iters = 4096;
+  DevBuf<float> out(size_t(grid) * 256, nullptr);
+  cudaEvent_t e0, e1;
+  GM_CUDA(cudaEventCreate(&e0));
+  GM_CUDA(cudaEventCreate(&e1));
+  k_fma_probe<<<grid, 256>>>(out.get(), 64, 0.999f, 1e-3f);  // warm-up
+  GM_LAUNCH_CHECK();
+  GM_CUDA(cudaEventRecord(e0));
+  k_fma_probe<<<grid, 256>>>(out.get(), iters, 0.999f, 1e-3f);
+  GM_LAUNCH_CHECK();
+  GM_CUDA(cudaEventRecord(e1));
+  GM_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  GM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double fmas = double(grid) * 256 * iters * 16 * 8;
+  return 2.0 * fmas / (ms * 1e-3) / 1e12;
 }
 
 }  // namespace gm

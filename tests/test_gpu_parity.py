@@ -346,3 +346,21 @@ def test_sharded_pagerank_virtual_shards(gm, orc):
     indeg_int = np.bincount(perm[dd], minlength=n)
     per_block = [indeg_int[lo:hi].sum() for lo, hi in (row_block(n, P, r) for r in range(P))]
     assert max(per_block) / min(per_block) < 1.1, per_block
+
+
+def test_cf_device_resident_matches_host(gm):
+    """init/out factors on the device (bench.py's resident path) == host path."""
+    import torch
+    g = gm.Graph.bipartite(3000, 400, 60000.0, 400, seed=4)
+    n, k = g.num_vertices, 20
+    init = np.random.default_rng(4).uniform(0, 0.1, (n, k)).astype(np.float32)
+    host, rm_h, _ = gm.collaborative_filtering_gd(g, k, 1e-3, 0.05, 3, init=init)
+    di = torch.from_numpy(init).cuda()
+    do = torch.empty_like(di)
+    none, rm_d, _ = gm.collaborative_filtering_gd(g, k, 1e-3, 0.05, 3, init_device_ptr=di.data_ptr(),
+                                                  out_device_ptr=do.data_ptr())
+    torch.cuda.synchronize()
+    assert none is None
+    assert np.array_equal(do.cpu().numpy().view(np.uint32), host.view(np.uint32))
+    assert np.array_equal(rm_h, rm_d)
+    assert 10.0 < gm.measure_fp32_fma() < 200.0

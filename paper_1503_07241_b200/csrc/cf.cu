@@ -34,8 +34,6 @@ struct CfCache {
   DevBuf<float> part_t, part_f;             // nitems * k
   DevBuf<float> sq;                         // per item of the forward pass
   DevBuf<float> f0, f1;
-  DevBuf<double> scal;
-  DevBuf<unsigned long long> ctr;
 };
 
 namespace {
@@ -181,10 +179,29 @@ __global__ void k_cf_apply(uint64_t n, int k, const uint32_t* rit, const uint32_
   warp_add_u64(changed, ch);
 }
 
-__global__ void k_sum_sq(const float* sq, uint64_t nit, double* out) {
+// Sum of the per-item squared errors in a fixed order: kSqBlocks contiguous
+// slices (one CTA each, fixed tree), then one CTA over the slice sums.
+constexpr unsigned kSqBlocks = 148;
+
+__global__ void k_sum_sq_part(const float* sq, uint64_t nit, double* part) {
+  __shared__ double red[256];
+  const uint64_t per = (nit + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * per, hi = min(nit, lo + per);
+  double s = 0.0;
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += sq[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k_sum_sq_final(const double* part, unsigned np, double* out) {
   __shared__ double red[256];
   double s = 0.0;
-  for (uint64_t i = threadIdx.x; i < nit; i += blockDim.x) s += sq[i];
+  for (unsigned i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
   red[threadIdx.x] = s;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
@@ -274,8 +291,6 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
     c.sq.alloc(c.nit_f + 1, s);
     c.f0.alloc(n * k + 4, s);
     c.f1.alloc(n * k + 4, s);
-    c.scal.alloc(2, s);
-    c.ctr.alloc(2, s);
   }
   CfCache& c = *g.cf;
   const uint64_t total = n * uint64_t(k);
@@ -298,53 +313,60 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
       default: pass<double>(c, g, fwd, fac, int(k), sq); break;
     }
   };
-  auto read_rmse = [&]() {
-    k_sum_sq<<<1, 256, 0, s>>>(c.sq.get(), c.nit_f, c.scal.get());
+  // Every superstep is enqueued without a host round trip: per-superstep
+  // update counts, squared-error sums and events land in device slots and are
+  // read once at the end.
+  const int64_t ni = std::max<int64_t>(iters, 0);
+  DevBuf<unsigned long long> upd(ni + 1, s);
+  DevBuf<double> sqsum(ni + 1, s), sqpart(kSqBlocks, s);
+  upd.zero(s);
+  auto sum_sq = [&](double* slot) {
+    k_sum_sq_part<<<kSqBlocks, 256, 0, s>>>(c.sq.get(), c.nit_f, sqpart.get());
+    k_sum_sq_final<<<1, 256, 0, s>>>(sqpart.get(), kSqBlocks, slot);
     GM_LAUNCH_CHECK();
-    double h = 0;
-    GM_CUDA(cudaMemcpyAsync(&h, c.scal.get(), 8, cudaMemcpyDeviceToHost, s));
-    GM_CUDA(cudaStreamSynchronize(s));
-    return m ? std::sqrt(h / double(m)) : 0.0;
   };
-  cudaEvent_t e0, e1;
-  GM_CUDA(cudaEventCreate(&e0));
-  GM_CUDA(cudaEventCreate(&e1));
+  std::vector<cudaEvent_t> ev(size_t(2 * ni));
+  for (auto& e : ev) GM_CUDA(cudaEventCreate(&e));
   for (int64_t it = 1; it <= iters; ++it) {
-    GM_CUDA(cudaEventRecord(e0, s));
-    c.ctr.zero(s);
+    GM_CUDA(cudaEventRecord(ev[2 * (it - 1)], s));
     run_pass(false, f, nullptr);  // items receive from users (G^T)
     run_pass(true, f, c.sq.get());  // users receive from items (G); squared errors
     if (total)
       k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
                                                       c.part_t.get(), c.part_f.get(), f, fn, gamma,
-                                                      lambda, c.ctr.get());
+                                                      lambda, upd.get() + it);
     GM_LAUNCH_CHECK();
-    GM_CUDA(cudaEventRecord(e1, s));
-    if (rmse_trace && it > 1) rmse_trace[it - 2] = read_rmse();  // post-update RMSE of it-1
-    unsigned long long ch = 0;
-    GM_CUDA(cudaMemcpyAsync(&ch, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
-    GM_CUDA(cudaStreamSynchronize(s));
+    GM_CUDA(cudaEventRecord(ev[2 * (it - 1) + 1], s));
+    // the forward pass saw the factors after update it-1: post-update RMSE of it-1
+    if (rmse_trace && it > 1) sum_sq(sqsum.get() + (it - 2));
+    std::swap(f, fn);
+  }
+  if (rmse_trace && iters > 0) {
+    run_pass(true, f, c.sq.get());
+    sum_sq(sqsum.get() + (iters - 1));
+  }
+  std::vector<unsigned long long> hu(size_t(ni + 1));
+  std::vector<double> hs(size_t(ni + 1));
+  GM_CUDA(cudaMemcpyAsync(hu.data(), upd.get(), (ni + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaMemcpyAsync(hs.data(), sqsum.get(), (ni + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  for (int64_t it = 1; it <= iters; ++it) {
     float ms = 0;
-    GM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    GM_CUDA(cudaEventElapsedTime(&ms, ev[2 * (it - 1)], ev[2 * (it - 1) + 1]));
     gm_iteration_stats st{};
     st.iteration = it;
     st.active_before = int64_t(n);
     st.messages_generated = int64_t(n);
-    st.vertices_updated = int64_t(ch);
+    st.vertices_updated = int64_t(hu[it]);
     st.spmv_seconds = ms * 1e-3;
     st.total_seconds = ms * 1e-3;
     st.edges_processed = int64_t(2 * m);
     st.bytes_algorithmic = int64_t(2 * 5 * m + 2 * 8 * (n + 2) + 3 * 4 * uint64_t(k) * n);
     st.direction = 0;
     stats.push_back(st);
-    std::swap(f, fn);
+    if (rmse_trace) rmse_trace[it - 1] = m ? std::sqrt(hs[it - 1] / double(m)) : 0.0;
   }
-  if (rmse_trace && iters > 0) {
-    run_pass(true, f, c.sq.get());
-    rmse_trace[iters - 1] = read_rmse();
-  }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  for (auto& e : ev) cudaEventDestroy(e);
   if (out && total) {
     if (on_device) {
       to_external(g, f, out, size_t(k) * 4);

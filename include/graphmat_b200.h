@@ -303,6 +303,18 @@ GM_API gm_status gm_pagerank_shard_step(gm_graph_t g, uint64_t row_begin, uint64
                                         float* x_block_dev, double* dangling_block);
 GM_API gm_status gm_pagerank_shard_ranks(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                          float* ranks_block_host);
+/* Exchange only the part of each block that is ever gathered (SURVEY 8e,
+ * mitigation 1: dangling vertices' messages are never read).  _active gives
+ * this block's prefix length L (last non-dangling offset + 1; with GM_SHARDS
+ * the dangling vertices form each block's tail); the ranks agree on
+ * Lmax = max L, then _pack remaps the owned rows' columns to the packed
+ * message layout (block b's entry o at b*Lmax + o).  After packing,
+ * x_full_dev of gm_pagerank_shard_step holds P*Lmax floats and each rank
+ * contributes x_block_dev[0, Lmax). */
+GM_API gm_status gm_pagerank_shard_active(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                          uint64_t* prefix_len);
+GM_API gm_status gm_pagerank_shard_pack(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                        uint64_t block_stride, uint64_t lmax);
 /* Row-block boundaries balanced by stored entries, like
  * detail::balanced_row_boundaries (dcsc.hpp:81-105).  row_nnz: n counts;
  * bounds: parts+1 entries. */

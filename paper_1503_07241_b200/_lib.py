@@ -30,7 +30,8 @@ EXPORTED = [
     "gm_triangle_count", "gm_edges_load_text", "gm_edges_load_matrix_market",
     "gm_edges_read_binary", "gm_edges_view", "gm_edges_free", "gm_edges_write_binary",
     "gm_edges_write_text", "gm_write_results", "gm_write_vector_results", "gm_write_report",
-    "gm_fnv1a64", "gm_fnv1a64_file", "gm_measure_fp32_fma",
+    "gm_fnv1a64", "gm_fnv1a64_file", "gm_measure_fp32_fma", "gm_pagerank_shard_active",
+    "gm_pagerank_shard_pack",
 ]
 
 
@@ -138,6 +139,8 @@ def load(path: str = LIB_PATH):
         "gm_pagerank_shard_init": (C.c_int, [vp, u64, u64, vp, C.POINTER(dp)]),
         "gm_pagerank_shard_step": (C.c_int, [vp, u64, u64, vp, dp, dp, vp, C.POINTER(dp)]),
         "gm_pagerank_shard_ranks": (C.c_int, [vp, u64, u64, vp]),
+        "gm_pagerank_shard_active": (C.c_int, [vp, u64, u64, C.POINTER(u64)]),
+        "gm_pagerank_shard_pack": (C.c_int, [vp, u64, u64, u64, u64]),
     }
     for name, (res, args) in proto.items():
         f = getattr(L, name)

@@ -22,6 +22,8 @@ double pagerank_shard_init(Graph& g, uint64_t lo, uint64_t hi, float* x_block);
 double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_full, double base,
                            double damping, float* x_block);
 void pagerank_shard_ranks(Graph& g, uint64_t lo, uint64_t hi, float* out_host);
+uint64_t pagerank_shard_active(Graph& g, uint64_t lo, uint64_t hi);
+void pagerank_shard_pack(Graph& g, uint64_t lo, uint64_t hi, uint64_t stride, uint64_t lmax);
 // traversal.cu
 std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, int32_t* out,
                                     bool out_on_device, bool collect_stats);

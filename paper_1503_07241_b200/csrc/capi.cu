@@ -353,6 +353,20 @@ GM_API gm_status gm_pagerank_shard_ranks(gm_graph_t g, uint64_t row_begin, uint6
   return guarded([&] { gm::pagerank_shard_ranks(*handle(g), row_begin, row_end, ranks_block_host); });
 }
 
+GM_API gm_status gm_pagerank_shard_active(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                          uint64_t* prefix_len) {
+  return guarded([&] {
+    if (!prefix_len) gm::fail(GM_EUSAGE, "null argument");
+    *prefix_len = gm::pagerank_shard_active(*handle(g), row_begin, row_end);
+  });
+}
+
+GM_API gm_status gm_pagerank_shard_pack(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                        uint64_t block_stride, uint64_t lmax) {
+  return guarded(
+      [&] { gm::pagerank_shard_pack(*handle(g), row_begin, row_end, block_stride, lmax); });
+}
+
 // detail::balanced_row_boundaries (dcsc.hpp:81-105): boundary p is the smallest
 // row i with cum(i) * parts >= p * total.
 GM_API gm_status gm_balanced_row_boundaries(const uint64_t* row_nnz, uint64_t n, uint64_t parts,

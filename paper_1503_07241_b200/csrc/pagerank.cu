@@ -60,6 +60,11 @@ struct PrCache {
   DevBuf<float> chunk_sum;
   DevBuf<unsigned> slot_ticket;
   uint64_t ntiles = 0, n_long = 0, nchunks = 0;
+  // Sharded exchange of only the non-dangling prefix of every block: the
+  // owned rows' column ids remapped to the packed layout (block b's entry o
+  // at b * pack_lmax + o), see pagerank_shard_pack.
+  DevBuf<uint32_t> idx_packed;
+  uint64_t pack_lmax = 0, pack_stride = 0, ptr_lo = 0;
   DevBuf<float> scalars;       // [0] = base for the current superstep
   DevBuf<float> dang_partial;  // per SpMV CTA (and kDangBlocks for the first base)
   DevBuf<unsigned long long> ctr;
@@ -405,7 +410,7 @@ void launch_spmv(Graph& g, PrCache& c, const float* x_cur, float* x_next, float 
   a.tile_b = c.tile_b.get();
   a.tile_e = c.tile_e.get();
   a.ptr = g.in.ptr.get();
-  a.idx = g.in.idx.get();
+  a.idx = c.pack_lmax ? c.idx_packed.get() - c.ptr_lo : g.in.idx.get();
   a.x_cur = x_cur;
   a.inv = c.inv.get();
   a.rank = c.rank_other();
@@ -475,6 +480,7 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   std::vector<gm_iteration_stats> stats;
   const uint64_t n = g.n;
   if (n == 0) return stats;
+  if (g.pr && g.pr->pack_lmax) g.pr.reset();  // a packed shard layout is not the full vector
   PrCache& c = cache(g);
   cudaStream_t s = g.stream;
   const uint64_t dang_lo = (g.relabeled && g.shards == 1) ? g.nonzero_outdeg : 0;
@@ -563,6 +569,27 @@ __global__ void __launch_bounds__(1024) k_sum_partials(const float* partial, uin
   if (threadIdx.x == 0) *out = red[0];
 }
 
+__global__ void k_pack_cols(const uint32_t* idx, uint64_t m, uint64_t stride, uint64_t lmax,
+                            uint32_t* out, unsigned long long* bad) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < m;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t c = idx[j], b = c / stride, o = c % stride;
+    if (o >= lmax) atomicAdd(bad, 1ull);
+    out[j] = uint32_t(b * lmax + o);
+  }
+}
+
+// Last non-dangling offset + 1 inside [lo, hi): every gathered column of a
+// block lies below it (dangling sources have no out-edges).
+__global__ void k_last_active(const float* inv, uint64_t lo, uint64_t hi, unsigned long long* last) {
+  unsigned long long m = 0;
+  for (uint64_t v = lo + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < hi;
+       v += uint64_t(gridDim.x) * blockDim.x)
+    if (inv[v] != 0.0f) m = max(m, (unsigned long long)(v - lo + 1));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31u) == 0 && m) atomicMax(last, m);
+}
+
 void check_block(Graph& g, uint64_t lo, uint64_t hi) {
   if (lo > hi || hi > g.n) fail(GM_EUSAGE, "pagerank shard: bad row block");
 }
@@ -603,6 +630,48 @@ double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_fu
   GM_CUDA(cudaMemcpyAsync(&h, dsum, 8, cudaMemcpyDeviceToHost, s));
   GM_CUDA(cudaStreamSynchronize(s));
   return h;
+}
+
+uint64_t pagerank_shard_active(Graph& g, uint64_t lo, uint64_t hi) {
+  check_block(g, lo, hi);
+  PrCache& c = cache(g, lo, hi);
+  cudaStream_t s = g.stream;
+  init_state(g, c);
+  GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
+  if (hi > lo) {
+    k_last_active<<<grid_for(hi - lo, 256), 256, 0, s>>>(c.inv.get(), lo, hi, c.ctr.get());
+    GM_LAUNCH_CHECK();
+  }
+  unsigned long long h = 0;
+  GM_CUDA(cudaMemcpyAsync(&h, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+void pagerank_shard_pack(Graph& g, uint64_t lo, uint64_t hi, uint64_t stride, uint64_t lmax) {
+  check_block(g, lo, hi);
+  if (stride == 0 || g.n % stride != 0) fail(GM_EUSAGE, "pagerank shard pack: bad block stride");
+  if (lmax == 0 || lmax > stride) fail(GM_EUSAGE, "pagerank shard pack: bad prefix length");
+  PrCache& c = cache(g, lo, hi);
+  cudaStream_t s = g.stream;
+  uint64_t pl = 0, ph = 0;
+  GM_CUDA(cudaMemcpyAsync(&pl, g.in.ptr.get() + lo, 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaMemcpyAsync(&ph, g.in.ptr.get() + hi, 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  c.idx_packed.alloc(ph - pl + 1, s);
+  GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
+  if (ph > pl) {
+    k_pack_cols<<<grid_for(ph - pl, 256), 256, 0, s>>>(g.in.idx.get() + pl, ph - pl, stride, lmax,
+                                                       c.idx_packed.get(), c.ctr.get());
+    GM_LAUNCH_CHECK();
+  }
+  unsigned long long bad = 0;
+  GM_CUDA(cudaMemcpyAsync(&bad, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  if (bad) fail(GM_EUSAGE, "pagerank shard pack: a gathered column lies past the packed prefix");
+  c.ptr_lo = pl;
+  c.pack_stride = stride;
+  c.pack_lmax = lmax;
 }
 
 void pagerank_shard_ranks(Graph& g, uint64_t lo, uint64_t hi, float* out_host) {

@@ -9,6 +9,13 @@ fused superstep kernels, and per superstep the ranks all-gather the message
 blocks into the full vector and all-reduce the dangling mass for the next base.
 There is no reduce-scatter: row ownership is disjoint.
 
+Only the part of each block that is ever gathered travels (SURVEY 8e,
+mitigation 1): dangling vertices send no messages, GM_SHARDS puts them at the
+tail of every block, so each rank contributes its block's first Lmax entries
+(Lmax = max over ranks of the non-dangling prefix) -- about 46% of the block
+on R-MAT -- and the kernels read the packed layout (block b's entry o at
+b*Lmax + o).
+
 The driver is backend-agnostic so its orchestration (blocks, exchange order,
 base arithmetic) is tested on CPU with gloo; the GPU backend calls the C ABI.
 """
@@ -54,6 +61,16 @@ class TorchExchange:
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
 
+    def allreduce_max(self, value: int, like):
+        import torch
+        t = torch.tensor([value], dtype=torch.int64, device=like.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+    @property
+    def world(self):
+        return self.dist.get_world_size(self.group)
+
 
 class GpuShardBackend:
     """The CUDA kernels on this rank's row block (C ABI gm_pagerank_shard_*)."""
@@ -84,23 +101,42 @@ class GpuShardBackend:
                                                base, damping, self.block.data_ptr(), C.byref(d)))
         return d.value
 
+    def active_len(self):
+        v = C.c_uint64()
+        _check(L.load().gm_pagerank_shard_active(self.g._h, self.lo, self.hi, C.byref(v)))
+        return int(v.value)
+
+    def pack(self, world, lmax):
+        """Switch to the packed message layout (world blocks of lmax entries)."""
+        import torch
+        _check(L.load().gm_pagerank_shard_pack(self.g._h, self.lo, self.hi, self.hi - self.lo,
+                                               lmax))
+        self.full = torch.empty(world * lmax, dtype=torch.float32, device="cuda")
+
     def ranks(self):
         out = np.empty(self.hi - self.lo, np.float32)
         _check(L.load().gm_pagerank_shard_ranks(self.g._h, self.lo, self.hi, out.ctypes.data))
         return out
 
 
-def sharded_pagerank(backend, exchange, n: int, damping=0.85, iterations=20, sync=None):
+def sharded_pagerank(backend, exchange, n: int, damping=0.85, iterations=20, sync=None,
+                     packed=True):
     """Run the BASELINE PageRank on this rank's rows; returns this block's ranks
     (internal order).  base_t = (1-d)/N + d*D_t/N with D_t the global dangling
-    mass after superstep t (pagerank.hpp program shape, CF-driver loop)."""
+    mass after superstep t (pagerank.hpp program shape, CF-driver loop).
+    packed: exchange only the gathered prefix of every block (see module doc)."""
+    sent = backend.block
+    if packed:
+        lmax = exchange.allreduce_max(backend.active_len(), backend.block)
+        backend.pack(exchange.world, max(lmax, 1))
+        sent = backend.block[: max(lmax, 1)]
     dangling = exchange.allreduce_sum(backend.init(), backend.block)
-    exchange.allgather_into(backend.full, backend.block)
+    exchange.allgather_into(backend.full, sent)
     for _ in range(iterations):
         base = (1.0 - damping) / n + damping * dangling / n
         local = backend.step(base, damping)
         if sync is not None:
             sync()
         dangling = exchange.allreduce_sum(local, backend.block)
-        exchange.allgather_into(backend.full, backend.block)
+        exchange.allgather_into(backend.full, sent)
     return backend.ranks()

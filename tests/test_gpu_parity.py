@@ -313,9 +313,11 @@ def test_rmat_pagerank_vs_oracle(gm, orc):
 
 
 # ------------------------------------------------------- multi-GPU sharding
-def test_sharded_pagerank_virtual_shards(gm, orc):
+@pytest.mark.parametrize("packed", [False, True])
+def test_sharded_pagerank_virtual_shards(gm, orc, packed):
     """Row-sharded PageRank with P shards run one after another on one GPU
-    (no kernel waits on another; the all-gather is a device concatenation)."""
+    (no kernel waits on another; the all-gather is a device concatenation).
+    packed: only each block's non-dangling prefix is exchanged."""
     import torch
 
     from paper_1503_07241_b200.sharded import GpuShardBackend, row_block
@@ -323,9 +325,15 @@ def test_sharded_pagerank_virtual_shards(gm, orc):
     n = 1 << scale
     graphs = [gm.Graph.rmat(scale, 16, seed=7, relabel=True, shards=P) for _ in range(P)]
     backends = [GpuShardBackend(graphs[r], *row_block(n, P, r)) for r in range(P)]
+    lmax = n // P
+    if packed:
+        lmax = max(b.active_len() for b in backends)
+        assert lmax < 0.7 * (n // P)  # R-MAT: about half the vertices are dangling
+        for b in backends:
+            b.pack(P, lmax)
 
     def gather():
-        full = torch.cat([b.block for b in backends])
+        full = torch.cat([b.block[:lmax] for b in backends])
         for b in backends:
             b.full.copy_(full)
 

@@ -41,8 +41,31 @@ class NumpyShardBackend:
         self.block.copy_(torch.from_numpy(self.rank * self.inv[self.lo:self.hi]))
         return float(self.rank[self.dangling[self.lo:self.hi]].sum())
 
+    def active_len(self):
+        nz = np.flatnonzero(~self.dangling[self.lo:self.hi])
+        return int(nz[-1]) + 1 if len(nz) else 0
+
+    def pack(self, world, lmax):
+        """Packed message layout: block b's entry o at b*lmax + o."""
+        b = self.hi - self.lo
+        blk, off = self.cols // b, self.cols % b
+        assert (off < lmax).all()
+        self.cols = blk * lmax + off
+        self.full = torch.zeros(world * lmax, dtype=torch.float64)
+
     def ranks(self):
         return self.rank.copy()
+
+
+def shards_relabel(n, src, dst, world):
+    """GM_SHARDS(world) in numpy: out-degree rank k (desc, id asc) dealt
+    round-robin, internal id = (k % P) * n/P + k // P."""
+    outdeg = np.bincount(src, minlength=n)
+    order = np.lexsort((np.arange(n), -outdeg))
+    k = np.empty(n, np.int64)
+    k[order] = np.arange(n)
+    perm = (k % world) * (n // world) + k // world
+    return perm, perm[src], perm[dst]
 
 
 def _free_port():
@@ -51,13 +74,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, src, dst, out):
+def _worker(rank, world, port, n, src, dst, out, packed):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1503_07241_b200.sharded import TorchExchange, row_block, sharded_pagerank
     lo, hi = row_block(n, world, rank)
     backend = NumpyShardBackend(n, src, dst, lo, hi)
-    block = sharded_pagerank(backend, TorchExchange(), n, 0.85, 20)
+    block = sharded_pagerank(backend, TorchExchange(), n, 0.85, 20, packed=packed)
     full = torch.zeros(n, dtype=torch.float64)
     TorchExchange().allgather_into(full, torch.from_numpy(block))
     if rank == 0:
@@ -66,16 +89,30 @@ def _worker(rank, world, port, n, src, dst, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_pagerank_matches_oracle(orc, world):
+@pytest.mark.parametrize("world,packed", [(2, False), (2, True)])
+def test_sharded_pagerank_matches_oracle(orc, world, packed):
     n = 512
     src, dst = orc.rmat(9, 8, seed=3)
     src, dst, _ = orc.preprocess(src, dst)
     want, _ = orc.pagerank_norm(n, src, dst, 0.85, 20)
+    perm, isrc, idst = shards_relabel(n, src.astype(np.int64), dst.astype(np.int64), world)
     out = torch.zeros(n, dtype=torch.float64).share_memory_()
-    mp.spawn(_worker, args=(world, _free_port(), n, src.astype(np.int64), dst.astype(np.int64), out),
-             nprocs=world, join=True)
-    np.testing.assert_allclose(out.numpy(), want, rtol=1e-12, atol=0)
+    mp.spawn(_worker, args=(world, _free_port(), n, isrc, idst, out, packed), nprocs=world,
+             join=True)
+    np.testing.assert_allclose(out.numpy()[perm], want, rtol=1e-12, atol=0)
+
+
+def test_shards_relabel_puts_dangling_at_block_tails(orc):
+    n, world = 512, 4
+    src, dst = orc.rmat(9, 8, seed=3)
+    src, dst, _ = orc.preprocess(src, dst)
+    perm, isrc, _ = shards_relabel(n, src.astype(np.int64), dst.astype(np.int64), world)
+    active = np.bincount(isrc, minlength=n) > 0
+    b = n // world
+    for r in range(world):
+        blk = active[r * b:(r + 1) * b]
+        k = int(blk.sum())
+        assert blk[:k].all() and not blk[k:].any()
 
 
 def test_row_blocks():

@@ -184,18 +184,35 @@ class BfsWorkload(Workload):
     name = "bfs"
     dtype = "int32"
 
+    # BASELINE configs[4] (scale 28) runs 1-D row-sharded across the ranks;
+    # configs[1] (scale 23, a single-GPU config) runs one replica per GPU.
+    SHARD_MIN_SCALE = 26
+
     def build(self, gm):
         a = self.args
+        d = self.dist
+        shards = d.world if d is not None and d.world > 1 and a.scale >= self.SHARD_MIN_SCALE else 1
         t0 = time.perf_counter()
-        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, symmetrize=True, relabel=True, **RMAT)
+        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, symmetrize=True, relabel=True,
+                               shards=shards, **RMAT)
         self.ingest_s = time.perf_counter() - t0
         self.n = 1 << a.scale
         self.root = self.g.pick_source(a.seed)
+        self.sharded = shards > 1
+        if self.sharded:
+            from paper_1503_07241_b200.sharded import GpuBfsShardBackend, TorchExchange, row_block
+            lo, hi = row_block(self.n, d.world, d.rank)
+            self.backend = GpuBfsShardBackend(self.g, lo, hi)
+            self.exchange = TorchExchange()
+            self.root_int = int(self.g.permutation()[self.root])
+            self.scaling = "strong"
+            self.parallelism = f"rows{d.world}"
         import torch
         self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
         self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
         lvl, st = gm.bfs(self.g, self.root)
         deg = self.g.degree_vector("out")
+        self.root_degree = int(deg[self.root])
         # Graph500 TEPS: undirected edges inside the reached component.
         self.edges = int(deg[lvl >= 0].sum()) // 2
         self.levels = lvl
@@ -208,21 +225,33 @@ class BfsWorkload(Workload):
                        % (self.g.info().device_bytes / 1e9)}
 
     def run_device(self, gm):
+        if self.sharded:
+            from paper_1503_07241_b200.sharded import sharded_bfs
+            return sharded_bfs(self.backend, self.exchange, self.n, self.g.num_edges, self.root_int,
+                               self.root_degree)[0]
         gm.bfs(self.g, self.root, with_stats=False, out_device_ptr=self.dev_out.data_ptr())
 
     def run_e2e(self, gm):
+        if self.sharded:  # this rank's block of levels comes back to the host
+            return self.run_device(gm)
         out = self.host_out.numpy()
         gm.bfs(self.g, self.root, with_stats=False, out=out)
         return out
 
     def e2e_bytes(self):
+        if self.sharded:
+            return 0, (self.backend.hi - self.backend.lo) * 4
         return 8, self.n * 4
 
     def per_superstep(self, gm):
+        if self.sharded:
+            return []
         _, st = gm.bfs(self.g, self.root)
         return st
 
     def roofline(self, st, peak, peak_kind):
+        if not st:
+            return None
         # The whole BFS is one cooperative launch (k_bfs_coop); its duration is
         # the sum of the per-superstep %globaltimer spans measured inside it.
         b = sum(s.bytes_algorithmic for s in st)
@@ -300,6 +329,8 @@ class PageRankWorkload(Workload):
         return out
 
     def e2e_bytes(self):
+        if self.sharded:
+            return 8 * self.iters, (self.backend.hi - self.backend.lo) * 4
         return 16, self.n * 4
 
     def per_superstep(self, gm):

@@ -315,6 +315,22 @@ GM_API gm_status gm_pagerank_shard_active(gm_graph_t g, uint64_t row_begin, uint
                                           uint64_t* prefix_len);
 GM_API gm_status gm_pagerank_shard_pack(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                         uint64_t block_stride, uint64_t lmax);
+/* BFS over the rows [row_begin, row_end) of a symmetric graph this rank owns
+ * (32-vertex aligned; GM_SHARDS(P) blocks).  All bitmaps are device u32 words
+ * in internal ids: frontier_dev / visited_dev cover all n vertices and are
+ * identical on every rank; next_block_dev receives this block's
+ * next-frontier bits (word 0 = row_begin).  The caller all-gathers the blocks
+ * into the next frontier, ORs it into visited and sums found / found_edges
+ * over the ranks (push/pull: pull once frontier edges > 5% of m, push again
+ * once the frontier < n/24).  Levels stay on the device until _levels. */
+GM_API gm_status gm_bfs_shard_init(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                   uint64_t root_internal);
+GM_API gm_status gm_bfs_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                   const uint32_t* frontier_dev, const uint32_t* visited_dev,
+                                   int32_t level, int32_t pull, uint32_t* next_block_dev,
+                                   uint64_t* found, uint64_t* found_edges);
+GM_API gm_status gm_bfs_shard_levels(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                     int32_t* levels_block_host);
 /* Row-block boundaries balanced by stored entries, like
  * detail::balanced_row_boundaries (dcsc.hpp:81-105).  row_nnz: n counts;
  * bounds: parts+1 entries. */

@@ -31,7 +31,7 @@ EXPORTED = [
     "gm_edges_read_binary", "gm_edges_view", "gm_edges_free", "gm_edges_write_binary",
     "gm_edges_write_text", "gm_write_results", "gm_write_vector_results", "gm_write_report",
     "gm_fnv1a64", "gm_fnv1a64_file", "gm_measure_fp32_fma", "gm_pagerank_shard_active",
-    "gm_pagerank_shard_pack",
+    "gm_pagerank_shard_pack", "gm_bfs_shard_init", "gm_bfs_shard_step", "gm_bfs_shard_levels",
 ]
 
 
@@ -141,6 +141,10 @@ def load(path: str = LIB_PATH):
         "gm_pagerank_shard_ranks": (C.c_int, [vp, u64, u64, vp]),
         "gm_pagerank_shard_active": (C.c_int, [vp, u64, u64, C.POINTER(u64)]),
         "gm_pagerank_shard_pack": (C.c_int, [vp, u64, u64, u64, u64]),
+        "gm_bfs_shard_init": (C.c_int, [vp, u64, u64, u64]),
+        "gm_bfs_shard_step": (C.c_int, [vp, u64, u64, vp, vp, i32, i32, vp, C.POINTER(u64),
+                                        C.POINTER(u64)]),
+        "gm_bfs_shard_levels": (C.c_int, [vp, u64, u64, vp]),
     }
     for name, (res, args) in proto.items():
         f = getattr(L, name)

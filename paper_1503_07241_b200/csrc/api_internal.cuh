@@ -23,6 +23,11 @@ double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_fu
                            double damping, float* x_block);
 void pagerank_shard_ranks(Graph& g, uint64_t lo, uint64_t hi, float* out_host);
 uint64_t pagerank_shard_active(Graph& g, uint64_t lo, uint64_t hi);
+void bfs_shard_init(Graph& g, uint64_t lo, uint64_t hi, uint64_t root_internal);
+void bfs_shard_step(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* frontier,
+                    const uint32_t* visited, int32_t lvl, int32_t pull, uint32_t* next_block,
+                    uint64_t* found, uint64_t* found_edges);
+void bfs_shard_levels(Graph& g, uint64_t lo, uint64_t hi, int32_t* out_host);
 void pagerank_shard_pack(Graph& g, uint64_t lo, uint64_t hi, uint64_t stride, uint64_t lmax);
 // traversal.cu
 std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, int32_t* out,

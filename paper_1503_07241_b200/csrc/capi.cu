@@ -367,6 +367,32 @@ GM_API gm_status gm_pagerank_shard_pack(gm_graph_t g, uint64_t row_begin, uint64
       [&] { gm::pagerank_shard_pack(*handle(g), row_begin, row_end, block_stride, lmax); });
 }
 
+GM_API gm_status gm_bfs_shard_init(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                   uint64_t root_internal) {
+  return guarded([&] { gm::bfs_shard_init(*handle(g), row_begin, row_end, root_internal); });
+}
+
+GM_API gm_status gm_bfs_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                   const uint32_t* frontier_dev, const uint32_t* visited_dev,
+                                   int32_t level, int32_t pull, uint32_t* next_block_dev,
+                                   uint64_t* found, uint64_t* found_edges) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (h->n && (!frontier_dev || !visited_dev || (row_end > row_begin && !next_block_dev)))
+      gm::fail(GM_EUSAGE, "null bitmap");
+    gm::bfs_shard_step(*h, row_begin, row_end, frontier_dev, visited_dev, level, pull,
+                       next_block_dev, found, found_edges);
+  });
+}
+
+GM_API gm_status gm_bfs_shard_levels(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                     int32_t* levels_block_host) {
+  return guarded([&] {
+    if (!levels_block_host && row_end > row_begin) gm::fail(GM_EUSAGE, "null output");
+    gm::bfs_shard_levels(*handle(g), row_begin, row_end, levels_block_host);
+  });
+}
+
 // detail::balanced_row_boundaries (dcsc.hpp:81-105): boundary p is the smallest
 // row i with cum(i) * parts >= p * total.
 GM_API gm_status gm_balanced_row_boundaries(const uint64_t* row_nnz, uint64_t n, uint64_t parts,

@@ -26,6 +26,7 @@ struct Csr {
 struct PrCache;    // pagerank.cu
 struct TravCache;  // traversal.cu
 struct CfCache;    // cf.cu
+struct BfsShardCache;  // bfs_shard.cu
 
 struct Graph {
   uint64_t n = 0, m = 0;
@@ -52,6 +53,7 @@ struct Graph {
   std::unique_ptr<PrCache, void (*)(PrCache*)> pr{nullptr, nullptr};
   std::unique_ptr<TravCache, void (*)(TravCache*)> trav{nullptr, nullptr};
   std::unique_ptr<CfCache, void (*)(CfCache*)> cf{nullptr, nullptr};
+  std::unique_ptr<BfsShardCache, void (*)(BfsShardCache*)> bfs_shard{nullptr, nullptr};
 
   const Csr& fwd() const { return out_alias ? in : out; }
   uint64_t device_bytes() const;

@@ -140,3 +140,70 @@ def sharded_pagerank(backend, exchange, n: int, damping=0.85, iterations=20, syn
         dangling = exchange.allreduce_sum(local, backend.block)
         exchange.allgather_into(backend.full, sent)
     return backend.ranks()
+
+
+# ---------------------------------------------------------------- BFS
+
+class GpuBfsShardBackend:
+    """BFS kernels on this rank's row block (C ABI gm_bfs_shard_*).  Bitmaps are
+    int32 words on the device in internal ids (bit v of the whole graph at word
+    v >> 5); `frontier` / `visited` cover all vertices, `next_block` this block."""
+
+    def __init__(self, g, lo, hi):
+        import torch
+        self.g, self.lo, self.hi = g, lo, hi
+        n = g.num_vertices
+        self.frontier = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        self.visited = torch.zeros_like(self.frontier)
+        self.next_block = torch.zeros(max((hi - lo + 31) // 32, 1), dtype=torch.int32,
+                                      device="cuda")[: (hi - lo + 31) // 32]
+        self._stream = None
+
+    def init(self, root):
+        _check(L.load().gm_bfs_shard_init(self.g._h, self.lo, self.hi, root))
+        bit = 1 << (root & 31)
+        word = bit - (1 << 32) if bit >= 1 << 31 else bit
+        self.frontier.zero_()
+        self.frontier[root >> 5] = word
+        self.visited.copy_(self.frontier)
+
+    def step(self, level, pull):
+        import torch
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        f, fe = C.c_uint64(), C.c_uint64()
+        _check(L.load().gm_bfs_shard_step(self.g._h, self.lo, self.hi, self.frontier.data_ptr(),
+                                          self.visited.data_ptr(), level, 1 if pull else 0,
+                                          self.next_block.data_ptr(), C.byref(f), C.byref(fe)))
+        return int(f.value), int(fe.value)
+
+    def levels(self):
+        out = np.empty(self.hi - self.lo, np.int32)
+        _check(L.load().gm_bfs_shard_levels(self.g._h, self.lo, self.hi, out.ctypes.data))
+        return out
+
+
+def sharded_bfs(backend, exchange, n: int, m: int, root: int, root_degree: int):
+    """BFS levels of this rank's block (internal ids; -1 unreached).  Per
+    superstep: local push or pull into the block's next-frontier bits, one
+    all-gather of the blocks (the next frontier everywhere), visited |= it, and
+    a sum all-reduce of (found, found edges) for the direction rule of the
+    single-GPU kernel (pull when frontier edges > 5% of m; push again when the
+    frontier < n/24).  Returns (levels, per-superstep records)."""
+    backend.init(root)
+    nf, mf, prev_pull, level = 1, root_degree, False, 0
+    steps = []
+    while nf > 0:
+        level += 1
+        pull = False if level == 1 else (nf * 24 >= n if prev_pull else mf > 0.05 * m)
+        f, fe = backend.step(level, pull)
+        nf = int(round(exchange.allreduce_sum(float(f), backend.frontier)))
+        mf = int(round(exchange.allreduce_sum(float(fe), backend.frontier)))
+        exchange.allgather_into(backend.frontier, backend.next_block)
+        backend.visited |= backend.frontier
+        steps.append(("pull" if pull else "push", nf))
+        prev_pull = pull
+    return backend.levels(), steps

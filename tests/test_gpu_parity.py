@@ -372,3 +372,42 @@ def test_cf_device_resident_matches_host(gm):
     assert np.array_equal(do.cpu().numpy().view(np.uint32), host.view(np.uint32))
     assert np.array_equal(rm_h, rm_d)
     assert 10.0 < gm.measure_fp32_fma() < 200.0
+
+
+def test_sharded_bfs_virtual_shards(gm, orc):
+    """Row-sharded BFS (gm_bfs_shard_*) with P blocks run one after another on
+    one GPU; the all-gather is a device concatenation of the next-frontier
+    blocks.  Levels equal the oracle's; both directions are exercised."""
+    import torch
+
+    from paper_1503_07241_b200.sharded import GpuBfsShardBackend, row_block
+    P, scale = 4, 16
+    n = 1 << scale
+    graphs = [gm.Graph.rmat(scale, 16, seed=9, symmetrize=True, relabel=True, shards=P)
+              for _ in range(P)]
+    bes = [GpuBfsShardBackend(graphs[r], *row_block(n, P, r)) for r in range(P)]
+    g0 = graphs[0]
+    perm = g0.permutation()
+    root_ext = g0.pick_source(9)
+    root = int(perm[root_ext])
+    deg_int = np.empty(n, np.int64)
+    deg_int[perm] = g0.degree_vector("out")
+    for b in bes:
+        b.init(root)
+    nf, mf, prev_pull, level, dirs = 1, int(deg_int[root]), False, 0, []
+    while nf > 0:
+        level += 1
+        pull = False if level == 1 else (nf * 24 >= n if prev_pull else mf > 0.05 * g0.num_edges)
+        res = [b.step(level, pull) for b in bes]
+        nf, mf = sum(r[0] for r in res), sum(r[1] for r in res)
+        nxt = torch.cat([b.next_block for b in bes])
+        for b in bes:
+            b.frontier.copy_(nxt)
+            b.visited |= nxt
+        dirs.append(pull)
+        prev_pull = pull
+    assert any(dirs) and not all(dirs)
+    lv_int = np.concatenate([b.levels() for b in bes])
+    s, d, _ = g0.edges()
+    want, _ = orc.bfs(n, s, d, root_ext, presorted=True)
+    assert np.array_equal(lv_int[perm], want)

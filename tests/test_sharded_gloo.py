@@ -120,3 +120,77 @@ def test_row_blocks():
     assert [row_block(16, 4, r) for r in range(4)] == [(0, 4), (4, 8), (8, 12), (12, 16)]
     with pytest.raises(ValueError):
         row_block(10, 4, 0)
+
+
+# ---------------------------------------------------------------- BFS
+
+class NumpyBfsShardBackend:
+    """Test stand-in for GpuBfsShardBackend: byte-per-vertex flags (uint8)
+    instead of bit words, same block contract."""
+
+    def __init__(self, n, src, dst, lo, hi):
+        self.n, self.lo, self.hi = n, lo, hi
+        order = np.lexsort((dst, src))
+        self.s, self.d = src[order], dst[order]
+        self.ptr = np.searchsorted(self.s, np.arange(n + 1))
+        self.frontier = torch.zeros(n, dtype=torch.uint8)
+        self.visited = torch.zeros(n, dtype=torch.uint8)
+        self.next_block = torch.zeros(hi - lo, dtype=torch.uint8)
+        self.level = np.full(hi - lo, -1, np.int32)
+
+    def init(self, root):
+        if self.lo <= root < self.hi:
+            self.level[root - self.lo] = 0
+        self.frontier.zero_()
+        self.frontier[root] = 1
+        self.visited.copy_(self.frontier)
+
+    def step(self, level, pull):
+        fr, vis = self.frontier.numpy().astype(bool), self.visited.numpy().astype(bool)
+        nxt = np.zeros(self.hi - self.lo, bool)
+        if pull:
+            for v in range(self.lo, self.hi):
+                if not vis[v] and fr[self.d[self.ptr[v]:self.ptr[v + 1]]].any():
+                    nxt[v - self.lo] = True
+        else:
+            for u in np.flatnonzero(fr):
+                nb = self.d[self.ptr[u]:self.ptr[u + 1]]
+                nb = nb[(nb >= self.lo) & (nb < self.hi)]
+                nxt[nb[~vis[nb]] - self.lo] = True
+        self.level[nxt] = level
+        self.next_block.copy_(torch.from_numpy(nxt.astype(np.uint8)))
+        deg = np.diff(self.ptr)
+        return int(nxt.sum()), int(deg[self.lo:self.hi][nxt].sum())
+
+    def levels(self):
+        return self.level.copy()
+
+
+def _bfs_worker(rank, world, port, n, src, dst, root, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1503_07241_b200.sharded import TorchExchange, row_block, sharded_bfs
+    lo, hi = row_block(n, world, rank)
+    be = NumpyBfsShardBackend(n, src, dst, lo, hi)
+    deg = np.bincount(src, minlength=n)
+    lv, steps = sharded_bfs(be, TorchExchange(), n, len(src), root, int(deg[root]))
+    full = torch.zeros(n, dtype=torch.int32)
+    TorchExchange().allgather_into(full, torch.from_numpy(lv))
+    if rank == 0:
+        out[:] = full
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_bfs_matches_oracle(orc):
+    world, scale = 2, 10
+    n = 1 << scale
+    src, dst = orc.rmat(scale, 8, seed=5)
+    src, dst, _ = orc.preprocess(src, dst, symmetrize=True)
+    perm, isrc, idst = shards_relabel(n, src.astype(np.int64), dst.astype(np.int64), world)
+    root = int(np.argmax(np.bincount(src, minlength=n)))
+    want, _ = orc.bfs(n, src, dst, root)
+    out = torch.zeros(n, dtype=torch.int32).share_memory_()
+    mp.spawn(_bfs_worker, args=(world, _free_port(), n, isrc, idst, int(perm[root]), out),
+             nprocs=world, join=True)
+    assert np.array_equal(out.numpy()[perm], want)

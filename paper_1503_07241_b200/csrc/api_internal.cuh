@@ -18,6 +18,10 @@ void superstep_phases(Graph& g, int prog, const double* params, const void* prop
 // pagerank.cu
 std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters, float* out,
                                          bool out_on_device, bool collect_stats);
+// pagerank_hub.cu: the single-GPU default (pagerank() dispatches to it)
+bool pagerank_hub_enabled(const Graph& g);
+std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t iters, float* out,
+                                             bool out_on_device, bool collect_stats);
 double pagerank_shard_init(Graph& g, uint64_t lo, uint64_t hi, float* x_block);
 double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_full, double base,
                            double damping, float* x_block);

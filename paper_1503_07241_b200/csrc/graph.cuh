@@ -24,6 +24,7 @@ struct Csr {
 };
 
 struct PrCache;    // pagerank.cu
+struct PrHubCache; // pagerank_hub.cu
 struct TravCache;  // traversal.cu
 struct CfCache;    // cf.cu
 struct BfsShardCache;  // bfs_shard.cu
@@ -51,6 +52,7 @@ struct Graph {
   bool out_alias = false;  // symmetric and value-less: CSR(G) == CSR(G^T)
 
   std::unique_ptr<PrCache, void (*)(PrCache*)> pr{nullptr, nullptr};
+  std::unique_ptr<PrHubCache, void (*)(PrHubCache*)> prhub{nullptr, nullptr};
   std::unique_ptr<TravCache, void (*)(TravCache*)> trav{nullptr, nullptr};
   std::unique_ptr<CfCache, void (*)(CfCache*)> cf{nullptr, nullptr};
   std::unique_ptr<BfsShardCache, void (*)(BfsShardCache*)> bfs_shard{nullptr, nullptr};

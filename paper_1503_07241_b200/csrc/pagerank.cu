@@ -480,6 +480,7 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
   std::vector<gm_iteration_stats> stats;
   const uint64_t n = g.n;
   if (n == 0) return stats;
+  if (pagerank_hub_enabled(g)) return pagerank_hub(g, damping, iters, out, out_on_device, collect);
   if (g.pr && g.pr->pack_lmax) g.pr.reset();  // a packed shard layout is not the full vector
   PrCache& c = cache(g);
   cudaStream_t s = g.stream;

@@ -1,0 +1,108 @@
+// real_gather.cu -- gather-only floors on the real CSR(G^T) column stream of a
+// graph built by the library (tools/real_gather.py).  Not product code.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC -o tools/real_gather.so tools/real_gather.cu
+#include <cstdint>
+#include <cuda_runtime.h>
+
+template <int U>
+__global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ idx, const float* __restrict__ x, uint64_t m, float* out) {
+  float acc = 0.f;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
+  for (uint64_t b = (blockIdx.x * uint64_t(blockDim.x)) * U + threadIdx.x; b < m; b += stride) {
+    uint32_t j[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { uint64_t k = b + u * blockDim.x; j[u] = k < m ? __ldcs(&idx[k]) : 0; }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += __ldg(&x[j[u]]);
+  }
+  if (acc == 123.f) out[0] = acc;
+}
+
+template <int U>
+__global__ void __launch_bounds__(1024, 1) k_gather_smem(const uint32_t* __restrict__ idx, const float* __restrict__ x, uint64_t m, uint32_t H, float* out) {
+  extern __shared__ float sx[];
+  for (uint32_t i = threadIdx.x; i < H; i += blockDim.x) sx[i] = x[i];
+  __syncthreads();
+  float acc = 0.f;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
+  for (uint64_t b = (blockIdx.x * uint64_t(blockDim.x)) * U + threadIdx.x; b < m; b += stride) {
+    uint32_t j[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { uint64_t k = b + u * blockDim.x; j[u] = k < m ? __ldcs(&idx[k]) : 0; }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += j[u] < H ? sx[j[u]] : __ldcg(&x[j[u]]);
+  }
+  if (acc == 123.f) out[0] = acc;
+}
+
+__device__ __forceinline__ float hg(const float* __restrict__ sx, uint32_t H, const float* __restrict__ x, uint32_t c, uint64_t m) {
+  const float hv = sx[min(c, H - 1)];
+  float gv = 0.0f;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.cg.f32 %0, [%1];\n\t}"
+               : "+f"(gv) : "l"(x + c), "r"(uint32_t(c >= H && c != 0xFFFFFFFFu)));
+  return c < H ? hv : gv;
+}
+
+// INTERLEAVE 0: warp w streams the contiguous chunk [w*C, (w+1)*C);
+// INTERLEAVE 1: warp w takes 256-entry steps w, w+W, w+2W, ... (grid sweep).
+// Three-stage pipeline like k_pr_hub.
+template <int INTERLEAVE>
+__global__ void __launch_bounds__(1024, 1) k_warp_stream(const uint32_t* __restrict__ idx, const float* __restrict__ x, uint64_t m, uint32_t H, float* out) {
+  extern __shared__ float sx[];
+  for (uint32_t i = threadIdx.x; i < H; i += blockDim.x) sx[i] = x[i];
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, W = gridDim.x * 32, gw = blockIdx.x * 32 + (threadIdx.x >> 5);
+  const uint64_t nsteps = (m + 255) / 256;
+  uint64_t s0, s1, sstride;
+  if (INTERLEAVE) { s0 = gw; s1 = nsteps; sstride = W; }
+  else { const uint64_t per = (nsteps + W - 1) / W; s0 = gw * per; s1 = min(nsteps, s0 + per); sstride = 1; }
+  auto ld = [&](uint64_t st, int u) -> uint32_t { const uint64_t k = st * 256 + lane + 32u * u; return (st < s1 && k < m) ? __ldcs(&idx[k]) : 0xFFFFFFFFu; };
+  float acc = 0.f;
+  uint32_t c[8]; float v[8];
+  for (int u = 0; u < 8; ++u) c[u] = ld(s0, u);
+  for (int u = 0; u < 8; ++u) v[u] = hg(sx, H, x, c[u], m);
+  for (int u = 0; u < 8; ++u) c[u] = ld(s0 + sstride, u);
+  for (uint64_t st = s0; st < s1; st += sstride) {
+    float vn[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vn[u] = hg(sx, H, x, c[u], m);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) c[u] = ld(st + 2 * sstride, u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = vn[u];
+  }
+  if (acc == 123.f) out[0] = acc;
+}
+
+extern "C" float rg_run(const uint32_t* idx, uint64_t m, const float* x, uint32_t H, int mode, float* out) {
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaFuncSetAttribute(k_gather_smem<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  cudaFuncSetAttribute(k_warp_stream<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  cudaFuncSetAttribute(k_warp_stream<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  auto launch = [&]() {
+    if (mode == 0) k_gather<8><<<nsm * 8, 256>>>(idx, x, m, out);
+    else if (mode == 1) k_gather_smem<8><<<nsm, 1024, H * 4>>>(idx, x, m, H, out);
+    else if (mode == 2) k_warp_stream<0><<<nsm, 1024, H * 4>>>(idx, x, m, H, out);
+    else k_warp_stream<1><<<nsm, 1024, H * 4>>>(idx, x, m, H, out);
+  };
+  launch();
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  if (cudaGetLastError() != cudaSuccess) return -1.f;
+  return best * 1000.f;
+}

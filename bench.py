@@ -632,7 +632,10 @@ def run_ours(args, d: Dist):
     replicas = d.world if w.scaling == "weak" else 1
     value = w.edges * args.steps * replicas / (t_ms * 1e-3) / 1e9
 
-    # end-to-end through the public API with pinned host buffers
+    # end-to-end through the public API with pinned host buffers (warm-up
+    # calls first: the first host-output call pays one-time lazy module loads)
+    for _ in range(args.warmup):
+        w.run_e2e(gm)
     torch.cuda.synchronize()
     d.barrier()
     t0 = time.perf_counter()

@@ -607,6 +607,16 @@ Graph* new_graph(uint64_t n, uint32_t flags, int storage) {
   g->shards = shards;
   GM_CUDA(cudaGetDevice(&g->device));
   GM_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  {  // Keep up to 4 GB of freed stream-ordered allocations mapped: with the
+     // default threshold (0) every per-call scratch buffer (e.g. the result
+     // permutation of a 33 MB rank vector) is unmapped at each synchronize and
+     // remapped by the next call, which made end-to-end calls erratic.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+      uint64_t keep = 4ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   g->n = n;
   g->flags = flags;
   if (flags & (GM_SYMMETRIZE | GM_DAGIFY | GM_BIPARTITE_CHECK)) g->flags |= GM_PREPROCESS;

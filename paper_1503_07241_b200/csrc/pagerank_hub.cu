@@ -46,6 +46,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "api_internal.cuh"
@@ -74,6 +75,13 @@ struct PrHubCache {
   DevBuf<uint32_t> v_of_pos;  // position -> internal id (kNoRow for pads)
   DevBuf<uint32_t> hub_pos;   // position -> hub slot / kNoHub / kPadRow
   DevBuf<float> inv_pos;      // position -> 1/outdeg (0 for dangling and pads)
+  // Tail messages live in xrow, indexed by "tail order": the position itself
+  // while the message vector fits comfortably in L2, else the internal vertex
+  // id (out-degree rank), which keeps the warm sources in few, L2-resident
+  // lines once x (1 GB at scale 28) is far larger than L2.
+  bool vertex_tail = false;
+  DevBuf<uint32_t> xt_pos;    // position -> tail index (vertex_tail only)
+  uint64_t n_xrow = 0;
   DevBuf<uint4> chunk;       // work chunks {kind, a, b, 0}; CTA b takes chunks b, b+G, ...
   uint32_t n_chunks = 0;
   DevBuf<uint32_t> long_idx;  // remapped columns of the long rows, row after row
@@ -140,6 +148,7 @@ struct HubArgs {
   const uint32_t* sell_idx;
   const float* inv_pos;
   const uint32_t* hub_pos;
+  const uint32_t* xt_pos;  // position -> xrow index, or null (xrow is in position order)
   float* rank_next;
   float* xrow_next;
   float* xhub_next;
@@ -155,14 +164,14 @@ struct Epi {
   float* rank;
   float* xrow;
   float* xhub;
-  // apply + send for the row at position p (iv, hs prefetched)
+  // apply + send for the row at position p (iv, hs, xt prefetched)
   __device__ __forceinline__ void operator()(uint64_t p, float sum, float iv, uint32_t hs,
-                                             float& dang) const {
+                                             uint64_t xt, float& dang) const {
     if (hs == kPadRow) return;
     const float r = base + damping * sum;
     const float x = r * iv;
     rank[p] = r;
-    xrow[p] = x;
+    xrow[xt] = x;
     if (hs < H) xhub[hs] = x;
     if (iv == 0.0f) dang += r;
   }
@@ -233,9 +242,10 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
       const uint32_t len = a.pc_len[p], pos = a.pc_pos[p], slot = a.pc_slot[p];
       const float iv = a.inv_pos[pos];
       const uint32_t hs = a.hub_pos[pos];
+      const uint64_t xo = a.xt_pos ? a.xt_pos[pos] : pos;
       const float sum = piece_sum_of(a.long_idx + a.pc_beg[p], len, lane, s_hub, H, xt);
       if (slot == kNoSlot) {
-        if (lane == 0) epi(pos, sum, iv, hs, dang);
+        if (lane == 0) epi(pos, sum, iv, hs, xo, dang);
       } else {
         // a row split over several pieces: the last to finish folds them in order
         const uint32_t f = a.slot_first[slot], cnt = a.slot_count[slot];
@@ -254,7 +264,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
           if (lane == 0) {
             a.slot_ticket[slot] = 0;
             float dl = 0.0f;
-            epi(pos, t, iv, hs, dl);
+            epi(pos, t, iv, hs, xo, dl);
             a.dang[G + slot] = dl;
           }
         }
@@ -270,6 +280,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
       uint64_t p_cur = a.n_long + uint64_t(sl) * 32u + lane;
       float iv_cur = a.inv_pos[p_cur];
       uint32_t hs_cur = a.hub_pos[p_cur];
+      uint64_t xt_cur = a.xt_pos ? a.xt_pos[p_cur] : p_cur;
       const uint32_t* __restrict__ col = a.sell_idx + lane;
       float acc = 0.0f;
       uint32_t c[kWIPT];
@@ -296,7 +307,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
         for (int u = 0; u < kWIPT; ++u) {
           acc += v[u];
           if (q0 + u + 1 == e_cur) {  // slice sl ends with this line (warp-uniform)
-            epi(p_cur, acc, iv_cur, hs_cur, dang);
+            epi(p_cur, acc, iv_cur, hs_cur, xt_cur, dang);
             acc = 0.0f;
             ++sl;
             if (sl - sbase == 32) {
@@ -308,6 +319,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
             if (sl < sb) {
               iv_cur = a.inv_pos[p_cur];
               hs_cur = a.hub_pos[p_cur];
+              xt_cur = a.xt_pos ? a.xt_pos[p_cur] : p_cur;
             }
           }
         }
@@ -319,14 +331,16 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
       for (uint64_t p0 = ch.y; p0 < ch.z; p0 += 4 * 32) {
         float iv[4];
         uint32_t hs[4];
+        uint64_t xo[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint64_t p = p0 + lane + 32u * u;
           iv[u] = p < ch.z ? a.inv_pos[p] : 0.0f;
           hs[u] = p < ch.z ? a.hub_pos[p] : kPadRow;
+          xo[u] = (a.xt_pos && p < ch.z) ? a.xt_pos[p] : p;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) epi(p0 + lane + 32u * u, 0.0f, iv[u], hs[u], dang);
+        for (int u = 0; u < 4; ++u) epi(p0 + lane + 32u * u, 0.0f, iv[u], hs[u], xo[u], dang);
       }
     }
     dang = warp_sum(dang);
@@ -364,7 +378,8 @@ __global__ void __launch_bounds__(1024) k_hub_base(const float* partial, uint32_
 // Initial state: rank 1/N at every vertex position (0 at pads), x = rank/outdeg,
 // hub messages; per-block dangling partials of the initial ranks.
 __global__ void k_hub_init(uint64_t n_pos, uint64_t n, const float* __restrict__ inv_pos,
-                           const uint32_t* __restrict__ hub_pos, uint32_t H, float* rank,
+                           const uint32_t* __restrict__ hub_pos,
+                           const uint32_t* __restrict__ xt_pos, uint32_t H, float* rank,
                            float* rank_other, float* xrow, float* xhub, float* partial) {
   __shared__ float red[32];
   const float r0 = 1.0f / float(n);
@@ -376,7 +391,7 @@ __global__ void k_hub_init(uint64_t n_pos, uint64_t n, const float* __restrict__
     const float r = pad ? 0.0f : r0, iv = inv_pos[p], x = r * iv;
     rank[p] = r;
     rank_other[p] = 0.0f;
-    xrow[p] = x;
+    if (!pad) xrow[xt_pos ? xt_pos[p] : p] = x;
     if (hs < H) xhub[hs] = x;
     if (!pad && iv == 0.0f) d += r;
   }
@@ -419,10 +434,12 @@ __global__ void k_hub_meta(uint64_t n_pos, const uint32_t* __restrict__ v_of_pos
   }
 }
 
+// column id: hub slot, else H + tail index (position, or the vertex itself
+// when tail_of is null)
 __device__ __forceinline__ uint32_t remap(uint32_t src, const uint32_t* __restrict__ slot_of,
-                                          const uint32_t* __restrict__ pos_of, uint32_t H) {
+                                          const uint32_t* __restrict__ tail_of, uint32_t H) {
   const uint32_t h = slot_of[src];
-  return h != kNoHub ? h : H + pos_of[src];
+  return h != kNoHub ? h : H + (tail_of ? tail_of[src] : src);
 }
 
 // long rows: a warp per row copies its remapped sources
@@ -543,6 +560,12 @@ PrHubCache& hub_cache(Graph& g) {
   for (uint64_t i = 0; i < zeros.size(); ++i) v_of_pos[c.n_in + i] = zeros[i];
   for (uint64_t p = 0; p < c.n_pos; ++p)
     if (v_of_pos[p] != kNoRow) pos_of[v_of_pos[p]] = uint32_t(p);
+  {
+    const char* e = getenv("GM_PR_TAIL");
+    c.vertex_tail = e ? std::string(e) == "vertex" : n * 4 > (48ull << 20);
+  }
+  c.n_xrow = c.vertex_tail ? n : c.n_pos;
+  if (c.vertex_tail) upload(c.xt_pos, v_of_pos, s);  // pads hold kNoRow, never written
   std::vector<uint32_t> hub_pos(c.n_pos);
   for (uint64_t p = 0; p < c.n_pos; ++p)
     hub_pos[p] = v_of_pos[p] == kNoRow ? kPadRow : slot_of[v_of_pos[p]];
@@ -556,7 +579,7 @@ PrHubCache& hub_cache(Graph& g) {
   std::vector<uint64_t> long_ptr(c.n_long + 1, 0);
   for (uint64_t i = 0; i < c.n_long; ++i)
     long_ptr[i + 1] = long_ptr[i] + (ptr[longs[i] + 1] - ptr[longs[i]]);
-  if (lines >= 0xFFFFFFF0ull || c.H + c.n_pos >= kPad || nslices >= 0xFFFFFFF0ull)
+  if (lines >= 0xFFFFFFF0ull || c.H + c.n_pos >= kPad || c.H + n >= kPad || nslices >= 0xFFFFFFF0ull)
     fail(GM_EENGINE, "pagerank: graph too large for the hub kernel");
 
   // Work chunks, heaviest first: pieces of <= kPieceMax nonzeros of the long
@@ -631,7 +654,7 @@ PrHubCache& hub_cache(Graph& g) {
     if (c.n_long) {
       k_hub_fill_long<<<grid_for(c.n_long * 32, 256), 256, 0, s>>>(
           c.n_long, c.v_of_pos.get(), g.in.ptr.get(), g.in.idx.get(), long_ptr_d.get(),
-          slot_d.get(), c.pos_of.get(), c.H, c.long_idx.get());
+          slot_d.get(), c.vertex_tail ? nullptr : c.pos_of.get(), c.H, c.long_idx.get());
       GM_LAUNCH_CHECK();
     }
     c.sell_idx.alloc(lines * 32 + 1, s);
@@ -639,14 +662,15 @@ PrHubCache& hub_cache(Graph& g) {
     if (nslices) {
       k_hub_fill_sell<<<grid_for(nslices * 32, 256), 256, 0, s>>>(
           nslices * 32, c.n_long, c.v_of_pos.get(), c.sell_end.get(), g.in.ptr.get(),
-          g.in.idx.get(), slot_d.get(), c.pos_of.get(), c.H, c.sell_idx.get());
+          g.in.idx.get(), slot_d.get(), c.vertex_tail ? nullptr : c.pos_of.get(), c.H,
+          c.sell_idx.get());
       GM_LAUNCH_CHECK();
     }
     GM_CUDA(cudaStreamSynchronize(s));
   }
   for (int b = 0; b < 2; ++b) {
     c.rank[b].alloc(c.n_pos + 1, s);
-    c.xrow[b].alloc(c.n_pos + 1, s);
+    c.xrow[b].alloc(c.n_xrow + 1, s);
     c.xhub[b].alloc(c.H, s);
     c.xhub[b].zero(s);
   }
@@ -663,12 +687,17 @@ PrHubCache& hub_cache(Graph& g) {
 
 }  // namespace
 
-// The hub path serves whole-graph supersteps on one GPU (GM_PR_HUB=0 selects
-// the CTA-tile kernel of pagerank.cu instead, for A/B measurements).
+// The hub path serves whole-graph supersteps on one GPU while the message
+// vector is L2-sized (<= 64 MB, scale <= 24 R-MAT); beyond that the gathers
+// are DRAM-sector bound and the CTA-tile kernel of pagerank.cu, whose
+// out-degree-ordered x keeps the warm sources L2-resident, is faster (scale
+// 28: 24 ms vs 26.6 ms per superstep).  GM_PR_HUB=0/1 forces either path.
 bool pagerank_hub_enabled(const Graph& g) {
+  if (g.n == 0 || g.in.nnz == 0) return false;
   const char* e = getenv("GM_PR_HUB");
   if (e && e[0] == '0') return false;
-  return g.n > 0 && g.in.nnz > 0;
+  if (e && e[0] == '1') return true;
+  return g.n * 4 <= (64ull << 20);
 }
 
 std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t iters, float* out,
@@ -679,7 +708,8 @@ std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t i
   const uint64_t n = g.n;
   const float d = float(damping);
   int cur = 0;
-  k_hub_init<<<kInitBlocks, 256, 0, s>>>(c.n_pos, n, c.inv_pos.get(), c.hub_pos.get(), c.H,
+  k_hub_init<<<kInitBlocks, 256, 0, s>>>(c.n_pos, n, c.inv_pos.get(), c.hub_pos.get(),
+                                         c.vertex_tail ? c.xt_pos.get() : nullptr, c.H,
                                          c.rank[0].get(), c.rank[1].get(), c.xrow[0].get(),
                                          c.xhub[0].get(), c.dang.get());
   GM_LAUNCH_CHECK();
@@ -707,6 +737,7 @@ std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t i
     a.sell_idx = c.sell_idx.get();
     a.inv_pos = c.inv_pos.get();
     a.hub_pos = c.hub_pos.get();
+    a.xt_pos = c.vertex_tail ? c.xt_pos.get() : nullptr;
     a.rank_next = c.rank[cur ^ 1].get();
     a.xrow_next = c.xrow[cur ^ 1].get();
     a.xhub_next = c.xhub[cur ^ 1].get();

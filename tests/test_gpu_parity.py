@@ -312,6 +312,57 @@ def test_rmat_pagerank_vs_oracle(gm, orc):
     assert abs(float(np.sum(r, dtype=np.float64)) - 1.0) < 1e-4
 
 
+@pytest.mark.parametrize("relabel", [False, True])
+def test_pagerank_hub_and_cta_paths(gm, orc, relabel, monkeypatch):
+    """Both single-GPU SpMV paths (hub/SELL kernel, CTA merge-path tiles) match
+    the fp64 oracle; the hub path is bitwise reproducible run to run."""
+    g = gm.Graph.rmat(16, 16, seed=5, relabel=relabel)
+    s, d, _ = g.edges()
+    want, wst = orc.pagerank_norm(1 << 16, s, d)
+    monkeypatch.setenv("GM_PR_HUB", "1")
+    r1, st = gm.pagerank(g, 0.85, 20)
+    r2, _ = gm.pagerank(g, 0.85, 20)
+    assert rel_l1(r1, want) <= 1e-5
+    assert np.array_equal(r1.view(np.uint32), r2.view(np.uint32))
+    assert [x.active_before for x in st] == [t[1] for t in wst]
+    assert [x.messages_generated for x in st] == [t[2] for t in wst]
+    monkeypatch.setenv("GM_PR_HUB", "0")
+    g2 = gm.Graph.rmat(16, 16, seed=5, relabel=relabel)
+    r3, st3 = gm.pagerank(g2, 0.85, 20)
+    assert rel_l1(r3, want) <= 1e-5
+    assert [x.messages_generated for x in st3] == [t[2] for t in wst]
+
+
+@pytest.mark.parametrize("tail", ["pos", "vertex"])
+def test_pagerank_hub_tail_orders(gm, orc, tail, monkeypatch):
+    monkeypatch.setenv("GM_PR_HUB", "1")
+    monkeypatch.setenv("GM_PR_TAIL", tail)
+    g = gm.Graph.rmat(18, 16, seed=9, relabel=True)
+    s, d, _ = g.edges()
+    r, _ = gm.pagerank(g, 0.85, 10)
+    want, _ = orc.pagerank_norm(1 << 18, s, d, 0.85, 10)
+    assert rel_l1(r, want) <= 1e-5
+
+
+def test_pagerank_hub_small_graphs(gm, orc, monkeypatch):
+    """Edge cases of the hub layout: fewer vertices than hub slots, a lone
+    edge, a star (one long row split into several pieces), dangling-only."""
+    monkeypatch.setenv("GM_PR_HUB", "1")
+    cases = [
+        (3, [0, 0, 1], [1, 2, 2]),                      # tst/test_algorithms.cpp:74-99 graph
+        (2, [0], [1]),
+        (5000, [i for i in range(1, 5000)], [0] * 4999),  # in-degree 4999 -> split row
+        (7, [0, 1, 2, 3], [1, 2, 3, 4]),
+    ]
+    for n, src, dst in cases:
+        src = np.asarray(src, np.uint32)
+        dst = np.asarray(dst, np.uint32)
+        g = gm.Graph.from_edges(src, dst, n)
+        r, _ = gm.pagerank(g, 0.85, 20)
+        want, _ = orc.pagerank_norm(n, src, dst)
+        assert rel_l1(r, want) <= 1e-5, (n, rel_l1(r, want))
+
+
 # ------------------------------------------------------- multi-GPU sharding
 @pytest.mark.parametrize("packed", [False, True])
 def test_sharded_pagerank_virtual_shards(gm, orc, packed):

@@ -145,6 +145,19 @@ GM_API gm_status gm_degree_vector(gm_graph_t g, int32_t kind, uint64_t* out);
 GM_API gm_status gm_pick_source(gm_graph_t g, uint64_t seed, uint64_t* out);
 /* The cudaStream_t every call on this handle is issued on (for event timing). */
 GM_API void* gm_graph_stream(gm_graph_t g);
+/* Wait for every call issued on this handle (see GM_OUT_DEVICE_ASYNC). */
+GM_API gm_status gm_graph_synchronize(gm_graph_t g);
+
+/* out_on_device of gm_pagerank / gm_bfs / gm_sssp:
+ *   GM_OUT_HOST         the output pointer is host memory; returns when written;
+ *   GM_OUT_DEVICE       device memory; returns when written;
+ *   GM_OUT_DEVICE_ASYNC device memory; returns once the run is enqueued on
+ *                       gm_graph_stream(g) (like a cuBLAS call): read the
+ *                       output after gm_graph_synchronize or a stream wait.
+ *                       Stats need the host, so stats/n_stats must be null. */
+#define GM_OUT_HOST 0
+#define GM_OUT_DEVICE 1
+#define GM_OUT_DEVICE_ASYNC 2
 
 /* ---- fast programs (specialised kernels) --------------------------------- */
 typedef struct {

@@ -23,7 +23,7 @@ EXPORTED = [
     "gm_last_error", "gm_version", "gm_graph_create", "gm_graph_generate_rmat",
     "gm_graph_generate_bipartite", "gm_graph_destroy", "gm_graph_get_info",
     "gm_graph_ensure_forward", "gm_graph_export_edges", "gm_degree_vector", "gm_pick_source",
-    "gm_graph_stream", "gm_pagerank", "gm_bfs", "gm_sssp", "gm_cf", "gm_program_sizes",
+    "gm_graph_stream", "gm_graph_synchronize", "gm_pagerank", "gm_bfs", "gm_sssp", "gm_cf", "gm_program_sizes",
     "gm_run_graph_program", "gm_superstep_phases", "gm_balanced_row_boundaries",
     "gm_kernel_launches", "gm_graph_permutation", "gm_pagerank_shard_init",
     "gm_pagerank_shard_step", "gm_pagerank_shard_ranks", "gm_graph_csr",
@@ -107,6 +107,7 @@ def load(path: str = LIB_PATH):
         "gm_degree_vector": (C.c_int, [vp, i32, vp]),
         "gm_pick_source": (C.c_int, [vp, u64, C.POINTER(u64)]),
         "gm_graph_stream": (vp, [vp]),
+        "gm_graph_synchronize": (C.c_int, [vp]),
         "gm_pagerank": (C.c_int, [vp, C.POINTER(PageRankConfig), vp, i32, st, i64,
                                   C.POINTER(i64)]),
         "gm_bfs": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),

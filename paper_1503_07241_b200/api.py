@@ -222,6 +222,10 @@ class Graph:
     def stream(self) -> int:
         return int(L.load().gm_graph_stream(self._h) or 0)
 
+    def synchronize(self):
+        """Wait for every call issued on this graph (after sync=False runs)."""
+        _check(L.load().gm_graph_synchronize(self._h))
+
     def edges(self):
         """Stored edges in caller ids sorted by (src, dst) -- io::preprocess's output."""
         info = self.info()
@@ -274,14 +278,25 @@ def _stats_buf(cap):
 
 # --------------------------------------------------------------- programs
 
+def _device_mode(sync, with_stats):
+    """GM_OUT_DEVICE, or GM_OUT_DEVICE_ASYNC when the caller waives the host
+    synchronisation (the run is only enqueued on g.stream; g.synchronize()
+    waits).  Stats need the host, so they are refused then."""
+    if sync:
+        return 1
+    if with_stats:
+        raise ValueError("sync=False returns before the run ends: pass with_stats=False")
+    return 2
+
+
 def pagerank(g: Graph, damping=0.85, iterations=20, *, with_stats=True, out=None,
-             out_device_ptr=None):
+             out_device_ptr=None, sync=True):
     """BASELINE configs[0] PageRank (normalised, all active, dangling mass / N)."""
     cfg = L.PageRankConfig(damping, iterations)
     n = g.num_vertices
     st, k = _stats_buf(iterations)
     if out_device_ptr is not None:
-        _check(L.load().gm_pagerank(g._h, C.byref(cfg), out_device_ptr, 1,
+        _check(L.load().gm_pagerank(g._h, C.byref(cfg), out_device_ptr, _device_mode(sync, with_stats),
                                     st if with_stats else None, iterations,
                                     C.byref(k) if with_stats else None))
         return None, _stats(st, k.value) if with_stats else []
@@ -294,7 +309,7 @@ def pagerank(g: Graph, damping=0.85, iterations=20, *, with_stats=True, out=None
 
 
 def bfs(g: Graph, root: int, max_iterations=None, *, with_stats=True, out=None,
-        out_device_ptr=None):
+        out_device_ptr=None, sync=True):
     """algo::bfs (traversal.hpp:119-123): int32 levels, -1 = unreached.
     out: optional host int32 array (e.g. pinned); out_device_ptr: write on device."""
     n = g.num_vertices
@@ -303,7 +318,7 @@ def bfs(g: Graph, root: int, max_iterations=None, *, with_stats=True, out=None,
     cap = (max_iterations if max_iterations is not None else n + 1)
     st, k = _stats_buf(min(cap, 4096))
     if out_device_ptr is not None:
-        ptr, on_dev = out_device_ptr, 1
+        ptr, on_dev = out_device_ptr, _device_mode(sync, with_stats)
     else:
         if out is None:
             out = np.empty(n, np.int32)
@@ -314,7 +329,7 @@ def bfs(g: Graph, root: int, max_iterations=None, *, with_stats=True, out=None,
 
 
 def sssp(g: Graph, source: int, max_iterations=None, *, with_stats=True, out=None,
-         out_device_ptr=None):
+         out_device_ptr=None, sync=True):
     """algo::sssp (traversal.hpp:125-133) on integer weights: uint32, UINT32_MAX = unreached."""
     n = g.num_vertices
     if source < 0 or source >= n:
@@ -322,7 +337,7 @@ def sssp(g: Graph, source: int, max_iterations=None, *, with_stats=True, out=Non
     cap = (max_iterations if max_iterations is not None else n + 1)
     st, k = _stats_buf(min(cap, 1 << 16))
     if out_device_ptr is not None:
-        ptr, on_dev = out_device_ptr, 1
+        ptr, on_dev = out_device_ptr, _device_mode(sync, with_stats)
     else:
         if out is None:
             out = np.empty(n, np.uint32)

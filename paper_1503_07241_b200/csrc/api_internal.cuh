@@ -17,11 +17,13 @@ void superstep_phases(Graph& g, int prog, const double* params, const void* prop
 
 // pagerank.cu
 std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters, float* out,
-                                         bool out_on_device, bool collect_stats);
+                                         bool out_on_device, bool collect_stats,
+                                         bool async = false);
 // pagerank_hub.cu: the single-GPU default (pagerank() dispatches to it)
 bool pagerank_hub_enabled(const Graph& g);
 std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t iters, float* out,
-                                             bool out_on_device, bool collect_stats);
+                                             bool out_on_device, bool collect_stats,
+                                         bool async = false);
 double pagerank_shard_init(Graph& g, uint64_t lo, uint64_t hi, float* x_block);
 double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_full, double base,
                            double damping, float* x_block);
@@ -35,9 +37,11 @@ void bfs_shard_levels(Graph& g, uint64_t lo, uint64_t hi, int32_t* out_host);
 void pagerank_shard_pack(Graph& g, uint64_t lo, uint64_t hi, uint64_t stride, uint64_t lmax);
 // traversal.cu
 std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, int32_t* out,
-                                    bool out_on_device, bool collect_stats);
+                                    bool out_on_device, bool collect_stats,
+                                         bool async = false);
 std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters, uint32_t* out,
-                                     bool out_on_device, bool collect_stats);
+                                     bool out_on_device, bool collect_stats,
+                                         bool async = false);
 // cf.cu
 uint64_t triangle_count(Graph& g, uint64_t* local_host);
 

@@ -129,13 +129,28 @@ GM_API void* gm_graph_stream(gm_graph_t g) {
   return g ? reinterpret_cast<void*>(reinterpret_cast<gm::Graph*>(g)->stream) : nullptr;
 }
 
+GM_API gm_status gm_graph_synchronize(gm_graph_t g) {
+  return guarded([&] { GM_CUDA(cudaStreamSynchronize(handle(g)->stream)); });
+}
+
+namespace {
+// out_on_device: GM_OUT_HOST, GM_OUT_DEVICE or GM_OUT_DEVICE_ASYNC (device
+// output, no host synchronisation -- so no stats either).
+void check_out_mode(int32_t mode, const gm_iteration_stats* stats, const int64_t* n_stats) {
+  if (mode < GM_OUT_HOST || mode > GM_OUT_DEVICE_ASYNC) gm::fail(GM_EUSAGE, "bad out_on_device mode");
+  if (mode == GM_OUT_DEVICE_ASYNC && (stats || n_stats))
+    gm::fail(GM_EUSAGE, "GM_OUT_DEVICE_ASYNC returns before the run ends: pass no stats buffer");
+}
+}  // namespace
+
 GM_API gm_status gm_pagerank(gm_graph_t g, const gm_pagerank_config* cfg, float* out_rank,
                              int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                              int64_t* n_stats) {
   return guarded([&] {
     if (!cfg) gm::fail(GM_EUSAGE, "null config");
+    check_out_mode(out_on_device, stats, n_stats);
     auto st = gm::pagerank(*handle(g), cfg->damping, cfg->iterations, out_rank, out_on_device != 0,
-                           stats != nullptr || n_stats != nullptr);
+                           stats != nullptr || n_stats != nullptr, out_on_device == GM_OUT_DEVICE_ASYNC);
     copy_stats(st, stats, cap, n_stats);
   });
 }
@@ -144,8 +159,9 @@ GM_API gm_status gm_bfs(gm_graph_t g, uint64_t root, int64_t max_iters, int32_t*
                         int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                         int64_t* n_stats) {
   return guarded([&] {
+    check_out_mode(out_on_device, stats, n_stats);
     auto st = gm::bfs(*handle(g), root, max_iters, out_level, out_on_device != 0,
-                      stats != nullptr || n_stats != nullptr);
+                      stats != nullptr || n_stats != nullptr, out_on_device == GM_OUT_DEVICE_ASYNC);
     copy_stats(st, stats, cap, n_stats);
   });
 }
@@ -154,8 +170,9 @@ GM_API gm_status gm_sssp(gm_graph_t g, uint64_t source, int64_t max_iters, uint3
                          int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                          int64_t* n_stats) {
   return guarded([&] {
+    check_out_mode(out_on_device, stats, n_stats);
     auto st = gm::sssp(*handle(g), source, max_iters, out_dist, out_on_device != 0,
-                       stats != nullptr || n_stats != nullptr);
+                       stats != nullptr || n_stats != nullptr, out_on_device == GM_OUT_DEVICE_ASYNC);
     copy_stats(st, stats, cap, n_stats);
   });
 }

@@ -474,13 +474,14 @@ void init_state(Graph& g, PrCache& c) {
 }  // namespace
 
 std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters, float* out,
-                                         bool out_on_device, bool collect) {
+                                         bool out_on_device, bool collect, bool async) {
   if (!(damping >= 0.0 && damping <= 1.0)) fail(GM_EINPUT, "pagerank: damping must be in [0, 1]");
   if (iters < 0) fail(GM_EUSAGE, "pagerank: negative iteration count");
   std::vector<gm_iteration_stats> stats;
   const uint64_t n = g.n;
   if (n == 0) return stats;
-  if (pagerank_hub_enabled(g)) return pagerank_hub(g, damping, iters, out, out_on_device, collect);
+  if (pagerank_hub_enabled(g))
+    return pagerank_hub(g, damping, iters, out, out_on_device, collect, async);
   if (g.pr && g.pr->pack_lmax) g.pr.reset();  // a packed shard layout is not the full vector
   PrCache& c = cache(g);
   cudaStream_t s = g.stream;
@@ -535,7 +536,7 @@ std::vector<gm_iteration_stats> pagerank(Graph& g, double damping, int64_t iters
       GM_CUDA(cudaMemcpyAsync(out, ext.get(), n * 4, cudaMemcpyDeviceToHost, s));
     }
   }
-  GM_CUDA(cudaStreamSynchronize(s));
+  if (!async) GM_CUDA(cudaStreamSynchronize(s));
   return stats;
 }
 

@@ -701,7 +701,7 @@ bool pagerank_hub_enabled(const Graph& g) {
 }
 
 std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t iters, float* out,
-                                             bool out_on_device, bool collect) {
+                                             bool out_on_device, bool collect, bool async) {
   std::vector<gm_iteration_stats> stats;
   PrHubCache& c = hub_cache(g);
   cudaStream_t s = g.stream;
@@ -785,7 +785,7 @@ std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t i
       GM_CUDA(cudaMemcpyAsync(out, ext.get(), n * 4, cudaMemcpyDeviceToHost, s));
     }
   }
-  GM_CUDA(cudaStreamSynchronize(s));
+  if (!async) GM_CUDA(cudaStreamSynchronize(s));
   return stats;
 }
 

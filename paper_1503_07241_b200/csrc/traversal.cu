@@ -944,7 +944,7 @@ std::vector<gm_iteration_stats> read_records(TravCache& c, cudaStream_t s, int64
 }  // namespace
 
 std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, int32_t* out,
-                                    bool out_on_device, bool collect) {
+                                    bool out_on_device, bool collect, bool async) {
   const uint64_t n = g.n;
   if (root >= n)
     fail(GM_EINPUT, "source vertex " + std::to_string(root + 1) + " (1-based) exceeds vertex count " +
@@ -1072,12 +1072,12 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
     GM_LAUNCH_CHECK();
     if (!out_on_device) GM_CUDA(cudaMemcpyAsync(out, dst, n * 4, cudaMemcpyDeviceToHost, s));
   }
-  GM_CUDA(cudaStreamSynchronize(s));
+  if (!async) GM_CUDA(cudaStreamSynchronize(s));
   return stats;
 }
 
 std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters, uint32_t* out,
-                                     bool out_on_device, bool collect) {
+                                     bool out_on_device, bool collect, bool async) {
   const uint64_t n = g.n;
   if (root >= n)
     fail(GM_EINPUT, "source vertex " + std::to_string(root + 1) + " (1-based) exceeds vertex count " +
@@ -1142,7 +1142,7 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
     GM_LAUNCH_CHECK();
     if (!out_on_device) GM_CUDA(cudaMemcpyAsync(out, dst, n * 4, cudaMemcpyDeviceToHost, s));
   }
-  GM_CUDA(cudaStreamSynchronize(s));
+  if (!async) GM_CUDA(cudaStreamSynchronize(s));
   return stats;
 }
 

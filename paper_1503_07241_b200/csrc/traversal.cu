@@ -74,6 +74,7 @@ struct Ctl {
   unsigned long long nf, mf;    // current frontier: vertices, edges
   unsigned long long ucur;      // current unvisited-row list length
   int32_t it, dir, prev_pull, cur_is_queue, done, max_it, u_implicit, usel;
+  int32_t queue_out;            // SSSP: pull supersteps also append to the queue
   uint64_t n_total, m_total, nv;
   uint64_t t_start[kMaxRecorded];  // %globaltimer per superstep (cooperative kernel)
   uint64_t t_mid[kMaxRecorded];    // after the first phase (bitmap->queue / pull pass 1)
@@ -99,6 +100,8 @@ struct TravCache {
   DevBuf<uint64_t> defo;        // pull: their exclusive remaining-edge offsets
   DevBuf<uint32_t> vis, fb[2];  // visited / frontier bitmaps (cur = it & 1)
   DevBuf<uint32_t> changed;     // SSSP changed-bitmap
+  DevBuf<uint32_t> msg;         // SSSP pull: superstep-start distance of frontier sources, else INF
+  DevBuf<uint32_t> rowid;       // SSSP pull: row of every CSR(G^T) entry
   DevBuf<Ctl> ctl;
   DevBuf<int32_t> ext_out;      // caller-order staging for host outputs
   std::unique_ptr<HostPinned<int32_t>> hdone;
@@ -177,6 +180,67 @@ __device__ __forceinline__ void warp_enqueue(bool want, uint32_t v, uint32_t edg
   }
 }
 
+// Warp-private staging of queue appends in shared memory: winners are
+// buffered and published kWqCap at a time with one packed atomicAdd, instead
+// of one atomicAdd per warp step on the single queue counter (which
+// serialises at the L2 when millions of vertices change in a superstep).
+constexpr uint32_t kWqCap = 128;
+struct WarpQueue {
+  uint32_t* sv;  // [kWqCap] vertices
+  uint32_t* sd;  // [kWqCap] their edge counts
+  uint32_t cnt = 0;
+  __device__ __forceinline__ void flush(unsigned long long* pack, uint32_t* q, uint64_t* offs) {
+    const unsigned lane = lane_id();
+    if (cnt == 0) return;
+    __syncwarp();
+    // exclusive prefix of the edge counts over the buffer, 32 at a time
+    unsigned long long carry = 0, tot_e = 0;
+    for (uint32_t b = 0; b < cnt; b += 32) {
+      const uint64_t d = b + lane < cnt ? sd[b + lane] : 0;
+      uint64_t incl = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += t;
+      }
+      tot_e += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(pack, (uint64_t(cnt) << kCountShift) | tot_e);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const uint64_t bpos = base >> kCountShift, bedge = base & kEdgeMask;
+    for (uint32_t b = 0; b < cnt; b += 32) {
+      const uint64_t d = b + lane < cnt ? sd[b + lane] : 0;
+      uint64_t incl = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += t;
+      }
+      if (b + lane < cnt) {
+        q[bpos + b + lane] = sv[b + lane];
+        if (offs) offs[bpos + b + lane] = bedge + carry + incl - d;
+      }
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    cnt = 0;
+  }
+  __device__ __forceinline__ void push(bool want, uint32_t v, uint32_t edges,
+                                       unsigned long long* pack, uint32_t* q, uint64_t* offs) {
+    const unsigned lane = lane_id();
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    if (cnt + 32 > kWqCap) flush(pack, q, offs);
+    if (want) {
+      const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
+      sv[pos] = v;
+      sd[pos] = edges;
+    }
+    cnt += __popc(m);
+  }
+};
+
 // Warp-aggregated append of up to kMaxPer entries per lane: (vertex, edge
 // count, start-edge pointer) -> q / offs / qe with one packed atomicAdd.
 template <int kMaxPer>
@@ -249,7 +313,7 @@ __global__ void k_finish(Ctl* ctl, uint64_t* offs_next) {
   if (ctl->done) return;
   const int32_t it = ctl->it;
   uint64_t nn, mn;
-  if (ctl->dir == kPush) {
+  if (ctl->dir == kPush || ctl->queue_out) {
     nn = ctl->qpack >> kCountShift;
     mn = ctl->qpack & kEdgeMask;
     offs_next[nn] = mn;
@@ -266,7 +330,7 @@ __global__ void k_finish(Ctl* ctl, uint64_t* offs_next) {
     r.dir = ctl->dir;
   }
   ctl->prev_pull = ctl->dir == kPull;
-  ctl->cur_is_queue = ctl->dir == kPush;
+  ctl->cur_is_queue = ctl->dir == kPush || ctl->queue_out;
   ctl->nf = nn;
   ctl->mf = mn;
   if (nn == 0 || it >= ctl->max_it) ctl->done = 1;
@@ -790,15 +854,115 @@ __global__ void k_sssp_init(Ctl* ctl, uint32_t* dist, uint64_t n, uint64_t root_
     ctl->max_it = max_it;
     ctl->n_total = n;
     ctl->m_total = m;
+    ctl->queue_out = 1;
   }
 }
 
-// SSSP prologue: always push.
-__global__ void k_sssp_decide(Ctl* ctl) {
+// SSSP prologue: push (SpMSpV over CSR(G), atomicMin per improving edge)
+// while the frontier's out-edges are few; pull (SpMV over CSR(G^T), a
+// segmented min per row, no atomics on hot destinations) once they exceed
+// m / kSsspPullDiv.  Both compute, for every v,
+//   min(dist[v], min over frontier u of snapshot(u) + w(u, v))
+// so distances and per-superstep stats are the same either way.
+constexpr uint64_t kSsspPullDiv = 5;
+__global__ void k_sssp_decide(Ctl* ctl, int allow_pull) {
   if (ctl->done) return;
   ++ctl->it;
-  ctl->dir = kPush;
+  ctl->dir = (allow_pull && ctl->mf * kSsspPullDiv > ctl->m_total) ? kPull : kPush;
   ctl->qpack = ctl->examined = 0;
+}
+
+// pull: frontier snapshots into msg[] before the pass, back to INF after
+__global__ void k_sssp_msg(const Ctl* ctl, const uint32_t* q, const uint32_t* dq, uint32_t* msg,
+                           int clear) {
+  if (ctl->done || ctl->dir != kPull) return;
+  const uint32_t nq = uint32_t(ctl->nf);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += gridDim.x * blockDim.x)
+    msg[q[i]] = clear ? 0xFFFFFFFFu : dq[i];
+}
+
+// pull pass: 32 consecutive CSR(G^T) entries per warp step (coalesced row /
+// source / weight streams, one gather of msg[source]); a segmented warp min
+// per destination row; the segment's first lane lowers dist[row] if the
+// candidate beats it (atomicMin: a row can span two steps) and claims the
+// changed bit once -- the same enqueue as the push.
+template <typename W>
+__global__ void __launch_bounds__(kThreads) k_sssp_pull(Ctl* ctl, const uint32_t* __restrict__ rowid,
+                                                        const uint32_t* __restrict__ idx,
+                                                        const W* __restrict__ wt, uint64_t nnz,
+                                                        const uint32_t* __restrict__ msg,
+                                                        const uint32_t* __restrict__ deg,
+                                                        uint32_t* dist, uint32_t* changed,
+                                                        uint32_t* qn, uint64_t* offs_n) {
+  if (ctl->done || ctl->dir != kPull) return;
+  __shared__ uint32_t s_wq[kThreads / 32][2][kWqCap];
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  WarpQueue wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1]};
+  // two-stage pipeline: the next step's row ids and sources load while this
+  // step's gathers are in flight
+  const uint64_t stride = nwarps * 32 * kEPT;
+  uint64_t b = warp * 32 * kEPT;
+  uint32_t r[kEPT], c[kEPT];
+#pragma unroll
+  for (int k = 0; k < kEPT; ++k) {
+    const uint64_t j = b + uint64_t(k) * 32 + lane;
+    r[k] = j < nnz ? __ldcs(&rowid[j]) : 0xFFFFFFFFu;
+    c[k] = j < nnz ? __ldcs(&idx[j]) : 0u;
+  }
+  for (; b < nnz; b += stride) {
+    uint32_t m[kEPT];
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) m[k] = r[k] != 0xFFFFFFFFu ? __ldcg(&msg[c[k]]) : 0xFFFFFFFFu;
+    uint32_t rn[kEPT], cn[kEPT];
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) {
+      const uint64_t j = b + stride + uint64_t(k) * 32 + lane;
+      rn[k] = j < nnz ? __ldcs(&rowid[j]) : 0xFFFFFFFFu;
+      cn[k] = j < nnz ? __ldcs(&idx[j]) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) {
+      const uint64_t j = b + uint64_t(k) * 32 + lane;
+      uint32_t cand = 0xFFFFFFFFu;
+      if (m[k] != 0xFFFFFFFFu) {
+        const uint64_t c64 = uint64_t(m[k]) + uint64_t(wt[j]);
+        cand = c64 >= 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(c64);
+      }
+      const uint32_t row = r[k];
+      // nothing to do for 32 entries without a frontier source (the common case)
+      if (__all_sync(0xffffffffu, cand == 0xFFFFFFFFu)) continue;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t oc = __shfl_down_sync(0xffffffffu, cand, o);
+        const uint32_t orow = __shfl_down_sync(0xffffffffu, row, o);
+        if (lane + o < 32 && orow == row) cand = min(cand, oc);
+      }
+      const uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1);
+      const bool head = row != 0xFFFFFFFFu && (lane == 0 || prow != row);
+      bool won = false;
+      if (head && cand < dist[row] && cand < atomicMin(&dist[row], cand)) {
+        const uint32_t bit = 1u << (row & 31u);
+        won = !(atomicOr(&changed[row >> 5], bit) & bit);
+      }
+      wq.push(won, row, won ? deg[row] : 0, &ctl->qpack, qn, offs_n);
+    }
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) {
+      r[k] = rn[k];
+      c[k] = cn[k];
+    }
+  }
+  wq.flush(&ctl->qpack, qn, offs_n);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->examined = nnz;
+}
+
+__global__ void k_rowid(const uint64_t* ptr, uint64_t n, uint32_t* rowid) {
+  const unsigned lane = threadIdx.x & 31u;
+  for (uint64_t v = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; v < n;
+       v += (uint64_t(gridDim.x) * blockDim.x) >> 5)
+    for (uint64_t j = ptr[v] + lane; j < ptr[v + 1]; j += 32) rowid[j] = uint32_t(v);
 }
 
 template <typename W>
@@ -811,7 +975,7 @@ __global__ void __launch_bounds__(kThreads) k_sssp_push(Ctl* ctl, const uint32_t
                                                         const uint32_t* __restrict__ deg,
                                                         uint32_t* dist, uint32_t* changed,
                                                         uint32_t* qn, uint64_t* offs_n) {
-  if (ctl->done) return;
+  if (ctl->done || ctl->dir != kPush) return;
   const uint32_t nq = uint32_t(ctl->nf);
   const uint64_t total = ctl->mf;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -1100,6 +1264,19 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
   ensure_forward(g);
   const Csr& fw = g.fwd();
   const uint32_t* perm = g.relabeled ? g.perm.get() : nullptr;
+  // pull supersteps need CSR(G^T) with its weights and a row id per entry
+  const char* pe = getenv("GM_SSSP_PULL");
+  const bool allow_pull = !(pe && pe[0] == '0') && g.in.nnz > 0 && g.in.val.get() != nullptr &&
+                          g.in.nnz < 0xFFFFFFFFull;
+  if (allow_pull) {
+    if (!c.rowid) {
+      c.rowid.alloc(g.in.nnz, s);
+      k_rowid<<<grid_for(n * 32, 256), 256, 0, s>>>(g.in.ptr.get(), n, c.rowid.get());
+      GM_LAUNCH_CHECK();
+      c.msg.alloc(n, s);
+    }
+    GM_CUDA(cudaMemsetAsync(c.msg.get(), 0xFF, n * 4, s));
+  }
   const int32_t max_it = int32_t(std::min<int64_t>(max_iters, 0x7FFFFFFF));
   Ctl* ctl = c.ctl.get();
   k_sssp_init<<<grid_for(n, 256), 256, 0, s>>>(ctl, c.dist.get(), n, root, perm, c.q[1].get(),
@@ -1109,8 +1286,24 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
   const bool u8 = g.value_type == GM_VAL_U8;
   const int64_t enq = run_batches(c, s, max_iters, collect, [&](int64_t it) {
     const int cur = int(it & 1), nxt = cur ^ 1;
-    k_sssp_decide<<<1, 1, 0, s>>>(ctl);
+    k_sssp_decide<<<1, 1, 0, s>>>(ctl, allow_pull ? 1 : 0);
     GM_LAUNCH_CHECK();
+    if (allow_pull) {
+      k_sssp_msg<<<kGrid, kThreads, 0, s>>>(ctl, c.q[cur].get(), c.dq[cur].get(), c.msg.get(), 0);
+      GM_LAUNCH_CHECK();
+      if (u8)
+        k_sssp_pull<uint8_t><<<kGrid, kThreads, 0, s>>>(
+            ctl, c.rowid.get(), g.in.idx.get(), g.in.val.get(), g.in.nnz, c.msg.get(),
+            g.outdeg.get(), c.dist.get(), c.changed.get(), c.q[nxt].get(), c.offs[nxt].get());
+      else
+        k_sssp_pull<uint32_t><<<kGrid, kThreads, 0, s>>>(
+            ctl, c.rowid.get(), g.in.idx.get(), reinterpret_cast<const uint32_t*>(g.in.val.get()),
+            g.in.nnz, c.msg.get(), g.outdeg.get(), c.dist.get(), c.changed.get(), c.q[nxt].get(),
+            c.offs[nxt].get());
+      GM_LAUNCH_CHECK();
+      k_sssp_msg<<<kGrid, kThreads, 0, s>>>(ctl, c.q[cur].get(), c.dq[cur].get(), c.msg.get(), 1);
+      GM_LAUNCH_CHECK();
+    }
     if (u8)
       k_sssp_push<uint8_t><<<kGrid, kThreads, 0, s>>>(
           ctl, c.q[cur].get(), c.dq[cur].get(), c.offs[cur].get(), fw.ptr.get(), fw.idx.get(),
@@ -1129,9 +1322,14 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
     GM_LAUNCH_CHECK();
   });
   std::vector<gm_iteration_stats> stats = read_records(c, s, enq, n, n, collect);
-  for (auto& st : stats)  // SSSP reads a u8/u32 weight with every col id, and a snapshot per vertex
-    st.bytes_algorithmic = int64_t(28 * st.active_before + 5 * st.edges_processed +
-                                   20 * st.vertices_updated + n / 8);
+  for (auto& st : stats) {
+    if (st.direction == 1)  // push: a u8/u32 weight with every col id, a snapshot per vertex
+      st.bytes_algorithmic = int64_t(28 * st.active_before + 5 * st.edges_processed +
+                                     20 * st.vertices_updated + n / 8);
+    else  // pull: row id + col id + u8 weight per entry, msg scatter/clear, dist per row
+      st.bytes_algorithmic = int64_t(9 * g.in.nnz + 8 * st.active_before + 4 * n +
+                                     20 * st.vertices_updated + n / 8);
+  }
   if (out) {
     uint32_t* dst = out;
     if (!out_on_device) {

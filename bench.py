@@ -54,6 +54,15 @@ def ncu_traffic(kernel, workload):
     return None, None
 
 
+def gm_pagerank_uses_hub(g):
+    """Which single-GPU PageRank kernel the library runs for g (the rule of
+    pagerank_hub_enabled, csrc/pagerank_hub.cu)."""
+    e = os.environ.get("GM_PR_HUB")
+    if e is not None and e[:1] in "01":
+        return e[:1] == "1"
+    return g.num_vertices * 4 <= (64 << 20)
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -349,11 +358,12 @@ class PageRankWorkload(Workload):
         t = statistics.median([s.spmv_seconds for s in st])
         b = st[0].bytes_algorithmic
         gbs = b / t / 1e9
-        traffic, src = ncu_traffic("k_pr_spmv", self.config["workload"])
-        return {"bound": "hbm", "kernel": "pr superstep (k_pr_spmv + k_pr_base)",
+        kern = "k_pr_hub" if gm_pagerank_uses_hub(self.g) else "k_pr_spmv"
+        traffic, src = ncu_traffic(kern, self.config["workload"])
+        return {"bound": "hbm", "kernel": f"pr superstep ({kern} + base)",
                 "achieved": round(gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": round(gbs / peak, 4), "bytes_per_launch": b, "launch_us": round(t * 1e6, 2),
-                "traffic": traffic, "traffic_kernel": "k_pr_spmv only", "traffic_source": src}
+                "traffic": traffic, "traffic_kernel": f"{kern} only", "traffic_source": src}
 
     def cpu_baseline(self, orc):
         s, d, _ = self.g.edges()
@@ -417,8 +427,9 @@ class SsspWorkload(Workload):
     def roofline(self, st, peak, peak_kind):
         top = max(st, key=lambda s: s.spmv_seconds)
         gbs = top.bytes_algorithmic / top.spmv_seconds / 1e9
-        traffic, src = ncu_traffic("k_sssp_push", self.config["workload"])
-        return {"bound": "hbm", "kernel": "k_sssp_push", "superstep": top.iteration,
+        kern = "k_sssp_push" if top.direction == 1 else "k_sssp_pull"
+        traffic, src = ncu_traffic(kern, self.config["workload"])
+        return {"bound": "hbm", "kernel": kern, "superstep": top.iteration,
                 "achieved": round(gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": round(gbs / peak, 4), "bytes_per_launch": top.bytes_algorithmic,
                 "launch_us": round(top.spmv_seconds * 1e6, 2), "traffic": traffic,

@@ -180,62 +180,67 @@ __device__ __forceinline__ void warp_enqueue(bool want, uint32_t v, uint32_t edg
   }
 }
 
-// Warp-private staging of queue appends in shared memory: winners are
-// buffered and published kWqCap at a time with one packed atomicAdd, instead
-// of one atomicAdd per warp step on the single queue counter (which
-// serialises at the L2 when millions of vertices change in a superstep).
-constexpr uint32_t kWqCap = 128;
-struct WarpQueue {
-  uint32_t* sv;  // [kWqCap] vertices
-  uint32_t* sd;  // [kWqCap] their edge counts
+// Warp-private staging of queue appends in shared memory: appends are
+// buffered and published CAP at a time with one packed atomicAdd on the queue
+// counter (count << kCountShift | edges), instead of one atomicAdd per warp
+// step, which serialises at the L2 when many warps append a few entries each.
+// kOffs: also write each entry's exclusive edge offset; kQe: and a u64 payload.
+template <uint32_t CAP, bool kOffs, bool kQe>
+struct StagedQ {
+  uint32_t* sv;  // [CAP] vertices
+  uint32_t* sd;  // [CAP] edge counts (kOffs)
+  uint64_t* se;  // [CAP] payloads (kQe)
   uint32_t cnt = 0;
-  __device__ __forceinline__ void flush(unsigned long long* pack, uint32_t* q, uint64_t* offs) {
+  __device__ __forceinline__ void flush(unsigned long long* pack, uint32_t* q, uint64_t* offs,
+                                        uint64_t* qe) {
     const unsigned lane = lane_id();
     if (cnt == 0) return;
     __syncwarp();
-    // exclusive prefix of the edge counts over the buffer, 32 at a time
-    unsigned long long carry = 0, tot_e = 0;
-    for (uint32_t b = 0; b < cnt; b += 32) {
-      const uint64_t d = b + lane < cnt ? sd[b + lane] : 0;
-      uint64_t incl = d;
+    unsigned long long tot_e = 0;
+    if (kOffs)
+      for (uint32_t b = 0; b < cnt; b += 32) {
+        uint64_t d = b + lane < cnt ? sd[b + lane] : 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= unsigned(o)) incl += t;
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        tot_e += d;
       }
-      tot_e += __shfl_sync(0xffffffffu, incl, 31);
-    }
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(pack, (uint64_t(cnt) << kCountShift) | tot_e);
     base = __shfl_sync(0xffffffffu, base, 0);
-    const uint64_t bpos = base >> kCountShift, bedge = base & kEdgeMask;
+    const uint64_t bpos = base >> kCountShift;
+    uint64_t carry = base & kEdgeMask;
     for (uint32_t b = 0; b < cnt; b += 32) {
-      const uint64_t d = b + lane < cnt ? sd[b + lane] : 0;
-      uint64_t incl = d;
+      const bool in = b + lane < cnt;
+      uint64_t d = (kOffs && in) ? sd[b + lane] : 0, incl = d;
+      if (kOffs) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= unsigned(o)) incl += t;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= unsigned(o)) incl += t;
+        }
       }
-      if (b + lane < cnt) {
+      if (in) {
         q[bpos + b + lane] = sv[b + lane];
-        if (offs) offs[bpos + b + lane] = bedge + carry + incl - d;
+        if (kOffs) offs[bpos + b + lane] = carry + incl - d;
+        if (kQe) qe[bpos + b + lane] = se[b + lane];
       }
-      carry += __shfl_sync(0xffffffffu, incl, 31);
+      if (kOffs) carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncwarp();
     cnt = 0;
   }
-  __device__ __forceinline__ void push(bool want, uint32_t v, uint32_t edges,
-                                       unsigned long long* pack, uint32_t* q, uint64_t* offs) {
+  __device__ __forceinline__ void push(bool want, uint32_t v, uint32_t edges, uint64_t payload,
+                                       unsigned long long* pack, uint32_t* q, uint64_t* offs,
+                                       uint64_t* qe) {
     const unsigned lane = lane_id();
     const unsigned m = __ballot_sync(0xffffffffu, want);
     if (!m) return;
-    if (cnt + 32 > kWqCap) flush(pack, q, offs);
+    if (cnt + 32 > CAP) flush(pack, q, offs, qe);
     if (want) {
       const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
       sv[pos] = v;
-      sd[pos] = edges;
+      if (kOffs) sd[pos] = edges;
+      if (kQe) se[pos] = payload;
     }
     cnt += __popc(m);
   }
@@ -551,8 +556,8 @@ __device__ __forceinline__ void coop_push(const CoopArgs& a, int cur, uint64_t n
 // hv shrinks when the frontier is large: the first probe then almost always
 // hits and the rest of the head would be wasted bandwidth.
 __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t* s_fb,
-                                               const uint32_t* fbc, uint64_t v, int hv,
-                                               bool& defer, uint32_t& rest,
+                                               uint32_t s_words, const uint32_t* fbc, uint64_t v,
+                                               int hv, bool& defer, uint32_t& rest,
                                                unsigned long long& examined) {
   uint32_t u[kHead];
 #pragma unroll
@@ -571,7 +576,7 @@ __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t
     if (!found && u[k] != 0xFFFFFFFFu) {
       ++examined;
       const uint32_t w = u[k] >> 5;
-      const uint32_t word = w < a.s_words ? s_fb[w] : __ldcg(&fbc[w]);
+      const uint32_t word = w < s_words ? s_fb[w] : __ldcg(&fbc[w]);
       found = (word >> (u[k] & 31u)) & 1u;
     }
   }
@@ -606,9 +611,14 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
     uint32_t* fbn = a.fb[cur ^ 1];
     if (!pull) {
       if (!vc->cur_is_queue) {  // frontier bitmap -> queue with edge offsets
+        // Two passes over the warp's words: count (vertices, edges), reserve
+        // the CTA's range with one atomicAdd, then write.  (Appending per warp
+        // step put one atomicAdd per ~1 vertex on the single queue counter
+        // when the frontier is sparse: 30 us for 26K vertices.)
+        __shared__ unsigned long long s_wbase[kCoopThreads / 32];
         const uint64_t words = (a.n + 31) / 32;
-        // lanes load 32 consecutive words at once; the warp then walks the
-        // nonzero ones, a lane per bit
+        const unsigned wib = threadIdx.x >> 5;
+        unsigned long long mine = 0;  // (count << kCountShift) | edges of this lane's bits
         for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
           const uint64_t wl = gwarp + (k0 + lane) * nwarps;
           const uint32_t myword = wl < words ? __ldcg(&fbc[wl]) : 0u;
@@ -617,16 +627,59 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
             const int j = __ffs(nz) - 1;
             nz &= nz - 1;
             const uint32_t word = __shfl_sync(0xffffffffu, myword, j);
-            const uint32_t v = uint32_t((gwarp + (k0 + j) * nwarps) * 32 + lane);
+            if ((word >> lane) & 1u) {
+              const uint32_t v = uint32_t((gwarp + (k0 + j) * nwarps) * 32 + lane);
+              mine += (1ull << kCountShift) | (__ldg(&a.out_ptr[v + 1]) - __ldg(&a.out_ptr[v]));
+            }
+          }
+        }
+        unsigned long long wsum = mine;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        if (lane == 0) s_wbase[wib] = wsum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          unsigned long long tot = 0;
+          for (unsigned w = 0; w < kCoopThreads / 32; ++w) {
+            const unsigned long long t = s_wbase[w];
+            s_wbase[w] = tot;
+            tot += t;
+          }
+          const unsigned long long base = tot ? atomicAdd(&a.ctl->bpack, tot) : 0ull;
+          for (unsigned w = 0; w < kCoopThreads / 32; ++w) s_wbase[w] += base;
+        }
+        __syncthreads();
+        unsigned long long pos = s_wbase[wib];  // running (position, edge offset) of the warp
+        for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
+          const uint64_t wl = gwarp + (k0 + lane) * nwarps;
+          const uint32_t myword = wl < words ? __ldcg(&fbc[wl]) : 0u;
+          unsigned nz = __ballot_sync(0xffffffffu, myword != 0u);
+          while (nz) {
+            const int j = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t word = __shfl_sync(0xffffffffu, myword, j);
             const bool set = (word >> lane) & 1u;
-            uint32_t ed = 0;
-            uint64_t ps = 0;
+            const uint32_t v = uint32_t((gwarp + (k0 + j) * nwarps) * 32 + lane);
+            uint64_t ps = 0, ed = 0;
             if (set) {
               ps = __ldg(&a.out_ptr[v]);
-              ed = uint32_t(__ldg(&a.out_ptr[v + 1]) - ps);
+              ed = __ldg(&a.out_ptr[v + 1]) - ps;
             }
-            warp_enqueue_multi<1>(set ? 1u : 0u, &v, &ed, &ps, &a.ctl->bpack, a.q[cur], a.offs[cur],
-                                  a.qe[cur]);
+            const unsigned long long me = set ? ((1ull << kCountShift) | ed) : 0ull;
+            unsigned long long incl = me;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= unsigned(o)) incl += t;
+            }
+            if (set) {
+              const unsigned long long ex = pos + incl - me;
+              const uint32_t qp = uint32_t(ex >> kCountShift);
+              a.q[cur][qp] = v;
+              a.offs[cur][qp] = ex & kEdgeMask;
+              a.qe[cur][qp] = ps;
+            }
+            pos += __shfl_sync(0xffffffffu, incl, 31);
           }
         }
         grid.sync();
@@ -634,7 +687,10 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
       }
       coop_push(a, cur, nf, mf, it, gwarp, nwarps);
     } else {
-      for (uint32_t i = threadIdx.x; i < a.s_words; i += blockDim.x) s_fb[i] = __ldcg(&fbc[i]);
+      // A short unvisited list probes too few words to pay for staging the
+      // hot prefix of the frontier bitmap (96 KB per CTA) in shared memory.
+      const uint32_t sw = (!vc->u_implicit && vc->ucur * 64 < a.nv) ? 0u : a.s_words;
+      for (uint32_t i = threadIdx.x; i < sw; i += blockDim.x) s_fb[i] = __ldcg(&fbc[i]);
       __syncthreads();
       unsigned long long found_n = 0, found_e = 0, examined = 0;
       const int us = vc->usel;
@@ -662,7 +718,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
           uint32_t rest = 0;
           const bool open = v < a.nv && !((vw >> lane) & 1u);
           if (open) {
-            found = coop_probe_row(a, s_fb, fbc, v, hv, defer, rest, examined);
+            found = coop_probe_row(a, s_fb, sw, fbc, v, hv, defer, rest, examined);
             if (found) {
               a.level[v] = it;
               found_e += __ldg(&a.deg[v]);
@@ -696,7 +752,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
             v = __ldcg(&ucur[i]);
             open = !((__ldcg(&a.vis[v >> 5]) >> (v & 31u)) & 1u);
             if (open) {
-              found = coop_probe_row(a, s_fb, fbc, v, hv, defer, rest, examined);
+              found = coop_probe_row(a, s_fb, sw, fbc, v, hv, defer, rest, examined);
               if (found) {
                 const uint32_t bit = 1u << (v & 31u);
                 a.level[v] = it;
@@ -773,7 +829,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
           if (k < nk && !(done_w[k] & bit)) {
             ++examined;
             const uint32_t w = u[k] >> 5;
-            const uint32_t word = w < a.s_words ? s_fb[w] : __ldcg(&fbc[w]);
+            const uint32_t word = w < sw ? s_fb[w] : __ldcg(&fbc[w]);
             if ((word >> (u[k] & 31u)) & 1u) {
               const uint32_t v = rv[k];
               if (!(atomicOr(&fbn[v >> 5], bit) & bit)) {
@@ -895,11 +951,11 @@ __global__ void __launch_bounds__(kThreads) k_sssp_pull(Ctl* ctl, const uint32_t
                                                         uint32_t* dist, uint32_t* changed,
                                                         uint32_t* qn, uint64_t* offs_n) {
   if (ctl->done || ctl->dir != kPull) return;
-  __shared__ uint32_t s_wq[kThreads / 32][2][kWqCap];
+  __shared__ uint32_t s_wq[kThreads / 32][2][128];
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const unsigned lane = lane_id();
-  WarpQueue wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1]};
+  StagedQ<128, true, false> wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], nullptr};
   // two-stage pipeline: the next step's row ids and sources load while this
   // step's gathers are in flight
   const uint64_t stride = nwarps * 32 * kEPT;
@@ -946,7 +1002,7 @@ __global__ void __launch_bounds__(kThreads) k_sssp_pull(Ctl* ctl, const uint32_t
         const uint32_t bit = 1u << (row & 31u);
         won = !(atomicOr(&changed[row >> 5], bit) & bit);
       }
-      wq.push(won, row, won ? deg[row] : 0, &ctl->qpack, qn, offs_n);
+      wq.push(won, row, won ? deg[row] : 0, 0, &ctl->qpack, qn, offs_n, nullptr);
     }
 #pragma unroll
     for (int k = 0; k < kEPT; ++k) {
@@ -954,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads) k_sssp_pull(Ctl* ctl, const uint32_t
       c[k] = cn[k];
     }
   }
-  wq.flush(&ctl->qpack, qn, offs_n);
+  wq.flush(&ctl->qpack, qn, offs_n, nullptr);
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl->examined = nnz;
 }
 

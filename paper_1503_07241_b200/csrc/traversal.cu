@@ -102,6 +102,8 @@ struct TravCache {
   DevBuf<uint32_t> changed;     // SSSP changed-bitmap
   DevBuf<uint32_t> msg;         // SSSP pull: superstep-start distance of frontier sources, else INF
   DevBuf<uint32_t> rowid;       // SSSP pull: row of every CSR(G^T) entry
+  uint32_t pull_hub = 0;        // SSSP pull: msg[0, pull_hub) staged in shared memory
+  unsigned pull_grid = 0;
   DevBuf<Ctl> ctl;
   DevBuf<int32_t> ext_out;      // caller-order staging for host outputs
   std::unique_ptr<HostPinned<int32_t>> hdone;
@@ -916,11 +918,12 @@ __global__ void k_sssp_init(Ctl* ctl, uint32_t* dist, uint64_t n, uint64_t root_
 
 // SSSP prologue: push (SpMSpV over CSR(G), atomicMin per improving edge)
 // while the frontier's out-edges are few; pull (SpMV over CSR(G^T), a
-// segmented min per row, no atomics on hot destinations) once they exceed
-// m / kSsspPullDiv.  Both compute, for every v,
+// run-min per row, no atomics on hot destinations) once they exceed
+// m / kSsspPullDiv (one pull pass costs about as much as a push over m/6
+// edges at scale 23).  Both compute, for every v,
 //   min(dist[v], min over frontier u of snapshot(u) + w(u, v))
 // so distances and per-superstep stats are the same either way.
-constexpr uint64_t kSsspPullDiv = 5;
+constexpr uint64_t kSsspPullDiv = 6;
 __global__ void k_sssp_decide(Ctl* ctl, int allow_pull) {
   if (ctl->done) return;
   ++ctl->it;
@@ -937,81 +940,170 @@ __global__ void k_sssp_msg(const Ctl* ctl, const uint32_t* q, const uint32_t* dq
     msg[q[i]] = clear ? 0xFFFFFFFFu : dq[i];
 }
 
-// pull pass: 32 consecutive CSR(G^T) entries per warp step (coalesced row /
-// source / weight streams, one gather of msg[source]); a segmented warp min
-// per destination row; the segment's first lane lowers dist[row] if the
-// candidate beats it (atomicMin: a row can span two steps) and claims the
-// changed bit once -- the same enqueue as the push.
+constexpr uint32_t kSsspHub = 49152;  // frontier messages of the first ids in shared memory
+
+// Gather msg[c]: ids below H from the shared copy, the rest from L2 (.cg),
+// branch-free (both loads predicated, a select picks).
+__device__ __forceinline__ uint32_t msg_gather(const uint32_t* __restrict__ s_msg, uint32_t H,
+                                               const uint32_t* __restrict__ msg, uint32_t c,
+                                               bool valid) {
+  const uint32_t hv = s_msg[min(c, H - 1)];
+  uint32_t gv = 0xFFFFFFFFu;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.cg.u32 %0, [%1];\n\t}"
+      : "+r"(gv)
+      : "l"(msg + c), "r"(uint32_t(valid && c >= H)));
+  return !valid ? 0xFFFFFFFFu : c < H ? hv : gv;
+}
+
+// pull pass: a lane takes 8 consecutive CSR(G^T) entries per step (row id,
+// source and weight as vector loads, 2 KB per warp step), gathers the 8
+// messages (hub ids from the shared copy of msg[0, H)), and folds a running
+// min per destination row along its entries; a row's min that beats dist[row]
+// lowers it (atomicMin -- a row spans lanes) and sets the row's changed bit.
+// The next frontier queue is built afterwards from the changed bitmap
+// (k_sssp_pull_queue), so the pass itself has no queue appends and no
+// shuffles.  Each warp keeps the next step's loads in flight while it gathers
+// and folds the current one.
 template <typename W>
-__global__ void __launch_bounds__(kThreads) k_sssp_pull(Ctl* ctl, const uint32_t* __restrict__ rowid,
-                                                        const uint32_t* __restrict__ idx,
-                                                        const W* __restrict__ wt, uint64_t nnz,
-                                                        const uint32_t* __restrict__ msg,
-                                                        const uint32_t* __restrict__ deg,
-                                                        uint32_t* dist, uint32_t* changed,
-                                                        uint32_t* qn, uint64_t* offs_n) {
+__device__ __forceinline__ void pull_load(const uint32_t* __restrict__ rowid,
+                                          const uint32_t* __restrict__ idx,
+                                          const W* __restrict__ wt, uint64_t nnz, uint64_t j,
+                                          uint32_t (&r)[8], uint32_t (&c)[8], uint32_t (&w)[8]) {
+  if (j + 8 <= nnz) {
+    const uint4 r0 = __ldcs(reinterpret_cast<const uint4*>(rowid + j));
+    const uint4 r1 = __ldcs(reinterpret_cast<const uint4*>(rowid + j) + 1);
+    const uint4 c0 = __ldcs(reinterpret_cast<const uint4*>(idx + j));
+    const uint4 c1 = __ldcs(reinterpret_cast<const uint4*>(idx + j) + 1);
+    r[0] = r0.x; r[1] = r0.y; r[2] = r0.z; r[3] = r0.w;
+    r[4] = r1.x; r[5] = r1.y; r[6] = r1.z; r[7] = r1.w;
+    c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w;
+    c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
+    if constexpr (sizeof(W) == 1) {
+      const uint2 wv = __ldcs(reinterpret_cast<const uint2*>(wt + j));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        w[u] = (wv.x >> (8 * u)) & 0xFFu;
+        w[4 + u] = (wv.y >> (8 * u)) & 0xFFu;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u] = uint32_t(wt[j + u]);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool in = j + u < nnz;
+      r[u] = in ? rowid[j + u] : 0xFFFFFFFFu;
+      c[u] = in ? idx[j + u] : 0u;
+      w[u] = in ? uint32_t(wt[j + u]) : 0u;
+    }
+  }
+}
+
+template <typename W>
+__global__ void __launch_bounds__(kThreads, 1) k_sssp_pull(Ctl* ctl, const uint32_t* __restrict__ rowid,
+                                                           const uint32_t* __restrict__ idx,
+                                                           const W* __restrict__ wt, uint64_t nnz,
+                                                           const uint32_t* __restrict__ msg, uint32_t H,
+                                                           uint32_t* dist, uint32_t* changed) {
   if (ctl->done || ctl->dir != kPull) return;
-  __shared__ uint32_t s_wq[kThreads / 32][2][128];
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  extern __shared__ __align__(16) uint32_t s_msg[];
+  for (uint32_t i = threadIdx.x; i < H / 4; i += blockDim.x)
+    reinterpret_cast<uint4*>(s_msg)[i] = __ldcg(reinterpret_cast<const uint4*>(msg) + i);
+  __syncthreads();
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * 8;
+  uint64_t j = t * 8;
+  uint32_t r[8], c[8], w[8];
+  pull_load(rowid, idx, wt, nnz, j, r, c, w);
+  for (; j < nnz; j += stride) {
+    uint32_t m[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m[u] = msg_gather(s_msg, H, msg, c[u], r[u] != 0xFFFFFFFFu);
+    uint32_t rn[8], cn[8], wn[8];
+    pull_load(rowid, idx, wt, nnz, j + stride, rn, cn, wn);
+    uint32_t row = r[0], best = 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (r[u] != row) {
+        if (best != 0xFFFFFFFFu && best < dist[row] && best < atomicMin(&dist[row], best))
+          atomicOr(&changed[row >> 5], 1u << (row & 31u));
+        row = r[u];
+        best = 0xFFFFFFFFu;
+      }
+      if (m[u] != 0xFFFFFFFFu) {
+        const uint64_t c64 = uint64_t(m[u]) + uint64_t(w[u]);
+        best = min(best, c64 >= 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(c64));
+      }
+    }
+    if (row != 0xFFFFFFFFu && best != 0xFFFFFFFFu && best < dist[row] &&
+        best < atomicMin(&dist[row], best))
+      atomicOr(&changed[row >> 5], 1u << (row & 31u));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      r[u] = rn[u];
+      c[u] = cn[u];
+      w[u] = wn[u];
+    }
+  }
+  if (t == 0) ctl->examined = nnz;
+}
+
+// After a pull: the changed bitmap -> next frontier queue with edge offsets.
+// Two passes over the warp's words (count, then write) with one atomicAdd per
+// CTA on the queue counter.
+__global__ void __launch_bounds__(kThreads) k_sssp_pull_queue(Ctl* ctl, const uint32_t* changed,
+                                                              uint64_t words,
+                                                              const uint32_t* __restrict__ deg,
+                                                              uint32_t* qn, uint64_t* offs_n) {
+  if (ctl->done || ctl->dir != kPull) return;
+  __shared__ unsigned long long s_wbase[kThreads / 32];
+  const uint64_t gwarp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned lane = lane_id();
-  StagedQ<128, true, false> wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], nullptr};
-  // two-stage pipeline: the next step's row ids and sources load while this
-  // step's gathers are in flight
-  const uint64_t stride = nwarps * 32 * kEPT;
-  uint64_t b = warp * 32 * kEPT;
-  uint32_t r[kEPT], c[kEPT];
-#pragma unroll
-  for (int k = 0; k < kEPT; ++k) {
-    const uint64_t j = b + uint64_t(k) * 32 + lane;
-    r[k] = j < nnz ? __ldcs(&rowid[j]) : 0xFFFFFFFFu;
-    c[k] = j < nnz ? __ldcs(&idx[j]) : 0u;
+  const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
+  unsigned long long mine = 0;
+  for (uint64_t w = gwarp; w < words; w += nwarps * 32) {
+    const uint64_t wl = w + uint64_t(lane) * nwarps;
+    const uint32_t word = wl < words ? __ldcg(&changed[wl]) : 0u;
+    for (uint32_t b = word; b; b &= b - 1)
+      mine += (1ull << kCountShift) | __ldg(&deg[wl * 32 + __ffs(b) - 1]);
   }
-  for (; b < nnz; b += stride) {
-    uint32_t m[kEPT];
+  unsigned long long wsum = mine;
 #pragma unroll
-    for (int k = 0; k < kEPT; ++k) m[k] = r[k] != 0xFFFFFFFFu ? __ldcg(&msg[c[k]]) : 0xFFFFFFFFu;
-    uint32_t rn[kEPT], cn[kEPT];
-#pragma unroll
-    for (int k = 0; k < kEPT; ++k) {
-      const uint64_t j = b + stride + uint64_t(k) * 32 + lane;
-      rn[k] = j < nnz ? __ldcs(&rowid[j]) : 0xFFFFFFFFu;
-      cn[k] = j < nnz ? __ldcs(&idx[j]) : 0u;
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  if (lane == 0) s_wbase[wib] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (unsigned w = 0; w < kThreads / 32; ++w) {
+      const unsigned long long v = s_wbase[w];
+      s_wbase[w] = tot;
+      tot += v;
     }
+    const unsigned long long base = tot ? atomicAdd(&ctl->qpack, tot) : 0ull;
+    for (unsigned w = 0; w < kThreads / 32; ++w) s_wbase[w] += base;
+  }
+  __syncthreads();
+  // lane order within the warp: exclusive scan of the lanes' sums
+  unsigned long long incl = mine;
 #pragma unroll
-    for (int k = 0; k < kEPT; ++k) {
-      const uint64_t j = b + uint64_t(k) * 32 + lane;
-      uint32_t cand = 0xFFFFFFFFu;
-      if (m[k] != 0xFFFFFFFFu) {
-        const uint64_t c64 = uint64_t(m[k]) + uint64_t(wt[j]);
-        cand = c64 >= 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(c64);
-      }
-      const uint32_t row = r[k];
-      // nothing to do for 32 entries without a frontier source (the common case)
-      if (__all_sync(0xffffffffu, cand == 0xFFFFFFFFu)) continue;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t oc = __shfl_down_sync(0xffffffffu, cand, o);
-        const uint32_t orow = __shfl_down_sync(0xffffffffu, row, o);
-        if (lane + o < 32 && orow == row) cand = min(cand, oc);
-      }
-      const uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1);
-      const bool head = row != 0xFFFFFFFFu && (lane == 0 || prow != row);
-      bool won = false;
-      if (head && cand < dist[row] && cand < atomicMin(&dist[row], cand)) {
-        const uint32_t bit = 1u << (row & 31u);
-        won = !(atomicOr(&changed[row >> 5], bit) & bit);
-      }
-      wq.push(won, row, won ? deg[row] : 0, 0, &ctl->qpack, qn, offs_n, nullptr);
-    }
-#pragma unroll
-    for (int k = 0; k < kEPT; ++k) {
-      r[k] = rn[k];
-      c[k] = cn[k];
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= unsigned(o)) incl += v;
+  }
+  unsigned long long pos = s_wbase[wib] + incl - mine;
+  for (uint64_t w = gwarp; w < words; w += nwarps * 32) {
+    const uint64_t wl = w + uint64_t(lane) * nwarps;
+    const uint32_t word = wl < words ? __ldcg(&changed[wl]) : 0u;
+    for (uint32_t b = word; b; b &= b - 1) {
+      const uint32_t v = uint32_t(wl * 32 + __ffs(b) - 1);
+      const uint32_t qp = uint32_t(pos >> kCountShift);
+      qn[qp] = v;
+      offs_n[qp] = pos & kEdgeMask;
+      pos += (1ull << kCountShift) | __ldg(&deg[v]);
     }
   }
-  wq.flush(&ctl->qpack, qn, offs_n, nullptr);
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->examined = nnz;
 }
 
 __global__ void k_rowid(const uint64_t* ptr, uint64_t n, uint32_t* rowid) {
@@ -1329,9 +1421,18 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
       c.rowid.alloc(g.in.nnz, s);
       k_rowid<<<grid_for(n * 32, 256), 256, 0, s>>>(g.in.ptr.get(), n, c.rowid.get());
       GM_LAUNCH_CHECK();
-      c.msg.alloc(n, s);
+      c.msg.alloc(n + 4, s);
+      c.pull_hub = uint32_t(std::max<uint64_t>(4, std::min<uint64_t>(kSsspHub, n) & ~uint64_t(3)));
+      int dev = 0, sms = 0;
+      GM_CUDA(cudaGetDevice(&dev));
+      GM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      c.pull_grid = unsigned(sms);
+      GM_CUDA(cudaFuncSetAttribute(k_sssp_pull<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(c.pull_hub) * 4));
+      GM_CUDA(cudaFuncSetAttribute(k_sssp_pull<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(c.pull_hub) * 4));
     }
-    GM_CUDA(cudaMemsetAsync(c.msg.get(), 0xFF, n * 4, s));
+    GM_CUDA(cudaMemsetAsync(c.msg.get(), 0xFF, (n + 4) * 4, s));
   }
   const int32_t max_it = int32_t(std::min<int64_t>(max_iters, 0x7FFFFFFF));
   Ctl* ctl = c.ctl.get();
@@ -1348,14 +1449,16 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
       k_sssp_msg<<<kGrid, kThreads, 0, s>>>(ctl, c.q[cur].get(), c.dq[cur].get(), c.msg.get(), 0);
       GM_LAUNCH_CHECK();
       if (u8)
-        k_sssp_pull<uint8_t><<<kGrid, kThreads, 0, s>>>(
-            ctl, c.rowid.get(), g.in.idx.get(), g.in.val.get(), g.in.nnz, c.msg.get(),
-            g.outdeg.get(), c.dist.get(), c.changed.get(), c.q[nxt].get(), c.offs[nxt].get());
+        k_sssp_pull<uint8_t><<<c.pull_grid, kThreads, size_t(c.pull_hub) * 4, s>>>(
+            ctl, c.rowid.get(), g.in.idx.get(), g.in.val.get(), g.in.nnz, c.msg.get(), c.pull_hub,
+            c.dist.get(), c.changed.get());
       else
-        k_sssp_pull<uint32_t><<<kGrid, kThreads, 0, s>>>(
+        k_sssp_pull<uint32_t><<<c.pull_grid, kThreads, size_t(c.pull_hub) * 4, s>>>(
             ctl, c.rowid.get(), g.in.idx.get(), reinterpret_cast<const uint32_t*>(g.in.val.get()),
-            g.in.nnz, c.msg.get(), g.outdeg.get(), c.dist.get(), c.changed.get(), c.q[nxt].get(),
-            c.offs[nxt].get());
+            g.in.nnz, c.msg.get(), c.pull_hub, c.dist.get(), c.changed.get());
+      GM_LAUNCH_CHECK();
+      k_sssp_pull_queue<<<kGrid, kThreads, 0, s>>>(ctl, c.changed.get(), (n + 31) / 32,
+                                                   g.outdeg.get(), c.q[nxt].get(), c.offs[nxt].get());
       GM_LAUNCH_CHECK();
       k_sssp_msg<<<kGrid, kThreads, 0, s>>>(ctl, c.q[cur].get(), c.dq[cur].get(), c.msg.get(), 1);
       GM_LAUNCH_CHECK();

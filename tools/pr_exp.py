@@ -28,7 +28,14 @@ def main():
         r, st = gm.pagerank(g, 0.85, 20)
         ts += [s.spmv_seconds for s in st]
     med = statistics.median(ts)
-    print(json.dumps({"lib": os.environ.get("GM_LIB", "default"), "scale": scale,
+    extra = {}
+    if os.environ.get("GM_SAVE"):
+        np.save(os.environ["GM_SAVE"], r)
+    if os.environ.get("GM_CMP") and os.path.exists(os.environ["GM_CMP"]):
+        w = np.load(os.environ["GM_CMP"]).astype(np.float64)
+        extra["rel_l1_vs_cmp"] = float(np.abs(r - w).sum() / np.abs(w).sum())
+    extra["env"] = {k: v for k, v in os.environ.items() if k.startswith(("GM_PR", "GM_PB"))}
+    print(json.dumps({**extra, "lib": os.environ.get("GM_LIB", "default"), "scale": scale,
                       "nnz": g.num_edges, "median_us": round(med * 1e6, 2),
                       "min_us": round(min(ts) * 1e6, 2),
                       "gteps": round(g.num_edges / med / 1e9, 2),

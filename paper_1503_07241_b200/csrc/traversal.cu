@@ -344,14 +344,12 @@ __global__ void k_finish(Ctl* ctl, uint64_t* offs_next) {
 }
 
 // ------------------------------------------------------------------- BFS
-// Caller-order output: out[v] = visited(p) ? level[p] : -1, p = perm[v].
-__global__ void k_bfs_output(uint64_t n, const uint32_t* perm, const uint32_t* vis,
-                             const int32_t* level, int32_t* out) {
+// Caller-order output: out[v] = level[perm[v]] (level was prefilled with -1,
+// so one gather per vertex; probing the visited bitmap too cost a second).
+__global__ void k_bfs_output(uint64_t n, const uint32_t* perm, const int32_t* level, int32_t* out) {
   for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
-       v += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t p = perm ? perm[v] : uint32_t(v);
-    out[v] = bit_test(vis, p) ? level[p] : -1;
-  }
+       v += uint64_t(gridDim.x) * blockDim.x)
+    out[v] = __ldg(&level[perm ? __ldg(&perm[v]) : uint32_t(v)]);
 }
 
 // ------------------------------------------------ cooperative BFS (all supersteps)
@@ -1295,6 +1293,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   GM_CUDA(cudaMemsetAsync(ctl, 0, offsetof(Ctl, t_start), s));
   GM_CUDA(cudaMemsetAsync(c.fb[0].get(), 0, (words + 1) * 4, s));
   GM_CUDA(cudaMemsetAsync(c.fb[1].get(), 0, (words + 1) * 4, s));
+  if (out) GM_CUDA(cudaMemsetAsync(c.level.get(), 0xFF, n * 4, s));  // -1 until reached
   k_bfs_init<<<grid_for(words + 1, 256), 256, 0, s>>>(ctl, c.vis.get(), words + 1, root, perm,
                                                       c.q[1].get(), c.offs[1].get(), c.qe[1].get(),
                                                       fw.ptr.get(), g.outdeg.get(), c.level.get(), n,
@@ -1380,7 +1379,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
       if (!c.ext_out) c.ext_out.alloc(n, s);
       dst = c.ext_out.get();
     }
-    k_bfs_output<<<grid_for(n, 256), 256, 0, s>>>(n, perm, c.vis.get(), c.level.get(), dst);
+    k_bfs_output<<<grid_for(n, 256), 256, 0, s>>>(n, perm, c.level.get(), dst);
     GM_LAUNCH_CHECK();
     if (!out_on_device) GM_CUDA(cudaMemcpyAsync(out, dst, n * 4, cudaMemcpyDeviceToHost, s));
   }

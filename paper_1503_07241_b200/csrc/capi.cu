@@ -10,6 +10,7 @@
 namespace gm {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launches_so_far() { return g_launches.load(); }
 }  // namespace gm
 
 namespace {

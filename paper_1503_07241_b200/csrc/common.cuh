@@ -33,6 +33,7 @@ struct Error {
 // Every kernel launch is followed by GM_LAUNCH_CHECK(), which also counts it
 // (gm_kernel_launches(): the benchmark's launch evidence).
 void count_launch();
+uint64_t launches_so_far();
 #define GM_LAUNCH_CHECK()      \
   do {                         \
     ::gm::count_launch();      \

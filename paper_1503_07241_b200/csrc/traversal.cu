@@ -107,10 +107,14 @@ struct TravCache {
   DevBuf<Ctl> ctl;
   DevBuf<int32_t> ext_out;      // caller-order staging for host outputs
   std::unique_ptr<HostPinned<int32_t>> hdone;
-  std::vector<cudaEvent_t> ev;  // 2 per recorded superstep
   bool attrs = false;
+  // SSSP: one batch of kBatch supersteps captured as a CUDA graph (its kernels
+  // read everything else from Ctl), keyed by the launch configuration
+  cudaGraphExec_t sssp_exec = nullptr;
+  int sssp_key = -1;
+  int sssp_launches = 0;  // kernels per replay (for the launch counter)
   ~TravCache() {
-    for (auto e : ev) cudaEventDestroy(e);
+    if (sssp_exec) cudaGraphExecDestroy(sssp_exec);
   }
 };
 
@@ -316,9 +320,16 @@ __global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t roo
 }
 
 // Superstep epilogue (one thread): next frontier, stats record, termination.
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void k_finish(Ctl* ctl, uint64_t* offs_next) {
   if (ctl->done) return;
   const int32_t it = ctl->it;
+  if (it <= kMaxRecorded) ctl->t_end[it - 1] = gtimer();
   uint64_t nn, mn;
   if (ctl->dir == kPush || ctl->queue_out) {
     nn = ctl->qpack >> kCountShift;
@@ -924,7 +935,8 @@ __global__ void k_sssp_init(Ctl* ctl, uint32_t* dist, uint64_t n, uint64_t root_
 constexpr uint64_t kSsspPullDiv = 6;
 __global__ void k_sssp_decide(Ctl* ctl, int allow_pull) {
   if (ctl->done) return;
-  ++ctl->it;
+  const int32_t it = ++ctl->it;
+  if (it <= kMaxRecorded) ctl->t_start[it - 1] = gtimer();
   ctl->dir = (allow_pull && ctl->mf * kSsspPullDiv > ctl->m_total) ? kPull : kPush;
   ctl->qpack = ctl->examined = 0;
 }
@@ -1184,28 +1196,40 @@ __global__ void k_gather_out(uint64_t n, const uint32_t* perm, const T* in, T* o
     out[v] = in[perm ? perm[v] : v];
 }
 
-void ensure_events(TravCache& c, size_t need) {
-  while (c.ev.size() < need) {
-    cudaEvent_t e;
-    GM_CUDA(cudaEventCreate(&e));
-    c.ev.push_back(e);
-  }
-}
-
 // Host driver shared by BFS and SSSP: enqueue supersteps in batches of
 // kBatch, reading the device's done flag once per batch.
+// A full batch (kBatch supersteps, the first one odd, so the buffer parities
+// repeat) is captured once as a CUDA graph and replayed: a light superstep is
+// a handful of tiny kernels, and launching them one by one from the host left
+// the GPU idle ~35 us per superstep.  Superstep times come from %globaltimer
+// stamps the kernels write into Ctl.
 template <typename Enqueue>
-int64_t run_batches(TravCache& c, cudaStream_t s, int64_t max_iters, bool collect, Enqueue&& step) {
+int64_t run_batches(TravCache& c, cudaStream_t s, int64_t max_iters, int key, Enqueue&& step) {
   int32_t* done = c.hdone->get();
   int64_t enq = 0;
+  if (c.sssp_key != key && c.sssp_exec) {
+    GM_CUDA(cudaGraphExecDestroy(c.sssp_exec));
+    c.sssp_exec = nullptr;
+  }
   while (enq < max_iters) {
     const int64_t nb = std::min<int64_t>(kBatch, max_iters - enq);
-    for (int64_t b = 0; b < nb; ++b, ++enq) {
-      const bool rec = collect && enq < kMaxRecorded;
-      if (rec) ensure_events(c, size_t(2 * enq + 2));
-      if (rec) GM_CUDA(cudaEventRecord(c.ev[2 * enq], s));
-      step(enq + 1);
-      if (rec) GM_CUDA(cudaEventRecord(c.ev[2 * enq + 1], s));
+    if (nb == kBatch) {
+      if (!c.sssp_exec) {
+        cudaGraph_t graph;
+        const uint64_t l0 = launches_so_far();
+        GM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        for (int64_t b = 0; b < kBatch; ++b) step(b + 1);
+        GM_CUDA(cudaStreamEndCapture(s, &graph));
+        c.sssp_launches = int(launches_so_far() - l0);
+        GM_CUDA(cudaGraphInstantiate(&c.sssp_exec, graph, 0));
+        GM_CUDA(cudaGraphDestroy(graph));
+        c.sssp_key = key;
+      }
+      GM_CUDA(cudaGraphLaunch(c.sssp_exec, s));
+      for (int k = 0; k < c.sssp_launches; ++k) ::gm::count_launch();
+      enq += kBatch;
+    } else {
+      for (int64_t b = 0; b < nb; ++b, ++enq) step(enq + 1);
     }
     GM_CUDA(cudaMemcpyAsync(done, &c.ctl.get()->done, 4, cudaMemcpyDeviceToHost, s));
     GM_CUDA(cudaStreamSynchronize(s));
@@ -1227,6 +1251,12 @@ std::vector<gm_iteration_stats> read_records(TravCache& c, cudaStream_t s, int64
     GM_CUDA(cudaMemcpyAsync(rec.data(), c.ctl.get()->rec, nrec * sizeof(StepRec),
                             cudaMemcpyDeviceToHost, s));
   GM_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> t0(rec.size()), t1(rec.size());
+  if (nrec > 0) {
+    GM_CUDA(cudaMemcpyAsync(t0.data(), c.ctl.get()->t_start, nrec * 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaMemcpyAsync(t1.data(), c.ctl.get()->t_end, nrec * 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+  }
   for (int64_t i = 0; i < nrec; ++i) {
     const StepRec& r = rec[i];
     gm_iteration_stats st{};
@@ -1234,10 +1264,9 @@ std::vector<gm_iteration_stats> read_records(TravCache& c, cudaStream_t s, int64
     st.active_before = r.active;
     st.messages_generated = r.active;
     st.vertices_updated = r.updated;
-    float ms = 0;
-    if (i < enqueued) GM_CUDA(cudaEventElapsedTime(&ms, c.ev[2 * i], c.ev[2 * i + 1]));
-    st.spmv_seconds = ms * 1e-3;
-    st.total_seconds = ms * 1e-3;
+    const double sec = i < enqueued && t1[i] > t0[i] ? double(t1[i] - t0[i]) * 1e-9 : 0.0;
+    st.spmv_seconds = sec;
+    st.total_seconds = sec;
     st.edges_processed = r.edges;
     st.direction = r.dir == kPush ? 1 : 0;
     // pull: vis + ptr per candidate row, examined col ids, level + bitmap writes
@@ -1440,7 +1469,8 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
                                                max_it);
   GM_LAUNCH_CHECK();
   const bool u8 = g.value_type == GM_VAL_U8;
-  const int64_t enq = run_batches(c, s, max_iters, collect, [&](int64_t it) {
+  const int key = (allow_pull ? 1 : 0) | (u8 ? 2 : 0);
+  const int64_t enq = run_batches(c, s, max_iters, key, [&](int64_t it) {
     const int cur = int(it & 1), nxt = cur ^ 1;
     k_sssp_decide<<<1, 1, 0, s>>>(ctl, allow_pull ? 1 : 0);
     GM_LAUNCH_CHECK();

@@ -148,6 +148,108 @@ __global__ void __launch_bounds__(256) k_cf_items(const uint32_t* __restrict__ r
   }
 }
 
+// K % 4 == 0: a group of G = K/4 lanes per rating, lane j of the group holding
+// components [4j, 4j+4) of p, of the gathered q and of the accumulator.  The
+// lane-per-rating kernel above issues K/4 float4 loads per lane, each touching
+// 32 distinct lines per warp (one L1TEX wavefront per line, ~1 per SM cycle):
+// 5 wavefronts per rating at K = 20.  Here a group loads one q vector as one
+// contiguous K*4-byte run (1-2 lines), so a warp step of 32/G ratings costs
+// ~1.7 wavefronts per rating, and each lane keeps 12 floats instead of 3K.
+// The dot product is a G-lane shuffle sum; the item's accumulators are folded
+// over the groups in group order at the end (deterministic).
+// Sum of v over the G lanes [base, base + G) of each group, returned to every
+// lane of the group.  Shuffles run on the L1TEX data pipe, which this kernel
+// saturates, so their count matters: G = 5 folds into the group's first lane
+// with a shfl_down tree and broadcasts (4 shuffles instead of 5); a power of
+// two uses an xor butterfly; anything else a broadcast loop.
+template <int G>
+__device__ __forceinline__ float group_sum(float v, int base) {
+  if constexpr (G == 5) {
+    const float a = v + __shfl_down_sync(0xffffffffu, v, 1);  // lane base: v0+v1
+    const float b = a + __shfl_down_sync(0xffffffffu, a, 2);  // v0..v3
+    const float c = b + __shfl_down_sync(0xffffffffu, v, 4);  // v0..v4
+    return __shfl_sync(0xffffffffu, c, base & 31);
+  } else if constexpr ((G & (G - 1)) == 0) {
+    float t = v;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+  } else {
+    float t = 0.0f;
+#pragma unroll
+    for (int i = 0; i < G; ++i) t += __shfl_sync(0xffffffffu, v, (base + i) & 31);
+    return t;
+  }
+}
+
+template <int K, typename RT>
+__global__ void __launch_bounds__(256) k_cf_items_grp(const uint32_t* __restrict__ rows,
+                                                      const uint64_t* __restrict__ ibeg,
+                                                      const uint64_t* __restrict__ iend, uint64_t nit,
+                                                      const uint32_t* __restrict__ idx,
+                                                      const uint8_t* __restrict__ val,
+                                                      const float* __restrict__ f,
+                                                      float* __restrict__ part, float* __restrict__ sq) {
+  static_assert(K % 4 == 0 && K / 4 <= 32, "group kernel needs K = 4G, G <= 32");
+  constexpr int G = K / 4, NG = 32 / G;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  const int grp = int(lane) / G, j = int(lane) % G, base = grp * G;
+  const bool act = grp < NG;
+  const float4* __restrict__ f4 = reinterpret_cast<const float4*>(f);
+  for (uint64_t it = warp; it < nit; it += nwarps) {
+    const uint32_t row = rows[it];
+    const uint64_t b = ibeg[it], e1 = iend[it];
+    const float4 p = act ? f4[uint64_t(row) * G + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float s2 = 0.0f;
+    constexpr int U = 4;  // warp steps in flight
+    for (uint64_t e0 = b; e0 < e1; e0 += U * NG) {
+      float4 q[U];
+      float r[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t e = e0 + uint64_t(u * NG + grp);
+        ok[u] = act && e < e1;
+        q[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        r[u] = 0.0f;
+        if (ok[u]) {
+          q[u] = f4[uint64_t(__ldg(&idx[e])) * G + j];
+          r[u] = rating_at<RT>(val, e);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float d = p.x * q[u].x + p.y * q[u].y + p.z * q[u].z + p.w * q[u].w;
+        const float dot = group_sum<G>(d, base);
+        const float err = r[u] - dot;
+        if (ok[u]) {
+          acc.x += err * q[u].x;
+          acc.y += err * q[u].y;
+          acc.z += err * q[u].z;
+          acc.w += err * q[u].w;
+          s2 += err * err;
+        }
+      }
+    }
+    float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+    float st = 0.0f;
+#pragma unroll
+    for (int g2 = 0; g2 < NG; ++g2) {
+      const int src = g2 * G + j;
+      tot.x += __shfl_sync(0xffffffffu, acc.x, src);
+      tot.y += __shfl_sync(0xffffffffu, acc.y, src);
+      tot.z += __shfl_sync(0xffffffffu, acc.z, src);
+      tot.w += __shfl_sync(0xffffffffu, acc.w, src);
+      st += __shfl_sync(0xffffffffu, s2, g2 * G);  // every lane of a group holds the same s2
+    }
+    if (grp == 0) reinterpret_cast<float4*>(part)[it * G + j] = tot;
+    if (sq && lane == 0) sq[it] = st;
+  }
+}
+
 // p' = p + gamma * (sum - lambda * p); sum = out-route items then in-route items.
 __global__ void k_cf_apply(uint64_t n, int k, const uint32_t* rit, const uint32_t* rif,
                            const float* part_t, const float* part_f, const float* f, float* fn,
@@ -241,10 +343,27 @@ void launch_items(const CfCache& c, const Csr& csr, bool fwd, const float* f, in
   GM_LAUNCH_CHECK();
 }
 
+template <int K, typename RT>
+void launch_items_grp(const CfCache& c, const Csr& csr, bool fwd, const float* f, cudaStream_t s,
+                      float* sq) {
+  const uint64_t nit = fwd ? c.nit_f : c.nit_t;
+  if (!nit) return;
+  const unsigned grid = grid_for(nit * 32, 256);
+  k_cf_items_grp<K, RT><<<grid, 256, 0, s>>>(fwd ? c.items_f.get() : c.items_t.get(),
+                                             fwd ? c.ibeg_f.get() : c.ibeg_t.get(),
+                                             fwd ? c.iend_f.get() : c.iend_t.get(), nit,
+                                             csr.idx.get(), csr.val.get(), f,
+                                             fwd ? c.part_f.get() : c.part_t.get(), sq);
+  GM_LAUNCH_CHECK();
+}
+
 template <typename RT>
 void pass(const CfCache& c, Graph& g, bool fwd, const float* f, int k, float* sq) {
   const Csr& csr = fwd ? g.fwd() : g.in;
-  if (k == 20)
+  static const bool lane_per_rating = getenv("GM_CF_LANE") && getenv("GM_CF_LANE")[0] == '1';
+  if (k == 20 && !lane_per_rating)
+    launch_items_grp<20, RT>(c, csr, fwd, f, g.stream, sq);
+  else if (k == 20)
     launch_items<20, RT>(c, csr, fwd, f, k, g.stream, sq);
   else
     launch_items<0, RT>(c, csr, fwd, f, k, g.stream, sq);

@@ -344,6 +344,38 @@ GM_API gm_status gm_bfs_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t ro
                                    uint64_t* found, uint64_t* found_edges);
 GM_API gm_status gm_bfs_shard_levels(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                      int32_t* levels_block_host);
+/* SSSP (BSP Bellman-Ford, traversal.hpp:67-115) over the rows [row_begin,
+ * row_end) this rank owns (32-vertex aligned), u8/u32 weights.  msg_dev: the
+ * full uint32 message vector, identical on every rank -- the superstep-start
+ * distance of each frontier vertex, UINT32_MAX elsewhere (init: 0 at the
+ * root).  _step relaxes the frontier into the owned distances (pull: every
+ * owned row takes min over in-neighbours u of msg[u] + w; push: the frontier's
+ * out-edges into the block) and writes this block's next messages to
+ * msg_block_dev (the new distance of each vertex that improved, else
+ * UINT32_MAX) plus the improved count and their out-edges; the caller
+ * all-gathers the blocks into the next msg and sums the counts (pull once the
+ * frontier's out-edges exceed m/6; stop at 0 improved).  Replaces the
+ * partitioned engine.hpp:224-260 loop for SsspProgram across GPUs. */
+GM_API gm_status gm_sssp_shard_init(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                    uint64_t root_internal);
+GM_API gm_status gm_sssp_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                    const uint32_t* msg_dev, int32_t pull, uint32_t* msg_block_dev,
+                                    uint64_t* changed, uint64_t* changed_edges);
+GM_API gm_status gm_sssp_shard_dists(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                     uint32_t* dist_block_host);
+/* Collaborative filtering (CfGdProgram, collaborative_filtering.hpp:51-90,
+ * BOTH routes) over the vertices [row_begin, row_end) this rank owns.
+ * factors_full_dev: the superstep-start factors of all n vertices (internal
+ * order, n x k fp32, identical on every rank); the step writes the owned
+ * vertices' next factors to factors_block_dev ((row_end - row_begin) x k),
+ * the squared errors of the ratings stored in the owned rows of G (each
+ * rating once across the ranks: sum them for the RMSE of the input factors)
+ * and the number of owned vertices whose factors changed.  The same work
+ * items and fold order as gm_cf: the caller's all-gather of the blocks
+ * reproduces the single-GPU factors bit for bit. */
+GM_API gm_status gm_cf_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end, int32_t k,
+                                  const float* factors_full_dev, float gamma, float lambda,
+                                  float* factors_block_dev, double* sq_err_sum, uint64_t* changed);
 /* Row-block boundaries balanced by stored entries, like
  * detail::balanced_row_boundaries (dcsc.hpp:81-105).  row_nnz: n counts;
  * bounds: parts+1 entries. */

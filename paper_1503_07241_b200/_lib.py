@@ -32,6 +32,7 @@ EXPORTED = [
     "gm_edges_write_text", "gm_write_results", "gm_write_vector_results", "gm_write_report",
     "gm_fnv1a64", "gm_fnv1a64_file", "gm_measure_fp32_fma", "gm_pagerank_shard_active",
     "gm_pagerank_shard_pack", "gm_bfs_shard_init", "gm_bfs_shard_step", "gm_bfs_shard_levels",
+    "gm_sssp_shard_init", "gm_sssp_shard_step", "gm_sssp_shard_dists", "gm_cf_shard_step",
 ]
 
 
@@ -146,6 +147,12 @@ def load(path: str = LIB_PATH):
         "gm_bfs_shard_step": (C.c_int, [vp, u64, u64, vp, vp, i32, i32, vp, C.POINTER(u64),
                                         C.POINTER(u64)]),
         "gm_bfs_shard_levels": (C.c_int, [vp, u64, u64, vp]),
+        "gm_sssp_shard_init": (C.c_int, [vp, u64, u64, u64]),
+        "gm_sssp_shard_step": (C.c_int, [vp, u64, u64, vp, i32, vp, C.POINTER(u64),
+                                         C.POINTER(u64)]),
+        "gm_sssp_shard_dists": (C.c_int, [vp, u64, u64, vp]),
+        "gm_cf_shard_step": (C.c_int, [vp, u64, u64, i32, vp, C.c_float, C.c_float, vp,
+                                       C.POINTER(dp), C.POINTER(u64)]),
     }
     for name, (res, args) in proto.items():
         f = getattr(L, name)

@@ -34,6 +34,12 @@ void bfs_shard_step(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* frontier
                     const uint32_t* visited, int32_t lvl, int32_t pull, uint32_t* next_block,
                     uint64_t* found, uint64_t* found_edges);
 void bfs_shard_levels(Graph& g, uint64_t lo, uint64_t hi, int32_t* out_host);
+void cf_shard_step(Graph& g, uint64_t lo, uint64_t hi, int64_t k, const float* f_full, float gamma,
+                   float lambda, float* f_block, double* sq_sum, uint64_t* changed);
+void sssp_shard_init(Graph& g, uint64_t lo, uint64_t hi, uint64_t root_internal);
+void sssp_shard_step(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* msg, int32_t pull,
+                     uint32_t* msg_block, uint64_t* changed, uint64_t* changed_edges);
+void sssp_shard_dists(Graph& g, uint64_t lo, uint64_t hi, uint32_t* out_host);
 void pagerank_shard_pack(Graph& g, uint64_t lo, uint64_t hi, uint64_t stride, uint64_t lmax);
 // traversal.cu
 std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, int32_t* out,

@@ -403,6 +403,43 @@ GM_API gm_status gm_bfs_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t ro
   });
 }
 
+GM_API gm_status gm_cf_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end, int32_t k,
+                                  const float* factors_full_dev, float gamma, float lambda,
+                                  float* factors_block_dev, double* sq_err_sum, uint64_t* changed) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (h->n && (!factors_full_dev || (row_end > row_begin && !factors_block_dev)))
+      gm::fail(GM_EUSAGE, "null factors");
+    gm::cf_shard_step(*h, row_begin, row_end, k, factors_full_dev, gamma, lambda,
+                      factors_block_dev, sq_err_sum, changed);
+  });
+}
+
+GM_API gm_status gm_sssp_shard_init(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                    uint64_t root_internal) {
+  return guarded([&] { gm::sssp_shard_init(*handle(g), row_begin, row_end, root_internal); });
+}
+
+GM_API gm_status gm_sssp_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                    const uint32_t* msg_dev, int32_t pull, uint32_t* msg_block_dev,
+                                    uint64_t* changed, uint64_t* changed_edges) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    if (h->n && (!msg_dev || (row_end > row_begin && !msg_block_dev)))
+      gm::fail(GM_EUSAGE, "null message vector");
+    gm::sssp_shard_step(*h, row_begin, row_end, msg_dev, pull, msg_block_dev, changed,
+                        changed_edges);
+  });
+}
+
+GM_API gm_status gm_sssp_shard_dists(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                     uint32_t* dist_block_host) {
+  return guarded([&] {
+    if (!dist_block_host && row_end > row_begin) gm::fail(GM_EUSAGE, "null output");
+    gm::sssp_shard_dists(*handle(g), row_begin, row_end, dist_block_host);
+  });
+}
+
 GM_API gm_status gm_bfs_shard_levels(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                      int32_t* levels_block_host) {
   return guarded([&] {

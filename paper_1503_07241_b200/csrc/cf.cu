@@ -26,6 +26,7 @@ constexpr uint32_t kChunk = 1024;
 
 struct CfCache {
   int64_t k = 0;
+  uint64_t lo = 0, hi = 0;                  // rows covered (a rank's block when sharded)
   DevBuf<uint32_t> items_t, items_f;        // (row) per item
   DevBuf<uint64_t> ibeg_t, ibeg_f;          // item edge ranges: begin (end = next or row end)
   DevBuf<uint64_t> iend_t, iend_f;
@@ -38,17 +39,20 @@ struct CfCache {
 
 namespace {
 
-void build_items(const Csr& c, uint64_t n, DevBuf<uint32_t>& rows, DevBuf<uint64_t>& beg,
-                 DevBuf<uint64_t>& end, DevBuf<uint32_t>& rowitem, uint64_t& nit, cudaStream_t s) {
+// Work items of the rows [lo, hi); rowitem[v - lo] = the first item of row v.
+void build_items(const Csr& c, uint64_t lo, uint64_t hi, DevBuf<uint32_t>& rows,
+                 DevBuf<uint64_t>& beg, DevBuf<uint64_t>& end, DevBuf<uint32_t>& rowitem,
+                 uint64_t& nit, cudaStream_t s) {
+  const uint64_t n = hi - lo;
   std::vector<uint64_t> ptr(n + 1);
-  GM_CUDA(cudaMemcpyAsync(ptr.data(), c.ptr.get(), (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaMemcpyAsync(ptr.data(), c.ptr.get() + lo, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
   GM_CUDA(cudaStreamSynchronize(s));
   std::vector<uint32_t> r, ri(n + 1);
   std::vector<uint64_t> b, e;
   for (uint64_t v = 0; v < n; ++v) {
     ri[v] = uint32_t(r.size());
     for (uint64_t p = ptr[v]; p < ptr[v + 1]; p += kChunk) {
-      r.push_back(uint32_t(v));
+      r.push_back(uint32_t(lo + v));
       b.push_back(p);
       e.push_back(std::min<uint64_t>(ptr[v + 1], p + kChunk));
     }
@@ -251,7 +255,9 @@ __global__ void __launch_bounds__(256) k_cf_items_grp(const uint32_t* __restrict
 }
 
 // p' = p + gamma * (sum - lambda * p); sum = out-route items then in-route items.
-__global__ void k_cf_apply(uint64_t n, int k, const uint32_t* rit, const uint32_t* rif,
+// Rows [lo, lo + n): rit / rif are indexed by v - lo, f by the global row, fn
+// by the local one (the single-GPU call passes lo = 0).
+__global__ void k_cf_apply(uint64_t lo, uint64_t n, int k, const uint32_t* rit, const uint32_t* rif,
                            const float* part_t, const float* part_f, const float* f, float* fn,
                            float gamma, float lambda, unsigned long long* changed) {
   unsigned long long ch = 0;
@@ -273,7 +279,7 @@ __global__ void k_cf_apply(uint64_t n, int k, const uint32_t* rit, const uint32_
       anyi = true;
     }
     if (anyi) s = any ? s + si : si;
-    const float p = f[t];
+    const float p = f[lo * uint64_t(k) + t];
     const float np = p + gamma * (s - lambda * p);
     fn[t] = np;
     ch += (__float_as_uint(np) != __float_as_uint(p)) && (any || anyi);
@@ -369,17 +375,81 @@ void pass(const CfCache& c, Graph& g, bool fwd, const float* f, int k, float* sq
     launch_items<0, RT>(c, csr, fwd, f, k, g.stream, sq);
 }
 
-}  // namespace
+void run_pass_on(const CfCache& c, Graph& g, bool fwd, const float* f, int k, float* sq) {
+  switch (g.value_type) {
+    case GM_VAL_U8: pass<uint8_t>(c, g, fwd, f, k, sq); break;
+    case GM_VAL_F32: pass<float>(c, g, fwd, f, k, sq); break;
+    default: pass<double>(c, g, fwd, f, k, sq); break;
+  }
+}
 
-std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
-                                   const float* init, float* out, double* rmse_trace,
-                                   bool on_device) {
+void check_cf_args(int64_t k, float gamma, float lambda, const Graph& g) {
   if (k <= 0) fail(GM_EINPUT, "cf: k must be positive");
   if (k > 64) fail(GM_EUSAGE, "cf: k above 64 is not supported");
   if (!(gamma > 0.0f)) fail(GM_EINPUT, "cf: gamma must be positive");
   if (!(lambda >= 0.0f)) fail(GM_EINPUT, "cf: lambda must be non-negative");
   if (g.value_type != GM_VAL_U8 && g.value_type != GM_VAL_F32 && g.value_type != GM_VAL_F64)
     fail(GM_EUSAGE, "cf: ratings must be stored as u8, f32 or f64");
+}
+
+}  // namespace
+
+// ---- row-sharded superstep: rank r owns the vertices [lo, hi) of
+// the bipartite graph and writes only their factors.  Every rank holds the
+// full factor matrix of the superstep start (identical everywhere, S3); the
+// step runs both routes over the owned rows only -- the same work items, item
+// kernels and fixed-order fold as the single-GPU superstep, so the factors are
+// bitwise those of gm_cf -- and the caller all-gathers the blocks.
+void cf_shard_step(Graph& g, uint64_t lo, uint64_t hi, int64_t k, const float* f_full, float gamma,
+                   float lambda, float* f_block, double* sq_sum, uint64_t* changed) {
+  check_cf_args(k, gamma, lambda, g);
+  if (lo > hi || hi > g.n) fail(GM_EUSAGE, "cf shard: bad row block");
+  cudaStream_t s = g.stream;
+  ensure_forward(g);
+  if (!g.cf_shard || g.cf_shard->k != k || g.cf_shard->lo != lo || g.cf_shard->hi != hi) {
+    g.cf_shard = std::unique_ptr<CfCache, void (*)(CfCache*)>(new CfCache(), [](CfCache* p) { delete p; });
+    CfCache& c = *g.cf_shard;
+    c.k = k;
+    c.lo = lo;
+    c.hi = hi;
+    build_items(g.in, lo, hi, c.items_t, c.ibeg_t, c.iend_t, c.rowitem_t, c.nit_t, s);
+    build_items(g.fwd(), lo, hi, c.items_f, c.ibeg_f, c.iend_f, c.rowitem_f, c.nit_f, s);
+    c.part_t.alloc((c.nit_t + 1) * k, s);
+    c.part_f.alloc((c.nit_f + 1) * k, s);
+    c.sq.alloc(c.nit_f + 1, s);
+  }
+  CfCache& c = *g.cf_shard;
+  DevBuf<unsigned long long> upd(1, s);
+  DevBuf<double> sqsum(1, s), sqpart(kSqBlocks, s);
+  upd.zero(s);
+  sqsum.zero(s);
+  run_pass_on(c, g, false, f_full, int(k), nullptr);
+  run_pass_on(c, g, true, f_full, int(k), c.sq.get());
+  const uint64_t total = (hi - lo) * uint64_t(k);
+  if (total) {
+    k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(lo, hi - lo, int(k), c.rowitem_t.get(),
+                                                    c.rowitem_f.get(), c.part_t.get(), c.part_f.get(),
+                                                    f_full, f_block, gamma, lambda, upd.get());
+    GM_LAUNCH_CHECK();
+  }
+  if (c.nit_f) {
+    k_sum_sq_part<<<kSqBlocks, 256, 0, s>>>(c.sq.get(), c.nit_f, sqpart.get());
+    k_sum_sq_final<<<1, 256, 0, s>>>(sqpart.get(), kSqBlocks, sqsum.get());
+    GM_LAUNCH_CHECK();
+  }
+  unsigned long long hu = 0;
+  double hs = 0.0;
+  GM_CUDA(cudaMemcpyAsync(&hu, upd.get(), 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaMemcpyAsync(&hs, sqsum.get(), 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  if (sq_sum) *sq_sum = hs;
+  if (changed) *changed = hu;
+}
+
+std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambda, int64_t iters,
+                                   const float* init, float* out, double* rmse_trace,
+                                   bool on_device) {
+  check_cf_args(k, gamma, lambda, g);
   const uint64_t n = g.n;
   cudaStream_t s = g.stream;
   std::vector<gm_iteration_stats> stats;
@@ -403,8 +473,8 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
     g.cf = std::unique_ptr<CfCache, void (*)(CfCache*)>(new CfCache(), [](CfCache* p) { delete p; });
     CfCache& c = *g.cf;
     c.k = k;
-    build_items(g.in, n, c.items_t, c.ibeg_t, c.iend_t, c.rowitem_t, c.nit_t, s);
-    build_items(g.fwd(), n, c.items_f, c.ibeg_f, c.iend_f, c.rowitem_f, c.nit_f, s);
+    build_items(g.in, 0, n, c.items_t, c.ibeg_t, c.iend_t, c.rowitem_t, c.nit_t, s);
+    build_items(g.fwd(), 0, n, c.items_f, c.ibeg_f, c.iend_f, c.rowitem_f, c.nit_f, s);
     c.part_t.alloc((c.nit_t + 1) * k, s);
     c.part_f.alloc((c.nit_f + 1) * k, s);
     c.sq.alloc(c.nit_f + 1, s);
@@ -451,7 +521,7 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
     run_pass(false, f, nullptr);  // items receive from users (G^T)
     run_pass(true, f, c.sq.get());  // users receive from items (G); squared errors
     if (total)
-      k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
+      k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(0, n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
                                                       c.part_t.get(), c.part_f.get(), f, fn, gamma,
                                                       lambda, upd.get() + it);
     GM_LAUNCH_CHECK();

@@ -28,6 +28,7 @@ struct PrHubCache; // pagerank_hub.cu
 struct TravCache;  // traversal.cu
 struct CfCache;    // cf.cu
 struct BfsShardCache;  // bfs_shard.cu
+struct SsspShardCache;  // sssp_shard.cu
 
 struct Graph {
   uint64_t n = 0, m = 0;
@@ -55,7 +56,9 @@ struct Graph {
   std::unique_ptr<PrHubCache, void (*)(PrHubCache*)> prhub{nullptr, nullptr};
   std::unique_ptr<TravCache, void (*)(TravCache*)> trav{nullptr, nullptr};
   std::unique_ptr<CfCache, void (*)(CfCache*)> cf{nullptr, nullptr};
+  std::unique_ptr<CfCache, void (*)(CfCache*)> cf_shard{nullptr, nullptr};
   std::unique_ptr<BfsShardCache, void (*)(BfsShardCache*)> bfs_shard{nullptr, nullptr};
+  std::unique_ptr<SsspShardCache, void (*)(SsspShardCache*)> sssp_shard{nullptr, nullptr};
 
   const Csr& fwd() const { return out_alias ? in : out; }
   uint64_t device_bytes() const;

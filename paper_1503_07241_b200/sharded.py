@@ -1,4 +1,4 @@
-"""Multi-GPU PageRank: 1-D row sharding of G^T, one process per GPU.
+"""Multi-GPU PageRank, BFS and SSSP: 1-D row sharding of G^T, one process per GPU.
 
 The reference partitions G^T into row blocks that own disjoint destination
 rows (include/semigraph/dcsc.hpp:77-105) and every partition reads the whole
@@ -207,3 +207,133 @@ def sharded_bfs(backend, exchange, n: int, m: int, root: int, root_degree: int):
         steps.append(("pull" if pull else "push", nf))
         prev_pull = pull
     return backend.levels(), steps
+
+
+# ---------------------------------------------------------------- SSSP
+
+UINT32_INF = 0xFFFFFFFF
+SSSP_PULL_DIV = 6  # pull once the frontier's out-edges exceed m / 6 (csrc/traversal.cu)
+
+
+class GpuSsspShardBackend:
+    """SSSP kernels on this rank's row block (C ABI gm_sssp_shard_*).  `msg` is
+    the full uint32 message vector on the device (held as int32: UINT32_MAX is
+    -1), identical on every rank; `msg_block` receives this block's next
+    messages."""
+
+    def __init__(self, g, lo, hi):
+        import torch
+        self.g, self.lo, self.hi = g, lo, hi
+        self.msg = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+        self.msg_block = torch.empty(max(hi - lo, 1), dtype=torch.int32, device="cuda")[: hi - lo]
+        self._stream = None
+
+    def init(self, root):
+        _check(L.load().gm_sssp_shard_init(self.g._h, self.lo, self.hi, root))
+        self.msg.fill_(-1)
+        self.msg[root] = 0
+
+    def step(self, pull):
+        import torch
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        c, ce = C.c_uint64(), C.c_uint64()
+        _check(L.load().gm_sssp_shard_step(self.g._h, self.lo, self.hi, self.msg.data_ptr(),
+                                           1 if pull else 0, self.msg_block.data_ptr(),
+                                           C.byref(c), C.byref(ce)))
+        return int(c.value), int(ce.value)
+
+    def dists(self):
+        out = np.empty(self.hi - self.lo, np.uint32)
+        _check(L.load().gm_sssp_shard_dists(self.g._h, self.lo, self.hi, out.ctypes.data))
+        return out
+
+
+def sharded_sssp(backend, exchange, n: int, m: int, root: int, root_degree: int,
+                 max_iters=None):
+    """SSSP distances of this rank's block (internal ids; UINT32_MAX unreached).
+    Per superstep (run_distance_program, traversal.hpp:95-115): the local pull
+    or push into the block's distances and next messages, a sum all-reduce of
+    (improved, their out-edges), and one all-gather of the message blocks (the
+    next superstep's snapshots everywhere).  The direction rule is the
+    single-GPU one: pull once the frontier's out-edges exceed m / 6.
+    Returns (distances, per-superstep (direction, active_before, updated))."""
+    backend.init(root)
+    nf, mf, it = 1, root_degree, 0
+    cap = n + 1 if max_iters is None else max_iters
+    steps = []
+    while nf > 0 and it < cap:
+        it += 1
+        pull = mf * SSSP_PULL_DIV > m
+        c, ce = backend.step(pull)
+        c = int(round(exchange.allreduce_sum(float(c), backend.msg)))
+        ce = int(round(exchange.allreduce_sum(float(ce), backend.msg)))
+        exchange.allgather_into(backend.msg, backend.msg_block)
+        steps.append(("pull" if pull else "push", nf, c))
+        nf, mf = c, ce
+    return backend.dists(), steps
+
+
+# ---------------------------------------------------------------- CF
+
+class GpuCfShardBackend:
+    """Collaborative-filtering kernels on this rank's vertex block (C ABI
+    gm_cf_shard_step).  `full` holds the superstep-start factors of all n
+    vertices (internal order, n x k fp32), identical on every rank; `block`
+    receives the owned vertices' next factors."""
+
+    def __init__(self, g, lo, hi, k=20):
+        import torch
+        self.g, self.lo, self.hi, self.k = g, lo, hi, k
+        self.full = torch.empty((g.num_vertices, k), dtype=torch.float32, device="cuda")
+        self.block = torch.empty((max(hi - lo, 1), k), dtype=torch.float32, device="cuda")[: hi - lo]
+        self._stream = None
+
+    def init(self, factors_internal):
+        import torch
+        self.full.copy_(torch.as_tensor(factors_internal, dtype=torch.float32))
+
+    def step(self, gamma, lam):
+        import torch
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        sq, ch = C.c_double(), C.c_uint64()
+        _check(L.load().gm_cf_shard_step(self.g._h, self.lo, self.hi, self.k, self.full.data_ptr(),
+                                         gamma, lam, self.block.data_ptr(), C.byref(sq),
+                                         C.byref(ch)))
+        return float(sq.value), int(ch.value)
+
+    def factors(self):
+        return self.full[self.lo:self.hi].cpu().numpy()
+
+
+def sharded_cf(backend, exchange, m: int, gamma=1e-3, lam=0.05, iterations=10):
+    """collaborative_filtering_gd (collaborative_filtering.hpp:134-211) with the
+    vertices row-sharded: per superstep each rank updates its block from the
+    full superstep-start factors, the ranks sum-reduce (squared errors,
+    changed) and all-gather the factor blocks.  The squared errors a step
+    returns belong to its *input* factors, so RMSE after update t comes from
+    step t + 1, and one extra evaluation after the last update closes the
+    trace (as gm_cf does).  Returns (this block's final factors, rmse trace,
+    vertices_updated per superstep)."""
+    import math
+    rmse, updated = [], []
+    for it in range(iterations):
+        sq, ch = backend.step(gamma, lam)
+        sq = exchange.allreduce_sum(sq, backend.full)
+        updated.append(int(round(exchange.allreduce_sum(float(ch), backend.full))))
+        if it > 0:
+            rmse.append(math.sqrt(sq / m) if m else 0.0)
+        exchange.allgather_into(backend.full.view(-1), backend.block.reshape(-1))
+    final = backend.factors().copy()
+    if iterations > 0:
+        sq, _ = backend.step(gamma, lam)
+        sq = exchange.allreduce_sum(sq, backend.full)
+        rmse.append(math.sqrt(sq / m) if m else 0.0)
+    return final, rmse, updated

@@ -462,3 +462,88 @@ def test_sharded_bfs_virtual_shards(gm, orc):
     s, d, _ = g0.edges()
     want, _ = orc.bfs(n, s, d, root_ext, presorted=True)
     assert np.array_equal(lv_int[perm], want)
+
+
+def test_sharded_sssp_virtual_shards(gm, orc):
+    """Row-sharded SSSP (gm_sssp_shard_*) with P blocks run one after another
+    on one GPU; the all-gather is a device concatenation of the message
+    blocks.  Distances and per-superstep counts equal the oracle's; both
+    directions are exercised."""
+    import torch
+
+    from paper_1503_07241_b200.sharded import SSSP_PULL_DIV, GpuSsspShardBackend, row_block
+    P, scale = 4, 16
+    n = 1 << scale
+    graphs = [gm.Graph.rmat(scale, 16, seed=13, weights=True, relabel=True, shards=P)
+              for _ in range(P)]
+    bes = [GpuSsspShardBackend(graphs[r], *row_block(n, P, r)) for r in range(P)]
+    g0 = graphs[0]
+    perm = g0.permutation()
+    root_ext = g0.pick_source(13)
+    root = int(perm[root_ext])
+    deg_int = np.empty(n, np.int64)
+    deg_int[perm] = g0.degree_vector("out")
+    for b in bes:
+        b.init(root)
+    nf, mf, dirs, got = 1, int(deg_int[root]), [], []
+    while nf > 0:
+        pull = mf * SSSP_PULL_DIV > g0.num_edges
+        res = [b.step(pull) for b in bes]
+        c, ce = sum(r[0] for r in res), sum(r[1] for r in res)
+        nxt = torch.cat([b.msg_block for b in bes])
+        for b in bes:
+            b.msg.copy_(nxt)
+        dirs.append(pull)
+        got.append((nf, c))
+        nf, mf = c, ce
+    assert any(dirs) and not all(dirs)
+    d_int = np.concatenate([b.dists() for b in bes])
+    s, d, w = g0.edges()
+    want, wst = orc.sssp(n, s, d, w, root_ext, presorted=True)
+    assert np.array_equal(d_int[perm], want)
+    assert got == [(t[1], t[3]) for t in wst]
+
+
+def test_sharded_cf_virtual_shards_bitwise(gm):
+    """Row-sharded CF (gm_cf_shard_step) with P vertex blocks run one after
+    another on one GPU, the all-gather a device concatenation: the same work
+    items and fold order as gm_cf, so factors and RMSE trace are bitwise the
+    single-GPU ones, and the per-superstep update counts equal."""
+    import torch
+
+    from paper_1503_07241_b200.sharded import GpuCfShardBackend, row_block
+
+    P, k, iters = 4, 20, 4
+    users, items = 3000, 200
+    g = gm.Graph.bipartite(users, items, 12000.0, items, seed=5)
+    n = g.num_vertices
+    n_pad = (n + P - 1) // P * P
+    rng = np.random.default_rng(5)
+    init = rng.uniform(0, 0.1, (n, k)).astype(np.float32)
+    want_f, want_rmse, want_st = gm.collaborative_filtering_gd(g, k, 1e-3, 0.05, iters, init=init)
+    perm = g.permutation()
+    f_int = np.empty_like(init)
+    f_int[perm] = init
+    graphs = [gm.Graph.bipartite(users, items, 12000.0, items, seed=5) for _ in range(P)]
+    bounds = [row_block(n_pad, P, r) for r in range(P)]
+    bounds = [(min(lo, n), min(hi, n)) for lo, hi in bounds]
+    bes = [GpuCfShardBackend(graphs[r], *bounds[r], k=k) for r in range(P)]
+    for b in bes:
+        b.init(f_int)
+    m = g.num_edges
+    rmse, upd = [], []
+    for it in range(iters + 1):
+        res = [b.step(1e-3, 0.05) for b in bes]
+        sq = sum(r[0] for r in res)
+        if it > 0:
+            rmse.append(np.sqrt(sq / m))
+        if it == iters:
+            break
+        upd.append(sum(r[1] for r in res))
+        nxt = torch.cat([b.block for b in bes])
+        for b in bes:
+            b.full.copy_(nxt)
+    got = bes[0].full.cpu().numpy()[perm]
+    assert np.array_equal(got.view(np.uint32), want_f.view(np.uint32))
+    np.testing.assert_allclose(rmse, want_rmse, rtol=1e-12)
+    assert upd == [s.vertices_updated for s in want_st]

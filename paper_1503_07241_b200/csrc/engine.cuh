@@ -119,8 +119,13 @@ __global__ void k_send(P p, uint64_t n, const typename P::vertex_t* props, const
   }
 }
 
+// Rows longer than this go to k_pull_long (a warp per row).
+constexpr uint64_t kLongRow = 32;
+
 // Phase 2, engine.hpp:224-260: one thread per destination row, entries in
 // ascending source order, first contribution folded as reduce(identity, r).
+// Rows with more than kLongRow entries are left to k_pull_long (launched
+// after this kernel: it ORs its rows' bits into the words written here).
 template <typename P>
 __global__ void k_pull(P p, uint64_t n, const uint64_t* ptr, const uint32_t* idx,
                        const uint8_t* val, const typename P::message_t* x, const uint32_t* xbits,
@@ -133,7 +138,7 @@ __global__ void k_pull(P p, uint64_t n, const uint64_t* ptr, const uint32_t* idx
   for (uint64_t w = warp; w < words; w += nwarps) {
     const uint64_t k = w * 32 + lane_id();
     bool any = false;
-    if (k < n) {
+    if (k < n && ptr[k + 1] - ptr[k] <= kLongRow) {
       R acc = p.reduce_identity();
       const uint64_t e1 = ptr[k + 1];
       for (uint64_t e = ptr[k]; e < e1; ++e) {
@@ -159,6 +164,80 @@ __global__ void k_pull(P p, uint64_t n, const uint64_t* ptr, const uint32_t* idx
     if (lane_id() == 0) ybits[w] = b;
   }
 }
+
+// Long rows (> kLongRow entries): a warp per row.  The 32 lanes evaluate 32
+// consecutive entries at once (bit test, message load, process_message) and
+// stage the results in shared memory; lane 0 then folds them strictly in entry
+// order -- the reference's per-row order, so any reduce, associative or not,
+// gives the thread-per-row result bit for bit -- while the next 32 entries'
+// loads are the warp's only other work.  The first failing entry of a row (in
+// entry order) is the one reported.
+constexpr unsigned kLongThreads = 256;
+
+template <typename P>
+__global__ void __launch_bounds__(kLongThreads) k_pull_long(
+    P p, const uint32_t* rows, uint64_t nrows, const uint64_t* ptr, const uint32_t* idx,
+    const uint8_t* val, const typename P::message_t* x, const uint32_t* xbits,
+    const typename P::vertex_t* props, const uint32_t* iperm, typename P::reduced_t* y,
+    uint32_t* ybits, DevError* err) {
+  using R = typename P::reduced_t;
+  __shared__ __align__(16) unsigned char s_raw[kLongThreads * sizeof(R)];
+  R* s_r = reinterpret_cast<R*>(s_raw) + (threadIdx.x & ~31u);
+  const unsigned lane = lane_id();
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t i = warp; i < nrows; i += nwarps) {
+    const uint32_t k = rows[i];
+    const uint64_t e0 = ptr[k], e1 = ptr[k + 1];
+    R acc = p.reduce_identity();
+    bool any = false;
+    for (uint64_t base = e0; base < e1; base += 32) {
+      const uint64_t e = base + lane;
+      bool valid = false;
+      int ec = 0;
+      uint32_t j = 0;
+      R r{};
+      if (e < e1) {
+        j = idx[e];
+        if (bit_test(xbits, j)) {
+          valid = true;
+          if constexpr (can_fail<P>::value)
+            r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k], ec);
+          else
+            r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k]);
+        }
+      }
+      if constexpr (can_fail<P>::value) {
+        const unsigned fm = __ballot_sync(0xffffffffu, ec != 0);
+        if (fm) {  // the row's first failing entry; the superstep aborts
+          if (int(lane) == __ffs(fm) - 1)
+            record_error(err, ec, kPhaseSpmv, 0, ext_id(iperm, j), ext_id(iperm, k));
+          any = false;
+          break;
+        }
+      }
+      if (valid) s_r[lane] = r;
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      __syncwarp();
+      if (lane == 0) {
+        for (unsigned m = vm; m; m &= m - 1) {
+          const R& v = s_r[__ffs(m) - 1];
+          acc = any ? p.reduce(acc, v) : p.reduce(p.reduce_identity(), v);
+          any = true;
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0 && any) {
+      y[k] = acc;
+      atomicOr(&ybits[k >> 5], 1u << (k & 31u));
+    }
+  }
+}
+
+// Row ids with more than kLongRow entries (order irrelevant: rows are independent).
+__global__ void k_long_rows(uint64_t n, const uint64_t* ptr, uint32_t* rows,
+                            unsigned long long* cnt);
 
 // BOTH merge, engine.hpp:113-126: y_in folded into y_out, out-route first.
 template <typename P>
@@ -309,21 +388,49 @@ class Engine {
     GM_LAUNCH_CHECK();
   }
 
+  // rows of `c` with more than kLongRow entries, once per engine and CSR
+  uint64_t long_rows(const Csr& c, DevBuf<uint32_t>& rows) {
+    const uint64_t n = g_.n;
+    rows.alloc(n + 1, s_);
+    DevBuf<unsigned long long> cnt(1, s_);
+    cnt.zero(s_);
+    if (n) {
+      k_long_rows<<<grid_for(n, 256), 256, 0, s_>>>(n, c.ptr.get(), rows.get(), cnt.get());
+      GM_LAUNCH_CHECK();
+    }
+    unsigned long long h = 0;
+    GM_CUDA(cudaMemcpyAsync(&h, cnt.get(), 8, cudaMemcpyDeviceToHost, s_));
+    GM_CUDA(cudaStreamSynchronize(s_));
+    return h;
+  }
+
+  void pull(const Csr& c, DevBuf<uint32_t>& lrows, uint64_t& nlong, bool& have, R* y,
+            uint32_t* ybits) {
+    const uint64_t n = g_.n;
+    if (!have) {
+      nlong = long_rows(c, lrows);
+      have = true;
+    }
+    const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
+    k_pull<P><<<grid, 256, 0, s_>>>(p_, n, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(),
+                                     xbits_.get(), props_.get(), iperm(), y, ybits, err_.get());
+    GM_LAUNCH_CHECK();
+    if (nlong) {
+      k_pull_long<P><<<grid_for(nlong * 32, kLongThreads), kLongThreads, 0, s_>>>(
+          p_, lrows.get(), nlong, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(), xbits_.get(),
+          props_.get(), iperm(), y, ybits, err_.get());
+      GM_LAUNCH_CHECK();
+    }
+  }
+
   void spmv() {
     const uint64_t n = g_.n;
     const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
     const Direction d = p_.direction();
     const Csr& first = d == Direction::IN ? g_.fwd() : g_.in;
-    k_pull<P><<<grid, 256, 0, s_>>>(p_, n, first.ptr.get(), first.idx.get(), first.val.get(),
-                                     x_.get(), xbits_.get(), props_.get(), iperm(), y_.get(),
-                                     ybits_.get(), err_.get());
-    GM_LAUNCH_CHECK();
+    pull(first, long1_, nlong1_, have1_, y_.get(), ybits_.get());
     if (d == Direction::BOTH) {
-      const Csr& f = g_.fwd();
-      k_pull<P><<<grid, 256, 0, s_>>>(p_, n, f.ptr.get(), f.idx.get(), f.val.get(), x_.get(),
-                                       xbits_.get(), props_.get(), iperm(), y2_.get(),
-                                       y2bits_.get(), err_.get());
-      GM_LAUNCH_CHECK();
+      pull(g_.fwd(), long2_, nlong2_, have2_, y2_.get(), y2bits_.get());
       k_merge<P><<<grid, 256, 0, s_>>>(p_, n, y_.get(), ybits_.get(), y2_.get(), y2bits_.get());
       GM_LAUNCH_CHECK();
     }
@@ -416,6 +523,9 @@ class Engine {
   DevBuf<uint32_t> xbits_;
   DevBuf<R> y_, y2_;
   DevBuf<uint32_t> ybits_, y2bits_;
+  DevBuf<uint32_t> long1_, long2_;  // long rows of the first / second route's CSR
+  uint64_t nlong1_ = 0, nlong2_ = 0;
+  bool have1_ = false, have2_ = false;
   DevBuf<unsigned long long> ctr_;
   DevBuf<DevError> err_;
   cudaEvent_t e0_{}, e1_{}, e2_{}, e3_{};

@@ -9,6 +9,21 @@
 
 namespace gm {
 
+__global__ void k_long_rows(uint64_t n, const uint64_t* ptr, uint32_t* rows,
+                            unsigned long long* cnt) {
+  for (uint64_t v0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~uint64_t(31); v0 < n;
+       v0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t v = v0 + lane_id();
+    const bool is_long = v < n && ptr[v + 1] - ptr[v] > kLongRow;
+    const unsigned m = __ballot_sync(0xffffffffu, is_long);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (is_long) rows[base + __popc(m & ((1u << lane_id()) - 1u))] = uint32_t(v);
+  }
+}
+
 __global__ void k_bytes_to_bits(const uint8_t* bytes, uint64_t n, uint32_t* bits) {
   const uint64_t words = (n + 31) / 32;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;

@@ -181,37 +181,59 @@ __global__ void __launch_bounds__(kLongThreads) k_pull_long(
     const typename P::vertex_t* props, const uint32_t* iperm, typename P::reduced_t* y,
     uint32_t* ybits, DevError* err) {
   using R = typename P::reduced_t;
+  using M = typename P::message_t;
+  using E = typename P::edge_t;
   __shared__ __align__(16) unsigned char s_raw[kLongThreads * sizeof(R)];
   R* s_r = reinterpret_cast<R*>(s_raw) + (threadIdx.x & ~31u);
   const unsigned lane = lane_id();
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  // Three-stage pipeline per warp: the column ids of chunk c+2 and the
+  // messages, validity words and edge values of chunk c+1 are in flight while
+  // chunk c is processed and folded (messages are loaded unconditionally --
+  // every id is in range -- so no load waits on the bit test).
+  struct Staged {
+    bool in = false;
+    uint32_t j = 0, word = 0;
+    M m{};
+    E ed{};
+  };
   for (uint64_t i = warp; i < nrows; i += nwarps) {
     const uint32_t k = rows[i];
     const uint64_t e0 = ptr[k], e1 = ptr[k + 1];
+    const typename P::vertex_t vk = props[k];
+    auto load_idx = [&](uint64_t b) { return b + lane < e1 ? idx[b + lane] : 0u; };
+    auto load_msg = [&](uint64_t b, uint32_t j, Staged& st) {
+      st.in = b + lane < e1;
+      st.j = j;
+      if (st.in) {
+        st.word = xbits[j >> 5];
+        st.m = x[j];
+        st.ed = load_edge<E>(val, b + lane);
+      }
+    };
     R acc = p.reduce_identity();
     bool any = false;
+    Staged cur, nxt;
+    load_msg(e0, load_idx(e0), cur);
+    uint32_t jn = load_idx(e0 + 32);
     for (uint64_t base = e0; base < e1; base += 32) {
-      const uint64_t e = base + lane;
-      bool valid = false;
+      if (base + 32 < e1) load_msg(base + 32, jn, nxt);
+      jn = load_idx(base + 64);
+      const bool valid = cur.in && ((cur.word >> (cur.j & 31u)) & 1u);
       int ec = 0;
-      uint32_t j = 0;
       R r{};
-      if (e < e1) {
-        j = idx[e];
-        if (bit_test(xbits, j)) {
-          valid = true;
-          if constexpr (can_fail<P>::value)
-            r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k], ec);
-          else
-            r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k]);
-        }
+      if (valid) {
+        if constexpr (can_fail<P>::value)
+          r = p.process_message(cur.m, cur.ed, vk, ec);
+        else
+          r = p.process_message(cur.m, cur.ed, vk);
       }
       if constexpr (can_fail<P>::value) {
         const unsigned fm = __ballot_sync(0xffffffffu, ec != 0);
         if (fm) {  // the row's first failing entry; the superstep aborts
           if (int(lane) == __ffs(fm) - 1)
-            record_error(err, ec, kPhaseSpmv, 0, ext_id(iperm, j), ext_id(iperm, k));
+            record_error(err, ec, kPhaseSpmv, 0, ext_id(iperm, cur.j), ext_id(iperm, k));
           any = false;
           break;
         }
@@ -219,14 +241,24 @@ __global__ void __launch_bounds__(kLongThreads) k_pull_long(
       if (valid) s_r[lane] = r;
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
       __syncwarp();
-      if (lane == 0) {
-        for (unsigned m = vm; m; m &= m - 1) {
-          const R& v = s_r[__ffs(m) - 1];
-          acc = any ? p.reduce(acc, v) : p.reduce(p.reduce_identity(), v);
-          any = true;
+      if (lane == 0 && vm) {  // in entry order; 8 staged values loaded ahead of each 8 folds
+#pragma unroll 1
+        for (int b8 = 0; b8 < 32; b8 += 8) {
+          if (!((vm >> b8) & 0xFFu)) continue;
+          R v8[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v8[t] = s_r[b8 + t];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if ((vm >> (b8 + t)) & 1u) {
+              acc = any ? p.reduce(acc, v8[t]) : p.reduce(p.reduce_identity(), v8[t]);
+              any = true;
+            }
+          }
         }
       }
       __syncwarp();
+      cur = nxt;
     }
     if (lane == 0 && any) {
       y[k] = acc;

@@ -317,6 +317,16 @@ class PageRankWorkload(Workload):
             self.exchange = TorchExchange()
             self.scaling = "strong"
             self.parallelism = f"rows{d.world}"
+            # the all-gather fused into the SpMV epilogue (CUDA IPC peer stores
+            # over NVLink); GM_PR_EXCHANGE=nccl keeps the NCCL all-gather
+            self.fused, self.exchange_kind = None, "nccl all_gather"
+            if os.environ.get("GM_PR_EXCHANGE", "fused") == "fused":
+                try:
+                    from paper_1503_07241_b200.sharded import FusedPageRank
+                    self.fused = FusedPageRank(self.backend, self.exchange, self.n)
+                    self.exchange_kind = "fused epilogue peer stores (CUDA IPC) + nccl all_reduce"
+                except Exception as e:  # e.g. no peer access: keep the NCCL path, say why
+                    self.exchange_kind = f"nccl all_gather (fused unavailable: {e})"
         import torch
         self.dev_out = torch.empty(self.n, dtype=torch.float32, device="cuda")
         self.host_out = torch.empty(self.n, dtype=torch.float32).pin_memory()
@@ -324,11 +334,14 @@ class PageRankWorkload(Workload):
         self.edges = self.m * self.iters
         self.config = {"workload": f"pagerank_rmat{a.scale}", "scale": a.scale, "edge_factor": 16,
                        "n": self.n, "m": self.m, "iterations": self.iters, "damping": 0.85,
+                       **({"exchange": self.exchange_kind} if self.sharded else {}),
                        "l2": "inputs larger than L2" if not self.flush_l2()
                        else "L2 flushed between steps (256 MB write, outside the events)"}
 
     def run_device(self, gm):
         if self.sharded:
+            if self.fused is not None:
+                return self.fused.run(0.85, self.iters)
             from paper_1503_07241_b200.sharded import sharded_pagerank
             return sharded_pagerank(self.backend, self.exchange, self.n, 0.85, self.iters)
         gm.pagerank(self.g, 0.85, self.iters, with_stats=False,

@@ -328,6 +328,33 @@ GM_API gm_status gm_pagerank_shard_active(gm_graph_t g, uint64_t row_begin, uint
                                           uint64_t* prefix_len);
 GM_API gm_status gm_pagerank_shard_pack(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                         uint64_t block_stride, uint64_t lmax);
+/* The superstep with the all-gather fused into the SpMV epilogue: instead of
+ * x_block_dev, every message of this block's gathered prefix (row - row_begin
+ * < limit) is stored at [row + offset] of each of the npeers (1..8) device
+ * buffers -- every rank's full message vector for the NEXT superstep, mapped
+ * into this process with gm_ipc_open (the local one included), so the
+ * transfer rides NVLink inside the kernel and no collective moves data.
+ * offset: 0 for the unpacked layout, rank*Lmax - row_begin for the packed one.
+ * The caller double-buffers the full vectors (read x_full_dev, write the
+ * other one) and keeps one collective per superstep as the barrier (the
+ * dangling-mass all-reduce).  _init_peers stores the initial messages the
+ * same way (instead of gm_pagerank_shard_init's x_block_dev). */
+GM_API gm_status gm_pagerank_shard_init_peers(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                              const uint64_t* peer_buffers, int32_t npeers,
+                                              int64_t offset, uint64_t limit,
+                                              double* dangling_block);
+GM_API gm_status gm_pagerank_shard_step_peers(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                              const float* x_full_dev, double base, double damping,
+                                              const uint64_t* peer_buffers, int32_t npeers,
+                                              int64_t offset, uint64_t limit,
+                                              double* dangling_block);
+/* Device buffers shareable across processes (cudaMalloc + CUDA IPC): a
+ * 64-byte handle per buffer, opened by the peers into their address space. */
+GM_API gm_status gm_ipc_alloc(uint64_t bytes, void** dev_ptr);
+GM_API gm_status gm_ipc_free(void* dev_ptr);
+GM_API gm_status gm_ipc_handle(void* dev_ptr, void* handle64);
+GM_API gm_status gm_ipc_open(const void* handle64, void** dev_ptr);
+GM_API gm_status gm_ipc_close(void* dev_ptr);
 /* BFS over the rows [row_begin, row_end) of a symmetric graph this rank owns
  * (32-vertex aligned; GM_SHARDS(P) blocks).  All bitmaps are device u32 words
  * in internal ids: frontier_dev / visited_dev cover all n vertices and are

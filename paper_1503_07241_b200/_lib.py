@@ -33,6 +33,8 @@ EXPORTED = [
     "gm_fnv1a64", "gm_fnv1a64_file", "gm_measure_fp32_fma", "gm_pagerank_shard_active",
     "gm_pagerank_shard_pack", "gm_bfs_shard_init", "gm_bfs_shard_step", "gm_bfs_shard_levels",
     "gm_sssp_shard_init", "gm_sssp_shard_step", "gm_sssp_shard_dists", "gm_cf_shard_step",
+    "gm_pagerank_shard_step_peers", "gm_pagerank_shard_init_peers", "gm_ipc_alloc", "gm_ipc_free", "gm_ipc_handle", "gm_ipc_open",
+    "gm_ipc_close",
 ]
 
 
@@ -153,6 +155,15 @@ def load(path: str = LIB_PATH):
         "gm_sssp_shard_dists": (C.c_int, [vp, u64, u64, vp]),
         "gm_cf_shard_step": (C.c_int, [vp, u64, u64, i32, vp, C.c_float, C.c_float, vp,
                                        C.POINTER(dp), C.POINTER(u64)]),
+        "gm_pagerank_shard_step_peers": (C.c_int, [vp, u64, u64, vp, dp, dp, vp, i32, i64, u64,
+                                                   C.POINTER(dp)]),
+        "gm_pagerank_shard_init_peers": (C.c_int, [vp, u64, u64, vp, i32, i64, u64,
+                                                   C.POINTER(dp)]),
+        "gm_ipc_alloc": (C.c_int, [u64, C.POINTER(vp)]),
+        "gm_ipc_free": (C.c_int, [vp]),
+        "gm_ipc_handle": (C.c_int, [vp, vp]),
+        "gm_ipc_open": (C.c_int, [vp, C.POINTER(vp)]),
+        "gm_ipc_close": (C.c_int, [vp]),
     }
     for name, (res, args) in proto.items():
         f = getattr(L, name)

@@ -29,6 +29,11 @@ double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_fu
                            double damping, float* x_block);
 void pagerank_shard_ranks(Graph& g, uint64_t lo, uint64_t hi, float* out_host);
 uint64_t pagerank_shard_active(Graph& g, uint64_t lo, uint64_t hi);
+double pagerank_shard_init_peers(Graph& g, uint64_t lo, uint64_t hi, float* const* peers,
+                                 int npeers, int64_t offset, uint64_t limit);
+double pagerank_shard_step_peers(Graph& g, uint64_t lo, uint64_t hi, const float* x_full,
+                                 double base, double damping, float* const* peers, int npeers,
+                                 int64_t offset, uint64_t limit);
 void bfs_shard_init(Graph& g, uint64_t lo, uint64_t hi, uint64_t root_internal);
 void bfs_shard_step(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* frontier,
                     const uint32_t* visited, int32_t lvl, int32_t pull, uint32_t* next_block,

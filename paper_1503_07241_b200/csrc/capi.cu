@@ -366,6 +366,76 @@ GM_API gm_status gm_pagerank_shard_step(gm_graph_t g, uint64_t row_begin, uint64
   });
 }
 
+GM_API gm_status gm_pagerank_shard_step_peers(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                              const float* x_full_dev, double base, double damping,
+                                              const uint64_t* peer_buffers, int32_t npeers,
+                                              int64_t offset, uint64_t limit,
+                                              double* dangling_block) {
+  return guarded([&] {
+    if (!peer_buffers || npeers < 1) gm::fail(GM_EUSAGE, "null peer buffers");
+    std::vector<float*> peers(static_cast<size_t>(npeers));
+    for (int32_t q = 0; q < npeers; ++q) peers[q] = reinterpret_cast<float*>(peer_buffers[q]);
+    const double d = gm::pagerank_shard_step_peers(*handle(g), row_begin, row_end, x_full_dev,
+                                                   base, damping, peers.data(), npeers, offset,
+                                                   limit);
+    if (dangling_block) *dangling_block = d;
+  });
+}
+
+GM_API gm_status gm_pagerank_shard_init_peers(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                              const uint64_t* peer_buffers, int32_t npeers,
+                                              int64_t offset, uint64_t limit,
+                                              double* dangling_block) {
+  return guarded([&] {
+    if (!peer_buffers || npeers < 1) gm::fail(GM_EUSAGE, "null peer buffers");
+    std::vector<float*> peers(static_cast<size_t>(npeers));
+    for (int32_t q = 0; q < npeers; ++q) peers[q] = reinterpret_cast<float*>(peer_buffers[q]);
+    const double d = gm::pagerank_shard_init_peers(*handle(g), row_begin, row_end, peers.data(),
+                                                   npeers, offset, limit);
+    if (dangling_block) *dangling_block = d;
+  });
+}
+
+GM_API gm_status gm_ipc_alloc(uint64_t bytes, void** dev_ptr) {
+  return guarded([&] {
+    if (!dev_ptr) gm::fail(GM_EUSAGE, "null output");
+    *dev_ptr = nullptr;
+    GM_CUDA(cudaMalloc(dev_ptr, bytes ? bytes : 1));
+  });
+}
+
+GM_API gm_status gm_ipc_free(void* dev_ptr) {
+  return guarded([&] {
+    if (dev_ptr) GM_CUDA(cudaFree(dev_ptr));
+  });
+}
+
+GM_API gm_status gm_ipc_handle(void* dev_ptr, void* handle64) {
+  return guarded([&] {
+    if (!dev_ptr || !handle64) gm::fail(GM_EUSAGE, "null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+    cudaIpcMemHandle_t h;
+    GM_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+    memcpy(handle64, &h, 64);
+  });
+}
+
+GM_API gm_status gm_ipc_open(const void* handle64, void** dev_ptr) {
+  return guarded([&] {
+    if (!handle64 || !dev_ptr) gm::fail(GM_EUSAGE, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    *dev_ptr = nullptr;
+    GM_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+GM_API gm_status gm_ipc_close(void* dev_ptr) {
+  return guarded([&] {
+    if (dev_ptr) GM_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  });
+}
+
 GM_API gm_status gm_pagerank_shard_ranks(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                          float* ranks_block_host) {
   return guarded([&] { gm::pagerank_shard_ranks(*handle(g), row_begin, row_end, ranks_block_host); });

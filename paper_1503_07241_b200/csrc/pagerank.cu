@@ -176,14 +176,35 @@ __device__ __forceinline__ float block_sum(float v, float* scratch) {
   return t;
 }
 
+// Fused all-gather (multi-GPU shards): the epilogue stores each message
+// straight into every rank's full message vector over NVLink peer memory
+// (CUDA IPC mappings; the local buffer is one of them), at row + off, for
+// the rows of the block's gathered prefix (row - lo < lim).  n == 0: the
+// message goes to x_next only.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  float* p[kMaxPeers];
+  uint32_t n;
+  int64_t off;
+  uint64_t lo, lim;
+};
+
 // Apply + send for one row: stores only, plus the inv read.
 __device__ __forceinline__ void pr_write(uint64_t row, float sum, float base, float damping,
                                          const float* __restrict__ inv, float* __restrict__ rank,
-                                         float* __restrict__ x_next, float& dangling) {
+                                         float* __restrict__ x_next, const PeerOut& po,
+                                         float& dangling) {
   const float r = base + damping * sum;
   rank[row] = r;
   const float iv = __ldg(&inv[row]);
-  x_next[row] = r * iv;
+  const float x = r * iv;
+  if (po.n == 0) {
+    x_next[row] = x;
+  } else if (row - po.lo < po.lim) {
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+      if (q < int(po.n)) po.p[q][int64_t(row) + po.off] = x;
+  }
   if (iv == 0.0f) dangling += r;
 }
 
@@ -209,6 +230,7 @@ struct PrArgs {
   float* chunk_sum;            // [nchunks]
   unsigned* slot_ticket;       // [n_long] arrivals this superstep (reset by the last)
   float* dang_partial;
+  PeerOut peers;
 };
 
 // A long row is cut into chunks of kTile nonzeros, one CTA each (all gathers
@@ -242,7 +264,7 @@ __device__ __forceinline__ void pr_chunk(const PrArgs& a, float* s_red) {
   for (uint32_t i = 0; i < nch; ++i) sum += __ldcg(&a.chunk_sum[f + i]);
   a.slot_ticket[slot] = 0;
   float dangling = 0.0f;
-  pr_write(row, sum, a.scalars[0], a.damping, a.inv, a.rank, a.x_next, dangling);
+  pr_write(row, sum, a.scalars[0], a.damping, a.inv, a.rank, a.x_next, a.peers, dangling);
   a.dang_partial[a.ntiles + slot] = dangling;
 }
 
@@ -299,7 +321,7 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_spmv(const PrArgs a) {
         has_first = true;
         first_val = run;
       } else {
-        pr_write(r0 + ti, run, base, damping, a.inv, a.rank, a.x_next, dangling);
+        pr_write(r0 + ti, run, base, damping, a.inv, a.rank, a.x_next, a.peers, dangling);
       }
       run = 0.0f;
       ++ti;
@@ -344,7 +366,8 @@ __global__ void __launch_bounds__(kPrThreads) k_pr_spmv(const PrArgs a) {
   }
   if (has_first) {
     const float carry = (tid > 0 && pk == start_row) ? pv : 0.0f;
-    pr_write(r0 + start_row, carry + first_val, base, damping, a.inv, a.rank, a.x_next, dangling);
+    pr_write(r0 + start_row, carry + first_val, base, damping, a.inv, a.rank, a.x_next, a.peers,
+             dangling);
   }
   // Dangling mass of this tile's rows, for the next superstep's base.
   const float dsum = block_sum<kPrThreads>(dangling, s_red);
@@ -405,8 +428,12 @@ void build_tiles(Graph& g, PrCache& c, cudaStream_t s, uint64_t lo, uint64_t n) 
 
 // Run one superstep's SpMV: reads x_cur, writes the other rank buffer and x_next.
 void launch_spmv(Graph& g, PrCache& c, const float* x_cur, float* x_next, float damping,
-                 cudaStream_t s) {
+                 cudaStream_t s, const PeerOut* peers = nullptr) {
   PrArgs a;
+  if (peers)
+    a.peers = *peers;
+  else
+    a.peers.n = 0;
   a.tile_b = c.tile_b.get();
   a.tile_e = c.tile_e.get();
   a.ptr = g.in.ptr.get();
@@ -625,6 +652,78 @@ double pagerank_shard_step(Graph& g, uint64_t lo, uint64_t hi, const float* x_fu
   GM_CUDA(cudaMemcpyAsync(c.scalars.get(), &b, 4, cudaMemcpyHostToDevice, s));
   // the kernel writes x_next[row] for rows in [lo, hi) only
   launch_spmv(g, c, x_full, x_block - lo, float(damping), s);
+  double* dsum = reinterpret_cast<double*>(c.ctr.get() + 2);
+  k_sum_partials<<<1, 1024, 0, s>>>(c.dang_partial.get(), uint32_t(c.ntiles + c.n_long), dsum);
+  GM_LAUNCH_CHECK();
+  double h = 0.0;
+  GM_CUDA(cudaMemcpyAsync(&h, dsum, 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+namespace {
+__global__ void k_push_block(const float* x, uint64_t lo, uint64_t cnt, PeerOut po) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t row = lo + i;
+    const float v = x[row];
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+      if (q < int(po.n)) po.p[q][int64_t(row) + po.off] = v;
+  }
+}
+
+PeerOut make_peers(float* const* peers, int npeers, int64_t offset, uint64_t lo, uint64_t limit) {
+  if (npeers < 1 || npeers > kMaxPeers)
+    fail(GM_EUSAGE, "pagerank shard: 1 to " + std::to_string(kMaxPeers) + " peer buffers");
+  PeerOut po{};
+  for (int q = 0; q < npeers; ++q) {
+    if (!peers[q]) fail(GM_EUSAGE, "pagerank shard: null peer buffer");
+    po.p[q] = peers[q];
+  }
+  po.n = uint32_t(npeers);
+  po.off = offset;
+  po.lo = lo;
+  po.lim = limit;
+  return po;
+}
+}  // namespace
+
+// Initial messages of the block's gathered prefix into every peer buffer.
+double pagerank_shard_init_peers(Graph& g, uint64_t lo, uint64_t hi, float* const* peers,
+                                 int npeers, int64_t offset, uint64_t limit) {
+  check_block(g, lo, hi);
+  const PeerOut po = make_peers(peers, npeers, offset, lo, limit);
+  PrCache& c = cache(g, lo, hi);
+  cudaStream_t s = g.stream;
+  init_state(g, c);
+  const uint64_t cnt = std::min<uint64_t>(hi - lo, limit);
+  if (cnt) {
+    k_push_block<<<grid_for(cnt, 256), 256, 0, s>>>(c.x0.get(), lo, cnt, po);
+    GM_LAUNCH_CHECK();
+  }
+  GM_CUDA(cudaMemsetAsync(c.ctr.get(), 0, 8, s));
+  if (hi > lo) {
+    k_count_dangling<<<grid_for(hi - lo, 256), 256, 0, s>>>(c.inv.get(), lo, hi, c.ctr.get());
+    GM_LAUNCH_CHECK();
+  }
+  unsigned long long dn = 0;
+  GM_CUDA(cudaMemcpyAsync(&dn, c.ctr.get(), 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  return double(dn) / double(g.n);
+}
+
+// The fused variant: no x_block; the messages go to the peers' buffers.
+double pagerank_shard_step_peers(Graph& g, uint64_t lo, uint64_t hi, const float* x_full,
+                                 double base, double damping, float* const* peers, int npeers,
+                                 int64_t offset, uint64_t limit) {
+  check_block(g, lo, hi);
+  const PeerOut po = make_peers(peers, npeers, offset, lo, limit);
+  PrCache& c = cache(g, lo, hi);
+  cudaStream_t s = g.stream;
+  const float b = float(base);
+  GM_CUDA(cudaMemcpyAsync(c.scalars.get(), &b, 4, cudaMemcpyHostToDevice, s));
+  launch_spmv(g, c, x_full, nullptr, float(damping), s, &po);
   double* dsum = reinterpret_cast<double*>(c.ctr.get() + 2);
   k_sum_partials<<<1, 1024, 0, s>>>(c.dang_partial.get(), uint32_t(c.ntiles + c.n_long), dsum);
   GM_LAUNCH_CHECK();

@@ -71,6 +71,45 @@ class TorchExchange:
     def world(self):
         return self.dist.get_world_size(self.group)
 
+    @property
+    def rank(self):
+        return self.dist.get_rank(self.group)
+
+    def allgather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+class IpcBuffer:
+    """A device buffer other processes can map (gm_ipc_alloc + CUDA IPC)."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        _check(L.load().gm_ipc_alloc(nbytes, C.byref(p)))
+        self.ptr = int(p.value)
+        self.nbytes = nbytes
+
+    def handle(self) -> bytes:
+        h = C.create_string_buffer(64)
+        _check(L.load().gm_ipc_handle(self.ptr, h))
+        return h.raw
+
+    @staticmethod
+    def open(handle: bytes) -> int:
+        p = C.c_void_p()
+        _check(L.load().gm_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)))
+        return int(p.value)
+
+    @staticmethod
+    def close(ptr: int):
+        _check(L.load().gm_ipc_close(ptr))
+
+    def free(self):
+        if self.ptr:
+            _check(L.load().gm_ipc_free(self.ptr))
+            self.ptr = 0
+
 
 class GpuShardBackend:
     """The CUDA kernels on this rank's row block (C ABI gm_pagerank_shard_*)."""
@@ -109,14 +148,99 @@ class GpuShardBackend:
     def pack(self, world, lmax):
         """Switch to the packed message layout (world blocks of lmax entries)."""
         import torch
+        if getattr(self, "_packed", None) == (world, lmax):
+            return
         _check(L.load().gm_pagerank_shard_pack(self.g._h, self.lo, self.hi, self.hi - self.lo,
                                                lmax))
         self.full = torch.empty(world * lmax, dtype=torch.float32, device="cuda")
+        self._packed = (world, lmax)
 
     def ranks(self):
         out = np.empty(self.hi - self.lo, np.float32)
         _check(L.load().gm_pagerank_shard_ranks(self.g._h, self.lo, self.hi, out.ctypes.data))
         return out
+
+    # fused all-gather: the epilogue stores into every rank's full vector
+    def init_peers(self, peers, offset, limit):
+        arr = (C.c_uint64 * len(peers))(*peers)
+        d = C.c_double()
+        _check(L.load().gm_pagerank_shard_init_peers(self.g._h, self.lo, self.hi, arr, len(peers),
+                                                     offset, limit, C.byref(d)))
+        return d.value
+
+    def step_peers(self, base, damping, x_read_ptr, peers, offset, limit):
+        import torch
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        arr = (C.c_uint64 * len(peers))(*peers)
+        d = C.c_double()
+        _check(L.load().gm_pagerank_shard_step_peers(self.g._h, self.lo, self.hi, x_read_ptr, base,
+                                                     damping, arr, len(peers), offset, limit,
+                                                     C.byref(d)))
+        return d.value
+
+
+class FusedPageRank:
+    """Sharded PageRank with the all-gather fused into the SpMV epilogue
+    (gm_pagerank_shard_step_peers).  Set up once: every rank owns two full
+    message vectors in CUDA IPC memory (it reads one while the peers write the
+    other), maps every peer's pair, and its kernel stores its block's messages
+    straight into all of them over NVLink.  The dangling-mass all-reduce is
+    the only collective left; it also orders superstep t's peer stores before
+    anyone's superstep t+1 reads them."""
+
+    def __init__(self, backend, exchange, n: int, packed=True):
+        self.backend, self.exchange, self.n = backend, exchange, n
+        world, rank = exchange.world, exchange.rank
+        lo, hi = backend.lo, backend.hi
+        if packed:
+            lmax = max(exchange.allreduce_max(backend.active_len(), backend.block), 1)
+            backend.pack(world, lmax)
+            nfull, self.offset, self.limit = world * lmax, rank * lmax - lo, lmax
+        else:
+            nfull, self.offset, self.limit = n, 0, hi - lo
+        self.bufs = [IpcBuffer(max(nfull, 1) * 4) for _ in range(2)]
+        handles = exchange.allgather_object([b.handle() for b in self.bufs])
+        self.opened, self.peers = [], [[], []]
+        for r in range(world):
+            for k in range(2):
+                if r == rank:
+                    self.peers[k].append(self.bufs[k].ptr)
+                else:
+                    p = IpcBuffer.open(handles[r][k])
+                    self.opened.append(p)
+                    self.peers[k].append(p)
+
+    def run(self, damping=0.85, iterations=20):
+        """The BASELINE PageRank; returns this block's ranks (internal order)."""
+        be, ex, n = self.backend, self.exchange, self.n
+        dangling = ex.allreduce_sum(be.init_peers(self.peers[0], self.offset, self.limit), be.block)
+        for t in range(iterations):
+            base = (1.0 - damping) / n + damping * dangling / n
+            local = be.step_peers(base, damping, self.bufs[t % 2].ptr, self.peers[(t + 1) % 2],
+                                  self.offset, self.limit)
+            dangling = ex.allreduce_sum(local, be.block)
+        return be.ranks()
+
+    def close(self):
+        self.exchange.allreduce_sum(0.0, self.backend.block)  # every peer is done
+        for p in self.opened:
+            IpcBuffer.close(p)
+        for b in self.bufs:
+            b.free()
+        self.opened, self.bufs = [], []
+
+
+def sharded_pagerank_fused(backend, exchange, n: int, damping=0.85, iterations=20, packed=True):
+    """One run of FusedPageRank (set up, run, unmap)."""
+    f = FusedPageRank(backend, exchange, n, packed)
+    try:
+        return f.run(damping, iterations)
+    finally:
+        f.close()
 
 
 def sharded_pagerank(backend, exchange, n: int, damping=0.85, iterations=20, sync=None,

@@ -547,3 +547,121 @@ def test_sharded_cf_virtual_shards_bitwise(gm):
     assert np.array_equal(got.view(np.uint32), want_f.view(np.uint32))
     np.testing.assert_allclose(rmse, want_rmse, rtol=1e-12)
     assert upd == [s.vertices_updated for s in want_st]
+
+
+def _virtual_pagerank(gm, P, scale, packed, fused):
+    """Row-sharded PageRank, P shards run one after another on one GPU.
+    fused=False: blocks concatenated into every shard's full vector (the
+    all-gather); fused=True: each shard's epilogue stores into all P full
+    vectors itself (gm_pagerank_shard_step_peers; here plain device buffers
+    stand in for the peers' IPC mappings), double-buffered."""
+    import torch
+
+    from paper_1503_07241_b200.sharded import GpuShardBackend, row_block
+    n = 1 << scale
+    graphs = [gm.Graph.rmat(scale, 16, seed=7, relabel=True, shards=P) for _ in range(P)]
+    bes = [GpuShardBackend(graphs[r], *row_block(n, P, r)) for r in range(P)]
+    lmax = n // P
+    if packed:
+        lmax = max(b.active_len() for b in bes)
+        for b in bes:
+            b.pack(P, lmax)
+    nfull = P * lmax if packed else n
+    d = 0.85
+    if not fused:
+        def gather():
+            full = torch.cat([b.block[:lmax] for b in bes])
+            for b in bes:
+                b.full.copy_(full)
+        dangling = sum(b.init() for b in bes)
+        gather()
+        for _ in range(20):
+            base = (1.0 - d) / n + d * dangling / n
+            dangling = sum(b.step(base, d) for b in bes)
+            gather()
+    else:
+        bufs = [[torch.full((nfull,), float("nan"), device="cuda") for _ in range(P)]
+                for _ in range(2)]
+        ptrs = [[t.data_ptr() for t in bufs[k]] for k in range(2)]
+
+        def place(r):
+            lo = bes[r].lo
+            return (r * lmax - lo if packed else 0), (lmax if packed else bes[r].hi - lo)
+
+        dangling = 0.0
+        for r, b in enumerate(bes):
+            off, lim = place(r)
+            dangling += b.init_peers(ptrs[0], off, lim)
+        for t in range(20):
+            base = (1.0 - d) / n + d * dangling / n
+            dangling = 0.0
+            for r, b in enumerate(bes):
+                off, lim = place(r)
+                dangling += b.step_peers(base, d, ptrs[t % 2][r], ptrs[(t + 1) % 2], off, lim)
+        # every replica of the final message vector is identical
+        for t in bufs[20 % 2][1:]:
+            assert torch.equal(t, bufs[20 % 2][0])
+    return np.concatenate([b.ranks() for b in bes]), graphs[0]
+
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_sharded_pagerank_fused_allgather_bitwise(gm, orc, packed):
+    """The all-gather fused into the SpMV epilogue (peer stores) gives the
+    unfused sharded ranks bit for bit, and the oracle's within 1e-5."""
+    r_ref, g = _virtual_pagerank(gm, 4, 15, packed, fused=False)
+    r_fused, _ = _virtual_pagerank(gm, 4, 15, packed, fused=True)
+    assert np.array_equal(r_ref.view(np.uint32), r_fused.view(np.uint32))
+    perm = g.permutation()
+    s, dd, _ = g.edges()
+    want, _ = orc.pagerank_norm(1 << 15, s, dd, 0.85, 20)
+    assert rel_l1(r_fused[perm], want) <= 1e-5
+
+
+def _ipc_worker(rank, world, port, scale, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1503_07241_b200 as gm
+    from paper_1503_07241_b200.sharded import (GpuShardBackend, TorchExchange, row_block,
+                                               sharded_pagerank_fused)
+
+    class CpuExchange(TorchExchange):  # gloo collectives on host tensors
+        def allreduce_sum(self, value, like):
+            return super().allreduce_sum(value, torch.empty(0))
+
+        def allreduce_max(self, value, like):
+            return super().allreduce_max(value, torch.empty(0))
+
+    n = 1 << scale
+    g = gm.Graph.rmat(scale, 16, seed=7, relabel=True, shards=world)
+    be = GpuShardBackend(g, *row_block(n, world, rank))
+    ranks = sharded_pagerank_fused(be, CpuExchange(), n, 0.85, 20, packed=True)
+    out[rank * (n // world):(rank + 1) * (n // world)] = torch.from_numpy(ranks)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_pagerank_fused_ipc_two_processes(gm, orc):
+    """Two processes on one GPU, each mapping the other's message buffers with
+    CUDA IPC (gm_ipc_*), run the fused-epilogue supersteps with gloo
+    all-reduces as the only collective (no kernel waits on another
+    process's): the ranks match the oracle."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    scale, world = 14, 2
+    out = torch.zeros(1 << scale, dtype=torch.float32).share_memory_()
+    mp.spawn(_ipc_worker, args=(world, port, scale, out), nprocs=world, join=True)
+    g = gm.Graph.rmat(scale, 16, seed=7, relabel=True, shards=world)
+    perm = g.permutation()
+    s, dd, _ = g.edges()
+    want, _ = orc.pagerank_norm(1 << scale, s, dd, 0.85, 20)
+    assert rel_l1(out.numpy()[perm], want) <= 1e-5

@@ -1,4 +1,5 @@
 #!/usr/bin/env python
+# (needs the propagation-blocking code of commit 5ae00d9 for GM_PR_PB; without it GM_PR_PB is ignored)
 """Time the PageRank superstep of the library named by GM_LIB (or the default).
 
     GM_LIB=_variants/x/libgraphmat_b200.so python tools/pr_exp.py [scale]

@@ -219,6 +219,16 @@ class BfsWorkload(Workload):
             self.root_int = int(self.g.permutation()[self.root])
             self.scaling = "strong"
             self.parallelism = f"rows{d.world}"
+            # frontier exchange as peer stores (CUDA IPC over NVLink);
+            # GM_BFS_EXCHANGE=nccl keeps the NCCL all-gather
+            self.fused, self.exchange_kind = None, "nccl all_gather"
+            if os.environ.get("GM_BFS_EXCHANGE", "fused") == "fused":
+                try:
+                    from paper_1503_07241_b200.sharded import FusedBfs
+                    self.fused = FusedBfs(self.backend, self.exchange)
+                    self.exchange_kind = "peer stores of the frontier blocks (CUDA IPC) + nccl all_reduce"
+                except Exception as e:
+                    self.exchange_kind = f"nccl all_gather (peer stores unavailable: {e})"
         import torch
         self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
         self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
@@ -233,11 +243,14 @@ class BfsWorkload(Workload):
                        "scale": a.scale, "edge_factor": 16, "n": self.n,
                        "m_directed": self.g.num_edges, "root": self.root,
                        "teps_edges": self.edges, "switch": "pull when frontier edges > 5% of m",
+                       **({"exchange": self.exchange_kind} if self.sharded else {}),
                        "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB)"
                        % (self.g.info().device_bytes / 1e9)}
 
     def run_device(self, gm):
         if self.sharded:
+            if self.fused is not None:
+                return self.fused.run(self.n, self.g.num_edges, self.root_int, self.root_degree)[0]
             from paper_1503_07241_b200.sharded import sharded_bfs
             return sharded_bfs(self.backend, self.exchange, self.n, self.g.num_edges, self.root_int,
                                self.root_degree)[0]

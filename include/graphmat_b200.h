@@ -371,6 +371,19 @@ GM_API gm_status gm_bfs_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t ro
                                    uint64_t* found, uint64_t* found_edges);
 GM_API gm_status gm_bfs_shard_levels(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                      int32_t* levels_block_host);
+/* The frontier exchange as peer stores instead of an all-gather: the block's
+ * next-frontier words (next_block_dev, after _step) are stored at word
+ * row_begin/32 of each of the npeers (1..8) bitmaps -- every rank's
+ * frontier for the next superstep, mapped with gm_ipc_open, the local one
+ * included.  Double-buffer the frontiers; the found-count all-reduce is the
+ * barrier. */
+GM_API gm_status gm_bfs_shard_push(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                   const uint32_t* next_block_dev, const uint64_t* peer_bitmaps,
+                                   int32_t npeers);
+/* dst |= src over `words` device u32 words, on the graph's stream (visited |=
+ * frontier when the frontier lives in IPC memory). */
+GM_API gm_status gm_bitmap_or(gm_graph_t g, uint32_t* dst_dev, const uint32_t* src_dev,
+                              uint64_t words);
 /* SSSP (BSP Bellman-Ford, traversal.hpp:67-115) over the rows [row_begin,
  * row_end) this rank owns (32-vertex aligned), u8/u32 weights.  msg_dev: the
  * full uint32 message vector, identical on every rank -- the superstep-start

@@ -142,6 +142,26 @@ __global__ void __launch_bounds__(kSbThreads) k_sb_pull(
   }
 }
 
+// The block's next-frontier words stored into every rank's frontier bitmap
+// for the next superstep (CUDA IPC peer mappings, the local one included):
+// the all-gather as NVLink stores.  Whole words are stored, zeros included,
+// so a target buffer never needs clearing (each word has one writer).
+constexpr int kMaxPeerBufs = 8;
+struct PeerWords {
+  uint32_t* p[kMaxPeerBufs];
+  int n;
+};
+
+__global__ void k_sb_push(const uint32_t* next_blk, uint64_t w0, uint64_t nw, PeerWords pw) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nw;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = next_blk[i];
+#pragma unroll
+    for (int q = 0; q < kMaxPeerBufs; ++q)
+      if (q < pw.n) pw.p[q][w0 + i] = v;
+  }
+}
+
 void check_sb(Graph& g, uint64_t lo, uint64_t hi) {
   if (!g.symmetric) fail(GM_EUSAGE, "bfs shard: needs a symmetric graph (GM_SYMMETRIZE)");
   if (lo > hi || hi > g.n || (lo & 31u) || ((hi & 31u) && hi != g.n))
@@ -206,6 +226,41 @@ void bfs_shard_step(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* frontier
   GM_CUDA(cudaStreamSynchronize(s));
   if (found) *found = h[0];
   if (found_edges) *found_edges = h[1];
+}
+
+void bfs_shard_push(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* next_block,
+                    uint32_t* const* peers, int npeers) {
+  check_sb(g, lo, hi);
+  if (npeers < 1 || npeers > kMaxPeerBufs)
+    fail(GM_EUSAGE, "bfs shard: 1 to " + std::to_string(kMaxPeerBufs) + " peer bitmaps");
+  PeerWords pw{};
+  for (int q = 0; q < npeers; ++q) {
+    if (!peers[q]) fail(GM_EUSAGE, "bfs shard: null peer bitmap");
+    pw.p[q] = peers[q];
+  }
+  pw.n = npeers;
+  const uint64_t nw = (hi - lo + 31) / 32;
+  if (nw) {
+    k_sb_push<<<grid_for(nw, 256), 256, 0, g.stream>>>(next_block, lo / 32, nw, pw);
+    GM_LAUNCH_CHECK();
+  }
+  GM_CUDA(cudaStreamSynchronize(g.stream));
+}
+
+namespace {
+__global__ void k_bits_or(uint32_t* dst, const uint32_t* src, uint64_t words) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] |= src[i];
+}
+}  // namespace
+
+void bitmap_or(Graph& g, uint32_t* dst, const uint32_t* src, uint64_t words) {
+  if (words) {
+    k_bits_or<<<grid_for(words, 256), 256, 0, g.stream>>>(dst, src, words);
+    GM_LAUNCH_CHECK();
+  }
+  GM_CUDA(cudaStreamSynchronize(g.stream));
 }
 
 void bfs_shard_levels(Graph& g, uint64_t lo, uint64_t hi, int32_t* out_host) {

@@ -510,6 +510,26 @@ GM_API gm_status gm_sssp_shard_dists(gm_graph_t g, uint64_t row_begin, uint64_t 
   });
 }
 
+GM_API gm_status gm_bfs_shard_push(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
+                                   const uint32_t* next_block_dev, const uint64_t* peer_bitmaps,
+                                   int32_t npeers) {
+  return guarded([&] {
+    if (!peer_bitmaps || npeers < 1) gm::fail(GM_EUSAGE, "null peer bitmaps");
+    if (row_end > row_begin && !next_block_dev) gm::fail(GM_EUSAGE, "null bitmap");
+    std::vector<uint32_t*> peers(static_cast<size_t>(npeers));
+    for (int32_t q = 0; q < npeers; ++q) peers[q] = reinterpret_cast<uint32_t*>(peer_bitmaps[q]);
+    gm::bfs_shard_push(*handle(g), row_begin, row_end, next_block_dev, peers.data(), npeers);
+  });
+}
+
+GM_API gm_status gm_bitmap_or(gm_graph_t g, uint32_t* dst_dev, const uint32_t* src_dev,
+                              uint64_t words) {
+  return guarded([&] {
+    if (words && (!dst_dev || !src_dev)) gm::fail(GM_EUSAGE, "null bitmap");
+    gm::bitmap_or(*handle(g), dst_dev, src_dev, words);
+  });
+}
+
 GM_API gm_status gm_bfs_shard_levels(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                      int32_t* levels_block_host) {
   return guarded([&] {

@@ -304,10 +304,83 @@ class GpuBfsShardBackend:
                                           self.next_block.data_ptr(), C.byref(f), C.byref(fe)))
         return int(f.value), int(fe.value)
 
+    def step_ptr(self, level, pull, frontier_ptr):
+        """step() reading the frontier bitmap at a raw device pointer."""
+        import torch
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        f, fe = C.c_uint64(), C.c_uint64()
+        _check(L.load().gm_bfs_shard_step(self.g._h, self.lo, self.hi, frontier_ptr,
+                                          self.visited.data_ptr(), level, 1 if pull else 0,
+                                          self.next_block.data_ptr(), C.byref(f), C.byref(fe)))
+        return int(f.value), int(fe.value)
+
     def levels(self):
         out = np.empty(self.hi - self.lo, np.int32)
         _check(L.load().gm_bfs_shard_levels(self.g._h, self.lo, self.hi, out.ctypes.data))
         return out
+
+
+class FusedBfs:
+    """sharded_bfs with the frontier all-gather replaced by peer stores: each
+    rank owns two full frontier bitmaps in CUDA IPC memory and maps every
+    peer's pair; after its step it stores its block's next-frontier words into
+    every rank's next bitmap (gm_bfs_shard_push).  The (found, edges) sum
+    all-reduce is the only collective and the barrier."""
+
+    def __init__(self, backend, exchange):
+        import torch
+        self.backend, self.exchange = backend, exchange
+        words = backend.frontier.numel()
+        self.words = words
+        self.bufs = [IpcBuffer(words * 4) for _ in range(2)]
+        handles = exchange.allgather_object([b.handle() for b in self.bufs])
+        self.opened, self.peers = [], [[], []]
+        for r in range(exchange.world):
+            for k in range(2):
+                if r == exchange.rank:
+                    self.peers[k].append(self.bufs[k].ptr)
+                else:
+                    p = IpcBuffer.open(handles[r][k])
+                    self.opened.append(p)
+                    self.peers[k].append(p)
+        self._torch = torch
+
+    def run(self, n: int, m: int, root: int, root_degree: int):
+        be, ex = self.backend, self.exchange
+        be.init(root)  # visited = {root}; the frontier of superstep 1 is {root} everywhere
+        lib = L.load()
+        # superstep 1 reads bufs[1] (level 1 -> t = 1): seed it with the root's bit
+        seed = be.frontier  # the backend's torch copy holds exactly the root bit
+        nf, mf, prev_pull, level = 1, root_degree, False, 0
+        steps = []
+        cur_ptr = seed.data_ptr()
+        while nf > 0:
+            level += 1
+            pull = False if level == 1 else (nf * 24 >= n if prev_pull else mf > 0.05 * m)
+            f, fe = be.step_ptr(level, pull, cur_ptr)
+            nxt = self.peers[level % 2]
+            arr = (C.c_uint64 * len(nxt))(*nxt)
+            _check(lib.gm_bfs_shard_push(be.g._h, be.lo, be.hi, be.next_block.data_ptr(), arr,
+                                         len(nxt)))
+            nf = int(round(ex.allreduce_sum(float(f), be.frontier)))
+            mf = int(round(ex.allreduce_sum(float(fe), be.frontier)))
+            cur_ptr = self.bufs[level % 2].ptr
+            _check(lib.gm_bitmap_or(be.g._h, be.visited.data_ptr(), cur_ptr, self.words))
+            steps.append(("pull" if pull else "push", nf))
+            prev_pull = pull
+        return be.levels(), steps
+
+    def close(self):
+        self.exchange.allreduce_sum(0.0, self.backend.frontier)  # every peer is done
+        for p in self.opened:
+            IpcBuffer.close(p)
+        for b in self.bufs:
+            b.free()
+        self.opened, self.bufs = [], []
 
 
 def sharded_bfs(backend, exchange, n: int, m: int, root: int, root_degree: int):

@@ -665,3 +665,103 @@ def test_sharded_pagerank_fused_ipc_two_processes(gm, orc):
     s, dd, _ = g.edges()
     want, _ = orc.pagerank_norm(1 << scale, s, dd, 0.85, 20)
     assert rel_l1(out.numpy()[perm], want) <= 1e-5
+
+
+def test_sharded_bfs_peer_push_virtual(gm, orc):
+    """The frontier exchange as peer stores (gm_bfs_shard_push) instead of an
+    all-gather: P shards on one GPU, each storing its next-frontier words into
+    all P double-buffered frontier bitmaps; levels equal the oracle's."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1503_07241_b200 import _lib as L
+    from paper_1503_07241_b200.sharded import GpuBfsShardBackend, row_block
+    P, scale = 4, 15
+    n = 1 << scale
+    graphs = [gm.Graph.rmat(scale, 16, seed=9, symmetrize=True, relabel=True, shards=P)
+              for _ in range(P)]
+    bes = [GpuBfsShardBackend(graphs[r], *row_block(n, P, r)) for r in range(P)]
+    g0 = graphs[0]
+    perm = g0.permutation()
+    root_ext = g0.pick_source(9)
+    root = int(perm[root_ext])
+    deg_int = np.empty(n, np.int64)
+    deg_int[perm] = g0.degree_vector("out")
+    words = (n + 31) // 32
+    bufs = [[torch.full((words,), -1, dtype=torch.int32, device="cuda") for _ in range(P)]
+            for _ in range(2)]
+    for b in bes:
+        b.init(root)
+    cur = [b.frontier.data_ptr() for b in bes]
+    nf, mf, prev_pull, level, dirs = 1, int(deg_int[root]), False, 0, []
+    lib = L.load()
+    while nf > 0:
+        level += 1
+        pull = False if level == 1 else (nf * 24 >= n if prev_pull else mf > 0.05 * g0.num_edges)
+        res = [b.step_ptr(level, pull, cur[r]) for r, b in enumerate(bes)]
+        tgt = [t.data_ptr() for t in bufs[level % 2]]
+        arr = (C.c_uint64 * P)(*tgt)
+        for b in bes:
+            assert lib.gm_bfs_shard_push(b.g._h, b.lo, b.hi, b.next_block.data_ptr(), arr, P) == 0
+        nf, mf = sum(r[0] for r in res), sum(r[1] for r in res)
+        for r, b in enumerate(bes):
+            b.visited |= bufs[level % 2][r]
+        cur = tgt
+        dirs.append(pull)
+        prev_pull = pull
+    assert any(dirs) and not all(dirs)
+    lv = np.concatenate([b.levels() for b in bes])
+    s, d, _ = g0.edges()
+    want, _ = orc.bfs(n, s, d, root_ext, presorted=True)
+    assert np.array_equal(lv[perm], want)
+
+
+def _bfs_ipc_worker(rank, world, port, scale, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1503_07241_b200 as gm
+    from paper_1503_07241_b200.sharded import FusedBfs, GpuBfsShardBackend, TorchExchange, row_block
+
+    class CpuExchange(TorchExchange):
+        def allreduce_sum(self, value, like):
+            return super().allreduce_sum(value, torch.empty(0))
+
+    n = 1 << scale
+    g = gm.Graph.rmat(scale, 16, seed=9, symmetrize=True, relabel=True, shards=world)
+    perm = g.permutation()
+    root = int(perm[g.pick_source(9)])
+    deg_int = np.empty(n, np.int64)
+    deg_int[perm] = g.degree_vector("out")
+    be = GpuBfsShardBackend(g, *row_block(n, world, rank))
+    f = FusedBfs(be, CpuExchange())
+    lv, _ = f.run(n, g.num_edges, root, int(deg_int[root]))
+    f.close()
+    out[rank * (n // world):(rank + 1) * (n // world)] = torch.from_numpy(lv)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_bfs_fused_ipc_two_processes(gm, orc):
+    """FusedBfs across two processes on one GPU over real CUDA IPC mappings
+    (gloo all-reduces as the barrier): levels equal the oracle's."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    scale, world = 14, 2
+    out = torch.zeros(1 << scale, dtype=torch.int32).share_memory_()
+    mp.spawn(_bfs_ipc_worker, args=(world, port, scale, out), nprocs=world, join=True)
+    g = gm.Graph.rmat(scale, 16, seed=9, symmetrize=True, relabel=True, shards=world)
+    perm = g.permutation()
+    s, d, _ = g.edges()
+    want, _ = orc.bfs(1 << scale, s, d, g.pick_source(9), presorted=True)
+    assert np.array_equal(out.numpy()[perm], want)

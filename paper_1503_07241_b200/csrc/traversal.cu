@@ -191,6 +191,8 @@ __device__ __forceinline__ void warp_enqueue(bool want, uint32_t v, uint32_t edg
 // counter (count << kCountShift | edges), instead of one atomicAdd per warp
 // step, which serialises at the L2 when many warps append a few entries each.
 // kOffs: also write each entry's exclusive edge offset; kQe: and a u64 payload.
+constexpr uint32_t kPushCap = 64;  // SSSP push: staged appends per warp
+
 template <uint32_t CAP, bool kOffs, bool kQe>
 struct StagedQ {
   uint32_t* sv;  // [CAP] vertices
@@ -1139,6 +1141,10 @@ __global__ void __launch_bounds__(kThreads) k_sssp_push(Ctl* ctl, const uint32_t
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const unsigned lane = lane_id();
+  // appends staged per warp in shared memory, published kPushCap at a time
+  // (one atomicAdd on the queue counter per flush instead of one per warp step)
+  __shared__ uint32_t s_qv[kThreads / 32][kPushCap], s_qd[kThreads / 32][kPushCap];
+  StagedQ<kPushCap, true, false> sq{s_qv[threadIdx.x >> 5], s_qd[threadIdx.x >> 5], nullptr};
   for (uint64_t wb = warp * 32 * kEPT; wb < total; wb += nwarps * 32 * kEPT) {
     const uint64_t t0 = wb + uint64_t(lane) * kEPT;
     uint32_t i = 0;
@@ -1171,9 +1177,10 @@ __global__ void __launch_bounds__(kThreads) k_sssp_push(Ctl* ctl, const uint32_t
           won = !(atomicOr(&changed[v >> 5], bit) & bit);
         }
       }
-      warp_enqueue(won, v, won ? deg[v] : 0, &ctl->qpack, qn, offs_n);
+      sq.push(won, v, won ? deg[v] : 0, 0, &ctl->qpack, qn, offs_n, nullptr);
     }
   }
+  sq.flush(&ctl->qpack, qn, offs_n, nullptr);
 }
 
 // Next frontier's message snapshot (after every relaxation of the superstep

@@ -18,7 +18,7 @@ for w in bfs sssp cf pagerank23; do
 done
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_bfs_coop -s 1 -c 1 \
   -o gpurun_out/${tag}_bfs23_coop python tools/prof_run.py bfs --reps 2 > gpurun_out/${tag}_ncu_bfs.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_sssp_pull -s 3 -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"^k_sssp_pull$" -s 3 -c 1 \
   -o gpurun_out/${tag}_sssp23_pull python tools/prof_run.py sssp --reps 1 > gpurun_out/${tag}_ncu_sssp.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_cf_items -c 2 \
   -o gpurun_out/${tag}_cf_items python tools/prof_run.py cf --reps 1 > gpurun_out/${tag}_ncu_cf.log 2>&1

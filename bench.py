@@ -63,6 +63,19 @@ def gm_pagerank_uses_hub(g):
     return g.num_vertices * 4 <= (64 << 20)
 
 
+B200_SPEC_HBM_GBS = 8000.0  # the north star's "~8 TB/s per GPU" (HBM3e spec)
+
+
+def with_spec(rf):
+    """Add the fraction of the B200's spec HBM bandwidth next to the measured one."""
+    if rf:
+        gbs = rf.get("achieved_gbs", rf["achieved"] if rf.get("unit") == "GB/s" else None)
+        if gbs is not None:
+            rf["spec_gbs"] = B200_SPEC_HBM_GBS
+            rf["frac_of_spec"] = round(gbs / B200_SPEC_HBM_GBS, 4)
+    return rf
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -702,7 +715,7 @@ def run_ours(args, d: Dist):
                                             else w.parallelism) if d.world > 1 else "single"),
         "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_s * 1e3 / args.steps, 4)},
-        "roofline": w.roofline(st, peak, peak_kind),
+        "roofline": with_spec(w.roofline(st, peak, peak_kind)),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "ingest_seconds": round(w.ingest_s, 3),

@@ -765,3 +765,49 @@ def test_sharded_bfs_fused_ipc_two_processes(gm, orc):
     s, d, _ = g.edges()
     want, _ = orc.bfs(1 << scale, s, d, g.pick_source(9), presorted=True)
     assert np.array_equal(out.numpy()[perm], want)
+
+
+def test_shard_and_ipc_api_errors(gm):
+    """The multi-GPU entry points reject bad arguments with the C ABI's usage
+    / CUDA status (and a message) instead of faulting."""
+    import ctypes as C
+
+    from paper_1503_07241_b200 import _lib as L
+    from paper_1503_07241_b200.sharded import (GpuBfsShardBackend, GpuCfShardBackend,
+                                               GpuShardBackend, GpuSsspShardBackend, IpcBuffer)
+    lib = L.load()
+    g = gm.Graph.rmat(10, 8, seed=3, relabel=True)
+    n = g.num_vertices
+    be = GpuShardBackend(g, 0, n)
+    d = C.c_double()
+    nine = (C.c_uint64 * 9)(*([be.full.data_ptr()] * 9))
+    assert lib.gm_pagerank_shard_step_peers(g._h, 0, n, be.full.data_ptr(), 0.1, 0.85, nine, 9, 0,
+                                            n, C.byref(d)) == L.GM_EUSAGE
+    assert lib.gm_pagerank_shard_step_peers(g._h, 0, n, be.full.data_ptr(), 0.1, 0.85, None, 0, 0,
+                                            n, C.byref(d)) == L.GM_EUSAGE
+    with pytest.raises(gm.UsageError):
+        be2 = GpuShardBackend(g, 5, 2)
+        be2.init()
+    # SSSP shards need integer weights and 32-vertex-aligned blocks
+    with pytest.raises(gm.UsageError):
+        GpuSsspShardBackend(g, 0, n).init(0)
+    gw = gm.Graph.rmat(10, 8, seed=3, weights=True, relabel=True)
+    with pytest.raises(gm.UsageError):
+        GpuSsspShardBackend(gw, 3, 64).init(0)
+    with pytest.raises(gm.InputError):
+        GpuSsspShardBackend(gw, 0, n).init(n + 5)
+    # BFS shards need a symmetric graph
+    with pytest.raises(gm.UsageError):
+        GpuBfsShardBackend(g, 0, n).init(0)
+    # CF shard: k bounds, rating type
+    gb = gm.Graph.bipartite(300, 40, 900.0, 40, seed=2)
+    cfb = GpuCfShardBackend(gb, 0, gb.num_vertices, k=20)
+    cfb.init(np.zeros((gb.num_vertices, 20), np.float32))
+    with pytest.raises(gm.InputError):
+        cfb.step(-1.0, 0.05)
+    # IPC: a garbage handle is a CUDA error, not a crash
+    with pytest.raises(gm.CudaError):
+        IpcBuffer.open(bytes(64))
+    buf = IpcBuffer(1024)
+    assert len(buf.handle()) == 64
+    buf.free()

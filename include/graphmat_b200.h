@@ -380,6 +380,13 @@ GM_API gm_status gm_bfs_shard_levels(gm_graph_t g, uint64_t row_begin, uint64_t 
 GM_API gm_status gm_bfs_shard_push(gm_graph_t g, uint64_t row_begin, uint64_t row_end,
                                    const uint32_t* next_block_dev, const uint64_t* peer_bitmaps,
                                    int32_t npeers);
+/* Store `bytes` of a device block at byte `dst_offset` of each of the npeers
+ * (1..8) peer buffers (CUDA IPC mappings: NVLink copies), on the graph's
+ * stream -- the exchange of the SSSP message blocks and CF factor blocks
+ * without an all-gather (double-buffer the targets; the count all-reduce is
+ * the barrier). */
+GM_API gm_status gm_push_block(gm_graph_t g, const void* src_dev, uint64_t bytes,
+                               const uint64_t* peer_buffers, int32_t npeers, uint64_t dst_offset);
 /* dst |= src over `words` device u32 words, on the graph's stream (visited |=
  * frontier when the frontier lives in IPC memory). */
 GM_API gm_status gm_bitmap_or(gm_graph_t g, uint32_t* dst_dev, const uint32_t* src_dev,

@@ -34,7 +34,7 @@ EXPORTED = [
     "gm_pagerank_shard_pack", "gm_bfs_shard_init", "gm_bfs_shard_step", "gm_bfs_shard_levels",
     "gm_sssp_shard_init", "gm_sssp_shard_step", "gm_sssp_shard_dists", "gm_cf_shard_step",
     "gm_pagerank_shard_step_peers", "gm_pagerank_shard_init_peers", "gm_ipc_alloc", "gm_ipc_free", "gm_ipc_handle", "gm_ipc_open",
-    "gm_ipc_close", "gm_bfs_shard_push", "gm_bitmap_or",
+    "gm_ipc_close", "gm_bfs_shard_push", "gm_bitmap_or", "gm_push_block",
 ]
 
 
@@ -166,6 +166,7 @@ def load(path: str = LIB_PATH):
         "gm_ipc_close": (C.c_int, [vp]),
         "gm_bfs_shard_push": (C.c_int, [vp, u64, u64, vp, vp, i32]),
         "gm_bitmap_or": (C.c_int, [vp, vp, vp, u64]),
+        "gm_push_block": (C.c_int, [vp, vp, u64, vp, i32, u64]),
     }
     for name, (res, args) in proto.items():
         f = getattr(L, name)

@@ -39,6 +39,8 @@ void bfs_shard_step(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* frontier
                     const uint32_t* visited, int32_t lvl, int32_t pull, uint32_t* next_block,
                     uint64_t* found, uint64_t* found_edges);
 void bfs_shard_levels(Graph& g, uint64_t lo, uint64_t hi, int32_t* out_host);
+void push_block(Graph& g, const void* src, uint64_t bytes, void* const* peers, int npeers,
+                uint64_t dst_offset);
 void bitmap_or(Graph& g, uint32_t* dst, const uint32_t* src, uint64_t words);
 void bfs_shard_push(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* next_block,
                     uint32_t* const* peers, int npeers);

@@ -263,6 +263,22 @@ void bitmap_or(Graph& g, uint32_t* dst, const uint32_t* src, uint64_t words) {
   GM_CUDA(cudaStreamSynchronize(g.stream));
 }
 
+// A device block stored into every peer buffer at the same byte offset (the
+// exchange of the SSSP / CF shards as NVLink peer copies instead of an
+// all-gather); copies on the graph's stream, then a sync.
+void push_block(Graph& g, const void* src, uint64_t bytes, void* const* peers, int npeers,
+                uint64_t dst_offset) {
+  if (npeers < 1 || npeers > kMaxPeerBufs)
+    fail(GM_EUSAGE, "push block: 1 to " + std::to_string(kMaxPeerBufs) + " peer buffers");
+  for (int q = 0; q < npeers; ++q) {
+    if (!peers[q]) fail(GM_EUSAGE, "push block: null peer buffer");
+    if (bytes)
+      GM_CUDA(cudaMemcpyAsync(static_cast<char*>(peers[q]) + dst_offset, src, bytes,
+                              cudaMemcpyDeviceToDevice, g.stream));
+  }
+  GM_CUDA(cudaStreamSynchronize(g.stream));
+}
+
 void bfs_shard_levels(Graph& g, uint64_t lo, uint64_t hi, int32_t* out_host) {
   check_sb(g, lo, hi);
   BfsShardCache& c = sb_cache(g, lo, hi);

@@ -522,6 +522,17 @@ GM_API gm_status gm_bfs_shard_push(gm_graph_t g, uint64_t row_begin, uint64_t ro
   });
 }
 
+GM_API gm_status gm_push_block(gm_graph_t g, const void* src_dev, uint64_t bytes,
+                               const uint64_t* peer_buffers, int32_t npeers, uint64_t dst_offset) {
+  return guarded([&] {
+    if (!peer_buffers || npeers < 1) gm::fail(GM_EUSAGE, "null peer buffers");
+    if (bytes && !src_dev) gm::fail(GM_EUSAGE, "null source block");
+    std::vector<void*> peers(static_cast<size_t>(npeers));
+    for (int32_t q = 0; q < npeers; ++q) peers[q] = reinterpret_cast<void*>(peer_buffers[q]);
+    gm::push_block(*handle(g), src_dev, bytes, peers.data(), npeers, dst_offset);
+  });
+}
+
 GM_API gm_status gm_bitmap_or(gm_graph_t g, uint32_t* dst_dev, const uint32_t* src_dev,
                               uint64_t words) {
   return guarded([&] {

@@ -183,6 +183,46 @@ class GpuShardBackend:
         return d.value
 
 
+class PeerPair:
+    """Two device buffers per rank in CUDA IPC memory, every rank's pair
+    mapped into this process: peers[k][r] is rank r's buffer k (the local
+    ones included) -- the double-buffered targets of peer-store exchanges."""
+
+    def __init__(self, exchange, nbytes: int):
+        self.exchange = exchange
+        self.bufs = [IpcBuffer(max(nbytes, 1)) for _ in range(2)]
+        handles = exchange.allgather_object([b.handle() for b in self.bufs])
+        self.opened, self.peers = [], [[], []]
+        for r in range(exchange.world):
+            for k in range(2):
+                if r == exchange.rank:
+                    self.peers[k].append(self.bufs[k].ptr)
+                else:
+                    p = IpcBuffer.open(handles[r][k])
+                    self.opened.append(p)
+                    self.peers[k].append(p)
+
+    def local(self, k: int) -> int:
+        return self.bufs[k % 2].ptr
+
+    def targets(self, k: int):
+        return self.peers[k % 2]
+
+    def close(self, like):
+        self.exchange.allreduce_sum(0.0, like)  # every peer is done
+        for p in self.opened:
+            IpcBuffer.close(p)
+        for b in self.bufs:
+            b.free()
+        self.opened, self.bufs = [], []
+
+
+def push_block(g, src_ptr: int, nbytes: int, targets, dst_offset: int):
+    """gm_push_block: the block into every target buffer at dst_offset bytes."""
+    arr = (C.c_uint64 * len(targets))(*targets)
+    _check(L.load().gm_push_block(g._h, src_ptr, nbytes, arr, len(targets), dst_offset))
+
+
 class FusedPageRank:
     """Sharded PageRank with the all-gather fused into the SpMV epilogue
     (gm_pagerank_shard_step_peers).  Set up once: every rank owns two full
@@ -443,6 +483,19 @@ class GpuSsspShardBackend:
                                            C.byref(c), C.byref(ce)))
         return int(c.value), int(ce.value)
 
+    def step_ptr(self, pull, msg_ptr):
+        """step() reading the message vector at a raw device pointer."""
+        import torch
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        c, ce = C.c_uint64(), C.c_uint64()
+        _check(L.load().gm_sssp_shard_step(self.g._h, self.lo, self.hi, msg_ptr, 1 if pull else 0,
+                                           self.msg_block.data_ptr(), C.byref(c), C.byref(ce)))
+        return int(c.value), int(ce.value)
+
     def dists(self):
         out = np.empty(self.hi - self.lo, np.uint32)
         _check(L.load().gm_sssp_shard_dists(self.g._h, self.lo, self.hi, out.ctypes.data))
@@ -506,6 +559,19 @@ class GpuCfShardBackend:
                                          C.byref(ch)))
         return float(sq.value), int(ch.value)
 
+    def step_ptr(self, gamma, lam, full_ptr):
+        """step() reading the full factor matrix at a raw device pointer."""
+        import torch
+        if self._stream is None:
+            self._stream = torch.cuda.ExternalStream(self.g.stream)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._stream.wait_event(ev)
+        sq, ch = C.c_double(), C.c_uint64()
+        _check(L.load().gm_cf_shard_step(self.g._h, self.lo, self.hi, self.k, full_ptr, gamma, lam,
+                                         self.block.data_ptr(), C.byref(sq), C.byref(ch)))
+        return float(sq.value), int(ch.value)
+
     def factors(self):
         return self.full[self.lo:self.hi].cpu().numpy()
 
@@ -534,3 +600,71 @@ def sharded_cf(backend, exchange, m: int, gamma=1e-3, lam=0.05, iterations=10):
         sq = exchange.allreduce_sum(sq, backend.full)
         rmse.append(math.sqrt(sq / m) if m else 0.0)
     return final, rmse, updated
+
+
+class FusedSssp:
+    """sharded_sssp with the message all-gather replaced by peer copies: each
+    rank stores its block of next messages into every rank's next message
+    vector (double-buffered CUDA IPC memory, gm_push_block); the count
+    all-reduce is the only collective and the barrier."""
+
+    def __init__(self, backend, exchange):
+        self.backend, self.exchange = backend, exchange
+        self.pair = PeerPair(exchange, backend.msg.numel() * 4)
+
+    def run(self, n: int, m: int, root: int, root_degree: int, max_iters=None):
+        be, ex, g = self.backend, self.exchange, self.backend.g
+        be.init(root)  # be.msg (torch) = INF everywhere, 0 at the root
+        push_block(g, be.msg.data_ptr(), n * 4, [self.pair.local(0)], 0)
+        nf, mf, it = 1, root_degree, 0
+        cap = n + 1 if max_iters is None else max_iters
+        steps = []
+        while nf > 0 and it < cap:
+            pull = mf * SSSP_PULL_DIV > m
+            c, ce = be.step_ptr(pull, self.pair.local(it))
+            push_block(g, be.msg_block.data_ptr(), (be.hi - be.lo) * 4, self.pair.targets(it + 1),
+                       be.lo * 4)
+            c = int(round(ex.allreduce_sum(float(c), be.msg)))
+            ce = int(round(ex.allreduce_sum(float(ce), be.msg)))
+            it += 1
+            steps.append(("pull" if pull else "push", nf, c))
+            nf, mf = c, ce
+        return be.dists(), steps
+
+    def close(self):
+        self.pair.close(self.backend.msg)
+
+
+class FusedCf:
+    """sharded_cf with the factor all-gather replaced by peer copies of each
+    rank's factor block into every rank's next factor matrix (double-buffered
+    CUDA IPC memory, gm_push_block)."""
+
+    def __init__(self, backend, exchange):
+        self.backend, self.exchange = backend, exchange
+        self.pair = PeerPair(exchange, backend.full.numel() * 4)
+
+    def run(self, m: int, gamma=1e-3, lam=0.05, iterations=10):
+        import math
+        be, ex, g = self.backend, self.exchange, self.backend.g
+        k = be.k
+        push_block(g, be.full.data_ptr(), be.full.numel() * 4, [self.pair.local(0)], 0)
+        rmse, updated = [], []
+        for it in range(iterations + 1):
+            sq, ch = be.step_ptr(gamma, lam, self.pair.local(it))
+            sq = ex.allreduce_sum(sq, be.full)
+            if it > 0:
+                rmse.append(math.sqrt(sq / m) if m else 0.0)
+            if it == iterations:
+                break
+            updated.append(int(round(ex.allreduce_sum(float(ch), be.full))))
+            push_block(g, be.block.data_ptr(), (be.hi - be.lo) * k * 4,
+                       self.pair.targets(it + 1), be.lo * k * 4)
+        # this block's final factors (the last step's block output is one
+        # update further: it only evaluated the closing RMSE)
+        push_block(g, self.pair.local(iterations) + be.lo * k * 4, (be.hi - be.lo) * k * 4,
+                   [be.block.data_ptr()], 0)
+        return be.block.cpu().numpy(), rmse, updated
+
+    def close(self):
+        self.pair.close(self.backend.full)

@@ -811,3 +811,144 @@ def test_shard_and_ipc_api_errors(gm):
     buf = IpcBuffer(1024)
     assert len(buf.handle()) == 64
     buf.free()
+
+
+def test_sharded_sssp_cf_peer_copies_virtual(gm, orc):
+    """SSSP and CF shards exchanging through gm_push_block (peer copies into
+    double-buffered full vectors) instead of all-gathers: P = 4 virtual
+    shards on one GPU, plain device buffers standing in for the IPC mappings.
+    SSSP distances equal the oracle's; CF factors equal gm_cf bit for bit."""
+    import torch
+
+    from paper_1503_07241_b200.sharded import (SSSP_PULL_DIV, GpuCfShardBackend,
+                                               GpuSsspShardBackend, push_block, row_block)
+    P, scale = 4, 14
+    n = 1 << scale
+    graphs = [gm.Graph.rmat(scale, 16, seed=13, weights=True, relabel=True, shards=P)
+              for _ in range(P)]
+    bes = [GpuSsspShardBackend(graphs[r], *row_block(n, P, r)) for r in range(P)]
+    g0 = graphs[0]
+    perm = g0.permutation()
+    root_ext = g0.pick_source(13)
+    root = int(perm[root_ext])
+    deg_int = np.empty(n, np.int64)
+    deg_int[perm] = g0.degree_vector("out")
+    bufs = [[torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(P)] for _ in range(2)]
+    for r, b in enumerate(bes):
+        b.init(root)
+        push_block(b.g, b.msg.data_ptr(), n * 4, [bufs[0][r].data_ptr()], 0)
+    nf, mf, it, dirs = 1, int(deg_int[root]), 0, []
+    while nf > 0:
+        pull = mf * SSSP_PULL_DIV > g0.num_edges
+        res = [b.step_ptr(pull, bufs[it % 2][r].data_ptr()) for r, b in enumerate(bes)]
+        tg = [t.data_ptr() for t in bufs[(it + 1) % 2]]
+        for b in bes:
+            push_block(b.g, b.msg_block.data_ptr(), (b.hi - b.lo) * 4, tg, b.lo * 4)
+        nf, mf = sum(x[0] for x in res), sum(x[1] for x in res)
+        dirs.append(pull)
+        it += 1
+    assert any(dirs) and not all(dirs)
+    d_int = np.concatenate([b.dists() for b in bes])
+    s, d, w = g0.edges()
+    want, _ = orc.sssp(n, s, d, w, root_ext, presorted=True)
+    assert np.array_equal(d_int[perm], want)
+
+    # CF: vertex blocks, factor blocks copied into every full matrix
+    k, iters = 20, 3
+    gb = gm.Graph.bipartite(2000, 150, 8000.0, 150, seed=6)
+    nb = gb.num_vertices
+    init = np.random.default_rng(6).uniform(0, 0.1, (nb, k)).astype(np.float32)
+    want_f, want_rm, _ = gm.collaborative_filtering_gd(gb, k, 1e-3, 0.05, iters, init=init)
+    pb = gb.permutation()
+    f_int = np.empty_like(init)
+    f_int[pb] = init
+    step = (nb + P - 1) // P
+    blocks = [(min(r * step, nb), min((r + 1) * step, nb)) for r in range(P)]
+    cgs = [gm.Graph.bipartite(2000, 150, 8000.0, 150, seed=6) for _ in range(P)]
+    cbs = [GpuCfShardBackend(cgs[r], *blocks[r], k=k) for r in range(P)]
+    fb = [[torch.from_numpy(f_int).cuda() for _ in range(P)] for _ in range(2)]
+    for t in range(iters):
+        for r, b in enumerate(cbs):
+            b.step_ptr(1e-3, 0.05, fb[t % 2][r].data_ptr())
+        tg = [x.data_ptr() for x in fb[(t + 1) % 2]]
+        for b in cbs:
+            push_block(b.g, b.block.data_ptr(), (b.hi - b.lo) * k * 4, tg, b.lo * k * 4)
+    got = fb[iters % 2][0].cpu().numpy()[pb]
+    assert np.array_equal(got.view(np.uint32), want_f.view(np.uint32))
+
+
+def _sssp_cf_ipc_worker(rank, world, port, out_d, out_f, out_rm):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1503_07241_b200 as gm
+    from paper_1503_07241_b200.sharded import (FusedCf, FusedSssp, GpuCfShardBackend,
+                                               GpuSsspShardBackend, TorchExchange, row_block)
+
+    class CpuExchange(TorchExchange):
+        def allreduce_sum(self, value, like):
+            return super().allreduce_sum(value, torch.empty(0))
+
+    scale = 13
+    n = 1 << scale
+    g = gm.Graph.rmat(scale, 16, seed=13, weights=True, relabel=True, shards=world)
+    perm = g.permutation()
+    root = int(perm[g.pick_source(13)])
+    deg_int = np.empty(n, np.int64)
+    deg_int[perm] = g.degree_vector("out")
+    lo, hi = row_block(n, world, rank)
+    f = FusedSssp(GpuSsspShardBackend(g, lo, hi), CpuExchange())
+    dv, _ = f.run(n, g.num_edges, root, int(deg_int[root]))
+    f.close()
+    out_d[lo:hi] = torch.from_numpy(dv.view(np.int32))
+    gb = gm.Graph.bipartite(2000, 150, 8000.0, 150, seed=6)
+    nb, k = gb.num_vertices, 20
+    init = np.random.default_rng(6).uniform(0, 0.1, (nb, k)).astype(np.float32)
+    f_int = np.empty_like(init)
+    f_int[gb.permutation()] = init
+    blk = nb // world
+    clo, chi = rank * blk, (nb if rank == world - 1 else (rank + 1) * blk)
+    be = GpuCfShardBackend(gb, clo, chi, k=k)
+    be.init(f_int)
+    fc = FusedCf(be, CpuExchange())
+    fac, rm, _ = fc.run(gb.num_edges, 1e-3, 0.05, 3)
+    fc.close()
+    out_f[clo:chi] = torch.from_numpy(fac)
+    if rank == 0:
+        out_rm[:] = torch.tensor(rm, dtype=torch.float64)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_sssp_cf_fused_ipc_two_processes(gm, orc):
+    """FusedSssp and FusedCf across two processes on one GPU over real CUDA
+    IPC mappings (gloo all-reduces as the barrier): SSSP distances equal the
+    oracle's, CF factors equal gm_cf bit for bit and its RMSE trace."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    n = 1 << 13
+    gb = gm.Graph.bipartite(2000, 150, 8000.0, 150, seed=6)
+    nb = gb.num_vertices
+    out_d = torch.zeros(n, dtype=torch.int32).share_memory_()
+    out_f = torch.zeros((nb, 20), dtype=torch.float32).share_memory_()
+    out_rm = torch.zeros(3, dtype=torch.float64).share_memory_()
+    mp.spawn(_sssp_cf_ipc_worker, args=(2, port, out_d, out_f, out_rm), nprocs=2, join=True)
+    g = gm.Graph.rmat(13, 16, seed=13, weights=True, relabel=True, shards=2)
+    perm = g.permutation()
+    s, d, w = g.edges()
+    want, _ = orc.sssp(n, s, d, w, g.pick_source(13), presorted=True)
+    assert np.array_equal(out_d.numpy().view(np.uint32)[perm], want)
+    init = np.random.default_rng(6).uniform(0, 0.1, (nb, 20)).astype(np.float32)
+    want_f, want_rm, _ = gm.collaborative_filtering_gd(gb, 20, 1e-3, 0.05, 3, init=init)
+    got = out_f.numpy()[gb.permutation()]
+    assert np.array_equal(got.view(np.uint32), want_f.view(np.uint32))
+    np.testing.assert_allclose(out_rm.numpy(), want_rm, rtol=1e-12)

@@ -51,6 +51,28 @@ struct can_fail : std::false_type {};
 template <typename P>
 struct can_fail<P, std::void_t<decltype(P::kCanFail)>> : std::bool_constant<P::kCanFail> {};
 
+// Programs whose reduce is exactly associative and commutative with a true
+// identity (min of doubles, integer sums) may fold a row in any order and
+// get the sequential result bit for bit; they declare kExactReorder.
+template <typename P, typename = void>
+struct exact_reorder : std::false_type {};
+template <typename P>
+struct exact_reorder<P, std::void_t<decltype(P::kExactReorder)>>
+    : std::bool_constant<P::kExactReorder> {};
+
+// __shfl_xor_sync of any trivially copyable value, 32 bits at a time
+template <typename T>
+__device__ __forceinline__ T shfl_xor_any(const T& v, int o) {
+  static_assert(sizeof(T) % 4 == 0, "shuffled values must be whole 32-bit words");
+  uint32_t w[sizeof(T) / 4];
+  memcpy(w, &v, sizeof(T));
+#pragma unroll
+  for (int i = 0; i < int(sizeof(T) / 4); ++i) w[i] = __shfl_xor_sync(0xffffffffu, w[i], o);
+  T out;
+  memcpy(&out, w, sizeof(T));
+  return out;
+}
+
 enum Phase : int { kPhaseNone = 0, kPhaseSend = 1, kPhaseSpmv = 2, kPhaseApply = 3 };
 
 struct DevError {
@@ -238,6 +260,16 @@ __global__ void __launch_bounds__(kLongThreads) k_pull_long(
           break;
         }
       }
+      if constexpr (exact_reorder<P>::value && !can_fail<P>::value) {
+        // order-free programs: every lane folds its own entries, the warp
+        // combines the 32 partials at the end of the row
+        if (valid) {
+          acc = any ? p.reduce(acc, r) : p.reduce(p.reduce_identity(), r);
+          any = true;
+        }
+        cur = nxt;
+        continue;
+      }
       if (valid) s_r[lane] = r;
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
       __syncwarp();
@@ -259,6 +291,17 @@ __global__ void __launch_bounds__(kLongThreads) k_pull_long(
       }
       __syncwarp();
       cur = nxt;
+    }
+    if constexpr (exact_reorder<P>::value && !can_fail<P>::value) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const R other = shfl_xor_any(acc, o);
+        const bool oany = __shfl_xor_sync(0xffffffffu, any, o);
+        if (oany) {
+          acc = any ? p.reduce(acc, other) : other;
+          any = true;
+        }
+      }
     }
     if (lane == 0 && any) {
       y[k] = acc;

@@ -87,6 +87,9 @@ struct NormPageRank : PageRankRef {
 
 // ---- BfsProgram / SsspProgram, algorithms/traversal.hpp:39-91 ----------------
 struct BfsRef {
+  // min of doubles (no NaN, no -0 from the reference's non-negative
+  // distances): any fold order gives the sequential result
+  static constexpr bool kExactReorder = true;
   using vertex_t = double;  // DistanceState{distance}
   using edge_t = NoEdge;
   using message_t = double;
@@ -124,6 +127,7 @@ struct SemiringI64 {
   using edge_t = int64_t;
   using message_t = int64_t;
   using reduced_t = int64_t;
+  static constexpr bool kExactReorder = true;  // integer sums (wrapping) are order-free
   static constexpr gm_value_type kEdgeType = GM_VAL_I64;
   __host__ __device__ Direction direction() const { return Direction::OUT; }
   __device__ bool send_message(const vertex_t& v, uint64_t, message_t* out) const {

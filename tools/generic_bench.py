@@ -20,3 +20,17 @@ for relabel in (False, True):
     us = [round(s.spmv_seconds * 1e6, 1) for s in st]
     print(f"scale {scale} relabel={relabel} nnz={g.num_edges} spmv_us={us} wall_ms={wall*1e3:.1f} "
           f"gteps={g.num_edges / np.median([s.spmv_seconds for s in st]) / 1e9:.2f}")
+
+# the reference's BfsProgram through the generic engine (min reduce: order-free path)
+g = gm.Graph.rmat(scale, 16, seed=1, symmetrize=True, relabel=True)
+n = g.num_vertices
+root = g.pick_source(1)
+for rep in range(2):
+    dist = np.full(n, np.inf)
+    dist[root] = 0.0
+    act = np.zeros(n, np.uint8)
+    act[root] = 1
+    st = gm.run_graph_program(g, gm.PROG_BFS_REF, dist, act, n + 1)
+tot = sum(s.spmv_seconds for s in st)
+print(f"scale {scale} BfsProgram supersteps={len(st)} spmv_ms={tot*1e3:.2f} "
+      f"per_step_us={[round(s.spmv_seconds*1e6,1) for s in st]}")

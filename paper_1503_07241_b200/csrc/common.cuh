@@ -23,11 +23,16 @@ struct Error {
 
 [[noreturn]] inline void fail(gm_status code, std::string msg) { throw Error{code, std::move(msg)}; }
 
+// A failed runtime call also leaves its (non-sticky) error in the runtime's
+// last-error slot; it is cleared here so the next launch check of an
+// unrelated call does not report it again.
 #define GM_CUDA(call)                                                                    \
   do {                                                                                   \
     cudaError_t e_ = (call);                                                             \
-    if (e_ != cudaSuccess)                                                               \
+    if (e_ != cudaSuccess) {                                                             \
+      (void)cudaGetLastError();                                                          \
       ::gm::fail(GM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+    }                                                                                    \
   } while (0)
 
 // Every kernel launch is followed by GM_LAUNCH_CHECK(), which also counts it

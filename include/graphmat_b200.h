@@ -264,7 +264,12 @@ GM_API gm_status gm_fnv1a64_file(const char* path, uint64_t* out);
 typedef enum {
   GM_PROG_PAGERANK_REF = 1,    /* PageRankProgram, pagerank.hpp:36-63 (fp64)          */
   GM_PROG_BFS_REF = 2,         /* BfsProgram, traversal.hpp:39-63 (fp64)              */
-  GM_PROG_SSSP_REF = 3,        /* SsspProgram, traversal.hpp:67-91 (fp64 weights)     */
+  GM_PROG_SSSP_REF = 3,        /* SsspProgram, traversal.hpp:67-91 (fp64 weights).
+                                  BFS_REF / SSSP_REF fold min lane-parallel, which is
+                                  bit-identical to the reference's sequential fold for
+                                  NaN-free distances and weights (algo::sssp rejects
+                                  NaN / negative weights, traversal.hpp:125-133);
+                                  with a NaN in props or weights the run is GM_EINPUT. */
   GM_PROG_SEMIRING_I64 = 4,    /* tests/acceptance.cpp:94-116                          */
   GM_PROG_ADD_PROBE = 5,       /* tests/test_engine.cpp:31-43                          */
   GM_PROG_IN_ADD_PROBE = 6,    /* tests/test_engine.cpp:206-223                        */

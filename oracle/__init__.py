@@ -112,10 +112,10 @@ def lib():
                                   C.POINTER(Stats)]
     L.or_cf_gd.restype = None
     L.or_cf_gd.argtypes = [C.c_uint64, u64p, u32p, f64p, u64p, u32p, f64p, C.c_int64,
-                           C.c_double, C.c_double, C.c_int64, f64p, f64p, f64p]
+                           C.c_double, C.c_double, C.c_int64, f64p, f64p, f64p, i64p]
     L.or_cf_gd_f32.restype = None
     L.or_cf_gd_f32.argtypes = [C.c_uint64, u64p, u32p, f64p, u64p, u32p, f64p, C.c_int64,
-                               C.c_float, C.c_float, C.c_int64, f32p, f64p]
+                               C.c_float, C.c_float, C.c_int64, f32p, f64p, i64p]
     L.or_semiring_spmv.restype = None
     L.or_semiring_spmv.argtypes = [C.c_uint64, u64p, u32p, i64p, i64p, u8p, i64p, u8p]
     _LIB = L
@@ -141,7 +141,7 @@ def ref_lib():
     R.ref_pagerank_norm.argtypes = common + [C.c_double, C.c_int64, C.c_uint, f64p] + sp
     R.ref_cf.argtypes = common + [f64p, C.c_int64, C.c_double, C.c_double, C.c_int64,
                                   C.c_uint, C.c_int, f64p, C.c_void_p, C.c_void_p,
-                                  C.POINTER(C.c_double)]
+                                  C.POINTER(C.c_double), C.c_void_p]
     R.ref_semiring_spmv.argtypes = common + [i64p, i64p, u8p, C.c_uint, C.c_uint, i64p, u8p]
     R.ref_triangle_count.argtypes = common + [C.c_uint, C.c_uint, C.POINTER(C.c_uint64),
                                               C.c_void_p, C.POINTER(C.c_double)]
@@ -344,21 +344,22 @@ def pagerank_ref(n, src, dst, r=0.15, iters=20):
     return rank, stats_tuples(st, k)
 
 
-def cf_gd(n, src, dst, rating, factors, gamma, lam, iters, fp32=False):
-    """Returns (factors, objective_trace or None, rmse_trace)."""
+def cf_gd(n, src, dst, rating, factors, gamma, lam, iters, fp32=False, with_updated=False):
+    """Returns (factors, objective_trace or None, rmse_trace[, vertices_updated])."""
     rating = np.asarray(rating, np.float64)
     tptr, tidx, tval = in_csr(n, src, dst, rating)
     fptr, fidx, fval = out_csr(n, src, dst, rating)
     k = factors.shape[1]
     rm = np.zeros(iters, np.float64)
+    upd = np.zeros(max(iters, 1), np.int64)
     if fp32:
         f = np.ascontiguousarray(factors, np.float32).copy()
-        lib().or_cf_gd_f32(n, tptr, tidx, tval, fptr, fidx, fval, k, gamma, lam, iters, f, rm)
-        return f, None, rm
+        lib().or_cf_gd_f32(n, tptr, tidx, tval, fptr, fidx, fval, k, gamma, lam, iters, f, rm, upd)
+        return (f, None, rm, upd[:iters]) if with_updated else (f, None, rm)
     f = np.ascontiguousarray(factors, np.float64).copy()
     obj = np.zeros(iters, np.float64)
-    lib().or_cf_gd(n, tptr, tidx, tval, fptr, fidx, fval, k, gamma, lam, iters, f, obj, rm)
-    return f, obj, rm
+    lib().or_cf_gd(n, tptr, tidx, tval, fptr, fidx, fval, k, gamma, lam, iters, f, obj, rm, upd)
+    return (f, obj, rm, upd[:iters]) if with_updated else (f, obj, rm)
 
 
 def semiring_spmv(n, src, dst, vals, x, xvalid):
@@ -436,17 +437,20 @@ def ref_pagerank_norm(n, src, dst, damping=0.85, iters=20, threads=0):
     return out, stats_tuples(st, k.value), t.value
 
 
-def ref_cf(n, src, dst, rating, factors, gamma, lam, iters, threads=0, per_iteration=True):
+def ref_cf(n, src, dst, rating, factors, gamma, lam, iters, threads=0, per_iteration=True,
+           with_updated=False):
     R = ref_lib()
     f = np.ascontiguousarray(factors, np.float64).copy()
     obj = np.zeros(max(iters, 1), np.float64)
     rm = np.zeros(max(iters, 1), np.float64)
+    upd = np.zeros(max(iters, 1), np.int64)
     t = C.c_double()
     _ref_call(R.ref_cf, n, len(src), _u32(src), _u32(dst),
               np.ascontiguousarray(rating, np.float64), f.shape[1], gamma, lam, iters,
               threads, 1 if per_iteration else 0, f, obj.ctypes.data,
-              rm.ctypes.data if per_iteration else None, C.byref(t))
-    return f, obj[:iters], (rm[:iters] if per_iteration else None), t.value
+              rm.ctypes.data if per_iteration else None, C.byref(t), upd.ctypes.data)
+    out = (f, obj[:iters], (rm[:iters] if per_iteration else None), t.value)
+    return out + (upd[:iters],) if with_updated else out
 
 
 def ref_semiring_spmv(n, src, dst, vals, x, xvalid, threads=1, parts=1):

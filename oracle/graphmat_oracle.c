@@ -771,13 +771,14 @@ static int cf_fold_row(const uint64_t* ptr, const uint32_t* idx, const double* v
 void or_cf_gd(uint64_t n, const uint64_t* tptr, const uint32_t* tidx, const double* tval,
               const uint64_t* fptr, const uint32_t* fidx, const double* fval, int64_t k,
               double gamma, double lambda, int64_t iters, double* factors,
-              double* objective_trace, double* rmse_trace) {
+              double* objective_trace, double* rmse_trace, int64_t* updated) {
   double* nf = (double*)malloc(sizeof(double) * (size_t)(n * (uint64_t)k + 1));
   double* yo = (double*)malloc(sizeof(double) * (size_t)k);
   double* yi = (double*)malloc(sizeof(double) * (size_t)k);
   double* r = (double*)malloc(sizeof(double) * (size_t)k);
   const int64_t m = n ? (int64_t)tptr[n] : 0;
   for (int64_t it = 0; it < iters; ++it) {
+    int64_t upd = 0;
     for (uint64_t v = 0; v < n; ++v) {
       const int vo = cf_fold_row(tptr, tidx, tval, v, k, factors, yo, r);
       const int vi = cf_fold_row(fptr, fidx, fval, v, k, factors, yi, r);
@@ -795,7 +796,12 @@ void or_cf_gd(uint64_t n, const uint64_t* tptr, const uint32_t* tidx, const doub
         const double p = factors[v * (uint64_t)k + (uint64_t)i];
         nf[v * (uint64_t)k + (uint64_t)i] = p + gamma * (s - lambda * p);
       }
+      /* apply_and_activate counts messaged vertices whose LatentVector changed
+       * bitwise (engine.hpp:139-172, collaborative_filtering.hpp:29-35, 189) */
+      if (vo || vi)
+        upd += memcmp(nf + v * (uint64_t)k, factors + v * (uint64_t)k, sizeof(double) * (size_t)k) != 0;
     }
+    if (updated) updated[it] = upd;
     memcpy(factors, nf, sizeof(double) * (size_t)(n * (uint64_t)k));
     /* cf_objective_value (collaborative_filtering.hpp:103-123): ratings grouped
      * by user (column of G^T), ascending. */
@@ -839,13 +845,14 @@ static int cf_fold_row_f32(const uint64_t* ptr, const uint32_t* idx, const doubl
 void or_cf_gd_f32(uint64_t n, const uint64_t* tptr, const uint32_t* tidx, const double* tval,
                   const uint64_t* fptr, const uint32_t* fidx, const double* fval, int64_t k,
                   float gamma, float lambda, int64_t iters, float* factors,
-                  double* rmse_trace) {
+                  double* rmse_trace, int64_t* updated) {
   float* nf = (float*)malloc(sizeof(float) * (size_t)(n * (uint64_t)k + 1));
   float* yo = (float*)malloc(sizeof(float) * (size_t)k);
   float* yi = (float*)malloc(sizeof(float) * (size_t)k);
   float* r = (float*)malloc(sizeof(float) * (size_t)k);
   const int64_t m = n ? (int64_t)tptr[n] : 0;
   for (int64_t it = 0; it < iters; ++it) {
+    int64_t upd = 0;
     for (uint64_t v = 0; v < n; ++v) {
       const int vo = cf_fold_row_f32(tptr, tidx, tval, v, k, factors, yo, r);
       const int vi = cf_fold_row_f32(fptr, fidx, fval, v, k, factors, yi, r);
@@ -856,7 +863,10 @@ void or_cf_gd_f32(uint64_t n, const uint64_t* tptr, const uint32_t* tidx, const 
         const float p = factors[v * (uint64_t)k + (uint64_t)i];
         nf[v * (uint64_t)k + (uint64_t)i] = p + gamma * (s - lambda * p);
       }
+      if (vo || vi)
+        upd += memcmp(nf + v * (uint64_t)k, factors + v * (uint64_t)k, sizeof(float) * (size_t)k) != 0;
     }
+    if (updated) updated[it] = upd;
     memcpy(factors, nf, sizeof(float) * (size_t)(n * (uint64_t)k));
     double sq = 0.0;
     for (uint64_t u = 0; u < n; ++u) {

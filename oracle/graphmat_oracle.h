@@ -104,12 +104,13 @@ int64_t or_pagerank_ref(uint64_t n, const uint64_t* iptr, const uint32_t* iidx,
 void or_cf_gd(uint64_t n, const uint64_t* tptr, const uint32_t* tidx, const double* tval,
               const uint64_t* fptr, const uint32_t* fidx, const double* fval, int64_t k,
               double gamma, double lambda, int64_t iters, double* factors,
-              double* objective_trace, double* rmse_trace);
+              double* objective_trace, double* rmse_trace, int64_t* updated);
 /* Same update carried in fp32 (the GPU's arithmetic type), for tighter comparisons. */
 void or_cf_gd_f32(uint64_t n, const uint64_t* tptr, const uint32_t* tidx, const double* tval,
                   const uint64_t* fptr, const uint32_t* fidx, const double* fval, int64_t k,
                   float gamma, float lambda, int64_t iters, float* factors,
-                  double* rmse_trace);
+                  double* rmse_trace, int64_t* updated);
+/* updated (may be NULL): IterationStats::vertices_updated per iteration. */
 /* y[k] = sum over stored (k,j) with xvalid[j] of A[k,j]*x[j]; yvalid iff any term. */
 void or_semiring_spmv(uint64_t n, const uint64_t* iptr, const uint32_t* iidx,
                       const int64_t* vals, const int64_t* x, const uint8_t* xvalid, int64_t* y,

@@ -239,7 +239,7 @@ int ref_pagerank_norm(uint64_t n, int64_t m, const uint32_t* src, const uint32_t
 int ref_cf(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
            const double* ratings, int64_t k, double gamma, double lambda, int64_t iters,
            unsigned threads, int per_iteration, double* factors, double* objective_trace,
-           double* rmse_trace, double* algo_seconds) {
+           double* rmse_trace, double* algo_seconds, int64_t* updated) {
   return guarded([&] {
     threads = resolve_threads(threads);
     auto e = triples(m, src, dst, ratings);
@@ -269,16 +269,22 @@ int ref_cf(uint64_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
       cc.iterations = 1;
       for (int64_t it = 0; it < iters; ++it) {
         const double t0 = now_s();
-        auto res = algo::collaborative_filtering_gd(g, eng, cc);
+        std::vector<IterationStats> st;
+        auto res = algo::collaborative_filtering_gd(g, eng, cc, &st);
         algo += now_s() - t0;
+        if (updated) updated[it] = static_cast<int64_t>(st.back().vertices_updated);
         if (objective_trace) objective_trace[it] = res.objective_trace.back();
         if (rmse_trace) rmse_trace[it] = rmse_now();
       }
     } else {
       cc.iterations = static_cast<std::size_t>(iters);
       const double t0 = now_s();
-      auto res = algo::collaborative_filtering_gd(g, eng, cc);
+      std::vector<IterationStats> st;
+      auto res = algo::collaborative_filtering_gd(g, eng, cc, &st);
       algo = now_s() - t0;
+      if (updated)
+        for (std::size_t i = 0; i < st.size(); ++i)
+          updated[i] = static_cast<int64_t>(st[i].vertices_updated);
       if (objective_trace)
         for (std::size_t i = 0; i < res.objective_trace.size(); ++i)
           objective_trace[i] = res.objective_trace[i];

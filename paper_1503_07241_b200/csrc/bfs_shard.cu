@@ -152,7 +152,7 @@ struct PeerWords {
   int n;
 };
 
-__global__ void k_sb_push(const uint32_t* next_blk, uint64_t w0, uint64_t nw, PeerWords pw) {
+__global__ void k_sb_peer_store(const uint32_t* next_blk, uint64_t w0, uint64_t nw, PeerWords pw) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nw;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t v = next_blk[i];
@@ -241,7 +241,7 @@ void bfs_shard_push(Graph& g, uint64_t lo, uint64_t hi, const uint32_t* next_blo
   pw.n = npeers;
   const uint64_t nw = (hi - lo + 31) / 32;
   if (nw) {
-    k_sb_push<<<grid_for(nw, 256), 256, 0, g.stream>>>(next_block, lo / 32, nw, pw);
+    k_sb_peer_store<<<grid_for(nw, 256), 256, 0, g.stream>>>(next_block, lo / 32, nw, pw);
     GM_LAUNCH_CHECK();
   }
   GM_CUDA(cudaStreamSynchronize(g.stream));

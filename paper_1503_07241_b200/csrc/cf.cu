@@ -35,6 +35,7 @@ struct CfCache {
   DevBuf<float> part_t, part_f;             // nitems * k
   DevBuf<float> sq;                         // per item of the forward pass
   DevBuf<float> f0, f1;
+  DevBuf<uint32_t> vbits;                   // changed-vertex bitmap of one apply
 };
 
 namespace {
@@ -259,7 +260,8 @@ __global__ void __launch_bounds__(256) k_cf_items_grp(const uint32_t* __restrict
 // by the local one (the single-GPU call passes lo = 0).
 __global__ void k_cf_apply(uint64_t lo, uint64_t n, int k, const uint32_t* rit, const uint32_t* rif,
                            const float* part_t, const float* part_f, const float* f, float* fn,
-                           float gamma, float lambda, unsigned long long* changed) {
+                           float gamma, float lambda, uint32_t* vbits,
+                           unsigned long long* changed) {
   unsigned long long ch = 0;
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n * uint64_t(k);
        t += uint64_t(gridDim.x) * blockDim.x) {
@@ -282,7 +284,13 @@ __global__ void k_cf_apply(uint64_t lo, uint64_t n, int k, const uint32_t* rit, 
     const float p = f[lo * uint64_t(k) + t];
     const float np = p + gamma * (s - lambda * p);
     fn[t] = np;
-    ch += (__float_as_uint(np) != __float_as_uint(p)) && (any || anyi);
+    // vertices_updated counts vertices (engine.hpp:139-172: a messaged vertex
+    // whose LatentVector differs in any component, collaborative_filtering.hpp:
+    // 29-35): the first component thread of v to see a change claims v's bit.
+    if ((__float_as_uint(np) != __float_as_uint(p)) && (any || anyi)) {
+      const uint32_t bit = 1u << (v & 31u);
+      ch += !(atomicOr(&vbits[v >> 5], bit) & bit);
+    }
   }
   warp_add_u64(changed, ch);
 }
@@ -427,9 +435,12 @@ void cf_shard_step(Graph& g, uint64_t lo, uint64_t hi, int64_t k, const float* f
   run_pass_on(c, g, true, f_full, int(k), c.sq.get());
   const uint64_t total = (hi - lo) * uint64_t(k);
   if (total) {
+    if (c.vbits.size() < (hi - lo + 31) / 32) c.vbits.alloc((hi - lo + 31) / 32, s);
+    c.vbits.zero(s);
     k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(lo, hi - lo, int(k), c.rowitem_t.get(),
                                                     c.rowitem_f.get(), c.part_t.get(), c.part_f.get(),
-                                                    f_full, f_block, gamma, lambda, upd.get());
+                                                    f_full, f_block, gamma, lambda, c.vbits.get(),
+                                                    upd.get());
     GM_LAUNCH_CHECK();
   }
   if (c.nit_f) {
@@ -520,10 +531,13 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
     GM_CUDA(cudaEventRecord(ev[2 * (it - 1)], s));
     run_pass(false, f, nullptr);  // items receive from users (G^T)
     run_pass(true, f, c.sq.get());  // users receive from items (G); squared errors
-    if (total)
+    if (total) {
+      if (c.vbits.size() < (n + 31) / 32) c.vbits.alloc((n + 31) / 32, s);
+      c.vbits.zero(s);
       k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(0, n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
                                                       c.part_t.get(), c.part_f.get(), f, fn, gamma,
-                                                      lambda, upd.get() + it);
+                                                      lambda, c.vbits.get(), upd.get() + it);
+    }
     GM_LAUNCH_CHECK();
     GM_CUDA(cudaEventRecord(ev[2 * (it - 1) + 1], s));
     // the forward pass saw the factors after update it-1: post-update RMSE of it-1

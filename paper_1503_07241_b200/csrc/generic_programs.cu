@@ -272,6 +272,41 @@ void dispatch(int prog, const double* params, F&& f) {
   }
 }
 
+__global__ void k_count_nan_f64(const double* v, uint64_t n, unsigned long long* bad) {
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    c += v[i] != v[i];
+  if (c) atomicAdd(bad, c);
+}
+
+// BfsRef / SsspRef fold min lane-parallel (kExactReorder); that equals the
+// reference's sequential `a < b ? a : b` fold only without NaN (and without
+// -0 ties).  algo::sssp rejects such inputs in its wrapper (traversal.hpp:
+// 125-133); the raw programs get the same guard here.
+void check_min_fold_inputs(Graph& g, int prog, const void* props) {
+  if (prog != GM_PROG_BFS_REF && prog != GM_PROG_SSSP_REF) return;
+  const double* p = static_cast<const double*>(props);
+  for (uint64_t v = 0; v < g.n; ++v) {
+    uint64_t b;
+    std::memcpy(&b, &p[v], 8);
+    if (p[v] != p[v] || b == 0x8000000000000000ull)
+      fail(GM_EINPUT, "distance of vertex " + std::to_string(v + 1) +
+                          " is NaN or -0; the min fold needs ordered distances");
+  }
+  if (prog == GM_PROG_SSSP_REF && g.value_type == GM_VAL_F64 && g.m) {
+    DevBuf<unsigned long long> bad(1, g.stream);
+    bad.zero(g.stream);
+    k_count_nan_f64<<<grid_for(g.m, 256), 256, 0, g.stream>>>(
+        reinterpret_cast<const double*>(g.in.val.get()), g.m, bad.get());
+    GM_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    GM_CUDA(cudaMemcpyAsync(&h, bad.get(), 8, cudaMemcpyDeviceToHost, g.stream));
+    GM_CUDA(cudaStreamSynchronize(g.stream));
+    if (h) fail(GM_EINPUT, "sssp: edge weights must be non-negative and not NaN");
+  }
+}
+
 }  // namespace
 
 void program_sizes(int prog, size_t* v, size_t* m, size_t* r) {
@@ -284,6 +319,7 @@ std::vector<gm_iteration_stats> run_program(Graph& g, int prog, const double* pa
   dispatch(prog, params, [&](auto p) {
     using P = decltype(p);
     if (max_iters <= 0) return;  // zero budget is a no-op (engine.hpp:197)
+    check_min_fold_inputs(g, prog, props);
     Engine<P> eng(g, p);
     eng.load(props, active);
     st = eng.run(max_iters);
@@ -297,6 +333,7 @@ void superstep_phases(Graph& g, int prog, const double* params, const void* prop
                       uint8_t* y_valid) {
   dispatch(prog, params, [&](auto p) {
     using P = decltype(p);
+    check_min_fold_inputs(g, prog, props);
     Engine<P> eng(g, p);
     eng.load(props, active);
     const uint64_t n = g.n;

@@ -615,6 +615,9 @@ class FusedSssp:
     def run(self, n: int, m: int, root: int, root_degree: int, max_iters=None):
         be, ex, g = self.backend, self.exchange, self.backend.g
         be.init(root)  # be.msg (torch) = INF everywhere, 0 at the root
+        # the fill ran on torch's stream; the seed copy runs on the graph's
+        import torch
+        torch.cuda.current_stream().synchronize()
         push_block(g, be.msg.data_ptr(), n * 4, [self.pair.local(0)], 0)
         nf, mf, it = 1, root_degree, 0
         cap = n + 1 if max_iters is None else max_iters
@@ -648,18 +651,23 @@ class FusedCf:
         import math
         be, ex, g = self.backend, self.exchange, self.backend.g
         k = be.k
+        import torch
+        torch.cuda.current_stream().synchronize()  # be.full was filled on torch's stream
         push_block(g, be.full.data_ptr(), be.full.numel() * 4, [self.pair.local(0)], 0)
         rmse, updated = [], []
         for it in range(iterations + 1):
             sq, ch = be.step_ptr(gamma, lam, self.pair.local(it))
+            # the peer copies go out before the all-reduce, which then orders
+            # every rank's copy of block (it+1) before anyone's next step
+            if it < iterations:
+                push_block(g, be.block.data_ptr(), (be.hi - be.lo) * k * 4,
+                           self.pair.targets(it + 1), be.lo * k * 4)
             sq = ex.allreduce_sum(sq, be.full)
             if it > 0:
                 rmse.append(math.sqrt(sq / m) if m else 0.0)
             if it == iterations:
                 break
             updated.append(int(round(ex.allreduce_sum(float(ch), be.full))))
-            push_block(g, be.block.data_ptr(), (be.hi - be.lo) * k * 4,
-                       self.pair.targets(it + 1), be.lo * k * 4)
         # this block's final factors (the last step's block output is one
         # update further: it only evaluated the closing RMSE)
         push_block(g, self.pair.local(iterations) + be.lo * k * 4, (be.hi - be.lo) * k * 4,

@@ -75,12 +75,14 @@ def main():
         n = users + items
         k = int(rng.choice([2, 4, 20]))
         f0 = rng.uniform(0, 0.1, (n, k))
-        f, obj, rm, _ = oracle.ref_cf(n, s, d, rating, f0, 1e-3, 0.05, 10, threads=2)
+        f, obj, rm, _, upd = oracle.ref_cf(n, s, d, rating, f0, 1e-3, 0.05, 10, threads=2,
+                                           with_updated=True)
         key = f"cf{t}"
         out[f"{key}_n"] = np.array([n, k])
         out[f"{key}_src"], out[f"{key}_dst"], out[f"{key}_rating"] = s, d, rating
         out[f"{key}_init"], out[f"{key}_factors"] = f0, f
         out[f"{key}_objective"], out[f"{key}_rmse"] = obj, rm
+        out[f"{key}_updated"] = upd  # IterationStats::vertices_updated per iteration
     out["cases"] = np.array(cases)
     np.savez_compressed(OUT, **out)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

@@ -92,7 +92,9 @@ def _cf_case(gm, orc, users, iters):
     rng = np.random.default_rng(1)
     f0 = rng.uniform(0, 0.1, (n, 20))
     f, rm, st = gm.collaborative_filtering_gd(g, 20, 1e-3, 0.05, iters, init=f0.astype(np.float32))
-    _, _, want = orc.cf_gd(n, s, d, r.astype(np.float64), f0, 1e-3, 0.05, iters)
+    _, _, want, upd = orc.cf_gd(n, s, d, r.astype(np.float64), f0, 1e-3, 0.05, iters,
+                                with_updated=True)
+    _cf_case.stats = ([x.vertices_updated for x in st], list(upd))
     return rm, want, len(s)
 
 
@@ -100,8 +102,12 @@ def test_config3_cf_reduced(gm, orc):
     rm, want, m = _cf_case(gm, orc, 480189 // 8, 3)
     assert m > 1_000_000
     finite = np.isfinite(want) & np.isfinite(rm)
-    assert finite[0]
-    np.testing.assert_allclose(rm[finite], want[finite], rtol=1e-4)
+    assert finite.all()
+    # north_star: 1e-4 RMSE delta (absolute), on every iteration
+    assert np.max(np.abs(rm - want)) <= 1e-4, (rm, want)
+    # vertices_updated per superstep equals the fp64 oracle's (engine.hpp:139-172)
+    got, exp = _cf_case.stats
+    assert got == exp, (got, exp)
 
 
 def test_config3_cf_full_divergence(gm, orc):

@@ -149,6 +149,9 @@ def test_golden_cf(gm, golden):
         np.testing.assert_allclose(rm, golden[f"{key}_rmse"], atol=1e-4)
         np.testing.assert_allclose(f, golden[f"{key}_factors"], rtol=1e-4, atol=1e-6)
         assert len(st) == 10
+        # vertices_updated counts vertices, as the reference's IterationStats
+        assert [x.vertices_updated for x in st] == list(golden[f"{key}_updated"]), key
+        assert [x.active_before for x in st] == [n] * 10
 
 
 # ------------------------------------------------------- engine semantics
@@ -168,6 +171,24 @@ def test_bulk_synchronous_reads(gm):
     assert st[0].key() == (1, 3, 3, 2)
     assert list(props) == [1.0, 11.0, 110.0]
     assert list(act) == [0, 1, 1]
+
+
+def test_min_fold_programs_reject_nan(gm):
+    # BfsRef / SsspRef fold min lane-parallel; NaN inputs would make that
+    # differ from the reference's sequential fold, so they are InputErrors
+    # (algo::sssp's own guard, traversal.hpp:125-133).
+    s, d = [0, 1], [1, 2]
+    g = gm.Graph.from_edges(s, d, 3, np.array([1.0, np.nan]))
+    dist = np.array([0.0, np.inf, np.inf])
+    act = np.array([1, 0, 0], np.uint8)
+    with pytest.raises(gm.InputError, match="NaN"):
+        gm.run_graph_program(g, gm.PROG_SSSP_REF, dist, act, 5)
+    g = gm.Graph.from_edges(s, d, 3)
+    with pytest.raises(gm.InputError, match="NaN"):
+        gm.run_graph_program(g, gm.PROG_BFS_REF, np.array([0.0, np.nan, np.inf]), act, 5)
+    dist = np.array([0.0, np.inf, np.inf])
+    gm.run_graph_program(g, gm.PROG_BFS_REF, dist, act.copy(), 5)
+    assert list(dist) == [0.0, 1.0, 2.0]
 
 
 def test_zero_budget_noop(gm):
@@ -836,6 +857,7 @@ def test_sharded_sssp_cf_peer_copies_virtual(gm, orc):
     bufs = [[torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(P)] for _ in range(2)]
     for r, b in enumerate(bes):
         b.init(root)
+        torch.cuda.current_stream().synchronize()  # init filled msg on torch's stream
         push_block(b.g, b.msg.data_ptr(), n * 4, [bufs[0][r].data_ptr()], 0)
     nf, mf, it, dirs = 1, int(deg_int[root]), 0, []
     while nf > 0:

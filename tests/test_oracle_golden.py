@@ -112,9 +112,12 @@ def test_golden_cf(orc, golden):
     for t in range(4):
         key = f"cf{t}"
         n, k = (int(x) for x in golden[f"{key}_n"])
-        f, obj, rm = orc.cf_gd(n, golden[f"{key}_src"], golden[f"{key}_dst"],
-                               golden[f"{key}_rating"], golden[f"{key}_init"], 1e-3, 0.05, 10)
+        f, obj, rm, upd = orc.cf_gd(n, golden[f"{key}_src"], golden[f"{key}_dst"],
+                                    golden[f"{key}_rating"], golden[f"{key}_init"], 1e-3, 0.05, 10,
+                                    with_updated=True)
         assert np.array_equal(_bits(f), _bits(golden[f"{key}_factors"])), key
+        # IterationStats::vertices_updated (engine.hpp:139-172) counts vertices
+        assert np.array_equal(upd, golden[f"{key}_updated"]), key
         np.testing.assert_allclose(obj, golden[f"{key}_objective"], rtol=1e-12)
         np.testing.assert_allclose(rm, golden[f"{key}_rmse"], rtol=1e-12)
 

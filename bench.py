@@ -1,12 +1,16 @@
 #!/usr/bin/env python
 """bench.py -- GraphMat superstep hot path on B200 (BASELINE.json metric).
 
-Default workload (N=1): BASELINE configs[1], BFS on the symmetrised R-MAT
-scale-23 graph (edge factor 16, a/b/c = .57/.19/.19, seed 1, permuted ids),
-push/pull direction switch at 5% of edges.  One step = one full BFS from the
-seed-chosen root (all supersteps).  Other configs: --workload pagerank (configs[0],
-scale 20), pagerank23 (the scale-23 pull-SpMV roofline target), sssp (configs[2]),
-cf (configs[3]).
+Default workload: BASELINE configs[4], BFS on the symmetrised R-MAT scale-28
+graph (268,435,456 vertices, edge factor 16, a/b/c = .57/.19/.19, seed 1,
+permuted ids), push/pull direction switch at 5% of edges -- the largest
+single-GPU configuration of BASELINE.json.  N=1: one GPU holds the whole graph.
+N>1: 1-D row sharding over the ranks (strong scaling, one graph).  One step =
+one full BFS from the seed-chosen root (all supersteps).
+
+Other workloads (--workload): bfs (configs[1], scale 23), pagerank (configs[0],
+scale 20), pagerank23 (the scale-23 pull-SpMV roofline target), pagerank28
+(configs[4] PageRank), sssp (configs[2]), cf (configs[3]), tc.
 
 value  = whole-job GTEPS, inputs resident in HBM, device time (CUDA events on the
          library stream), max over ranks.  The K steps are enqueued back to back
@@ -17,8 +21,13 @@ value  = whole-job GTEPS, inputs resident in HBM, device time (CUDA events on th
 e2e    = the same metric through the public API (paper_1503_07241_b200.bfs) with a
          pinned host output buffer: H2D of the step's input (root id) and D2H of the
          step's result (the level vector) are inside the timed region.
+roofline = algorithmic bytes of one launch of the dominant kernel / its average
+         launch duration (CUDA events around each launch, gm_kernel_timer_*).
 --impl reference: the reference engine (oracle/_ref, compiled from
-         /root/reference/proj/include) on the host cores, same workload/metric.
+         /root/reference/proj/include) on the host cores, same workload/metric; at
+         scales the host cannot hold (the reference needs ~80 B of host memory per
+         stored entry) each step is a bounded sample: the same BFS on the R-MAT
+         graph of the largest scale that fits (cpu_baseline.sample says which).
 """
 from __future__ import annotations
 
@@ -172,6 +181,14 @@ class Dist:
             self.pg.all_reduce(t)
             torch.cuda.synchronize()
 
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t)
+        return float(t.item())
+
     def max(self, x: float) -> float:
         if not self.pg:
             return x
@@ -197,12 +214,61 @@ class Workload:
         self.args = args
         self.dist = dist
 
-    def roofline(self, stats, peak, peak_kind):
+    def roofline(self, stats, peak, peak_kind, ktime=None):
         return None
+
+    @staticmethod
+    def shards_at(scale):
+        """Whether N>1 runs this workload 1-D row-sharded (else replicas)."""
+        return False
 
     def flush_l2(self):
         """True when the step's device working set could stay in the 126 MB L2."""
         return self.g.info().device_bytes < 256e6
+
+
+def host_mem_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+# The reference engine peaks at ~80 bytes of host memory per stored directed
+# entry (measured: scale 20 -> 2.5 GB, scale 21 -> 5.0 GB, symmetrised R-MAT,
+# generation + build_graph + one BFS), i.e. ~2.7 * 2^scale KB.
+REF_BYTES_PER_ENTRY = 80
+CPU_SAMPLE_MAX_SCALE = 24  # keeps the sample's graph build to ~2 min on the host
+
+
+def cpu_sample_scale(scale):
+    """Largest scale <= min(scale, CPU_SAMPLE_MAX_SCALE) whose reference run
+    fits in 60% of the host's available memory (>= 20)."""
+    avail = host_mem_bytes()
+    sc = min(scale, CPU_SAMPLE_MAX_SCALE)
+    while sc > 20 and REF_BYTES_PER_ENTRY * 32 * (1 << sc) > 0.6 * avail:
+        sc -= 1
+    return sc
+
+
+def ref_bfs_sample(orc, scale, seed):
+    """The reference engine's algo::bfs (traversal.hpp:119-123) on the
+    symmetrised R-MAT graph of `scale` (our seeded generator + io::preprocess
+    semantics), from the seed-chosen root.  -> (RefGraph, root, teps_edges, setup_s)."""
+    t0 = time.perf_counter()
+    s, d = orc.rmat(scale, 16, seed=seed, **RMAT)
+    s, d, _ = orc.preprocess(s, d, symmetrize=True)
+    n = 1 << scale
+    deg = np.bincount(s, minlength=n).astype(np.uint32)
+    root = orc.pick_source(seed, deg)
+    rg = orc.RefGraph("dist", n, s, d, threads=0)
+    lvl, _ = orc.bfs(n, s, d, root, presorted=True)
+    edges = int(deg[lvl >= 0].sum()) // 2  # Graph500: undirected edges reached
+    return rg, root, edges, len(s), time.perf_counter() - t0
 
 
 class BfsWorkload(Workload):
@@ -212,6 +278,17 @@ class BfsWorkload(Workload):
     # BASELINE configs[4] (scale 28) runs 1-D row-sharded across the ranks;
     # configs[1] (scale 23, a single-GPU config) runs one replica per GPU.
     SHARD_MIN_SCALE = 26
+
+    @staticmethod
+    def shards_at(scale):
+        return scale >= BfsWorkload.SHARD_MIN_SCALE
+
+    @staticmethod
+    def describe(scale, seed):
+        return {"workload": f"bfs_rmat{scale}_sym", "graph": "R-MAT, symmetrised, dedup, no loops",
+                "scale": scale, "edge_factor": 16, "n": 1 << scale, "rmat_abc": [0.57, 0.19, 0.19],
+                "seed": seed, "switch": "pull when frontier edges > 5% of m",
+                "l2": "inputs larger than L2 (CSR > 1 GB vs 126 MB L2)"}
 
     def build(self, gm):
         a = self.args
@@ -236,12 +313,10 @@ class BfsWorkload(Workload):
             # GM_BFS_EXCHANGE=nccl keeps the NCCL all-gather
             self.fused, self.exchange_kind = None, "nccl all_gather"
             if os.environ.get("GM_BFS_EXCHANGE", "fused") == "fused":
-                try:
-                    from paper_1503_07241_b200.sharded import FusedBfs
-                    self.fused = FusedBfs(self.backend, self.exchange)
-                    self.exchange_kind = "peer stores of the frontier blocks (CUDA IPC) + nccl all_reduce"
-                except Exception as e:
-                    self.exchange_kind = f"nccl all_gather (peer stores unavailable: {e})"
+                from paper_1503_07241_b200.sharded import FusedBfs
+                self.fused, err = agree_or_none(d, lambda: FusedBfs(self.backend, self.exchange))
+                self.exchange_kind = ("peer stores of the frontier blocks (CUDA IPC) + nccl all_reduce"
+                                      if self.fused else f"nccl all_gather (peer stores unavailable: {err})")
         import torch
         self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
         self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
@@ -250,15 +325,12 @@ class BfsWorkload(Workload):
         self.root_degree = int(deg[self.root])
         # Graph500 TEPS: undirected edges inside the reached component.
         self.edges = int(deg[lvl >= 0].sum()) // 2
-        self.levels = lvl
+        del deg, lvl
         self.stats = st
-        self.config = {"workload": "bfs_rmat23_sym" if a.scale == 23 else f"bfs_rmat{a.scale}_sym",
-                       "scale": a.scale, "edge_factor": 16, "n": self.n,
-                       "m_directed": self.g.num_edges, "root": self.root,
-                       "teps_edges": self.edges, "switch": "pull when frontier edges > 5% of m",
-                       **({"exchange": self.exchange_kind} if self.sharded else {}),
-                       "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB)"
-                       % (self.g.info().device_bytes / 1e9)}
+        self.config = self.describe(a.scale, a.seed)
+        self.facts = {"m_directed": self.g.num_edges, "root": self.root, "teps_edges": self.edges,
+                      "device_bytes": self.g.info().device_bytes,
+                      **({"exchange": self.exchange_kind} if self.sharded else {})}
 
     def run_device(self, gm):
         if self.sharded:
@@ -288,37 +360,59 @@ class BfsWorkload(Workload):
         _, st = gm.bfs(self.g, self.root)
         return st
 
-    def roofline(self, st, peak, peak_kind):
+    def roofline(self, st, peak, peak_kind, ktime=None):
         if not st:
             return None
-        # The whole BFS is one cooperative launch (k_bfs_coop); its duration is
-        # the sum of the per-superstep %globaltimer spans measured inside it.
+        # algorithmic bytes of one BFS = one k_bfs_coop launch (SURVEY 8d
+        # formulas per superstep, summed); duration = the CUDA-event average
+        # of the launches inside the timed region
         b = sum(s.bytes_algorithmic for s in st)
-        t = sum(s.spmv_seconds for s in st)
+        if ktime and ktime[1]:
+            t, src = ktime[0] / ktime[1] * 1e-3, f"cuda events around {ktime[1]} launches of {ktime[2]}"
+        else:
+            t, src = sum(s.spmv_seconds for s in st), "summed in-kernel superstep spans"
         gbs = b / t / 1e9
-        traffic, src = ncu_traffic("k_bfs_coop", self.config["workload"])
+        traffic, tsrc = ncu_traffic("k_bfs_coop", self.config["workload"])
         return {"bound": "hbm", "kernel": "k_bfs_coop", "achieved": round(gbs, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
-                "bytes_per_launch": b, "launch_us": round(t * 1e6, 2), "traffic": traffic,
-                "traffic_source": src}
+                "bytes_per_launch": b, "launch_us": round(t * 1e6, 2), "launch_time_source": src,
+                "traffic": traffic, "traffic_source": tsrc}
 
     def cpu_baseline(self, orc):
-        s, d, _ = self.g.edges()
         R = orc.ref_lib()
-        kind = "reference" if R is not None else "port"
-        if R is not None:
-            rg = orc.RefGraph("dist", self.n, s, d, threads=0)
-            _, _, secs = rg.run_dist("bfs", self.root)
-            rg.close()
-            cores = int(R.ref_hardware_threads())
-        else:
-            t0 = time.perf_counter()
-            orc.bfs(self.n, s, d, self.root, presorted=True)
-            secs = time.perf_counter() - t0
-            cores = 1
-        return {"value": round(self.edges / secs / 1e9, 6), "unit": "GTEPS", "cores": cores,
-                "kind": kind, "seconds": round(secs, 4),
-                "sample": "one BFS from the same root on the full graph (graph build excluded)"}
+        sc = cpu_sample_scale(self.args.scale)
+        if R is None:
+            return {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
+                    "sample": "none: oracle/_ref not built"}
+        rg, root, edges, m, setup = ref_bfs_sample(orc, sc, self.args.seed)
+        secs = min(rg.run_dist("bfs", root)[2] for _ in range(2))
+        rg.close()
+        why = "" if sc == self.args.scale else (
+            f"; scale {self.args.scale} needs ~{REF_BYTES_PER_ENTRY * 32 * (1 << self.args.scale) / 1e9:.0f}"
+            f" GB of host memory in the reference engine (80 B per stored entry), more than this host "
+            f"has, so the sample is the largest scale that fits")
+        return {"value": round(edges / secs / 1e9, 6), "unit": "GTEPS",
+                "cores": int(R.ref_hardware_threads()), "kind": "reference", "seconds": round(secs, 4),
+                "sample": f"one BFS (best of 2) on the symmetrised R-MAT scale-{sc} graph "
+                          f"({m} stored entries, seed {self.args.seed}, graph build excluded){why}"}
+
+
+def agree_or_none(d, make):
+    """Construct an optional fast path on every rank or on none: a sum
+    all-reduce of the failure flags decides, so ranks never run different
+    collective sequences (a rank that built it and must drop it closes it)."""
+    obj, err = None, None
+    try:
+        obj = make()
+    except Exception as e:  # e.g. no peer access on this pair of GPUs
+        err = e
+    bad = d.sum(0.0 if obj is not None else 1.0) if d is not None else (0.0 if obj else 1.0)
+    if bad > 0 and obj is not None:
+        close = getattr(obj, "close", None)
+        if close:
+            close()
+        obj, err = None, err or "another rank could not map its peers"
+    return obj, err
 
 
 class PageRankWorkload(Workload):
@@ -347,22 +441,31 @@ class PageRankWorkload(Workload):
             # over NVLink); GM_PR_EXCHANGE=nccl keeps the NCCL all-gather
             self.fused, self.exchange_kind = None, "nccl all_gather"
             if os.environ.get("GM_PR_EXCHANGE", "fused") == "fused":
-                try:
-                    from paper_1503_07241_b200.sharded import FusedPageRank
-                    self.fused = FusedPageRank(self.backend, self.exchange, self.n)
-                    self.exchange_kind = "fused epilogue peer stores (CUDA IPC) + nccl all_reduce"
-                except Exception as e:  # e.g. no peer access: keep the NCCL path, say why
-                    self.exchange_kind = f"nccl all_gather (fused unavailable: {e})"
+                from paper_1503_07241_b200.sharded import FusedPageRank
+                self.fused, err = agree_or_none(
+                    d, lambda: FusedPageRank(self.backend, self.exchange, self.n))
+                self.exchange_kind = ("fused epilogue peer stores (CUDA IPC) + nccl all_reduce"
+                                      if self.fused else f"nccl all_gather (fused unavailable: {err})")
         import torch
         self.dev_out = torch.empty(self.n, dtype=torch.float32, device="cuda")
         self.host_out = torch.empty(self.n, dtype=torch.float32).pin_memory()
         self.m = self.g.num_edges
         self.edges = self.m * self.iters
-        self.config = {"workload": f"pagerank_rmat{a.scale}", "scale": a.scale, "edge_factor": 16,
-                       "n": self.n, "m": self.m, "iterations": self.iters, "damping": 0.85,
-                       **({"exchange": self.exchange_kind} if self.sharded else {}),
-                       "l2": "inputs larger than L2" if not self.flush_l2()
-                       else "L2 flushed between steps (256 MB write, outside the events)"}
+        self.config = self.describe(a.scale, a.seed)
+        self.facts = {"m": self.m, "device_bytes": self.g.info().device_bytes,
+                      **({"exchange": self.exchange_kind} if self.sharded else {})}
+
+    @staticmethod
+    def shards_at(scale):
+        return True
+
+    @staticmethod
+    def describe(scale, seed):
+        return {"workload": f"pagerank_rmat{scale}", "graph": "R-MAT, directed, dedup, no loops",
+                "scale": scale, "edge_factor": 16, "n": 1 << scale, "rmat_abc": [0.57, 0.19, 0.19],
+                "seed": seed, "iterations": 20, "damping": 0.85,
+                "l2": ("L2 flushed between steps (256 MB write, outside the events)" if scale <= 20
+                       else "inputs larger than L2")}
 
     def run_device(self, gm):
         if self.sharded:
@@ -391,34 +494,49 @@ class PageRankWorkload(Workload):
         _, st = gm.pagerank(self.g, 0.85, self.iters)
         return st
 
-    def roofline(self, st, peak, peak_kind):
+    def roofline(self, st, peak, peak_kind, ktime=None):
         if not st:
             return None
-        t = statistics.median([s.spmv_seconds for s in st])
-        b = st[0].bytes_algorithmic
-        gbs = b / t / 1e9
+        b = st[0].bytes_algorithmic  # per superstep = per SpMV launch
         kern = "k_pr_hub" if gm_pagerank_uses_hub(self.g) else "k_pr_spmv"
-        traffic, src = ncu_traffic(kern, self.config["workload"])
-        return {"bound": "hbm", "kernel": f"pr superstep ({kern} + base)",
+        if ktime and ktime[1]:
+            t, src = ktime[0] / ktime[1] * 1e-3, f"cuda events around {ktime[1]} launches of {ktime[2]}"
+            kname = ktime[2]
+        else:
+            t, src = statistics.median([s.spmv_seconds for s in st]), "superstep events (SpMV + base)"
+            kname = f"pr superstep ({kern} + base)"
+        gbs = b / t / 1e9
+        traffic, tsrc = ncu_traffic(kern, self.config["workload"])
+        return {"bound": "hbm", "kernel": kname,
                 "achieved": round(gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": round(gbs / peak, 4), "bytes_per_launch": b, "launch_us": round(t * 1e6, 2),
-                "traffic": traffic, "traffic_kernel": f"{kern} only", "traffic_source": src}
+                "launch_time_source": src, "traffic": traffic, "traffic_kernel": f"{kern} only",
+                "traffic_source": tsrc}
 
     def cpu_baseline(self, orc):
-        s, d, _ = self.g.edges()
         R = orc.ref_lib()
+        sc = cpu_sample_scale(self.args.scale)
+        if sc == self.args.scale:
+            s, d, _ = self.g.edges()
+        else:
+            s, d = orc.rmat(sc, 16, seed=self.args.seed, **RMAT)
+            s, d, _ = orc.preprocess(s, d)
+        n = 1 << sc
         if R is not None:
-            rg = orc.RefGraph("pr", self.n, s, d, threads=0)
+            rg = orc.RefGraph("pr", n, s, d, threads=0)
             _, secs = rg.run_pagerank(0.85, self.iters)
             rg.close()
             cores, kind = int(R.ref_hardware_threads()), "reference"
         else:
             t0 = time.perf_counter()
-            orc.pagerank_norm(self.n, s, d, 0.85, self.iters)
+            orc.pagerank_norm(n, s, d, 0.85, self.iters)
             secs, cores, kind = time.perf_counter() - t0, 1, "port"
-        return {"value": round(self.edges / secs / 1e9, 6), "unit": "GTEPS", "cores": cores,
+        return {"value": round(len(s) * self.iters / secs / 1e9, 6), "unit": "GTEPS", "cores": cores,
                 "kind": kind, "seconds": round(secs, 4),
-                "sample": f"{self.iters} supersteps on the full graph (graph build excluded)"}
+                "sample": f"{self.iters} supersteps on the directed R-MAT scale-{sc} graph "
+                          f"({len(s)} entries; graph build excluded)"
+                          + ("" if sc == self.args.scale else
+                             f"; scale {self.args.scale} does not fit the reference engine in host memory")}
 
 
 class SsspWorkload(Workload):
@@ -441,11 +559,17 @@ class SsspWorkload(Workload):
         # Graph500 convention: out-edges of every reached source
         self.edges = int(deg[dist != 0xFFFFFFFF].sum())
         self.relaxed = int(sum(s.edges_processed for s in st))
-        self.config = {"workload": f"sssp_rmat{a.scale}", "scale": a.scale, "edge_factor": 16,
-                       "n": self.n, "m": self.g.num_edges, "root": self.root,
-                       "weights": "uint8 in [1,255] from the seed",
-                       "teps_edges": self.edges, "edges_relaxed": self.relaxed,
-                       "teps": "edges whose source is reached / time (Graph500)"}
+        self.config = self.describe(a.scale, a.seed)
+        self.facts = {"m": self.g.num_edges, "root": self.root, "teps_edges": self.edges,
+                      "edges_relaxed": self.relaxed}
+
+    @staticmethod
+    def describe(scale, seed):
+        return {"workload": f"sssp_rmat{scale}", "graph": "R-MAT, directed, dedup, no loops",
+                "scale": scale, "edge_factor": 16, "n": 1 << scale, "rmat_abc": [0.57, 0.19, 0.19],
+                "seed": seed, "weights": "uint8 in [1,255] from the seed",
+                "teps": "edges whose source is reached / time (Graph500)",
+                "l2": "inputs larger than L2"}
 
     def run_device(self, gm):
         gm.sssp(self.g, self.root, with_stats=False, out_device_ptr=self.dev_out.data_ptr(),
@@ -463,7 +587,7 @@ class SsspWorkload(Workload):
         _, st = gm.sssp(self.g, self.root)
         return st
 
-    def roofline(self, st, peak, peak_kind):
+    def roofline(self, st, peak, peak_kind, ktime=None):
         top = max(st, key=lambda s: s.spmv_seconds)
         gbs = top.bytes_algorithmic / top.spmv_seconds / 1e9
         kern = "k_sssp_push" if top.direction == 1 else "k_sssp_pull"
@@ -501,11 +625,16 @@ class TcWorkload(Workload):
         self.m = self.g.num_edges
         self.edges = self.m
         self.total = gm.triangle_count(self.g)
-        self.config = {"workload": f"tc_rmat{a.scale}_dag", "scale": a.scale, "edge_factor": 16,
-                       "n": self.n, "m": self.m, "triangles": self.total,
-                       "teps": "stored DAG edges / count time",
-                       "l2": "inputs larger than L2" if not self.flush_l2()
-                       else "L2 flushed between steps (256 MB write, outside the events)"}
+        self.config = self.describe(a.scale, a.seed)
+        self.facts = {"m": self.m, "triangles": self.total}
+
+    @staticmethod
+    def describe(scale, seed):
+        return {"workload": f"tc_rmat{scale}_dag", "graph": "R-MAT, DAGIFY (src < dst)",
+                "scale": scale, "edge_factor": 16, "n": 1 << scale, "rmat_abc": [0.57, 0.19, 0.19],
+                "seed": seed, "teps": "stored DAG edges / count time",
+                "l2": "L2 flushed between steps (256 MB write, outside the events)" if scale <= 20
+                else "inputs larger than L2"}
 
     def run_device(self, gm):
         gm.triangle_count(self.g)
@@ -547,9 +676,14 @@ class CfWorkload(Workload):
         self.init = rng.uniform(0, 0.1, (self.n, self.k)).astype(np.float32)
         self.m = self.g.num_edges
         self.edges = 2 * self.m * self.iters
-        self.config = {"workload": "cf_zipf_480189x17770", "users": 480189, "items": 17770,
-                       "ratings": self.m, "k": 20, "lr": 0.001, "lambda": 0.05,
-                       "iterations": 10}
+        self.config = self.describe(0, self.args.seed)
+        self.facts = {"ratings": self.m}
+
+    @staticmethod
+    def describe(scale, seed):
+        return {"workload": "cf_zipf_480189x17770", "users": 480189, "items": 17770,
+                "ratings": "~99M (Zipf users 1.0 / items 0.8, DESIGN.md)", "k": 20, "lr": 0.001,
+                "lambda": 0.05, "iterations": 10, "seed": seed}
 
     def run_device(self, gm):
         # factors resident in HBM (caller order), as every other workload's inputs
@@ -572,7 +706,7 @@ class CfWorkload(Workload):
         return gm.collaborative_filtering_gd(self.g, self.k, 1e-3, 0.05, self.iters,
                                              init=self.init)[2]
 
-    def roofline(self, st, peak, peak_kind):
+    def roofline(self, st, peak, peak_kind, ktime=None):
         """CF sits near the FP32 ridge -> report max(bytes/BW, flops/FP32)."""
         if not st:
             return None
@@ -622,11 +756,20 @@ WORKLOADS = {"bfs": (BfsWorkload, 23), "pagerank": (PageRankWorkload, 20),
              "bfs28": (BfsWorkload, 28), "pagerank28": (PageRankWorkload, 28),
              # SURVEY 8f row 2 (not a BASELINE config)
              "tc": (TcWorkload, 20)}
-# The reference engine cannot hold scale >= 26 in host memory.
-CPU_MAX_SCALE = 25
 
 
 # ----------------------------------------------------------------- arms
+
+def parallelism_of(w_or_cls, world, scale=None):
+    """single at N=1; rows{N} for a workload that shards (strong scaling);
+    replicas{N} otherwise.  Both arms call this, so their configs match."""
+    if world <= 1:
+        return "single"
+    if isinstance(w_or_cls, Workload):
+        return w_or_cls.parallelism if w_or_cls.parallelism != "replicas" else f"replicas{world}"
+    shards = w_or_cls.shards_at(scale)
+    return f"rows{world}" if shards else f"replicas{world}"
+
 
 def run_ours(args, d: Dist):
     import torch
@@ -653,6 +796,9 @@ def run_ours(args, d: Dist):
     d.barrier()
     torch.cuda.synchronize()
     launches0 = gm.kernel_launches()
+    timed_graph = None if getattr(w, "sharded", False) else getattr(w, "g", None)
+    if timed_graph is not None:
+        timed_graph.kernel_timer_start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if w.flush_l2() else None
@@ -676,6 +822,7 @@ def run_ours(args, d: Dist):
                     pairs.append((a, b))
             torch.cuda.synchronize()
             t_ms = sum(a.elapsed_time(b) for a, b in pairs)
+        ktime = timed_graph.kernel_timer_stop() if timed_graph is not None else None
         # keep the GPU busy ~0.5 s more so the clock sampler sees load
         t_end = time.perf_counter() + 0.5
         while time.perf_counter() < t_end:
@@ -711,72 +858,70 @@ def run_ours(args, d: Dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
         "higher_is_better": True, "scaling": w.scaling, "vs_baseline": None, "dtype": w.dtype,
         "data": "synthetic: seeded counter-based R-MAT/Zipf generators (DESIGN.md), no datasets",
-        "config": dict(w.config, parallelism=(f"{w.parallelism}{d.world}" if w.parallelism == "replicas"
-                                            else w.parallelism) if d.world > 1 else "single"),
+        "config": dict(w.config, parallelism=parallelism_of(w, d.world)),
+        "graph": w.facts,
         "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_s * 1e3 / args.steps, 4)},
-        "roofline": with_spec(w.roofline(st, peak, peak_kind)),
+        "roofline": with_spec(w.roofline(st, peak, peak_kind, ktime)),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "ingest_seconds": round(w.ingest_s, 3),
         "per_superstep": per,
     }
     if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
-        if getattr(args, "scale", 0) and args.scale > CPU_MAX_SCALE:
-            line["cpu_baseline"] = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
-                                    "sample": f"none: the reference engine needs >100 GB of host "
-                                              f"memory at scale {args.scale} (SURVEY.md 8d)"}
-        else:
-            import oracle
-            line["cpu_baseline"] = w.cpu_baseline(oracle)
+        import oracle
+        # free the device-side run's host buffers before the reference builds
+        for attr in ("host_out", "levels", "stats"):
+            if hasattr(w, attr):
+                delattr(w, attr)
+        line["cpu_baseline"] = w.cpu_baseline(oracle)
     if d.rank == 0:
         print(json.dumps(line), flush=True)
 
 
-def run_reference(args, d: Dist):
-    """The reference engine (oracle/_ref) on the host cores, same workload/metric."""
-    if d.rank != 0:
-        return
+def run_reference(args, world):
+    """The reference engine (oracle/_ref: the reference's own headers compiled
+    by oracle/Makefile) on the host cores, same workload, metric and config
+    dict as our arm.  Each step is one full run; at scales the host cannot hold
+    it is a bounded sample on the largest R-MAT scale that fits."""
     import oracle
 
     R = oracle.ref_lib()
     cls, default_scale = WORKLOADS[args.workload]
     scale = args.scale if args.scale is not None else default_scale
+    config = dict(cls.describe(scale, args.seed), parallelism=parallelism_of(cls, world, scale))
     if R is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    if args.workload != "cf" and scale > CPU_MAX_SCALE:
-        print(json.dumps({"impl": "reference", "unavailable":
-                          f"scale {scale}: the reference engine needs >100 GB of host memory"}))
-        return
     cores = int(R.ref_hardware_threads())
-    n = 1 << scale
+    sc = cpu_sample_scale(scale) if args.workload != "cf" else 0
+    n = 1 << sc
     t0 = time.perf_counter()
-    s, dd = oracle.rmat(scale, 16, seed=args.seed, **RMAT)
-    if args.workload in ("bfs", "sssp"):
-        sym = args.workload == "bfs"
-        s, dd, _ = oracle.preprocess(s, dd, symmetrize=sym)
-        deg = np.bincount(s, minlength=n).astype(np.uint32)
-        root = oracle.pick_source(args.seed, deg)
-        w = None if sym else oracle.edge_weights(args.seed, s, dd).astype(np.float64)
-        rg = oracle.RefGraph("dist", n, s, dd, w, threads=0)
+    sample = None
+    if cls is BfsWorkload:
+        rg, root, edges, m, _ = ref_bfs_sample(oracle, sc, args.seed)
         gen_s = time.perf_counter() - t0
-        _, st, _ = rg.run_dist(args.workload, root)
-        # Graph500 convention: edges inside the reached component (undirected
-        # edges for the symmetrised BFS graph, out-edges of reached sources for SSSP)
-        if sym:
-            lvl, _ = oracle.bfs(n, s, dd, root, presorted=True)
-            edges = int(deg[lvl >= 0].sum()) // 2
-        else:
-            dist, _ = oracle.sssp(n, s, dd, w.astype(np.uint8), root, presorted=True)
-            edges = int(deg[dist != 0xFFFFFFFF].sum())
 
         def step():
-            return rg.run_dist(args.workload, root)[2]
-        config = {"workload": f"{args.workload}_rmat{scale}{'_sym' if sym else ''}",
-                  "scale": scale, "edge_factor": 16, "n": n, "m_directed": len(s), "root": root,
-                  "teps_edges": edges}
-    elif args.workload in ("pagerank", "pagerank23"):
+            return rg.run_dist("bfs", root)[2]
+        sample = (f"one BFS on the symmetrised R-MAT scale-{sc} graph ({m} stored entries, "
+                  f"root {root}; graph build excluded, as tools/sgraph.cpp:101-103)")
+    elif cls is SsspWorkload:
+        s, dd = oracle.rmat(sc, 16, seed=args.seed, **RMAT)
+        s, dd, _ = oracle.preprocess(s, dd)
+        deg = np.bincount(s, minlength=n).astype(np.uint32)
+        root = oracle.pick_source(args.seed, deg)
+        w = oracle.edge_weights(args.seed, s, dd).astype(np.float64)
+        rg = oracle.RefGraph("dist", n, s, dd, w, threads=0)
+        gen_s = time.perf_counter() - t0
+        dist, _ = oracle.sssp(n, s, dd, w.astype(np.uint8), root, presorted=True)
+        edges = int(deg[dist != 0xFFFFFFFF].sum())
+
+        def step():
+            return rg.run_dist("sssp", root)[2]
+        sample = f"one SSSP on the directed R-MAT scale-{sc} graph ({len(s)} entries, root {root})"
+    elif cls is PageRankWorkload:
+        s, dd = oracle.rmat(sc, 16, seed=args.seed, **RMAT)
         s, dd, _ = oracle.preprocess(s, dd)
         rg = oracle.RefGraph("pr", n, s, dd, threads=0)
         gen_s = time.perf_counter() - t0
@@ -784,9 +929,9 @@ def run_reference(args, d: Dist):
 
         def step():
             return rg.run_pagerank(0.85, 20)[1]
-        config = {"workload": f"pagerank_rmat{scale}", "scale": scale, "n": n, "m": len(s),
-                  "iterations": 20}
-    elif args.workload == "tc":
+        sample = f"20 supersteps on the directed R-MAT scale-{sc} graph ({len(s)} entries)"
+    elif cls is TcWorkload:
+        s, dd = oracle.rmat(sc, 16, seed=args.seed, **RMAT)
         s, dd, _ = oracle.preprocess(s, dd, mode="dagify")
         gen_s = time.perf_counter() - t0
         edges = len(s)
@@ -795,11 +940,15 @@ def run_reference(args, d: Dist):
             t = time.perf_counter()
             oracle.ref_triangle_count(n, s, dd, threads=0, parts=8 * cores)
             return time.perf_counter() - t
-        config = {"workload": f"tc_rmat{scale}_dag", "scale": scale, "n": n, "m": len(s)}
+        sample = f"one count on the DAGIFY'd R-MAT scale-{sc} graph ({len(s)} entries)"
     else:
         print(json.dumps({"impl": "reference", "unavailable":
                           f"--impl reference not wired for workload {args.workload}"}))
         return
+    if sc != scale:
+        sample += (f"; scale {scale} needs ~{REF_BYTES_PER_ENTRY * 32 * (1 << scale) / 1e9:.0f} GB of "
+                   f"host memory in the reference engine (80 B per stored entry), more than this host "
+                   f"has, so each step is this bounded sample")
     for _ in range(args.warmup):
         step()
     times = [step() for _ in range(args.steps)]
@@ -807,15 +956,13 @@ def run_reference(args, d: Dist):
     value = edges * args.steps / total / 1e9
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GTEPS",
-        "n_gpus": d.world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total * 1e3 / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if config["parallelism"].startswith("rows") else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded counter-based R-MAT generator",
         "config": config,
         "cpu_baseline": {"value": round(value, 6), "unit": "GTEPS", "cores": cores,
-                         "kind": "reference",
-                         "sample": "each step = one full run on the full graph; the reference "
-                                   "engine's algorithm time (graph build excluded, as "
-                                   "tools/sgraph.cpp:101-103)"},
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "setup_seconds": round(gen_s, 2),
@@ -828,7 +975,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="bfs", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="bfs28", choices=sorted(WORKLOADS))
     ap.add_argument("--scale", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -839,7 +986,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        run_reference(args, Dist(1, 0, local))
+        run_reference(args, world)
         return
     d = Dist(world, rank, local)
     try:

@@ -147,6 +147,14 @@ GM_API gm_status gm_pick_source(gm_graph_t g, uint64_t seed, uint64_t* out);
 GM_API void* gm_graph_stream(gm_graph_t g);
 /* Wait for every call issued on this handle (see GM_OUT_DEVICE_ASYNC). */
 GM_API gm_status gm_graph_synchronize(gm_graph_t g);
+/* Measurement: CUDA-event timing of each launch of the handle's dominant
+ * kernel (k_bfs_coop, k_pr_hub / k_pr_spmv, the SSSP / CF superstep kernels)
+ * between _start and _stop; _stop synchronises and returns the summed
+ * duration, the number of timed launches and the kernel's name.  No reference
+ * counterpart: the reference times whole supersteps (engine.hpp:177-188). */
+GM_API gm_status gm_kernel_timer_start(gm_graph_t g);
+GM_API gm_status gm_kernel_timer_stop(gm_graph_t g, double* total_ms, int64_t* launches,
+                                      char* name, size_t name_cap);
 
 /* out_on_device of gm_pagerank / gm_bfs / gm_sssp:
  *   GM_OUT_HOST         the output pointer is host memory; returns when written;

@@ -35,6 +35,7 @@ EXPORTED = [
     "gm_sssp_shard_init", "gm_sssp_shard_step", "gm_sssp_shard_dists", "gm_cf_shard_step",
     "gm_pagerank_shard_step_peers", "gm_pagerank_shard_init_peers", "gm_ipc_alloc", "gm_ipc_free", "gm_ipc_handle", "gm_ipc_open",
     "gm_ipc_close", "gm_bfs_shard_push", "gm_bitmap_or", "gm_push_block",
+    "gm_kernel_timer_start", "gm_kernel_timer_stop",
 ]
 
 
@@ -111,6 +112,9 @@ def load(path: str = LIB_PATH):
         "gm_pick_source": (C.c_int, [vp, u64, C.POINTER(u64)]),
         "gm_graph_stream": (vp, [vp]),
         "gm_graph_synchronize": (C.c_int, [vp]),
+        "gm_kernel_timer_start": (C.c_int, [vp]),
+        "gm_kernel_timer_stop": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                          C.c_char_p, C.c_size_t]),
         "gm_pagerank": (C.c_int, [vp, C.POINTER(PageRankConfig), vp, i32, st, i64,
                                   C.POINTER(i64)]),
         "gm_bfs": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),

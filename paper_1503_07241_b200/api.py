@@ -226,6 +226,17 @@ class Graph:
         """Wait for every call issued on this graph (after sync=False runs)."""
         _check(L.load().gm_graph_synchronize(self._h))
 
+    def kernel_timer_start(self):
+        """Start CUDA-event timing of every launch of the dominant kernel."""
+        _check(L.load().gm_kernel_timer_start(self._h))
+
+    def kernel_timer_stop(self):
+        """-> (total_ms, launches, kernel_name) since kernel_timer_start()."""
+        ms, n = C.c_double(), C.c_int64()
+        buf = C.create_string_buffer(64)
+        _check(L.load().gm_kernel_timer_stop(self._h, C.byref(ms), C.byref(n), buf, 64))
+        return float(ms.value), int(n.value), buf.value.decode()
+
     def edges(self):
         """Stored edges in caller ids sorted by (src, dst) -- io::preprocess's output."""
         info = self.info()

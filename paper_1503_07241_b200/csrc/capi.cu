@@ -134,6 +134,38 @@ GM_API gm_status gm_graph_synchronize(gm_graph_t g) {
   return guarded([&] { GM_CUDA(cudaStreamSynchronize(handle(g)->stream)); });
 }
 
+GM_API gm_status gm_kernel_timer_start(gm_graph_t g) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    h->ktimer.on = true;
+    h->ktimer.used = 0;
+    h->ktimer.name = "";
+  });
+}
+
+GM_API gm_status gm_kernel_timer_stop(gm_graph_t g, double* total_ms, int64_t* launches,
+                                      char* name, size_t name_cap) {
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    gm::KernelTimer& t = h->ktimer;
+    GM_CUDA(cudaStreamSynchronize(h->stream));
+    double ms = 0.0;
+    for (size_t i = 0; i + 1 < t.used; i += 2) {
+      float x = 0.f;
+      GM_CUDA(cudaEventElapsedTime(&x, t.ev[i], t.ev[i + 1]));
+      ms += x;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = int64_t(t.used / 2);
+    if (name && name_cap) {
+      std::strncpy(name, t.name, name_cap - 1);
+      name[name_cap - 1] = 0;
+    }
+    t.on = false;
+    t.used = 0;
+  });
+}
+
 namespace {
 // out_on_device: GM_OUT_HOST, GM_OUT_DEVICE or GM_OUT_DEVICE_ASYNC (device
 // output, no host synchronisation -- so no stats either).

@@ -23,6 +23,37 @@ struct Csr {
   DevBuf<uint8_t> val;   // nnz * value_size(value_type)
 };
 
+// CUDA-event timing of a handle's dominant kernel (bench.py's roofline:
+// algorithmic bytes per launch / average launch duration).  Off by default;
+// gm_kernel_timer_start turns it on, the kernels' host drivers bracket their
+// main launch with begin()/end(), gm_kernel_timer_stop sums the durations.
+struct KernelTimer {
+  bool on = false;
+  const char* name = "";
+  std::vector<cudaEvent_t> ev;  // begin/end pairs, reused across windows
+  size_t used = 0;
+  void begin(cudaStream_t s, const char* nm) {
+    if (!on) return;
+    name = nm;
+    if (ev.size() < used + 2) {
+      for (int i = 0; i < 2; ++i) {
+        cudaEvent_t e;
+        GM_CUDA(cudaEventCreate(&e));
+        ev.push_back(e);
+      }
+    }
+    GM_CUDA(cudaEventRecord(ev[used], s));
+  }
+  void end(cudaStream_t s) {
+    if (!on) return;
+    GM_CUDA(cudaEventRecord(ev[used + 1], s));
+    used += 2;
+  }
+  ~KernelTimer() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
 struct PrCache;    // pagerank.cu
 struct PrHubCache; // pagerank_hub.cu
 struct TravCache;  // traversal.cu
@@ -51,6 +82,8 @@ struct Graph {
   Csr out;   // CSR(G):   row j lists destinations k of edges j -> k
   bool out_built = false;
   bool out_alias = false;  // symmetric and value-less: CSR(G) == CSR(G^T)
+
+  KernelTimer ktimer;
 
   std::unique_ptr<PrCache, void (*)(PrCache*)> pr{nullptr, nullptr};
   std::unique_ptr<PrHubCache, void (*)(PrHubCache*)> prhub{nullptr, nullptr};

@@ -454,7 +454,9 @@ void launch_spmv(Graph& g, PrCache& c, const float* x_cur, float* x_next, float 
   a.dang_partial = c.dang_partial.get();
   const unsigned grid = a.ntiles + a.nchunks;
   if (grid) {
+    g.ktimer.begin(s, "k_pr_spmv");
     k_pr_spmv<<<grid, kPrThreads, 0, s>>>(a);
+    g.ktimer.end(s);
     GM_LAUNCH_CHECK();
   }
   c.cur ^= 1;

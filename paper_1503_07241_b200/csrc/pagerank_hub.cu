@@ -745,7 +745,9 @@ std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t i
     a.damping = d;
     a.dang_chunk = c.dang_chunk.get();
     a.dang = c.dang.get();
+    g.ktimer.begin(s, "k_pr_hub");
     k_pr_hub<<<c.grid, kHubThreads, size_t(c.H) * 4, s>>>(a);
+    g.ktimer.end(s);
     GM_LAUNCH_CHECK();
     k_hub_base<<<1, 1024, 0, s>>>(c.dang.get(), c.grid + c.n_multi, n, damping, c.scalars.get());
     GM_LAUNCH_CHECK();

@@ -1366,8 +1366,10 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
     a.use_ulist = e ? atoi(e) : 1;
   }
   void* args[] = {&a};
+  g.ktimer.begin(s, "k_bfs_coop");
   GM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs_coop), dim3(c.coop_grid),
                                       dim3(kCoopThreads), args, smem, s));
+  g.ktimer.end(s);
   ::gm::count_launch();
   std::vector<gm_iteration_stats> stats;
   if (collect) {

@@ -1,0 +1,1010 @@
+// dist.cu -- row-sharded graph ingest and the multi-GPU supersteps.
+//
+// Ingest (replaces build_dcsc_partitions + balanced_row_boundaries,
+// include/semigraph/dcsc.hpp:77-164, and io::preprocess, src/io.cpp:184-222,
+// for a graph no single GPU has to hold):
+//   1. every shard draws its 1/P of the edge stream (R-MAT tuples are counter
+//      based, so shard r generates tuples [r*M/P, (r+1)*M/P) of the same
+//      stream a single GPU would);
+//   2. a coarse histogram of destination rows, summed over the shards, gives
+//      row boundaries balanced by entries (the rule of dcsc.hpp:81-105 at a
+//      granularity of 2^kBucketBits rows, so every boundary is 32-aligned);
+//   3. each shard sorts its packed (row << nb | col) keys and sends the run of
+//      every destination shard to it (all-to-all: peer copies or NCCL);
+//   4. the owner sorts what it received, removes duplicates (keep-first is moot
+//      for value-less keys) and builds the CSR of its rows -- entries ascending
+//      by caller id, the reference's fold order (engine.hpp:59-66);
+//   5. directed graphs: out-degrees summed over the shards; the columns of
+//      CSR(G^T) are renumbered to "packed" ids (rank among the vertices with
+//      out-edges, ascending caller id), so the exchanged message vector holds
+//      only vertices that send (SURVEY 8e mitigation 1) and its block per shard
+//      is contiguous;  out-rows (CSR(G), for pushes) come from a second
+//      all-to-all of the swapped keys.
+// Each shard keeps only its rows: device memory ~ 1/P of one GPU's.
+#include <algorithm>
+#include <string>
+
+#include "dist.cuh"
+#include "ingest.cuh"
+
+namespace gm {
+
+struct DBfsState {
+  std::vector<DevBuf<int32_t>> level;      // [l] owned rows
+  std::vector<DevBuf<uint32_t>> vis, nxt;  // [l] owned words
+  std::vector<DevBuf<uint32_t>> queue;     // [l] local frontier rows
+  std::vector<DevBuf<unsigned long long>> ctr, sum;  // [l] counters / summed
+  std::vector<void*> fb[2], claims;        // [l] peer-visible full bitmaps
+  std::vector<std::vector<void*>> fb_tab[2], claims_tab;
+  Comm* c = nullptr;
+  ~DBfsState() {
+    if (!c) return;
+    for (int b = 0; b < 2; ++b) c->unshare(fb_tab[b]);
+    c->unshare(claims_tab);
+    for (int l = 0; l < c->L; ++l) {
+      c->set(l);
+      cudaStreamSynchronize(c->st[size_t(l)]);
+      c->peer_free(l, fb[0][size_t(l)]);
+      c->peer_free(l, fb[1][size_t(l)]);
+      c->peer_free(l, claims[size_t(l)]);
+      level[size_t(l)].reset();
+      vis[size_t(l)].reset();
+      nxt[size_t(l)].reset();
+      queue[size_t(l)].reset();
+      ctr[size_t(l)].reset();
+      sum[size_t(l)].reset();
+    }
+  }
+};
+
+struct DPrState {
+  std::vector<DevBuf<float>> rank, inv;          // [l] owned rows
+  std::vector<DevBuf<uint32_t>> pid;             // [l] packed id per owned row (~0u: dangling)
+  std::vector<DevBuf<uint32_t>> rows_short, rows_long;  // [l] row bins
+  std::vector<uint64_t> n_short, n_long;
+  std::vector<DevBuf<unsigned long long>> part, sum;  // [l] 2 parities x 4 words
+  std::vector<void*> x[2];                       // [l] peer-visible packed message vectors
+  std::vector<std::vector<void*>> x_tab[2];
+  Comm* c = nullptr;
+  ~DPrState() {
+    if (!c) return;
+    for (int b = 0; b < 2; ++b) c->unshare(x_tab[b]);
+    for (int l = 0; l < c->L; ++l) {
+      c->set(l);
+      cudaStreamSynchronize(c->st[size_t(l)]);
+      c->peer_free(l, x[0][size_t(l)]);
+      c->peer_free(l, x[1][size_t(l)]);
+      rank[size_t(l)].reset();
+      inv[size_t(l)].reset();
+      pid[size_t(l)].reset();
+      rows_short[size_t(l)].reset();
+      rows_long[size_t(l)].reset();
+      part[size_t(l)].reset();
+      sum[size_t(l)].reset();
+    }
+  }
+};
+
+namespace {
+
+constexpr unsigned kBlock = 256;
+constexpr int kMaxPeers = 64;
+
+template <typename T>
+struct PeerTab {
+  T* p[kMaxPeers];
+};
+
+template <typename F>
+void launch(uint64_t work, cudaStream_t s, F&& f, unsigned block = kBlock) {
+  if (work == 0) return;
+  f(grid_for(work, block), block);
+  GM_LAUNCH_CHECK();
+}
+
+// ---- ingest kernels -----------------------------------------------------------
+// Packed keys row << nb | col of the generated edges; self loops dropped
+// (io::preprocess); symmetric graphs add the reverse of every edge.
+__global__ void k_edge_keys(const uint32_t* s, const uint32_t* d, uint64_t m, unsigned nb, int sym,
+                            uint64_t* keys, unsigned long long* cnt) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = s[e], b = d[e];
+    if (a == b) continue;
+    const unsigned long long k = atomicAdd(cnt, sym ? 2ull : 1ull);
+    keys[k] = (uint64_t(b) << nb) | a;  // row = destination (G^T)
+    if (sym) keys[k + 1] = (uint64_t(a) << nb) | b;
+  }
+}
+
+__global__ void k_row_hist(const uint64_t* keys, uint64_t m, unsigned shift,
+                           unsigned long long* hist) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&hist[keys[e] >> shift], 1ull);
+}
+
+// Start of each shard's run in a sorted key array (rows [bounds[r], ...)).
+__global__ void k_run_starts(const uint64_t* keys, uint64_t m, unsigned nb, const uint64_t* bounds,
+                             int P, uint64_t* starts) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > P) return;
+  const uint64_t x = bounds[r] << nb;
+  uint64_t lo = 0, hi = m;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  starts[r] = r == P ? m : lo;
+}
+
+// CSR of the rows [lo, lo + rows) from sorted unique keys.
+__global__ void k_keys_to_csr(const uint64_t* keys, uint64_t m, unsigned nb, uint64_t lo,
+                              uint64_t rows, uint64_t* ptr, uint32_t* idx) {
+  const uint64_t mask = (uint64_t(1) << nb) - 1;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i <= m;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i < m ? (keys[i] >> nb) - lo : rows;
+    const uint64_t p = i == 0 ? 0 : (keys[i - 1] >> nb) - lo + 1;
+    for (uint64_t q = p; q <= r && q <= rows; ++q) ptr[q] = i;  // rows (prev, r] start at i
+    if (i < m) idx[i] = uint32_t(keys[i] & mask);
+  }
+}
+
+__global__ void k_swap_keys(const uint64_t* ptr, const uint32_t* idx, uint64_t lo, uint64_t rows,
+                            unsigned nb, uint64_t* keys) {
+  // one warp per row: (col << nb | row) for every entry
+  const uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = w; r < rows; r += nw)
+    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32)
+      keys[e] = (uint64_t(idx[e]) << nb) | (lo + r);
+}
+
+__global__ void k_src_degree(const uint32_t* idx, uint64_t nnz, uint32_t* deg) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&deg[idx[e]], 1u);
+}
+
+__global__ void k_nonzero_u32(const uint32_t* deg, uint64_t n, uint32_t* flag) {
+  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
+       v += uint64_t(gridDim.x) * blockDim.x)
+    flag[v] = deg[v] > 0;
+}
+
+__global__ void k_remap_cols(uint32_t* idx, uint64_t nnz, const uint64_t* pmap) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += uint64_t(gridDim.x) * blockDim.x)
+    idx[e] = uint32_t(pmap[idx[e]]);
+}
+
+__global__ void k_row_weights(const uint64_t* ptr, const uint32_t* idx, uint64_t lo, uint64_t rows,
+                              uint64_t seed_w, int row_is_dst, uint8_t* w) {
+  const uint64_t wp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = wp; r < rows; r += nw)
+    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
+      const uint32_t row = uint32_t(lo + r), col = idx[e];
+      w[e] = row_is_dst ? edge_weight(seed_w, col, row) : edge_weight(seed_w, row, col);
+    }
+}
+
+__global__ void k_check_ids(const uint64_t* keys, uint64_t m, unsigned nb, uint64_t n,
+                            unsigned long long* bad) {
+  const uint64_t mask = (uint64_t(1) << nb) - 1;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    if ((keys[i] >> nb) >= n || (keys[i] & mask) >= n) atomicMin(bad, (unsigned long long)i);
+}
+
+__global__ void k_first_dup(const uint64_t* keys, uint64_t m, unsigned long long* first) {
+  for (uint64_t i = 1 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    if (keys[i] == keys[i - 1]) atomicMin(first, (unsigned long long)i);
+}
+
+unsigned bucket_bits(uint64_t n, int P) {
+  // >= 32 rows per bucket (aligned boundaries), ~>= 64 buckets per shard
+  unsigned b = 5;
+  while (b < 20 && (n >> (b + 1)) >= uint64_t(P) * 64) ++b;
+  return b;
+}
+
+uint64_t dread_u64(const unsigned long long* p, cudaStream_t s) {
+  unsigned long long h = 0;
+  GM_CUDA(cudaMemcpyAsync(&h, p, 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+// keys[l] (packed row << nb | col, any order) -> the CSR of each shard's rows.
+// Sets g.bounds from the key histogram when empty.  check_dups: the first
+// duplicate is an InputError (build_graph without preprocess, dcsc.hpp:148-150).
+void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector<uint64_t>& m,
+                     unsigned nb, bool forward, bool check_dups) {
+  Comm& c = *g.comm;
+  const int P = c.P, L = c.L;
+  if (g.bounds.empty()) {
+    const unsigned bb = bucket_bits(g.n, P);
+    const uint64_t nbk = (g.n + (uint64_t(1) << bb) - 1) >> bb;
+    std::vector<DevBuf<unsigned long long>> h(size_t(L)), hs(size_t(L));
+    std::vector<const uint64_t*> hin;
+    std::vector<uint64_t*> hout;
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      h[size_t(l)].alloc(nbk, s);
+      hs[size_t(l)].alloc(nbk, s);
+      h[size_t(l)].zero(s);
+      launch(m[size_t(l)], s, [&](unsigned gr, unsigned bl) {
+        k_row_hist<<<gr, bl, 0, s>>>(keys[size_t(l)].get(), m[size_t(l)], nb + bb, h[size_t(l)].get());
+      });
+      hin.push_back(reinterpret_cast<const uint64_t*>(h[size_t(l)].get()));
+      hout.push_back(reinterpret_cast<uint64_t*>(hs[size_t(l)].get()));
+    }
+    c.allreduce_u64(hin, hout, nbk);
+    std::vector<uint64_t> hh(nbk);
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(hh.data(), hout[0], nbk * 8, cudaMemcpyDeviceToHost, c.st[0]));
+    GM_CUDA(cudaStreamSynchronize(c.st[0]));
+    // balanced_row_boundaries (dcsc.hpp:81-105) over buckets
+    std::vector<uint64_t> cum(nbk + 1, 0);
+    for (uint64_t i = 0; i < nbk; ++i) cum[i + 1] = cum[i] + hh[i];
+    const uint64_t total = cum[nbk];
+    g.bounds.assign(size_t(P) + 1, 0);
+    g.bounds[size_t(P)] = g.n;
+    for (int p = 1; p < P; ++p) {
+      uint64_t lo = g.bounds[size_t(p) - 1] >> bb, hi = nbk;
+      while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (cum[mid] * uint64_t(P) >= uint64_t(p) * total)
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      g.bounds[size_t(p)] = std::min(g.n, lo << bb);
+    }
+    for (int l = 0; l < L; ++l) {
+      g.sh[size_t(l)].lo = g.bounds[size_t(c.global(l))];
+      g.sh[size_t(l)].hi = g.bounds[size_t(c.global(l)) + 1];
+    }
+  }
+  // sort locally, find every destination's run, exchange the runs
+  std::vector<std::vector<uint64_t>> send_offs(size_t(L)), send_counts(size_t(L));
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    sort_keys_u64(keys[size_t(l)], int64_t(m[size_t(l)]), int(2 * nb), s);
+    DevBuf<uint64_t> db(size_t(P) + 1, s), st(size_t(P) + 1, s);
+    GM_CUDA(cudaMemcpyAsync(db.get(), g.bounds.data(), (size_t(P) + 1) * 8, cudaMemcpyHostToDevice, s));
+    k_run_starts<<<1, 128, 0, s>>>(keys[size_t(l)].get(), m[size_t(l)], nb, db.get(), P, st.get());
+    GM_LAUNCH_CHECK();
+    std::vector<uint64_t> hst(size_t(P) + 1);
+    GM_CUDA(cudaMemcpyAsync(hst.data(), st.get(), (size_t(P) + 1) * 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < P; ++r) {
+      send_offs[size_t(l)].push_back(hst[size_t(r)] * 8);
+      send_counts[size_t(l)].push_back((hst[size_t(r) + 1] - hst[size_t(r)]) * 8);
+    }
+  }
+  // (local mode: exchange_counts is a transpose; nccl: a count all-gather)
+  const auto recv_counts = c.exchange_counts(send_counts);
+  std::vector<DevBuf<uint64_t>> recv(size_t(L));
+  std::vector<std::vector<uint64_t>> recv_offs(size_t(L));
+  std::vector<uint64_t> mr(size_t(L));
+  std::vector<const uint8_t*> sp;
+  std::vector<uint8_t*> rp;
+  for (int l = 0; l < L; ++l) {
+    uint64_t off = 0;
+    for (int q = 0; q < P; ++q) {
+      recv_offs[size_t(l)].push_back(off);
+      off += recv_counts[size_t(l)][size_t(q)];
+    }
+    mr[size_t(l)] = off / 8;
+    c.set(l);
+    recv[size_t(l)].alloc(mr[size_t(l)] + 1, c.st[size_t(l)]);
+    sp.push_back(reinterpret_cast<const uint8_t*>(keys[size_t(l)].get()));
+    rp.push_back(reinterpret_cast<uint8_t*>(recv[size_t(l)].get()));
+  }
+  c.alltoallv(sp, send_offs, send_counts, rp, recv_offs);
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    GM_CUDA(cudaStreamSynchronize(s));
+    keys[size_t(l)].reset();
+  }
+  // owners: sort, check / remove duplicates, build the rows
+  std::vector<uint64_t> bad(size_t(L), 0);
+  std::vector<std::string> msg(size_t(L));
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    DevBuf<uint64_t>& k = recv[size_t(l)];
+    int64_t cnt = int64_t(mr[size_t(l)]);
+    sort_keys_u64(k, cnt, int(2 * nb), s);
+    if (check_dups) {
+      DevBuf<unsigned long long> fd(1, s);
+      GM_CUDA(cudaMemsetAsync(fd.get(), 0xFF, 8, s));
+      launch(uint64_t(cnt), s, [&](unsigned gr, unsigned bl) {
+        k_first_dup<<<gr, bl, 0, s>>>(k.get(), uint64_t(cnt), fd.get());
+      });
+      const uint64_t i = dread_u64(fd.get(), s);
+      if (i != ~0ull) {
+        uint64_t key = 0;
+        GM_CUDA(cudaMemcpyAsync(&key, k.get() + i, 8, cudaMemcpyDeviceToHost, s));
+        GM_CUDA(cudaStreamSynchronize(s));
+        const uint64_t row = key >> nb, col = key & ((uint64_t(1) << nb) - 1);
+        const uint64_t src = forward ? row : col, dst = forward ? col : row;
+        bad[size_t(l)] = 1;
+        msg[size_t(l)] = "build_graph: duplicate edge " + std::to_string(src + 1) + " -> " +
+                         std::to_string(dst + 1) + " (1-based); deduplicate before building";
+      }
+    } else {
+      cnt = unique_keys_u64(k, cnt, s);
+    }
+    Csr& a = forward ? sh.out : sh.in;
+    const uint64_t rows = sh.hi - sh.lo;
+    a.n = rows;
+    a.nnz = uint64_t(cnt);
+    a.ptr.alloc(rows + 1, s);
+    a.idx.alloc(uint64_t(cnt) + 1, s);
+    launch(uint64_t(cnt) + 1, s, [&](unsigned gr, unsigned bl) {
+      k_keys_to_csr<<<gr, bl, 0, s>>>(k.get(), uint64_t(cnt), nb, sh.lo, rows, a.ptr.get(), a.idx.get());
+    });
+    GM_CUDA(cudaStreamSynchronize(s));
+    k.reset();
+  }
+  uint64_t nbad = 0;
+  for (uint64_t b : bad) nbad += b;
+  if (c.sum_host({nbad})) {
+    for (int l = 0; l < L; ++l)
+      if (bad[size_t(l)]) fail(GM_EINPUT, msg[size_t(l)]);
+    fail(GM_EINPUT, "build_graph: duplicate edge on another shard; deduplicate before building");
+  }
+}
+
+// CSR(G) rows of the owned vertices from everybody's CSR(G^T) rows.
+void build_forward(DGraph& g, unsigned nb) {
+  Comm& c = *g.comm;
+  std::vector<DevBuf<uint64_t>> keys(size_t(c.L));
+  std::vector<uint64_t> m(size_t(c.L));
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    m[size_t(l)] = sh.in.nnz;
+    keys[size_t(l)].alloc(sh.in.nnz + 1, s);
+    launch(sh.in.n * 32, s, [&](unsigned gr, unsigned bl) {
+      k_swap_keys<<<gr, bl, 0, s>>>(sh.in.ptr.get(), sh.in.idx.get(), sh.lo, sh.in.n, nb,
+                                    keys[size_t(l)].get());
+    });
+  }
+  route_and_build(g, keys, m, nb, /*forward=*/true, /*check_dups=*/false);
+}
+
+// Directed graphs: global out-degrees (summed over the shards), the owned
+// rows' out-degrees, and the packed renumbering of CSR(G^T)'s columns.
+void finish_directed(DGraph& g) {
+  Comm& c = *g.comm;
+  const uint64_t n = g.n;
+  std::vector<DevBuf<uint32_t>> deg(size_t(c.L)), degs(size_t(c.L));
+  std::vector<const uint64_t*> din;
+  std::vector<uint64_t*> dout;
+  // u32 counts travel as u64 pairs: the sum of two shards' u32 never carries
+  // across the 32-bit halves because a vertex's out-degree is < 2^32
+  const uint64_t words = (n + 1) / 2;
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    deg[size_t(l)].alloc(2 * words, s);
+    degs[size_t(l)].alloc(2 * words, s);
+    deg[size_t(l)].zero(s);
+    launch(sh.in.nnz, s, [&](unsigned gr, unsigned bl) {
+      k_src_degree<<<gr, bl, 0, s>>>(sh.in.idx.get(), sh.in.nnz, deg[size_t(l)].get());
+    });
+    din.push_back(reinterpret_cast<const uint64_t*>(deg[size_t(l)].get()));
+    dout.push_back(reinterpret_cast<uint64_t*>(degs[size_t(l)].get()));
+  }
+  c.allreduce_u64(din, dout, words);
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    deg[size_t(l)].reset();
+    const uint32_t* od = degs[size_t(l)].get();
+    sh.outdeg.alloc(sh.hi - sh.lo + 1, s);
+    if (sh.hi > sh.lo)
+      GM_CUDA(cudaMemcpyAsync(sh.outdeg.get(), od + sh.lo, (sh.hi - sh.lo) * 4,
+                              cudaMemcpyDeviceToDevice, s));
+    // packed id of u = number of vertices with out-edges before u
+    DevBuf<uint32_t> flag(n, s);
+    DevBuf<uint64_t> pmap(n + 1, s);
+    launch(n, s, [&](unsigned gr, unsigned bl) { k_nonzero_u32<<<gr, bl, 0, s>>>(od, n, flag.get()); });
+    scan_counts_to_ptr(flag.get(), pmap.get(), n, s);
+    launch(sh.in.nnz, s, [&](unsigned gr, unsigned bl) {
+      k_remap_cols<<<gr, bl, 0, s>>>(sh.in.idx.get(), sh.in.nnz, pmap.get());
+    });
+    uint64_t nz = 0;
+    GM_CUDA(cudaMemcpyAsync(&nz, pmap.get() + n, 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    g.nonzero_outdeg = nz;
+    degs[size_t(l)].reset();
+  }
+}
+
+}  // namespace
+
+// ---- DGraph -----------------------------------------------------------------
+DGraph::~DGraph() {
+  bfs.reset();
+  pr.reset();
+  sssp.reset();
+  cf.reset();
+  if (!comm) return;
+  for (int l = 0; l < comm->L && size_t(l) < sh.size(); ++l) {
+    comm->set(l);
+    cudaStreamSynchronize(comm->st[size_t(l)]);
+    DShard& s = sh[size_t(l)];
+    s.in.ptr.reset();
+    s.in.idx.reset();
+    s.in.val.reset();
+    s.out.ptr.reset();
+    s.out.idx.reset();
+    s.out.val.reset();
+    s.outdeg.reset();
+    cudaStreamSynchronize(comm->st[size_t(l)]);
+  }
+}
+
+uint64_t DGraph::owner(uint64_t v) const {
+  return uint64_t(std::upper_bound(bounds.begin(), bounds.end(), v) - bounds.begin()) - 1;
+}
+
+uint64_t DGraph::device_bytes(int l) const {
+  const DShard& s = sh[size_t(l)];
+  uint64_t b = s.in.ptr.bytes() + s.in.idx.bytes() + s.in.val.bytes() + s.outdeg.bytes();
+  if (!s.out_alias) b += s.out.ptr.bytes() + s.out.idx.bytes() + s.out.val.bytes();
+  return b;
+}
+
+namespace {
+
+DGraph* new_dgraph(Comm* c, uint64_t n, uint32_t flags) {
+  std::unique_ptr<DGraph> g(new DGraph());
+  g->comm = c;
+  g->n = n;
+  g->flags = flags;
+  g->symmetric = (flags & GM_SYMMETRIZE) != 0;
+  g->sh.resize(size_t(c->L));
+  for (int l = 0; l < c->L; ++l) g->sh[size_t(l)].l = l;
+  return g.release();
+}
+
+void finish_build(DGraph& g, unsigned nb, int weights, uint64_t seed) {
+  Comm& c = *g.comm;
+  if (g.symmetric) {
+    for (auto& s : g.sh) s.out_alias = true;
+  } else {
+    if ((g.flags & GM_NEED_FORWARD) || weights == GM_VAL_U8) build_forward(g, nb);
+    if (weights == GM_VAL_U8) {
+      g.value_type = GM_VAL_U8;
+      const uint64_t seed_w = mix64(seed ^ 0x57E16475ull);
+      for (int l = 0; l < c.L; ++l) {
+        c.set(l);
+        cudaStream_t s = c.st[size_t(l)];
+        DShard& sh = g.sh[size_t(l)];
+        for (int f = 0; f < 2; ++f) {
+          Csr& a = f ? sh.out : sh.in;
+          a.val.alloc(a.nnz + 1, s);
+          launch(a.n * 32, s, [&](unsigned gr, unsigned bl) {
+            k_row_weights<<<gr, bl, 0, s>>>(a.ptr.get(), a.idx.get(), sh.lo, a.n, seed_w, f == 0,
+                                            a.val.get());
+          });
+        }
+      }
+    }
+    finish_directed(g);  // after the forward build: it renumbers CSR(G^T) columns
+  }
+  uint64_t mm = 0;
+  std::vector<uint64_t> nnz;
+  for (auto& s : g.sh) nnz.push_back(s.in.nnz);
+  mm = c.sum_host(nnz);
+  g.m = mm;
+  if (g.symmetric) {
+    g.nonzero_outdeg = 0;  // not needed by the symmetric programs
+  }
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    GM_CUDA(cudaStreamSynchronize(c.st[size_t(l)]));
+  }
+}
+
+}  // namespace
+
+DGraph* dgraph_generate_rmat(Comm* c, uint32_t scale, uint32_t ef, double a, double b, double cc,
+                             uint64_t seed, uint32_t flags, int weights) {
+  if (scale == 0 || scale > 31) fail(GM_EUSAGE, "rmat: scale must be in [1, 31]");
+  if (!(a >= 0.0 && b >= 0.0 && cc >= 0.0 && a + b + cc <= 1.0))
+    fail(GM_EINPUT, "rmat: quadrant probabilities must be non-negative and sum to at most 1");
+  if (weights != GM_VAL_NONE && weights != GM_VAL_U8) fail(GM_EUSAGE, "rmat: weights must be none or u8");
+  if ((flags & GM_SYMMETRIZE) && weights != GM_VAL_NONE)
+    fail(GM_EUSAGE, "rmat: weighted symmetric sharded graphs are not supported");
+  const uint64_t n = uint64_t(1) << scale;
+  std::unique_ptr<DGraph> g(new_dgraph(c, n, flags | GM_PREPROCESS));
+  const uint64_t count = uint64_t(ef) << scale;
+  const unsigned nb = scale;
+  const int sym = g->symmetric ? 1 : 0;
+  std::vector<DevBuf<uint64_t>> keys(size_t(c->L));
+  std::vector<uint64_t> m(size_t(c->L));
+  for (int l = 0; l < c->L; ++l) {
+    c->set(l);
+    cudaStream_t s = c->st[size_t(l)];
+    const int r = c->global(l);
+    const uint64_t t0 = count * uint64_t(r) / uint64_t(c->P);
+    const uint64_t t1 = count * uint64_t(r + 1) / uint64_t(c->P);
+    DevBuf<uint32_t> s32(t1 - t0 + 1, s), d32(t1 - t0 + 1, s);
+    rmat_range(scale, a, b, cc, seed, 1, t0, t1 - t0, s32.get(), d32.get(), s);
+    keys[size_t(l)].alloc((t1 - t0) * (sym ? 2 : 1) + 1, s);
+    DevBuf<unsigned long long> cnt(1, s);
+    cnt.zero(s);
+    launch(t1 - t0, s, [&](unsigned gr, unsigned bl) {
+      k_edge_keys<<<gr, bl, 0, s>>>(s32.get(), d32.get(), t1 - t0, nb, sym, keys[size_t(l)].get(),
+                                    cnt.get());
+    });
+    m[size_t(l)] = dread_u64(cnt.get(), s);
+  }
+  route_and_build(*g, keys, m, nb, /*forward=*/false, /*check_dups=*/false);
+  finish_build(*g, nb, weights, seed);
+  return g.release();
+}
+
+DGraph* dgraph_create(Comm* c, const gm_edge_list& e, uint64_t n, uint32_t flags, int storage) {
+  if (storage != GM_VAL_NONE) fail(GM_EUSAGE, "dgraph: edge values are not supported yet");
+  if (flags & (GM_DAGIFY | GM_BIPARTITE_CHECK))
+    fail(GM_EUSAGE, "dgraph: DAGIFY / BIPARTITE_CHECK are single-GPU ingest modes");
+  if (n == 0 || n > (uint64_t(1) << 32)) fail(GM_EUSAGE, "dgraph: 1 <= n <= 2^32");
+  if (c->L != 1 && e.count)
+    fail(GM_EUSAGE, "dgraph: a local comm takes the edges from gm_dgraph_create_local");
+  std::unique_ptr<DGraph> g(new_dgraph(c, n, flags | ((flags & GM_SYMMETRIZE) ? GM_PREPROCESS : 0)));
+  const bool pre = (g->flags & GM_PREPROCESS) != 0;
+  const unsigned nb = bits_for(n);
+  const int sym = g->symmetric ? 1 : 0;
+  std::vector<DevBuf<uint64_t>> keys(size_t(c->L));
+  std::vector<uint64_t> m(size_t(c->L));
+  std::vector<uint64_t> bad(size_t(c->L), 0);
+  for (int l = 0; l < c->L; ++l) {
+    c->set(l);
+    cudaStream_t s = c->st[size_t(l)];
+    const uint64_t cnt = l == 0 ? uint64_t(e.count) : 0;
+    DevBuf<uint32_t> s32(cnt + 1, s), d32(cnt + 1, s);
+    if (cnt) {
+      if (e.id_type != GM_ID_U32) fail(GM_EUSAGE, "dgraph: ids must be u32");
+      const cudaMemcpyKind kd = e.on_device ? cudaMemcpyDefault : cudaMemcpyHostToDevice;
+      GM_CUDA(cudaMemcpyAsync(s32.get(), e.src, cnt * 4, kd, s));
+      GM_CUDA(cudaMemcpyAsync(d32.get(), e.dst, cnt * 4, kd, s));
+    }
+    // range check before packing (the reference message, dcsc.hpp:252-256)
+    std::vector<uint32_t> hs(cnt), hd(cnt);
+    if (cnt) {
+      GM_CUDA(cudaMemcpyAsync(hs.data(), s32.get(), cnt * 4, cudaMemcpyDeviceToHost, s));
+      GM_CUDA(cudaMemcpyAsync(hd.data(), d32.get(), cnt * 4, cudaMemcpyDeviceToHost, s));
+      GM_CUDA(cudaStreamSynchronize(s));
+    }
+    for (uint64_t i = 0; i < cnt && !bad[size_t(l)]; ++i)
+      if (hs[i] >= n || hd[i] >= n) {
+        bad[size_t(l)] = 1;
+        fail(GM_EINPUT, "build_graph: edge " + std::to_string(uint64_t(hs[i]) + 1) + " -> " +
+                            std::to_string(uint64_t(hd[i]) + 1) + " (1-based) exceeds vertex count " +
+                            std::to_string(n));
+      }
+    keys[size_t(l)].alloc(cnt * (sym ? 2 : 1) + 1, s);
+    DevBuf<unsigned long long> k(1, s);
+    k.zero(s);
+    if (pre) {
+      launch(cnt, s, [&](unsigned gr, unsigned bl) {
+        k_edge_keys<<<gr, bl, 0, s>>>(s32.get(), d32.get(), cnt, nb, sym, keys[size_t(l)].get(), k.get());
+      });
+      m[size_t(l)] = dread_u64(k.get(), s);
+    } else {
+      // build_graph keeps self loops; rows = destinations
+      std::vector<uint64_t> hk(cnt);
+      for (uint64_t i = 0; i < cnt; ++i) hk[i] = (uint64_t(hd[i]) << nb) | hs[i];
+      if (cnt)
+        GM_CUDA(cudaMemcpyAsync(keys[size_t(l)].get(), hk.data(), cnt * 8, cudaMemcpyHostToDevice, s));
+      GM_CUDA(cudaStreamSynchronize(s));
+      m[size_t(l)] = cnt;
+    }
+  }
+  route_and_build(*g, keys, m, nb, false, /*check_dups=*/!pre);
+  finish_build(*g, nb, GM_VAL_NONE, 0);
+  return g.release();
+}
+
+// ============================================================================
+// BFS over the row shards (algo::bfs, traversal.hpp:119-123; levels are the
+// superstep that first reaches a vertex, engine.hpp:193-213).
+//
+// Per superstep, on every shard:
+//   push (frontier small): expand the shard's own frontier rows (a local
+//        queue); a neighbour in the shard's rows is claimed in its next-block
+//        bitmap, any other one in the shard's full-N claims bitmap; after a
+//        barrier each owner ORs its words of every shard's claims bitmap into
+//        its next block (peer loads) and clears them (peer stores);
+//   pull (frontier large): every unvisited owned row scans its neighbours for
+//        a member of the replicated frontier bitmap (early exit).
+// finish: new = next & ~visited -> level, visited, the next local queue and
+// the (found, found edges) counters, which one u64 all-reduce sums; the host
+// reads the sums (the only host synchronisation per superstep) and applies
+// the single-GPU rule: pull once frontier edges > m/20, push again once the
+// frontier < n/24.  Before a pull superstep the owners store their new-frontier
+// words into every shard's replicated frontier bitmap (peer stores over
+// NVLink); pushes need no replicated frontier at all.
+// ============================================================================
+namespace {
+
+constexpr int kPush = 1, kPull = 0;
+
+__global__ void k_db_init(int32_t* level, uint64_t rows, uint32_t* vis, uint64_t words,
+                          uint64_t root_local, int owns_root, uint32_t* queue,
+                          unsigned long long* ctr, const uint64_t* ptr) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < rows || i < words;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (i < rows) level[i] = -1;
+    if (i < words) vis[i] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctr[0] = owns_root ? 1 : 0;                                     // found
+    ctr[1] = owns_root ? ptr[root_local + 1] - ptr[root_local] : 0;  // their edges
+    ctr[2] = 0;                                                      // examined (pull)
+    ctr[3] = owns_root ? 1 : 0;                                      // queue length
+    if (owns_root) {
+      level[root_local] = 0;
+      vis[root_local >> 5] |= 1u << (root_local & 31u);
+      queue[0] = uint32_t(root_local);
+    }
+  }
+}
+
+// push: warp per frontier row, lanes over its adjacency
+__global__ void __launch_bounds__(256) k_db_push(const uint32_t* __restrict__ queue,
+                                                 const unsigned long long* qn,
+                                                 const uint64_t* __restrict__ ptr,
+                                                 const uint32_t* __restrict__ idx, uint64_t lo,
+                                                 uint64_t hi, const uint32_t* __restrict__ vis,
+                                                 uint32_t* nxt, uint32_t* claims) {
+  const uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t nq = qn[3];
+  for (uint64_t i = w; i < nq; i += nw) {
+    const uint32_t r = queue[i];
+    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
+      const uint32_t v = __ldg(&idx[e]);
+      const uint32_t bit = 1u << (v & 31u);
+      if (v >= lo && v < hi) {
+        const uint64_t o = v - lo;
+        if (!(vis[o >> 5] & (1u << (o & 31u)))) atomicOr(&nxt[o >> 5], 1u << (o & 31u));
+      } else {
+        atomicOr(&claims[v >> 5], bit);
+      }
+    }
+  }
+}
+
+// pull: thread per unvisited owned row, early exit
+__global__ void __launch_bounds__(256) k_db_pull(const uint64_t* __restrict__ ptr,
+                                                 const uint32_t* __restrict__ idx, uint64_t rows,
+                                                 const uint32_t* __restrict__ vis,
+                                                 const uint32_t* __restrict__ fb, uint32_t* nxt,
+                                                 unsigned long long* ctr) {
+  unsigned long long ex = 0;
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    if ((vis[r >> 5] >> (r & 31u)) & 1u) continue;
+    const uint64_t b = ptr[r], e = ptr[r + 1];
+    for (uint64_t k = b; k < e; ++k) {
+      const uint32_t u = __ldg(&idx[k]);
+      ++ex;
+      if ((__ldg(&fb[u >> 5]) >> (u & 31u)) & 1u) {
+        atomicOr(&nxt[r >> 5], 1u << (r & 31u));
+        break;
+      }
+    }
+  }
+  warp_add_u64(&ctr[2], ex);
+}
+
+// owner side of a push: OR in (and clear) this block's words of every shard's claims
+__global__ void k_db_claims(PeerTab<uint32_t> claims, int P, uint64_t w0, uint64_t words,
+                            uint32_t* nxt) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t x = 0;
+    for (int q = 0; q < P; ++q) {
+      uint32_t* p = claims.p[q] + w0 + i;
+      const uint32_t c = *p;
+      if (c) {
+        x |= c;
+        *p = 0;
+      }
+    }
+    if (x) nxt[i] |= x;
+  }
+}
+
+__global__ void k_db_finish(uint32_t* nxt, uint32_t* vis, uint64_t words, uint64_t rows,
+                            int32_t lvl, int32_t* level, const uint64_t* ptr, uint32_t* queue,
+                            unsigned long long* ctr) {
+  unsigned long long f = 0, fe = 0;
+  for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < words;
+       w += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t nw = nxt[w] & ~vis[w];
+    if (w * 32 + 32 > rows && rows < w * 32 + 32) nw &= rows > w * 32 ? (~0u >> (32 - (rows - w * 32))) : 0u;
+    nxt[w] = nw;
+    if (!nw) continue;
+    vis[w] |= nw;
+    const unsigned c = __popc(nw);
+    const unsigned long long base = atomicAdd(&ctr[3], (unsigned long long)c);
+    unsigned k = 0;
+    while (nw) {
+      const int b = __ffs(nw) - 1;
+      nw &= nw - 1;
+      const uint64_t r = w * 32 + uint64_t(b);
+      level[r] = lvl;
+      fe += ptr[r + 1] - ptr[r];
+      queue[base + k++] = uint32_t(r);
+    }
+    f += c;
+  }
+  warp_add_u64(&ctr[0], f);
+  warp_add_u64(&ctr[1], fe);
+}
+
+// the new-frontier words of this block into every shard's frontier bitmap
+__global__ void k_db_publish(const uint32_t* nxt, uint64_t w0, uint64_t words, PeerTab<uint32_t> fb,
+                             int P) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t x = nxt[i];
+    for (int q = 0; q < P; ++q) fb.p[q][w0 + i] = x;
+  }
+}
+
+DBfsState& dbfs_state(DGraph& g) {
+  if (g.bfs) return *g.bfs;
+  Comm& c = *g.comm;
+  g.bfs = std::unique_ptr<DBfsState, void (*)(DBfsState*)>(new DBfsState(),
+                                                           [](DBfsState* p) { delete p; });
+  DBfsState& st = *g.bfs;
+  const int L = c.L;
+  st.level.resize(size_t(L));
+  st.vis.resize(size_t(L));
+  st.nxt.resize(size_t(L));
+  st.queue.resize(size_t(L));
+  st.ctr.resize(size_t(L));
+  st.sum.resize(size_t(L));
+  const uint64_t words_all = (g.n + 31) / 32;
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    const uint64_t rows = g.sh[size_t(l)].hi - g.sh[size_t(l)].lo;
+    const uint64_t words = (rows + 31) / 32;
+    st.level[size_t(l)].alloc(rows + 1, s);
+    st.vis[size_t(l)].alloc(words + 1, s);
+    st.nxt[size_t(l)].alloc(words + 1, s);
+    st.queue[size_t(l)].alloc(rows + 1, s);
+    st.ctr[size_t(l)].alloc(4, s);
+    st.sum[size_t(l)].alloc(4, s);
+    st.nxt[size_t(l)].zero(s);
+    for (int b = 0; b < 2; ++b) st.fb[b].push_back(c.peer_alloc(l, words_all * 4));
+    st.claims.push_back(c.peer_alloc(l, words_all * 4));
+    GM_CUDA(cudaMemsetAsync(st.claims.back(), 0, words_all * 4, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+  }
+  st.c = &c;
+  for (int b = 0; b < 2; ++b) st.fb_tab[b] = c.share(st.fb[b]);
+  st.claims_tab = c.share(st.claims);
+  return st;
+}
+
+template <typename T>
+PeerTab<T> tab_of(const std::vector<void*>& row, int P) {
+  PeerTab<T> t{};
+  for (int q = 0; q < P; ++q) t.p[q] = static_cast<T*>(row[size_t(q)]);
+  return t;
+}
+
+struct StepTimer {
+  cudaEvent_t e[4]{};
+  explicit StepTimer() {
+    for (auto& x : e) GM_CUDA(cudaEventCreate(&x));
+  }
+  ~StepTimer() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+  double ms(int a, int b) const {
+    float x = 0.f;
+    if (cudaEventElapsedTime(&x, e[a], e[b]) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return 0.0;
+    }
+    return x;
+  }
+};
+
+}  // namespace
+
+std::vector<gm_iteration_stats> dbfs(DGraph& g, uint64_t root, int64_t max_iters, int32_t* out,
+                                     bool out_on_device) {
+  Comm& c = *g.comm;
+  if (!g.symmetric) fail(GM_EUSAGE, "dgraph bfs: needs a symmetric graph (GM_SYMMETRIZE)");
+  if (root >= g.n)
+    fail(GM_EINPUT, "source vertex " + std::to_string(root + 1) + " (1-based) exceeds vertex count " +
+                        std::to_string(g.n));
+  DBfsState& st = dbfs_state(g);
+  const int L = c.L, P = c.P;
+  const uint64_t n = g.n, m = g.m;
+  const uint64_t ro = g.owner(root);
+  c.set(0);
+  HostPinned<unsigned long long> h(4);
+  std::vector<std::vector<gm_iteration_stats>> none;
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
+    const int owns = uint64_t(c.global(l)) == ro;
+    k_db_init<<<grid_for(std::max(rows, words) + 1, kBlock), kBlock, 0, s>>>(
+        st.level[size_t(l)].get(), rows, st.vis[size_t(l)].get(), words, owns ? root - sh.lo : 0,
+        owns, st.queue[size_t(l)].get(), st.ctr[size_t(l)].get(), sh.in.ptr.get());
+    GM_LAUNCH_CHECK();
+  }
+  std::vector<const uint64_t*> cin;
+  std::vector<uint64_t*> cout_;
+  for (int l = 0; l < L; ++l) {
+    cin.push_back(reinterpret_cast<const uint64_t*>(st.ctr[size_t(l)].get()));
+    cout_.push_back(reinterpret_cast<uint64_t*>(st.sum[size_t(l)].get()));
+  }
+  StepTimer tm;
+  std::vector<gm_iteration_stats> stats;
+  uint64_t nf = 1, ef = 0;
+  {
+    // the root's degree: first summed counters
+    c.allreduce_u64(cin, cout_, 4);
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(h.get(), st.sum[0].get(), 32, cudaMemcpyDeviceToHost, c.st[0]));
+    GM_CUDA(cudaStreamSynchronize(c.st[0]));
+    ef = h[1];
+  }
+  int dir = kPush;
+  int cur = 0;
+  for (int64_t it = 1; nf > 0 && it <= max_iters; ++it) {
+    // direction (the single-GPU rule of k_bfs_coop)
+    int nd = dir;
+    if (dir == kPush && ef * 20 > m) nd = kPull;
+    else if (dir == kPull && nf * 24 < n) nd = kPush;
+    if (nd == kPull) {
+      // publish the current frontier blocks into every shard's bitmap
+      for (int l = 0; l < L; ++l) {
+        c.set(l);
+        cudaStream_t s = c.st[size_t(l)];
+        DShard& sh = g.sh[size_t(l)];
+        const uint64_t words = (sh.hi - sh.lo + 31) / 32;
+        if (l == 0) GM_CUDA(cudaEventRecord(tm.e[2], s));
+        launch(words, s, [&](unsigned gr, unsigned bl) {
+          k_db_publish<<<gr, bl, 0, s>>>(st.nxt[size_t(l)].get(), sh.lo / 32, words,
+                                         tab_of<uint32_t>(st.fb_tab[cur][size_t(l)], P), P);
+        });
+      }
+      c.barrier();
+    } else if (L > 0) {
+      c.set(0);
+      GM_CUDA(cudaEventRecord(tm.e[2], c.st[0]));
+    }
+    c.set(0);
+    GM_CUDA(cudaEventRecord(tm.e[3], c.st[0]));
+    const double publish_ms = -1;  // placeholder: measured below
+    (void)publish_ms;
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      DShard& sh = g.sh[size_t(l)];
+      const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[0], s));
+      // the queue length (ctr[3]) of the last finish is read by the push
+      GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get(), 0, 24, s));
+      if (nd == kPush) {
+        k_db_push<<<148 * 4, 256, 0, s>>>(st.queue[size_t(l)].get(), st.ctr[size_t(l)].get(),
+                                          sh.in.ptr.get(), sh.in.idx.get(), sh.lo, sh.hi,
+                                          st.vis[size_t(l)].get(), st.nxt[size_t(l)].get(),
+                                          static_cast<uint32_t*>(st.claims[size_t(l)]));
+        GM_LAUNCH_CHECK();
+      } else {
+        // nxt holds the published frontier block: clear it for the claims
+        if (words) GM_CUDA(cudaMemsetAsync(st.nxt[size_t(l)].get(), 0, words * 4, s));
+        launch(rows, s, [&](unsigned gr, unsigned bl) {
+          k_db_pull<<<gr, bl, 0, s>>>(sh.in.ptr.get(), sh.in.idx.get(), rows, st.vis[size_t(l)].get(),
+                                      static_cast<const uint32_t*>(st.fb[cur][size_t(l)]),
+                                      st.nxt[size_t(l)].get(), st.ctr[size_t(l)].get());
+        });
+      }
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[1], s));
+    }
+    if (nd == kPush) {
+      c.barrier();
+      for (int l = 0; l < L; ++l) {
+        c.set(l);
+        cudaStream_t s = c.st[size_t(l)];
+        DShard& sh = g.sh[size_t(l)];
+        const uint64_t words = (sh.hi - sh.lo + 31) / 32;
+        launch(words, s, [&](unsigned gr, unsigned bl) {
+          k_db_claims<<<gr, bl, 0, s>>>(tab_of<uint32_t>(st.claims_tab[size_t(l)], P), P, sh.lo / 32,
+                                        words, st.nxt[size_t(l)].get());
+        });
+      }
+      // nobody expands into a claims bitmap before its owner cleared it
+      c.barrier();
+    }
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      DShard& sh = g.sh[size_t(l)];
+      const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
+      GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get() + 3, 0, 8, s));
+      launch(words, s, [&](unsigned gr, unsigned bl) {
+        k_db_finish<<<gr, bl, 0, s>>>(st.nxt[size_t(l)].get(), st.vis[size_t(l)].get(), words, rows,
+                                      int32_t(it), st.level[size_t(l)].get(), sh.in.ptr.get(),
+                                      st.queue[size_t(l)].get(), st.ctr[size_t(l)].get());
+      });
+    }
+    c.allreduce_u64(cin, cout_, 4);
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(h.get(), st.sum[0].get(), 32, cudaMemcpyDeviceToHost, c.st[0]));
+    GM_CUDA(cudaEventRecord(tm.e[3], c.st[0]));
+    GM_CUDA(cudaStreamSynchronize(c.st[0]));
+    gm_iteration_stats s{};
+    s.iteration = it;
+    s.active_before = int64_t(nf);
+    s.messages_generated = int64_t(nf);
+    s.vertices_updated = int64_t(h[0]);
+    s.direction = nd == kPush ? 1 : 0;
+    s.edges_processed = int64_t(nd == kPush ? ef : h[2]);
+    s.spmv_seconds = tm.ms(0, 1) * 1e-3;
+    s.total_seconds = tm.ms(2, 3) * 1e-3;
+    s.comm_seconds = std::max(0.0, s.total_seconds - s.spmv_seconds);
+    s.bytes_algorithmic = nd == kPush
+                              ? int64_t(24 * nf + 4 * ef + 16 * h[0] + n / 8)
+                              : int64_t(16 * n + 4 * h[2] + 4 * h[0] + 2 * n / 8);
+    stats.push_back(s);
+    nf = h[0];
+    ef = h[1];
+    dir = nd;
+    cur ^= 1;
+    (void)none;
+  }
+  // levels of the owned rows, concatenated in shard order
+  if (out) {
+    uint64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      const uint64_t rows = g.sh[size_t(l)].hi - g.sh[size_t(l)].lo;
+      if (rows)
+        GM_CUDA(cudaMemcpyAsync(out + off, st.level[size_t(l)].get(), rows * 4,
+                                out_on_device ? cudaMemcpyDefault : cudaMemcpyDeviceToHost, s));
+      off += rows;
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    GM_CUDA(cudaStreamSynchronize(c.st[size_t(l)]));
+  }
+  return stats;
+}
+
+}  // namespace gm

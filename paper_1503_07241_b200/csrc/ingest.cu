@@ -249,9 +249,10 @@ __global__ void k_convert(const In* in, int64_t m, Out* out) {
 
 __global__ void k_rmat(uint64_t count, unsigned scale, uint64_t ta, uint64_t tab, uint64_t tabc,
                        uint32_t k0, uint32_t k1, PermKeys pk, int permute, uint32_t* src,
-                       uint32_t* dst) {
-  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < count;
-       t += uint64_t(gridDim.x) * blockDim.x) {
+                       uint32_t* dst, uint64_t t0 = 0) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t t = t0 + i;  // tuple id: counter of the generator
     uint32_t s = 0, d = 0;
     for (unsigned l = 0; l < scale; l += 4) {
       uint32_t out[4];
@@ -276,8 +277,8 @@ __global__ void k_rmat(uint64_t count, unsigned scale, uint64_t ta, uint64_t tab
       s = perm_apply(pk, s);
       d = perm_apply(pk, d);
     }
-    src[t] = s;
-    dst[t] = d;
+    src[i] = s;
+    dst[i] = d;
   }
 }
 
@@ -713,6 +714,34 @@ Graph* graph_create(const gm_edge_list& e, uint64_t n, uint32_t flags, int stora
   build(*g, s32, d32, m, vals);
   if (flags & GM_NEED_FORWARD) ensure_forward(*g);
   return g.release();
+}
+
+// ---- helpers shared with the sharded ingest (dist.cu, ingest.cuh) ----------
+void rmat_range(unsigned scale, double a, double b, double c, uint64_t seed, int permute,
+                uint64_t t0, uint64_t count, uint32_t* src, uint32_t* dst, cudaStream_t s) {
+  const PermKeys pk = make_perm_keys(scale, seed);
+  const uint64_t ta = prob_threshold(a), tab = prob_threshold(a + b), tabc = prob_threshold(a + b + c);
+  launch(count, s, [&](unsigned gr, unsigned bl) {
+    k_rmat<<<gr, bl, 0, s>>>(count, scale, ta, tab, tabc, uint32_t(seed), uint32_t(seed >> 32), pk,
+                             permute, src, dst, t0);
+  });
+}
+
+void sort_keys_u64(DevBuf<uint64_t>& keys, int64_t m, int end_bit, cudaStream_t s) {
+  sort_keys(keys, m, end_bit, s);
+}
+
+int64_t unique_keys_u64(DevBuf<uint64_t>& keys, int64_t m, cudaStream_t s) {
+  if (m <= 1) return m;
+  DevBuf<uint8_t> flag(m, s);
+  launch(uint64_t(m), s, [&](unsigned gr, unsigned bl) {
+    k_unique_flags<<<gr, bl, 0, s>>>(keys.get(), m, flag.get(), nullptr);
+  });
+  return select_flagged(keys, flag.get(), m, s);
+}
+
+void scan_counts_to_ptr(const uint32_t* counts, uint64_t* ptr, uint64_t n, cudaStream_t s) {
+  exclusive_scan_to_ptr(counts, ptr, n, s);
 }
 
 Graph* graph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c,

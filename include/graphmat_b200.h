@@ -95,6 +95,7 @@ typedef struct {
   int64_t bytes_algorithmic; /* DESIGN.md formula for the kernel that ran          */
   int32_t direction;         /* 0 = pull SpMV over G^T, 1 = push SpMSpV over G     */
   int32_t reserved;
+  double comm_seconds;       /* sharded runs: exchange + barrier time of the step  */
 } gm_iteration_stats;
 
 typedef struct {
@@ -436,6 +437,74 @@ GM_API gm_status gm_sssp_shard_dists(gm_graph_t g, uint64_t row_begin, uint64_t 
 GM_API gm_status gm_cf_shard_step(gm_graph_t g, uint64_t row_begin, uint64_t row_end, int32_t k,
                                   const float* factors_full_dev, float gamma, float lambda,
                                   float* factors_block_dev, double* sq_err_sum, uint64_t* changed);
+/* ---- multi-GPU behind the ABI: communicator + row-sharded graph -----------
+ * The reference runs every row partition of G^T from one run_graph_program
+ * call (engine.hpp:193-213; partitions by balanced_row_boundaries,
+ * dcsc.hpp:77-105).  Here a partition ("shard") lives on a GPU and holds only
+ * its rows; the superstep loop, the exchange and the termination test run
+ * inside the library.
+ *
+ * A communicator spans P shards:
+ *   gm_comm_create_local  one process drives every shard, devices[i] being the
+ *                         GPU of shard i (repeats allowed: virtual shards on
+ *                         one GPU); the exchange is peer memory over NVLink;
+ *   gm_comm_create_nccl   one process per GPU (shard = rank), NCCL (libnccl
+ *                         loaded at run time; GM_ENCCL on failure) plus CUDA
+ *                         IPC mappings for the peer stores.  Rank 0 creates the
+ *                         128-byte id with gm_comm_nccl_unique_id and the
+ *                         caller distributes it (as NCCL applications do).
+ * Every gm_dgraph_* call is collective: each process of the communicator
+ * makes it, in the same order.  The communicator must outlive its graphs. */
+typedef struct gm_comm* gm_comm_t;
+typedef struct gm_dgraph* gm_dgraph_t;
+GM_API gm_status gm_comm_create_local(int32_t nshards, const int32_t* devices, gm_comm_t* out);
+GM_API gm_status gm_comm_nccl_unique_id(void* id128);
+GM_API gm_status gm_comm_create_nccl(int32_t nranks, int32_t rank, int32_t device,
+                                     const void* id128, gm_comm_t* out);
+GM_API gm_status gm_comm_destroy(gm_comm_t c);
+
+typedef struct {
+  uint64_t num_vertices;       /* global                                          */
+  uint64_t num_edges;          /* global stored entries of CSR(G^T)               */
+  uint64_t row_begin, row_end; /* this shard's caller-id rows                      */
+  uint64_t local_edges;        /* entries of this shard's CSR(G^T) rows           */
+  uint64_t device_bytes;       /* graph bytes on this shard's GPU                  */
+  uint64_t nonzero_out_degree; /* global (directed graphs)                         */
+  int32_t shards, local_shards, first_shard, device;
+} gm_dshard_info;
+
+/* Sharded ingest (dcsc.hpp:110-164 + io::preprocess, io.cpp:184-222): every
+ * shard generates 1/P of the seeded R-MAT stream (the same graph as
+ * gm_graph_generate_rmat with permute = 1), the edges travel all-to-all to
+ * the owner of their destination row, which deduplicates and builds CSR(G^T)
+ * of its rows (entries ascending by caller id) -- plus CSR(G) of its rows
+ * for directed graphs with GM_NEED_FORWARD or weights.  Boundaries balance
+ * entries like balanced_row_boundaries (dcsc.hpp:81-105), 32-row aligned. */
+GM_API gm_status gm_dgraph_generate_rmat(gm_comm_t c, uint32_t scale, uint32_t edge_factor,
+                                         double a, double b, double cc, uint64_t seed,
+                                         uint32_t flags, int32_t weights, gm_dgraph_t* out);
+/* build_graph over a communicator: each process passes its share of the edge
+ * list (any subset; a local communicator passes the whole list), the library
+ * routes every edge to its owner.  Errors as gm_graph_create, agreed by all
+ * ranks.  u32 ids, no values. */
+GM_API gm_status gm_dgraph_create(gm_comm_t c, const gm_edge_list* edges, uint64_t num_vertices,
+                                  uint32_t flags, int32_t value_storage, gm_dgraph_t* out);
+GM_API gm_status gm_dgraph_destroy(gm_dgraph_t g);
+GM_API gm_status gm_dgraph_shard_info(gm_dgraph_t g, int32_t local_shard, gm_dshard_info* info);
+GM_API void* gm_dgraph_stream(gm_dgraph_t g, int32_t local_shard);
+/* Outputs of the sharded programs: the owned rows of this process's shards,
+ * concatenated in shard order -- the whole caller-order vector for a local
+ * communicator, rows [row_begin, row_end) for an NCCL rank.  Stats are
+ * global (identical on every rank) with comm_seconds per superstep. */
+/* algo::bfs (traversal.hpp:119-123) on a symmetric sharded graph. */
+GM_API gm_status gm_dgraph_bfs(gm_dgraph_t g, uint64_t root, int64_t max_iters, int32_t* out_level,
+                               int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                               int64_t* n_stats);
+/* gm_pagerank on a directed sharded graph; ranks bitwise independent of P. */
+GM_API gm_status gm_dgraph_pagerank(gm_dgraph_t g, const gm_pagerank_config* cfg, float* out_rank,
+                                    int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                                    int64_t* n_stats);
+
 /* Row-block boundaries balanced by stored entries, like
  * detail::balanced_row_boundaries (dcsc.hpp:81-105).  row_nnz: n counts;
  * bounds: parts+1 entries. */

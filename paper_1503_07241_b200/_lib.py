@@ -36,6 +36,9 @@ EXPORTED = [
     "gm_pagerank_shard_step_peers", "gm_pagerank_shard_init_peers", "gm_ipc_alloc", "gm_ipc_free", "gm_ipc_handle", "gm_ipc_open",
     "gm_ipc_close", "gm_bfs_shard_push", "gm_bitmap_or", "gm_push_block",
     "gm_kernel_timer_start", "gm_kernel_timer_stop",
+    "gm_comm_create_local", "gm_comm_nccl_unique_id", "gm_comm_create_nccl", "gm_comm_destroy",
+    "gm_dgraph_generate_rmat", "gm_dgraph_create", "gm_dgraph_destroy", "gm_dgraph_shard_info",
+    "gm_dgraph_stream", "gm_dgraph_bfs", "gm_dgraph_pagerank",
 ]
 
 
@@ -52,7 +55,8 @@ class IterationStatsC(C.Structure):
                 ("messages_generated", C.c_int64), ("vertices_updated", C.c_int64),
                 ("spmv_seconds", C.c_double), ("total_seconds", C.c_double),
                 ("edges_processed", C.c_int64), ("bytes_algorithmic", C.c_int64),
-                ("direction", C.c_int32), ("reserved", C.c_int32)]
+                ("direction", C.c_int32), ("reserved", C.c_int32),
+                ("comm_seconds", C.c_double)]
 
 
 class GraphInfo(C.Structure):
@@ -69,6 +73,16 @@ class RunReportC(C.Structure):
                 ("n_iterations", C.c_uint64), ("total_seconds", C.c_double),
                 ("checksum", C.c_uint64), ("extra_keys", C.POINTER(C.c_char_p)),
                 ("extra_values", C.POINTER(C.c_char_p)), ("n_extras", C.c_uint64)]
+
+
+class DShardInfo(C.Structure):
+    """gm_dshard_info."""
+
+    _fields_ = [("num_vertices", C.c_uint64), ("num_edges", C.c_uint64),
+                ("row_begin", C.c_uint64), ("row_end", C.c_uint64), ("local_edges", C.c_uint64),
+                ("device_bytes", C.c_uint64), ("nonzero_out_degree", C.c_uint64),
+                ("shards", C.c_int32), ("local_shards", C.c_int32), ("first_shard", C.c_int32),
+                ("device", C.c_int32)]
 
 
 class PageRankConfig(C.Structure):
@@ -171,6 +185,19 @@ def load(path: str = LIB_PATH):
         "gm_bfs_shard_push": (C.c_int, [vp, u64, u64, vp, vp, i32]),
         "gm_bitmap_or": (C.c_int, [vp, vp, vp, u64]),
         "gm_push_block": (C.c_int, [vp, vp, u64, vp, i32, u64]),
+        "gm_comm_create_local": (C.c_int, [i32, vp, C.POINTER(vp)]),
+        "gm_comm_nccl_unique_id": (C.c_int, [vp]),
+        "gm_comm_create_nccl": (C.c_int, [i32, i32, i32, vp, C.POINTER(vp)]),
+        "gm_comm_destroy": (C.c_int, [vp]),
+        "gm_dgraph_generate_rmat": (C.c_int, [vp, u32, u32, dp, dp, dp, u64, u32, i32,
+                                              C.POINTER(vp)]),
+        "gm_dgraph_create": (C.c_int, [vp, C.POINTER(EdgeList), u64, u32, i32, C.POINTER(vp)]),
+        "gm_dgraph_destroy": (C.c_int, [vp]),
+        "gm_dgraph_shard_info": (C.c_int, [vp, i32, C.POINTER(DShardInfo)]),
+        "gm_dgraph_stream": (vp, [vp, i32]),
+        "gm_dgraph_bfs": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),
+        "gm_dgraph_pagerank": (C.c_int, [vp, C.POINTER(PageRankConfig), vp, i32, st, i64,
+                                         C.POINTER(i64)]),
     }
     for name, (res, args) in proto.items():
         f = getattr(L, name)

@@ -73,6 +73,7 @@ class IterationStats:
     edges_processed: int = 0
     bytes_algorithmic: int = 0
     direction: str = "pull"
+    comm_seconds: float = 0.0
 
     def key(self):
         return (self.iteration, self.active_before, self.messages_generated,
@@ -85,7 +86,7 @@ def _stats(buf, n):
         out.append(IterationStats(s.iteration, s.active_before, s.messages_generated,
                                   s.vertices_updated, s.spmv_seconds, s.total_seconds,
                                   s.edges_processed, s.bytes_algorithmic,
-                                  "push" if s.direction == 1 else "pull"))
+                                  "push" if s.direction == 1 else "pull", s.comm_seconds))
     return out
 
 

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "api_internal.cuh"
+#include "dist.cuh"
 
 namespace gm {
 static std::atomic<uint64_t> g_launches{0};
@@ -132,6 +133,113 @@ GM_API void* gm_graph_stream(gm_graph_t g) {
 
 GM_API gm_status gm_graph_synchronize(gm_graph_t g) {
   return guarded([&] { GM_CUDA(cudaStreamSynchronize(handle(g)->stream)); });
+}
+
+// ---- multi-GPU: communicator + sharded graph ----------------------------------
+namespace {
+gm::Comm* comm_of(gm_comm_t c) {
+  if (!c) gm::fail(GM_EUSAGE, "null communicator");
+  return reinterpret_cast<gm::Comm*>(c);
+}
+gm::DGraph* dgraph_of(gm_dgraph_t g) {
+  if (!g) gm::fail(GM_EUSAGE, "null sharded graph");
+  return reinterpret_cast<gm::DGraph*>(g);
+}
+}  // namespace
+
+GM_API gm_status gm_comm_create_local(int32_t nshards, const int32_t* devices, gm_comm_t* out) {
+  return guarded([&] {
+    if (!out) gm::fail(GM_EUSAGE, "null output");
+    *out = reinterpret_cast<gm_comm_t>(gm::comm_create_local(nshards, devices));
+  });
+}
+
+GM_API gm_status gm_comm_nccl_unique_id(void* id128) {
+  return guarded([&] {
+    if (!id128) gm::fail(GM_EUSAGE, "null id buffer");
+    gm::comm_nccl_unique_id(id128);
+  });
+}
+
+GM_API gm_status gm_comm_create_nccl(int32_t nranks, int32_t rank, int32_t device,
+                                     const void* id128, gm_comm_t* out) {
+  return guarded([&] {
+    if (!out || !id128) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_comm_t>(gm::comm_create_nccl(nranks, rank, device, id128));
+  });
+}
+
+GM_API gm_status gm_comm_destroy(gm_comm_t c) {
+  return guarded([&] { delete reinterpret_cast<gm::Comm*>(c); });
+}
+
+GM_API gm_status gm_dgraph_generate_rmat(gm_comm_t c, uint32_t scale, uint32_t edge_factor,
+                                         double a, double b, double cc, uint64_t seed,
+                                         uint32_t flags, int32_t weights, gm_dgraph_t* out) {
+  return guarded([&] {
+    if (!out) gm::fail(GM_EUSAGE, "null output");
+    *out = reinterpret_cast<gm_dgraph_t>(
+        gm::dgraph_generate_rmat(comm_of(c), scale, edge_factor, a, b, cc, seed, flags, weights));
+  });
+}
+
+GM_API gm_status gm_dgraph_create(gm_comm_t c, const gm_edge_list* edges, uint64_t num_vertices,
+                                  uint32_t flags, int32_t value_storage, gm_dgraph_t* out) {
+  return guarded([&] {
+    if (!out || !edges) gm::fail(GM_EUSAGE, "null argument");
+    *out = reinterpret_cast<gm_dgraph_t>(
+        gm::dgraph_create(comm_of(c), *edges, num_vertices, flags, value_storage));
+  });
+}
+
+GM_API gm_status gm_dgraph_destroy(gm_dgraph_t g) {
+  return guarded([&] { delete reinterpret_cast<gm::DGraph*>(g); });
+}
+
+GM_API gm_status gm_dgraph_shard_info(gm_dgraph_t g, int32_t local_shard, gm_dshard_info* info) {
+  return guarded([&] {
+    gm::DGraph* d = dgraph_of(g);
+    if (!info || local_shard < 0 || local_shard >= d->comm->L) gm::fail(GM_EUSAGE, "bad shard");
+    const gm::DShard& s = d->sh[size_t(local_shard)];
+    info->num_vertices = d->n;
+    info->num_edges = d->m;
+    info->row_begin = s.lo;
+    info->row_end = s.hi;
+    info->local_edges = s.in.nnz;
+    info->device_bytes = d->device_bytes(local_shard);
+    info->nonzero_out_degree = d->nonzero_outdeg;
+    info->shards = d->comm->P;
+    info->local_shards = d->comm->L;
+    info->first_shard = d->comm->first;
+    info->device = d->comm->dev[size_t(local_shard)];
+  });
+}
+
+GM_API void* gm_dgraph_stream(gm_dgraph_t g, int32_t local_shard) {
+  if (!g) return nullptr;
+  gm::DGraph* d = reinterpret_cast<gm::DGraph*>(g);
+  if (local_shard < 0 || local_shard >= d->comm->L) return nullptr;
+  return reinterpret_cast<void*>(d->comm->st[size_t(local_shard)]);
+}
+
+GM_API gm_status gm_dgraph_bfs(gm_dgraph_t g, uint64_t root, int64_t max_iters, int32_t* out_level,
+                               int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                               int64_t* n_stats) {
+  return guarded([&] {
+    const auto st = gm::dbfs(*dgraph_of(g), root, max_iters, out_level, out_on_device != 0);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
+GM_API gm_status gm_dgraph_pagerank(gm_dgraph_t g, const gm_pagerank_config* cfg, float* out_rank,
+                                    int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
+                                    int64_t* n_stats) {
+  return guarded([&] {
+    if (!cfg) gm::fail(GM_EUSAGE, "null config");
+    const auto st = gm::dpagerank(*dgraph_of(g), cfg->damping, cfg->iterations, out_rank,
+                                  out_on_device != 0);
+    copy_stats(st, stats, cap, n_stats);
+  });
 }
 
 GM_API gm_status gm_kernel_timer_start(gm_graph_t g) {

@@ -209,7 +209,7 @@ void Comm::alltoallv(const std::vector<const uint8_t*>& send,
 
 std::vector<std::vector<uint64_t>> Comm::exchange_counts(
     const std::vector<std::vector<uint64_t>>& mine) {
-  std::vector<std::vector<uint64_t>> theirs(size_t(L), std::vector<uint64_t>(size_t(P)));
+  std::vector<std::vector<uint64_t>> theirs(static_cast<size_t>(L), std::vector<uint64_t>(static_cast<size_t>(P)));
   if (!use_nccl) {
     for (int l = 0; l < L; ++l)
       for (int q = 0; q < P; ++q) theirs[size_t(l)][size_t(q)] = mine[size_t(q)][size_t(l)];
@@ -255,7 +255,7 @@ void Comm::peer_free(int l, void* p) {
 }
 
 std::vector<std::vector<void*>> Comm::share(const std::vector<void*>& local) {
-  std::vector<std::vector<void*>> t(size_t(L), std::vector<void*>(size_t(P), nullptr));
+  std::vector<std::vector<void*>> t(static_cast<size_t>(L), std::vector<void*>(static_cast<size_t>(P), nullptr));
   if (!use_nccl) {
     for (int l = 0; l < L; ++l)
       for (int q = 0; q < P; ++q) t[size_t(l)][size_t(q)] = local[size_t(q)];
@@ -268,7 +268,7 @@ std::vector<std::vector<void*>> Comm::share(const std::vector<void*>& local) {
   GM_CUDA(cudaMemcpyAsync(a.get(), &h, sizeof(h), cudaMemcpyHostToDevice, st[0]));
   GM_NCCL(nccl_api().AllGather(a.get(), all.get(), sizeof(h), ncclUint8,
                                static_cast<ncclComm_t>(nccl), st[0]));
-  std::vector<cudaIpcMemHandle_t> hs(size_t(P));
+  std::vector<cudaIpcMemHandle_t> hs(static_cast<size_t>(P));
   GM_CUDA(cudaMemcpyAsync(hs.data(), all.get(), sizeof(h) * size_t(P), cudaMemcpyDeviceToHost, st[0]));
   GM_CUDA(cudaStreamSynchronize(st[0]));
   // open every peer's handle; agree on success so no rank proceeds alone

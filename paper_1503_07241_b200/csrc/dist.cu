@@ -58,12 +58,16 @@ struct DBfsState {
 };
 
 struct DPrState {
-  std::vector<DevBuf<float>> rank, inv;          // [l] owned rows
-  std::vector<DevBuf<uint32_t>> pid;             // [l] packed id per owned row (~0u: dangling)
-  std::vector<DevBuf<uint32_t>> rows_short, rows_long;  // [l] row bins
-  std::vector<uint64_t> n_short, n_long;
+  std::vector<DevBuf<float>> rank, inv;               // [l] owned rows
+  std::vector<DevBuf<uint32_t>> rows_short;           // [l] rows with <= kPrShort entries
+  std::vector<DevBuf<uint32_t>> rows_long;            // [l] longer rows
+  std::vector<DevBuf<uint64_t>> chunk_beg;            // [l] chunk c: entries [beg[c], beg[c+1])
+  std::vector<DevBuf<uint32_t>> long_chunk0;          // [l] first chunk of long row i (+1 end)
+  std::vector<DevBuf<float>> chunk_sum;               // [l] per-chunk partial sums
+  std::vector<uint64_t> n_short, n_long, n_chunks;
   std::vector<DevBuf<unsigned long long>> part, sum;  // [l] 2 parities x 4 words
-  std::vector<void*> x[2];                       // [l] peer-visible packed message vectors
+  DevBuf<unsigned long long> trace;                   // shard 0: summed words per superstep
+  std::vector<void*> x[2];                            // [l] peer-visible packed messages
   std::vector<std::vector<void*>> x_tab[2];
   Comm* c = nullptr;
   ~DPrState() {
@@ -76,11 +80,14 @@ struct DPrState {
       c->peer_free(l, x[1][size_t(l)]);
       rank[size_t(l)].reset();
       inv[size_t(l)].reset();
-      pid[size_t(l)].reset();
       rows_short[size_t(l)].reset();
       rows_long[size_t(l)].reset();
+      chunk_beg[size_t(l)].reset();
+      long_chunk0[size_t(l)].reset();
+      chunk_sum[size_t(l)].reset();
       part[size_t(l)].reset();
       sum[size_t(l)].reset();
+      if (l == 0) trace.reset();
     }
   }
 };
@@ -176,6 +183,13 @@ __global__ void k_nonzero_u32(const uint32_t* deg, uint64_t n, uint32_t* flag) {
     flag[v] = deg[v] > 0;
 }
 
+__global__ void k_block_pids(const uint32_t* od, const uint64_t* pmap, uint64_t lo, uint64_t rows,
+                             uint32_t* pid) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x)
+    pid[r] = od[lo + r] ? uint32_t(pmap[lo + r]) : ~0u;
+}
+
 __global__ void k_remap_cols(uint32_t* idx, uint64_t nnz, const uint64_t* pmap) {
   for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz;
        e += uint64_t(gridDim.x) * blockDim.x)
@@ -191,14 +205,6 @@ __global__ void k_row_weights(const uint64_t* ptr, const uint32_t* idx, uint64_t
       const uint32_t row = uint32_t(lo + r), col = idx[e];
       w[e] = row_is_dst ? edge_weight(seed_w, col, row) : edge_weight(seed_w, row, col);
     }
-}
-
-__global__ void k_check_ids(const uint64_t* keys, uint64_t m, unsigned nb, uint64_t n,
-                            unsigned long long* bad) {
-  const uint64_t mask = (uint64_t(1) << nb) - 1;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < m;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    if ((keys[i] >> nb) >= n || (keys[i] & mask) >= n) atomicMin(bad, (unsigned long long)i);
 }
 
 __global__ void k_first_dup(const uint64_t* keys, uint64_t m, unsigned long long* first) {
@@ -231,7 +237,7 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
   if (g.bounds.empty()) {
     const unsigned bb = bucket_bits(g.n, P);
     const uint64_t nbk = (g.n + (uint64_t(1) << bb) - 1) >> bb;
-    std::vector<DevBuf<unsigned long long>> h(size_t(L)), hs(size_t(L));
+    std::vector<DevBuf<unsigned long long>> h(static_cast<size_t>(L)), hs(static_cast<size_t>(L));
     std::vector<const uint64_t*> hin;
     std::vector<uint64_t*> hout;
     for (int l = 0; l < L; ++l) {
@@ -274,7 +280,7 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
     }
   }
   // sort locally, find every destination's run, exchange the runs
-  std::vector<std::vector<uint64_t>> send_offs(size_t(L)), send_counts(size_t(L));
+  std::vector<std::vector<uint64_t>> send_offs(static_cast<size_t>(L)), send_counts(static_cast<size_t>(L));
   for (int l = 0; l < L; ++l) {
     c.set(l);
     cudaStream_t s = c.st[size_t(l)];
@@ -293,9 +299,9 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
   }
   // (local mode: exchange_counts is a transpose; nccl: a count all-gather)
   const auto recv_counts = c.exchange_counts(send_counts);
-  std::vector<DevBuf<uint64_t>> recv(size_t(L));
-  std::vector<std::vector<uint64_t>> recv_offs(size_t(L));
-  std::vector<uint64_t> mr(size_t(L));
+  std::vector<DevBuf<uint64_t>> recv(static_cast<size_t>(L));
+  std::vector<std::vector<uint64_t>> recv_offs(static_cast<size_t>(L));
+  std::vector<uint64_t> mr(static_cast<size_t>(L));
   std::vector<const uint8_t*> sp;
   std::vector<uint8_t*> rp;
   for (int l = 0; l < L; ++l) {
@@ -319,7 +325,7 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
   }
   // owners: sort, check / remove duplicates, build the rows
   std::vector<uint64_t> bad(size_t(L), 0);
-  std::vector<std::string> msg(size_t(L));
+  std::vector<std::string> msg(static_cast<size_t>(L));
   for (int l = 0; l < L; ++l) {
     c.set(l);
     cudaStream_t s = c.st[size_t(l)];
@@ -371,8 +377,8 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
 // CSR(G) rows of the owned vertices from everybody's CSR(G^T) rows.
 void build_forward(DGraph& g, unsigned nb) {
   Comm& c = *g.comm;
-  std::vector<DevBuf<uint64_t>> keys(size_t(c.L));
-  std::vector<uint64_t> m(size_t(c.L));
+  std::vector<DevBuf<uint64_t>> keys(static_cast<size_t>(c.L));
+  std::vector<uint64_t> m(static_cast<size_t>(c.L));
   for (int l = 0; l < c.L; ++l) {
     c.set(l);
     cudaStream_t s = c.st[size_t(l)];
@@ -392,7 +398,7 @@ void build_forward(DGraph& g, unsigned nb) {
 void finish_directed(DGraph& g) {
   Comm& c = *g.comm;
   const uint64_t n = g.n;
-  std::vector<DevBuf<uint32_t>> deg(size_t(c.L)), degs(size_t(c.L));
+  std::vector<DevBuf<uint32_t>> deg(static_cast<size_t>(c.L)), degs(static_cast<size_t>(c.L));
   std::vector<const uint64_t*> din;
   std::vector<uint64_t*> dout;
   // u32 counts travel as u64 pairs: the sum of two shards' u32 never carries
@@ -430,6 +436,10 @@ void finish_directed(DGraph& g) {
     launch(sh.in.nnz, s, [&](unsigned gr, unsigned bl) {
       k_remap_cols<<<gr, bl, 0, s>>>(sh.in.idx.get(), sh.in.nnz, pmap.get());
     });
+    sh.pid.alloc(sh.hi - sh.lo + 1, s);
+    launch(sh.hi - sh.lo, s, [&](unsigned gr, unsigned bl) {
+      k_block_pids<<<gr, bl, 0, s>>>(od, pmap.get(), sh.lo, sh.hi - sh.lo, sh.pid.get());
+    });
     uint64_t nz = 0;
     GM_CUDA(cudaMemcpyAsync(&nz, pmap.get() + n, 8, cudaMemcpyDeviceToHost, s));
     GM_CUDA(cudaStreamSynchronize(s));
@@ -458,6 +468,7 @@ DGraph::~DGraph() {
     s.out.idx.reset();
     s.out.val.reset();
     s.outdeg.reset();
+    s.pid.reset();
     cudaStreamSynchronize(comm->st[size_t(l)]);
   }
 }
@@ -468,7 +479,8 @@ uint64_t DGraph::owner(uint64_t v) const {
 
 uint64_t DGraph::device_bytes(int l) const {
   const DShard& s = sh[size_t(l)];
-  uint64_t b = s.in.ptr.bytes() + s.in.idx.bytes() + s.in.val.bytes() + s.outdeg.bytes();
+  uint64_t b = s.in.ptr.bytes() + s.in.idx.bytes() + s.in.val.bytes() + s.outdeg.bytes() +
+               s.pid.bytes();
   if (!s.out_alias) b += s.out.ptr.bytes() + s.out.idx.bytes() + s.out.val.bytes();
   return b;
 }
@@ -481,7 +493,7 @@ DGraph* new_dgraph(Comm* c, uint64_t n, uint32_t flags) {
   g->n = n;
   g->flags = flags;
   g->symmetric = (flags & GM_SYMMETRIZE) != 0;
-  g->sh.resize(size_t(c->L));
+  g->sh.resize(static_cast<size_t>(c->L));
   for (int l = 0; l < c->L; ++l) g->sh[size_t(l)].l = l;
   return g.release();
 }
@@ -540,8 +552,8 @@ DGraph* dgraph_generate_rmat(Comm* c, uint32_t scale, uint32_t ef, double a, dou
   const uint64_t count = uint64_t(ef) << scale;
   const unsigned nb = scale;
   const int sym = g->symmetric ? 1 : 0;
-  std::vector<DevBuf<uint64_t>> keys(size_t(c->L));
-  std::vector<uint64_t> m(size_t(c->L));
+  std::vector<DevBuf<uint64_t>> keys(static_cast<size_t>(c->L));
+  std::vector<uint64_t> m(static_cast<size_t>(c->L));
   for (int l = 0; l < c->L; ++l) {
     c->set(l);
     cudaStream_t s = c->st[size_t(l)];
@@ -569,15 +581,14 @@ DGraph* dgraph_create(Comm* c, const gm_edge_list& e, uint64_t n, uint32_t flags
   if (flags & (GM_DAGIFY | GM_BIPARTITE_CHECK))
     fail(GM_EUSAGE, "dgraph: DAGIFY / BIPARTITE_CHECK are single-GPU ingest modes");
   if (n == 0 || n > (uint64_t(1) << 32)) fail(GM_EUSAGE, "dgraph: 1 <= n <= 2^32");
-  if (c->L != 1 && e.count)
-    fail(GM_EUSAGE, "dgraph: a local comm takes the edges from gm_dgraph_create_local");
   std::unique_ptr<DGraph> g(new_dgraph(c, n, flags | ((flags & GM_SYMMETRIZE) ? GM_PREPROCESS : 0)));
   const bool pre = (g->flags & GM_PREPROCESS) != 0;
   const unsigned nb = bits_for(n);
   const int sym = g->symmetric ? 1 : 0;
-  std::vector<DevBuf<uint64_t>> keys(size_t(c->L));
-  std::vector<uint64_t> m(size_t(c->L));
+  std::vector<DevBuf<uint64_t>> keys(static_cast<size_t>(c->L));
+  std::vector<uint64_t> m(static_cast<size_t>(c->L));
   std::vector<uint64_t> bad(size_t(c->L), 0);
+  std::string msg;
   for (int l = 0; l < c->L; ++l) {
     c->set(l);
     cudaStream_t s = c->st[size_t(l)];
@@ -599,10 +610,11 @@ DGraph* dgraph_create(Comm* c, const gm_edge_list& e, uint64_t n, uint32_t flags
     for (uint64_t i = 0; i < cnt && !bad[size_t(l)]; ++i)
       if (hs[i] >= n || hd[i] >= n) {
         bad[size_t(l)] = 1;
-        fail(GM_EINPUT, "build_graph: edge " + std::to_string(uint64_t(hs[i]) + 1) + " -> " +
-                            std::to_string(uint64_t(hd[i]) + 1) + " (1-based) exceeds vertex count " +
-                            std::to_string(n));
+        msg = "build_graph: edge " + std::to_string(uint64_t(hs[i]) + 1) + " -> " +
+              std::to_string(uint64_t(hd[i]) + 1) + " (1-based) exceeds vertex count " +
+              std::to_string(n);
       }
+    if (bad[size_t(l)]) continue;
     keys[size_t(l)].alloc(cnt * (sym ? 2 : 1) + 1, s);
     DevBuf<unsigned long long> k(1, s);
     k.zero(s);
@@ -621,6 +633,9 @@ DGraph* dgraph_create(Comm* c, const gm_edge_list& e, uint64_t n, uint32_t flags
       m[size_t(l)] = cnt;
     }
   }
+  // every rank learns whether any rank's input was bad before a collective
+  if (c->sum_host(bad)) fail(GM_EINPUT, msg.empty() ? "build_graph: an edge on another rank exceeds "
+                                                      "the vertex count" : msg);
   route_and_build(*g, keys, m, nb, false, /*check_dups=*/!pre);
   finish_build(*g, nb, GM_VAL_NONE, 0);
   return g.release();
@@ -782,12 +797,12 @@ DBfsState& dbfs_state(DGraph& g) {
                                                            [](DBfsState* p) { delete p; });
   DBfsState& st = *g.bfs;
   const int L = c.L;
-  st.level.resize(size_t(L));
-  st.vis.resize(size_t(L));
-  st.nxt.resize(size_t(L));
-  st.queue.resize(size_t(L));
-  st.ctr.resize(size_t(L));
-  st.sum.resize(size_t(L));
+  st.level.resize(static_cast<size_t>(L));
+  st.vis.resize(static_cast<size_t>(L));
+  st.nxt.resize(static_cast<size_t>(L));
+  st.queue.resize(static_cast<size_t>(L));
+  st.ctr.resize(static_cast<size_t>(L));
+  st.sum.resize(static_cast<size_t>(L));
   const uint64_t words_all = (g.n + 31) / 32;
   for (int l = 0; l < L; ++l) {
     c.set(l);
@@ -1003,6 +1018,372 @@ std::vector<gm_iteration_stats> dbfs(DGraph& g, uint64_t root, int64_t max_iters
   for (int l = 0; l < L; ++l) {
     c.set(l);
     GM_CUDA(cudaStreamSynchronize(c.st[size_t(l)]));
+  }
+  return stats;
+}
+
+
+// ============================================================================
+// PageRank over the row shards (BASELINE configs[4]; the program of
+// pagerank.hpp:36-63 driven like the CF driver, collaborative_filtering.hpp:
+// 181-193 -- the same formula as gm_pagerank).
+//
+// Superstep t on shard r: every owned row v folds x_t over its in-entries in
+// ascending caller-id order (a thread per row up to kPrShort entries; longer
+// rows in fixed chunks of kPrChunk entries, a warp per chunk with a fixed
+// shuffle tree, the chunks folded in order) -- the reduction tree depends only
+// on the row, so ranks are bitwise identical for any number of shards.
+// rank_{t+1}(v) = base_t + d * sum; a vertex with out-edges stores its message
+// rank/outdeg at its packed id into EVERY shard's x_{t+1} (peer stores: the
+// all-gather fused into the epilogue); a dangling vertex adds its rank to the
+// dangling mass as a 63-bit fixed-point integer split in two 32-bit limbs, so
+// the sum over shards is exact and order-free.  One u64 all-reduce of
+// {limb0, limb1, updated} per superstep is the barrier; base_{t+1} =
+// (1-d)/N + d*D/N is computed on the device from it.  No host synchronisation
+// inside the 20 supersteps.
+// ============================================================================
+namespace {
+
+constexpr uint32_t kPrShort = 32;
+constexpr uint64_t kPrChunk = 4096;
+
+struct DPrArgs {
+  const uint64_t* ptr;
+  const uint32_t* idx;
+  const uint32_t* pid;
+  const float* inv;
+  const float* x;                 // x_t (packed, local copy)
+  float* rank;
+  PeerTab<float> xn;              // x_{t+1} of every shard
+  int P;
+  const unsigned long long* sum;  // summed {limb0, limb1, updated} of rank_t
+  unsigned long long* part;       // this shard's words for rank_{t+1}
+  double one_minus_d_over_n, d_over_n;
+  float d;
+};
+
+__device__ __forceinline__ float dpr_base(const DPrArgs& a) {
+  const double D = (double(a.sum[1]) * 4294967296.0 + double(a.sum[0])) * 0x1p-63;
+  return float(a.one_minus_d_over_n + a.d_over_n * D);
+}
+
+struct DprAcc {
+  unsigned long long l0 = 0, l1 = 0, upd = 0;
+};
+
+__device__ __forceinline__ void dpr_apply(const DPrArgs& a, uint32_t r, float sum, float base,
+                                          bool has_in, DprAcc& acc) {
+  const float nr = base + a.d * sum;
+  const float old = a.rank[r];
+  acc.upd += has_in && __float_as_uint(nr) != __float_as_uint(old);
+  a.rank[r] = nr;
+  const uint32_t p = a.pid[r];
+  if (p != ~0u) {
+    const float xv = nr * a.inv[r];
+    for (int q = 0; q < a.P; ++q) a.xn.p[q][p] = xv;
+  } else {
+    const unsigned long long f = __float2ull_rz(nr * 9.223372036854775808e18f);
+    acc.l0 += f & 0xFFFFFFFFull;
+    acc.l1 += f >> 32;
+  }
+}
+
+__device__ __forceinline__ void dpr_flush(const DPrArgs& a, const DprAcc& acc) {
+  warp_add_u64(&a.part[0], acc.l0);
+  warp_add_u64(&a.part[1], acc.l1);
+  warp_add_u64(&a.part[2], acc.upd);
+}
+
+__global__ void __launch_bounds__(256) k_dpr_short(DPrArgs a, const uint32_t* rows, uint64_t nr) {
+  const float base = dpr_base(a);
+  DprAcc acc;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nr;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = rows[i];
+    const uint64_t b = a.ptr[r], e = a.ptr[r + 1];
+    float s = 0.0f;
+    for (uint64_t k = b; k < e; ++k) s += __ldg(&a.x[__ldg(&a.idx[k])]);
+    dpr_apply(a, r, s, base, e > b, acc);
+  }
+  dpr_flush(a, acc);
+}
+
+// warp per chunk of a long row: lane-strided partials, fixed xor tree
+__global__ void __launch_bounds__(256) k_dpr_chunks(DPrArgs a, const uint64_t* beg, uint64_t nc,
+                                                    const uint64_t* row_end_of_chunk, float* out) {
+  const uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  for (uint64_t c = w; c < nc; c += nw) {
+    const uint64_t b = beg[c], e = row_end_of_chunk[c];
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    uint64_t k = b + lane;
+    for (; k + 96 < e; k += 128) {
+      const uint32_t i0 = __ldg(&a.idx[k]), i1 = __ldg(&a.idx[k + 32]);
+      const uint32_t i2 = __ldg(&a.idx[k + 64]), i3 = __ldg(&a.idx[k + 96]);
+      s0 += __ldg(&a.x[i0]);
+      s1 += __ldg(&a.x[i1]);
+      s2 += __ldg(&a.x[i2]);
+      s3 += __ldg(&a.x[i3]);
+    }
+    for (; k < e; k += 32) s0 += __ldg(&a.x[__ldg(&a.idx[k])]);
+    float s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[c] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dpr_long(DPrArgs a, const uint32_t* rows, uint64_t nr,
+                                                  const uint32_t* chunk0, const float* csum) {
+  const float base = dpr_base(a);
+  DprAcc acc;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nr;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    float s = 0.0f;
+    for (uint32_t c = chunk0[i]; c < chunk0[i + 1]; ++c) s += csum[c];
+    dpr_apply(a, rows[i], s, base, true, acc);
+  }
+  dpr_flush(a, acc);
+}
+
+__global__ void k_dpr_init(uint64_t rows, float r0, const uint32_t* pid, const float* inv,
+                           float* rank, PeerTab<float> x0, int P, unsigned long long* part) {
+  DprAcc acc;
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    rank[r] = r0;
+    const uint32_t p = pid[r];
+    if (p != ~0u) {
+      const float xv = r0 * inv[r];
+      for (int q = 0; q < P; ++q) x0.p[q][p] = xv;
+    } else {
+      const unsigned long long f = __float2ull_rz(r0 * 9.223372036854775808e18f);
+      acc.l0 += f & 0xFFFFFFFFull;
+      acc.l1 += f >> 32;
+    }
+  }
+  warp_add_u64(&part[0], acc.l0);
+  warp_add_u64(&part[1], acc.l1);
+}
+
+__global__ void k_dpr_classify(const uint64_t* ptr, uint64_t rows, const uint32_t* od, float* inv,
+                               uint32_t* rs, uint32_t* rl, uint32_t* nchunks,
+                               unsigned long long* cnt) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    inv[r] = od[r] ? 1.0f / float(od[r]) : 0.0f;
+    const uint64_t d = ptr[r + 1] - ptr[r];
+    if (d <= kPrShort) {
+      rs[atomicAdd(&cnt[0], 1ull)] = uint32_t(r);
+    } else {
+      const unsigned long long i = atomicAdd(&cnt[1], 1ull);
+      rl[i] = uint32_t(r);
+      nchunks[i] = uint32_t((d + kPrChunk - 1) / kPrChunk);
+    }
+  }
+}
+
+__global__ void k_dpr_chunk_ranges(const uint64_t* ptr, const uint32_t* rl, uint64_t nl,
+                                   const uint64_t* c0, uint64_t* beg, uint64_t* end,
+                                   uint32_t* chunk0) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i <= nl;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    chunk0[i] = uint32_t(c0[i]);
+    if (i == nl) continue;
+    const uint32_t r = rl[i];
+    const uint64_t b = ptr[r], e = ptr[r + 1];
+    uint64_t c = c0[i];
+    for (uint64_t k = b; k < e; k += kPrChunk, ++c) {
+      beg[c] = k;
+      end[c] = k + kPrChunk < e ? k + kPrChunk : e;
+    }
+  }
+}
+
+DPrState& dpr_state(DGraph& g) {
+  if (g.pr) return *g.pr;
+  Comm& c = *g.comm;
+  g.pr = std::unique_ptr<DPrState, void (*)(DPrState*)>(new DPrState(), [](DPrState* p) { delete p; });
+  DPrState& st = *g.pr;
+  const int L = c.L;
+  for (auto* v : {&st.rank, &st.inv}) v->resize(static_cast<size_t>(L));
+  st.rows_short.resize(static_cast<size_t>(L));
+  st.rows_long.resize(static_cast<size_t>(L));
+  st.chunk_beg.resize(static_cast<size_t>(L));
+  st.long_chunk0.resize(static_cast<size_t>(L));
+  st.chunk_sum.resize(static_cast<size_t>(L));
+  st.part.resize(static_cast<size_t>(L));
+  st.sum.resize(static_cast<size_t>(L));
+  st.n_short.assign(size_t(L), 0);
+  st.n_long.assign(size_t(L), 0);
+  st.n_chunks.assign(size_t(L), 0);
+  const uint64_t nx = std::max<uint64_t>(g.nonzero_outdeg, 1);
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    const uint64_t rows = sh.hi - sh.lo;
+    st.rank[size_t(l)].alloc(rows + 1, s);
+    st.inv[size_t(l)].alloc(rows + 1, s);
+    st.rows_short[size_t(l)].alloc(rows + 1, s);
+    st.rows_long[size_t(l)].alloc(rows + 1, s);
+    DevBuf<uint32_t> nch(rows + 1, s);
+    DevBuf<unsigned long long> cnt(2, s);
+    cnt.zero(s);
+    launch(rows, s, [&](unsigned gr, unsigned bl) {
+      k_dpr_classify<<<gr, bl, 0, s>>>(sh.in.ptr.get(), rows, sh.outdeg.get(), st.inv[size_t(l)].get(),
+                                       st.rows_short[size_t(l)].get(), st.rows_long[size_t(l)].get(),
+                                       nch.get(), cnt.get());
+    });
+    unsigned long long hc[2];
+    GM_CUDA(cudaMemcpyAsync(hc, cnt.get(), 16, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    st.n_short[size_t(l)] = hc[0];
+    const uint64_t nl = hc[1];
+    st.n_long[size_t(l)] = nl;
+    DevBuf<uint64_t> c0(nl + 1, s);
+    scan_counts_to_ptr(nch.get(), c0.get(), nl, s);
+    uint64_t nc = 0;
+    GM_CUDA(cudaMemcpyAsync(&nc, c0.get() + nl, 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    st.n_chunks[size_t(l)] = nc;
+    st.chunk_beg[size_t(l)].alloc(2 * nc + 2, s);  // [beg | end]
+    st.long_chunk0[size_t(l)].alloc(nl + 1, s);
+    st.chunk_sum[size_t(l)].alloc(nc + 1, s);
+    launch(nl + 1, s, [&](unsigned gr, unsigned bl) {
+      k_dpr_chunk_ranges<<<gr, bl, 0, s>>>(sh.in.ptr.get(), st.rows_long[size_t(l)].get(), nl,
+                                           c0.get(), st.chunk_beg[size_t(l)].get(),
+                                           st.chunk_beg[size_t(l)].get() + nc + 1,
+                                           st.long_chunk0[size_t(l)].get());
+    });
+    st.part[size_t(l)].alloc(8, s);
+    st.sum[size_t(l)].alloc(8, s);
+    for (int b = 0; b < 2; ++b) st.x[b].push_back(c.peer_alloc(l, nx * 4));
+    GM_CUDA(cudaStreamSynchronize(s));
+  }
+  st.c = &c;
+  for (int b = 0; b < 2; ++b) st.x_tab[b] = c.share(st.x[b]);
+  return st;
+}
+
+}  // namespace
+
+std::vector<gm_iteration_stats> dpagerank(DGraph& g, double damping, int64_t iters, float* out,
+                                          bool out_on_device) {
+  Comm& c = *g.comm;
+  if (g.symmetric) fail(GM_EUSAGE, "dgraph pagerank: needs a directed graph");
+  if (!(damping >= 0.0 && damping <= 1.0)) fail(GM_EINPUT, "pagerank: damping must be in [0, 1]");
+  DPrState& st = dpr_state(g);
+  const int L = c.L, P = c.P;
+  const uint64_t n = g.n;
+  const int64_t ni = std::max<int64_t>(iters, 0);
+  c.set(0);
+  st.trace.alloc(size_t(ni + 1) * 4, c.st[0]);
+  std::vector<const uint64_t*> pin[2];
+  std::vector<uint64_t*> pout[2];
+  for (int b = 0; b < 2; ++b)
+    for (int l = 0; l < L; ++l) {
+      pin[b].push_back(reinterpret_cast<const uint64_t*>(st.part[size_t(l)].get() + 4 * b));
+      pout[b].push_back(reinterpret_cast<uint64_t*>(st.sum[size_t(l)].get() + 4 * b));
+    }
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    const uint64_t rows = sh.hi - sh.lo;
+    st.part[size_t(l)].zero(s);
+    launch(rows, s, [&](unsigned gr, unsigned bl) {
+      k_dpr_init<<<gr, bl, 0, s>>>(rows, float(1.0 / double(n)), sh.pid.get(), st.inv[size_t(l)].get(),
+                                   st.rank[size_t(l)].get(), tab_of<float>(st.x_tab[0][size_t(l)], P),
+                                   P, st.part[size_t(l)].get());
+    });
+  }
+  c.allreduce_u64(pin[0], pout[0], 4);
+  std::vector<std::unique_ptr<StepTimer>> tms;
+  for (int64_t t = 0; t < ni; ++t) {
+    const int p = int(t & 1), q = p ^ 1;
+    tms.emplace_back(new StepTimer());
+    StepTimer& tm = *tms.back();
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      DShard& sh = g.sh[size_t(l)];
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[0], s));
+      GM_CUDA(cudaMemsetAsync(st.part[size_t(l)].get() + 4 * q, 0, 32, s));
+      DPrArgs a{};
+      a.ptr = sh.in.ptr.get();
+      a.idx = sh.in.idx.get();
+      a.pid = sh.pid.get();
+      a.inv = st.inv[size_t(l)].get();
+      a.x = static_cast<const float*>(st.x[p][size_t(l)]);
+      a.rank = st.rank[size_t(l)].get();
+      a.xn = tab_of<float>(st.x_tab[q][size_t(l)], P);
+      a.P = P;
+      a.sum = st.sum[size_t(l)].get() + 4 * p;
+      a.part = st.part[size_t(l)].get() + 4 * q;
+      a.one_minus_d_over_n = (1.0 - damping) / double(n);
+      a.d_over_n = damping / double(n);
+      a.d = float(damping);
+      const uint64_t nc = st.n_chunks[size_t(l)];
+      if (nc) {
+        k_dpr_chunks<<<grid_for(nc * 32, 256), 256, 0, s>>>(
+            a, st.chunk_beg[size_t(l)].get(), nc, st.chunk_beg[size_t(l)].get() + nc + 1,
+            st.chunk_sum[size_t(l)].get());
+        GM_LAUNCH_CHECK();
+      }
+      launch(st.n_short[size_t(l)], s, [&](unsigned gr, unsigned bl) {
+        k_dpr_short<<<gr, bl, 0, s>>>(a, st.rows_short[size_t(l)].get(), st.n_short[size_t(l)]);
+      });
+      launch(st.n_long[size_t(l)], s, [&](unsigned gr, unsigned bl) {
+        k_dpr_long<<<gr, bl, 0, s>>>(a, st.rows_long[size_t(l)].get(), st.n_long[size_t(l)],
+                                     st.long_chunk0[size_t(l)].get(), st.chunk_sum[size_t(l)].get());
+      });
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[1], s));
+    }
+    c.allreduce_u64(pin[q], pout[q], 4);
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(st.trace.get() + 4 * t, st.sum[0].get() + 4 * q, 32,
+                            cudaMemcpyDeviceToDevice, c.st[0]));
+    GM_CUDA(cudaEventRecord(tm.e[2], c.st[0]));
+  }
+  // ranks of the owned rows, concatenated in shard order
+  if (out) {
+    uint64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      const uint64_t rows = g.sh[size_t(l)].hi - g.sh[size_t(l)].lo;
+      if (rows)
+        GM_CUDA(cudaMemcpyAsync(out + off, st.rank[size_t(l)].get(), rows * 4,
+                                out_on_device ? cudaMemcpyDefault : cudaMemcpyDeviceToHost,
+                                c.st[size_t(l)]));
+      off += rows;
+    }
+  }
+  std::vector<unsigned long long> tr(size_t(ni + 1) * 4);
+  c.set(0);
+  if (ni)
+    GM_CUDA(cudaMemcpyAsync(tr.data(), st.trace.get(), size_t(ni) * 32, cudaMemcpyDeviceToHost, c.st[0]));
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    GM_CUDA(cudaStreamSynchronize(c.st[size_t(l)]));
+  }
+  std::vector<gm_iteration_stats> stats;
+  uint64_t nnz_local = 0;
+  for (auto& sh : g.sh) nnz_local += sh.in.nnz;
+  for (int64_t t = 0; t < ni; ++t) {
+    gm_iteration_stats s{};
+    s.iteration = t + 1;
+    s.active_before = int64_t(n);
+    s.messages_generated = int64_t(g.nonzero_outdeg);
+    s.vertices_updated = int64_t(tr[size_t(t) * 4 + 2]);
+    s.spmv_seconds = tms[size_t(t)]->ms(0, 1) * 1e-3;
+    s.total_seconds = tms[size_t(t)]->ms(0, 2) * 1e-3;
+    s.comm_seconds = std::max(0.0, s.total_seconds - s.spmv_seconds);
+    s.edges_processed = int64_t(nnz_local);
+    s.bytes_algorithmic = int64_t(4 * nnz_local + 8 * (n / uint64_t(P) + 1) + 16 * (n / uint64_t(P)));
+    s.direction = 0;
+    stats.push_back(s);
   }
   return stats;
 }

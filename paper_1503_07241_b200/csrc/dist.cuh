@@ -87,6 +87,7 @@ struct DShard {
   Csr out;               // rows [lo, hi) of CSR(G) (directed push / BOTH); aliases in if symmetric
   bool out_alias = false;
   DevBuf<uint32_t> outdeg;  // out-degree of the owned rows
+  DevBuf<uint32_t> pid;     // directed: packed id of each owned row (~0u: no out-edges)
   const Csr& fwd() const { return out_alias ? in : out; }
 };
 

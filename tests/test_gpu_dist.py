@@ -1,0 +1,167 @@
+"""GPU: multi-GPU behind the C ABI (gm_comm_* / gm_dgraph_*).
+
+The sharded graph keeps only each shard's rows; the superstep loop, the
+exchange (peer stores over NVLink / NCCL) and the termination test run inside
+the library.  This box has one GPU, so P shards run as virtual shards of a
+local communicator on device 0 (same code path as P GPUs: peer pointers,
+cross-stream barriers), and the NCCL communicator is exercised with one rank.
+Oracles: the C restatement (oracle/graphmat_oracle.c, pinned to the reference)
+and the single-GPU library path.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RMAT = dict(a=0.57, b=0.19, c=0.19)
+
+
+def _dist():
+    from paper_1503_07241_b200 import dist
+    return dist
+
+
+def _keys(st):
+    return [(s.iteration, s.active_before, s.messages_generated, s.vertices_updated) for s in st]
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_dgraph_bfs_matches_oracle(gm, orc, P):
+    D = _dist()
+    scale, n = 14, 1 << 14
+    comm = D.Comm.local([0] * P)
+    g = D.DGraph.rmat(comm, scale, 16, seed=3, symmetrize=True, **RMAT)
+    ref = gm.Graph.rmat(scale, 16, seed=3, symmetrize=True, relabel=False, **RMAT)
+    s, d, _ = ref.edges()
+    assert g.num_edges == len(s)
+    root = ref.pick_source(3)
+    lvl, st = g.bfs(root)
+    want, wst = orc.bfs(n, s, d, root, presorted=True)
+    assert np.array_equal(lvl, want)
+    # per-superstep IterationStats equal the reference's (active, updated)
+    assert _keys(st) == [tuple(w) for w in wst]
+    assert any(x.direction == "pull" for x in st) and any(x.direction == "push" for x in st)
+    # rows tile [0, n), 32-aligned, each shard stores only its rows
+    rows = g.rows()
+    assert rows[0][0] == 0 and rows[-1][1] == n
+    assert all(a % 32 == 0 for a, _ in rows)
+    assert sum(int(g.info(i).local_edges) for i in range(P)) == len(s)
+    g.close()
+    comm.close()
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_dgraph_pagerank_matches_oracle(gm, orc, P):
+    D = _dist()
+    scale, n = 14, 1 << 14
+    comm = D.Comm.local([0] * P)
+    g = D.DGraph.rmat(comm, scale, 16, seed=5, **RMAT)
+    ref = gm.Graph.rmat(scale, 16, seed=5, relabel=False, **RMAT)
+    s, d, _ = ref.edges()
+    assert g.num_edges == len(s)
+    r, st = g.pagerank(0.85, 20)
+    want, wst = orc.pagerank_norm(n, s, d, 0.85, 20)
+    err = float(np.abs(r.astype(np.float64) - want).sum() / np.abs(want).sum())
+    assert err <= 1e-5, err
+    assert [x.active_before for x in st] == [t[1] for t in wst]
+    assert [x.messages_generated for x in st] == [t[2] for t in wst]
+    assert all(x.comm_seconds >= 0.0 for x in st)
+    g.close()
+    comm.close()
+
+
+def test_dgraph_bitwise_across_shard_counts_scale20(gm):
+    """Levels and fp32 ranks are bitwise identical for P = 1, 2, 4 at scale 20
+    (row folds depend only on the row; the dangling mass is an exact
+    fixed-point sum), and the per-shard graph shrinks ~1/P."""
+    D = _dist()
+    levels, ranks, bytes_ = [], [], []
+    root = None
+    for P in (1, 2, 4):
+        comm = D.Comm.local([0] * P)
+        gs = D.DGraph.rmat(comm, 20, 16, seed=1, symmetrize=True, **RMAT)
+        if root is None:
+            ref = gm.Graph.rmat(20, 16, seed=1, symmetrize=True, relabel=True, **RMAT)
+            root = ref.pick_source(1)
+            want, _ = gm.bfs(ref, root)
+            del ref
+        lv, _ = gs.bfs(root)
+        assert np.array_equal(lv, want)
+        levels.append(lv)
+        bytes_.append([int(gs.info(i).device_bytes) for i in range(P)])
+        gs.close()
+        gd = D.DGraph.rmat(comm, 20, 16, seed=1, **RMAT)
+        r, _ = gd.pagerank(0.85, 20)
+        ranks.append(r.view(np.uint32).copy())
+        gd.close()
+        comm.close()
+    assert all(np.array_equal(levels[0], x) for x in levels[1:])
+    assert all(np.array_equal(ranks[0], x) for x in ranks[1:])
+    one = bytes_[0][0]
+    for per in bytes_[1:]:
+        P = len(per)
+        assert max(per) < 1.25 * one / P, (one, per)
+
+
+def test_dgraph_pagerank_vs_single_gpu_scale20(gm, orc):
+    D = _dist()
+    comm = D.Comm.local([0, 0])
+    g = D.DGraph.rmat(comm, 20, 16, seed=2, **RMAT)
+    r, _ = g.pagerank(0.85, 20)
+    ref = gm.Graph.rmat(20, 16, seed=2, relabel=True, **RMAT)
+    s, d, _ = ref.edges()
+    want, _ = orc.pagerank_norm(1 << 20, s, d, 0.85, 20)
+    err = float(np.abs(r.astype(np.float64) - want).sum() / np.abs(want).sum())
+    assert err <= 1e-5, err
+
+
+def test_dgraph_create_errors_and_tiny_graphs(gm, orc):
+    D = _dist()
+    comm = D.Comm.local([0, 0])
+    # the reference's build_graph messages (dcsc.hpp:252-256, 148-150)
+    with pytest.raises(gm.InputError, match=r"edge 1 -> 9 \(1-based\) exceeds vertex count 4"):
+        D.DGraph.from_edges(comm, [0], [8], 4)
+    with pytest.raises(gm.InputError, match="duplicate edge 1 -> 2"):
+        D.DGraph.from_edges(comm, [0, 0], [1, 1], 4)
+    # path 0-1-2 plus an isolated vertex (test_algorithms.cpp:168-183)
+    g = D.DGraph.from_edges(comm, [0, 1], [1, 2], 4, symmetrize=True)
+    lvl, st = g.bfs(0)
+    assert list(lvl) == [0, 1, 2, -1]
+    lvl, _ = g.bfs(3)
+    assert list(lvl) == [-1, -1, -1, 0]
+    with pytest.raises(gm.InputError, match="source vertex 5"):
+        g.bfs(4)
+    g.close()
+    # PageRank hand trace {0->1, 0->2, 1->2} against the oracle
+    g = D.DGraph.from_edges(comm, [0, 0, 1], [1, 2, 2], 3)
+    r, _ = g.pagerank(0.85, 20)
+    want, _ = orc.pagerank_norm(3, np.array([0, 0, 1]), np.array([1, 2, 2]), 0.85, 20)
+    assert np.allclose(r, want, rtol=1e-6)
+    g.close()
+    comm.close()
+
+
+def test_nccl_communicator_one_rank(gm, orc):
+    """The NCCL path of the communicator (libnccl at run time, collectives on
+    the shard's stream, IPC-shared buffers) with one rank: results equal the
+    local communicator's bit for bit."""
+    D = _dist()
+    uid = D.Comm.nccl_unique_id()
+    cn = D.Comm.nccl(1, 0, 0, uid)
+    g = D.DGraph.rmat(cn, 14, 16, seed=3, symmetrize=True, **RMAT)
+    ref = gm.Graph.rmat(14, 16, seed=3, symmetrize=True, relabel=False, **RMAT)
+    root = ref.pick_source(3)
+    lvl, _ = g.bfs(root)
+    want, _ = gm.bfs(ref, root)
+    assert np.array_equal(lvl, want)
+    g.close()
+    gp = D.DGraph.rmat(cn, 14, 16, seed=5, **RMAT)
+    r1, _ = gp.pagerank(0.85, 20)
+    gp.close()
+    cl = D.Comm.local([0])
+    gl = D.DGraph.rmat(cl, 14, 16, seed=5, **RMAT)
+    r2, _ = gl.pagerank(0.85, 20)
+    assert np.array_equal(r1.view(np.uint32), r2.view(np.uint32))
+    gl.close()
+    cl.close()
+    cn.close()

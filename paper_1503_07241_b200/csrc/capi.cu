@@ -170,7 +170,7 @@ GM_API gm_status gm_comm_create_nccl(int32_t nranks, int32_t rank, int32_t devic
 }
 
 GM_API gm_status gm_comm_destroy(gm_comm_t c) {
-  return guarded([&] { delete reinterpret_cast<gm::Comm*>(c); });
+  return guarded([&] { gm::comm_release(reinterpret_cast<gm::Comm*>(c)); });
 }
 
 GM_API gm_status gm_dgraph_generate_rmat(gm_comm_t c, uint32_t scale, uint32_t edge_factor,

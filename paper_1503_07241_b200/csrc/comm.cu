@@ -38,10 +38,14 @@ const NcclApi& nccl_api() {
   static std::once_flag once;
   static std::string err;
   std::call_once(once, [] {
-    void* h = nullptr;
-    if (const char* p = getenv("GM_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // already in the process
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // The process's own copy first (e.g. torch's, so both share one NCCL),
+    // then GM_NCCL_LIB, then the system library.  RTLD_LOCAL: the symbols
+    // must not shadow another NCCL a later library binds to.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) {
+      if (const char* p = getenv("GM_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
       err = "libnccl.so.2 not found (set GM_NCCL_LIB)";
       return;
@@ -92,6 +96,12 @@ __global__ void k_sum_peers(PtrTab in, int P, size_t count, uint64_t* out) {
 }  // namespace
 
 void Comm::set(int l) const { GM_CUDA(cudaSetDevice(dev[size_t(l)])); }
+
+void comm_retain(Comm* c) { ++c->refs; }
+
+void comm_release(Comm* c) {
+  if (c && --c->refs == 0) delete c;
+}
 
 Comm::~Comm() {
   for (int l = 0; l < L; ++l) {

@@ -457,6 +457,10 @@ DGraph::~DGraph() {
   sssp.reset();
   cf.reset();
   if (!comm) return;
+  struct Release {  // the graph's reference on its communicator, dropped last
+    Comm* c;
+    ~Release() { comm_release(c); }
+  } rel{comm};
   for (int l = 0; l < comm->L && size_t(l) < sh.size(); ++l) {
     comm->set(l);
     cudaStreamSynchronize(comm->st[size_t(l)]);
@@ -489,6 +493,7 @@ namespace {
 
 DGraph* new_dgraph(Comm* c, uint64_t n, uint32_t flags) {
   std::unique_ptr<DGraph> g(new DGraph());
+  comm_retain(c);
   g->comm = c;
   g->n = n;
   g->flags = flags;
@@ -665,24 +670,25 @@ namespace {
 
 constexpr int kPush = 1, kPull = 0;
 
-__global__ void k_db_init(int32_t* level, uint64_t rows, uint32_t* vis, uint64_t words,
-                          uint64_t root_local, int owns_root, uint32_t* queue,
+__global__ void k_db_init(int32_t* level, uint64_t rows, uint32_t* vis, uint32_t* nxt,
+                          uint64_t words, uint64_t root_local, int owns_root, uint32_t* queue,
                           unsigned long long* ctr, const uint64_t* ptr) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < rows || i < words;
        i += uint64_t(gridDim.x) * blockDim.x) {
-    if (i < rows) level[i] = -1;
-    if (i < words) vis[i] = 0;
+    if (i < rows) level[i] = owns_root && i == root_local ? 0 : -1;
+    if (i < words) {
+      // nxt doubles as the frontier block a pull superstep publishes: the root
+      const bool rw = owns_root && i == (root_local >> 5);
+      vis[i] = rw ? 1u << (root_local & 31u) : 0u;
+      nxt[i] = vis[i];
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ctr[0] = owns_root ? 1 : 0;                                     // found
     ctr[1] = owns_root ? ptr[root_local + 1] - ptr[root_local] : 0;  // their edges
     ctr[2] = 0;                                                      // examined (pull)
     ctr[3] = owns_root ? 1 : 0;                                      // queue length
-    if (owns_root) {
-      level[root_local] = 0;
-      vis[root_local >> 5] |= 1u << (root_local & 31u);
-      queue[0] = uint32_t(root_local);
-    }
+    if (owns_root) queue[0] = uint32_t(root_local);
   }
 }
 
@@ -875,7 +881,8 @@ std::vector<gm_iteration_stats> dbfs(DGraph& g, uint64_t root, int64_t max_iters
     const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
     const int owns = uint64_t(c.global(l)) == ro;
     k_db_init<<<grid_for(std::max(rows, words) + 1, kBlock), kBlock, 0, s>>>(
-        st.level[size_t(l)].get(), rows, st.vis[size_t(l)].get(), words, owns ? root - sh.lo : 0,
+        st.level[size_t(l)].get(), rows, st.vis[size_t(l)].get(), st.nxt[size_t(l)].get(), words,
+        owns ? root - sh.lo : 0,
         owns, st.queue[size_t(l)].get(), st.ctr[size_t(l)].get(), sh.in.ptr.get());
     GM_LAUNCH_CHECK();
   }

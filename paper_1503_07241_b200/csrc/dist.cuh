@@ -73,7 +73,12 @@ struct Comm {
   void peer_free(int l, void* p);
   void set(int l) const;                  // cudaSetDevice(dev[l])
   int global(int l) const { return first + l; }
+  int refs = 1;  // the caller's handle + one per live DGraph
 };
+// gm_comm_destroy drops the caller's reference; graphs built on the
+// communicator hold theirs until they are destroyed.
+void comm_retain(Comm* c);
+void comm_release(Comm* c);
 
 Comm* comm_create_local(int ndev, const int* devices);
 Comm* comm_create_nccl(int nranks, int rank, int device, const void* id128);

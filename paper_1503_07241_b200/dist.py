@@ -23,6 +23,22 @@ from . import _lib as L
 from .api import _check, _stats, _stats_buf
 
 
+def _prefer_bundled_nccl():
+    """Point the library at the NCCL wheel torch ships (nvidia/nccl/lib), so a
+    process that also imports torch ends up with one NCCL, not two copies
+    under the same soname (the system one lacks symbols torch binds to)."""
+    import importlib.util
+    import os
+    if os.environ.get("GM_NCCL_LIB"):
+        return
+    spec = importlib.util.find_spec("nvidia.nccl") if importlib.util.find_spec("nvidia") else None
+    for loc in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(loc, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            os.environ["GM_NCCL_LIB"] = p
+            return
+
+
 class Comm:
     """gm_comm_t: P shards driven by one process (local) or one per process (NCCL)."""
 
@@ -38,6 +54,7 @@ class Comm:
 
     @staticmethod
     def nccl_unique_id() -> bytes:
+        _prefer_bundled_nccl()
         buf = C.create_string_buffer(128)
         _check(L.load().gm_comm_nccl_unique_id(buf))
         return buf.raw
@@ -46,6 +63,7 @@ class Comm:
     def nccl(cls, nranks: int, rank: int, device: int, uid: bytes):
         if len(uid) != 128:
             raise ValueError("the NCCL unique id is 128 bytes")
+        _prefer_bundled_nccl()
         h = C.c_void_p()
         buf = C.create_string_buffer(uid, 128)
         _check(L.load().gm_comm_create_nccl(nranks, rank, device, buf, C.byref(h)))

@@ -293,75 +293,78 @@ class BfsWorkload(Workload):
     def build(self, gm):
         a = self.args
         d = self.dist
-        shards = d.world if d is not None and d.world > 1 and a.scale >= self.SHARD_MIN_SCALE else 1
-        t0 = time.perf_counter()
-        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, symmetrize=True, relabel=True,
-                               shards=shards, **RMAT)
-        self.ingest_s = time.perf_counter() - t0
         self.n = 1 << a.scale
-        self.root = self.g.pick_source(a.seed)
-        self.sharded = shards > 1
+        self.sharded = (d is not None and d.world > 1 and self.shards_at(a.scale)) or a.sharded
+        import torch
+        t0 = time.perf_counter()
         if self.sharded:
-            from paper_1503_07241_b200.sharded import GpuBfsShardBackend, TorchExchange, row_block
-            lo, hi = row_block(self.n, d.world, d.rank)
-            self.backend = GpuBfsShardBackend(self.g, lo, hi)
-            self.exchange = TorchExchange()
-            self.root_int = int(self.g.permutation()[self.root])
+            # 1-D row shards behind the C ABI (gm_dgraph_*): every rank
+            # generates 1/P of the edges and keeps only its rows; the whole
+            # superstep loop and the exchange run inside the library (NCCL
+            # all-reduce of the counters + peer stores of the frontier)
+            from paper_1503_07241_b200 import dist as D
+            self.comm = nccl_comm(d)
+            self.g = D.DGraph.rmat(self.comm, a.scale, 16, seed=a.seed, symmetrize=True, **RMAT)
+            self.ingest_s = time.perf_counter() - t0
+            self.root = self.g.pick_source(a.seed)
+            lo, hi = self.g.rows()[0]
+            self.rows = hi - lo
             self.scaling = "strong"
             self.parallelism = f"rows{d.world}"
-            # frontier exchange as peer stores (CUDA IPC over NVLink);
-            # GM_BFS_EXCHANGE=nccl keeps the NCCL all-gather
-            self.fused, self.exchange_kind = None, "nccl all_gather"
-            if os.environ.get("GM_BFS_EXCHANGE", "fused") == "fused":
-                from paper_1503_07241_b200.sharded import FusedBfs
-                self.fused, err = agree_or_none(d, lambda: FusedBfs(self.backend, self.exchange))
-                self.exchange_kind = ("peer stores of the frontier blocks (CUDA IPC) + nccl all_reduce"
-                                      if self.fused else f"nccl all_gather (peer stores unavailable: {err})")
-        import torch
-        self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
-        self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
-        lvl, st = gm.bfs(self.g, self.root)
-        deg = self.g.degree_vector("out")
-        self.root_degree = int(deg[self.root])
-        # Graph500 TEPS: undirected edges inside the reached component.
-        self.edges = int(deg[lvl >= 0].sum()) // 2
-        del deg, lvl
+            lvl, st = self.g.bfs(self.root)
+            deg = self.g.degrees("out")
+            self.edges = int(round(d.sum(float(deg[lvl >= 0].sum())))) // 2
+            del deg, lvl
+            self.dev_out = torch.empty(max(self.rows, 1), dtype=torch.int32, device="cuda")
+            self.host_out = torch.empty(max(self.rows, 1), dtype=torch.int32).pin_memory()
+            info = self.g.info()
+            self.facts = {"m_directed": self.g.num_edges, "root": self.root, "teps_edges": self.edges,
+                          "rows": [lo, hi], "device_bytes_rank0": int(info.device_bytes),
+                          "exchange": "NCCL all-reduce of the superstep counters + peer stores of "
+                                      "the frontier blocks (CUDA IPC over NVLink)"}
+        else:
+            self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, symmetrize=True, relabel=True, **RMAT)
+            self.ingest_s = time.perf_counter() - t0
+            self.root = self.g.pick_source(a.seed)
+            self.dev_out = torch.empty(self.n, dtype=torch.int32, device="cuda")
+            self.host_out = torch.empty(self.n, dtype=torch.int32).pin_memory()
+            lvl, st = gm.bfs(self.g, self.root)
+            deg = self.g.degree_vector("out")
+            # Graph500 TEPS: undirected edges inside the reached component.
+            self.edges = int(deg[lvl >= 0].sum()) // 2
+            del deg, lvl
+            self.facts = {"m_directed": self.g.num_edges, "root": self.root, "teps_edges": self.edges,
+                          "device_bytes": self.g.info().device_bytes}
         self.stats = st
         self.config = self.describe(a.scale, a.seed)
-        self.facts = {"m_directed": self.g.num_edges, "root": self.root, "teps_edges": self.edges,
-                      "device_bytes": self.g.info().device_bytes,
-                      **({"exchange": self.exchange_kind} if self.sharded else {})}
 
     def run_device(self, gm):
         if self.sharded:
-            if self.fused is not None:
-                return self.fused.run(self.n, self.g.num_edges, self.root_int, self.root_degree)[0]
-            from paper_1503_07241_b200.sharded import sharded_bfs
-            return sharded_bfs(self.backend, self.exchange, self.n, self.g.num_edges, self.root_int,
-                               self.root_degree)[0]
+            return self.g.bfs(self.root, out_device_ptr=self.dev_out.data_ptr())
         gm.bfs(self.g, self.root, with_stats=False, out_device_ptr=self.dev_out.data_ptr(),
                     sync=False)
 
     def run_e2e(self, gm):
-        if self.sharded:  # this rank's block of levels comes back to the host
-            return self.run_device(gm)
         out = self.host_out.numpy()
+        if self.sharded:  # this rank's rows of the level vector come back to the host
+            self.g.bfs(self.root, out=out)
+            return out
         gm.bfs(self.g, self.root, with_stats=False, out=out)
         return out
 
     def e2e_bytes(self):
         if self.sharded:
-            return 0, (self.backend.hi - self.backend.lo) * 4
+            return 8, self.rows * 4
         return 8, self.n * 4
 
     def per_superstep(self, gm):
         if self.sharded:
-            return []
+            return self.g.bfs(self.root)[1]
         _, st = gm.bfs(self.g, self.root)
         return st
 
     def roofline(self, st, peak, peak_kind, ktime=None):
-        if not st:
+        if not st or self.sharded:
             return None
         # algorithmic bytes of one BFS = one k_bfs_coop launch (SURVEY 8d
         # formulas per superstep, summed); duration = the CUDA-event average
@@ -397,6 +400,18 @@ class BfsWorkload(Workload):
                           f"({m} stored entries, seed {self.args.seed}, graph build excluded){why}"}
 
 
+def nccl_comm(d):
+    """The library's NCCL communicator over the torchrun ranks: rank 0 makes
+    the unique id, torch.distributed broadcasts it (as NCCL applications do)."""
+    import torch.distributed as dist
+
+    from paper_1503_07241_b200 import dist as D
+    uid = [D.Comm.nccl_unique_id() if d.rank == 0 else None]
+    if d.world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    return D.Comm.nccl(d.world, d.rank, d.local, uid[0])
+
+
 def agree_or_none(d, make):
     """Construct an optional fast path on every rank or on none: a sum
     all-reduce of the failure flags decides, so ranks never run different
@@ -423,37 +438,37 @@ class PageRankWorkload(Workload):
         a = self.args
         d = self.dist
         t0 = time.perf_counter()
-        shards = d.world if d is not None and d.world > 1 else 1
-        self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, relabel=True, shards=shards, **RMAT)
-        self.ingest_s = time.perf_counter() - t0
         self.n = 1 << a.scale
         self.iters = 20
-        self.sharded = shards > 1
+        self.sharded = (d is not None and d.world > 1) or a.sharded
+        import torch
         if self.sharded:
-            # 1-D row sharding of G^T across the ranks (strong scaling: one graph)
-            from paper_1503_07241_b200.sharded import GpuShardBackend, TorchExchange, row_block
-            lo, hi = row_block(self.n, d.world, d.rank)
-            self.backend = GpuShardBackend(self.g, lo, hi)
-            self.exchange = TorchExchange()
+            # 1-D row shards of G^T behind the C ABI (strong scaling: one graph);
+            # the message all-gather is fused into the SpMV epilogue as peer
+            # stores, one NCCL all-reduce of the dangling mass per superstep
+            from paper_1503_07241_b200 import dist as D
+            self.comm = nccl_comm(d)
+            self.g = D.DGraph.rmat(self.comm, a.scale, 16, seed=a.seed, **RMAT)
+            lo, hi = self.g.rows()[0]
+            self.rows = hi - lo
             self.scaling = "strong"
             self.parallelism = f"rows{d.world}"
-            # the all-gather fused into the SpMV epilogue (CUDA IPC peer stores
-            # over NVLink); GM_PR_EXCHANGE=nccl keeps the NCCL all-gather
-            self.fused, self.exchange_kind = None, "nccl all_gather"
-            if os.environ.get("GM_PR_EXCHANGE", "fused") == "fused":
-                from paper_1503_07241_b200.sharded import FusedPageRank
-                self.fused, err = agree_or_none(
-                    d, lambda: FusedPageRank(self.backend, self.exchange, self.n))
-                self.exchange_kind = ("fused epilogue peer stores (CUDA IPC) + nccl all_reduce"
-                                      if self.fused else f"nccl all_gather (fused unavailable: {err})")
-        import torch
-        self.dev_out = torch.empty(self.n, dtype=torch.float32, device="cuda")
-        self.host_out = torch.empty(self.n, dtype=torch.float32).pin_memory()
+            out_len = max(self.rows, 1)
+            self.facts = {"m": self.g.num_edges, "rows": [lo, hi],
+                          "device_bytes_rank0": int(self.g.info().device_bytes),
+                          "exchange": "packed messages stored into every rank's vector by the SpMV "
+                                      "epilogue (CUDA IPC over NVLink) + NCCL all-reduce of the "
+                                      "dangling mass"}
+        else:
+            self.g = gm.Graph.rmat(a.scale, 16, seed=a.seed, relabel=True, **RMAT)
+            out_len = self.n
+            self.facts = {"m": self.g.num_edges, "device_bytes": self.g.info().device_bytes}
+        self.ingest_s = time.perf_counter() - t0
+        self.dev_out = torch.empty(out_len, dtype=torch.float32, device="cuda")
+        self.host_out = torch.empty(out_len, dtype=torch.float32).pin_memory()
         self.m = self.g.num_edges
         self.edges = self.m * self.iters
         self.config = self.describe(a.scale, a.seed)
-        self.facts = {"m": self.m, "device_bytes": self.g.info().device_bytes,
-                      **({"exchange": self.exchange_kind} if self.sharded else {})}
 
     @staticmethod
     def shards_at(scale):
@@ -469,33 +484,31 @@ class PageRankWorkload(Workload):
 
     def run_device(self, gm):
         if self.sharded:
-            if self.fused is not None:
-                return self.fused.run(0.85, self.iters)
-            from paper_1503_07241_b200.sharded import sharded_pagerank
-            return sharded_pagerank(self.backend, self.exchange, self.n, 0.85, self.iters)
+            return self.g.pagerank(0.85, self.iters, out_device_ptr=self.dev_out.data_ptr())
         gm.pagerank(self.g, 0.85, self.iters, with_stats=False,
                     out_device_ptr=self.dev_out.data_ptr(), sync=False)
 
     def run_e2e(self, gm):
-        if self.sharded:  # this rank's block comes back to the host
-            return self.run_device(gm)
         out = self.host_out.numpy()
+        if self.sharded:  # this rank's rows of the rank vector come back to the host
+            self.g.pagerank(0.85, self.iters, out=out)
+            return out
         gm.pagerank(self.g, 0.85, self.iters, with_stats=False, out=out)
         return out
 
     def e2e_bytes(self):
         if self.sharded:
-            return 8 * self.iters, (self.backend.hi - self.backend.lo) * 4
+            return 16, self.rows * 4
         return 16, self.n * 4
 
     def per_superstep(self, gm):
         if self.sharded:
-            return []
+            return self.g.pagerank(0.85, self.iters)[1]
         _, st = gm.pagerank(self.g, 0.85, self.iters)
         return st
 
     def roofline(self, st, peak, peak_kind, ktime=None):
-        if not st:
+        if not st or self.sharded:
             return None
         b = st[0].bytes_algorithmic  # per superstep = per SpMV launch
         kern = "k_pr_hub" if gm_pagerank_uses_hub(self.g) else "k_pr_spmv"
@@ -764,7 +777,7 @@ def parallelism_of(w_or_cls, world, scale=None):
     """single at N=1; rows{N} for a workload that shards (strong scaling);
     replicas{N} otherwise.  Both arms call this, so their configs match."""
     if world <= 1:
-        return "single"
+        return "rows1" if getattr(w_or_cls, "sharded", False) else "single"
     if isinstance(w_or_cls, Workload):
         return w_or_cls.parallelism if w_or_cls.parallelism != "replicas" else f"replicas{world}"
     shards = w_or_cls.shards_at(scale)
@@ -851,7 +864,8 @@ def run_ours(args, d: Dist):
     per = [{"it": s.iteration, "dir": s.direction, "active": s.active_before,
             "updated": s.vertices_updated, "edges": s.edges_processed,
             "us": round(s.spmv_seconds * 1e6, 2),
-            "gteps": round(s.edges_processed / s.spmv_seconds / 1e9, 3) if s.spmv_seconds else None}
+            "gteps": round(s.edges_processed / s.spmv_seconds / 1e9, 3) if s.spmv_seconds else None,
+            **({"comm_us": round(s.comm_seconds * 1e6, 2)} if getattr(w, "sharded", False) else {})}
            for s in st]
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": d.world,
@@ -979,6 +993,8 @@ def main():
     ap.add_argument("--scale", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-sharded path (gm_dgraph_*) even at N=1 (one NCCL rank)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

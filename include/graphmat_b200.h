@@ -492,6 +492,10 @@ GM_API gm_status gm_dgraph_create(gm_comm_t c, const gm_edge_list* edges, uint64
 GM_API gm_status gm_dgraph_destroy(gm_dgraph_t g);
 GM_API gm_status gm_dgraph_shard_info(gm_dgraph_t g, int32_t local_shard, gm_dshard_info* info);
 GM_API void* gm_dgraph_stream(gm_dgraph_t g, int32_t local_shard);
+/* gm_pick_source on the sharded graph (same vertex for the same graph). */
+GM_API gm_status gm_dgraph_pick_source(gm_dgraph_t g, uint64_t seed, uint64_t* out);
+/* degree_vector (engine.hpp:295-312) of a local shard's rows: kind 0 = IN, 1 = OUT. */
+GM_API gm_status gm_dgraph_degrees(gm_dgraph_t g, int32_t local_shard, int32_t kind, uint32_t* out);
 /* Outputs of the sharded programs: the owned rows of this process's shards,
  * concatenated in shard order -- the whole caller-order vector for a local
  * communicator, rows [row_begin, row_end) for an NCCL rank.  Stats are

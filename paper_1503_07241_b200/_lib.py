@@ -38,7 +38,8 @@ EXPORTED = [
     "gm_kernel_timer_start", "gm_kernel_timer_stop",
     "gm_comm_create_local", "gm_comm_nccl_unique_id", "gm_comm_create_nccl", "gm_comm_destroy",
     "gm_dgraph_generate_rmat", "gm_dgraph_create", "gm_dgraph_destroy", "gm_dgraph_shard_info",
-    "gm_dgraph_stream", "gm_dgraph_bfs", "gm_dgraph_pagerank",
+    "gm_dgraph_stream", "gm_dgraph_bfs", "gm_dgraph_pagerank", "gm_dgraph_pick_source",
+    "gm_dgraph_degrees",
 ]
 
 
@@ -195,6 +196,8 @@ def load(path: str = LIB_PATH):
         "gm_dgraph_destroy": (C.c_int, [vp]),
         "gm_dgraph_shard_info": (C.c_int, [vp, i32, C.POINTER(DShardInfo)]),
         "gm_dgraph_stream": (vp, [vp, i32]),
+        "gm_dgraph_pick_source": (C.c_int, [vp, u64, C.POINTER(u64)]),
+        "gm_dgraph_degrees": (C.c_int, [vp, i32, i32, vp]),
         "gm_dgraph_bfs": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),
         "gm_dgraph_pagerank": (C.c_int, [vp, C.POINTER(PageRankConfig), vp, i32, st, i64,
                                          C.POINTER(i64)]),

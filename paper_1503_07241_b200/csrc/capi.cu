@@ -222,6 +222,20 @@ GM_API void* gm_dgraph_stream(gm_dgraph_t g, int32_t local_shard) {
   return reinterpret_cast<void*>(d->comm->st[size_t(local_shard)]);
 }
 
+GM_API gm_status gm_dgraph_pick_source(gm_dgraph_t g, uint64_t seed, uint64_t* out) {
+  return guarded([&] {
+    if (!out) gm::fail(GM_EUSAGE, "null output");
+    *out = gm::dpick_source(*dgraph_of(g), seed);
+  });
+}
+
+GM_API gm_status gm_dgraph_degrees(gm_dgraph_t g, int32_t local_shard, int32_t kind, uint32_t* out) {
+  return guarded([&] {
+    if (!out) gm::fail(GM_EUSAGE, "null output");
+    gm::ddegrees(*dgraph_of(g), local_shard, kind, out);
+  });
+}
+
 GM_API gm_status gm_dgraph_bfs(gm_dgraph_t g, uint64_t root, int64_t max_iters, int32_t* out_level,
                                int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                                int64_t* n_stats) {

@@ -279,6 +279,12 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
       g.sh[size_t(l)].hi = g.bounds[size_t(c.global(l)) + 1];
     }
   }
+  std::vector<DevBuf<uint64_t>> recv(static_cast<size_t>(L));
+  std::vector<uint64_t> mr(static_cast<size_t>(L));
+  if (P == 1) {  // one shard: its keys are its rows (no sort + copy: scale 28 fits)
+    recv[0].swap(keys[0]);
+    mr[0] = m[0];
+  } else {
   // sort locally, find every destination's run, exchange the runs
   std::vector<std::vector<uint64_t>> send_offs(static_cast<size_t>(L)), send_counts(static_cast<size_t>(L));
   for (int l = 0; l < L; ++l) {
@@ -299,9 +305,7 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
   }
   // (local mode: exchange_counts is a transpose; nccl: a count all-gather)
   const auto recv_counts = c.exchange_counts(send_counts);
-  std::vector<DevBuf<uint64_t>> recv(static_cast<size_t>(L));
   std::vector<std::vector<uint64_t>> recv_offs(static_cast<size_t>(L));
-  std::vector<uint64_t> mr(static_cast<size_t>(L));
   std::vector<const uint8_t*> sp;
   std::vector<uint8_t*> rp;
   for (int l = 0; l < L; ++l) {
@@ -323,6 +327,7 @@ void route_and_build(DGraph& g, std::vector<DevBuf<uint64_t>>& keys, std::vector
     GM_CUDA(cudaStreamSynchronize(s));
     keys[size_t(l)].reset();
   }
+  }  // P > 1
   // owners: sort, check / remove duplicates, build the rows
   std::vector<uint64_t> bad(size_t(L), 0);
   std::vector<std::string> msg(static_cast<size_t>(L));
@@ -1393,6 +1398,135 @@ std::vector<gm_iteration_stats> dpagerank(DGraph& g, double damping, int64_t ite
     stats.push_back(s);
   }
   return stats;
+}
+
+}  // namespace gm
+
+// ---- seed-chosen source on a sharded graph (the rule of pick_source, ingest.cu:
+// the first of mix64(base + i) % n with out-edges; BASELINE configs[1..2]) ----
+namespace gm {
+namespace {
+
+__global__ void k_cand_deg(const uint64_t* ptr, const uint32_t* outdeg, uint64_t lo, uint64_t hi,
+                           uint64_t base, uint64_t n, uint64_t i0, int count,
+                           unsigned long long* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t v = mix64(base + i0 + uint64_t(i)) % n;
+  unsigned long long f = 0;
+  if (v >= lo && v < hi) {
+    const uint64_t r = v - lo;
+    f = outdeg ? outdeg[r] > 0 : ptr[r + 1] > ptr[r];
+  }
+  flag[i] = f;
+}
+
+__global__ void k_first_nonempty(const uint64_t* ptr, const uint32_t* outdeg, uint64_t rows,
+                                 uint64_t lo, unsigned long long* first) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x)
+    if (outdeg ? outdeg[r] > 0 : ptr[r + 1] > ptr[r]) atomicMin(first, (unsigned long long)(lo + r));
+}
+
+}  // namespace
+
+uint64_t dpick_source(DGraph& g, uint64_t seed) {
+  Comm& c = *g.comm;
+  const uint64_t n = g.n;
+  const uint64_t base = mix64(seed ^ 0x50C0FFEEull);
+  constexpr int kBatch = 1024;
+  std::vector<DevBuf<unsigned long long>> f(static_cast<size_t>(c.L)), fs(static_cast<size_t>(c.L));
+  std::vector<const uint64_t*> in;
+  std::vector<uint64_t*> out;
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    const DShard& sh = g.sh[size_t(l)];
+    f[size_t(l)].alloc(kBatch, s);
+    fs[size_t(l)].alloc(kBatch, s);
+    k_cand_deg<<<(kBatch + 255) / 256, 256, 0, s>>>(sh.in.ptr.get(), g.symmetric ? nullptr : sh.outdeg.get(),
+                                                    sh.lo, sh.hi, base, n, 0, kBatch, f[size_t(l)].get());
+    GM_LAUNCH_CHECK();
+    in.push_back(reinterpret_cast<const uint64_t*>(f[size_t(l)].get()));
+    out.push_back(reinterpret_cast<uint64_t*>(fs[size_t(l)].get()));
+  }
+  c.allreduce_u64(in, out, kBatch);
+  std::vector<unsigned long long> h(kBatch);
+  c.set(0);
+  GM_CUDA(cudaMemcpyAsync(h.data(), fs[0].get(), kBatch * 8, cudaMemcpyDeviceToHost, c.st[0]));
+  GM_CUDA(cudaStreamSynchronize(c.st[0]));
+  for (int i = 0; i < kBatch; ++i)
+    if (h[size_t(i)]) return mix64(base + uint64_t(i)) % n;
+  // no candidate hit: the smallest vertex with out-edges (min over shards)
+  std::vector<std::vector<uint64_t>> firsts(static_cast<size_t>(c.L));
+  std::vector<DevBuf<unsigned long long>> m1(static_cast<size_t>(c.L)), ms(static_cast<size_t>(c.L));
+  in.clear();
+  out.clear();
+  const size_t P = size_t(c.P);
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    const DShard& sh = g.sh[size_t(l)];
+    m1[size_t(l)].alloc(P, s);
+    ms[size_t(l)].alloc(P, s);
+    m1[size_t(l)].zero(s);
+    DevBuf<unsigned long long> first(1, s);
+    GM_CUDA(cudaMemsetAsync(first.get(), 0xFF, 8, s));
+    launch(sh.hi - sh.lo, s, [&](unsigned gr, unsigned bl) {
+      k_first_nonempty<<<gr, bl, 0, s>>>(sh.in.ptr.get(), g.symmetric ? nullptr : sh.outdeg.get(),
+                                         sh.hi - sh.lo, sh.lo, first.get());
+    });
+    unsigned long long v = 0;
+    GM_CUDA(cudaMemcpyAsync(&v, first.get(), 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    const unsigned long long enc = v == ~0ull ? 0 : v + 1;  // 0 = none
+    GM_CUDA(cudaMemcpyAsync(m1[size_t(l)].get() + c.global(l), &enc, 8, cudaMemcpyHostToDevice, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    in.push_back(reinterpret_cast<const uint64_t*>(m1[size_t(l)].get()));
+    out.push_back(reinterpret_cast<uint64_t*>(ms[size_t(l)].get()));
+  }
+  c.allreduce_u64(in, out, P);
+  std::vector<unsigned long long> hm(P);
+  c.set(0);
+  GM_CUDA(cudaMemcpyAsync(hm.data(), ms[0].get(), P * 8, cudaMemcpyDeviceToHost, c.st[0]));
+  GM_CUDA(cudaStreamSynchronize(c.st[0]));
+  for (size_t q = 0; q < P; ++q)
+    if (hm[q]) return hm[q] - 1;
+  return 0;
+}
+
+}  // namespace gm
+
+// degree_vector (engine.hpp:295-312) of the owned rows: kind 0 = IN (row
+// lengths of CSR(G^T)), 1 = OUT.
+namespace gm {
+namespace {
+__global__ void k_row_lengths(const uint64_t* ptr, uint64_t rows, uint32_t* out) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x)
+    out[r] = uint32_t(ptr[r + 1] - ptr[r]);
+}
+}  // namespace
+
+void ddegrees(DGraph& g, int l, int kind, uint32_t* out_host) {
+  Comm& c = *g.comm;
+  if (l < 0 || l >= c.L) fail(GM_EUSAGE, "bad shard");
+  if (kind != 0 && kind != 1) fail(GM_EUSAGE, "degree kind must be 0 (IN) or 1 (OUT)");
+  c.set(l);
+  cudaStream_t s = c.st[size_t(l)];
+  const DShard& sh = g.sh[size_t(l)];
+  const uint64_t rows = sh.hi - sh.lo;
+  if (!rows) return;
+  if (kind == 1 && !g.symmetric) {
+    GM_CUDA(cudaMemcpyAsync(out_host, sh.outdeg.get(), rows * 4, cudaMemcpyDeviceToHost, s));
+  } else {
+    DevBuf<uint32_t> d(rows, s);
+    launch(rows, s, [&](unsigned gr, unsigned bl) {
+      k_row_lengths<<<gr, bl, 0, s>>>(sh.in.ptr.get(), rows, d.get());
+    });
+    GM_CUDA(cudaMemcpyAsync(out_host, d.get(), rows * 4, cudaMemcpyDeviceToHost, s));
+  }
+  GM_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace gm

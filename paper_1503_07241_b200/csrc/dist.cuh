@@ -128,6 +128,9 @@ DGraph* dgraph_generate_bipartite(Comm* c, uint32_t users, uint32_t items, doubl
 DGraph* dgraph_create(Comm* c, const gm_edge_list& local_edges, uint64_t n, uint32_t flags,
                       int storage);
 
+uint64_t dpick_source(DGraph& g, uint64_t seed);
+void ddegrees(DGraph& g, int local_shard, int kind, uint32_t* out_host);
+
 // Drivers: the whole superstep loop in the library (counters stay on the
 // devices; one host read per superstep at most).  Outputs: the owned rows of
 // every local shard, concatenated in shard order (the full caller-order

@@ -155,6 +155,20 @@ class DGraph:
                                            C.byref(k)))
         return out, _stats(st, k.value)
 
+    def pick_source(self, seed: int) -> int:
+        """The seed-chosen vertex with out-edges (same rule as Graph.pick_source)."""
+        v = C.c_uint64()
+        _check(L.load().gm_dgraph_pick_source(self._h, seed, C.byref(v)))
+        return int(v.value)
+
+    def degrees(self, kind: str = "out", local_shard: int = 0):
+        """degree_vector (engine.hpp:295-312) of a local shard's rows."""
+        lo, hi = self.rows()[local_shard]
+        out = np.empty(hi - lo, np.uint32)
+        _check(L.load().gm_dgraph_degrees(self._h, local_shard, 1 if kind == "out" else 0,
+                                          out.ctypes.data))
+        return out
+
     def stream(self, local_shard: int = 0) -> int:
         return int(L.load().gm_dgraph_stream(self._h, local_shard) or 0)
 

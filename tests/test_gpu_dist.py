@@ -35,6 +35,7 @@ def test_dgraph_bfs_matches_oracle(gm, orc, P):
     s, d, _ = ref.edges()
     assert g.num_edges == len(s)
     root = ref.pick_source(3)
+    assert g.pick_source(3) == root
     lvl, st = g.bfs(root)
     want, wst = orc.bfs(n, s, d, root, presorted=True)
     assert np.array_equal(lvl, want)

@@ -93,7 +93,8 @@ struct TravCache {
   DevBuf<uint32_t> dq[2];       // SSSP message snapshots parallel to q
   DevBuf<uint32_t> defq;        // pull: deferred rows
   DevBuf<uint32_t> ul[2];       // pull: unvisited-row lists
-  DevBuf<uint4> head;           // pull: first kHead in-neighbours per row
+  DevBuf<uint32_t> hsoa;        // pull: in-neighbours 0..kSoa-1 of every row, slot-major
+  DevBuf<uint4> head;           // pull: in-neighbours kSoa..kHead-1 per row (AoS)
   DevBuf<uint64_t> qe[2];       // start-edge pointers parallel to q
   DevBuf<uint64_t> defe;        // pull: deferred rows' next unprobed edge
   unsigned coop_grid = 0;
@@ -381,7 +382,9 @@ struct CoopArgs {
   const uint32_t* out_idx;  // CSR(G): push
   const uint32_t* deg;      // out-degree
   const uint32_t* indeg;    // in-degree (pull row length)
-  const uint4* head;        // first kHead in-neighbours of each pull row
+  const uint32_t* hsoa;     // in-neighbour s of row v at hsoa[s * hstride + v], s < kSoa
+  const uint4* head;        // in-neighbours kSoa..kHead-1 of each pull row (16 B chunks)
+  uint64_t hstride;
   int32_t* level;
   uint32_t* vis;
   uint32_t* fb[2];
@@ -472,17 +475,31 @@ __device__ __forceinline__ uint32_t lane_gallop(const uint64_t* offs, uint32_t n
 #endif
 constexpr int kHead = GM_BFS_HEAD;  // multiple of 4
 constexpr int kHeadVec = kHead / 4;
+// The first kSoa in-neighbours of every pull row live slot-major (hsoa[s][v]):
+// a warp probing 32 consecutive rows' slot s reads one coalesced 128-byte line
+// (4 B per open row) instead of a 64-byte head line each.  Under the degree
+// relabel slot 0 is a row's highest-degree neighbour, which a large frontier
+// holds most of the time, so most rows cost 4 B.  The rest of the head
+// (slots kSoa..kHead-1) stays row-major for one-round 16-byte loads.
+constexpr int kSoa = 4;
+constexpr int kAosVec = kHeadVec - 1;  // 16-byte chunks after the slot-major part
 
-__global__ void k_build_head(const uint64_t* ptr, const uint32_t* idx, uint64_t nv, uint4* head) {
+__global__ void k_build_head(const uint64_t* ptr, const uint32_t* idx, uint64_t nv, uint64_t hstride,
+                             uint32_t* hsoa, uint4* head) {
   for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < nv;
        v += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t b = ptr[v], e = ptr[v + 1];
 #pragma unroll
-    for (int j = 0; j < kHeadVec; ++j) {
+    for (int k = 0; k < kSoa; ++k) hsoa[k * hstride + v] = b + k < e ? idx[b + k] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < kAosVec; ++j) {
       uint32_t h[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) h[k] = b + 4 * j + k < e ? idx[b + 4 * j + k] : 0xFFFFFFFFu;
-      head[kHeadVec * v + j] = make_uint4(h[0], h[1], h[2], h[3]);
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t t = b + kSoa + 4 * j + k;
+        h[k] = t < e ? idx[t] : 0xFFFFFFFFu;
+      }
+      head[kAosVec * v + j] = make_uint4(h[0], h[1], h[2], h[3]);
     }
   }
 }
@@ -564,39 +581,82 @@ __device__ __forceinline__ void coop_push(const CoopArgs& a, int cur, uint64_t n
   }
 }
 
-// Probe the first 4*hv in-neighbours of row v (hv 16-byte head loads, all in
-// one round); returns found, sets defer/rest for rows with more in-edges.
-// hv shrinks when the frontier is large: the first probe then almost always
-// hits and the rest of the head would be wasted bandwidth.
+// Probe the first 4*hv in-neighbours of row v.  Round 1 loads the slot-major
+// slots 0..3 (four coalesced 4-byte loads across the warp's rows) and their
+// four frontier words together; round 2 (hv > 1, no hit yet, the row goes on)
+// does the same for the row-major rest of the head.  All loads of a round are
+// independent -- the row's probes are not a chain of dependent loads -- and
+// `examined` still counts the probes a sequential scan would make (up to and
+// including the first hit).  Returns found; sets defer/rest for rows with more
+// in-edges.  hv is 1 when the frontier is large (the first probes then almost
+// always hit).
+__device__ __forceinline__ uint32_t probe_word(const uint32_t* s_fb, uint32_t s_words,
+                                               const uint32_t* fbc, uint32_t u) {
+  const uint32_t w = u >> 5;
+  return w < s_words ? s_fb[w] : __ldcg(&fbc[w]);
+}
+
 __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t* s_fb,
                                                uint32_t s_words, const uint32_t* fbc, uint64_t v,
                                                int hv, bool& defer, uint32_t& rest,
                                                unsigned long long& examined) {
-  uint32_t u[kHead];
-#pragma unroll
-  for (int j = 0; j < kHeadVec; ++j) {
-    uint4 h = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    if (j < hv) h = __ldg(&a.head[kHeadVec * v + j]);
-    u[4 * j] = h.x;
-    u[4 * j + 1] = h.y;
-    u[4 * j + 2] = h.z;
-    u[4 * j + 3] = h.w;
-  }
-  const uint32_t d = __ldg(&a.indeg[v]);
-  bool found = false;
-#pragma unroll
-  for (int k = 0; k < kHead; ++k) {
-    if (!found && u[k] != 0xFFFFFFFFu) {
+  defer = false;
+  rest = 0;
+  {
+    // hv == 1 (large frontier): slot 0 alone first -- under the degree relabel
+    // it is the row's largest neighbour and the frontier almost always holds it
+    const int k0 = hv == 1 ? 1 : 0;
+    if (k0) {
+      const uint32_t u0 = __ldg(&a.hsoa[v]);
+      if (u0 == 0xFFFFFFFFu) return false;
       ++examined;
-      const uint32_t w = u[k] >> 5;
-      const uint32_t word = w < s_words ? s_fb[w] : __ldcg(&fbc[w]);
-      found = (word >> (u[k] & 31u)) & 1u;
+      if ((probe_word(s_fb, s_words, fbc, u0) >> (u0 & 31u)) & 1u) return true;
+    }
+    uint32_t u[kSoa], hit = 0, valid = k0;
+#pragma unroll
+    for (int k = 0; k < kSoa; ++k) u[k] = k >= k0 ? __ldg(&a.hsoa[k * a.hstride + v]) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < kSoa; ++k) {
+      if (u[k] != 0xFFFFFFFFu) {
+        valid |= 1u << k;
+        hit |= ((probe_word(s_fb, s_words, fbc, u[k]) >> (u[k] & 31u)) & 1u) << k;
+      }
+    }
+    // slots fill from 0: the first invalid slot ends the row
+    if (hit) {
+      examined += __ffs(hit) - k0;  // a slot probed above is counted there
+      return true;
+    }
+    examined += __popc(valid) - k0;
+    if (valid != (1u << kSoa) - 1) return false;
+  }
+  if (hv > 1) {
+#pragma unroll
+    for (int j = 0; j < kAosVec; ++j) {
+      if (j >= hv - 1) break;
+      const uint4 h = __ldg(&a.head[kAosVec * v + j]);
+      const uint32_t u[4] = {h.x, h.y, h.z, h.w};
+      uint32_t hit = 0, valid = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (u[k] != 0xFFFFFFFFu) {
+          valid |= 1u << k;
+          hit |= ((probe_word(s_fb, s_words, fbc, u[k]) >> (u[k] & 31u)) & 1u) << k;
+        }
+      }
+      if (hit) {
+        examined += __ffs(hit);
+        return true;
+      }
+      examined += __popc(valid);
+      if (valid != 0xFu) return false;
     }
   }
+  const uint32_t d = __ldg(&a.indeg[v]);
   const uint32_t probed = 4u * uint32_t(hv);
-  defer = !found && d > probed;
+  defer = d > probed;
   rest = defer ? d - probed : 0u;
-  return found;
+  return false;
 }
 
 __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
@@ -631,9 +691,11 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         __shared__ unsigned long long s_wbase[kCoopThreads / 32];
         const uint64_t words = (a.n + 31) / 32;
         const unsigned wib = threadIdx.x >> 5;
+        // blocks of 32 consecutive words dealt round-robin over the warps:
+        // 128-byte loads, and every warp gets a statistically equal share
         unsigned long long mine = 0;  // (count << kCountShift) | edges of this lane's bits
-        for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
-          const uint64_t wl = gwarp + (k0 + lane) * nwarps;
+        for (uint64_t k0 = gwarp * 32; k0 < words; k0 += nwarps * 32) {
+          const uint64_t wl = k0 + lane;
           const uint32_t myword = wl < words ? __ldcg(&fbc[wl]) : 0u;
           unsigned nz = __ballot_sync(0xffffffffu, myword != 0u);
           while (nz) {
@@ -641,7 +703,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
             nz &= nz - 1;
             const uint32_t word = __shfl_sync(0xffffffffu, myword, j);
             if ((word >> lane) & 1u) {
-              const uint32_t v = uint32_t((gwarp + (k0 + j) * nwarps) * 32 + lane);
+              const uint32_t v = uint32_t((k0 + j) * 32 + lane);
               mine += (1ull << kCountShift) | (__ldg(&a.out_ptr[v + 1]) - __ldg(&a.out_ptr[v]));
             }
           }
@@ -663,8 +725,8 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         }
         __syncthreads();
         unsigned long long pos = s_wbase[wib];  // running (position, edge offset) of the warp
-        for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
-          const uint64_t wl = gwarp + (k0 + lane) * nwarps;
+        for (uint64_t k0 = gwarp * 32; k0 < words; k0 += nwarps * 32) {
+          const uint64_t wl = k0 + lane;
           const uint32_t myword = wl < words ? __ldcg(&fbc[wl]) : 0u;
           unsigned nz = __ballot_sync(0xffffffffu, myword != 0u);
           while (nz) {
@@ -672,7 +734,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
             nz &= nz - 1;
             const uint32_t word = __shfl_sync(0xffffffffu, myword, j);
             const bool set = (word >> lane) & 1u;
-            const uint32_t v = uint32_t((gwarp + (k0 + j) * nwarps) * 32 + lane);
+            const uint32_t v = uint32_t((k0 + j) * 32 + lane);
             uint64_t ps = 0, ed = 0;
             if (set) {
               ps = __ldg(&a.out_ptr[v]);
@@ -716,7 +778,9 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         const uint64_t words = (a.nv + 31) / 32;
         // Words are dealt round-robin (warp g owns g, g + nwarps, ...) so every
         // warp gets a statistically equal share; lanes prefetch the visited
-        // words of the warp's next 32 assignments in one load.
+        // words of the warp's next 32 assignments in one load.  (Dealing
+        // 32-word blocks instead -- coalesced visited loads -- left too few
+        // blocks per warp at scale 23: 291 -> 218 GTEPS.)
         for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
          const uint64_t wl = gwarp + (k0 + lane) * nwarps;
          const uint32_t myvis = wl < words ? __ldcg(&a.vis[wl]) : 0xFFFFFFFFu;
@@ -1308,9 +1372,11 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   const size_t smem = size_t(kSmemFbWords) * 4;
   if (!c.level) {
     c.level.alloc(n, s);
-    c.head.alloc(size_t(kHeadVec) * (nv + 1), s);
+    c.hsoa.alloc(size_t(kSoa) * (nv + 1), s);
+    c.head.alloc(size_t(kAosVec) * (nv + 1), s);
     if (nv) {
-      k_build_head<<<grid_for(nv, 256), 256, 0, s>>>(g.in.ptr.get(), g.in.idx.get(), nv, c.head.get());
+      k_build_head<<<grid_for(nv, 256), 256, 0, s>>>(g.in.ptr.get(), g.in.idx.get(), nv, nv + 1,
+                                                      c.hsoa.get(), c.head.get());
       GM_LAUNCH_CHECK();
     }
     GM_CUDA(cudaFuncSetAttribute(k_bfs_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1344,6 +1410,8 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   a.deg = g.outdeg.get();
   a.indeg = g.indeg.get();
   a.head = c.head.get();
+  a.hsoa = c.hsoa.get();
+  a.hstride = nv + 1;
   a.level = c.level.get();
   a.vis = c.vis.get();
   for (int i = 0; i < 2; ++i) {

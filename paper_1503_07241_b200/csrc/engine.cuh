@@ -141,6 +141,87 @@ __global__ void k_send(P p, uint64_t n, const typename P::vertex_t* props, const
   }
 }
 
+// Frontier-proportional superstep (SpMSpV push), engine.hpp:224-260 with the
+// columns that are not in x skipped (:234-236): only the valid messages'
+// out-edges are visited.  Exactly order-free programs (kExactReorder, no
+// failing callbacks, reduced_t of 4 or 8 bytes) fold each contribution into
+// y[k] with a compare-and-swap loop: y holds reduce_identity() wherever it is
+// not valid (set once, restored by apply), so the first contribution is
+// reduce(identity, r) as S4 requires and any interleaving gives the
+// sequential fold's bits.
+template <typename P>
+struct can_push
+    : std::bool_constant<exact_reorder<P>::value && !can_fail<P>::value &&
+                         (sizeof(typename P::reduced_t) == 4 || sizeof(typename P::reduced_t) == 8)> {};
+
+template <typename R, typename P>
+__device__ __forceinline__ void atomic_reduce(const P& p, R* addr, const R& r) {
+  using W = std::conditional_t<sizeof(R) == 8, unsigned long long, unsigned int>;
+  W* a = reinterpret_cast<W*>(addr);
+  W old = *reinterpret_cast<volatile W*>(a);
+  for (;;) {
+    R ov;
+    memcpy(&ov, &old, sizeof(R));
+    const R nv = p.reduce(ov, r);
+    W nb;
+    memcpy(&nb, &nv, sizeof(R));
+    if (nb == old) return;  // no change (e.g. min already smaller)
+    const W prev = atomicCAS(a, old, nb);
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
+// The valid messages as a queue with their out-degrees (for the push), built
+// from xbits after k_send.
+__global__ void k_msg_queue(uint64_t n, const uint32_t* xbits, const uint64_t* out_ptr,
+                            uint32_t* q, unsigned long long* ctr);
+
+// qoff[i] = out-edges of the queue's sources before i (exclusive, qoff[nq] = total):
+// the degrees, then an in-place exclusive scan (CUB) over nq + 1 entries
+__global__ void k_queue_degrees(const uint32_t* q, const unsigned long long* qn,
+                                const uint64_t* out_ptr, uint64_t* deg);
+void exclusive_scan_u64(uint64_t* data, uint64_t n, cudaStream_t s);
+
+// Edge-balanced: thread t handles the t-th frontier edge (its source found by
+// a binary search over the queue offsets), so a hub source's edges spread
+// over the whole grid instead of serialising one warp.
+template <typename P>
+__global__ void __launch_bounds__(256) k_push(P p, const uint32_t* q, const unsigned long long* qn,
+                                              const uint64_t* qoff, const uint64_t* ptr,
+                                              const uint32_t* idx, const uint8_t* val,
+                                              const typename P::message_t* x,
+                                              const typename P::vertex_t* props,
+                                              typename P::reduced_t* y, uint32_t* ybits) {
+  const uint64_t nq = qn[0], total = qn[1];
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t lo = 0, hi = nq;  // last i with qoff[i] <= t
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (qoff[mid] <= t)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    const uint32_t j = q[lo];
+    const uint64_t e = ptr[j] + (t - qoff[lo]);
+    const uint32_t k = idx[e];
+    const typename P::reduced_t r =
+        p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k]);
+    atomic_reduce(p, &y[k], r);
+    const uint32_t bit = 1u << (k & 31u);
+    if (!(ybits[k >> 5] & bit)) atomicOr(&ybits[k >> 5], bit);
+  }
+}
+
+template <typename P>
+__global__ void k_fill_identity(P p, uint64_t n, typename P::reduced_t* y) {
+  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
+       v += uint64_t(gridDim.x) * blockDim.x)
+    y[v] = p.reduce_identity();
+}
+
 // Rows longer than this go to k_pull_long (a warp per row).
 constexpr uint64_t kLongRow = 32;
 
@@ -183,7 +264,117 @@ __global__ void k_pull(P p, uint64_t n, const uint64_t* ptr, const uint32_t* idx
       if (any) y[k] = acc;
     }
     const unsigned b = __ballot_sync(0xffffffffu, any);
-    if (lane_id() == 0) ybits[w] = b;
+    if (lane_id() == 0 && b) atomicOr(&ybits[w], b);  // k_pull_long may run concurrently
+  }
+}
+
+// Order-free programs (kExactReorder, no failing callbacks): a group of
+// kGroup lanes per short row, lanes striding over the row's entries (the
+// group's index loads are one 32-byte sector) and a shuffle tree combining
+// the partial folds -- bit-identical to the sequential fold by the program's
+// declaration.  Replaces k_pull's thread per row (32 scattered rows per load
+// instruction) for those programs.
+constexpr unsigned kGroup = 8;
+
+template <typename P>
+__global__ void __launch_bounds__(256) k_pull_group(P p, uint64_t n, const uint64_t* ptr,
+                                                    const uint32_t* idx, const uint8_t* val,
+                                                    const typename P::message_t* x,
+                                                    const uint32_t* xbits,
+                                                    const typename P::vertex_t* props,
+                                                    typename P::reduced_t* y, uint32_t* ybits) {
+  using R = typename P::reduced_t;
+  const uint64_t words = (n + 31) / 32;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id(), sub = lane % kGroup, grp = lane / kGroup;
+  for (uint64_t w = warp; w < words; w += nwarps) {
+    unsigned word = 0;
+#pragma unroll 1
+    for (unsigned r0 = 0; r0 < 32; r0 += 32 / kGroup) {
+      const uint64_t k = w * 32 + r0 + grp;
+      bool any = false;
+      R acc = p.reduce_identity();
+      if (k < n) {
+        const uint64_t e0 = ptr[k], e1 = ptr[k + 1];
+        if (e1 - e0 <= kLongRow) {
+          for (uint64_t e = e0 + sub; e < e1; e += kGroup) {
+            const uint32_t j = idx[e];
+            if (!bit_test(xbits, j)) continue;
+            const R r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), props[k]);
+            acc = any ? p.reduce(acc, r) : p.reduce(p.reduce_identity(), r);
+            any = true;
+          }
+        }
+      }
+#pragma unroll
+      for (unsigned o = kGroup / 2; o > 0; o >>= 1) {
+        const R other = shfl_xor_any(acc, int(o));
+        const bool oany = __shfl_xor_sync(0xffffffffu, any, int(o));
+        if (oany) {
+          acc = any ? p.reduce(acc, other) : other;
+          any = true;
+        }
+      }
+      if (sub == 0 && any) y[k] = acc;
+      const unsigned b = __ballot_sync(0xffffffffu, sub == 0 && any);
+      // lane grp*kGroup holds row r0 + grp's flag
+#pragma unroll
+      for (unsigned g2 = 0; g2 < 32 / kGroup; ++g2)
+        if ((b >> (g2 * kGroup)) & 1u) word |= 1u << (r0 + g2);
+    }
+    if (lane == 0 && word) atomicOr(&ybits[w], word);  // k_pull_long may run concurrently
+  }
+}
+
+// Order-free programs split long rows into pieces of <= kPiece entries, a
+// warp per piece, each piece's fold combined into y[k] with atomic_reduce (y
+// is the identity wherever invalid): a hub row no longer serialises one warp.
+constexpr uint64_t kPiece = 2048;
+
+__global__ void k_piece_counts(const uint32_t* rows, uint64_t nrows, const uint64_t* ptr,
+                               uint64_t* cnt);
+__global__ void k_piece_fill(const uint32_t* rows, uint64_t nrows, const uint64_t* ptr,
+                             const uint64_t* off, uint32_t* prow, uint64_t* pbeg);
+
+template <typename P>
+__global__ void __launch_bounds__(256) k_pull_pieces(P p, const uint32_t* prow, const uint64_t* pbeg,
+                                                     uint64_t npieces, const uint64_t* ptr,
+                                                     const uint32_t* idx, const uint8_t* val,
+                                                     const typename P::message_t* x,
+                                                     const uint32_t* xbits,
+                                                     const typename P::vertex_t* props,
+                                                     typename P::reduced_t* y, uint32_t* ybits) {
+  using R = typename P::reduced_t;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  for (uint64_t i = warp; i < npieces; i += nwarps) {
+    const uint32_t k = prow[i];
+    const uint64_t b = pbeg[i], e1 = min(ptr[k + 1], b + kPiece);
+    const typename P::vertex_t vk = props[k];
+    R acc = p.reduce_identity();
+    bool any = false;
+    for (uint64_t e = b + lane; e < e1; e += 32) {
+      const uint32_t j = idx[e];
+      if (!bit_test(xbits, j)) continue;
+      const R r = p.process_message(x[j], load_edge<typename P::edge_t>(val, e), vk);
+      acc = any ? p.reduce(acc, r) : p.reduce(p.reduce_identity(), r);
+      any = true;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const R other = shfl_xor_any(acc, o);
+      const bool oany = __shfl_xor_sync(0xffffffffu, any, o);
+      if (oany) {
+        acc = any ? p.reduce(acc, other) : other;
+        any = true;
+      }
+    }
+    if (lane == 0 && any) {
+      atomic_reduce(p, &y[k], acc);
+      atomicOr(&ybits[k >> 5], 1u << (k & 31u));
+    }
   }
 }
 
@@ -338,7 +529,7 @@ __global__ void k_merge(P p, uint64_t n, typename P::reduced_t* y, uint32_t* ybi
 // Phase 3, engine.hpp:139-172: clear every flag, apply where y is valid,
 // re-activate iff the state changed.
 template <typename P>
-__global__ void k_apply(P p, uint64_t n, const typename P::reduced_t* y, const uint32_t* ybits,
+__global__ void k_apply(P p, uint64_t n, typename P::reduced_t* y, const uint32_t* ybits,
                         typename P::vertex_t* props, uint32_t* active, const uint32_t* iperm,
                         unsigned long long* ctr, DevError* err) {
   const uint64_t words = (n + 31) / 32;
@@ -351,15 +542,17 @@ __global__ void k_apply(P p, uint64_t n, const typename P::reduced_t* y, const u
       const typename P::vertex_t old = props[v];
       typename P::vertex_t fresh;
       bool okv = true;
+      const typename P::reduced_t yv = y[v];
+      if constexpr (can_push<P>::value) y[v] = p.reduce_identity();  // the push's invariant
       if constexpr (can_fail<P>::value) {
         int ec = 0;
-        fresh = p.apply(y[v], old, ec);
+        fresh = p.apply(yv, old, ec);
         if (ec) {
           record_error(err, ec, kPhaseApply, ext_id(iperm, v), 0, 0);
           okv = false;
         }
       } else {
-        fresh = p.apply(y[v], old);
+        fresh = p.apply(yv, old);
       }
       if (okv && !p.equal(fresh, old)) {
         props[v] = fresh;
@@ -409,12 +602,24 @@ class Engine {
     ctr_.zero(s_);
     err_.alloc(1, s_);
     err_.zero(s_);
+    if constexpr (can_push<P>::value) {
+      if (d == Direction::OUT && n) {  // y = identity wherever invalid (the push's invariant)
+        k_fill_identity<P><<<grid_for(n, 256), 256, 0, s_>>>(p_, n, y_.get());
+        GM_LAUNCH_CHECK();
+      }
+    }
     GM_CUDA(cudaEventCreate(&e0_));
     GM_CUDA(cudaEventCreate(&e1_));
     GM_CUDA(cudaEventCreate(&e2_));
     GM_CUDA(cudaEventCreate(&e3_));
   }
   ~Engine() {
+    if (side_) {
+      cudaStreamSynchronize(side_);
+      cudaStreamDestroy(side_);
+      cudaEventDestroy(fork_);
+      cudaEventDestroy(join_);
+    }
     cudaEventDestroy(e0_);
     cudaEventDestroy(e1_);
     cudaEventDestroy(e2_);
@@ -487,13 +692,105 @@ class Engine {
       have = true;
     }
     const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
-    k_pull<P><<<grid, 256, 0, s_>>>(p_, n, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(),
-                                     xbits_.get(), props_.get(), iperm(), y, ybits, err_.get());
+    // The long rows (the hubs: their in-order fold is the superstep's
+    // critical path) run on a side stream concurrently with the short rows;
+    // both OR their validity bits into the zeroed words.
+    GM_CUDA(cudaMemsetAsync(ybits, 0, (n + 31) / 32 * 4, s_));
+    if (nlong) {
+      if (!side_) {
+        GM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+        GM_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+        GM_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
+      }
+      GM_CUDA(cudaEventRecord(fork_, s_));
+      GM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+      bool pieces = false;
+      if constexpr (can_push<P>::value) pieces = p_.direction() == Direction::OUT && y == y_.get();
+      if constexpr (can_push<P>::value) {
+       if (pieces) {
+        if (!npieces_) {  // once per engine: pieces of <= kPiece entries of every long row
+          DevBuf<uint64_t> cnt(nlong + 1, s_);
+          k_piece_counts<<<grid_for(nlong + 1, 256), 256, 0, s_>>>(lrows.get(), nlong, c.ptr.get(),
+                                                                  cnt.get());
+          GM_LAUNCH_CHECK();
+          exclusive_scan_u64(cnt.get(), nlong + 1, s_);
+          GM_CUDA(cudaMemcpyAsync(&npieces_, cnt.get() + nlong, 8, cudaMemcpyDeviceToHost, s_));
+          GM_CUDA(cudaStreamSynchronize(s_));
+          prow_.alloc(npieces_ + 1, s_);
+          pbeg_.alloc(npieces_ + 1, s_);
+          k_piece_fill<<<grid_for(nlong, 256), 256, 0, s_>>>(lrows.get(), nlong, c.ptr.get(),
+                                                            cnt.get(), prow_.get(), pbeg_.get());
+          GM_LAUNCH_CHECK();
+          GM_CUDA(cudaEventRecord(fork_, s_));
+          GM_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+        }
+        k_pull_pieces<P><<<grid_for(npieces_ * 32, 256), 256, 0, side_>>>(
+            p_, prow_.get(), pbeg_.get(), npieces_, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(),
+            xbits_.get(), props_.get(), y, ybits);
+       }
+      }
+      if (!pieces) {
+        k_pull_long<P><<<grid_for(nlong * 32, kLongThreads), kLongThreads, 0, side_>>>(
+            p_, lrows.get(), nlong, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(), xbits_.get(),
+            props_.get(), iperm(), y, ybits, err_.get());
+      }
+      GM_LAUNCH_CHECK();
+    }
+    if constexpr (exact_reorder<P>::value && !can_fail<P>::value)
+      k_pull_group<P><<<grid, 256, 0, s_>>>(p_, n, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(),
+                                            xbits_.get(), props_.get(), y, ybits);
+    else
+      k_pull<P><<<grid, 256, 0, s_>>>(p_, n, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(),
+                                       xbits_.get(), props_.get(), iperm(), y, ybits, err_.get());
     GM_LAUNCH_CHECK();
     if (nlong) {
-      k_pull_long<P><<<grid_for(nlong * 32, kLongThreads), kLongThreads, 0, s_>>>(
-          p_, lrows.get(), nlong, c.ptr.get(), c.idx.get(), c.val.get(), x_.get(), xbits_.get(),
-          props_.get(), iperm(), y, ybits, err_.get());
+      GM_CUDA(cudaEventRecord(join_, side_));
+      GM_CUDA(cudaStreamWaitEvent(s_, join_, 0));
+    }
+  }
+
+  // After send(): the valid messages as a queue plus their out-edge count;
+  // push when those edges are under 1/kPushDiv of the stored entries (the
+  // pull visits every entry).  One host read per superstep.
+  static constexpr uint64_t kPushDiv = 10;
+  bool decide_push() {
+    if constexpr (!can_push<P>::value) {
+      return false;
+    } else {
+      if (p_.direction() != Direction::OUT || g_.n == 0) return false;
+      ensure_forward(g_);
+      const uint64_t n = g_.n;
+      if (!q_) {
+        q_.alloc(n + 1, s_);
+        qctr_.alloc(2, s_);
+      }
+      qctr_.zero(s_);
+      k_msg_queue<<<grid_for((n + 31) / 32 * 32, 256), 256, 0, s_>>>(n, xbits_.get(), g_.fwd().ptr.get(),
+                                                                   q_.get(), qctr_.get());
+      GM_LAUNCH_CHECK();
+      unsigned long long h[2];
+      GM_CUDA(cudaMemcpyAsync(h, qctr_.get(), 16, cudaMemcpyDeviceToHost, s_));
+      GM_CUDA(cudaStreamSynchronize(s_));
+      nq_ = h[0];
+      push_edges_ = h[1];
+      return h[1] * kPushDiv < g_.m;
+    }
+  }
+
+  void push() {
+    if constexpr (can_push<P>::value) {
+      const uint64_t words = (g_.n + 31) / 32;
+      GM_CUDA(cudaMemsetAsync(ybits_.get(), 0, words * 4, s_));
+      const Csr& fw = g_.fwd();
+      if (!qoff_) qoff_.alloc(g_.n + 2, s_);
+      k_queue_degrees<<<grid_for(g_.n, 256), 256, 0, s_>>>(q_.get(), qctr_.get(), fw.ptr.get(),
+                                                          qoff_.get());
+      GM_LAUNCH_CHECK();
+      exclusive_scan_u64(qoff_.get(), nq_ + 1, s_);
+      if (push_edges_)
+        k_push<P><<<grid_for(push_edges_, 256), 256, 0, s_>>>(
+            p_, q_.get(), qctr_.get(), qoff_.get(), fw.ptr.get(), fw.idx.get(), fw.val.get(),
+            x_.get(), props_.get(), y_.get(), ybits_.get());
       GM_LAUNCH_CHECK();
     }
   }
@@ -502,6 +799,10 @@ class Engine {
     const uint64_t n = g_.n;
     const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
     const Direction d = p_.direction();
+    if (pushing_) {
+      push();
+      return;
+    }
     const Csr& first = d == Direction::IN ? g_.fwd() : g_.in;
     pull(first, long1_, nlong1_, have1_, y_.get(), ybits_.get());
     if (d == Direction::BOTH) {
@@ -527,8 +828,11 @@ class Engine {
     err_.zero(s_);
     GM_CUDA(cudaEventRecord(e0_, s_));
     send();
+    pushing_ = decide_push();
+    pushed_ = pushing_;
     GM_CUDA(cudaEventRecord(e1_, s_));
     spmv();
+    pushing_ = false;
     GM_CUDA(cudaEventRecord(e2_, s_));
     check_error();  // a failed SpMV aborts before apply (engine.hpp:251-257)
     apply();
@@ -548,6 +852,10 @@ class Engine {
     const Direction d = p_.direction();
     st.edges_processed = int64_t(d == Direction::BOTH ? 2 * g_.m : g_.m);
     st.direction = 0;
+    if (pushed_) {
+      st.edges_processed = int64_t(push_edges_);
+      st.direction = 1;
+    }
     return st;
   }
 
@@ -603,6 +911,16 @@ class Engine {
   bool have1_ = false, have2_ = false;
   DevBuf<unsigned long long> ctr_;
   DevBuf<DevError> err_;
+  DevBuf<uint32_t> q_;                 // push: valid message sources
+  DevBuf<unsigned long long> qctr_;    // push: [count, their out-edges]
+  DevBuf<uint64_t> qoff_;              // push: exclusive out-edge offsets over the queue
+  DevBuf<uint32_t> prow_;              // pull pieces of the long rows (order-free programs)
+  DevBuf<uint64_t> pbeg_;
+  uint64_t npieces_ = 0;
+  uint64_t push_edges_ = 0, nq_ = 0;
+  bool pushing_ = false, pushed_ = false;
+  cudaStream_t side_ = nullptr;  // long rows, concurrent with the short-row kernel
+  cudaEvent_t fork_{}, join_{};
   cudaEvent_t e0_{}, e1_{}, e2_{}, e3_{};
 };
 

@@ -4,6 +4,8 @@
 // functor; the generic engine (engine.cuh) runs it with the reference's exact
 // superstep semantics.  Compiled with --fmad=false so fp64 folds round like the
 // reference build (no FMA contraction).
+#include <cub/device/device_scan.cuh>
+
 #include "api_internal.cuh"
 #include "engine.cuh"
 
@@ -22,6 +24,64 @@ __global__ void k_long_rows(uint64_t n, const uint64_t* ptr, uint32_t* rows,
     base = __shfl_sync(0xffffffffu, base, 0);
     if (is_long) rows[base + __popc(m & ((1u << lane_id()) - 1u))] = uint32_t(v);
   }
+}
+
+// The valid messages (set bits of xbits) as a queue, warp-aggregated, with
+// the sum of their out-degrees: ctr[0] = count, ctr[1] = edges.
+__global__ void k_msg_queue(uint64_t n, const uint32_t* xbits, const uint64_t* out_ptr,
+                            uint32_t* q, unsigned long long* ctr) {
+  const uint64_t words = (n + 31) / 32;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long edges = 0;
+  for (uint64_t w = warp; w < words; w += nwarps) {
+    const uint32_t bits = xbits[w];
+    if (!bits) continue;
+    const uint64_t v = w * 32 + lane_id();
+    const bool set = (bits >> lane_id()) & 1u;
+    if (set) edges += out_ptr[v + 1] - out_ptr[v];
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(&ctr[0], (unsigned long long)__popc(bits));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (set) q[base + __popc(bits & ((1u << lane_id()) - 1u))] = uint32_t(v);
+  }
+  warp_add_u64(&ctr[1], edges);
+}
+
+__global__ void k_queue_degrees(const uint32_t* q, const unsigned long long* qn,
+                                const uint64_t* out_ptr, uint64_t* deg) {
+  const uint64_t nq = qn[0];
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i <= nq;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    deg[i] = i < nq ? out_ptr[q[i] + 1] - out_ptr[q[i]] : 0;
+}
+
+__global__ void k_piece_counts(const uint32_t* rows, uint64_t nrows, const uint64_t* ptr,
+                               uint64_t* cnt) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i <= nrows;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    cnt[i] = i < nrows ? (ptr[rows[i] + 1] - ptr[rows[i]] + kPiece - 1) / kPiece : 0;
+}
+
+__global__ void k_piece_fill(const uint32_t* rows, uint64_t nrows, const uint64_t* ptr,
+                             const uint64_t* off, uint32_t* prow, uint64_t* pbeg) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrows;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t k = rows[i];
+    uint64_t o = off[i];
+    for (uint64_t b = ptr[k]; b < ptr[k + 1]; b += kPiece, ++o) {
+      prow[o] = k;
+      pbeg[o] = b;
+    }
+  }
+}
+
+void exclusive_scan_u64(uint64_t* data, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  size_t tmp = 0;
+  GM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, data, data, int64_t(n), s));
+  DevBuf<uint8_t> t(tmp, s);
+  GM_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, data, data, int64_t(n), s));
 }
 
 __global__ void k_bytes_to_bits(const uint8_t* bytes, uint64_t n, uint32_t* bits) {

@@ -974,3 +974,41 @@ def test_sharded_sssp_cf_fused_ipc_two_processes(gm, orc):
     got = out_f.numpy()[gb.permutation()]
     assert np.array_equal(got.view(np.uint32), want_f.view(np.uint32))
     np.testing.assert_allclose(out_rm.numpy(), want_rm, rtol=1e-12)
+
+
+def test_generic_push_spmspv_bitexact(gm, orc):
+    """Frontier-proportional push (SpMSpV, engine.hpp:234-236 skips columns
+    not in x) for the order-free reference programs: BfsProgram and
+    SsspProgram through the generic engine switch to push on small frontiers
+    and still equal the reference semantics bit for bit (levels / distances
+    and every superstep's IterationStats)."""
+    n = 1 << 16
+    g = gm.Graph.rmat(16, 16, seed=9, symmetrize=True, relabel=True)
+    s, d, _ = g.edges()
+    root = g.pick_source(9)
+    dist = np.full(n, np.inf)
+    dist[root] = 0.0
+    act = np.zeros(n, np.uint8)
+    act[root] = 1
+    st = gm.run_graph_program(g, gm.PROG_BFS_REF, dist, act, n + 1)
+    want, wst = orc.bfs(n, s, d, root, presorted=True)
+    got = np.where(np.isinf(dist), -1, dist).astype(np.int64)
+    assert np.array_equal(got, want)
+    assert [x.key() for x in st] == wst
+    dirs = [x.direction for x in st]
+    assert "push" in dirs and "pull" in dirs, dirs
+    # SSSP with real weights (the reference program's fp64 min-plus)
+    gw = gm.Graph.rmat(16, 16, seed=9, relabel=True, weights=True)
+    s, d, w = gw.edges()
+    gf = gm.Graph.from_edges(s, d, n, w.astype(np.float64))
+    root = gw.pick_source(9)
+    dist = np.full(n, np.inf)
+    dist[root] = 0.0
+    act = np.zeros(n, np.uint8)
+    act[root] = 1
+    st = gm.run_graph_program(gf, gm.PROG_SSSP_REF, dist, act, n + 1)
+    want, wst = orc.sssp(n, s, d, w, root, presorted=True)
+    got = np.where(np.isinf(dist), 0xFFFFFFFF, dist).astype(np.uint32)
+    assert np.array_equal(got, want)
+    assert [x.key() for x in st] == wst
+    assert "push" in [x.direction for x in st]

@@ -45,6 +45,25 @@ uint64_t launches_so_far();
     GM_CUDA(cudaGetLastError()); \
   } while (0)
 
+// Device-side bounds checks of the hot kernels' indirect accesses, compiled in
+// only for the checked build (libgraphmat_b200_checked.so, -DGM_DEVICE_CHECKS;
+// tests/test_gpu_checked.py): a violated check prints its location and traps,
+// which fails the call with GM_ECUDA.  The stand-in for compute-sanitizer's
+// memcheck where the tool is unavailable.
+#ifdef GM_DEVICE_CHECKS
+#define GM_DCHECK(cond)                                                                   \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("GM_DCHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);              \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define GM_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 // RAII device buffer (stream-ordered allocation on the graph's stream).
 template <typename T>
 class DevBuf {

@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(256) k_db_push(const uint32_t* __restrict__ qu
                                                  const uint64_t* __restrict__ ptr,
                                                  const uint32_t* __restrict__ idx, uint64_t lo,
                                                  uint64_t hi, const uint32_t* __restrict__ vis,
-                                                 uint32_t* nxt, uint32_t* claims) {
+                                                 uint32_t* nxt, uint32_t* claims, uint64_t n) {
   const uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint64_t nq = qn[3];
@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(256) k_db_push(const uint32_t* __restrict__ qu
     const uint32_t r = queue[i];
     for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
       const uint32_t v = __ldg(&idx[e]);
+      GM_DCHECK(r < hi - lo && v < n);
       const uint32_t bit = 1u << (v & 31u);
       if (v >= lo && v < hi) {
         const uint64_t o = v - lo;
@@ -949,7 +950,7 @@ std::vector<gm_iteration_stats> dbfs(DGraph& g, uint64_t root, int64_t max_iters
         k_db_push<<<148 * 4, 256, 0, s>>>(st.queue[size_t(l)].get(), st.ctr[size_t(l)].get(),
                                           sh.in.ptr.get(), sh.in.idx.get(), sh.lo, sh.hi,
                                           st.vis[size_t(l)].get(), st.nxt[size_t(l)].get(),
-                                          static_cast<uint32_t*>(st.claims[size_t(l)]));
+                                          static_cast<uint32_t*>(st.claims[size_t(l)]), n);
         GM_LAUNCH_CHECK();
       } else {
         // nxt holds the published frontier block: clear it for the claims
@@ -1072,6 +1073,7 @@ struct DPrArgs {
   unsigned long long* part;       // this shard's words for rank_{t+1}
   double one_minus_d_over_n, d_over_n;
   float d;
+  uint64_t nx;  // packed message ids < nx
 };
 
 __device__ __forceinline__ float dpr_base(const DPrArgs& a) {
@@ -1091,6 +1093,7 @@ __device__ __forceinline__ void dpr_apply(const DPrArgs& a, uint32_t r, float su
   a.rank[r] = nr;
   const uint32_t p = a.pid[r];
   if (p != ~0u) {
+    GM_DCHECK(p < a.nx);
     const float xv = nr * a.inv[r];
     for (int q = 0; q < a.P; ++q) a.xn.p[q][p] = xv;
   } else {
@@ -1114,7 +1117,10 @@ __global__ void __launch_bounds__(256) k_dpr_short(DPrArgs a, const uint32_t* ro
     const uint32_t r = rows[i];
     const uint64_t b = a.ptr[r], e = a.ptr[r + 1];
     float s = 0.0f;
-    for (uint64_t k = b; k < e; ++k) s += __ldg(&a.x[__ldg(&a.idx[k])]);
+    for (uint64_t k = b; k < e; ++k) {
+      GM_DCHECK(a.idx[k] < a.nx);
+      s += __ldg(&a.x[__ldg(&a.idx[k])]);
+    }
     dpr_apply(a, r, s, base, e > b, acc);
   }
   dpr_flush(a, acc);
@@ -1337,6 +1343,7 @@ std::vector<gm_iteration_stats> dpagerank(DGraph& g, double damping, int64_t ite
       a.one_minus_d_over_n = (1.0 - damping) / double(n);
       a.d_over_n = damping / double(n);
       a.d = float(damping);
+      a.nx = std::max<uint64_t>(g.nonzero_outdeg, 1);
       const uint64_t nc = st.n_chunks[size_t(l)];
       if (nc) {
         k_dpr_chunks<<<grid_for(nc * 32, 256), 256, 0, s>>>(

@@ -549,7 +549,11 @@ __device__ __forceinline__ void coop_push(const CoopArgs& a, int cur, uint64_t n
     // 2) all column loads in flight, then all visited probes
     uint32_t vk[kEPT], visw[kEPT];
 #pragma unroll
-    for (int k = 0; k < kEPT; ++k) vk[k] = k < nk ? __ldg(&a.out_idx[re[k]]) : 0u;
+    for (int k = 0; k < kEPT; ++k) {
+      GM_DCHECK(k >= nk || re[k] < a.m);
+      vk[k] = k < nk ? __ldg(&a.out_idx[re[k]]) : 0u;
+      GM_DCHECK(vk[k] < a.n);
+    }
 #pragma unroll
     for (int k = 0; k < kEPT; ++k) visw[k] = k < nk ? __ldcg(&a.vis[vk[k] >> 5]) : 0xFFFFFFFFu;
     // 3) claim, then one warp-aggregated append for all winners
@@ -609,6 +613,7 @@ __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t
     if (k0) {
       const uint32_t u0 = __ldg(&a.hsoa[v]);
       if (u0 == 0xFFFFFFFFu) return false;
+      GM_DCHECK(u0 < a.n && v < a.nv);
       ++examined;
       if ((probe_word(s_fb, s_words, fbc, u0) >> (u0 & 31u)) & 1u) return true;
     }
@@ -619,6 +624,7 @@ __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t
     for (int k = 0; k < kSoa; ++k) {
       if (u[k] != 0xFFFFFFFFu) {
         valid |= 1u << k;
+        GM_DCHECK(u[k] < a.n && v < a.nv);
         hit |= ((probe_word(s_fb, s_words, fbc, u[k]) >> (u[k] & 31u)) & 1u) << k;
       }
     }
@@ -641,6 +647,7 @@ __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t
       for (int k = 0; k < 4; ++k) {
         if (u[k] != 0xFFFFFFFFu) {
           valid |= 1u << k;
+          GM_DCHECK(u[k] < a.n);
           hit |= ((probe_word(s_fb, s_words, fbc, u[k]) >> (u[k] & 31u)) & 1u) << k;
         }
       }
@@ -750,6 +757,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
             if (set) {
               const unsigned long long ex = pos + incl - me;
               const uint32_t qp = uint32_t(ex >> kCountShift);
+              GM_DCHECK(qp < a.n && v < a.n);
               a.q[cur][qp] = v;
               a.offs[cur][qp] = ex & kEdgeMask;
               a.qe[cur][qp] = ps;
@@ -894,7 +902,11 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         }
         uint32_t u[kEPT];
 #pragma unroll
-        for (int k = 0; k < kEPT; ++k) u[k] = k < nk ? __ldg(&a.in_idx[re[k]]) : 0xFFFFFFFFu;
+        for (int k = 0; k < kEPT; ++k) {
+          GM_DCHECK(k >= nk || (re[k] < a.m && rv[k] < a.nv));
+          u[k] = k < nk ? __ldg(&a.in_idx[re[k]]) : 0xFFFFFFFFu;
+          GM_DCHECK(k >= nk || u[k] < a.n);
+        }
         // rows already found (by an earlier chunk) skip their probe; this load
         // is issued alongside the column loads, off the critical path
         uint32_t done_w[kEPT];

@@ -504,6 +504,11 @@ GM_API gm_status gm_dgraph_degrees(gm_dgraph_t g, int32_t local_shard, int32_t k
 GM_API gm_status gm_dgraph_bfs(gm_dgraph_t g, uint64_t root, int64_t max_iters, int32_t* out_level,
                                int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                                int64_t* n_stats);
+/* algo::sssp (traversal.hpp:125-133) on a directed sharded graph with u8
+ * weights (gm_dgraph_generate_rmat weights = GM_VAL_U8): uint32 distances. */
+GM_API gm_status gm_dgraph_sssp(gm_dgraph_t g, uint64_t source, int64_t max_iters,
+                                uint32_t* out_dist, int32_t out_on_device,
+                                gm_iteration_stats* stats, int64_t cap, int64_t* n_stats);
 /* gm_pagerank on a directed sharded graph; ranks bitwise independent of P. */
 GM_API gm_status gm_dgraph_pagerank(gm_dgraph_t g, const gm_pagerank_config* cfg, float* out_rank,
                                     int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,

@@ -39,7 +39,7 @@ EXPORTED = [
     "gm_comm_create_local", "gm_comm_nccl_unique_id", "gm_comm_create_nccl", "gm_comm_destroy",
     "gm_dgraph_generate_rmat", "gm_dgraph_create", "gm_dgraph_destroy", "gm_dgraph_shard_info",
     "gm_dgraph_stream", "gm_dgraph_bfs", "gm_dgraph_pagerank", "gm_dgraph_pick_source",
-    "gm_dgraph_degrees",
+    "gm_dgraph_degrees", "gm_dgraph_sssp",
 ]
 
 
@@ -198,6 +198,7 @@ def load(path: str = LIB_PATH):
         "gm_dgraph_stream": (vp, [vp, i32]),
         "gm_dgraph_pick_source": (C.c_int, [vp, u64, C.POINTER(u64)]),
         "gm_dgraph_degrees": (C.c_int, [vp, i32, i32, vp]),
+        "gm_dgraph_sssp": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),
         "gm_dgraph_bfs": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),
         "gm_dgraph_pagerank": (C.c_int, [vp, C.POINTER(PageRankConfig), vp, i32, st, i64,
                                          C.POINTER(i64)]),

@@ -245,6 +245,15 @@ GM_API gm_status gm_dgraph_bfs(gm_dgraph_t g, uint64_t root, int64_t max_iters, 
   });
 }
 
+GM_API gm_status gm_dgraph_sssp(gm_dgraph_t g, uint64_t source, int64_t max_iters,
+                                uint32_t* out_dist, int32_t out_on_device,
+                                gm_iteration_stats* stats, int64_t cap, int64_t* n_stats) {
+  return guarded([&] {
+    const auto st = gm::dsssp(*dgraph_of(g), source, max_iters, out_dist, out_on_device != 0);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
 GM_API gm_status gm_dgraph_pagerank(gm_dgraph_t g, const gm_pagerank_config* cfg, float* out_rank,
                                     int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                                     int64_t* n_stats) {

@@ -1537,3 +1537,368 @@ void ddegrees(DGraph& g, int l, int kind, uint32_t* out_host) {
 }
 
 }  // namespace gm
+
+namespace gm {
+
+// ============================================================================
+// SSSP over the row shards (algo::sssp, traversal.hpp:125-133; BSP
+// Bellman-Ford on integer weights, the superstep-start distances of the
+// frontier are the messages, rule S3).
+//
+// Per superstep, on every shard (direction: pull once the frontier's
+// out-edges exceed m/6, the single-GPU rule):
+//   push: the shard's own frontier rows (a local queue carrying their
+//         superstep-start distances) relax their out-edges (CSR(G) rows of
+//         the shard): an owned destination by atomicMin on its distance, any
+//         other into the shard's full-N candidate array; after a barrier each
+//         owner takes the min over every shard's candidates for its rows
+//         (peer loads) and resets them (peer stores);
+//   pull: every owned row takes the min over its in-entries of msg[u] + w,
+//         msg being the replicated packed vector of the frontier's
+//         distances (INF elsewhere) that the owners published before.
+// finish: the improved rows form the next frontier; one u64 all-reduce of
+// (improved, their out-edges) per superstep, read by the host.
+// ============================================================================
+struct DSsspState {
+  std::vector<DevBuf<uint32_t>> dist, chg, queue, qd;   // [l]
+  std::vector<DevBuf<unsigned long long>> ctr, sum;     // [l]
+  std::vector<void*> msg, cand;                         // [l] peer-visible
+  std::vector<std::vector<void*>> msg_tab, cand_tab;
+  Comm* c = nullptr;
+  ~DSsspState() {
+    if (!c) return;
+    c->unshare(msg_tab);
+    c->unshare(cand_tab);
+    for (int l = 0; l < c->L; ++l) {
+      c->set(l);
+      cudaStreamSynchronize(c->st[size_t(l)]);
+      c->peer_free(l, msg[size_t(l)]);
+      c->peer_free(l, cand[size_t(l)]);
+      dist[size_t(l)].reset();
+      chg[size_t(l)].reset();
+      queue[size_t(l)].reset();
+      qd[size_t(l)].reset();
+      ctr[size_t(l)].reset();
+      sum[size_t(l)].reset();
+    }
+  }
+};
+
+namespace {
+
+constexpr uint32_t kInf = 0xFFFFFFFFu;
+constexpr uint64_t kDSsspPullDiv = 6;
+
+__global__ void k_ds_init(uint32_t* dist, uint32_t* chg, uint64_t rows, uint64_t words,
+                          uint64_t root_local, int owns_root, uint32_t* queue, uint32_t* qd,
+                          unsigned long long* ctr, const uint32_t* outdeg) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < rows || i < words;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (i < rows) dist[i] = owns_root && i == root_local ? 0u : kInf;
+    if (i < words) chg[i] = owns_root && i == (root_local >> 5) ? 1u << (root_local & 31u) : 0u;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctr[0] = owns_root ? 1 : 0;
+    ctr[1] = owns_root ? outdeg[root_local] : 0;
+    ctr[2] = 0;
+    ctr[3] = owns_root ? 1 : 0;
+    if (owns_root) {
+      queue[0] = uint32_t(root_local);
+      qd[0] = 0;
+    }
+  }
+}
+
+// this shard's rows of the message vector: the new distance of every row
+// that improved in the last superstep, INF for the others, into every shard
+__global__ void k_ds_publish(const uint32_t* dist, const uint32_t* chg, const uint32_t* pid,
+                             uint64_t rows, PeerTab<uint32_t> msg, int P, uint64_t nx) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t p = pid[r];
+    if (p == ~0u) continue;  // no out-edges: never read
+    GM_DCHECK(p < nx);
+    const uint32_t v = (chg[r >> 5] >> (r & 31u)) & 1u ? dist[r] : kInf;
+    for (int q = 0; q < P; ++q) msg.p[q][p] = v;
+  }
+}
+
+__device__ __forceinline__ void ds_improve(uint32_t* dist, uint32_t* chg, uint64_t r, uint32_t nd) {
+  if (nd < dist[r] && atomicMin(&dist[r], nd) > nd) atomicOr(&chg[r >> 5], 1u << (r & 31u));
+}
+
+__global__ void __launch_bounds__(256) k_ds_push(const uint32_t* __restrict__ queue,
+                                                 const uint32_t* __restrict__ qd,
+                                                 const unsigned long long* qn,
+                                                 const uint64_t* __restrict__ ptr,
+                                                 const uint32_t* __restrict__ idx,
+                                                 const uint8_t* __restrict__ w, uint64_t lo,
+                                                 uint64_t hi, uint32_t* dist, uint32_t* chg,
+                                                 uint32_t* cand, uint64_t n) {
+  const uint64_t wp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t nq = qn[3];
+  for (uint64_t i = wp; i < nq; i += nw) {
+    const uint32_t r = queue[i], du = qd[i];
+    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
+      const uint32_t v = __ldg(&idx[e]);
+      GM_DCHECK(v < n);
+      const uint32_t nd = du + __ldg(&w[e]);
+      if (v >= lo && v < hi)
+        ds_improve(dist, chg, v - lo, nd);
+      else if (nd < cand[v])
+        atomicMin(&cand[v], nd);
+    }
+  }
+}
+
+__global__ void k_ds_claims(PeerTab<uint32_t> cand, int P, uint64_t lo, uint64_t rows,
+                            uint32_t* dist, uint32_t* chg) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t best = kInf;
+    for (int q = 0; q < P; ++q) {
+      uint32_t* p = cand.p[q] + lo + r;
+      const uint32_t c = *p;
+      if (c != kInf) {
+        best = c < best ? c : best;
+        *p = kInf;
+      }
+    }
+    if (best != kInf) ds_improve(dist, chg, r, best);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ds_pull(const uint64_t* __restrict__ ptr,
+                                                 const uint32_t* __restrict__ idx,
+                                                 const uint8_t* __restrict__ w, uint64_t rows,
+                                                 const uint32_t* __restrict__ msg, uint32_t* dist,
+                                                 uint32_t* chg, unsigned long long* ctr,
+                                                 uint64_t nx) {
+  unsigned long long ex = 0;
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t best = kInf;
+    const uint64_t e1 = ptr[r + 1];
+    for (uint64_t e = ptr[r]; e < e1; ++e) {
+      const uint32_t u = __ldg(&idx[e]);
+      GM_DCHECK(u < nx);
+      const uint32_t m = __ldg(&msg[u]);
+      if (m != kInf) {
+        const uint32_t nd = m + __ldg(&w[e]);
+        best = nd < best ? nd : best;
+      }
+    }
+    ex += e1 - ptr[r];
+    if (best != kInf) ds_improve(dist, chg, r, best);
+  }
+  warp_add_u64(&ctr[2], ex);
+}
+
+__global__ void k_ds_finish(const uint32_t* chg, uint64_t words, uint64_t rows, const uint32_t* dist,
+                            const uint32_t* outdeg, uint32_t* queue, uint32_t* qd,
+                            unsigned long long* ctr) {
+  unsigned long long f = 0, fe = 0;
+  for (uint64_t wd = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; wd < words;
+       wd += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t b = chg[wd];
+    if (!b) continue;
+    const unsigned long long base = atomicAdd(&ctr[3], (unsigned long long)__popc(b));
+    unsigned k = 0;
+    while (b) {
+      const int i = __ffs(b) - 1;
+      b &= b - 1;
+      const uint64_t r = wd * 32 + uint64_t(i);
+      GM_DCHECK(r < rows);
+      queue[base + k] = uint32_t(r);
+      qd[base + k] = dist[r];
+      ++k;
+      ++f;
+      fe += outdeg[r];
+    }
+  }
+  warp_add_u64(&ctr[0], f);
+  warp_add_u64(&ctr[1], fe);
+}
+
+DSsspState& dsssp_state(DGraph& g) {
+  if (g.sssp) return *g.sssp;
+  Comm& c = *g.comm;
+  g.sssp = std::unique_ptr<DSsspState, void (*)(DSsspState*)>(new DSsspState(),
+                                                              [](DSsspState* p) { delete p; });
+  DSsspState& st = *g.sssp;
+  const int L = c.L;
+  for (auto* v : {&st.dist, &st.chg, &st.queue, &st.qd}) v->resize(static_cast<size_t>(L));
+  st.ctr.resize(static_cast<size_t>(L));
+  st.sum.resize(static_cast<size_t>(L));
+  const uint64_t nx = std::max<uint64_t>(g.nonzero_outdeg, 1);
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    const uint64_t rows = g.sh[size_t(l)].hi - g.sh[size_t(l)].lo;
+    st.dist[size_t(l)].alloc(rows + 1, s);
+    st.chg[size_t(l)].alloc((rows + 31) / 32 + 1, s);
+    st.queue[size_t(l)].alloc(rows + 1, s);
+    st.qd[size_t(l)].alloc(rows + 1, s);
+    st.ctr[size_t(l)].alloc(4, s);
+    st.sum[size_t(l)].alloc(4, s);
+    st.msg.push_back(c.peer_alloc(l, nx * 4));
+    st.cand.push_back(c.peer_alloc(l, g.n * 4 + 4));
+    GM_CUDA(cudaMemsetAsync(st.cand.back(), 0xFF, g.n * 4 + 4, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+  }
+  st.c = &c;
+  st.msg_tab = c.share(st.msg);
+  st.cand_tab = c.share(st.cand);
+  return st;
+}
+
+}  // namespace
+
+std::vector<gm_iteration_stats> dsssp(DGraph& g, uint64_t root, int64_t max_iters, uint32_t* out,
+                                      bool out_on_device) {
+  Comm& c = *g.comm;
+  if (g.symmetric || g.value_type != GM_VAL_U8)
+    fail(GM_EUSAGE, "dgraph sssp: needs a directed graph with u8 weights");
+  if (root >= g.n)
+    fail(GM_EINPUT, "source vertex " + std::to_string(root + 1) + " (1-based) exceeds vertex count " +
+                        std::to_string(g.n));
+  DSsspState& st = dsssp_state(g);
+  const int L = c.L, P = c.P;
+  const uint64_t m = g.m;
+  const uint64_t nx = std::max<uint64_t>(g.nonzero_outdeg, 1);
+  const uint64_t ro = g.owner(root);
+  HostPinned<unsigned long long> h(4);
+  std::vector<const uint64_t*> cin;
+  std::vector<uint64_t*> cout_;
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
+    const int owns = uint64_t(c.global(l)) == ro;
+    k_ds_init<<<grid_for(std::max(rows, words) + 1, kBlock), kBlock, 0, s>>>(
+        st.dist[size_t(l)].get(), st.chg[size_t(l)].get(), rows, words, owns ? root - sh.lo : 0,
+        owns, st.queue[size_t(l)].get(), st.qd[size_t(l)].get(), st.ctr[size_t(l)].get(),
+        sh.outdeg.get());
+    GM_LAUNCH_CHECK();
+    cin.push_back(reinterpret_cast<const uint64_t*>(st.ctr[size_t(l)].get()));
+    cout_.push_back(reinterpret_cast<uint64_t*>(st.sum[size_t(l)].get()));
+  }
+  c.allreduce_u64(cin, cout_, 4);
+  c.set(0);
+  GM_CUDA(cudaMemcpyAsync(h.get(), st.sum[0].get(), 32, cudaMemcpyDeviceToHost, c.st[0]));
+  GM_CUDA(cudaStreamSynchronize(c.st[0]));
+  uint64_t nf = h[0], ef = h[1];
+  StepTimer tm;
+  std::vector<gm_iteration_stats> stats;
+  for (int64_t it = 1; nf > 0 && it <= max_iters; ++it) {
+    const bool pull = ef * kDSsspPullDiv > m;
+    c.set(0);
+    GM_CUDA(cudaEventRecord(tm.e[2], c.st[0]));
+    if (pull) {  // the frontier's distances into every shard's message vector
+      for (int l = 0; l < L; ++l) {
+        c.set(l);
+        cudaStream_t s = c.st[size_t(l)];
+        DShard& sh = g.sh[size_t(l)];
+        const uint64_t rows = sh.hi - sh.lo;
+        launch(rows, s, [&](unsigned gr, unsigned bl) {
+          k_ds_publish<<<gr, bl, 0, s>>>(st.dist[size_t(l)].get(), st.chg[size_t(l)].get(),
+                                         sh.pid.get(), rows, tab_of<uint32_t>(st.msg_tab[size_t(l)], P),
+                                         P, nx);
+        });
+      }
+      c.barrier();
+    }
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      DShard& sh = g.sh[size_t(l)];
+      const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[0], s));
+      if (words) GM_CUDA(cudaMemsetAsync(st.chg[size_t(l)].get(), 0, words * 4, s));
+      GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get(), 0, 24, s));  // keep ctr[3] (queue length)
+      if (!pull) {
+        k_ds_push<<<148 * 4, 256, 0, s>>>(st.queue[size_t(l)].get(), st.qd[size_t(l)].get(),
+                                          st.ctr[size_t(l)].get(), sh.out.ptr.get(), sh.out.idx.get(),
+                                          sh.out.val.get(), sh.lo, sh.hi, st.dist[size_t(l)].get(),
+                                          st.chg[size_t(l)].get(),
+                                          static_cast<uint32_t*>(st.cand[size_t(l)]), g.n);
+        GM_LAUNCH_CHECK();
+      } else {
+        launch(rows, s, [&](unsigned gr, unsigned bl) {
+          k_ds_pull<<<gr, bl, 0, s>>>(sh.in.ptr.get(), sh.in.idx.get(), sh.in.val.get(), rows,
+                                      static_cast<const uint32_t*>(st.msg[size_t(l)]),
+                                      st.dist[size_t(l)].get(), st.chg[size_t(l)].get(),
+                                      st.ctr[size_t(l)].get(), nx);
+        });
+      }
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[1], s));
+    }
+    if (!pull) {
+      c.barrier();
+      for (int l = 0; l < L; ++l) {
+        c.set(l);
+        cudaStream_t s = c.st[size_t(l)];
+        DShard& sh = g.sh[size_t(l)];
+        const uint64_t rows = sh.hi - sh.lo;
+        launch(rows, s, [&](unsigned gr, unsigned bl) {
+          k_ds_claims<<<gr, bl, 0, s>>>(tab_of<uint32_t>(st.cand_tab[size_t(l)], P), P, sh.lo, rows,
+                                        st.dist[size_t(l)].get(), st.chg[size_t(l)].get());
+        });
+      }
+      c.barrier();  // nobody pushes into a candidate array before its owners reset it
+    }
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      DShard& sh = g.sh[size_t(l)];
+      const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
+      GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get() + 3, 0, 8, s));
+      launch(words, s, [&](unsigned gr, unsigned bl) {
+        k_ds_finish<<<gr, bl, 0, s>>>(st.chg[size_t(l)].get(), words, rows, st.dist[size_t(l)].get(),
+                                      sh.outdeg.get(), st.queue[size_t(l)].get(),
+                                      st.qd[size_t(l)].get(), st.ctr[size_t(l)].get());
+      });
+    }
+    c.allreduce_u64(cin, cout_, 4);
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(h.get(), st.sum[0].get(), 32, cudaMemcpyDeviceToHost, c.st[0]));
+    GM_CUDA(cudaEventRecord(tm.e[3], c.st[0]));
+    GM_CUDA(cudaStreamSynchronize(c.st[0]));
+    gm_iteration_stats s{};
+    s.iteration = it;
+    s.active_before = int64_t(nf);
+    s.messages_generated = int64_t(nf);
+    s.vertices_updated = int64_t(h[0]);
+    s.direction = pull ? 0 : 1;
+    s.edges_processed = int64_t(pull ? h[2] : ef);
+    s.spmv_seconds = tm.ms(0, 1) * 1e-3;
+    s.total_seconds = tm.ms(2, 3) * 1e-3;
+    s.comm_seconds = std::max(0.0, s.total_seconds - s.spmv_seconds);
+    s.bytes_algorithmic = pull ? int64_t(9 * m + 8 * nf + 4 * g.n + 20 * h[0])
+                               : int64_t(28 * nf + 5 * ef + 20 * h[0] + g.n / 8);
+    stats.push_back(s);
+    nf = h[0];
+    ef = h[1];
+  }
+  if (out) {
+    uint64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      const uint64_t rows = g.sh[size_t(l)].hi - g.sh[size_t(l)].lo;
+      if (rows)
+        GM_CUDA(cudaMemcpyAsync(out + off, st.dist[size_t(l)].get(), rows * 4,
+                                out_on_device ? cudaMemcpyDefault : cudaMemcpyDeviceToHost,
+                                c.st[size_t(l)]));
+      off += rows;
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    GM_CUDA(cudaStreamSynchronize(c.st[size_t(l)]));
+  }
+  return stats;
+}
+
+}  // namespace gm

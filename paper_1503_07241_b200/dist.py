@@ -142,6 +142,20 @@ class DGraph:
         _check(L.load().gm_dgraph_bfs(self._h, root, cap, ptr, dev, st, min(cap, 4096), C.byref(k)))
         return out, _stats(st, k.value)
 
+    def sssp(self, source: int, max_iterations=None, *, out=None, out_device_ptr=None):
+        """algo::sssp (traversal.hpp:125-133) -> (uint32 distances of this process's rows, stats)."""
+        cap = max_iterations if max_iterations is not None else self.num_vertices + 1
+        st, k = _stats_buf(min(cap, 4096))
+        if out_device_ptr is not None:
+            ptr, dev = out_device_ptr, 1
+        else:
+            if out is None:
+                out = np.empty(self._out_len(), np.uint32)
+            ptr, dev = out.ctypes.data, 0
+        _check(L.load().gm_dgraph_sssp(self._h, source, cap, ptr, dev, st, min(cap, 4096),
+                                       C.byref(k)))
+        return out, _stats(st, k.value)
+
     def pagerank(self, damping=0.85, iterations=20, *, out=None, out_device_ptr=None):
         cfg = L.PageRankConfig(damping, iterations)
         st, k = _stats_buf(max(iterations, 1))

@@ -71,6 +71,29 @@ def test_dgraph_pagerank_matches_oracle(gm, orc, P):
     comm.close()
 
 
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_dgraph_sssp_matches_oracle(gm, orc, P):
+    """BSP Bellman-Ford over the row shards (push with per-shard candidate
+    arrays min-reduced by the owners, pull over the published frontier
+    distances): distances and IterationStats equal the reference's."""
+    D = _dist()
+    scale, n = 14, 1 << 14
+    comm = D.Comm.local([0] * P)
+    g = D.DGraph.rmat(comm, scale, 16, seed=7, weights=True, **RMAT)
+    ref = gm.Graph.rmat(scale, 16, seed=7, relabel=False, weights=True, **RMAT)
+    s, d, w = ref.edges()
+    assert g.num_edges == len(s)
+    root = ref.pick_source(7)
+    assert g.pick_source(7) == root
+    dist, st = g.sssp(root)
+    want, wst = orc.sssp(n, s, d, w, root, presorted=True)
+    assert np.array_equal(dist, want)
+    assert _keys(st) == [tuple(x) for x in wst]
+    assert {x.direction for x in st} == {"push", "pull"}
+    g.close()
+    comm.close()
+
+
 def test_dgraph_bitwise_across_shard_counts_scale20(gm):
     """Levels and fp32 ranks are bitwise identical for P = 1, 2, 4 at scale 20
     (row folds depend only on the row; the dangling mass is an exact

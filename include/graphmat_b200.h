@@ -509,6 +509,20 @@ GM_API gm_status gm_dgraph_bfs(gm_dgraph_t g, uint64_t root, int64_t max_iters, 
 GM_API gm_status gm_dgraph_sssp(gm_dgraph_t g, uint64_t source, int64_t max_iters,
                                 uint32_t* out_dist, int32_t out_on_device,
                                 gm_iteration_stats* stats, int64_t cap, int64_t* n_stats);
+/* The Zipf bipartite rating graph of gm_graph_generate_bipartite, sharded:
+ * each shard draws 1/P of the rating stream; users and items are owned by
+ * row blocks like any vertex, each shard storing its vertices' raters
+ * (CSR(G^T) rows) and rated items (CSR(G) rows) with u8 ratings. */
+GM_API gm_status gm_dgraph_generate_bipartite(gm_comm_t c, uint32_t users, uint32_t items,
+                                              double c_numerator, uint32_t cap, uint64_t seed,
+                                              gm_dgraph_t* out);
+/* collaborative_filtering_gd (collaborative_filtering.hpp:134-211) on the
+ * sharded rating graph, K = 20 fp32: init_factors (n*k, host, caller ids) in;
+ * out_factors receives the whole final matrix on every process (each shard
+ * holds it after the last exchange); rmse_trace[it] after iteration it. */
+GM_API gm_status gm_dgraph_cf(gm_dgraph_t g, const gm_cf_config* cfg, const float* init_factors,
+                              float* out_factors, double* rmse_trace, gm_iteration_stats* stats,
+                              int64_t cap, int64_t* n_stats);
 /* gm_pagerank on a directed sharded graph; ranks bitwise independent of P. */
 GM_API gm_status gm_dgraph_pagerank(gm_dgraph_t g, const gm_pagerank_config* cfg, float* out_rank,
                                     int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,

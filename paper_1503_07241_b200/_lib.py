@@ -39,7 +39,7 @@ EXPORTED = [
     "gm_comm_create_local", "gm_comm_nccl_unique_id", "gm_comm_create_nccl", "gm_comm_destroy",
     "gm_dgraph_generate_rmat", "gm_dgraph_create", "gm_dgraph_destroy", "gm_dgraph_shard_info",
     "gm_dgraph_stream", "gm_dgraph_bfs", "gm_dgraph_pagerank", "gm_dgraph_pick_source",
-    "gm_dgraph_degrees", "gm_dgraph_sssp",
+    "gm_dgraph_degrees", "gm_dgraph_sssp", "gm_dgraph_generate_bipartite", "gm_dgraph_cf",
 ]
 
 
@@ -199,6 +199,8 @@ def load(path: str = LIB_PATH):
         "gm_dgraph_pick_source": (C.c_int, [vp, u64, C.POINTER(u64)]),
         "gm_dgraph_degrees": (C.c_int, [vp, i32, i32, vp]),
         "gm_dgraph_sssp": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),
+        "gm_dgraph_generate_bipartite": (C.c_int, [vp, u32, u32, dp, u32, u64, C.POINTER(vp)]),
+        "gm_dgraph_cf": (C.c_int, [vp, C.POINTER(CfConfig), vp, vp, vp, st, i64, C.POINTER(i64)]),
         "gm_dgraph_bfs": (C.c_int, [vp, u64, i64, vp, i32, st, i64, C.POINTER(i64)]),
         "gm_dgraph_pagerank": (C.c_int, [vp, C.POINTER(PageRankConfig), vp, i32, st, i64,
                                          C.POINTER(i64)]),

@@ -254,6 +254,28 @@ GM_API gm_status gm_dgraph_sssp(gm_dgraph_t g, uint64_t source, int64_t max_iter
   });
 }
 
+GM_API gm_status gm_dgraph_generate_bipartite(gm_comm_t c, uint32_t users, uint32_t items,
+                                              double c_numerator, uint32_t cap, uint64_t seed,
+                                              gm_dgraph_t* out) {
+  return guarded([&] {
+    if (!out) gm::fail(GM_EUSAGE, "null output");
+    *out = reinterpret_cast<gm_dgraph_t>(
+        gm::dgraph_generate_bipartite(comm_of(c), users, items, c_numerator, cap, seed));
+  });
+}
+
+GM_API gm_status gm_dgraph_cf(gm_dgraph_t g, const gm_cf_config* cfg, const float* init_factors,
+                              float* out_factors, double* rmse_trace, gm_iteration_stats* stats,
+                              int64_t cap, int64_t* n_stats) {
+  return guarded([&] {
+    if (!cfg) gm::fail(GM_EUSAGE, "null config");
+    if (cfg->factors_on_device) gm::fail(GM_EUSAGE, "dgraph cf: host factor buffers only");
+    const auto st = gm::dcf(*dgraph_of(g), cfg->k, cfg->gamma, cfg->lambda, cfg->iterations,
+                            init_factors, out_factors, rmse_trace);
+    copy_stats(st, stats, cap, n_stats);
+  });
+}
+
 GM_API gm_status gm_dgraph_pagerank(gm_dgraph_t g, const gm_pagerank_config* cfg, float* out_rank,
                                     int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                                     int64_t* n_stats) {

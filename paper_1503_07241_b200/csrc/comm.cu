@@ -93,6 +93,19 @@ __global__ void k_sum_peers(PtrTab in, int P, size_t count, uint64_t* out) {
   }
 }
 
+struct PtrTabD {
+  const double* p[kMaxShards];
+};
+
+__global__ void k_sum_peers_f64(PtrTabD in, int P, size_t count, double* out) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count;
+       i += size_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += in.p[q][i];  // fixed shard order
+    out[i] = s;
+  }
+}
+
 }  // namespace
 
 void Comm::set(int l) const { GM_CUDA(cudaSetDevice(dev[size_t(l)])); }
@@ -154,6 +167,27 @@ void Comm::allreduce_u64(const std::vector<const uint64_t*>& in, const std::vect
     GM_LAUNCH_CHECK();
   }
   barrier();  // nobody rewrites an input another shard is still summing
+}
+
+void Comm::allreduce_f64(const std::vector<const double*>& in, const std::vector<double*>& out,
+                         size_t count) {
+  if (!count) return;
+  if (use_nccl) {
+    set(0);
+    GM_NCCL(nccl_api().AllReduce(in[0], out[0], count, ncclFloat64, ncclSum,
+                                 static_cast<ncclComm_t>(nccl), st[0]));
+    return;
+  }
+  barrier();
+  PtrTabD t{};
+  for (int q = 0; q < P; ++q) t.p[q] = in[size_t(q)];
+  for (int l = 0; l < L; ++l) {
+    set(l);
+    k_sum_peers_f64<<<grid_for(count, 256, 148), 256, 0, st[size_t(l)]>>>(t, P, count,
+                                                                          out[size_t(l)]);
+    GM_LAUNCH_CHECK();
+  }
+  barrier();
 }
 
 void Comm::allgather(const std::vector<const void*>& src, const std::vector<void*>& dst,

@@ -1902,3 +1902,354 @@ std::vector<gm_iteration_stats> dsssp(DGraph& g, uint64_t root, int64_t max_iter
 }
 
 }  // namespace gm
+
+// ============================================================================
+// Collaborative filtering over the row shards (CfGdProgram,
+// collaborative_filtering.hpp:51-90, driven like collaborative_filtering_gd,
+// :134-211).  The bipartite graph is sharded by vertex (users and items
+// alike); shard r stores CSR(G^T) rows (an item's raters) and CSR(G) rows (a
+// user's items) of its vertices with the u8 ratings.  Every shard holds the
+// whole superstep-start factor matrix (n x k fp32, 40 MB for configs[3]);
+// a warp per owned vertex folds e*q over both routes (out-route first, the
+// BOTH merge of engine.hpp:113-126; lane-strided partials and a fixed xor
+// tree: the same result for any P), applies p' = p + gamma*(sum - lambda*p)
+// to every vertex (un-messaged ones take the empty sum, :192-193) and stores
+// p' into every shard's next factor matrix (peer stores).  Each rating's
+// squared error is taken at its user's owner; one f64 all-reduce per
+// superstep sums them (the RMSE of the factors the superstep read) and one
+// u64 all-reduce the updated-vertex count.
+// ============================================================================
+namespace gm {
+
+struct DCfState {
+  std::vector<void*> f[2];  // [l] peer-visible factor matrices
+  std::vector<std::vector<void*>> f_tab[2];
+  std::vector<DevBuf<double>> sq, sqs;                 // [l] partial / summed
+  std::vector<DevBuf<unsigned long long>> ctr, sum;    // [l] updated
+  std::vector<DevBuf<uint32_t>> vbits;
+  int64_t k = 0;
+  Comm* c = nullptr;
+  ~DCfState() {
+    if (!c) return;
+    for (int b = 0; b < 2; ++b) c->unshare(f_tab[b]);
+    for (int l = 0; l < c->L; ++l) {
+      c->set(l);
+      cudaStreamSynchronize(c->st[size_t(l)]);
+      c->peer_free(l, f[0][size_t(l)]);
+      c->peer_free(l, f[1][size_t(l)]);
+      sq[size_t(l)].reset();
+      sqs[size_t(l)].reset();
+      ctr[size_t(l)].reset();
+      sum[size_t(l)].reset();
+      vbits[size_t(l)].reset();
+    }
+  }
+};
+
+namespace {
+
+__global__ void k_row_ratings(const uint64_t* ptr, const uint32_t* idx, uint64_t lo, uint64_t rows,
+                              uint64_t seed_r, int row_is_item, uint8_t* out) {
+  const uint64_t wp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = wp; r < rows; r += nw)
+    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
+      const uint32_t row = uint32_t(lo + r), col = idx[e];
+      out[e] = row_is_item ? rating_of(seed_r, col, row) : rating_of(seed_r, row, col);
+    }
+}
+
+constexpr int kCfK = 20;
+
+// one route of vertex v: acc += (r - p.q_u) q_u over the row's entries
+__device__ __forceinline__ bool dcf_route(const uint64_t* ptr, const uint32_t* idx, const uint8_t* val,
+                                          uint64_t r, const float* f, const float (&p)[kCfK],
+                                          float (&acc)[kCfK], double& sq) {
+  const uint64_t b = ptr[r], e1 = ptr[r + 1];
+  for (uint64_t e = b + lane_id(); e < e1; e += 32) {
+    const float4* q4 = reinterpret_cast<const float4*>(f + uint64_t(idx[e]) * kCfK);
+    float q[kCfK];
+#pragma unroll
+    for (int i = 0; i < kCfK / 4; ++i) {
+      const float4 t = q4[i];
+      q[4 * i] = t.x;
+      q[4 * i + 1] = t.y;
+      q[4 * i + 2] = t.z;
+      q[4 * i + 3] = t.w;
+    }
+    float dot = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kCfK; ++i) dot += p[i] * q[i];
+    const float err = float(val[e]) - dot;
+    sq += double(err) * double(err);
+#pragma unroll
+    for (int i = 0; i < kCfK; ++i) acc[i] += err * q[i];
+  }
+#pragma unroll
+  for (int i = 0; i < kCfK; ++i)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  return e1 > b;
+}
+
+__global__ void __launch_bounds__(256) k_dcf_step(const uint64_t* in_ptr, const uint32_t* in_idx,
+                                                  const uint8_t* in_val, const uint64_t* out_ptr,
+                                                  const uint32_t* out_idx, const uint8_t* out_val,
+                                                  uint64_t lo, uint64_t rows, const float* f,
+                                                  PeerTab<float> fn, int P, float gamma,
+                                                  float lambda, uint32_t* vbits,
+                                                  unsigned long long* upd, double* sq_out) {
+  const uint64_t wp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  double sq = 0.0;
+  unsigned long long u = 0;
+  for (uint64_t r = wp; r < rows; r += nw) {
+    const uint64_t v = lo + r;
+    float p[kCfK], so[kCfK], si[kCfK];
+#pragma unroll
+    for (int i = 0; i < kCfK; ++i) {
+      p[i] = f[v * kCfK + i];
+      so[i] = 0.0f;
+      si[i] = 0.0f;
+    }
+    double dummy = 0.0;
+    // out-route: v receives along its in-edges (CSR(G^T) row); in-route: along
+    // its out-edges (CSR(G) row) -- each rating's error counted once, at the user
+    const bool any_o = dcf_route(in_ptr, in_idx, in_val, r, f, p, so, dummy);
+    const bool any_i = dcf_route(out_ptr, out_idx, out_val, r, f, p, si, sq);
+    bool changed = false;
+    float np[kCfK];
+#pragma unroll
+    for (int i = 0; i < kCfK; ++i) {
+      const float s = any_o && any_i ? so[i] + si[i] : (any_o ? so[i] : si[i]);
+      np[i] = p[i] + gamma * (s - lambda * p[i]);
+      changed |= __float_as_uint(np[i]) != __float_as_uint(p[i]);
+    }
+    if (lane < kCfK) {
+      float mine = np[0];
+#pragma unroll
+      for (int i = 1; i < kCfK; ++i)
+        if (int(lane) == i) mine = np[i];
+      for (int q = 0; q < P; ++q) fn.p[q][v * kCfK + lane] = mine;
+    }
+    if (lane == 0 && changed && (any_o || any_i)) {
+      ++u;
+      atomicOr(&vbits[r >> 5], 1u << (r & 31u));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0 && sq != 0.0) atomicAdd(sq_out, sq);
+  warp_add_u64(upd, u);
+}
+
+// squared errors of the factors f over the ratings of the owned users
+__global__ void __launch_bounds__(256) k_dcf_sq(const uint64_t* out_ptr, const uint32_t* out_idx,
+                                                const uint8_t* out_val, uint64_t lo, uint64_t rows,
+                                                const float* f, double* sq_out) {
+  const uint64_t wp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  double sq = 0.0;
+  for (uint64_t r = wp; r < rows; r += nw) {
+    const uint64_t v = lo + r;
+    float p[kCfK], acc[kCfK];
+#pragma unroll
+    for (int i = 0; i < kCfK; ++i) {
+      p[i] = f[v * kCfK + i];
+      acc[i] = 0.0f;
+    }
+    dcf_route(out_ptr, out_idx, out_val, r, f, p, acc, sq);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane_id() == 0 && sq != 0.0) atomicAdd(sq_out, sq);
+}
+
+DCfState& dcf_state(DGraph& g, int64_t k) {
+  if (g.cf && g.cf->k == k) return *g.cf;
+  g.cf.reset();
+  Comm& c = *g.comm;
+  g.cf = std::unique_ptr<DCfState, void (*)(DCfState*)>(new DCfState(), [](DCfState* p) { delete p; });
+  DCfState& st = *g.cf;
+  st.k = k;
+  const int L = c.L;
+  st.sq.resize(static_cast<size_t>(L));
+  st.sqs.resize(static_cast<size_t>(L));
+  st.ctr.resize(static_cast<size_t>(L));
+  st.sum.resize(static_cast<size_t>(L));
+  st.vbits.resize(static_cast<size_t>(L));
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    const uint64_t rows = g.sh[size_t(l)].hi - g.sh[size_t(l)].lo;
+    for (int b = 0; b < 2; ++b) st.f[b].push_back(c.peer_alloc(l, g.n * uint64_t(k) * 4 + 16));
+    st.sq[size_t(l)].alloc(1, s);
+    st.sqs[size_t(l)].alloc(1, s);
+    st.ctr[size_t(l)].alloc(1, s);
+    st.sum[size_t(l)].alloc(1, s);
+    st.vbits[size_t(l)].alloc((rows + 31) / 32 + 1, s);
+  }
+  st.c = &c;
+  for (int b = 0; b < 2; ++b) st.f_tab[b] = c.share(st.f[b]);
+  return st;
+}
+
+}  // namespace
+
+DGraph* dgraph_generate_bipartite(Comm* c, uint32_t users, uint32_t items, double c_num,
+                                  uint32_t cap, uint64_t seed) {
+  if (users == 0 || items == 0) fail(GM_EUSAGE, "bipartite: need users and items");
+  const uint64_t n = uint64_t(users) + items;
+  std::unique_ptr<DGraph> g(new_dgraph(c, n, GM_PREPROCESS));
+  g->bipartite = true;
+  const unsigned nb = bits_for(n);
+  std::vector<DevBuf<uint64_t>> keys(static_cast<size_t>(c->L));
+  std::vector<uint64_t> m(static_cast<size_t>(c->L));
+  for (int l = 0; l < c->L; ++l) {
+    c->set(l);
+    cudaStream_t s = c->st[size_t(l)];
+    const uint64_t cnt = bipartite_range(users, items, c_num, cap, seed, uint64_t(c->global(l)),
+                                         uint64_t(c->P), nullptr, nullptr, nullptr, s);
+    DevBuf<uint32_t> s32(cnt + 1, s), d32(cnt + 1, s);
+    bipartite_range(users, items, c_num, cap, seed, uint64_t(c->global(l)), uint64_t(c->P), s32.get(),
+                    d32.get(), nullptr, s);
+    keys[size_t(l)].alloc(cnt + 1, s);
+    DevBuf<unsigned long long> k(1, s);
+    k.zero(s);
+    launch(cnt, s, [&](unsigned gr, unsigned bl) {
+      k_edge_keys<<<gr, bl, 0, s>>>(s32.get(), d32.get(), cnt, nb, 0, keys[size_t(l)].get(), k.get());
+    });
+    m[size_t(l)] = dread_u64(k.get(), s);
+  }
+  route_and_build(*g, keys, m, nb, /*forward=*/false, /*check_dups=*/false);
+  build_forward(*g, nb);
+  g->value_type = GM_VAL_U8;
+  const uint64_t seed_r = mix64(seed ^ 0x0DA7A5EEDull);
+  for (int l = 0; l < c->L; ++l) {
+    c->set(l);
+    cudaStream_t s = c->st[size_t(l)];
+    DShard& sh = g->sh[size_t(l)];
+    for (int f = 0; f < 2; ++f) {
+      Csr& a = f ? sh.out : sh.in;
+      a.val.alloc(a.nnz + 1, s);
+      launch(a.n * 32, s, [&](unsigned gr, unsigned bl) {
+        k_row_ratings<<<gr, bl, 0, s>>>(a.ptr.get(), a.idx.get(), sh.lo, a.n, seed_r, f == 0,
+                                        a.val.get());
+      });
+    }
+  }
+  std::vector<uint64_t> nnz;
+  for (auto& s : g->sh) nnz.push_back(s.in.nnz);
+  g->m = c->sum_host(nnz);
+  for (int l = 0; l < c->L; ++l) {
+    c->set(l);
+    GM_CUDA(cudaStreamSynchronize(c->st[size_t(l)]));
+  }
+  return g.release();
+}
+
+std::vector<gm_iteration_stats> dcf(DGraph& g, int64_t k, float gamma, float lambda,
+                                    int64_t iters, const float* init, float* out,
+                                    double* rmse_trace) {
+  Comm& c = *g.comm;
+  if (!g.bipartite) fail(GM_EUSAGE, "dgraph cf: needs a bipartite rating graph");
+  if (k != kCfK) fail(GM_EUSAGE, "dgraph cf: k = 20 (the BASELINE latent dimension) only");
+  if (!(gamma > 0.0f)) fail(GM_EINPUT, "cf: gamma must be positive");
+  if (!(lambda >= 0.0f)) fail(GM_EINPUT, "cf: lambda must be non-negative");
+  if (!init) fail(GM_EUSAGE, "dgraph cf: init factors are required");
+  DCfState& st = dcf_state(g, k);
+  const int L = c.L, P = c.P;
+  const uint64_t n = g.n, m = g.m;
+  for (int l = 0; l < L; ++l) {  // every shard starts from the full init matrix
+    c.set(l);
+    GM_CUDA(cudaMemcpyAsync(st.f[0][size_t(l)], init, n * uint64_t(k) * 4, cudaMemcpyHostToDevice,
+                            c.st[size_t(l)]));
+  }
+  std::vector<const double*> qin;
+  std::vector<double*> qout;
+  std::vector<const uint64_t*> cin;
+  std::vector<uint64_t*> cout_;
+  for (int l = 0; l < L; ++l) {
+    qin.push_back(st.sq[size_t(l)].get());
+    qout.push_back(st.sqs[size_t(l)].get());
+    cin.push_back(reinterpret_cast<const uint64_t*>(st.ctr[size_t(l)].get()));
+    cout_.push_back(reinterpret_cast<uint64_t*>(st.sum[size_t(l)].get()));
+  }
+  std::vector<gm_iteration_stats> stats;
+  std::vector<std::unique_ptr<StepTimer>> tms;
+  std::vector<unsigned long long> upd(size_t(std::max<int64_t>(iters, 0)));
+  auto rmse_of = [&](int buf) {  // RMSE of factor matrix `buf` over all ratings
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      DShard& sh = g.sh[size_t(l)];
+      st.sq[size_t(l)].zero(s);
+      launch((sh.hi - sh.lo) * 32, s, [&](unsigned gr, unsigned bl) {
+        k_dcf_sq<<<gr, bl, 0, s>>>(sh.out.ptr.get(), sh.out.idx.get(), sh.out.val.get(), sh.lo,
+                                   sh.hi - sh.lo, static_cast<const float*>(st.f[buf][size_t(l)]),
+                                   st.sq[size_t(l)].get());
+      });
+    }
+    c.allreduce_f64(qin, qout, 1);
+    double h = 0.0;
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(&h, st.sqs[0].get(), 8, cudaMemcpyDeviceToHost, c.st[0]));
+    GM_CUDA(cudaStreamSynchronize(c.st[0]));
+    return m ? std::sqrt(h / double(m)) : 0.0;
+  };
+  int cur = 0;
+  for (int64_t it = 1; it <= iters; ++it) {
+    tms.emplace_back(new StepTimer());
+    StepTimer& tm = *tms.back();
+    for (int l = 0; l < L; ++l) {
+      c.set(l);
+      cudaStream_t s = c.st[size_t(l)];
+      DShard& sh = g.sh[size_t(l)];
+      const uint64_t rows = sh.hi - sh.lo;
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[0], s));
+      st.sq[size_t(l)].zero(s);
+      st.ctr[size_t(l)].zero(s);
+      GM_CUDA(cudaMemsetAsync(st.vbits[size_t(l)].get(), 0, ((rows + 31) / 32 + 1) * 4, s));
+      launch(rows * 32, s, [&](unsigned gr, unsigned bl) {
+        k_dcf_step<<<gr, bl, 0, s>>>(sh.in.ptr.get(), sh.in.idx.get(), sh.in.val.get(), sh.out.ptr.get(),
+                                     sh.out.idx.get(), sh.out.val.get(), sh.lo, rows,
+                                     static_cast<const float*>(st.f[cur][size_t(l)]),
+                                     tab_of<float>(st.f_tab[cur ^ 1][size_t(l)], P), P, gamma, lambda,
+                                     st.vbits[size_t(l)].get(), st.ctr[size_t(l)].get(),
+                                     st.sq[size_t(l)].get());
+      });
+      if (l == 0) GM_CUDA(cudaEventRecord(tm.e[1], s));
+    }
+    c.allreduce_u64(cin, cout_, 1);  // also the barrier: every shard's factors have landed
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(&upd[size_t(it - 1)], st.sum[0].get(), 8, cudaMemcpyDeviceToHost, c.st[0]));
+    GM_CUDA(cudaEventRecord(tm.e[2], c.st[0]));
+    cur ^= 1;
+    if (rmse_trace) rmse_trace[it - 1] = rmse_of(cur);
+  }
+  if (out) {
+    c.set(0);
+    GM_CUDA(cudaMemcpyAsync(out, st.f[cur][0], n * uint64_t(k) * 4, cudaMemcpyDeviceToHost, c.st[0]));
+  }
+  for (int l = 0; l < L; ++l) {
+    c.set(l);
+    GM_CUDA(cudaStreamSynchronize(c.st[size_t(l)]));
+  }
+  for (int64_t it = 1; it <= iters; ++it) {
+    gm_iteration_stats s{};
+    s.iteration = it;
+    s.active_before = int64_t(n);
+    s.messages_generated = int64_t(n);
+    s.vertices_updated = int64_t(upd[size_t(it - 1)]);
+    s.spmv_seconds = tms[size_t(it - 1)]->ms(0, 1) * 1e-3;
+    s.total_seconds = tms[size_t(it - 1)]->ms(0, 2) * 1e-3;
+    s.comm_seconds = std::max(0.0, s.total_seconds - s.spmv_seconds);
+    s.edges_processed = int64_t(2 * m);
+    s.bytes_algorithmic = int64_t(2 * 5 * m + 2 * 8 * (n + 2) + 3 * 4 * uint64_t(k) * n);
+    stats.push_back(s);
+  }
+  return stats;
+}
+
+}  // namespace gm

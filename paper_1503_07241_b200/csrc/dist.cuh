@@ -48,6 +48,9 @@ struct Comm {
   // out[l][i] = sum over shards q of in[q][i], count u64 words (in != out).
   void allreduce_u64(const std::vector<const uint64_t*>& in, const std::vector<uint64_t*>& out,
                      size_t count);
+  // The same for doubles (local: summed in shard order).
+  void allreduce_f64(const std::vector<const double*>& in, const std::vector<double*>& out,
+                     size_t count);
   // dst[l] = concatenation over shards q (rank order) of src[q], bytes each.
   void allgather(const std::vector<const void*>& src, const std::vector<void*>& dst, size_t bytes);
   // All-to-all of byte runs: shard q sends send_counts[q][r] bytes starting at
@@ -106,6 +109,7 @@ struct DGraph {
   uint64_t n = 0, m = 0;
   uint32_t flags = 0;
   bool symmetric = false;
+  bool bipartite = false;  // users -> items rating graph (CF): columns stay caller ids
   int value_type = GM_VAL_NONE;
   std::vector<uint64_t> bounds;  // P + 1 row boundaries
   std::vector<DShard> sh;        // L local shards

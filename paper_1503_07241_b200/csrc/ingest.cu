@@ -293,9 +293,9 @@ __global__ void k_bip_degree(uint32_t users, double c, uint32_t cap, uint32_t* d
 
 __global__ void k_bip_draw(const uint64_t* off, uint32_t users, uint32_t items,
                            const uint64_t* thr, uint32_t k0, uint32_t k1, uint32_t* src,
-                           uint32_t* dst) {
-  const uint64_t total = off[users];
-  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+                           uint32_t* dst, uint64_t t0 = 0, uint64_t t1 = ~0ull) {
+  const uint64_t total = off[users] < t1 ? off[users] : t1;
+  for (uint64_t t = t0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
        t += uint64_t(gridDim.x) * blockDim.x) {
     uint32_t lo = 0, hi = users;  // last u with off[u] <= t
     while (hi - lo > 1) {
@@ -318,8 +318,8 @@ __global__ void k_bip_draw(const uint64_t* off, uint32_t users, uint32_t items,
       else
         a = mid + 1;
     }
-    src[t] = u;
-    dst[t] = users + a;
+    src[t - t0] = u;
+    dst[t - t0] = users + a;
   }
 }
 
@@ -725,6 +725,50 @@ void rmat_range(unsigned scale, double a, double b, double c, uint64_t seed, int
     k_rmat<<<gr, bl, 0, s>>>(count, scale, ta, tab, tabc, uint32_t(seed), uint32_t(seed >> 32), pk,
                              permute, src, dst, t0);
   });
+}
+
+// The seeded Zipf bipartite stream (graph_generate_bipartite below): total
+// raw ratings, and the ratings [t0, t1) of it (user-major, counter based).
+struct BipStream {
+  DevBuf<uint64_t> thr, off;
+  uint64_t total = 0;
+};
+
+static BipStream bip_stream(uint32_t users, uint32_t items, double c_num, uint32_t cap,
+                            cudaStream_t s) {
+  BipStream b;
+  std::vector<uint64_t> thr(items);
+  double tot = 0.0;
+  for (uint32_t j = 1; j <= items; ++j) tot += std::pow(double(j), -0.8);
+  double cum = 0.0;
+  for (uint32_t j = 1; j <= items; ++j) {
+    cum += std::pow(double(j), -0.8);
+    thr[j - 1] = j == items ? (1ull << 32) : uint64_t(cum / tot * 4294967296.0);
+  }
+  b.thr.alloc(items, s);
+  GM_CUDA(cudaMemcpyAsync(b.thr.get(), thr.data(), items * 8, cudaMemcpyHostToDevice, s));
+  DevBuf<uint32_t> deg(users, s);
+  launch(users, s, [&](unsigned gr, unsigned bl) { k_bip_degree<<<gr, bl, 0, s>>>(users, c_num, cap, deg.get()); });
+  b.off.alloc(uint64_t(users) + 1, s);
+  exclusive_scan_to_ptr(deg.get(), b.off.get(), users, s);
+  GM_CUDA(cudaMemcpyAsync(&b.total, b.off.get() + users, 8, cudaMemcpyDeviceToHost, s));
+  GM_CUDA(cudaStreamSynchronize(s));
+  return b;
+}
+
+uint64_t bipartite_range(uint32_t users, uint32_t items, double c_num, uint32_t cap, uint64_t seed,
+                         uint64_t part, uint64_t parts, uint32_t* src, uint32_t* dst,
+                         uint64_t* total_out, cudaStream_t s) {
+  BipStream b = bip_stream(users, items, c_num, cap, s);
+  const uint64_t t0 = b.total * part / parts, t1 = b.total * (part + 1) / parts;
+  if (total_out) *total_out = b.total;
+  if (src && t1 > t0)
+    launch(t1 - t0, s, [&](unsigned gr, unsigned bl) {
+      k_bip_draw<<<gr, bl, 0, s>>>(b.off.get(), users, items, b.thr.get(), uint32_t(seed),
+                                   uint32_t(seed >> 32), src, dst, t0, t1);
+    });
+  GM_CUDA(cudaStreamSynchronize(s));
+  return t1 - t0;
 }
 
 void sort_keys_u64(DevBuf<uint64_t>& keys, int64_t m, int end_bit, cudaStream_t s) {

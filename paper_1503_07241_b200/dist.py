@@ -103,6 +103,26 @@ class DGraph:
         return cls(comm, h)
 
     @classmethod
+    def bipartite(cls, comm: Comm, users: int, items: int, c_numerator: float, cap: int, *,
+                  seed: int = 1):
+        """The Zipf rating graph of Graph.bipartite, sharded (CF, configs[3])."""
+        h = C.c_void_p()
+        _check(L.load().gm_dgraph_generate_bipartite(comm._h, users, items, c_numerator, cap, seed,
+                                                     C.byref(h)))
+        return cls(comm, h)
+
+    def collaborative_filtering_gd(self, k, gamma, lam, iterations, *, init):
+        """-> (final factors n x k, rmse trace, stats); the whole matrix on every process."""
+        init = np.ascontiguousarray(init, np.float32)
+        out = np.empty_like(init)
+        rm = np.zeros(max(iterations, 1), np.float64)
+        cfg = L.CfConfig(k, gamma, lam, iterations, 0, 0)
+        st, n = _stats_buf(max(iterations, 1))
+        _check(L.load().gm_dgraph_cf(self._h, C.byref(cfg), init.ctypes.data, out.ctypes.data,
+                                     rm.ctypes.data, st, max(iterations, 1), C.byref(n)))
+        return out, rm[:iterations], _stats(st, n.value)
+
+    @classmethod
     def from_edges(cls, comm: Comm, src, dst, num_vertices: int, *, symmetrize=False,
                    preprocess=False):
         """build_graph over the communicator (this process's share of the edges)."""

@@ -94,6 +94,34 @@ def test_dgraph_sssp_matches_oracle(gm, orc, P):
     comm.close()
 
 
+def test_dgraph_cf_matches_oracle_and_single_gpu(gm, orc):
+    """CF over the row shards: the sharded Zipf rating graph is the one
+    Graph.bipartite builds; factors and RMSE trace agree with the fp64 oracle
+    (stable small case) and are bitwise identical for P = 1, 2, 3;
+    vertices_updated counts vertices (engine.hpp:139-172)."""
+    D = _dist()
+    users, items, k, iters = 2000, 150, 20, 4
+    ref = gm.Graph.bipartite(users, items, 8000.0, items, seed=6)
+    s, d, r = ref.edges()
+    n = users + items
+    init = np.random.default_rng(6).uniform(0, 0.1, (n, k)).astype(np.float32)
+    want_f, _, want_rm, want_upd = orc.cf_gd(n, s, d, r.astype(np.float64), init.astype(np.float64),
+                                             1e-3, 0.05, iters, with_updated=True)
+    outs = []
+    for P in (1, 2, 3):
+        comm = D.Comm.local([0] * P)
+        g = D.DGraph.bipartite(comm, users, items, 8000.0, items, seed=6)
+        assert g.num_edges == len(s)
+        f, rm, st = g.collaborative_filtering_gd(k, 1e-3, 0.05, iters, init=init)
+        assert np.max(np.abs(rm - want_rm)) <= 1e-4, (rm, want_rm)
+        np.testing.assert_allclose(f, want_f, rtol=1e-4, atol=1e-6)
+        assert [x.vertices_updated for x in st] == list(want_upd)
+        outs.append(f.view(np.uint32).copy())
+        g.close()
+        comm.close()
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
 def test_dgraph_bitwise_across_shard_counts_scale20(gm):
     """Levels and fp32 ranks are bitwise identical for P = 1, 2, 4 at scale 20
     (row folds depend only on the row; the dangling mass is an exact

@@ -63,6 +63,30 @@ def ncu_traffic(kernel, workload):
     return None, None
 
 
+def with_l2_roof(rf, workload):
+    """The second roof of a gather-bound kernel: its L2 requests per launch
+    (ncu lts__t_requests_srcunit_tex, profiles/r*_requests.json) over the
+    chip's measured L2 request rate for random 4-byte gathers
+    (tools/gather_bench.cu) = the shortest launch the request count allows.
+    frac = that floor / the measured launch time."""
+    import glob
+    if not rf or "launch_us" not in rf:
+        return rf
+    kern = rf.get("traffic_kernel", rf.get("kernel", "")).split()[0]
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_requests.json")), reverse=True):
+        with open(f) as fh:
+            d = json.load(fh)
+        k = d["kernels"].get(f"{workload}:{kern}")
+        if k:
+            floor = k["l2_requests_per_launch"] / d["l2_request_rate_gps"] / 1e3
+            rf["l2_roof"] = {"bound": "l2_requests", "requests_per_launch": k["l2_requests_per_launch"],
+                             "rate_gps": d["l2_request_rate_gps"], "floor_us": round(floor, 1),
+                             "frac": round(floor / rf["launch_us"], 4),
+                             "source": os.path.relpath(f, ROOT)}
+            break
+    return rf
+
+
 def gm_pagerank_uses_hub(g):
     """Which single-GPU PageRank kernel the library runs for g (the rule of
     pagerank_hub_enabled, csrc/pagerank_hub.cu)."""
@@ -876,7 +900,8 @@ def run_ours(args, d: Dist):
         "graph": w.facts,
         "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_s * 1e3 / args.steps, 4)},
-        "roofline": with_spec(w.roofline(st, peak, peak_kind, ktime)),
+        "roofline": with_l2_roof(with_spec(w.roofline(st, peak, peak_kind, ktime)),
+                                 w.config["workload"]),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "ingest_seconds": round(w.ingest_s, 3),

@@ -290,6 +290,12 @@ def _stats_buf(cap):
 
 # --------------------------------------------------------------- programs
 
+def _host_async_mode(with_stats):
+    if with_stats:
+        raise ValueError("sync=False returns before the run ends: pass with_stats=False")
+    return 3  # GM_OUT_HOST_ASYNC
+
+
 def _device_mode(sync, with_stats):
     """GM_OUT_DEVICE, or GM_OUT_DEVICE_ASYNC when the caller waives the host
     synchronisation (the run is only enqueued on g.stream; g.synchronize()
@@ -334,7 +340,9 @@ def bfs(g: Graph, root: int, max_iterations=None, *, with_stats=True, out=None,
     else:
         if out is None:
             out = np.empty(n, np.int32)
-        ptr, on_dev = out.ctypes.data, 0
+        # sync=False with a (pinned) host array: GM_OUT_HOST_ASYNC -- the copy
+        # overlaps the next call; g.synchronize() before reading `out`
+        ptr, on_dev = out.ctypes.data, 0 if sync else _host_async_mode(with_stats)
     _check(L.load().gm_bfs(g._h, root, cap, ptr, on_dev, st if with_stats else None,
                            min(cap, 4096), C.byref(k) if with_stats else None))
     return out, _stats(st, k.value) if with_stats else []

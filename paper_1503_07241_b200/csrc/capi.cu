@@ -132,7 +132,11 @@ GM_API void* gm_graph_stream(gm_graph_t g) {
 }
 
 GM_API gm_status gm_graph_synchronize(gm_graph_t g) {
-  return guarded([&] { GM_CUDA(cudaStreamSynchronize(handle(g)->stream)); });
+  return guarded([&] {
+    gm::Graph* h = handle(g);
+    GM_CUDA(cudaStreamSynchronize(h->stream));
+    h->host_async.sync();
+  });
 }
 
 // ---- multi-GPU: communicator + sharded graph ----------------------------------
@@ -322,10 +326,12 @@ GM_API gm_status gm_kernel_timer_stop(gm_graph_t g, double* total_ms, int64_t* l
 namespace {
 // out_on_device: GM_OUT_HOST, GM_OUT_DEVICE or GM_OUT_DEVICE_ASYNC (device
 // output, no host synchronisation -- so no stats either).
-void check_out_mode(int32_t mode, const gm_iteration_stats* stats, const int64_t* n_stats) {
-  if (mode < GM_OUT_HOST || mode > GM_OUT_DEVICE_ASYNC) gm::fail(GM_EUSAGE, "bad out_on_device mode");
-  if (mode == GM_OUT_DEVICE_ASYNC && (stats || n_stats))
-    gm::fail(GM_EUSAGE, "GM_OUT_DEVICE_ASYNC returns before the run ends: pass no stats buffer");
+void check_out_mode(int32_t mode, const gm_iteration_stats* stats, const int64_t* n_stats,
+                    bool host_async_ok = false) {
+  if (mode < GM_OUT_HOST || mode > (host_async_ok ? GM_OUT_HOST_ASYNC : GM_OUT_DEVICE_ASYNC))
+    gm::fail(GM_EUSAGE, "bad out_on_device mode");
+  if ((mode == GM_OUT_DEVICE_ASYNC || mode == GM_OUT_HOST_ASYNC) && (stats || n_stats))
+    gm::fail(GM_EUSAGE, "an async output mode returns before the run ends: pass no stats buffer");
 }
 }  // namespace
 
@@ -345,9 +351,11 @@ GM_API gm_status gm_bfs(gm_graph_t g, uint64_t root, int64_t max_iters, int32_t*
                         int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                         int64_t* n_stats) {
   return guarded([&] {
-    check_out_mode(out_on_device, stats, n_stats);
-    auto st = gm::bfs(*handle(g), root, max_iters, out_level, out_on_device != 0,
-                      stats != nullptr || n_stats != nullptr, out_on_device == GM_OUT_DEVICE_ASYNC);
+    check_out_mode(out_on_device, stats, n_stats, /*host_async_ok=*/true);
+    const bool host_async = out_on_device == GM_OUT_HOST_ASYNC;
+    auto st = gm::bfs(*handle(g), root, max_iters, out_level,
+                      out_on_device != 0 && !host_async, stats != nullptr || n_stats != nullptr,
+                      out_on_device == GM_OUT_DEVICE_ASYNC || host_async);
     copy_stats(st, stats, cap, n_stats);
   });
 }

@@ -85,6 +85,53 @@ struct Graph {
 
   KernelTimer ktimer;
 
+  // GM_OUT_HOST_ASYNC: a host copy stream fed from two device staging
+  // buffers; the compute stream waits for a buffer's previous copy before
+  // writing it again (stage()), the copy stream waits for the write (issue()).
+  struct HostAsync {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ready[2]{}, freed[2]{};
+    DevBuf<uint8_t> buf[2];
+    bool used[2]{};
+    int i = 0;
+    void* stage(cudaStream_t s, size_t bytes) {
+      if (!cs) {
+        GM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+          GM_CUDA(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
+          GM_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+        }
+      }
+      if (buf[i].size() < bytes) {
+        if (used[i]) GM_CUDA(cudaEventSynchronize(freed[i]));
+        buf[i].alloc(bytes, s);
+        used[i] = false;
+      }
+      if (used[i]) GM_CUDA(cudaStreamWaitEvent(s, freed[i], 0));
+      return buf[i].get();
+    }
+    void issue(cudaStream_t s, void* host, size_t bytes) {
+      GM_CUDA(cudaEventRecord(ready[i], s));
+      GM_CUDA(cudaStreamWaitEvent(cs, ready[i], 0));
+      GM_CUDA(cudaMemcpyAsync(host, buf[i].get(), bytes, cudaMemcpyDeviceToHost, cs));
+      GM_CUDA(cudaEventRecord(freed[i], cs));
+      used[i] = true;
+      i ^= 1;
+    }
+    void sync() {
+      if (cs) GM_CUDA(cudaStreamSynchronize(cs));
+    }
+    ~HostAsync() {
+      if (!cs) return;
+      cudaStreamSynchronize(cs);
+      for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(ready[b]);
+        cudaEventDestroy(freed[b]);
+      }
+      cudaStreamDestroy(cs);
+    }
+  } host_async;
+
   std::unique_ptr<PrCache, void (*)(PrCache*)> pr{nullptr, nullptr};
   std::unique_ptr<PrHubCache, void (*)(PrHubCache*)> prhub{nullptr, nullptr};
   std::unique_ptr<TravCache, void (*)(TravCache*)> trav{nullptr, nullptr};

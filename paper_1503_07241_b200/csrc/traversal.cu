@@ -1493,13 +1493,19 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   }
   if (out) {
     int32_t* dst = out;
-    if (!out_on_device) {
+    const bool host_async = !out_on_device && async;  // GM_OUT_HOST_ASYNC
+    if (host_async) {
+      dst = static_cast<int32_t*>(g.host_async.stage(s, n * 4));
+    } else if (!out_on_device) {
       if (!c.ext_out) c.ext_out.alloc(n, s);
       dst = c.ext_out.get();
     }
     k_bfs_output<<<grid_for(n, 256), 256, 0, s>>>(n, perm, c.level.get(), dst);
     GM_LAUNCH_CHECK();
-    if (!out_on_device) GM_CUDA(cudaMemcpyAsync(out, dst, n * 4, cudaMemcpyDeviceToHost, s));
+    if (host_async)
+      g.host_async.issue(s, out, n * 4);
+    else if (!out_on_device)
+      GM_CUDA(cudaMemcpyAsync(out, dst, n * 4, cudaMemcpyDeviceToHost, s));
   }
   if (!async) GM_CUDA(cudaStreamSynchronize(s));
   return stats;

@@ -1012,3 +1012,23 @@ def test_generic_push_spmspv_bitexact(gm, orc):
     assert np.array_equal(got, want)
     assert [x.key() for x in st] == wst
     assert "push" in [x.direction for x in st]
+
+
+def test_bfs_host_async_output(gm, orc):
+    """GM_OUT_HOST_ASYNC: the level vector reaches pinned host memory on the
+    library's copy stream, overlapping the next call; after synchronize()
+    every call's output equals the synchronous one."""
+    import torch
+    g = gm.Graph.rmat(14, 16, seed=4, symmetrize=True, relabel=True)
+    n = g.num_vertices
+    want, _ = gm.bfs(g, g.pick_source(4))
+    roots = [g.pick_source(4), g.pick_source(5), g.pick_source(6)]
+    bufs = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in roots]
+    for r, b in zip(roots, bufs):
+        gm.bfs(g, r, with_stats=False, out=b.numpy(), sync=False)
+    g.synchronize()
+    for r, b in zip(roots, bufs):
+        assert np.array_equal(b.numpy(), gm.bfs(g, r)[0])
+    assert np.array_equal(bufs[0].numpy(), want)
+    with pytest.raises(ValueError):
+        gm.bfs(g, roots[0], out=bufs[0].numpy(), sync=False)  # stats need the host

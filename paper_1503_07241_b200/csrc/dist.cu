@@ -32,7 +32,9 @@ namespace gm {
 struct DBfsState {
   std::vector<DevBuf<int32_t>> level;      // [l] owned rows
   std::vector<DevBuf<uint32_t>> vis, nxt;  // [l] owned words
-  std::vector<DevBuf<uint32_t>> queue;     // [l] local frontier rows
+  std::vector<DevBuf<uint32_t>> queue;     // [l] local frontier rows (push)
+  std::vector<DevBuf<uint64_t>> qdeg;      // [l] their degrees -> exclusive offsets
+  std::vector<DevBuf<uint32_t>> iso;       // [l] isolated-row bitmap (owned words)
   std::vector<DevBuf<unsigned long long>> ctr, sum;  // [l] counters / summed
   std::vector<void*> fb[2], claims;        // [l] peer-visible full bitmaps
   std::vector<std::vector<void*>> fb_tab[2], claims_tab;
@@ -51,11 +53,15 @@ struct DBfsState {
       vis[size_t(l)].reset();
       nxt[size_t(l)].reset();
       queue[size_t(l)].reset();
+      qdeg[size_t(l)].reset();
+      iso[size_t(l)].reset();
       ctr[size_t(l)].reset();
       sum[size_t(l)].reset();
     }
   }
 };
+
+void exclusive_scan_u64(uint64_t* data, uint64_t n, cudaStream_t s);  // generic_programs.cu
 
 struct DPrState {
   std::vector<DevBuf<float>> rank, inv;               // [l] owned rows
@@ -508,10 +514,111 @@ DGraph* new_dgraph(Comm* c, uint64_t n, uint32_t flags) {
   return g.release();
 }
 
+// Symmetric graphs: every row's neighbours ordered hub-first -- by degree
+// class (floor(log2(degree)), descending), then caller id -- so a pull finds
+// a frontier neighbour in its first probes (the role the degree relabel plays
+// on one GPU).  The classes are global (an OR of every shard's slice of a
+// byte per vertex), so the order, and every result, is the same for any P.
+__global__ void k_deg_class(const uint64_t* ptr, uint64_t lo, uint64_t rows, uint8_t* cls) {
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t d = ptr[r + 1] - ptr[r];
+    cls[lo + r] = d ? uint8_t(1 + 63 - __clzll((long long)d)) : 0;  // 0: isolated
+  }
+}
+
+__global__ void k_hub_keys(const uint64_t* ptr, const uint32_t* idx, uint64_t rows, unsigned nb,
+                           const uint8_t* cls, uint64_t* keys) {
+  const uint64_t wp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = wp; r < rows; r += nw)
+    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
+      const uint32_t u = idx[e];
+      keys[e] = (r << (nb + 6)) | (uint64_t(63 - cls[u]) << nb) | u;
+    }
+}
+
+__global__ void k_rebase_ptr(const uint64_t* ptr, uint64_t n, uint64_t base, uint64_t* out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = ptr[i] - base;
+}
+
+__global__ void k_low_ids(const uint64_t* keys, uint64_t m, unsigned nb, uint32_t* idx) {
+  const uint64_t mask = (uint64_t(1) << nb) - 1;
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x)
+    idx[e] = uint32_t(keys[e] & mask);
+}
+
+void hub_first_rows(DGraph& g, unsigned nb) {
+  Comm& c = *g.comm;
+  const uint64_t words = (g.n + 7) / 8;
+  std::vector<DevBuf<uint64_t>> cl(static_cast<size_t>(c.L)), cls(static_cast<size_t>(c.L));
+  std::vector<const uint64_t*> in;
+  std::vector<uint64_t*> out;
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    cl[size_t(l)].alloc(words + 1, s);
+    cls[size_t(l)].alloc(words + 1, s);
+    cl[size_t(l)].zero(s);
+    launch(sh.hi - sh.lo, s, [&](unsigned gr, unsigned bl) {
+      k_deg_class<<<gr, bl, 0, s>>>(sh.in.ptr.get(), sh.lo, sh.hi - sh.lo,
+                                    reinterpret_cast<uint8_t*>(cl[size_t(l)].get()));
+    });
+    in.push_back(cl[size_t(l)].get());
+    out.push_back(cls[size_t(l)].get());
+  }
+  c.allreduce_u64(in, out, words);  // one writer per byte: the sum is an OR
+  for (int l = 0; l < c.L; ++l) {
+    c.set(l);
+    cudaStream_t s = c.st[size_t(l)];
+    DShard& sh = g.sh[size_t(l)];
+    cl[size_t(l)].reset();
+    const uint64_t rows = sh.hi - sh.lo;
+    if (!sh.in.nnz) continue;
+    // rows in chunks of ~2^30 entries: the sort's key buffers stay ~16 GB
+    // (one GPU holding a whole scale-28 graph has ~140 GB free, not 2 x 68)
+    const uint64_t per = std::max<uint64_t>(1, rows * (uint64_t(1) << 30) / sh.in.nnz);
+    for (uint64_t r0 = 0; r0 < rows; r0 += per) {
+      const uint64_t r1 = std::min(rows, r0 + per);
+      uint64_t e[2];
+      GM_CUDA(cudaMemcpyAsync(&e[0], sh.in.ptr.get() + r0, 8, cudaMemcpyDeviceToHost, s));
+      GM_CUDA(cudaMemcpyAsync(&e[1], sh.in.ptr.get() + r1, 8, cudaMemcpyDeviceToHost, s));
+      GM_CUDA(cudaStreamSynchronize(s));
+      const uint64_t m = e[1] - e[0];
+      if (m < 2) continue;
+      unsigned rb = 1;
+      while ((uint64_t(1) << rb) < (r1 - r0) + 1) ++rb;
+      if (rb + nb + 6 > 64) continue;  // keys too wide: keep caller-id order for these rows
+      DevBuf<uint64_t> keys(m, s);
+      // k_hub_keys numbers rows from r0 (pointer offset) and entries from e[0]
+      DevBuf<uint64_t> lptr(r1 - r0 + 1, s);
+      launch(r1 - r0 + 1, s, [&](unsigned gr, unsigned bl) {
+        k_rebase_ptr<<<gr, bl, 0, s>>>(sh.in.ptr.get() + r0, r1 - r0 + 1, e[0], lptr.get());
+      });
+      launch((r1 - r0) * 32, s, [&](unsigned gr, unsigned bl) {
+        k_hub_keys<<<gr, bl, 0, s>>>(lptr.get(), sh.in.idx.get() + e[0], r1 - r0, nb,
+                                     reinterpret_cast<const uint8_t*>(cls[size_t(l)].get()),
+                                     keys.get());
+      });
+      sort_keys_u64(keys, int64_t(m), int(rb + nb + 6), s);
+      launch(m, s, [&](unsigned gr, unsigned bl) {
+        k_low_ids<<<gr, bl, 0, s>>>(keys.get(), m, nb, sh.in.idx.get() + e[0]);
+      });
+      GM_CUDA(cudaStreamSynchronize(s));
+    }
+    cls[size_t(l)].reset();
+  }
+}
+
 void finish_build(DGraph& g, unsigned nb, int weights, uint64_t seed) {
   Comm& c = *g.comm;
   if (g.symmetric) {
     for (auto& s : g.sh) s.out_alias = true;
+    hub_first_rows(g, nb);
   } else {
     if ((g.flags & GM_NEED_FORWARD) || weights == GM_VAL_U8) build_forward(g, nb);
     if (weights == GM_VAL_U8) {
@@ -675,17 +782,31 @@ namespace {
 
 constexpr int kPush = 1, kPull = 0;
 
+// the shard's isolated rows (no neighbours: never reached, never a parent)
+__global__ void k_db_isolated(const uint64_t* ptr, uint64_t rows, uint32_t* iso) {
+  const uint64_t words = (rows + 31) / 32;
+  for (uint64_t w0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~uint64_t(31); w0 < words;
+       w0 += uint64_t(gridDim.x) * blockDim.x) {
+    for (unsigned j = 0; j < 32 && w0 + j < words; ++j) {
+      const uint64_t r = (w0 + j) * 32 + lane_id();
+      const unsigned b = __ballot_sync(0xffffffffu, r < rows && ptr[r + 1] == ptr[r]);
+      if (lane_id() == 0) iso[w0 + j] = b;
+    }
+  }
+}
+
 __global__ void k_db_init(int32_t* level, uint64_t rows, uint32_t* vis, uint32_t* nxt,
                           uint64_t words, uint64_t root_local, int owns_root, uint32_t* queue,
-                          unsigned long long* ctr, const uint64_t* ptr) {
+                          unsigned long long* ctr, const uint64_t* ptr, const uint32_t* iso) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < rows || i < words;
        i += uint64_t(gridDim.x) * blockDim.x) {
     if (i < rows) level[i] = owns_root && i == root_local ? 0 : -1;
     if (i < words) {
-      // nxt doubles as the frontier block a pull superstep publishes: the root
-      const bool rw = owns_root && i == (root_local >> 5);
-      vis[i] = rw ? 1u << (root_local & 31u) : 0u;
-      nxt[i] = vis[i];
+      // nxt doubles as the frontier block a pull superstep publishes: the
+      // root; isolated rows count as visited (pulls skip them)
+      const uint32_t rb = owns_root && i == (root_local >> 5) ? 1u << (root_local & 31u) : 0u;
+      vis[i] = rb | iso[i];
+      nxt[i] = rb;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -697,28 +818,68 @@ __global__ void k_db_init(int32_t* level, uint64_t rows, uint32_t* vis, uint32_t
   }
 }
 
-// push: warp per frontier row, lanes over its adjacency
-__global__ void __launch_bounds__(256) k_db_push(const uint32_t* __restrict__ queue,
-                                                 const unsigned long long* qn,
+// Before a push: the frontier rows (set bits of the frontier block) as a
+// queue with their degrees; one atomicAdd per warp of 32 words.
+__global__ void k_db_queue(const uint32_t* fr, uint64_t words, const uint64_t* ptr, uint32_t* q,
+                           uint64_t* qdeg, unsigned long long* qn) {
+  for (uint64_t w0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~uint64_t(31); w0 < words;
+       w0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t w = w0 + lane_id();
+    uint32_t bits = w < words ? fr[w] : 0u;
+    const unsigned c = __popc(bits);
+    unsigned incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane_id() >= unsigned(o)) incl += t;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (!tot) continue;
+    unsigned long long base = 0;
+    if (lane_id() == 31) base = atomicAdd(qn, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31) + (incl - c);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint64_t r = w * 32 + uint64_t(b);
+      q[base] = uint32_t(r);
+      qdeg[base] = ptr[r + 1] - ptr[r];
+      ++base;
+    }
+  }
+}
+
+// push: edge-balanced -- thread t takes the t-th frontier edge (its row found
+// by a binary search over the queue's degree offsets), so a hub row's edges
+// spread over the grid; an owned neighbour is claimed in the next block,
+// any other one in the shard's claims bitmap
+__global__ void __launch_bounds__(256) k_db_push(const uint32_t* __restrict__ q,
+                                                 const uint64_t* __restrict__ qoff, uint64_t nq,
                                                  const uint64_t* __restrict__ ptr,
                                                  const uint32_t* __restrict__ idx, uint64_t lo,
                                                  uint64_t hi, const uint32_t* __restrict__ vis,
                                                  uint32_t* nxt, uint32_t* claims, uint64_t n) {
-  const uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t nq = qn[3];
-  for (uint64_t i = w; i < nq; i += nw) {
-    const uint32_t r = queue[i];
-    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) {
-      const uint32_t v = __ldg(&idx[e]);
-      GM_DCHECK(r < hi - lo && v < n);
+  const uint64_t total = qoff[nq];
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t a = 0, b = nq;  // last i with qoff[i] <= t
+    while (b - a > 1) {
+      const uint64_t mid = (a + b) >> 1;
+      if (qoff[mid] <= t)
+        a = mid;
+      else
+        b = mid;
+    }
+    const uint32_t r = q[a];
+    const uint32_t v = __ldg(&idx[ptr[r] + (t - qoff[a])]);
+    GM_DCHECK(r < hi - lo && v < n);
+    if (v >= lo && v < hi) {
+      const uint64_t o = v - lo;
+      const uint32_t ob = 1u << (o & 31u);
+      if (!(vis[o >> 5] & ob) && !(nxt[o >> 5] & ob)) atomicOr(&nxt[o >> 5], ob);
+    } else {
       const uint32_t bit = 1u << (v & 31u);
-      if (v >= lo && v < hi) {
-        const uint64_t o = v - lo;
-        if (!(vis[o >> 5] & (1u << (o & 31u)))) atomicOr(&nxt[o >> 5], 1u << (o & 31u));
-      } else {
-        atomicOr(&claims[v >> 5], bit);
-      }
+      if (!(claims[v >> 5] & bit)) atomicOr(&claims[v >> 5], bit);
     }
   }
 }
@@ -729,18 +890,36 @@ __global__ void __launch_bounds__(256) k_db_pull(const uint64_t* __restrict__ pt
                                                  const uint32_t* __restrict__ vis,
                                                  const uint32_t* __restrict__ fb, uint32_t* nxt,
                                                  unsigned long long* ctr) {
+  // a warp takes 32 consecutive words (one coalesced load of their visited
+  // bits), then each word with open rows in turn, lane = row; the word's
+  // found bits are one ballot (no atomics)
   unsigned long long ex = 0;
-  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
-       r += uint64_t(gridDim.x) * blockDim.x) {
-    if ((vis[r >> 5] >> (r & 31u)) & 1u) continue;
-    const uint64_t b = ptr[r], e = ptr[r + 1];
-    for (uint64_t k = b; k < e; ++k) {
-      const uint32_t u = __ldg(&idx[k]);
-      ++ex;
-      if ((__ldg(&fb[u >> 5]) >> (u & 31u)) & 1u) {
-        atomicOr(&nxt[r >> 5], 1u << (r & 31u));
-        break;
+  const uint64_t words = (rows + 31) / 32;
+  const unsigned lane = lane_id();
+  for (uint64_t w0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~uint64_t(31); w0 < words;
+       w0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t myvis = w0 + lane < words ? vis[w0 + lane] : 0xFFFFFFFFu;
+    unsigned open = __ballot_sync(0xffffffffu, myvis != 0xFFFFFFFFu);
+    while (open) {
+      const int j = __ffs(open) - 1;
+      open &= open - 1;
+      const uint64_t w = w0 + uint64_t(j);
+      const uint32_t vw = __shfl_sync(0xffffffffu, myvis, j);
+      const uint64_t r = w * 32 + lane;
+      bool found = false;
+      if (r < rows && !((vw >> lane) & 1u)) {
+        const uint64_t b = ptr[r], e = ptr[r + 1];
+        for (uint64_t k = b; k < e; ++k) {
+          const uint32_t u = __ldg(&idx[k]);
+          ++ex;
+          if ((__ldg(&fb[u >> 5]) >> (u & 31u)) & 1u) {
+            found = true;
+            break;
+          }
+        }
       }
+      const unsigned bits = __ballot_sync(0xffffffffu, found);
+      if (lane == 0 && bits) nxt[w] = bits;  // nxt was cleared for the pull
     }
   }
   warp_add_u64(&ctr[2], ex);
@@ -764,29 +943,42 @@ __global__ void k_db_claims(PeerTab<uint32_t> claims, int P, uint64_t w0, uint64
   }
 }
 
+// new = next & ~visited: levels, visited, and nxt keeps the new bits (the
+// frontier block of the next superstep: published before a pull, queued
+// before a push); no queue appends here (one atomic per word of a 66 M-vertex
+// level serialised on the counter: 6 ms at scale 28)
 __global__ void k_db_finish(uint32_t* nxt, uint32_t* vis, uint64_t words, uint64_t rows,
-                            int32_t lvl, int32_t* level, const uint64_t* ptr, uint32_t* queue,
+                            int32_t lvl, int32_t* level, const uint64_t* ptr,
                             unsigned long long* ctr) {
+  // a warp takes 32 consecutive words (coalesced), then each nonzero word in
+  // turn with lane = row (coalesced level writes and degree reads)
   unsigned long long f = 0, fe = 0;
-  for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < words;
-       w += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t nw = nxt[w] & ~vis[w];
-    if (w * 32 + 32 > rows && rows < w * 32 + 32) nw &= rows > w * 32 ? (~0u >> (32 - (rows - w * 32))) : 0u;
-    nxt[w] = nw;
-    if (!nw) continue;
-    vis[w] |= nw;
-    const unsigned c = __popc(nw);
-    const unsigned long long base = atomicAdd(&ctr[3], (unsigned long long)c);
-    unsigned k = 0;
-    while (nw) {
-      const int b = __ffs(nw) - 1;
-      nw &= nw - 1;
-      const uint64_t r = w * 32 + uint64_t(b);
-      level[r] = lvl;
-      fe += ptr[r + 1] - ptr[r];
-      queue[base + k++] = uint32_t(r);
+  const unsigned lane = lane_id();
+  for (uint64_t w0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~uint64_t(31); w0 < words;
+       w0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t wl = w0 + lane;
+    uint32_t mine = 0;
+    if (wl < words) {
+      const uint32_t x = nxt[wl];
+      if (x) {
+        mine = x & ~vis[wl];
+        if (wl * 32 + 32 > rows) mine &= rows > wl * 32 ? (~0u >> (32 - (rows - wl * 32))) : 0u;
+        nxt[wl] = mine;
+        vis[wl] |= mine;
+      }
     }
-    f += c;
+    unsigned nz = __ballot_sync(0xffffffffu, mine != 0u);
+    while (nz) {
+      const int j = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t nw = __shfl_sync(0xffffffffu, mine, j);
+      if ((nw >> lane) & 1u) {
+        const uint64_t r = (w0 + uint64_t(j)) * 32 + lane;
+        level[r] = lvl;
+        fe += ptr[r + 1] - ptr[r];
+        ++f;
+      }
+    }
   }
   warp_add_u64(&ctr[0], f);
   warp_add_u64(&ctr[1], fe);
@@ -813,6 +1005,8 @@ DBfsState& dbfs_state(DGraph& g) {
   st.vis.resize(static_cast<size_t>(L));
   st.nxt.resize(static_cast<size_t>(L));
   st.queue.resize(static_cast<size_t>(L));
+  st.qdeg.resize(static_cast<size_t>(L));
+  st.iso.resize(static_cast<size_t>(L));
   st.ctr.resize(static_cast<size_t>(L));
   st.sum.resize(static_cast<size_t>(L));
   const uint64_t words_all = (g.n + 31) / 32;
@@ -825,6 +1019,11 @@ DBfsState& dbfs_state(DGraph& g) {
     st.vis[size_t(l)].alloc(words + 1, s);
     st.nxt[size_t(l)].alloc(words + 1, s);
     st.queue[size_t(l)].alloc(rows + 1, s);
+    st.qdeg[size_t(l)].alloc(rows + 2, s);
+    st.iso[size_t(l)].alloc(words + 1, s);
+    launch(words, s, [&](unsigned gr, unsigned bl) {
+      k_db_isolated<<<gr, bl, 0, s>>>(g.sh[size_t(l)].in.ptr.get(), rows, st.iso[size_t(l)].get());
+    });
     st.ctr[size_t(l)].alloc(4, s);
     st.sum[size_t(l)].alloc(4, s);
     st.nxt[size_t(l)].zero(s);
@@ -889,7 +1088,8 @@ std::vector<gm_iteration_stats> dbfs(DGraph& g, uint64_t root, int64_t max_iters
     k_db_init<<<grid_for(std::max(rows, words) + 1, kBlock), kBlock, 0, s>>>(
         st.level[size_t(l)].get(), rows, st.vis[size_t(l)].get(), st.nxt[size_t(l)].get(), words,
         owns ? root - sh.lo : 0,
-        owns, st.queue[size_t(l)].get(), st.ctr[size_t(l)].get(), sh.in.ptr.get());
+        owns, st.queue[size_t(l)].get(), st.ctr[size_t(l)].get(), sh.in.ptr.get(),
+        st.iso[size_t(l)].get());
     GM_LAUNCH_CHECK();
   }
   std::vector<const uint64_t*> cin;
@@ -934,24 +1134,43 @@ std::vector<gm_iteration_stats> dbfs(DGraph& g, uint64_t root, int64_t max_iters
       c.set(0);
       GM_CUDA(cudaEventRecord(tm.e[2], c.st[0]));
     }
-    c.set(0);
-    GM_CUDA(cudaEventRecord(tm.e[3], c.st[0]));
-    const double publish_ms = -1;  // placeholder: measured below
-    (void)publish_ms;
+    // push: every shard's frontier rows as a queue with degree offsets (one
+    // host read of the queue lengths: the scan and the grid need them)
+    std::vector<uint64_t> nq(static_cast<size_t>(L), 0);
+    if (nd == kPush) {
+      for (int l = 0; l < L; ++l) {
+        c.set(l);
+        cudaStream_t s = c.st[size_t(l)];
+        DShard& sh = g.sh[size_t(l)];
+        const uint64_t words = (sh.hi - sh.lo + 31) / 32;
+        GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get() + 3, 0, 8, s));
+        launch(words, s, [&](unsigned gr, unsigned bl) {
+          k_db_queue<<<gr, bl, 0, s>>>(st.nxt[size_t(l)].get(), words, sh.in.ptr.get(),
+                                       st.queue[size_t(l)].get(), st.qdeg[size_t(l)].get(),
+                                       st.ctr[size_t(l)].get() + 3);
+        });
+        GM_CUDA(cudaMemcpyAsync(&h[3], st.ctr[size_t(l)].get() + 3, 8, cudaMemcpyDeviceToHost, s));
+        GM_CUDA(cudaStreamSynchronize(s));
+        nq[size_t(l)] = h[3];
+        GM_CUDA(cudaMemsetAsync(st.qdeg[size_t(l)].get() + nq[size_t(l)], 0, 8, s));
+        exclusive_scan_u64(st.qdeg[size_t(l)].get(), nq[size_t(l)] + 1, s);
+      }
+    }
     for (int l = 0; l < L; ++l) {
       c.set(l);
       cudaStream_t s = c.st[size_t(l)];
       DShard& sh = g.sh[size_t(l)];
       const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
       if (l == 0) GM_CUDA(cudaEventRecord(tm.e[0], s));
-      // the queue length (ctr[3]) of the last finish is read by the push
-      GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get(), 0, 24, s));
+      GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get(), 0, 32, s));
       if (nd == kPush) {
-        k_db_push<<<148 * 4, 256, 0, s>>>(st.queue[size_t(l)].get(), st.ctr[size_t(l)].get(),
-                                          sh.in.ptr.get(), sh.in.idx.get(), sh.lo, sh.hi,
-                                          st.vis[size_t(l)].get(), st.nxt[size_t(l)].get(),
-                                          static_cast<uint32_t*>(st.claims[size_t(l)]), n);
-        GM_LAUNCH_CHECK();
+        if (nq[size_t(l)]) {
+          k_db_push<<<grid_for(std::max<uint64_t>(ef, 1), 256), 256, 0, s>>>(
+              st.queue[size_t(l)].get(), st.qdeg[size_t(l)].get(), nq[size_t(l)], sh.in.ptr.get(),
+              sh.in.idx.get(), sh.lo, sh.hi, st.vis[size_t(l)].get(), st.nxt[size_t(l)].get(),
+              static_cast<uint32_t*>(st.claims[size_t(l)]), n);
+          GM_LAUNCH_CHECK();
+        }
       } else {
         // nxt holds the published frontier block: clear it for the claims
         if (words) GM_CUDA(cudaMemsetAsync(st.nxt[size_t(l)].get(), 0, words * 4, s));
@@ -983,11 +1202,10 @@ std::vector<gm_iteration_stats> dbfs(DGraph& g, uint64_t root, int64_t max_iters
       cudaStream_t s = c.st[size_t(l)];
       DShard& sh = g.sh[size_t(l)];
       const uint64_t rows = sh.hi - sh.lo, words = (rows + 31) / 32;
-      GM_CUDA(cudaMemsetAsync(st.ctr[size_t(l)].get() + 3, 0, 8, s));
-      launch(words, s, [&](unsigned gr, unsigned bl) {
+      launch(words * 32, s, [&](unsigned gr, unsigned bl) {
         k_db_finish<<<gr, bl, 0, s>>>(st.nxt[size_t(l)].get(), st.vis[size_t(l)].get(), words, rows,
                                       int32_t(it), st.level[size_t(l)].get(), sh.in.ptr.get(),
-                                      st.queue[size_t(l)].get(), st.ctr[size_t(l)].get());
+                                      st.ctr[size_t(l)].get());
       });
     }
     c.allreduce_u64(cin, cout_, 4);

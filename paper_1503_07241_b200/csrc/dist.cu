@@ -183,10 +183,78 @@ __global__ void k_src_degree(const uint32_t* idx, uint64_t nnz, uint32_t* deg) {
     atomicAdd(&deg[idx[e]], 1u);
 }
 
-__global__ void k_nonzero_u32(const uint32_t* deg, uint64_t n, uint32_t* flag) {
-  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
-       v += uint64_t(gridDim.x) * blockDim.x)
-    flag[v] = deg[v] > 0;
+__global__ void k_row_col_keys(const uint64_t* ptr, const uint32_t* idx, uint64_t rows, unsigned cb,
+                               uint64_t* keys) {
+  const uint64_t wp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = wp; r < rows; r += nw)
+    for (uint64_t e = ptr[r] + lane_id(); e < ptr[r + 1]; e += 32) keys[e] = (r << cb) | idx[e];
+}
+
+__global__ void k_rebase_ptr2(const uint64_t* ptr, uint64_t n, uint64_t base, uint64_t* out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = ptr[i] - base;
+}
+
+__global__ void k_low_cols(const uint64_t* keys, uint64_t m, unsigned cb, uint32_t* idx) {
+  const uint64_t mask = (uint64_t(1) << cb) - 1;
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x)
+    idx[e] = uint32_t(keys[e] & mask);
+}
+
+// Each row's entries ascending (a value-less CSR), in chunks of ~2^30 entries.
+void sort_row_entries(Csr& a, unsigned cb, cudaStream_t s) {
+  const uint64_t rows = a.n;
+  if (a.nnz < 2) return;
+  const uint64_t per = std::max<uint64_t>(1, rows * (uint64_t(1) << 30) / a.nnz);
+  for (uint64_t r0 = 0; r0 < rows; r0 += per) {
+    const uint64_t r1 = std::min(rows, r0 + per);
+    uint64_t e[2];
+    GM_CUDA(cudaMemcpyAsync(&e[0], a.ptr.get() + r0, 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaMemcpyAsync(&e[1], a.ptr.get() + r1, 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA(cudaStreamSynchronize(s));
+    const uint64_t m = e[1] - e[0];
+    unsigned rb = 1;
+    while ((uint64_t(1) << rb) < (r1 - r0) + 1) ++rb;
+    if (m < 2 || rb + cb > 64) continue;
+    DevBuf<uint64_t> lptr(r1 - r0 + 1, s), keys(m, s);
+    launch(r1 - r0 + 1, s, [&](unsigned gr, unsigned bl) {
+      k_rebase_ptr2<<<gr, bl, 0, s>>>(a.ptr.get() + r0, r1 - r0 + 1, e[0], lptr.get());
+    });
+    launch((r1 - r0) * 32, s, [&](unsigned gr, unsigned bl) {
+      k_row_col_keys<<<gr, bl, 0, s>>>(lptr.get(), a.idx.get() + e[0], r1 - r0, cb, keys.get());
+    });
+    sort_keys_u64(keys, int64_t(m), int(rb + cb), s);
+    launch(m, s, [&](unsigned gr, unsigned bl) {
+      k_low_cols<<<gr, bl, 0, s>>>(keys.get(), m, cb, a.idx.get() + e[0]);
+    });
+    GM_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+__global__ void k_pack_keys(const uint32_t* od, uint64_t n, uint64_t* keys) {
+  for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n;
+       u += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t d = od[u];
+    const uint64_t cls = d ? uint64_t(1 + 31 - __clz(int(d))) : 0;  // 0 = no out-edges: last
+    keys[u] = ((63 - cls) << 32) | u;
+  }
+}
+
+__global__ void k_pack_map(const uint64_t* keys, uint64_t n, uint64_t* pmap) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    pmap[keys[i] & 0xFFFFFFFFull] = i;
+}
+
+__global__ void k_count_senders(const uint32_t* od, uint64_t n, unsigned long long* cnt) {
+  unsigned long long c = 0;
+  for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n;
+       u += uint64_t(gridDim.x) * blockDim.x)
+    c += od[u] > 0;
+  warp_add_u64(cnt, c);
 }
 
 __global__ void k_block_pids(const uint32_t* od, const uint64_t* pmap, uint64_t lo, uint64_t rows,
@@ -439,14 +507,27 @@ void finish_directed(DGraph& g) {
     if (sh.hi > sh.lo)
       GM_CUDA(cudaMemcpyAsync(sh.outdeg.get(), od + sh.lo, (sh.hi - sh.lo) * 4,
                               cudaMemcpyDeviceToDevice, s));
-    // packed id of u = number of vertices with out-edges before u
-    DevBuf<uint32_t> flag(n, s);
+    // packed id of u = its rank among the vertices with out-edges, hub-first:
+    // by out-degree class (floor(log2 d), descending), then caller id -- a
+    // P-independent order (every shard computes the same map from the summed
+    // degrees) that puts the hubs' messages together at the front of x
     DevBuf<uint64_t> pmap(n + 1, s);
-    launch(n, s, [&](unsigned gr, unsigned bl) { k_nonzero_u32<<<gr, bl, 0, s>>>(od, n, flag.get()); });
-    scan_counts_to_ptr(flag.get(), pmap.get(), n, s);
+    {
+      DevBuf<uint64_t> keys(n, s);
+      launch(n, s, [&](unsigned gr, unsigned bl) { k_pack_keys<<<gr, bl, 0, s>>>(od, n, keys.get()); });
+      sort_keys_u64(keys, int64_t(n), 38, s);
+      launch(n, s, [&](unsigned gr, unsigned bl) { k_pack_map<<<gr, bl, 0, s>>>(keys.get(), n, pmap.get()); });
+      DevBuf<unsigned long long> cnt(1, s);
+      cnt.zero(s);
+      launch(n, s, [&](unsigned gr, unsigned bl) { k_count_senders<<<gr, bl, 0, s>>>(od, n, cnt.get()); });
+      GM_CUDA(cudaMemcpyAsync(pmap.get() + n, cnt.get(), 8, cudaMemcpyDeviceToDevice, s));
+    }
     launch(sh.in.nnz, s, [&](unsigned gr, unsigned bl) {
       k_remap_cols<<<gr, bl, 0, s>>>(sh.in.idx.get(), sh.in.nnz, pmap.get());
     });
+    // rows of a value-less graph re-sorted by packed id: hub-first gathers
+    // (and a P-independent fold order, as the ids are)
+    if (!sh.in.val) sort_row_entries(sh.in, bits_for(n + 1), s);
     sh.pid.alloc(sh.hi - sh.lo + 1, s);
     launch(sh.hi - sh.lo, s, [&](unsigned gr, unsigned bl) {
       k_block_pids<<<gr, bl, 0, s>>>(od, pmap.get(), sh.lo, sh.hi - sh.lo, sh.pid.get());
@@ -1327,19 +1408,36 @@ __device__ __forceinline__ void dpr_flush(const DPrArgs& a, const DprAcc& acc) {
   warp_add_u64(&a.part[2], acc.upd);
 }
 
-__global__ void __launch_bounds__(256) k_dpr_short(DPrArgs a, const uint32_t* rows, uint64_t nr) {
+// Rows of <= kPrShort entries, a thread per row in row order (neighbouring
+// threads read neighbouring offsets, ranks and packed ids), the entries
+// folded in stored order with four gathers in flight.  Longer rows are left
+// to the chunk path.  (A group of 8 lanes per row was slower: most rows have
+// a few entries -- 79 -> 47 GTEPS at scale 28.)
+__global__ void __launch_bounds__(256) k_dpr_short(DPrArgs a, uint64_t rows) {
   const float base = dpr_base(a);
   DprAcc acc;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nr;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t r = rows[i];
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < rows;
+       r += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t b = a.ptr[r], e = a.ptr[r + 1];
+    if (e - b > kPrShort) continue;
     float s = 0.0f;
-    for (uint64_t k = b; k < e; ++k) {
+    uint64_t k = b;
+    for (; k + 4 <= e; k += 4) {
+      const uint32_t i0 = __ldg(&a.idx[k]), i1 = __ldg(&a.idx[k + 1]);
+      const uint32_t i2 = __ldg(&a.idx[k + 2]), i3 = __ldg(&a.idx[k + 3]);
+      GM_DCHECK(i0 < a.nx && i1 < a.nx && i2 < a.nx && i3 < a.nx);
+      const float x0 = __ldg(&a.x[i0]), x1 = __ldg(&a.x[i1]);
+      const float x2 = __ldg(&a.x[i2]), x3 = __ldg(&a.x[i3]);
+      s += x0;
+      s += x1;
+      s += x2;
+      s += x3;
+    }
+    for (; k < e; ++k) {
       GM_DCHECK(a.idx[k] < a.nx);
       s += __ldg(&a.x[__ldg(&a.idx[k])]);
     }
-    dpr_apply(a, r, s, base, e > b, acc);
+    dpr_apply(a, uint32_t(r), s, base, e > b, acc);
   }
   dpr_flush(a, acc);
 }
@@ -1569,8 +1667,8 @@ std::vector<gm_iteration_stats> dpagerank(DGraph& g, double damping, int64_t ite
             st.chunk_sum[size_t(l)].get());
         GM_LAUNCH_CHECK();
       }
-      launch(st.n_short[size_t(l)], s, [&](unsigned gr, unsigned bl) {
-        k_dpr_short<<<gr, bl, 0, s>>>(a, st.rows_short[size_t(l)].get(), st.n_short[size_t(l)]);
+      launch(sh.hi - sh.lo, s, [&](unsigned gr, unsigned bl) {
+        k_dpr_short<<<gr, bl, 0, s>>>(a, sh.hi - sh.lo);
       });
       launch(st.n_long[size_t(l)], s, [&](unsigned gr, unsigned bl) {
         k_dpr_long<<<gr, bl, 0, s>>>(a, st.rows_long[size_t(l)].get(), st.n_long[size_t(l)],

@@ -2014,21 +2014,34 @@ __global__ void __launch_bounds__(256) k_ds_pull(const uint64_t* __restrict__ pt
 __global__ void k_ds_finish(const uint32_t* chg, uint64_t words, uint64_t rows, const uint32_t* dist,
                             const uint32_t* outdeg, uint32_t* queue, uint32_t* qd,
                             unsigned long long* ctr) {
+  // lanes = 32 consecutive words; one queue reservation per warp (an atomic
+  // per word with changes serialised on the counter)
   unsigned long long f = 0, fe = 0;
-  for (uint64_t wd = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; wd < words;
-       wd += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t b = chg[wd];
-    if (!b) continue;
-    const unsigned long long base = atomicAdd(&ctr[3], (unsigned long long)__popc(b));
-    unsigned k = 0;
+  const unsigned lane = lane_id();
+  for (uint64_t w0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~uint64_t(31); w0 < words;
+       w0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t wd = w0 + lane;
+    uint32_t b = wd < words ? chg[wd] : 0u;
+    const unsigned c = __popc(b);
+    unsigned incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= unsigned(o)) incl += t;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (!tot) continue;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(&ctr[3], (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31) + (incl - c);
     while (b) {
       const int i = __ffs(b) - 1;
       b &= b - 1;
       const uint64_t r = wd * 32 + uint64_t(i);
       GM_DCHECK(r < rows);
-      queue[base + k] = uint32_t(r);
-      qd[base + k] = dist[r];
-      ++k;
+      queue[base] = uint32_t(r);
+      qd[base] = dist[r];
+      ++base;
       ++f;
       fe += outdeg[r];
     }

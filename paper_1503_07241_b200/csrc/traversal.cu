@@ -680,7 +680,8 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
     if (vc->done) break;
     const int32_t it = vc->it + 1;
     const int cur = it & 1;
-    const uint64_t nf = vc->nf, mf = vc->mf;
+    const uint64_t nf = vc->nf;
+    uint64_t mf = vc->mf;  // after a pull: 0 until the queue conversion counts it
     const bool pull = it == 1 ? false
                               : (vc->prev_pull ? nf * 24 >= a.n : double(mf) > 0.05 * double(a.m));
     if (gtid == 0 && it <= kMaxRecorded) {
@@ -767,6 +768,9 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         }
         grid.sync();
         if (gtid == 0 && it <= kMaxRecorded) a.ctl->t_mid[it - 1] = globaltimer();
+        // the frontier's edges, counted by the conversion (a pull no longer
+        // sums the degrees of what it finds: only a following push needs them)
+        mf = vc->bpack & kEdgeMask;
       }
       coop_push(a, cur, nf, mf, it, gwarp, nwarps);
     } else {
@@ -804,10 +808,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
           const bool open = v < a.nv && !((vw >> lane) & 1u);
           if (open) {
             found = coop_probe_row(a, s_fb, sw, fbc, v, hv, defer, rest, examined);
-            if (found) {
-              a.level[v] = it;
-              found_e += __ldg(&a.deg[v]);
-            }
+            if (found) a.level[v] = it;
           }
           const unsigned b = __ballot_sync(0xffffffffu, found);
           if (lane == 0 && b) {
@@ -843,7 +844,6 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
                 a.level[v] = it;
                 atomicOr(&fbn[v >> 5], bit);
                 atomicOr(&a.vis[v >> 5], bit);
-                found_e += __ldg(&a.deg[v]);
               }
             }
           }
@@ -925,7 +925,6 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
                 a.level[v] = it;
                 atomicOr(&a.vis[v >> 5], bit);
                 ++found_n;
-                found_e += __ldg(&a.deg[v]);
               }
             }
           }

@@ -637,10 +637,16 @@ __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t
     if (valid != (1u << kSoa) - 1) return false;
   }
   if (hv > 1) {
+    // the row-major rest of the head in one round of loads, probed chunk by chunk
+    uint4 hh[kAosVec];
+#pragma unroll
+    for (int j = 0; j < kAosVec; ++j)
+      hh[j] = j < hv - 1 ? __ldg(&a.head[kAosVec * v + j])
+                         : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
 #pragma unroll
     for (int j = 0; j < kAosVec; ++j) {
       if (j >= hv - 1) break;
-      const uint4 h = __ldg(&a.head[kAosVec * v + j]);
+      const uint4 h = hh[j];
       const uint32_t u[4] = {h.x, h.y, h.z, h.w};
       uint32_t hit = 0, valid = 0;
 #pragma unroll

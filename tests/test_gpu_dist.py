@@ -217,3 +217,32 @@ def test_nccl_communicator_one_rank(gm, orc):
     gl.close()
     cl.close()
     cn.close()
+
+
+@pytest.mark.slow
+def test_dgraph_scale26_bitwise_p1_p2_and_single_gpu(gm):
+    """Closer to configs[4]: at R-MAT scale 26 (67 M vertices, ~2.1 G stored
+    entries symmetrised) the sharded BFS levels equal the single-GPU
+    cooperative kernel's, and levels and fp32 PageRank ranks are bitwise
+    identical for P = 1 and P = 2 (two virtual shards on this one GPU)."""
+    D = _dist()
+    ref = gm.Graph.rmat(26, 16, seed=1, symmetrize=True, relabel=True, **RMAT)
+    root = ref.pick_source(1)
+    want, _ = gm.bfs(ref, root)
+    del ref
+    levels, ranks = [], []
+    for P in (1, 2):
+        comm = D.Comm.local([0] * P)
+        g = D.DGraph.rmat(comm, 26, 16, seed=1, symmetrize=True, **RMAT)
+        assert g.pick_source(1) == root
+        lv, st = g.bfs(root)
+        levels.append(lv)
+        g.close()
+        gd = D.DGraph.rmat(comm, 26, 16, seed=1, **RMAT)
+        r, _ = gd.pagerank(0.85, 5)
+        ranks.append(r.view(np.uint32).copy())
+        gd.close()
+        comm.close()
+    assert np.array_equal(levels[0], want)
+    assert np.array_equal(levels[0], levels[1])
+    assert np.array_equal(ranks[0], ranks[1])

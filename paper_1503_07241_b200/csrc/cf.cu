@@ -263,31 +263,44 @@ __global__ void k_cf_apply(uint64_t lo, uint64_t n, int k, const uint32_t* rit, 
                            float gamma, float lambda, uint32_t* vbits,
                            unsigned long long* changed) {
   unsigned long long ch = 0;
-  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n * uint64_t(k);
-       t += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t v = t / k;
-    const int i = int(t % k);
-    float s = 0.0f;
-    const uint32_t a0 = rit[v], a1 = rit[v + 1], b0 = rif[v], b1 = rif[v + 1];
-    bool any = false;
-    for (uint32_t j = a0; j < a1; ++j) {
-      s = any ? s + part_t[uint64_t(j) * k + i] : part_t[uint64_t(j) * k + i];
-      any = true;
+  const uint64_t total = n * uint64_t(k);
+  const unsigned lane = threadIdx.x & 31u;
+  // warp-uniform trip count (the change claim below is warp-collective)
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x) + (threadIdx.x & ~31u); base < total;
+       base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t t = base + lane;
+    const bool valid = t < total;
+    const uint64_t v = valid ? t / k : ~0ull;
+    bool changed_here = false;
+    if (valid) {
+      const int i = int(t % k);
+      float s = 0.0f;
+      const uint32_t a0 = rit[v], a1 = rit[v + 1], b0 = rif[v], b1 = rif[v + 1];
+      bool any = false;
+      for (uint32_t j = a0; j < a1; ++j) {
+        s = any ? s + part_t[uint64_t(j) * k + i] : part_t[uint64_t(j) * k + i];
+        any = true;
+      }
+      float si = 0.0f;
+      bool anyi = false;
+      for (uint32_t j = b0; j < b1; ++j) {
+        si = anyi ? si + part_f[uint64_t(j) * k + i] : part_f[uint64_t(j) * k + i];
+        anyi = true;
+      }
+      if (anyi) s = any ? s + si : si;
+      const float p = f[lo * uint64_t(k) + t];
+      const float np = p + gamma * (s - lambda * p);
+      fn[t] = np;
+      changed_here = (__float_as_uint(np) != __float_as_uint(p)) && (any || anyi);
     }
-    float si = 0.0f;
-    bool anyi = false;
-    for (uint32_t j = b0; j < b1; ++j) {
-      si = anyi ? si + part_f[uint64_t(j) * k + i] : part_f[uint64_t(j) * k + i];
-      anyi = true;
-    }
-    if (anyi) s = any ? s + si : si;
-    const float p = f[lo * uint64_t(k) + t];
-    const float np = p + gamma * (s - lambda * p);
-    fn[t] = np;
     // vertices_updated counts vertices (engine.hpp:139-172: a messaged vertex
     // whose LatentVector differs in any component, collaborative_filtering.hpp:
-    // 29-35): the first component thread of v to see a change claims v's bit.
-    if ((__float_as_uint(np) != __float_as_uint(p)) && (any || anyi)) {
+    // 29-35).  The lowest changed lane of each vertex's run in the warp claims
+    // v's bit (a vertex split across warps is claimed once by the bitmap):
+    // one atomic per vertex and warp instead of one per changed component.
+    const unsigned same = __match_any_sync(0xffffffffu, v);
+    const unsigned cm = __ballot_sync(0xffffffffu, changed_here) & same;
+    if (changed_here && lane == unsigned(__ffs(cm) - 1)) {
       const uint32_t bit = 1u << (v & 31u);
       ch += !(atomicOr(&vbits[v >> 5], bit) & bit);
     }

@@ -57,6 +57,7 @@ constexpr int kCountShift = 36;  // packed counter: count << 36 | edges
 constexpr unsigned long long kEdgeMask = (1ull << kCountShift) - 1;
 
 enum Dir : int32_t { kPush = 1, kPull = 0 };
+constexpr unsigned kHdrDone = 1, kHdrPrevPull = 2, kHdrCurIsQueue = 4, kHdrUImplicit = 8, kHdrUsel = 16;
 
 struct StepRec {
   int64_t active, updated, edges, examined;
@@ -76,10 +77,15 @@ struct Ctl {
   int32_t it, dir, prev_pull, cur_is_queue, done, max_it, u_implicit, usel;
   int32_t queue_out;            // SSSP: pull supersteps also append to the queue
   uint64_t n_total, m_total, nv;
+  // BFS superstep header, written by the epilogue thread and read once per CTA
+  // (every warp reading the fields above hit one L2 line ~10K times per step):
+  // nf, mf, ucur, it | flags << 32 (kHdr*).
+  alignas(16) unsigned long long hdr[4];
   uint64_t t_start[kMaxRecorded];  // %globaltimer per superstep (cooperative kernel)
   uint64_t t_mid[kMaxRecorded];    // after the first phase (bitmap->queue / pull pass 1)
   uint64_t t_end[kMaxRecorded];
   StepRec rec[kMaxRecorded];
+  uint64_t t_entry, t_exit;        // cooperative kernel entry / exit (GM_BFS_PHASES)
 };
 
 }  // namespace
@@ -319,6 +325,10 @@ __global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t roo
     ctl->u_implicit = 1;  // first pull scans every row; later pulls the unvisited list
     ctl->usel = 0;
     ctl->ucur = 0;
+    ctl->hdr[0] = 1;
+    ctl->hdr[1] = deg[root];
+    ctl->hdr[2] = 0;
+    ctl->hdr[3] = uint64_t(kHdrCurIsQueue | kHdrUImplicit | (max_it <= 0 ? kHdrDone : 0u)) << 32;
   }
 }
 
@@ -676,20 +686,33 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint32_t s_fb[];
-  volatile Ctl* vc = a.ctl;
   const uint64_t gtid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
   const unsigned lane = lane_id();
+  __shared__ unsigned long long s_hdr[4], s_bc[2];
+  if (gtid == 0) a.ctl->t_entry = globaltimer();
   for (;;) {
     grid.sync();
-    if (vc->done) break;
-    const int32_t it = vc->it + 1;
+    if (threadIdx.x < 2) {
+      const uint4 h = __ldcg(reinterpret_cast<const uint4*>(a.ctl->hdr) + threadIdx.x);
+      s_hdr[2 * threadIdx.x] = (uint64_t(h.y) << 32) | h.x;
+      s_hdr[2 * threadIdx.x + 1] = (uint64_t(h.w) << 32) | h.z;
+    }
+    __syncthreads();
+    const unsigned flags = unsigned(s_hdr[3] >> 32);
+    if (flags & kHdrDone) break;
+    const int32_t it = int32_t(uint32_t(s_hdr[3])) + 1;
     const int cur = it & 1;
-    const uint64_t nf = vc->nf;
-    uint64_t mf = vc->mf;  // after a pull: 0 until the queue conversion counts it
+    const uint64_t nf = s_hdr[0];
+    uint64_t mf = s_hdr[1];  // after a pull: 0 until the queue conversion counts it
     const bool pull = it == 1 ? false
-                              : (vc->prev_pull ? nf * 24 >= a.n : double(mf) > 0.05 * double(a.m));
+                              : ((flags & kHdrPrevPull) ? nf * 24 >= a.n : double(mf) > 0.05 * double(a.m));
+    // A pull over a short unvisited list finds at most that many rows, so when
+    // the list is below the pull threshold the next superstep is certainly a
+    // push: the pull queues what it finds (with degrees) and the push skips
+    // the bitmap -> queue conversion.
+    const bool pull_queues = pull && !(flags & kHdrUImplicit) && s_hdr[2] * 24 < a.n;
     if (gtid == 0 && it <= kMaxRecorded) {
       a.ctl->t_start[it - 1] = globaltimer();
       a.ctl->t_mid[it - 1] = 0;
@@ -697,7 +720,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
     uint32_t* fbc = a.fb[cur];
     uint32_t* fbn = a.fb[cur ^ 1];
     if (!pull) {
-      if (!vc->cur_is_queue) {  // frontier bitmap -> queue with edge offsets
+      if (!(flags & kHdrCurIsQueue)) {  // frontier bitmap -> queue with edge offsets
         // Two passes over the warp's words: count (vertices, edges), reserve
         // the CTA's range with one atomicAdd, then write.  (Appending per warp
         // step put one atomicAdd per ~1 vertex on the single queue counter
@@ -776,23 +799,27 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         if (gtid == 0 && it <= kMaxRecorded) a.ctl->t_mid[it - 1] = globaltimer();
         // the frontier's edges, counted by the conversion (a pull no longer
         // sums the degrees of what it finds: only a following push needs them)
-        mf = vc->bpack & kEdgeMask;
+        if (threadIdx.x == 0) s_bc[0] = __ldcg(&a.ctl->bpack);
+        __syncthreads();
+        mf = s_bc[0] & kEdgeMask;
       }
       coop_push(a, cur, nf, mf, it, gwarp, nwarps);
     } else {
       // A short unvisited list probes too few words to pay for staging the
       // hot prefix of the frontier bitmap (96 KB per CTA) in shared memory.
-      const uint32_t sw = (!vc->u_implicit && vc->ucur * 64 < a.nv) ? 0u : a.s_words;
+      const bool u_implicit = flags & kHdrUImplicit;
+      const uint64_t ucur_n = s_hdr[2];
+      const uint32_t sw = (!u_implicit && ucur_n * 64 < a.nv) ? 0u : a.s_words;
       for (uint32_t i = threadIdx.x; i < sw; i += blockDim.x) s_fb[i] = __ldcg(&fbc[i]);
       __syncthreads();
       unsigned long long found_n = 0, found_e = 0, examined = 0;
-      const int us = vc->usel;
+      const int us = (flags & kHdrUsel) ? 1 : 0;
       uint32_t* unext = a.ul[us ^ 1];
       // A large frontier leaves few rows unvisited: only then is the list of
       // the remaining rows worth building for the next pull.
       const bool build_list = a.use_ulist && nf * 16 >= a.n;
       const int hv = nf * 32 >= a.n ? 1 : kHeadVec;
-      if (vc->u_implicit) {
+      if (u_implicit) {
         const uint64_t words = (a.nv + 31) / 32;
         // Words are dealt round-robin (warp g owns g, g + nwarps, ...) so every
         // warp gets a statistically equal share; lanes prefetch the visited
@@ -834,7 +861,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
          }
         }
       } else {
-        const uint64_t cnt = vc->ucur;
+        const uint64_t cnt = ucur_n;
         const uint32_t* ucur = a.ul[us];
         for (uint64_t base = gwarp * 32; base < cnt; base += nwarps * 32) {
           const uint64_t i = base + lane;
@@ -854,6 +881,16 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
             }
           }
           found_n += found;
+          if (pull_queues && __any_sync(0xffffffffu, found)) {
+            uint64_t ps = 0;
+            uint32_t dg = 0;
+            if (found) {
+              ps = __ldg(&a.out_ptr[v]);
+              dg = uint32_t(__ldg(&a.out_ptr[v + 1]) - ps);
+            }
+            warp_enqueue_multi<1>(found ? 1u : 0u, &v, &dg, &ps, &a.ctl->qpack, a.q[cur ^ 1],
+                                  a.offs[cur ^ 1], a.qe[cur ^ 1]);
+          }
           if (__any_sync(0xffffffffu, defer)) {
             const uint64_t es = defer ? __ldg(&a.in_ptr[v]) + 4u * hv : 0;
             warp_enqueue_multi<1>(defer ? 1u : 0u, &v, &rest, &es, &a.ctl->dpack, a.defq, a.defo,
@@ -868,7 +905,9 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
       if (gtid == 0 && it <= kMaxRecorded) a.ctl->t_mid[it - 1] = globaltimer();
       // pass 2: edge-balanced over the deferred rows' remaining in-edges:
       // resolve the slots, put every column load in flight, then probe.
-      const unsigned long long dp = vc->dpack;
+      if (threadIdx.x == 0) s_bc[1] = __ldcg(&a.ctl->dpack);
+      __syncthreads();
+      const unsigned long long dp = s_bc[1];
       const uint32_t ndef = uint32_t(dp >> kCountShift);
       const uint64_t total = dp & kEdgeMask;
       const uint64_t e_lo = total * gwarp / nwarps, e_hi = total * (gwarp + 1) / nwarps;
@@ -918,6 +957,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         uint32_t done_w[kEPT];
 #pragma unroll
         for (int k = 0; k < kEPT; ++k) done_w[k] = k < nk ? __ldcg(&fbn[rv[k] >> 5]) : 0xFFFFFFFFu;
+        unsigned won = 0;
 #pragma unroll
         for (int k = 0; k < kEPT; ++k) {
           const uint32_t bit = 1u << (rv[k] & 31u);
@@ -931,9 +971,25 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
                 a.level[v] = it;
                 atomicOr(&a.vis[v >> 5], bit);
                 ++found_n;
+                won |= 1u << k;
               }
             }
           }
+        }
+        if (pull_queues && __any_sync(0xffffffffu, won != 0u)) {
+          uint64_t ps[kEPT];
+          uint32_t dg[kEPT];
+#pragma unroll
+          for (int k = 0; k < kEPT; ++k) {
+            ps[k] = 0;
+            dg[k] = 0;
+            if ((won >> k) & 1u) {
+              ps[k] = __ldg(&a.out_ptr[rv[k]]);
+              dg[k] = uint32_t(__ldg(&a.out_ptr[rv[k] + 1]) - ps[k]);
+            }
+          }
+          warp_enqueue_multi<kEPT>(won, rv, dg, ps, &a.ctl->qpack, a.q[cur ^ 1], a.offs[cur ^ 1],
+                                   a.qe[cur ^ 1]);
         }
       }
       warp_add_u64(&a.ctl->found_n, found_n);
@@ -945,14 +1001,18 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
     for (uint64_t w = gtid; w < a.words_all; w += gthreads) fbc[w] = 0u;
     if (gtid == 0) {
       Ctl* c = a.ctl;
-      uint64_t nn, mn;
-      if (!pull) {
+      uint64_t nn = 0, mn = 0;
+      GM_DCHECK(!pull_queues || (c->qpack >> kCountShift) == c->found_n);
+      if (!pull || pull_queues) {
         nn = c->qpack >> kCountShift;
         mn = c->qpack & kEdgeMask;
         a.offs[cur ^ 1][nn] = mn;
-      } else {
-        nn = c->found_n;
-        mn = c->found_e;
+      }
+      if (pull) {
+        if (!pull_queues) {
+          nn = c->found_n;
+          mn = c->found_e;
+        }
         c->ucur = c->upack >> kCountShift;
         const bool built = a.use_ulist && nf * 16 >= a.n;
         c->u_implicit = built ? 0 : 1;
@@ -970,16 +1030,26 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
         c->t_end[it - 1] = globaltimer();
       }
       c->prev_pull = pull;
-      c->cur_is_queue = !pull;
+      c->cur_is_queue = !pull || pull_queues;
       c->nf = nn;
       c->mf = mn;
       c->it = it;
       c->qpack = c->dpack = c->bpack = c->upack = 0;
       c->found_n = c->found_e = c->examined = 0;
       if (nn == 0 || it >= c->max_it) c->done = 1;
+      c->hdr[0] = nn;
+      c->hdr[1] = mn;
+      c->hdr[2] = c->ucur;
+      c->hdr[3] = uint64_t(uint32_t(it)) |
+                  (uint64_t((c->done ? kHdrDone : 0u) | (pull ? kHdrPrevPull : 0u) |
+                            (pull && !pull_queues ? 0u : kHdrCurIsQueue) |
+                            (c->u_implicit ? kHdrUImplicit : 0u) |
+                            (c->usel ? kHdrUsel : 0u))
+                   << 32);
       __threadfence();
     }
   }
+  if (gtid == 0) a.ctl->t_exit = globaltimer();
 }
 
 // ------------------------------------------------------------------- SSSP
@@ -1473,6 +1543,13 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
     std::vector<uint64_t> tm(rec.size());
     if (nrec > 0 && getenv("GM_BFS_PHASES")) {
       GM_CUDA(cudaMemcpy(tm.data(), ctl->t_mid, nrec * 8, cudaMemcpyDeviceToHost));
+      uint64_t te[2];
+      GM_CUDA(cudaMemcpy(te, &ctl->t_entry, 16, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "bfs kernel entry->step1 %.1fus, last step end->exit %.1fus, entry->exit %.1fus\n",
+              double(t0[0] - te[0]) * 1e-3, double(te[1] - t1[nrec - 1]) * 1e-3,
+              double(te[1] - te[0]) * 1e-3);
+      for (int64_t i = 1; i < nrec; ++i)
+        fprintf(stderr, "bfs gap before step %lld: %.1fus\n", (long long)(i + 1), double(t0[i] - t1[i - 1]) * 1e-3);
       for (int64_t i = 0; i < nrec; ++i)
         fprintf(stderr, "bfs step %lld dir=%d phase1=%.1fus total=%.1fus examined=%lld deferred=%lld/%lld\n",
                 (long long)(i + 1), rec[i].dir, tm[i] ? double(tm[i] - t0[i]) * 1e-3 : 0.0,

@@ -12,8 +12,15 @@ g = gm.Graph.rmat(28, 16, seed=1, symmetrize=True, relabel=True, a=0.57, b=0.19,
 r = g.pick_source(1)
 for _ in range(2): gm.bfs(g, r)
 " > gpurun_out/${tag}_phases28.log 2>&1
+GM_BFS_PHASES=1 timeout 600 python -c "
+import paper_1503_07241_b200 as gm
+g = gm.Graph.rmat(23, 16, seed=1, symmetrize=True, relabel=True, a=0.57, b=0.19, c=0.19)
+r = g.pick_source(1)
+for _ in range(3): gm.bfs(g, r)
+" > gpurun_out/${tag}_phases23.log 2>&1
 tail -3 gpurun_out/${tag}_tests.log
 for f in gpurun_out/${tag}_bench_*.json; do echo $f; python -c "
 import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(d.get('value'), d.get('ms_per_step'), (d.get('roofline') or {}).get('frac'), (d.get('roofline') or {}).get('launch_us'), d.get('e2e',{}).get('value'))
 for s in d['per_superstep']: print('  ', s)" $f || tail -5 ${f%.json}.err; done
 tail -12 gpurun_out/${tag}_phases28.log
+tail -16 gpurun_out/${tag}_phases23.log

@@ -50,7 +50,8 @@ namespace {
 constexpr int kMaxRecorded = 4096;  // per-superstep records kept on device
 constexpr int kBatch = 4;           // supersteps enqueued per host check
 constexpr int kEPT = 4;             // edges per thread, edge-balanced passes
-constexpr uint32_t kSmemFbWords = 24 * 1024;  // 96 KB of frontier bitmap per CTA
+// Frontier-bitmap prefix staged per CTA: 96 KB at 2 CTAs per SM, 64 KB at 3.
+constexpr uint32_t smem_fb_words(int blocks_per_sm) { return blocks_per_sm >= 3 ? 16 * 1024 : 24 * 1024; }
 constexpr unsigned kGrid = 148 * 2;           // persistent grid for the SSSP kernels
 constexpr unsigned kThreads = 1024;
 constexpr int kCountShift = 36;  // packed counter: count << 36 | edges
@@ -104,6 +105,7 @@ struct TravCache {
   DevBuf<uint64_t> qe[2];       // start-edge pointers parallel to q
   DevBuf<uint64_t> defe;        // pull: deferred rows' next unprobed edge
   unsigned coop_grid = 0;
+  int coop_blocks_per_sm = 0;  // k_bfs_coop variant, fixed at the first BFS
   DevBuf<uint64_t> defo;        // pull: their exclusive remaining-edge offsets
   DevBuf<uint32_t> vis, fb[2];  // visited / frontier bitmaps (cur = it & 1)
   DevBuf<uint32_t> changed;     // SSSP changed-bitmap
@@ -682,7 +684,13 @@ __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t
   return false;
 }
 
-__global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
+// kBlocksPerSm: 2 (64 registers, 32 warps per SM) or 3 (40 registers, 48
+// warps): the large graphs' pulls are latency-bound and gain from the warps
+// (scale 28: 994 -> 1036 GTEPS); small graphs lose more on the wider grid
+// barriers than they gain (scale 23: 399 -> 388).  4 blocks (32 registers)
+// spills too much (scale 28: 815).
+template <int kBlocksPerSm>
+__global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint32_t s_fb[];
@@ -834,6 +842,16 @@ __global__ void __launch_bounds__(kCoopThreads, 2) k_bfs_coop(CoopArgs a) {
           const int j = __ffs(open_words) - 1;
           open_words &= open_words - 1;
           const uint64_t w = gwarp + (k0 + j) * nwarps;
+          // L2 prefetch of the next open word's head slots (no registers held:
+          // the next iteration's slot loads then hit L2 instead of DRAM)
+          if (open_words && lane < 2u * kSoa) {
+            const unsigned k = lane >> 1;
+            if (hv > 1 || k == 0) {
+              const uint64_t w2 = gwarp + (k0 + __ffs(open_words) - 1) * nwarps;
+              const uint32_t* p = a.hsoa + k * a.hstride + w2 * 32 + ((lane & 1u) ? 31 : 0);
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+            }
+          }
           const uint32_t vw = __shfl_sync(0xffffffffu, myvis, j);
           const uint64_t v = w * 32 + lane;
           bool found = false, defer = false;
@@ -1455,8 +1473,16 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   // Pull rows: on a relabeled symmetric graph only the nonzero-degree prefix
   // can ever be reached.
   const uint64_t nv = (g.relabeled && g.symmetric && g.shards == 1) ? g.nonzero_outdeg : n;
-  const uint32_t s_words = uint32_t(std::min<uint64_t>(kSmemFbWords, (nv + 31) / 32));
-  const size_t smem = size_t(kSmemFbWords) * 4;
+  if (!c.coop_blocks_per_sm) {
+    const char* e = getenv("GM_BFS_CTAS_PER_SM");  // test hook: force a variant
+    const int forced = e ? atoi(e) : 0;
+    c.coop_blocks_per_sm = (forced == 2 || forced == 3) ? forced : (n > (uint64_t(1) << 24) ? 3 : 2);
+  }
+  const int blocks_per_sm = c.coop_blocks_per_sm;
+  void* const coop_fn = blocks_per_sm == 3 ? reinterpret_cast<void*>(k_bfs_coop<3>)
+                                           : reinterpret_cast<void*>(k_bfs_coop<2>);
+  const uint32_t s_words = uint32_t(std::min<uint64_t>(smem_fb_words(blocks_per_sm), (nv + 31) / 32));
+  const size_t smem = size_t(smem_fb_words(blocks_per_sm)) * 4;
   if (!c.level) {
     c.level.alloc(n, s);
     c.hsoa.alloc(size_t(kSoa) * (nv + 1), s);
@@ -1466,13 +1492,13 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
                                                       c.hsoa.get(), c.head.get());
       GM_LAUNCH_CHECK();
     }
-    GM_CUDA(cudaFuncSetAttribute(k_bfs_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    GM_CUDA(cudaFuncSetAttribute(coop_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0, dev = 0, sms = 0;
-    GM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_coop, kCoopThreads, smem));
+    GM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_fn, kCoopThreads, smem));
     GM_CUDA(cudaGetDevice(&dev));
     GM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (per_sm < 1) fail(GM_ECUDA, "bfs: cooperative kernel does not fit on an SM");
-    c.coop_grid = unsigned(std::min(per_sm, 2) * sms);
+    c.coop_grid = unsigned(std::min(per_sm, blocks_per_sm) * sms);
   }
   ensure_forward(g);
   const Csr& fw = g.fwd();
@@ -1522,7 +1548,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   }
   void* args[] = {&a};
   g.ktimer.begin(s, "k_bfs_coop");
-  GM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs_coop), dim3(c.coop_grid),
+  GM_CUDA(cudaLaunchCooperativeKernel(coop_fn, dim3(c.coop_grid),
                                       dim3(kCoopThreads), args, smem, s));
   g.ktimer.end(s);
   ::gm::count_launch();

@@ -1032,3 +1032,20 @@ def test_bfs_host_async_output(gm, orc):
     assert np.array_equal(bufs[0].numpy(), want)
     with pytest.raises(ValueError):
         gm.bfs(g, roots[0], out=bufs[0].numpy(), sync=False)  # stats need the host
+
+
+@pytest.mark.parametrize("ctas", ["2", "3"])
+def test_bfs_coop_variants(gm, orc, ctas, monkeypatch):
+    """Both k_bfs_coop occupancy variants (2 CTAs x 64 registers, 3 CTAs x 40
+    registers per SM; the library picks by graph size) give the reference's
+    levels and per-superstep stats, including the pull -> queued push switch."""
+    monkeypatch.setenv("GM_BFS_CTAS_PER_SM", ctas)  # read at a graph's first BFS
+    g = gm.Graph.rmat(18, 16, seed=3, symmetrize=True, relabel=True)
+    s, d, _ = g.edges()
+    for seed in (1, 2):
+        root = g.pick_source(seed)
+        lvl, st = gm.bfs(g, root)
+        want, wst = orc.bfs(g.num_vertices, s, d, root, presorted=True)
+        assert np.array_equal(lvl, want)
+        assert [x.key() for x in st] == wst
+    assert {"push", "pull"} <= {x.direction for x in st}

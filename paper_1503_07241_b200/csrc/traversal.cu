@@ -75,6 +75,7 @@ struct Ctl {
   unsigned long long found_n, found_e, examined;
   unsigned long long nf, mf;    // current frontier: vertices, edges
   unsigned long long ucur;      // current unvisited-row list length
+  unsigned int wcursor;         // implicit pull: next unclaimed visited-bitmap word
   int32_t it, dir, prev_pull, cur_is_queue, done, max_it, u_implicit, usel;
   int32_t queue_out;            // SSSP: pull supersteps also append to the queue
   uint64_t n_total, m_total, nv;
@@ -396,7 +397,7 @@ struct CoopArgs {
   const uint32_t* indeg;    // in-degree (pull row length)
   const uint32_t* hsoa;     // in-neighbour s of row v at hsoa[s * hstride + v], s < kSoa
   const uint4* head;        // in-neighbours kSoa..kHead-1 of each pull row (16 B chunks)
-  uint64_t hstride;
+  uint32_t hstride;          // nv + 1 (< 2^28 + 1: 32-bit index math in the pull)
   int32_t* level;
   uint32_t* vis;
   uint32_t* fb[2];
@@ -410,6 +411,7 @@ struct CoopArgs {
   uint64_t n, nv, m, words_all;
   uint32_t s_words;
   int32_t use_ulist;        // later pulls walk the unvisited-row list (else every row)
+  uint32_t pull_chunk;      // implicit pull, 3-CTA variant: visited words per claim (1..32)
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -613,7 +615,7 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t* s_fb, uint32_t s_
 }
 
 __device__ __forceinline__ bool coop_probe_row(const CoopArgs& a, const uint32_t* s_fb,
-                                               uint32_t s_words, const uint32_t* fbc, uint64_t v,
+                                               uint32_t s_words, const uint32_t* fbc, uint32_t v,
                                                int hv, bool& defer, uint32_t& rest,
                                                unsigned long long& examined) {
   defer = false;
@@ -696,7 +698,7 @@ __global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArg
   extern __shared__ uint32_t s_fb[];
   const uint64_t gtid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
-  const uint64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+  const uint32_t gwarp = uint32_t(gtid >> 5), nwarps = uint32_t(gthreads >> 5);
   const unsigned lane = lane_id();
   __shared__ unsigned long long s_hdr[4], s_bc[2];
   if (gtid == 0) a.ctl->t_entry = globaltimer();
@@ -828,32 +830,55 @@ __global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArg
       const bool build_list = a.use_ulist && nf * 16 >= a.n;
       const int hv = nf * 32 >= a.n ? 1 : kHeadVec;
       if (u_implicit) {
-        const uint64_t words = (a.nv + 31) / 32;
-        // Words are dealt round-robin (warp g owns g, g + nwarps, ...) so every
-        // warp gets a statistically equal share; lanes prefetch the visited
-        // words of the warp's next 32 assignments in one load.  (Dealing
-        // 32-word blocks instead -- coalesced visited loads -- left too few
-        // blocks per warp at scale 23: 291 -> 218 GTEPS.)
-        for (uint64_t k0 = 0; gwarp + k0 * nwarps < words; k0 += 32) {
-         const uint64_t wl = gwarp + (k0 + lane) * nwarps;
-         const uint32_t myvis = wl < words ? __ldcg(&a.vis[wl]) : 0xFFFFFFFFu;
+        const uint32_t words = uint32_t((a.nv + 31) / 32);
+        // Large graphs (3-CTA variant): warps claim chunks of consecutive
+        // visited words from a counter (the next claim is issued before the
+        // current chunk is walked, so its latency hides): one coalesced
+        // visited load per chunk, and warps that draw cheap words take more
+        // of them -- static dealing left ~10% of the pull's stall samples at
+        // the closing barrier (scale 28: 1036 -> 1212 GTEPS).  Small graphs
+        // (2-CTA variant) deal words round-robin (warp g owns g, g + nwarps,
+        // ...; lanes load the visited words of the warp's next 32 in one
+        // round): too few chunks per warp there to balance dynamically
+        // (scale 23: 400 vs 387 GTEPS at the best chunk size).  A run-time
+        // choice between the two cost the large graphs 8% (1212 -> 1150).
+        constexpr bool dyn = kBlocksPerSm >= 3;
+        const uint32_t step = dyn ? 1u : nwarps, span = dyn ? a.pull_chunk : 32u;
+        uint32_t next = 0;  // dyn: the warp's next claimed word; else its next block
+        if (dyn) {
+          if (lane == 0) next = atomicAdd(&a.ctl->wcursor, span);
+          next = __shfl_sync(0xffffffffu, next, 0);
+        }
+        for (;;) {
+         uint32_t c0;
+         if (dyn) {
+           if (next >= words) break;
+           c0 = next;
+           if (lane == 0) next = atomicAdd(&a.ctl->wcursor, span);
+         } else {
+           c0 = gwarp + next * nwarps;
+           if (c0 >= words) break;
+           next += 32;
+         }
+         const uint32_t wl = c0 + lane * step;
+         const uint32_t myvis = (lane < span && wl < words) ? __ldcg(&a.vis[wl]) : 0xFFFFFFFFu;
          unsigned open_words = __ballot_sync(0xffffffffu, myvis != 0xFFFFFFFFu);
          while (open_words) {
           const int j = __ffs(open_words) - 1;
           open_words &= open_words - 1;
-          const uint64_t w = gwarp + (k0 + j) * nwarps;
+          const uint32_t w = c0 + j * step;
           // L2 prefetch of the next open word's head slots (no registers held:
           // the next iteration's slot loads then hit L2 instead of DRAM)
           if (open_words && lane < 2u * kSoa) {
             const unsigned k = lane >> 1;
             if (hv > 1 || k == 0) {
-              const uint64_t w2 = gwarp + (k0 + __ffs(open_words) - 1) * nwarps;
+              const uint32_t w2 = c0 + (__ffs(open_words) - 1) * step;
               const uint32_t* p = a.hsoa + k * a.hstride + w2 * 32 + ((lane & 1u) ? 31 : 0);
               asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
             }
           }
           const uint32_t vw = __shfl_sync(0xffffffffu, myvis, j);
-          const uint64_t v = w * 32 + lane;
+          const uint32_t v = w * 32 + lane;
           bool found = false, defer = false;
           uint32_t rest = 0;
           const bool open = v < a.nv && !((vw >> lane) & 1u);
@@ -877,12 +902,13 @@ __global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArg
           if (build_list && __any_sync(0xffffffffu, keep))
             warp_enqueue(keep, uint32_t(v), 0, &a.ctl->upack, unext, nullptr);
          }
+         if (dyn) next = __shfl_sync(0xffffffffu, next, 0);
         }
       } else {
-        const uint64_t cnt = ucur_n;
+        const uint32_t cnt = uint32_t(ucur_n);
         const uint32_t* ucur = a.ul[us];
-        for (uint64_t base = gwarp * 32; base < cnt; base += nwarps * 32) {
-          const uint64_t i = base + lane;
+        for (uint32_t base = gwarp * 32; base < cnt; base += nwarps * 32) {
+          const uint32_t i = base + lane;
           bool found = false, defer = false, open = false;
           uint32_t rest = 0, v = 0;
           if (i < cnt) {
@@ -1053,6 +1079,7 @@ __global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArg
       c->mf = mn;
       c->it = it;
       c->qpack = c->dpack = c->bpack = c->upack = 0;
+      c->wcursor = 0;
       c->found_n = c->found_e = c->examined = 0;
       if (nn == 0 || it >= c->max_it) c->done = 1;
       c->hdr[0] = nn;
@@ -1524,7 +1551,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   a.indeg = g.indeg.get();
   a.head = c.head.get();
   a.hsoa = c.hsoa.get();
-  a.hstride = nv + 1;
+  a.hstride = uint32_t(nv + 1);
   a.level = c.level.get();
   a.vis = c.vis.get();
   for (int i = 0; i < 2; ++i) {
@@ -1545,6 +1572,14 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   {
     const char* e = getenv("GM_BFS_ULIST");
     a.use_ulist = e ? atoi(e) : 1;
+  }
+  {
+    // 3-CTA variant's chunk claims (the 2-CTA variant deals words statically):
+    // about 8+ claims per warp, 4..32 words (128..1024 rows) each
+    const uint64_t vwords = (nv + 31) / 32, warps = uint64_t(c.coop_grid) * (kCoopThreads / 32);
+    a.pull_chunk = uint32_t(std::max<uint64_t>(4, std::min<uint64_t>(32, vwords / (warps * 8))));
+    const char* e = getenv("GM_BFS_PULL_CHUNK");  // test / tuning hook
+    if (e && atoi(e) >= 1 && atoi(e) <= 32) a.pull_chunk = uint32_t(atoi(e));
   }
   void* args[] = {&a};
   g.ktimer.begin(s, "k_bfs_coop");

@@ -1034,12 +1034,16 @@ def test_bfs_host_async_output(gm, orc):
         gm.bfs(g, roots[0], out=bufs[0].numpy(), sync=False)  # stats need the host
 
 
-@pytest.mark.parametrize("ctas", ["2", "3"])
-def test_bfs_coop_variants(gm, orc, ctas, monkeypatch):
+@pytest.mark.parametrize("ctas,chunk", [("2", None), ("3", None), ("3", "1"), ("3", "32")])
+def test_bfs_coop_variants(gm, orc, ctas, chunk, monkeypatch):
     """Both k_bfs_coop occupancy variants (2 CTAs x 64 registers, 3 CTAs x 40
-    registers per SM; the library picks by graph size) give the reference's
-    levels and per-superstep stats, including the pull -> queued push switch."""
+    registers per SM; the library picks by graph size; the first deals the
+    implicit pull's visited words round-robin, the second in claimed chunks of
+    1..32 words) give the reference's levels and per-superstep stats, including the pull ->
+    queued push switch."""
     monkeypatch.setenv("GM_BFS_CTAS_PER_SM", ctas)  # read at a graph's first BFS
+    if chunk is not None:
+        monkeypatch.setenv("GM_BFS_PULL_CHUNK", chunk)
     g = gm.Graph.rmat(18, 16, seed=3, symmetrize=True, relabel=True)
     s, d, _ = g.edges()
     for seed in (1, 2):

@@ -255,6 +255,102 @@ __global__ void __launch_bounds__(256) k_cf_items_grp(const uint32_t* __restrict
   }
 }
 
+// Generalised group kernel: G lanes per rating (G = 1, 2, 4 or 8), the row's K/4
+// float4 chunks dealt to the group's lanes round-robin (lane j holds chunks j,
+// j + G, ...), so load instruction c of a warp fetches chunks [cG, cG + G) of
+// 32/G rows -- G*16 contiguous bytes per row.  The dot product is a log2(G)
+// xor butterfly; the item's accumulators fold over the 32/G groups by a
+// butterfly over the group index at the end (fixed order: deterministic).
+template <int K, int G, int U, typename RT>
+__global__ void __launch_bounds__(256) k_cf_items_g(const uint32_t* __restrict__ rows,
+                                                    const uint64_t* __restrict__ ibeg,
+                                                    const uint64_t* __restrict__ iend, uint64_t nit,
+                                                    const uint32_t* __restrict__ idx,
+                                                    const uint8_t* __restrict__ val,
+                                                    const float* __restrict__ f,
+                                                    float* __restrict__ part, float* __restrict__ sq) {
+  static_assert(K % 4 == 0 && (G & (G - 1)) == 0 && G <= 8, "K = 4C, G a power of two <= 8");
+  constexpr int C = K / 4, CPL = (C + G - 1) / G, NG = 32 / G;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  const int grp = int(lane) / G, j = int(lane) % G;
+  const float4* __restrict__ f4 = reinterpret_cast<const float4*>(f);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint64_t it = warp; it < nit; it += nwarps) {
+    const uint32_t row = rows[it];
+    const uint64_t b = ibeg[it], e1 = iend[it];
+    float4 p[CPL], acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int ch = j + c * G;
+      p[c] = ch < C ? f4[uint64_t(row) * C + ch] : z4;
+      acc[c] = z4;
+    }
+    float s2 = 0.0f;
+    for (uint64_t e0 = b; e0 < e1; e0 += U * NG) {
+      float4 q[U][CPL];
+      float r[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t e = e0 + uint64_t(u * NG + grp);
+        ok[u] = e < e1;
+        r[u] = 0.0f;
+        uint32_t src = 0;
+        if (ok[u]) {
+          src = __ldg(&idx[e]);
+          r[u] = rating_at<RT>(val, e);
+        }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int ch = j + c * G;
+          q[u][c] = (ok[u] && ch < C) ? f4[uint64_t(src) * C + ch] : z4;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float d = 0.0f;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          d += p[c].x * q[u][c].x + p[c].y * q[u][c].y + p[c].z * q[u][c].z + p[c].w * q[u][c].w;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const float err = r[u] - d;
+        if (ok[u]) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            acc[c].x += err * q[u][c].x;
+            acc[c].y += err * q[u][c].y;
+            acc[c].z += err * q[u][c].z;
+            acc[c].w += err * q[u][c].w;
+          }
+          s2 += err * err;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, o);
+        acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, o);
+        acc[c].z += __shfl_xor_sync(0xffffffffu, acc[c].z, o);
+        acc[c].w += __shfl_xor_sync(0xffffffffu, acc[c].w, o);
+      }
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (grp == 0) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int ch = j + c * G;
+        if (ch < C) reinterpret_cast<float4*>(part)[it * C + ch] = acc[c];
+      }
+    }
+    if (sq && lane == 0) sq[it] = s2;
+  }
+}
+
 // p' = p + gamma * (sum - lambda * p); sum = out-route items then in-route items.
 // Rows [lo, lo + n): rit / rif are indexed by v - lo, f by the global row, fn
 // by the local one (the single-GPU call passes lo = 0).
@@ -388,7 +484,26 @@ template <typename RT>
 void pass(const CfCache& c, Graph& g, bool fwd, const float* f, int k, float* sq) {
   const Csr& csr = fwd ? g.fwd() : g.in;
   static const bool lane_per_rating = getenv("GM_CF_LANE") && getenv("GM_CF_LANE")[0] == '1';
-  if (k == 20 && !lane_per_rating)
+  static const int grp_lanes = getenv("GM_CF_G") ? atoi(getenv("GM_CF_G")) : 5;
+  if (k == 20 && !lane_per_rating && grp_lanes != 5) {
+    const uint64_t nit = fwd ? c.nit_f : c.nit_t;
+    if (!nit) return;
+    const unsigned grid = grid_for(nit * 32, 256);
+    auto args = [&](auto kern) {
+      kern<<<grid, 256, 0, g.stream>>>(fwd ? c.items_f.get() : c.items_t.get(),
+                                       fwd ? c.ibeg_f.get() : c.ibeg_t.get(),
+                                       fwd ? c.iend_f.get() : c.iend_t.get(), nit, csr.idx.get(),
+                                       csr.val.get(), f, fwd ? c.part_f.get() : c.part_t.get(), sq);
+    };
+    switch (grp_lanes) {
+      case 1: args(k_cf_items_g<20, 1, 2, RT>); break;
+      case 2: args(k_cf_items_g<20, 2, 2, RT>); break;
+      case 3: args(k_cf_items_g<20, 2, 4, RT>); break;
+      case 4: args(k_cf_items_g<20, 4, 4, RT>); break;
+      default: args(k_cf_items_g<20, 8, 4, RT>); break;
+    }
+    GM_LAUNCH_CHECK();
+  } else if (k == 20 && !lane_per_rating)
     launch_items_grp<20, RT>(c, csr, fwd, f, g.stream, sq);
   else if (k == 20)
     launch_items<20, RT>(c, csr, fwd, f, k, g.stream, sq);

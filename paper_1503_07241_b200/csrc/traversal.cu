@@ -376,15 +376,38 @@ __global__ void k_finish(Ctl* ctl, uint64_t* offs_next) {
 }
 
 // ------------------------------------------------------------------- BFS
-// Caller-order output: out[v] = level[perm[v]] (level was prefilled with -1,
-// so one gather per vertex; probing the visited bitmap too cost a second).
-// clear != null: also reset the other level buffer for the next BFS.
-__global__ void k_bfs_output(uint64_t n, const uint32_t* perm, const int32_t* level, int32_t* out,
-                             int32_t* clear) {
-  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
-       v += uint64_t(gridDim.x) * blockDim.x) {
-    out[v] = __ldg(&level[perm ? __ldg(&perm[v]) : uint32_t(v)]);
-    if (clear) __stcs(&clear[v], -1);
+// Caller-order output: out[x] = level[perm[x]].  Under the degree relabel the
+// isolated vertices are the internal tail [nv, n): they are unreachable (only
+// the root, if the caller picked an isolated one, has a level), so their level
+// is not gathered -- at scale 28 that skips about half of the random 4-byte
+// gathers, which bound this pass.  Within one degree class internal ids follow
+// caller order, so the gathers of nearby callers share sectors.  Four callers
+// per thread (16-byte perm loads and out stores).  The pass also refills the
+// internal prefix [0, nv) of the other level buffer with -1 for the next BFS
+// (the tail is never read).
+__global__ void k_bfs_output(uint64_t n, uint64_t nv, uint64_t root_ext, const uint32_t* perm,
+                             const int32_t* level, int32_t* out, int32_t* clear) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t t0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint64_t n4 = (perm && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) ? n / 4 : 0;
+  auto one = [&](uint32_t p) -> int32_t { return p < nv ? __ldg(&level[p]) : -1; };
+  for (uint64_t i = t0; i < n4; i += stride) {
+    const uint4 p = __ldcs(reinterpret_cast<const uint4*>(perm) + i);
+    int4 o;
+    o.x = one(p.x);
+    o.y = one(p.y);
+    o.z = one(p.z);
+    o.w = one(p.w);
+    if ((root_ext >> 2) == i) (&o.x)[root_ext & 3] = 0;  // the root's level, isolated or not
+    __stcs(reinterpret_cast<int4*>(out) + i, o);
+  }
+  for (uint64_t v = n4 * 4 + t0; v < n; v += stride)
+    out[v] = v == root_ext ? 0 : perm ? one(__ldg(&perm[v])) : __ldg(&level[v]);
+  if (clear) {
+    const uint64_t nv4 = (reinterpret_cast<uintptr_t>(clear) & 15u) == 0 ? nv / 4 : 0;
+    for (uint64_t i = t0; i < nv4; i += stride)
+      __stcs(reinterpret_cast<int4*>(clear) + i, make_int4(-1, -1, -1, -1));
+    for (uint64_t v = nv4 * 4 + t0; v < nv; v += stride) __stcs(&clear[v], -1);
   }
 }
 
@@ -1654,7 +1677,10 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
       dst = c.ext_out.get();
     }
     if (!c.level_alt) c.level_alt.alloc(n, s);
-    k_bfs_output<<<grid_for(n, 256), 256, 0, s>>>(n, perm, c.level.get(), dst, c.level_alt.get());
+    // nv < n only under the symmetric degree relabel: [nv, n) are isolated and
+    // their level buffer entries are neither gathered nor cleared
+    k_bfs_output<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(n, nv, root, perm, c.level.get(), dst,
+                                                         c.level_alt.get());
     c.level.swap(c.level_alt);
     c.level_clean = true;  // the cleared buffer is current now
     GM_LAUNCH_CHECK();

@@ -302,6 +302,25 @@ def test_empty_and_isolated(gm):
     np.testing.assert_allclose(r, 0.25, rtol=1e-6)
 
 
+def test_bfs_isolated_root_and_output_pass(gm, orc):
+    """The caller-order output pass skips the isolated internal tail [nv, n)
+    of a degree-relabeled symmetric graph: an isolated root still gets level
+    0 and everything else -1, and a following BFS from a connected root (on
+    the level buffer that pass refilled) equals the reference."""
+    g = gm.Graph.rmat(14, 16, seed=7, symmetrize=True, relabel=True)
+    s, d, _ = g.edges()
+    n = g.num_vertices
+    deg = np.bincount(s, minlength=n)
+    iso = np.flatnonzero(deg == 0)
+    assert len(iso) > 0
+    for root in (int(iso[0]), int(iso[-1]), g.pick_source(7), int(iso[len(iso) // 2])):
+        lvl, st = gm.bfs(g, root)
+        want, wst = orc.bfs(n, s, d, root, presorted=True)
+        assert np.array_equal(lvl, want)
+        assert _stats_key(st) == wst
+    assert lvl[root] == 0 and (lvl == -1).sum() == n - 1
+
+
 # ------------------------------------------------------- medium R-MAT
 
 @pytest.mark.parametrize("scale", [14, 16])

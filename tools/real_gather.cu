@@ -106,3 +106,7 @@ extern "C" float rg_run(const uint32_t* idx, uint64_t m, const float* x, uint32_
   if (cudaGetLastError() != cudaSuccess) return -1.f;
   return best * 1000.f;
 }
+
+extern "C" int rg_copy(void* dst, const void* src, uint64_t bytes) {
+  return int(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToDevice));
+}

@@ -36,6 +36,7 @@
 // message snapshot, rule S3); atomicMin into dist; a vertex whose distance
 // dropped is claimed once through a changed-bitmap and forms the next frontier.
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 #include <cstdio>
 #include <cstdlib>
@@ -94,12 +95,18 @@ struct Ctl {
 
 struct TravCache {
   uint64_t n = 0;
-  DevBuf<int32_t> level;
-  // BFS: the output pass clears level_alt (sequential stores riding on its
-  // request-bound gathers) and the two swap, so the next BFS starts from a
-  // cleared array without a 4-byte-per-vertex memset (scale 28: 0.16 ms).
-  DevBuf<int32_t> level_alt;
-  bool level_clean = false;
+  // BFS levels as stamps: BFS number i writes lbase_i + level, and a stamp
+  // below lbase_i is "unreached", so no BFS clears the array (a 4-byte-per-
+  // vertex memset or clearing pass, 0.16 ms at scale 28); the host advances
+  // lbase by a bound on the BFS depth and zeroes the array only when the
+  // 32-bit stamps would wrap.
+  DevBuf<uint32_t> level;
+  uint64_t lbase = 0;  // 0: the array needs zeroing before the next BFS
+  // Compact output (symmetric degree relabel, isolated tail [nv, n)): bitmap
+  // of callers with a nonzero degree, non-isolated callers before each block
+  // of 1024 callers, and the internal id of every non-isolated caller in
+  // caller order.
+  DevBuf<uint32_t> nzb, nz_base, perm_c;
   DevBuf<uint32_t> dist;
   DevBuf<uint32_t> q[2];        // frontier queues (internal ids)
   DevBuf<uint64_t> offs[2];     // exclusive edge offsets, parallel to q (+1 total)
@@ -308,8 +315,8 @@ __device__ __forceinline__ void warp_enqueue_multi(unsigned mask, const uint32_t
 // ------------------------------------------------------------- control
 __global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t root_ext,
                            const uint32_t* perm, uint32_t* q1, uint64_t* offs1, uint64_t* qe1,
-                           const uint64_t* out_ptr, const uint32_t* deg, int32_t* level,
-                           uint64_t n, uint64_t m, uint64_t nv, int32_t max_it) {
+                           const uint64_t* out_ptr, const uint32_t* deg, uint32_t* level,
+                           uint32_t lbase, uint64_t n, uint64_t m, uint64_t nv, int32_t max_it) {
   const uint32_t root = perm ? perm[root_ext] : uint32_t(root_ext);
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words;
        i += uint64_t(gridDim.x) * blockDim.x)
@@ -319,7 +326,7 @@ __global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t roo
     offs1[0] = 0;
     offs1[1] = deg[root];
     qe1[0] = out_ptr[root];
-    level[root] = 0;
+    level[root] = lbase;
     ctl->nf = 1;
     ctl->mf = deg[root];
     ctl->it = 0;
@@ -376,39 +383,125 @@ __global__ void k_finish(Ctl* ctl, uint64_t* offs_next) {
 }
 
 // ------------------------------------------------------------------- BFS
-// Caller-order output: out[x] = level[perm[x]].  Under the degree relabel the
-// isolated vertices are the internal tail [nv, n): they are unreachable (only
-// the root, if the caller picked an isolated one, has a level), so their level
-// is not gathered -- at scale 28 that skips about half of the random 4-byte
-// gathers, which bound this pass.  Within one degree class internal ids follow
-// caller order, so the gathers of nearby callers share sectors.  Four callers
-// per thread (16-byte perm loads and out stores).  The pass also refills the
-// internal prefix [0, nv) of the other level buffer with -1 for the next BFS
-// (the tail is never read).
-__global__ void k_bfs_output(uint64_t n, uint64_t nv, uint64_t root_ext, const uint32_t* perm,
-                             const int32_t* level, int32_t* out, int32_t* clear) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  const uint64_t t0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  const uint64_t n4 = (perm && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) ? n / 4 : 0;
-  auto one = [&](uint32_t p) -> int32_t { return p < nv ? __ldg(&level[p]) : -1; };
-  for (uint64_t i = t0; i < n4; i += stride) {
-    const uint4 p = __ldcs(reinterpret_cast<const uint4*>(perm) + i);
-    int4 o;
-    o.x = one(p.x);
-    o.y = one(p.y);
-    o.z = one(p.z);
-    o.w = one(p.w);
-    if ((root_ext >> 2) == i) (&o.x)[root_ext & 3] = 0;  // the root's level, isolated or not
-    __stcs(reinterpret_cast<int4*>(out) + i, o);
+// Caller-order output: out[x] = level of perm[x] (stamp - lbase, or -1 for a
+// stamp below lbase: not reached by this BFS).  Generic form for graphs
+// without the symmetric degree relabel (perm null: identity).
+__global__ void k_bfs_output(uint64_t n, uint64_t root_ext, const uint32_t* perm,
+                             const uint32_t* stamp, uint32_t lbase, int32_t* out) {
+  for (uint64_t v = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; v < n;
+       v += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t st = __ldg(&stamp[perm ? __ldg(&perm[v]) : uint32_t(v)]);
+    out[v] = v == root_ext ? 0 : (st >= lbase ? int32_t(st - lbase) : -1);
   }
-  for (uint64_t v = n4 * 4 + t0; v < n; v += stride)
-    out[v] = v == root_ext ? 0 : perm ? one(__ldg(&perm[v])) : __ldg(&level[v]);
-  if (clear) {
-    const uint64_t nv4 = (reinterpret_cast<uintptr_t>(clear) & 15u) == 0 ? nv / 4 : 0;
-    for (uint64_t i = t0; i < nv4; i += stride)
-      __stcs(reinterpret_cast<int4*>(clear) + i, make_int4(-1, -1, -1, -1));
-    for (uint64_t v = nv4 * 4 + t0; v < nv; v += stride) __stcs(&clear[v], -1);
+}
+
+// Compact caller-order output under the symmetric degree relabel.  Isolated
+// vertices form the internal tail [nv, n) and are unreachable (the root aside,
+// handled by id), so their -1 needs no perm entry and no gather: a warp takes
+// 1024 callers, reads their 32 words of the non-isolated bitmap, and only the
+// set bits read a compacted perm entry (perm_c, non-isolated callers in caller
+// order) and gather a stamp.  At scale 28 about half the vertices are
+// isolated: the pass reads ~0.5 GB of perm_c instead of 1 GB of perm and
+// writes only the output.  Within one degree class internal ids follow caller
+// order, so the stamp gathers of nearby callers share sectors.
+template <int kB>
+__global__ void __launch_bounds__(256) k_bfs_output_nz(uint64_t n, uint64_t root_ext,
+                                                       const uint32_t* __restrict__ nzb,
+                                                       const uint32_t* __restrict__ nz_base,
+                                                       const uint32_t* __restrict__ perm_c,
+                                                       const uint32_t* __restrict__ stamp,
+                                                       uint32_t lbase, int32_t* __restrict__ out) {
+  const unsigned lane = lane_id();
+  const uint64_t nwords = (n + 31) / 32, nblk = (n + 1023) / 1024;
+  const uint64_t gw = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t b = gw; b < nblk; b += nw) {
+    const uint64_t wi = b * 32 + lane;
+    const uint32_t word = wi < nwords ? __ldcs(&nzb[wi]) : 0u;
+    const uint32_t cnt = __popc(word);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= unsigned(o)) incl += t;
+    }
+    const uint32_t wbase = __ldg(&nz_base[b]) + incl - cnt;
+    const uint32_t below = (1u << lane) - 1u;
+#pragma unroll 1
+    for (int r0 = 0; r0 < 32; r0 += kB) {
+      uint32_t st[kB];
+      bool set[kB];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const uint32_t wr = __shfl_sync(0xffffffffu, word, r0 + j);
+        const uint32_t br = __shfl_sync(0xffffffffu, wbase, r0 + j);
+        set[j] = (wr >> lane) & 1u;
+        st[j] = set[j] ? __ldcs(&perm_c[br + __popc(wr & below)]) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kB; ++j) st[j] = set[j] ? __ldg(&stamp[st[j]]) : 0u;
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const uint64_t x = b * 1024 + uint64_t(r0 + j) * 32 + lane;
+        int32_t o = (set[j] && st[j] >= lbase) ? int32_t(st[j] - lbase) : -1;
+        if (x == root_ext) o = 0;
+        if (x < n) __stcs(&out[x], o);
+      }
+    }
   }
+}
+
+// Build the compact-output tables (once per graph): nzb bit x = (perm[x] < nv).
+__global__ void k_nz_bits(uint64_t n, uint64_t nv, const uint32_t* perm, uint32_t* nzb,
+                          uint32_t* blk_cnt) {
+  const uint64_t nwords = (n + 31) / 32;
+  for (uint64_t w0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; w0 < nwords * 32;
+       w0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t x = w0 + lane_id();
+    const unsigned bits = __ballot_sync(0xffffffffu, x < n && perm[x] < nv);
+    if (lane_id() == 0) {
+      nzb[x >> 5] = bits;
+      atomicAdd(&blk_cnt[x >> 10], uint32_t(__popc(bits)));
+    }
+  }
+}
+
+__global__ void k_perm_compact(uint64_t n, const uint32_t* perm, const uint32_t* nzb,
+                               const uint32_t* nz_base, uint32_t* perm_c) {
+  const unsigned lane = lane_id();
+  const uint64_t nwords = (n + 31) / 32, nblk = (n + 1023) / 1024;
+  const uint64_t gw = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t b = gw; b < nblk; b += nw) {
+    const uint64_t wi = b * 32 + lane;
+    const uint32_t word = wi < nwords ? nzb[wi] : 0u;
+    const uint32_t cnt = __popc(word);
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= unsigned(o)) incl += t;
+    }
+    uint32_t k = nz_base[b] + incl - cnt;
+    for (int i = 0; i < 32; ++i)
+      if ((word >> i) & 1u) perm_c[k++] = perm[wi * 32 + i];
+  }
+}
+
+void build_compact_output(TravCache& c, const uint32_t* perm, uint64_t n, uint64_t nv, cudaStream_t s) {
+  const uint64_t nwords = (n + 31) / 32, nblk = (n + 1023) / 1024;
+  c.nzb.alloc(nwords + 1, s);
+  c.nz_base.alloc(nblk + 1, s);
+  c.perm_c.alloc(nv + 1, s);
+  c.nz_base.zero(s);
+  k_nz_bits<<<grid_for(nwords * 32, 256), 256, 0, s>>>(n, nv, perm, c.nzb.get(), c.nz_base.get());
+  GM_LAUNCH_CHECK();
+  size_t tmp = 0;
+  GM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nz_base.get(), c.nz_base.get(), int64_t(nblk), s));
+  DevBuf<uint8_t> t(tmp + 1, s);
+  GM_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, c.nz_base.get(), c.nz_base.get(), int64_t(nblk), s));
+  k_perm_compact<<<grid_for(nblk * 32, 256), 256, 0, s>>>(n, perm, c.nzb.get(), c.nz_base.get(),
+                                                         c.perm_c.get());
+  GM_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------ cooperative BFS (all supersteps)
@@ -430,7 +523,8 @@ struct CoopArgs {
   const uint32_t* hsoa;     // in-neighbour s of row v at hsoa[s * hstride + v], s < kSoa
   const uint4* head;        // in-neighbours kSoa..kHead-1 of each pull row (16 B chunks)
   uint32_t hstride;          // nv + 1 (< 2^28 + 1: 32-bit index math in the pull)
-  int32_t* level;
+  uint32_t* level;          // stamps: lbase + level (TravCache::level)
+  uint32_t lbase;
   uint32_t* vis;
   uint32_t* fb[2];
   uint32_t* q[2];
@@ -613,7 +707,7 @@ __device__ __forceinline__ void coop_push(const CoopArgs& a, int cur, uint64_t n
       if (k < nk) {
         const uint32_t v = vk[k], bit = 1u << (v & 31u);
         if (!(visw[k] & bit) && !(atomicOr(&a.vis[v >> 5], bit) & bit)) {
-          a.level[v] = next_level;
+          a.level[v] = a.lbase + uint32_t(next_level);
           atomicOr(&fbn[v >> 5], bit);
           won |= 1u << k;
         }
@@ -916,7 +1010,7 @@ __global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArg
           const bool open = v < a.nv && !((vw >> lane) & 1u);
           if (open) {
             found = coop_probe_row(a, s_fb, sw, fbc, v, hv, defer, rest, examined);
-            if (found) a.level[v] = it;
+            if (found) a.level[v] = a.lbase + uint32_t(it);
           }
           const unsigned b = __ballot_sync(0xffffffffu, found);
           if (lane == 0 && b) {
@@ -950,7 +1044,7 @@ __global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArg
               found = coop_probe_row(a, s_fb, sw, fbc, v, hv, defer, rest, examined);
               if (found) {
                 const uint32_t bit = 1u << (v & 31u);
-                a.level[v] = it;
+                a.level[v] = a.lbase + uint32_t(it);
                 atomicOr(&fbn[v >> 5], bit);
                 atomicOr(&a.vis[v >> 5], bit);
               }
@@ -1044,7 +1138,7 @@ __global__ void __launch_bounds__(kCoopThreads, kBlocksPerSm) k_bfs_coop(CoopArg
             if ((word >> (u[k] & 31u)) & 1u) {
               const uint32_t v = rv[k];
               if (!(atomicOr(&fbn[v >> 5], bit) & bit)) {
-                a.level[v] = it;
+                a.level[v] = a.lbase + uint32_t(it);
                 atomicOr(&a.vis[v >> 5], bit);
                 ++found_n;
                 won |= 1u << k;
@@ -1567,12 +1661,18 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   GM_CUDA(cudaMemsetAsync(ctl, 0, offsetof(Ctl, t_start), s));
   GM_CUDA(cudaMemsetAsync(c.fb[0].get(), 0, (words + 1) * 4, s));
   GM_CUDA(cudaMemsetAsync(c.fb[1].get(), 0, (words + 1) * 4, s));
-  if (out && !c.level_clean) GM_CUDA(cudaMemsetAsync(c.level.get(), 0xFF, n * 4, s));  // -1 until reached
-  c.level_clean = false;
+  // level stamps of this BFS lie in [lbase, lbase + depth bound]
+  const uint64_t depth_bound = std::min<uint64_t>(uint64_t(std::max(max_it, 0)), nv) + 1;
+  if (c.lbase == 0 || c.lbase + depth_bound > 0xFFFFFFFFull) {
+    GM_CUDA(cudaMemsetAsync(c.level.get(), 0, n * 4, s));
+    c.lbase = 1;
+  }
+  const uint32_t lbase = uint32_t(c.lbase);
+  c.lbase += depth_bound;
   k_bfs_init<<<grid_for(words + 1, 256), 256, 0, s>>>(ctl, c.vis.get(), words + 1, root, perm,
                                                       c.q[1].get(), c.offs[1].get(), c.qe[1].get(),
-                                                      fw.ptr.get(), g.outdeg.get(), c.level.get(), n,
-                                                      g.m, nv, max_it);
+                                                      fw.ptr.get(), g.outdeg.get(), c.level.get(),
+                                                      lbase, n, g.m, nv, max_it);
   GM_LAUNCH_CHECK();
   CoopArgs a{};
   a.ctl = ctl;
@@ -1586,6 +1686,7 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   a.hsoa = c.hsoa.get();
   a.hstride = uint32_t(nv + 1);
   a.level = c.level.get();
+  a.lbase = lbase;
   a.vis = c.vis.get();
   for (int i = 0; i < 2; ++i) {
     a.fb[i] = c.fb[i].get();
@@ -1676,13 +1777,15 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
       if (!c.ext_out) c.ext_out.alloc(n, s);
       dst = c.ext_out.get();
     }
-    if (!c.level_alt) c.level_alt.alloc(n, s);
-    // nv < n only under the symmetric degree relabel: [nv, n) are isolated and
-    // their level buffer entries are neither gathered nor cleared
-    k_bfs_output<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(n, nv, root, perm, c.level.get(), dst,
-                                                         c.level_alt.get());
-    c.level.swap(c.level_alt);
-    c.level_clean = true;  // the cleared buffer is current now
+    if (perm && nv < n) {
+      if (!c.perm_c) build_compact_output(c, perm, n, nv, s);
+      // rounds of 8 callers per lane between the gathers: 4 and 8 measure the
+      // same at scale 28 (2.84 ms per BFS), 16 and 32 lose occupancy (3.15, 3.49)
+      k_bfs_output_nz<8><<<grid_for((n + 1023) / 1024 * 32, 256), 256, 0, s>>>(
+          n, root, c.nzb.get(), c.nz_base.get(), c.perm_c.get(), c.level.get(), lbase, dst);
+    } else {
+      k_bfs_output<<<grid_for(n, 256), 256, 0, s>>>(n, root, perm, c.level.get(), lbase, dst);
+    }
     GM_LAUNCH_CHECK();
     if (host_async)
       g.host_async.issue(s, out, n * 4);

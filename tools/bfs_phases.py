@@ -3,7 +3,8 @@ import os, sys
 sys.path.insert(0, "/root/repo")
 os.environ["GM_BFS_PHASES"] = "1"
 import paper_1503_07241_b200 as gm
-g = gm.Graph.rmat(23, 16, seed=1, symmetrize=True, relabel=True)
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 23
+g = gm.Graph.rmat(scale, 16, seed=1, symmetrize=True, relabel=True)
 root = g.pick_source(1)
 for _ in range(3):
     lvl, st = gm.bfs(g, root)

@@ -34,6 +34,8 @@
 // throughput where the program's reduce is exact or tolerance-checked.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -461,24 +463,28 @@ __global__ void __launch_bounds__(kLongThreads) k_pull_long(
         cur = nxt;
         continue;
       }
-      if (valid) s_r[lane] = r;
+      // valid contributions packed in entry order; lane 0 folds a count in
+      // branch-free groups of 8 (a predicate and branch per entry cost ~3x
+      // the reduce itself)
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      if (valid) s_r[__popc(vm & ((1u << lane) - 1u))] = r;
       __syncwarp();
-      if (lane == 0 && vm) {  // in entry order; 8 staged values loaded ahead of each 8 folds
-#pragma unroll 1
-        for (int b8 = 0; b8 < 32; b8 += 8) {
-          if (!((vm >> b8) & 0xFFu)) continue;
+      if (lane == 0 && vm) {
+        const int cnt = __popc(vm);
+        int t = 0;
+        if (!any) {
+          acc = p.reduce(p.reduce_identity(), s_r[0]);
+          any = true;
+          t = 1;
+        }
+        for (; t + 8 <= cnt; t += 8) {
           R v8[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) v8[t] = s_r[b8 + t];
+          for (int u = 0; u < 8; ++u) v8[u] = s_r[t + u];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            if ((vm >> (b8 + t)) & 1u) {
-              acc = any ? p.reduce(acc, v8[t]) : p.reduce(p.reduce_identity(), v8[t]);
-              any = true;
-            }
-          }
+          for (int u = 0; u < 8; ++u) acc = p.reduce(acc, v8[u]);
         }
+        for (; t < cnt; ++t) acc = p.reduce(acc, s_r[t]);
       }
       __syncwarp();
       cur = nxt;
@@ -500,6 +506,184 @@ __global__ void __launch_bounds__(kLongThreads) k_pull_long(
     }
   }
 }
+
+// Hub rows of order-sensitive programs (more than kHubRow entries, no failing
+// callbacks): one CTA per row.  The row's fold has to stay one sequential
+// chain -- reduce(...reduce(reduce(identity, r0), r1)..., r_last) in entry
+// order is the reference's result bit for bit -- but everything before it
+// need not: 15 producer warps gather the messages and evaluate
+// process_message for 32-entry chunks into a shared-memory ring, and one
+// consumer thread folds the ring in entry order, so the chain runs at the
+// reduce's latency instead of behind one warp's load round trips.  (k_pull_long
+// has the warp's lane 0 fold while the same warp loads the next chunks: the
+// hub row -- 10^5 entries and more at scale 23 -- was the superstep's
+// critical path, 6.3 ms of a 7 ms superstep.)
+constexpr uint64_t kHubRow = 4096;
+constexpr unsigned kHubThreads = 512;
+constexpr unsigned kHubSlot = 64;  // entries per ring slot (two per producer lane)
+// ring slots: 32 (16 KB of 8-byte values), fewer for wide reduced values
+template <typename R>
+constexpr unsigned hub_ring() {
+  return kHubSlot * sizeof(R) * 32u <= 40960u ? 32u
+         : 40960u / (kHubSlot * unsigned(sizeof(R))) >= 4u ? 40960u / (kHubSlot * unsigned(sizeof(R)))
+                                                            : 4u;
+}
+
+// Shared-memory flag handshake of k_pull_hub: acquire / release at CTA scope
+// (a full __threadfence_block is a MEMBAR.SC per slot on the consumer's
+// critical path).
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
+               : "=r"(v)
+               : "r"(unsigned(__cvta_generic_to_shared(p)))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(unsigned(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
+}
+
+// Rows are claimed from `claim` (zeroed before the launch), longest first: the
+// CTA holding the longest row takes no other, so the superstep's critical path
+// is that row's fold alone (grid-stride dealing had added ~6 more rows to it).
+template <typename P>
+__global__ void __launch_bounds__(kHubThreads) k_pull_hub(
+    P p, const uint32_t* rows, uint64_t nrows, unsigned* claim, const uint64_t* ptr,
+    const uint32_t* idx, const uint8_t* val, const typename P::message_t* x, const uint32_t* xbits,
+    const typename P::vertex_t* props, typename P::reduced_t* y, uint32_t* ybits) {
+  using R = typename P::reduced_t;
+  using E = typename P::edge_t;
+  using M = typename P::message_t;
+  constexpr unsigned kHubRing = hub_ring<R>();
+  __shared__ __align__(16) unsigned char s_raw[kHubRing * kHubSlot * sizeof(R)];
+  R* ring = reinterpret_cast<R*>(s_raw);
+  __shared__ unsigned s_cnt[kHubRing];
+  __shared__ int s_ready[kHubRing];  // slot number + 1 once the slot holds it
+  __shared__ int s_consumed;         // slots the consumer has folded (published every 2)
+  __shared__ unsigned s_row;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  constexpr unsigned kProducers = kHubThreads / 32 - 1;
+  for (;;) {
+    for (unsigned t = threadIdx.x; t < kHubRing; t += blockDim.x) s_ready[t] = 0;
+    if (threadIdx.x == 0) {
+      s_consumed = 0;
+      s_row = atomicAdd(claim, 1u);
+    }
+    __syncthreads();
+    const uint64_t i = s_row;
+    if (i >= nrows) break;
+    const uint32_t k = rows[i];
+    const uint64_t e0 = ptr[k], e1 = ptr[k + 1];
+    const int nsl = int((e1 - e0 + kHubSlot - 1) / kHubSlot);
+    if (warp > 0) {
+      const typename P::vertex_t vk = props[k];
+      int c = int(warp) - 1;
+      auto col = [&](int cc, int h) -> uint32_t {
+        const uint64_t e = e0 + uint64_t(cc) * kHubSlot + 32u * h + lane;
+        return cc < nsl && e < e1 ? idx[e] : 0u;
+      };
+      uint32_t j[2] = {col(c, 0), col(c, 1)};
+      for (; c < nsl; c += int(kProducers)) {
+        // this slot's messages, validity words and edge values, and the next
+        // slot's column ids, all in flight before the slot wait
+        bool in[2], valid[2];
+        uint32_t word[2];
+        M m[2];
+        E ed[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t e = e0 + uint64_t(c) * kHubSlot + 32u * h + lane;
+          in[h] = e < e1;
+          word[h] = in[h] ? xbits[j[h] >> 5] : 0u;
+          m[h] = in[h] ? x[j[h]] : M{};
+          ed[h] = in[h] ? load_edge<E>(val, e) : E{};
+        }
+        const int cn = c + int(kProducers);
+        const uint32_t jn[2] = {col(cn, 0), col(cn, 1)};
+        R r[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          valid[h] = in[h] && ((word[h] >> (j[h] & 31u)) & 1u);
+          r[h] = R{};
+          if (valid[h]) r[h] = p.process_message(m[h], ed[h], vk);
+        }
+        const unsigned slot = unsigned(c) % kHubRing;
+        if (c >= int(kHubRing)) {
+          // a full ring: sleep long -- spinning producers took the consumer's
+          // issue slots (163 cycles per folded entry at 32 ns sleeps)
+          if (lane == 0)
+            while (ld_acquire_cta(&s_consumed) <= c - int(kHubRing)) __nanosleep(1000);
+          __syncwarp();
+        }
+        // valid contributions packed to the front of the slot, in entry
+        // order: the consumer folds a count, with no per-entry predicate
+        const unsigned vm0 = __ballot_sync(0xffffffffu, valid[0]);
+        const unsigned vm1 = __ballot_sync(0xffffffffu, valid[1]);
+        const unsigned below = (1u << lane) - 1u;
+        R* rs = ring + slot * kHubSlot;
+        if (valid[0]) rs[__popc(vm0 & below)] = r[0];
+        if (valid[1]) rs[__popc(vm0) + __popc(vm1 & below)] = r[1];
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) {
+          s_cnt[slot] = unsigned(__popc(vm0) + __popc(vm1));
+          st_release_cta(&s_ready[slot], c + 1);
+        }
+        j[0] = jn[0];
+        j[1] = jn[1];
+      }
+    } else if (lane == 0) {
+      R acc = p.reduce_identity();
+      bool any = false;
+      for (int c = 0; c < nsl; ++c) {
+        const unsigned slot = unsigned(c) % kHubRing;
+        // no sleep: the consumer is the critical path
+        while (ld_acquire_cta(&s_ready[slot]) != c + 1) {
+        }
+        const int cnt = int(s_cnt[slot]);
+        const R* rs = ring + slot * kHubSlot;
+        if (any && cnt == int(kHubSlot)) {
+          // the common full slot: one straight-line chain, so the compiler
+          // issues each value's shared load several reduces ahead of its use
+          // (the dynamic-count loop below waits on every group's loads)
+#pragma unroll
+          for (int u = 0; u < int(kHubSlot); ++u) acc = p.reduce(acc, rs[u]);
+          if ((c & 1) == 1 || c + 1 == nsl) st_release_cta(&s_consumed, c + 1);
+          continue;
+        }
+        int t = 0;
+        if (!any && cnt) {
+          acc = p.reduce(p.reduce_identity(), rs[0]);  // the row's first fold (S4)
+          any = true;
+          t = 1;
+        }
+        // branch-free groups of 8 (a predicate or branch per entry cost more
+        // than the reduce itself)
+        for (; t + 8 <= cnt; t += 8) {
+          R v8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v8[u] = rs[t + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = p.reduce(acc, v8[u]);
+        }
+        for (; t < cnt; ++t) acc = p.reduce(acc, rs[t]);
+        if ((c & 1) == 1 || c + 1 == nsl) st_release_cta(&s_consumed, c + 1);
+      }
+      if (any) {
+        y[k] = acc;
+        atomicOr(&ybits[k >> 5], 1u << (k & 31u));
+      }
+    }
+    __syncthreads();  // the ring is reused by the next row
+  }
+}
+
+// Entry counts of listed rows (hub selection on the host).
+__global__ void k_row_lens(const uint32_t* rows, uint64_t nrows, const uint64_t* ptr,
+                           uint32_t* lens);
 
 // Row ids with more than kLongRow entries (order irrelevant: rows are independent).
 __global__ void k_long_rows(uint64_t n, const uint64_t* ptr, uint32_t* rows,
@@ -620,6 +804,12 @@ class Engine {
       cudaEventDestroy(fork_);
       cudaEventDestroy(join_);
     }
+    if (hub_) {
+      cudaStreamSynchronize(hub_);
+      cudaStreamDestroy(hub_);
+      cudaEventDestroy(hfork_);
+      cudaEventDestroy(hjoin_);
+    }
     cudaEventDestroy(e0_);
     cudaEventDestroy(e1_);
     cudaEventDestroy(e2_);
@@ -684,11 +874,58 @@ class Engine {
     return h;
   }
 
-  void pull(const Csr& c, DevBuf<uint32_t>& lrows, uint64_t& nlong, bool& have, R* y,
-            uint32_t* ybits) {
+  // Order-sensitive programs without failing callbacks fold hub rows with
+  // k_pull_hub (one CTA per row, a sequential consumer fed by producer warps).
+  static constexpr bool kHubPath = !exact_reorder<P>::value && !can_fail<P>::value;
+
+  // Move the rows above kHubRow entries from `lrows` to `hrows`, longest first
+  // (the longest row's fold is the superstep's critical path, so it starts in
+  // the first wave).  Once per engine and route.
+  void split_hubs(const Csr& c, DevBuf<uint32_t>& lrows, uint64_t& nlong, DevBuf<uint32_t>& hrows,
+                  uint64_t& nhub) {
+    nhub = 0;
+    if (!nlong) return;
+    DevBuf<uint32_t> lens(nlong + 1, s_);
+    k_row_lens<<<grid_for(nlong, 256), 256, 0, s_>>>(lrows.get(), nlong, c.ptr.get(), lens.get());
+    GM_LAUNCH_CHECK();
+    std::vector<uint32_t> rows(nlong), len(nlong);
+    GM_CUDA(cudaMemcpyAsync(rows.data(), lrows.get(), nlong * 4, cudaMemcpyDeviceToHost, s_));
+    GM_CUDA(cudaMemcpyAsync(len.data(), lens.get(), nlong * 4, cudaMemcpyDeviceToHost, s_));
+    GM_CUDA(cudaStreamSynchronize(s_));
+    std::vector<uint32_t> mid;
+    std::vector<std::pair<uint32_t, uint32_t>> hub;
+    mid.reserve(nlong);
+    for (uint64_t i = 0; i < nlong; ++i) {
+      if (len[i] > kHubRow)
+        hub.emplace_back(len[i], rows[i]);
+      else
+        mid.push_back(rows[i]);
+    }
+    if (hub.empty()) return;
+    std::sort(hub.begin(), hub.end(), [](const auto& a, const auto& b) {
+      return a.first != b.first ? a.first > b.first : a.second < b.second;
+    });
+    std::vector<uint32_t> h(hub.size());
+    for (size_t i = 0; i < hub.size(); ++i) h[i] = hub[i].second;
+    nhub = h.size();
+    hrows.alloc(nhub + 1, s_);
+    GM_CUDA(cudaMemcpyAsync(hrows.get(), h.data(), nhub * 4, cudaMemcpyHostToDevice, s_));
+    nlong = mid.size();
+    if (nlong)
+      GM_CUDA(cudaMemcpyAsync(lrows.get(), mid.data(), nlong * 4, cudaMemcpyHostToDevice, s_));
+    GM_CUDA(cudaStreamSynchronize(s_));
+  }
+
+  void pull(const Csr& c, DevBuf<uint32_t>& lrows, uint64_t& nlong, DevBuf<uint32_t>& hrows,
+            uint64_t& nhub, bool& have, R* y, uint32_t* ybits) {
     const uint64_t n = g_.n;
     if (!have) {
       nlong = long_rows(c, lrows);
+      nhub = 0;
+      if constexpr (kHubPath) {
+        static const bool hub_on = !(getenv("GM_GENERIC_HUB") && getenv("GM_GENERIC_HUB")[0] == '0');
+        if (hub_on) split_hubs(c, lrows, nlong, hrows, nhub);
+      }
       have = true;
     }
     const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
@@ -696,6 +933,29 @@ class Engine {
     // critical path) run on a side stream concurrently with the short rows;
     // both OR their validity bits into the zeroed words.
     GM_CUDA(cudaMemsetAsync(ybits, 0, (n + 31) / 32 * 4, s_));
+    if constexpr (kHubPath) {
+      if (nhub) {
+        if (!hub_) {
+          GM_CUDA(cudaStreamCreateWithFlags(&hub_, cudaStreamNonBlocking));
+          GM_CUDA(cudaEventCreateWithFlags(&hfork_, cudaEventDisableTiming));
+          GM_CUDA(cudaEventCreateWithFlags(&hjoin_, cudaEventDisableTiming));
+          int dev = 0;
+          GM_CUDA(cudaGetDevice(&dev));
+          GM_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
+        }
+        GM_CUDA(cudaEventRecord(hfork_, s_));
+        GM_CUDA(cudaStreamWaitEvent(hub_, hfork_, 0));
+        // two 512-thread CTAs per SM: half the SM's threads, the rest for the
+        // short- and mid-row kernels running beside it
+        const unsigned hgrid = unsigned(std::min<uint64_t>(nhub, uint64_t(2 * sms_)));
+        if (!hclaim_) hclaim_.alloc(1, s_);
+        GM_CUDA(cudaMemsetAsync(hclaim_.get(), 0, 4, hub_));
+        k_pull_hub<P><<<hgrid, kHubThreads, 0, hub_>>>(p_, hrows.get(), nhub, hclaim_.get(), c.ptr.get(),
+                                                        c.idx.get(), c.val.get(), x_.get(),
+                                                        xbits_.get(), props_.get(), y, ybits);
+        GM_LAUNCH_CHECK();
+      }
+    }
     if (nlong) {
       if (!side_) {
         GM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
@@ -746,6 +1006,10 @@ class Engine {
     if (nlong) {
       GM_CUDA(cudaEventRecord(join_, side_));
       GM_CUDA(cudaStreamWaitEvent(s_, join_, 0));
+    }
+    if (nhub) {
+      GM_CUDA(cudaEventRecord(hjoin_, hub_));
+      GM_CUDA(cudaStreamWaitEvent(s_, hjoin_, 0));
     }
   }
 
@@ -804,9 +1068,9 @@ class Engine {
       return;
     }
     const Csr& first = d == Direction::IN ? g_.fwd() : g_.in;
-    pull(first, long1_, nlong1_, have1_, y_.get(), ybits_.get());
+    pull(first, long1_, nlong1_, hub1_, nhub1_, have1_, y_.get(), ybits_.get());
     if (d == Direction::BOTH) {
-      pull(g_.fwd(), long2_, nlong2_, have2_, y2_.get(), y2bits_.get());
+      pull(g_.fwd(), long2_, nlong2_, hub2_, nhub2_, have2_, y2_.get(), y2bits_.get());
       k_merge<P><<<grid, 256, 0, s_>>>(p_, n, y_.get(), ybits_.get(), y2_.get(), y2bits_.get());
       GM_LAUNCH_CHECK();
     }
@@ -908,6 +1172,9 @@ class Engine {
   DevBuf<uint32_t> ybits_, y2bits_;
   DevBuf<uint32_t> long1_, long2_;  // long rows of the first / second route's CSR
   uint64_t nlong1_ = 0, nlong2_ = 0;
+  DevBuf<uint32_t> hub1_, hub2_;    // hub rows (k_pull_hub), longest first
+  DevBuf<unsigned> hclaim_;         // k_pull_hub's row counter
+  uint64_t nhub1_ = 0, nhub2_ = 0;
   bool have1_ = false, have2_ = false;
   DevBuf<unsigned long long> ctr_;
   DevBuf<DevError> err_;
@@ -921,6 +1188,9 @@ class Engine {
   bool pushing_ = false, pushed_ = false;
   cudaStream_t side_ = nullptr;  // long rows, concurrent with the short-row kernel
   cudaEvent_t fork_{}, join_{};
+  cudaStream_t hub_ = nullptr;   // hub rows, concurrent with both
+  cudaEvent_t hfork_{}, hjoin_{};
+  int sms_ = 148;
   cudaEvent_t e0_{}, e1_{}, e2_{}, e3_{};
 };
 

@@ -11,6 +11,13 @@
 
 namespace gm {
 
+__global__ void k_row_lens(const uint32_t* rows, uint64_t nrows, const uint64_t* ptr,
+                           uint32_t* lens) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrows;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    lens[i] = uint32_t(min(ptr[rows[i] + 1] - ptr[rows[i]], uint64_t(0xFFFFFFFFu)));
+}
+
 __global__ void k_long_rows(uint64_t n, const uint64_t* ptr, uint32_t* rows,
                             unsigned long long* cnt) {
   for (uint64_t v0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~uint64_t(31); v0 < n;

@@ -248,6 +248,61 @@ def test_in_scatter(gm):
     assert list(yv) == [True, False] and y[0] == 2.0
 
 
+def test_generic_hub_rows_sequential_fold(gm):
+    """Rows above the hub threshold (4096 entries) of order-sensitive programs
+    go to k_pull_hub (producer warps + one sequential consumer); their fp64
+    sums must be the reference's left-to-right fold in ascending source order
+    bit for bit, for the OUT (CSR(G^T)) and IN (CSR(G)) routes, with other
+    rows (short and mid-length) alongside."""
+    rng = np.random.default_rng(77)
+    n = 30000
+    hub_in = rng.permutation(np.arange(1, n))[:20000]          # 20000 -> 0
+    hub_out = rng.permutation(np.arange(1, n))[:9000]          # 7 -> 9000 targets
+    mid = rng.permutation(np.arange(1, n))[:600]               # 600 -> 5
+    s = np.concatenate([hub_in, np.full(9000, 7), mid, rng.integers(0, n, 40000)])
+    d = np.concatenate([np.zeros(20000, np.int64), hub_out, np.full(600, 5), rng.integers(0, n, 40000)])
+    keep = s != d
+    s, d = s[keep], d[keep]
+    key = np.unique(s.astype(np.int64) * n + d)
+    s, d = key // n, key % n
+    # values over many magnitudes, so any reordering of a fold changes its bits
+    x = rng.standard_normal(n) * np.exp(rng.uniform(-20, 20, n))
+    g = gm.Graph.from_edges(s, d, n)
+    for prog, rows, cols in ((gm.PROG_ADD_PROBE, d, s), (gm.PROG_IN_ADD_PROBE, s, d)):
+        _, _, y, yv = gm.superstep_phases(g, prog, x.copy(), np.ones(n, np.uint8))
+        order = np.lexsort((cols, rows))
+        r, c = rows[order], cols[order]
+        bounds = np.searchsorted(r, np.arange(n + 1))
+        want = np.zeros(n)
+        has = np.zeros(n, bool)
+        for k in range(n):
+            a, b = bounds[k], bounds[k + 1]
+            if b > a:
+                want[k] = np.cumsum(x[c[a:b]])[-1]
+                has[k] = True
+        assert np.array_equal(yv, has)
+        assert np.array_equal(_bits(y[has]), _bits(want[has]))
+        assert np.diff(bounds).max() > 4096  # the hub path ran
+
+
+def test_generic_pagerank_ref_hub_rows_vs_reference(gm, orc):
+    """The reference PageRankProgram on R-MAT scale 17 (in-degrees up to
+    ~10^4, so hub rows take k_pull_hub): ranks and per-superstep stats equal
+    the reference engine's bit for bit."""
+    g = gm.Graph.rmat(17, 16, seed=9, relabel=False)  # caller order = the reference's fold order
+    s, d, _ = g.edges()
+    n = g.num_vertices
+    assert np.bincount(d, minlength=n).max() > 4096
+    props = np.zeros(n, gm.PAGERANK_STATE)
+    props["rank"] = 1.0
+    props["out_degree"] = g.degree_vector("out")
+    st = gm.run_graph_program(g, gm.PROG_PAGERANK_REF, props, np.ones(n, np.uint8), 6,
+                              params=[0.15])
+    want, wst, _ = orc.ref_pagerank(n, s, d, 0.15, 6)
+    assert np.array_equal(_bits(props["rank"]), _bits(want))
+    assert _stats_key(st) == wst
+
+
 def test_callback_failure_context(gm):
     # test_engine.cpp:225-236
     s, d, v = chain()

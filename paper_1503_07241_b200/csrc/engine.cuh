@@ -106,6 +106,26 @@ __device__ __forceinline__ uint64_t ext_id(const uint32_t* iperm, uint64_t v) {
   return iperm ? uint64_t(iperm[v]) : v;
 }
 
+// Adds lane 0's counts of every warp to ctr[0] (a) and ctr[1] (b, if nonzero
+// anywhere) with one atomic per CTA: an atomic per warp step on one counter
+// serialised at its L2 slice (k_send 0.36 ms at scale 23, 262 K words x 2).
+// Every thread of the CTA must call it.
+__device__ __forceinline__ void block_add_u64(unsigned long long* ctr, unsigned long long a,
+                                              unsigned long long b) {
+  __shared__ unsigned long long s_ab[2];
+  if (threadIdx.x == 0) s_ab[0] = s_ab[1] = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31u) == 0) {
+    if (a) atomicAdd(&s_ab[0], a);
+    if (b) atomicAdd(&s_ab[1], b);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_ab[0]) atomicAdd(&ctr[0], s_ab[0]);
+    if (s_ab[1]) atomicAdd(&ctr[1], s_ab[1]);
+  }
+}
+
 // ---------------------------------------------------------------- kernels
 // Phase 1, engine.hpp:76-98: x[v] = send(prop[v]) for active v.
 template <typename P>
@@ -115,6 +135,7 @@ __global__ void k_send(P p, uint64_t n, const typename P::vertex_t* props, const
   const uint64_t words = (n + 31) / 32;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long na = 0, no = 0;  // lane 0's running counts
   for (uint64_t w = warp; w < words; w += nwarps) {
     const uint64_t v = w * 32 + lane_id();
     const bool act = v < n && bit_test(active, uint32_t(v));
@@ -137,10 +158,11 @@ __global__ void k_send(P p, uint64_t n, const typename P::vertex_t* props, const
     const unsigned ob = __ballot_sync(0xffffffffu, ok);
     if (lane_id() == 0) {
       xbits[w] = ob;
-      if (ab) atomicAdd(&ctr[0], (unsigned long long)__popc(ab));
-      if (ob) atomicAdd(&ctr[1], (unsigned long long)__popc(ob));
+      na += __popc(ab);
+      no += __popc(ob);
     }
   }
+  block_add_u64(ctr, na, no);
 }
 
 // Frontier-proportional superstep (SpMSpV push), engine.hpp:224-260 with the
@@ -719,6 +741,7 @@ __global__ void k_apply(P p, uint64_t n, typename P::reduced_t* y, const uint32_
   const uint64_t words = (n + 31) / 32;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long nu = 0;  // lane 0's running count
   for (uint64_t w = warp; w < words; w += nwarps) {
     const uint64_t v = w * 32 + lane_id();
     bool upd = false;
@@ -746,9 +769,10 @@ __global__ void k_apply(P p, uint64_t n, typename P::reduced_t* y, const uint32_
     const unsigned b = __ballot_sync(0xffffffffu, upd);
     if (lane_id() == 0) {
       active[w] = b;
-      if (b) atomicAdd(&ctr[2], (unsigned long long)__popc(b));
+      nu += __popc(b);
     }
   }
+  block_add_u64(ctr + 2, nu, 0);
 }
 
 __global__ void k_bytes_to_bits(const uint8_t* bytes, uint64_t n, uint32_t* bits);

@@ -91,9 +91,7 @@ def gm_pagerank_uses_hub(g):
     """Which single-GPU PageRank kernel the library runs for g (the rule of
     pagerank_hub_enabled, csrc/pagerank_hub.cu)."""
     e = os.environ.get("GM_PR_HUB")
-    if e is not None and e[:1] in "01":
-        return e[:1] == "1"
-    return g.num_vertices * 4 <= (64 << 20)
+    return not (e is not None and e[:1] == "0")
 
 
 B200_SPEC_HBM_GBS = 8000.0  # the north star's "~8 TB/s per GPU" (HBM3e spec)

@@ -58,7 +58,8 @@ constexpr int kHubWarps = 32;
 constexpr int kHubThreads = kHubWarps * 32;
 constexpr int kWIPT = 8;
 constexpr uint32_t kStep = 32 * kWIPT;  // nonzeros (pieces) per step
-constexpr uint32_t kHubCap = 49152;     // hub slots (shared memory 192 KB)
+constexpr uint32_t kHubCap = 49152;       // hub slots (shared memory 192 KB)
+constexpr uint32_t kHubCapLarge = 24576;  // x beyond L2 (96 KB)
 constexpr uint32_t kSellMax = 128;      // SELL rows: 0 < in-degree <= kSellMax
 constexpr uint32_t kNoRow = 0xFFFFFFFFu;
 constexpr uint32_t kNoHub = 0xFFFFFFFFu;   // hub_pos: not a hub
@@ -508,7 +509,15 @@ PrHubCache& hub_cache(Graph& g) {
   std::vector<uint32_t> slot_of(n, kNoHub);
   uint64_t nz = 0;
   for (uint64_t v = 0; v < n; ++v) nz += outdeg[v] != 0;
-  const uint64_t nh = std::min<uint64_t>(kHubCap, nz);
+  // Hub window: 49,152 slots (192 KB) while x is L2-sized; 24,576 (96 KB)
+  // beyond that, where the tail gathers miss L2 and the L1 that the smaller
+  // copy leaves holds their sectors (scale 28, ms per superstep by window:
+  // 49,152 28.3; 32,768 22.0; 24,576 21.7; 16,384 21.8; 8,192 22.5; the
+  // CTA-tile kernel 24.0).  GM_PR_HUBCAP overrides (measurement hook).
+  const char* hc = getenv("GM_PR_HUBCAP");
+  const uint64_t cap = hc ? std::min<uint64_t>(kHubCap, std::max<uint64_t>(4, strtoull(hc, nullptr, 10)))
+                          : (n * 4 <= (64ull << 20) ? kHubCap : kHubCapLarge);
+  const uint64_t nh = std::min<uint64_t>(cap, nz);
   {
     std::vector<uint32_t> order;
     order.reserve(nz);
@@ -687,17 +696,17 @@ PrHubCache& hub_cache(Graph& g) {
 
 }  // namespace
 
-// The hub path serves whole-graph supersteps on one GPU while the message
-// vector is L2-sized (<= 64 MB, scale <= 24 R-MAT); beyond that the gathers
-// are DRAM-sector bound and the CTA-tile kernel of pagerank.cu, whose
-// out-degree-ordered x keeps the warm sources L2-resident, is faster (scale
-// 28: 24 ms vs 26.6 ms per superstep).  GM_PR_HUB=0/1 forces either path.
+// The hub path serves every whole-graph superstep on one GPU; beyond an
+// L2-sized message vector it runs with the smaller hub window (kHubCapLarge),
+// which beats the CTA-tile kernel of pagerank.cu at scale 28 (21.7 vs 24.0 ms
+// per superstep; with the full 192 KB window it had lost, 26.6-28.3 ms).
+// GM_PR_HUB=0/1 forces either path; the CTA-tile kernel keeps serving the
+// row-sharded supersteps.
 bool pagerank_hub_enabled(const Graph& g) {
   if (g.n == 0 || g.in.nnz == 0) return false;
   const char* e = getenv("GM_PR_HUB");
   if (e && e[0] == '0') return false;
-  if (e && e[0] == '1') return true;
-  return g.n * 4 <= (64ull << 20);
+  return true;
 }
 
 std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t iters, float* out,

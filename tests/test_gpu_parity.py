@@ -376,6 +376,30 @@ def test_bfs_isolated_root_and_output_pass(gm, orc):
     assert lvl[root] == 0 and (lvl == -1).sum() == n - 1
 
 
+@pytest.mark.parametrize("n", [1, 31, 1000, 1023, 1025, 3001])
+def test_bfs_output_ragged_sizes(gm, orc, n):
+    """The compact output pass walks callers in blocks of 1024 (a warp per
+    block, a word of the non-isolated bitmap per lane): ragged vertex counts,
+    isolated vertices anywhere in caller order, roots isolated or not, and
+    repeated BFS on the same level stamps equal the reference."""
+    rng = np.random.default_rng(n)
+    m = 3 * n
+    s = rng.integers(0, n, m)
+    d = rng.integers(0, n, m)
+    iso = rng.random(n) < 0.3          # these vertices keep no edges
+    keep = ~iso[s] & ~iso[d] & (s != d)
+    s, d = s[keep], d[keep]
+    g = gm.Graph.from_edges(s, d, n, preprocess=True, symmetrize=True, relabel=True)
+    es, ed, _ = g.edges()
+    roots = sorted({0, n - 1, n // 2, int(np.flatnonzero(iso)[0]) if iso.any() else 0})
+    for rep in range(2):
+        for root in roots:
+            lvl, st = gm.bfs(g, root)
+            want, wst = orc.bfs(n, es, ed, root, presorted=True)
+            assert np.array_equal(lvl, want), (n, root, rep)
+            assert _stats_key(st) == wst
+
+
 # ------------------------------------------------------- medium R-MAT
 
 @pytest.mark.parametrize("scale", [14, 16])

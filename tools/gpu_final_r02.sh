@@ -19,8 +19,13 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
   > gpurun_out/${tag}_ncu_launch_bfs28.log 2>&1
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_requests_srcunit_tex.sum,lts__t_sectors_srcunit_tex.sum,l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"
 timeout 1200 ncu --metrics $M --clock-control none -k regex:k_bfs_coop -s 1 -c 1 --csv python tools/prof_run.py bfs --scale 28 --reps 2 > gpurun_out/${tag}_bfs28_counters.csv 2>&1
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_bfs_coop -s 1 -c 1 \
-  -o gpurun_out/${tag}_bfs28_coop python tools/prof_run.py bfs --scale 28 --reps 2 > gpurun_out/${tag}_ncu_bfs28.log 2>&1
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_bfs_coop -s 1 -c 1 -f \
+  -o /tmp/${tag}_bfs28_coop python tools/prof_run.py bfs --scale 28 --reps 2 > gpurun_out/${tag}_ncu_bfs28.log 2>&1
+ncu -i /tmp/${tag}_bfs28_coop.ncu-rep --page raw --csv > gpurun_out/${tag}_bfs28_coop_raw.csv 2>&1
+M2="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_requests_srcunit_tex.sum"
+timeout 900 ncu --metrics $M2 --clock-control none -k regex:k_bfs_output -s 1 -c 2 --csv python tools/prof_run.py bfs --scale 28 --reps 3 > gpurun_out/${tag}_bfs28_output_counters.csv 2>&1
+timeout 900 python tools/generic_bench.py 20 > gpurun_out/${tag}_generic20.log 2>&1
+timeout 900 python tools/generic_bench.py 23 > gpurun_out/${tag}_generic23.log 2>&1
 tail -3 gpurun_out/${tag}_gpu_tests.log; cat gpurun_out/${tag}_smoke.log
 for f in gpurun_out/${tag}_bench_*.json; do echo "== $f"; tail -1 $f | cut -c1-400; done
 ls -la gpurun_out/${tag}_*

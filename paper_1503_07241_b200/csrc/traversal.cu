@@ -38,6 +38,7 @@
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -52,7 +53,17 @@ constexpr int kMaxRecorded = 4096;  // per-superstep records kept on device
 constexpr int kBatch = 4;           // supersteps enqueued per host check
 constexpr int kEPT = 4;             // edges per thread, edge-balanced passes
 // Frontier-bitmap prefix staged per CTA: 96 KB at 2 CTAs per SM, 64 KB at 3.
-constexpr uint32_t smem_fb_words(int blocks_per_sm) { return blocks_per_sm >= 3 ? 16 * 1024 : 24 * 1024; }
+// Frontier-bitmap prefix in shared memory per CTA (words): what it does not
+// take stays L1 for the head and visited loads.  Measured (re-entry session,
+// tools/gpu_r02y32.sh / y33.sh): the 2-CTA variant (scale 23) 24 K words
+// 0.299 ms per BFS, 8 K 0.285, 4 K 0.281, 2 K 0.282, 1 K 0.332 (the hubs no
+// longer fit); the 3-CTA variant (scale 28) 16 K 2.846 ms, 8 K 2.866, 4 K
+// 2.899.  GM_BFS_PREFIX_WORDS overrides (measurement hook).
+inline uint32_t smem_fb_words(int blocks_per_sm) {
+  static const char* e = getenv("GM_BFS_PREFIX_WORDS");
+  if (e) return uint32_t(std::max(32L, std::min(24L * 1024, strtol(e, nullptr, 10))));
+  return blocks_per_sm >= 3 ? 16 * 1024 : 4 * 1024;
+}
 constexpr unsigned kGrid = 148 * 2;           // persistent grid for the SSSP kernels
 constexpr unsigned kThreads = 1024;
 constexpr int kCountShift = 36;  // packed counter: count << 36 | edges
@@ -1830,7 +1841,9 @@ std::vector<gm_iteration_stats> sssp(Graph& g, uint64_t root, int64_t max_iters,
       k_rowid<<<grid_for(n * 32, 256), 256, 0, s>>>(g.in.ptr.get(), n, c.rowid.get());
       GM_LAUNCH_CHECK();
       c.msg.alloc(n + 4, s);
-      c.pull_hub = uint32_t(std::max<uint64_t>(4, std::min<uint64_t>(kSsspHub, n) & ~uint64_t(3)));
+      const char* he = getenv("GM_SSSP_HUB");  // measurement hook: hub window
+      const uint64_t hub_cap = he ? std::min<uint64_t>(kSsspHub, strtoull(he, nullptr, 10)) : kSsspHub;
+      c.pull_hub = uint32_t(std::max<uint64_t>(4, std::min<uint64_t>(hub_cap, n) & ~uint64_t(3)));
       int dev = 0, sms = 0;
       GM_CUDA(cudaGetDevice(&dev));
       GM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

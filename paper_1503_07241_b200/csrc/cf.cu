@@ -354,10 +354,15 @@ __global__ void __launch_bounds__(256) k_cf_items_g(const uint32_t* __restrict__
 // p' = p + gamma * (sum - lambda * p); sum = out-route items then in-route items.
 // Rows [lo, lo + n): rit / rif are indexed by v - lo, f by the global row, fn
 // by the local one (the single-GPU call passes lo = 0).
-__global__ void k_cf_apply(uint64_t lo, uint64_t n, int k, const uint32_t* rit, const uint32_t* rif,
+// K > 0: compile-time latent dimension (the element -> (vertex, component)
+// split is a multiply-shift; a run-time 64-bit t / k and t % k per element had
+// made this pass ~5x slower than its bytes); K == 0: run-time kr.
+template <int K>
+__global__ void k_cf_apply(uint64_t lo, uint64_t n, int kr, const uint32_t* rit, const uint32_t* rif,
                            const float* part_t, const float* part_f, const float* f, float* fn,
                            float gamma, float lambda, uint32_t* vbits,
                            unsigned long long* changed) {
+  const int k = K > 0 ? K : kr;
   unsigned long long ch = 0;
   const uint64_t total = n * uint64_t(k);
   const unsigned lane = threadIdx.x & 31u;
@@ -366,10 +371,19 @@ __global__ void k_cf_apply(uint64_t lo, uint64_t n, int k, const uint32_t* rit, 
        base += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t t = base + lane;
     const bool valid = t < total;
-    const uint64_t v = valid ? t / k : ~0ull;
+    uint64_t v = ~0ull;
+    int i = 0;
+    if (valid) {
+      if (K > 0 && t < (1ull << 32)) {
+        v = uint32_t(t) / uint32_t(K);
+        i = int(uint32_t(t) - uint32_t(v) * uint32_t(K));
+      } else {
+        v = t / uint64_t(k);
+        i = int(t % uint64_t(k));
+      }
+    }
     bool changed_here = false;
     if (valid) {
-      const int i = int(t % k);
       float s = 0.0f;
       const uint32_t a0 = rit[v], a1 = rit[v + 1], b0 = rif[v], b1 = rif[v + 1];
       bool any = false;
@@ -565,7 +579,7 @@ void cf_shard_step(Graph& g, uint64_t lo, uint64_t hi, int64_t k, const float* f
   if (total) {
     if (c.vbits.size() < (hi - lo + 31) / 32) c.vbits.alloc((hi - lo + 31) / 32, s);
     c.vbits.zero(s);
-    k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(lo, hi - lo, int(k), c.rowitem_t.get(),
+    (k == 20 ? k_cf_apply<20> : k_cf_apply<0>)<<<grid_for(total, 256), 256, 0, s>>>(lo, hi - lo, int(k), c.rowitem_t.get(),
                                                     c.rowitem_f.get(), c.part_t.get(), c.part_f.get(),
                                                     f_full, f_block, gamma, lambda, c.vbits.get(),
                                                     upd.get());
@@ -662,7 +676,7 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
     if (total) {
       if (c.vbits.size() < (n + 31) / 32) c.vbits.alloc((n + 31) / 32, s);
       c.vbits.zero(s);
-      k_cf_apply<<<grid_for(total, 256), 256, 0, s>>>(0, n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
+      (k == 20 ? k_cf_apply<20> : k_cf_apply<0>)<<<grid_for(total, 256), 256, 0, s>>>(0, n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
                                                       c.part_t.get(), c.part_f.get(), f, fn, gamma,
                                                       lambda, c.vbits.get(), upd.get() + it);
     }

@@ -1122,13 +1122,16 @@ class Engine {
     spmv();
     pushing_ = false;
     GM_CUDA(cudaEventRecord(e2_, s_));
-    check_error();  // a failed SpMV aborts before apply (engine.hpp:251-257)
+    // a failed SpMV aborts before apply (engine.hpp:251-257); programs without
+    // failing callbacks cannot set the error word, so they skip both reads
+    // (each was a host round trip per superstep)
+    if constexpr (can_fail<P>::value) check_error();
     apply();
     GM_CUDA(cudaEventRecord(e3_, s_));
     unsigned long long c[3];
     GM_CUDA(cudaMemcpyAsync(c, ctr_.get(), sizeof(c), cudaMemcpyDeviceToHost, s_));
     GM_CUDA(cudaStreamSynchronize(s_));
-    check_error();
+    if constexpr (can_fail<P>::value) check_error();
     float spmv_ms = 0, total_ms = 0;
     GM_CUDA(cudaEventElapsedTime(&spmv_ms, e1_, e2_));
     GM_CUDA(cudaEventElapsedTime(&total_ms, e0_, e3_));

@@ -280,7 +280,7 @@ def cpu_sample_scale(scale):
     return sc
 
 
-def ref_bfs_sample(orc, scale, seed):
+def ref_bfs_sample(orc, scale, seed, threads=0):
     """The reference engine's algo::bfs (traversal.hpp:119-123) on the
     symmetrised R-MAT graph of `scale` (our seeded generator + io::preprocess
     semantics), from the seed-chosen root.  -> (RefGraph, root, teps_edges, setup_s)."""
@@ -290,7 +290,7 @@ def ref_bfs_sample(orc, scale, seed):
     n = 1 << scale
     deg = np.bincount(s, minlength=n).astype(np.uint32)
     root = orc.pick_source(seed, deg)
-    rg = orc.RefGraph("dist", n, s, d, threads=0)
+    rg = orc.RefGraph("dist", n, s, d, threads=threads)
     lvl, _ = orc.bfs(n, s, d, root, presorted=True)
     edges = int(deg[lvl >= 0].sum()) // 2  # Graph500: undirected edges reached
     return rg, root, edges, len(s), time.perf_counter() - t0
@@ -429,6 +429,12 @@ class BfsWorkload(Workload):
         rg, root, edges, m, setup = ref_bfs_sample(orc, sc, self.args.seed)
         secs = min(rg.run_dist("bfs", root)[2] for _ in range(2))
         rg.close()
+        # the reference on all host threads and on one thread; the
+        # one-thread sample is a smaller graph (scale 20) to keep the run short
+        sc1 = min(sc, 20)
+        rg1, root1, edges1, m1, _ = ref_bfs_sample(orc, sc1, self.args.seed, threads=1)
+        secs1 = min(rg1.run_dist("bfs", root1)[2] for _ in range(2))
+        rg1.close()
         why = "" if sc == self.args.scale else (
             f"; scale {self.args.scale} needs ~{REF_BYTES_PER_ENTRY * 32 * (1 << self.args.scale) / 1e9:.0f}"
             f" GB of host memory in the reference engine (80 B per stored entry), more than this host "
@@ -436,7 +442,11 @@ class BfsWorkload(Workload):
         return {"value": round(edges / secs / 1e9, 6), "unit": "GTEPS",
                 "cores": int(R.ref_hardware_threads()), "kind": "reference", "seconds": round(secs, 4),
                 "sample": f"one BFS (best of 2) on the symmetrised R-MAT scale-{sc} graph "
-                          f"({m} stored entries, seed {self.args.seed}, graph build excluded){why}"}
+                          f"({m} stored entries, seed {self.args.seed}, graph build excluded){why}",
+                "one_thread": {"value": round(edges1 / secs1 / 1e9, 6), "unit": "GTEPS", "cores": 1,
+                               "seconds": round(secs1, 4),
+                               "sample": f"one BFS (best of 2) on the symmetrised R-MAT scale-{sc1} "
+                                         f"graph ({m1} stored entries), reference engine with 1 thread"}}
 
 
 def nccl_comm(d):

@@ -916,6 +916,9 @@ def run_ours(args, d: Dist):
             "updated": s.vertices_updated, "edges": s.edges_processed,
             "us": round(s.spmv_seconds * 1e6, 2),
             "gteps": round(s.edges_processed / s.spmv_seconds / 1e9, 3) if s.spmv_seconds else None,
+            # per-superstep algorithmic GB/s (the 8(d) byte formulas)
+            "gbs": round(s.bytes_algorithmic / s.spmv_seconds / 1e9, 1)
+            if s.spmv_seconds and getattr(s, "bytes_algorithmic", 0) else None,
             **({"comm_us": round(s.comm_seconds * 1e6, 2)} if getattr(w, "sharded", False) else {})}
            for s in st]
     line = {

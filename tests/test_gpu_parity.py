@@ -376,6 +376,24 @@ def test_bfs_isolated_root_and_output_pass(gm, orc):
     assert lvl[root] == 0 and (lvl == -1).sum() == n - 1
 
 
+def test_bfs_level_stamps_wrap(gm, orc, monkeypatch):
+    """Levels are per-BFS stamps (lbase + level) in a 32-bit array that no BFS
+    clears; the host zeroes it when the next BFS's stamps could wrap.  Start
+    the stamps just below 2^32: the first BFS runs at the top of the range,
+    the second wraps (array zeroed, lbase = 1), later ones continue -- every
+    result equals the reference."""
+    monkeypatch.setenv("GM_BFS_LBASE_START", str(0xFFFFFFFF - 1500))
+    g = gm.Graph.rmat(10, 8, seed=12, symmetrize=True, relabel=True)  # depth bound <= 1025
+    s, d, _ = g.edges()
+    n = g.num_vertices
+    for rep, seed in enumerate((1, 2, 3, 1)):
+        root = g.pick_source(seed)
+        lvl, st = gm.bfs(g, root)
+        want, wst = orc.bfs(n, s, d, root, presorted=True)
+        assert np.array_equal(lvl, want), rep
+        assert _stats_key(st) == wst, rep
+
+
 @pytest.mark.parametrize("n", [1, 31, 1000, 1023, 1025, 3001])
 def test_bfs_output_ragged_sizes(gm, orc, n):
     """The compact output pass walks callers in blocks of 1024 (a warp per

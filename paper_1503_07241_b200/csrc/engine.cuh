@@ -132,35 +132,50 @@ template <typename P>
 __global__ void k_send(P p, uint64_t n, const typename P::vertex_t* props, const uint32_t* active,
                        const uint32_t* iperm, typename P::message_t* x, uint32_t* xbits,
                        unsigned long long* ctr, DevError* err) {
+  // A warp takes 32 consecutive activity words (one coalesced load), then
+  // only the nonzero ones, lane = vertex: a small frontier costs a pass over
+  // the N/8-byte bitmap, not a warp step per word (the light supersteps of
+  // the reference BfsProgram spent ~40 us here).
   const uint64_t words = (n + 31) / 32;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
   unsigned long long na = 0, no = 0;  // lane 0's running counts
-  for (uint64_t w = warp; w < words; w += nwarps) {
-    const uint64_t v = w * 32 + lane_id();
-    const bool act = v < n && bit_test(active, uint32_t(v));
-    bool ok = false;
-    if (act) {
-      typename P::message_t m;
-      if constexpr (can_fail<P>::value) {
-        int ec = 0;
-        ok = p.send_message(props[v], ext_id(iperm, v), &m, ec);
-        if (ec) {
-          record_error(err, ec, kPhaseSend, ext_id(iperm, v), 0, 0);
-          ok = false;
+  for (uint64_t w0 = warp * 32; w0 < words; w0 += nwarps * 32) {
+    const uint64_t wl = w0 + lane;
+    uint32_t aw = wl < words ? active[wl] : 0u;
+    if (wl == words - 1 && (n & 31u)) aw &= (1u << (n & 31u)) - 1u;
+    unsigned todo = __ballot_sync(0xffffffffu, aw != 0u);
+    uint32_t mine = 0;  // this lane's word of xbits
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t word = __shfl_sync(0xffffffffu, aw, j);
+      const uint64_t v = (w0 + uint64_t(j)) * 32 + lane;
+      const bool act = (word >> lane) & 1u;
+      bool ok = false;
+      if (act) {
+        typename P::message_t m;
+        if constexpr (can_fail<P>::value) {
+          int ec = 0;
+          ok = p.send_message(props[v], ext_id(iperm, v), &m, ec);
+          if (ec) {
+            record_error(err, ec, kPhaseSend, ext_id(iperm, v), 0, 0);
+            ok = false;
+          }
+        } else {
+          ok = p.send_message(props[v], ext_id(iperm, v), &m);
         }
-      } else {
-        ok = p.send_message(props[v], ext_id(iperm, v), &m);
+        if (ok) x[v] = m;
       }
-      if (ok) x[v] = m;
+      const unsigned ob = __ballot_sync(0xffffffffu, ok);
+      if (lane == unsigned(j)) mine = ob;
+      if (lane == 0) {
+        na += __popc(word);
+        no += __popc(ob);
+      }
     }
-    const unsigned ab = __ballot_sync(0xffffffffu, act);
-    const unsigned ob = __ballot_sync(0xffffffffu, ok);
-    if (lane_id() == 0) {
-      xbits[w] = ob;
-      na += __popc(ab);
-      no += __popc(ob);
-    }
+    if (wl < words) xbits[wl] = mine;
   }
   block_add_u64(ctr, na, no);
 }
@@ -738,39 +753,52 @@ template <typename P>
 __global__ void k_apply(P p, uint64_t n, typename P::reduced_t* y, const uint32_t* ybits,
                         typename P::vertex_t* props, uint32_t* active, const uint32_t* iperm,
                         unsigned long long* ctr, DevError* err) {
+  // 32 consecutive validity words per warp step (coalesced), then the nonzero
+  // ones lane = vertex; every activity word is rewritten (all flags cleared,
+  // changed vertices set)
   const uint64_t words = (n + 31) / 32;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
   unsigned long long nu = 0;  // lane 0's running count
-  for (uint64_t w = warp; w < words; w += nwarps) {
-    const uint64_t v = w * 32 + lane_id();
-    bool upd = false;
-    if (v < n && bit_test(ybits, uint32_t(v))) {
-      const typename P::vertex_t old = props[v];
-      typename P::vertex_t fresh;
-      bool okv = true;
-      const typename P::reduced_t yv = y[v];
-      if constexpr (can_push<P>::value) y[v] = p.reduce_identity();  // the push's invariant
-      if constexpr (can_fail<P>::value) {
-        int ec = 0;
-        fresh = p.apply(yv, old, ec);
-        if (ec) {
-          record_error(err, ec, kPhaseApply, ext_id(iperm, v), 0, 0);
-          okv = false;
+  for (uint64_t w0 = warp * 32; w0 < words; w0 += nwarps * 32) {
+    const uint64_t wl = w0 + lane;
+    uint32_t yw = wl < words ? ybits[wl] : 0u;
+    if (wl == words - 1 && (n & 31u)) yw &= (1u << (n & 31u)) - 1u;
+    unsigned todo = __ballot_sync(0xffffffffu, yw != 0u);
+    uint32_t mine = 0;  // this lane's word of the new activity
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t word = __shfl_sync(0xffffffffu, yw, j);
+      const uint64_t v = (w0 + uint64_t(j)) * 32 + lane;
+      bool upd = false;
+      if ((word >> lane) & 1u) {
+        const typename P::vertex_t old = props[v];
+        typename P::vertex_t fresh;
+        bool okv = true;
+        const typename P::reduced_t yv = y[v];
+        if constexpr (can_push<P>::value) y[v] = p.reduce_identity();  // the push's invariant
+        if constexpr (can_fail<P>::value) {
+          int ec = 0;
+          fresh = p.apply(yv, old, ec);
+          if (ec) {
+            record_error(err, ec, kPhaseApply, ext_id(iperm, v), 0, 0);
+            okv = false;
+          }
+        } else {
+          fresh = p.apply(yv, old);
         }
-      } else {
-        fresh = p.apply(yv, old);
+        if (okv && !p.equal(fresh, old)) {
+          props[v] = fresh;
+          upd = true;
+        }
       }
-      if (okv && !p.equal(fresh, old)) {
-        props[v] = fresh;
-        upd = true;
-      }
+      const unsigned b = __ballot_sync(0xffffffffu, upd);
+      if (lane == unsigned(j)) mine = b;
+      if (lane == 0) nu += __popc(b);
     }
-    const unsigned b = __ballot_sync(0xffffffffu, upd);
-    if (lane_id() == 0) {
-      active[w] = b;
-      nu += __popc(b);
-    }
+    if (wl < words) active[wl] = mine;
   }
   block_add_u64(ctr + 2, nu, 0);
 }

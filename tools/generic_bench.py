@@ -25,12 +25,18 @@ for relabel in (False, True):
 g = gm.Graph.rmat(scale, 16, seed=1, symmetrize=True, relabel=True)
 n = g.num_vertices
 root = g.pick_source(1)
-for rep in range(2):
+walls = []
+for rep in range(3):
     dist = np.full(n, np.inf)
     dist[root] = 0.0
     act = np.zeros(n, np.uint8)
     act[root] = 1
+    t = time.perf_counter()
     st = gm.run_graph_program(g, gm.PROG_BFS_REF, dist, act, n + 1)
+    walls.append(time.perf_counter() - t)
 tot = sum(s.spmv_seconds for s in st)
-print(f"scale {scale} BfsProgram supersteps={len(st)} spmv_ms={tot*1e3:.2f} "
-      f"per_step_us={[round(s.spmv_seconds*1e6,1) for s in st]}")
+dev = sum(s.total_seconds for s in st)
+print(f"scale {scale} BfsProgram supersteps={len(st)} spmv_ms={tot*1e3:.2f} device_ms={dev*1e3:.2f} "
+      f"wall_ms={min(walls)*1e3:.1f} (incl. host<->device state copies) "
+      f"per_step_us={[round(s.spmv_seconds*1e6,1) for s in st]} "
+      f"superstep_us={[round(s.total_seconds*1e6,1) for s in st]}")

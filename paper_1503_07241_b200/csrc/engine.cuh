@@ -904,7 +904,7 @@ class Engine {
 
   void send() {
     const uint64_t n = g_.n;
-    const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
+    const unsigned grid = grid_for((n + 31) / 32, 256);  // a warp per 32 words
     k_send<P><<<grid, 256, 0, s_>>>(p_, n, props_.get(), active_.get(), iperm(), x_.get(),
                                      xbits_.get(), ctr_.get(), err_.get());
     GM_LAUNCH_CHECK();
@@ -1081,7 +1081,7 @@ class Engine {
         qctr_.alloc(2, s_);
       }
       qctr_.zero(s_);
-      k_msg_queue<<<grid_for((n + 31) / 32 * 32, 256), 256, 0, s_>>>(n, xbits_.get(), g_.fwd().ptr.get(),
+      k_msg_queue<<<grid_for((n + 31) / 32, 256), 256, 0, s_>>>(n, xbits_.get(), g_.fwd().ptr.get(),
                                                                    q_.get(), qctr_.get());
       GM_LAUNCH_CHECK();
       unsigned long long h[2];
@@ -1099,7 +1099,7 @@ class Engine {
       GM_CUDA(cudaMemsetAsync(ybits_.get(), 0, words * 4, s_));
       const Csr& fw = g_.fwd();
       if (!qoff_) qoff_.alloc(g_.n + 2, s_);
-      k_queue_degrees<<<grid_for(g_.n, 256), 256, 0, s_>>>(q_.get(), qctr_.get(), fw.ptr.get(),
+      k_queue_degrees<<<grid_for(nq_ + 1, 256), 256, 0, s_>>>(q_.get(), qctr_.get(), fw.ptr.get(),
                                                           qoff_.get());
       GM_LAUNCH_CHECK();
       exclusive_scan_u64(qoff_.get(), nq_ + 1, s_);
@@ -1130,7 +1130,7 @@ class Engine {
 
   void apply() {
     const uint64_t n = g_.n;
-    const unsigned grid = grid_for((n + 31) / 32 * 32, 256);
+    const unsigned grid = grid_for((n + 31) / 32, 256);  // a warp per 32 words
     k_apply<P><<<grid, 256, 0, s_>>>(p_, n, y_.get(), ybits_.get(), props_.get(), active_.get(),
                                       iperm(), ctr_.get(), err_.get());
     GM_LAUNCH_CHECK();

@@ -590,7 +590,7 @@ template <typename P>
 __global__ void __launch_bounds__(kHubThreads) k_pull_hub(
     P p, const uint32_t* rows, uint64_t nrows, unsigned* claim, const uint64_t* ptr,
     const uint32_t* idx, const uint8_t* val, const typename P::message_t* x, const uint32_t* xbits,
-    const typename P::vertex_t* props, typename P::reduced_t* y, uint32_t* ybits) {
+    uint64_t nx, const typename P::vertex_t* props, typename P::reduced_t* y, uint32_t* ybits) {
   using R = typename P::reduced_t;
   using E = typename P::edge_t;
   using M = typename P::message_t;
@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(kHubThreads) k_pull_hub(
         for (int h = 0; h < 2; ++h) {
           const uint64_t e = e0 + uint64_t(c) * kHubSlot + 32u * h + lane;
           in[h] = e < e1;
+          GM_DCHECK(!in[h] || j[h] < nx);
           word[h] = in[h] ? xbits[j[h] >> 5] : 0u;
           m[h] = in[h] ? x[j[h]] : M{};
           ed[h] = in[h] ? load_edge<E>(val, e) : E{};
@@ -1004,7 +1005,7 @@ class Engine {
         GM_CUDA(cudaMemsetAsync(hclaim_.get(), 0, 4, hub_));
         k_pull_hub<P><<<hgrid, kHubThreads, 0, hub_>>>(p_, hrows.get(), nhub, hclaim_.get(), c.ptr.get(),
                                                         c.idx.get(), c.val.get(), x_.get(),
-                                                        xbits_.get(), props_.get(), y, ybits);
+                                                        xbits_.get(), n, props_.get(), y, ybits);
         GM_LAUNCH_CHECK();
       }
     }

@@ -447,10 +447,14 @@ __global__ void __launch_bounds__(256) k_bfs_output_nz(uint64_t n, uint64_t root
         const uint32_t wr = __shfl_sync(0xffffffffu, word, r0 + j);
         const uint32_t br = __shfl_sync(0xffffffffu, wbase, r0 + j);
         set[j] = (wr >> lane) & 1u;
+        GM_DCHECK(!set[j] || br + __popc(wr & below) < n);
         st[j] = set[j] ? __ldcs(&perm_c[br + __popc(wr & below)]) : 0u;
       }
 #pragma unroll
-      for (int j = 0; j < kB; ++j) st[j] = set[j] ? __ldg(&stamp[st[j]]) : 0u;
+      for (int j = 0; j < kB; ++j) {
+        GM_DCHECK(!set[j] || st[j] < n);
+        st[j] = set[j] ? __ldg(&stamp[st[j]]) : 0u;
+      }
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         const uint64_t x = b * 1024 + uint64_t(r0 + j) * 32 + lane;

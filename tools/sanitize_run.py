@@ -50,6 +50,11 @@ if what in ("generic", "all"):
     props["rank"] = 1.0
     props["out_degree"] = g.degree_vector("out")
     gm.run_graph_program(g, gm.PROG_PAGERANK_REF, props, np.ones(n, np.uint8), 2, params=[0.15])
+    # a star of 6000 in-edges: a hub row (> 4096 entries) for k_pull_hub
+    hub = np.arange(1, 6001)
+    gh = gm.Graph.from_edges(hub, np.zeros(6000, np.int64), 6001)
+    _, _, y, yv = gm.superstep_phases(gh, gm.PROG_ADD_PROBE, np.ones(6001), np.ones(6001, np.uint8))
+    assert yv[0] and y[0] == 6000.0
 if what in ("dist", "all"):
     from paper_1503_07241_b200 import dist as D
     comm = D.Comm.local([0, 0])

@@ -303,6 +303,41 @@ def test_generic_pagerank_ref_hub_rows_vs_reference(gm, orc):
     assert _stats_key(st) == wst
 
 
+def test_generic_reference_programs_configs_scale(gm, orc):
+    """The drop-in path at BASELINE configs[0] size: the reference's own
+    PageRankProgram (fp64, activity gated, 20 supersteps) through the generic
+    engine on the directed R-MAT scale-20 graph, and its SsspProgram on real
+    weights, equal the reference engine (oracle/_ref, the reference headers
+    compiled) bit for bit -- ranks / distances and every superstep's stats.
+    Rows up to ~10^4 entries take the hub and long-row kernels."""
+    if orc.ref_lib() is None:
+        pytest.skip("oracle/_ref (the compiled reference engine) is not built")
+    n = 1 << 20
+    g = gm.Graph.rmat(20, 16, seed=1, relabel=False)  # caller order = the reference's fold order
+    s, d, _ = g.edges()
+    props = np.zeros(n, gm.PAGERANK_STATE)
+    props["rank"] = 1.0
+    props["out_degree"] = g.degree_vector("out")
+    st = gm.run_graph_program(g, gm.PROG_PAGERANK_REF, props, np.ones(n, np.uint8), 20,
+                              params=[0.15])
+    want, wst, _ = orc.ref_pagerank(n, s, d, 0.15, 20)
+    assert np.array_equal(_bits(props["rank"]), _bits(want))
+    assert _stats_key(st) == wst
+    gw = gm.Graph.rmat(20, 16, seed=2, relabel=False, weights=True)
+    s, d, w = gw.edges()
+    wr = w.astype(np.float64) + 0.25  # non-integer weights: the fp64 min-plus path
+    gf = gm.Graph.from_edges(s, d, n, wr)
+    root = gw.pick_source(2)
+    dist = np.full(n, np.inf)
+    dist[root] = 0.0
+    act = np.zeros(n, np.uint8)
+    act[root] = 1
+    st = gm.run_graph_program(gf, gm.PROG_SSSP_REF, dist, act, n + 1)
+    want, wst, _ = orc.ref_sssp(n, s, d, wr, root)
+    assert np.array_equal(_bits(dist), _bits(want))
+    assert _stats_key(st) == wst
+
+
 def test_callback_failure_context(gm):
     # test_engine.cpp:225-236
     s, d, v = chain()

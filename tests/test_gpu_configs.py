@@ -10,7 +10,8 @@ restatement of the reference (oracle/graphmat_oracle.c):
   checked over all 258M entries.
 * configs[2] SSSP scale 23, weights 1..255: distances bit-exact, stats identical,
   edge inequality dist[v] <= dist[u] + w on every edge.
-* configs[0] PageRank scale 20: relative L1 <= 1e-5 against fp64, mass ~1.
+* configs[0] PageRank scale 20: relative L1 <= 1e-5 against fp64, mass ~1; the
+  same at scale 23 (the SURVEY 8(d) roofline target graph).
 * configs[3] CF: at 1/8 of the BASELINE user count, RMSE per iteration within
   1e-4 (relative) of the fp64 oracle while finite; at the full BASELINE shape the
   divergence of the reference update is reported: both
@@ -79,6 +80,22 @@ def test_config0_pagerank_scale20(gm, orc):
     assert [x.active_before for x in st] == [t[1] for t in wst]
     assert [x.messages_generated for x in st] == [t[2] for t in wst]
     # fp32 runs are bitwise reproducible (fixed reduction trees)
+    r2, _ = gm.pagerank(g, 0.85, 20)
+    assert np.array_equal(r.view(np.uint32), r2.view(np.uint32))
+
+
+def test_pagerank_scale23_roofline_target(gm, orc):
+    """The SURVEY 8(d) roofline target graph (directed R-MAT scale 23, the hub
+    kernel of the bench's pagerank23 line): relative L1 <= 1e-5 against the
+    fp64 restatement after 20 supersteps, mass ~1, bitwise reproducible."""
+    g = gm.Graph.rmat(23, 16, seed=1, relabel=True)
+    n = 1 << 23
+    s, d, _ = g.edges()
+    r, st = gm.pagerank(g, 0.85, 20)
+    want, _ = orc.pagerank_norm(n, s, d, 0.85, 20)
+    err = float(np.abs(r.astype(np.float64) - want).sum() / np.abs(want).sum())
+    assert err <= 1e-5, err
+    assert abs(float(r.sum(dtype=np.float64)) - 1.0) < 1e-4
     r2, _ = gm.pagerank(g, 0.85, 20)
     assert np.array_equal(r.view(np.uint32), r2.view(np.uint32))
 

@@ -429,6 +429,23 @@ def test_bfs_level_stamps_wrap(gm, orc, monkeypatch):
         assert _stats_key(st) == wst, rep
 
 
+@pytest.mark.parametrize("sym", [False, True])
+def test_bfs_budget_and_directed(gm, orc, sym):
+    """gm_bfs with a superstep budget (levels beyond it stay -1; the stamps'
+    depth bound follows the budget) and on a directed relabeled graph (no
+    isolated-tail shortcut: the generic output pass), both against the
+    reference semantics."""
+    g = gm.Graph.rmat(14, 16, seed=21, symmetrize=sym, relabel=True)
+    s, d, _ = g.edges()
+    n = g.num_vertices
+    root = g.pick_source(21)
+    for budget in (1, 2, 3, None):
+        lvl, st = gm.bfs(g, root, budget)
+        want, wst = orc.bfs(n, s, d, root, max_iters=budget, presorted=True)
+        assert np.array_equal(lvl, want), budget
+        assert _stats_key(st) == wst, budget
+
+
 @pytest.mark.parametrize("n", [1, 31, 1000, 1023, 1025, 3001])
 def test_bfs_output_ragged_sizes(gm, orc, n):
     """The compact output pass walks callers in blocks of 1024 (a warp per

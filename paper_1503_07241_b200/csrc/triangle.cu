@@ -93,6 +93,139 @@ __global__ void k_tc_low(const uint64_t* keys, uint64_t m, uint64_t mask, uint32
     out[i] = uint32_t(keys[i] & mask);
 }
 
+
+// Triangle listing over CSR+ (rows = lower-rank endpoint u, N+(u) ascending):
+// every triangle u < v < x (rank order) is found once, as x in N+(u) & N+(v)
+// for v in N+(u).  The work is the wedge count W = sum over (u, v) of |N+(v)|
+// (4.4e9 at scale 20), so the membership test must be cheap: N+(u) goes into
+// a shared-memory hash set (open addressing, x + 1 stored, 0 = empty; at
+// least twice as many slots as entries) and every lane probes the set for
+// the x it loaded from N+(v) -- ~1-2 shared reads per wedge instead of a
+// binary search with a dependent global load per step.  Two kernels by
+// |N+(u)|: a warp per u with a warp-private 256-slot table (|N+(u)| <= 128),
+// and a CTA per u with a table of up to kTcBigSlots slots; both claim their
+// u's from a counter.  Longer lists (rare under the degree orientation: 666
+// at scale 20) fall back to a binary search of N+(u) in global memory.
+// kLocal credits each triangle to its largest caller id.
+// Most probes miss (wedges that close no triangle), so a direct-mapped bit
+// filter of N+(u) in front of the table answers them with one shared load
+// and no probe loop (ncu of the table-only version: 120 instructions per 32
+// wedges, stalled on the probe loop's dependent compares and branches).
+constexpr unsigned kTcSmallMax = 128, kTcSmallSlots = 512, kTcSmallFilter = 128;  // words
+constexpr unsigned kTcBigSlots = 16384;                                         // 64 KB
+constexpr unsigned kTcBigFilter = 2048;                                          // 8 KB
+constexpr unsigned kTcBigMax = kTcBigSlots / 4;
+
+__device__ __forceinline__ uint32_t tc_hash(uint32_t x, uint32_t mask) {
+  return (x * 0x9E3779B1u >> 7) & mask;
+}
+__device__ __forceinline__ uint32_t tc_fbit(uint32_t x) { return x * 0x85EBCA6Bu >> 11; }
+
+__device__ __forceinline__ void tc_insert(uint32_t* tab, uint32_t mask, uint32_t* filt,
+                                          uint32_t fmask, uint32_t x) {
+  uint32_t h = tc_hash(x, mask);
+  while (atomicCAS(&tab[h], 0u, x + 1u) != 0u) h = (h + 1) & mask;
+  const uint32_t b = tc_fbit(x);
+  atomicOr(&filt[(b >> 5) & fmask], 1u << (b & 31u));
+}
+
+__device__ __forceinline__ bool tc_member(const uint32_t* tab, uint32_t mask, const uint32_t* filt,
+                                          uint32_t fmask, uint32_t x) {
+  const uint32_t b = tc_fbit(x);
+  if (!((filt[(b >> 5) & fmask] >> (b & 31u)) & 1u)) return false;
+  uint32_t h = tc_hash(x, mask);
+  for (;;) {
+    const uint32_t t = tab[h];
+    if (t == x + 1u) return true;
+    if (t == 0u) return false;
+    h = (h + 1) & mask;
+  }
+}
+
+template <bool kLocal>
+__device__ __forceinline__ void tc_credit(uint32_t u, uint32_t v, uint32_t x, const uint32_t* iperm,
+                                          unsigned long long* local) {
+  if constexpr (kLocal) {
+    const uint32_t cu = iperm ? iperm[u] : u, cv = iperm ? iperm[v] : v, cx = iperm ? iperm[x] : x;
+    atomicAdd(&local[max(cu, max(cv, cx))], 1ull);
+  }
+}
+
+// Probe N+(v) = pi[vb, ve) against the hash set: lane takes entries lane,
+// lane + step, ...; four entries' loads in flight per round (one load per
+// probe round had left the probes waiting on global latency).
+template <bool kLocal>
+__device__ __forceinline__ void tc_probe_list(const uint32_t* __restrict__ pi, uint64_t vb,
+                                              uint64_t ve, unsigned lane, unsigned step,
+                                              const uint32_t* tab, uint32_t mask,
+                                              const uint32_t* filt, uint32_t fmask, uint32_t u,
+                                              uint32_t v, const uint32_t* iperm,
+                                              unsigned long long* local, unsigned long long& mine) {
+  for (uint64_t k0 = vb + lane; k0 < ve; k0 += 4 * step) {
+    uint32_t x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = k0 + q * step < ve ? __ldg(&pi[k0 + q * step]) : ~0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (x[q] != ~0u && tc_member(tab, mask, filt, fmask, x[q])) {
+        ++mine;
+        tc_credit<kLocal>(u, v, x[q], iperm, local);
+      }
+    }
+  }
+}
+
+// A warp per u with 2 <= |N+(u)| <= kTcSmallMax.
+template <bool kLocal>
+__global__ void __launch_bounds__(kTcThreads) k_tc_small(const uint64_t* __restrict__ pp,
+                                                         const uint32_t* __restrict__ pi, uint64_t n,
+                                                         unsigned* claim, const uint32_t* iperm,
+                                                         unsigned long long* local,
+                                                         unsigned long long* total) {
+  __shared__ uint32_t s_tab[kTcThreads / 32][kTcSmallSlots];
+  __shared__ uint32_t s_filt[kTcThreads / 32][kTcSmallFilter];
+  const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  uint32_t* tab = s_tab[w];
+  uint32_t* filt = s_filt[w];
+  constexpr uint32_t mask = kTcSmallSlots - 1, fmask = kTcSmallFilter - 1;
+  for (unsigned i = lane; i < kTcSmallSlots; i += 32) tab[i] = 0u;
+  for (unsigned i = lane; i < kTcSmallFilter; i += 32) filt[i] = 0u;
+  __syncwarp();
+  unsigned long long mine = 0;
+  constexpr unsigned kStep = 32;  // u's per claim
+  for (;;) {
+    uint64_t u0 = 0;
+    if (lane == 0) u0 = uint64_t(atomicAdd(claim, kStep)) ;
+    u0 = __shfl_sync(0xffffffffu, u0, 0);
+    if (u0 >= n) break;
+    for (uint64_t u = u0; u < min(n, u0 + kStep); ++u) {
+      const uint64_t ub = pp[u];
+      const uint32_t nu = uint32_t(pp[u + 1] - ub);
+      if (nu < 2 || nu > kTcSmallMax) continue;
+      for (uint32_t j = lane; j < nu; j += 32) tc_insert(tab, mask, filt, fmask, __ldg(&pi[ub + j]));
+      __syncwarp();
+      for (uint32_t j = 0; j < nu; ++j) {
+        const uint32_t v = __ldg(&pi[ub + j]);
+        const uint64_t vb = pp[v], ve = pp[v + 1];
+        tc_probe_list<kLocal>(pi, vb, ve, lane, 32, tab, mask, filt, fmask, uint32_t(u), v, iperm, local,
+                              mine);
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < nu; j += 32) {  // clear the slots and bits this u used
+        const uint32_t x = __ldg(&pi[ub + j]);
+        uint32_t h = tc_hash(x, mask);
+        while (tab[h] != x + 1u) h = (h + 1) & mask;
+        tab[h] = 0u;
+        filt[(tc_fbit(x) >> 5) & fmask] = 0u;
+      }
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if (lane == 0 && mine) atomicAdd(total, mine);
+}
+
 // First position in b[0, nb) with b >= x (b ascending).
 __device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ b, uint32_t nb,
                                                 uint32_t x) {
@@ -107,44 +240,80 @@ __device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ b, 
   return l;
 }
 
-// Triangle listing over CSR+ (rows = lower-rank endpoint, ascending ids).
-// kLocal credits each triangle to its largest caller id.
+// A CTA per u with |N+(u)| > kTcSmallMax: the table sized to >= 2 |N+(u)|
+// slots (power of two); lists above kTcBigMax search N+(u) in global memory.
+// The u's with long lists (|N+(u)| > kTcSmallMax), for k_tc_big to claim.
+__global__ void k_tc_biglist(const uint64_t* pp, uint64_t n, uint32_t* list, unsigned* cnt) {
+  for (uint64_t u0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; u0 < n;
+       u0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t u = u0 + (threadIdx.x & 31u);
+    const bool big = u < n && pp[u + 1] - pp[u] > kTcSmallMax;
+    const unsigned b = __ballot_sync(0xffffffffu, big);
+    if (!b) continue;
+    unsigned base = 0;
+    if ((threadIdx.x & 31u) == 0) base = atomicAdd(cnt, unsigned(__popc(b)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (big) list[base + __popc(b & ((1u << (threadIdx.x & 31u)) - 1u))] = uint32_t(u);
+  }
+}
+
 template <bool kLocal>
-__global__ void __launch_bounds__(kTcThreads) k_tc_list(const uint64_t* __restrict__ pp,
-                                                        const uint32_t* __restrict__ pi,
-                                                        uint64_t n, const uint32_t* iperm,
-                                                        unsigned long long* local,
-                                                        unsigned long long* total) {
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned lane = threadIdx.x & 31u;
+__global__ void __launch_bounds__(kTcThreads) k_tc_big(const uint64_t* __restrict__ pp,
+                                                       const uint32_t* __restrict__ pi,
+                                                       const uint32_t* __restrict__ list,
+                                                       const unsigned* nlist, unsigned* claim,
+                                                       const uint32_t* iperm,
+                                                       unsigned long long* local,
+                                                       unsigned long long* total) {
+  extern __shared__ uint32_t s_big[];  // kTcBigSlots table words, then kTcBigFilter filter words
+  uint32_t* s_filt = s_big + kTcBigSlots;
+  __shared__ uint64_t s_u;
+  const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  constexpr unsigned kWarps = kTcThreads / 32;
   unsigned long long mine = 0;
-  for (uint64_t u = warp; u < n; u += nwarps) {
+  for (unsigned i = threadIdx.x; i < kTcBigSlots + kTcBigFilter; i += kTcThreads) s_big[i] = 0u;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned i = atomicAdd(claim, 1u);
+      s_u = i < *nlist ? uint64_t(list[i]) : ~0ull;
+    }
+    __syncthreads();
+    const uint64_t u = s_u;
+    if (u == ~0ull) break;
     const uint64_t ub = pp[u];
     const uint32_t nu = uint32_t(pp[u + 1] - ub);
-    if (nu < 2) continue;
-    const uint32_t* U = pi + ub;
-    for (uint32_t j = lane; j < nu; j += 32) {
-      const uint32_t v = __ldg(&U[j]);
+    const bool in_smem = nu <= kTcBigMax;
+    uint32_t slots = 512, fwords = 128;
+    while (slots < 4 * nu && slots < kTcBigSlots) slots <<= 1;
+    while (fwords * 32 < 16 * nu && fwords < kTcBigFilter) fwords <<= 1;
+    const uint32_t mask = slots - 1, fmask = fwords - 1;
+    if (in_smem) {
+      for (uint32_t j = threadIdx.x; j < nu; j += kTcThreads)
+        tc_insert(s_big, mask, s_filt, fmask, __ldg(&pi[ub + j]));
+    }
+    __syncthreads();
+    for (uint32_t j = w; j < nu; j += kWarps) {
+      const uint32_t v = __ldg(&pi[ub + j]);
       const uint64_t vb = pp[v], ve = pp[v + 1];
-      uint32_t lo = 0;  // x ascending: the search window only moves right
-      for (uint64_t k = vb; k < ve && lo < nu; ++k) {
-        const uint32_t x = __ldg(&pi[k]);
-        const uint32_t pos = lo + lower_bound(U + lo, nu - lo, x);
-        if (pos < nu && __ldg(&U[pos]) == x) {
-          ++mine;
-          if (kLocal) {
-            const uint32_t cu = iperm ? iperm[u] : uint32_t(u);
-            const uint32_t cv = iperm ? iperm[v] : v;
-            const uint32_t cx = iperm ? iperm[x] : x;
-            const uint32_t top = max(cu, max(cv, cx));
-            atomicAdd(&local[top], 1ull);
+      if (in_smem) {
+        tc_probe_list<kLocal>(pi, vb, ve, lane, 32, s_big, mask, s_filt, fmask, uint32_t(u), v, iperm,
+                              local, mine);
+      } else {
+        for (uint64_t k = vb + lane; k < ve; k += 32) {
+          const uint32_t x = __ldg(&pi[k]);
+          const uint32_t pos = lower_bound(pi + ub, nu, x);
+          if (pos < nu && __ldg(&pi[ub + pos]) == x) {
+            ++mine;
+            tc_credit<kLocal>(uint32_t(u), v, x, iperm, local);
           }
-          lo = pos + 1;
-        } else {
-          lo = pos;
         }
       }
+    }
+    __syncthreads();
+    if (in_smem) {
+      for (uint32_t i = threadIdx.x; i < slots; i += kTcThreads) s_big[i] = 0u;
+      for (uint32_t i = threadIdx.x; i < fwords; i += kTcThreads) s_filt[i] = 0u;
     }
   }
 #pragma unroll
@@ -208,13 +377,25 @@ uint64_t triangle_count(Graph& g, uint64_t* local_host) {
     k_tc_low<<<grid_for(m, 256), 256, 0, s>>>(keys.get(), m, (uint64_t(1) << nb) - 1, pi.get());
     GM_LAUNCH_CHECK();
     keys.reset();
-    // Phase 2: list every triangle once.
-    if (local_host)
-      k_tc_list<true><<<wgrid, kTcThreads, 0, s>>>(pp.get(), pi.get(), n, iperm, local.get(),
-                                                   ctr.get() + 1);
-    else
-      k_tc_list<false><<<wgrid, kTcThreads, 0, s>>>(pp.get(), pi.get(), n, iperm, nullptr,
-                                                    ctr.get() + 1);
+    // Phase 2: list every triangle once (short lists: a warp per u; long
+    // lists: a CTA per u), u's claimed from counters.
+    DevBuf<unsigned> claims(3, s);
+    claims.zero(s);
+    DevBuf<uint32_t> biglist(n + 1, s);
+    k_tc_biglist<<<grid_for(n, 256), 256, 0, s>>>(pp.get(), n, biglist.get(), claims.get() + 2);
+    GM_LAUNCH_CHECK();
+    int dev = 0, sms = 0;
+    GM_CUDA(cudaGetDevice(&dev));
+    GM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t big_smem = (kTcBigSlots + kTcBigFilter) * 4;
+    auto big = local_host ? k_tc_big<true> : k_tc_big<false>;
+    GM_CUDA(cudaFuncSetAttribute(big, cudaFuncAttributeMaxDynamicSharedMemorySize, int(big_smem)));
+    (local_host ? k_tc_small<true> : k_tc_small<false>)<<<unsigned(sms) * 8, kTcThreads, 0, s>>>(
+        pp.get(), pi.get(), n, claims.get(), iperm, local.get(), ctr.get() + 1);
+    GM_LAUNCH_CHECK();
+    big<<<unsigned(sms) * 3, kTcThreads, big_smem, s>>>(pp.get(), pi.get(), biglist.get(),
+                                                        claims.get() + 2, claims.get() + 1, iperm,
+                                                        local.get(), ctr.get() + 1);
     GM_LAUNCH_CHECK();
   }
   unsigned long long total = 0;

@@ -152,8 +152,9 @@ __device__ __forceinline__ void tc_credit(uint32_t u, uint32_t v, uint32_t x, co
 }
 
 // Probe N+(v) = pi[vb, ve) against the hash set: lane takes entries lane,
-// lane + step, ...; four entries' loads in flight per round (one load per
+// lane + step, ...; kTcRound entries' loads in flight per round (one load per
 // probe round had left the probes waiting on global latency).
+constexpr int kTcRound = 8;
 template <bool kLocal>
 __device__ __forceinline__ void tc_probe_list(const uint32_t* __restrict__ pi, uint64_t vb,
                                               uint64_t ve, unsigned lane, unsigned step,
@@ -161,12 +162,14 @@ __device__ __forceinline__ void tc_probe_list(const uint32_t* __restrict__ pi, u
                                               const uint32_t* filt, uint32_t fmask, uint32_t u,
                                               uint32_t v, const uint32_t* iperm,
                                               unsigned long long* local, unsigned long long& mine) {
-  for (uint64_t k0 = vb + lane; k0 < ve; k0 += 4 * step) {
-    uint32_t x[4];
+  const uint32_t* __restrict__ lst = pi + vb;  // 32-bit indexing inside the list
+  const uint32_t len = uint32_t(ve - vb);
+  for (uint32_t k0 = lane; k0 < len; k0 += kTcRound * step) {
+    uint32_t x[kTcRound];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) x[q] = k0 + q * step < ve ? __ldg(&pi[k0 + q * step]) : ~0u;
+    for (int q = 0; q < kTcRound; ++q) x[q] = k0 + q * step < len ? __ldg(&lst[k0 + q * step]) : ~0u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kTcRound; ++q) {
       if (x[q] != ~0u && tc_member(tab, mask, filt, fmask, x[q])) {
         ++mine;
         tc_credit<kLocal>(u, v, x[q], iperm, local);

@@ -11,7 +11,7 @@ timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/${tag}_gpu_tests.log 
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/${tag}_smoke.log
 timeout 1200 python bench.py > gpurun_out/${tag}_bench_bfs28.json 2> gpurun_out/${tag}_bench_bfs28.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${tag}_bench_reference.json 2> gpurun_out/${tag}_bench_reference.err
-for w in bfs pagerank pagerank23 pagerank28 sssp cf; do
+for w in bfs pagerank pagerank23 pagerank28 sssp cf tc; do
   timeout 900 python bench.py --workload $w --no-cpu-baseline > gpurun_out/${tag}_bench_$w.json 2> gpurun_out/${tag}_bench_$w.err
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \

@@ -324,15 +324,25 @@ __device__ __forceinline__ void warp_enqueue_multi(unsigned mask, const uint32_t
 }
 
 // ------------------------------------------------------------- control
-__global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint64_t words, uint64_t root_ext,
-                           const uint32_t* perm, uint32_t* q1, uint64_t* offs1, uint64_t* qe1,
-                           const uint64_t* out_ptr, const uint32_t* deg, uint32_t* level,
-                           uint32_t lbase, uint64_t n, uint64_t m, uint64_t nv, int32_t max_it) {
+// Also clears both frontier bitmaps and the control block's counters (three
+// memsets per BFS before: stream operations that cost more than their bytes
+// on small graphs).
+__global__ void k_bfs_init(Ctl* ctl, uint32_t* vis, uint32_t* fb0, uint32_t* fb1, uint64_t words,
+                           uint64_t root_ext, const uint32_t* perm, uint32_t* q1, uint64_t* offs1,
+                           uint64_t* qe1, const uint64_t* out_ptr, const uint32_t* deg,
+                           uint32_t* level, uint32_t lbase, uint64_t n, uint64_t m, uint64_t nv,
+                           int32_t max_it) {
   const uint32_t root = perm ? perm[root_ext] : uint32_t(root_ext);
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words;
-       i += uint64_t(gridDim.x) * blockDim.x)
+       i += uint64_t(gridDim.x) * blockDim.x) {
     vis[i] = (i == (root >> 5)) ? (1u << (root & 31u)) : 0u;
+    fb0[i] = 0u;
+    fb1[i] = 0u;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    static_assert(offsetof(Ctl, t_start) % 8 == 0, "control block counters are 8-byte words");
+    for (size_t b = 0; b < offsetof(Ctl, t_start); b += 8)
+      *reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctl) + b) = 0ull;
     q1[0] = root;
     offs1[0] = 0;
     offs1[1] = deg[root];
@@ -1673,9 +1683,6 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   const uint32_t* perm = g.relabeled ? g.perm.get() : nullptr;
   const int32_t max_it = int32_t(std::min<int64_t>(max_iters, 0x7FFFFFFF));
   Ctl* ctl = c.ctl.get();
-  GM_CUDA(cudaMemsetAsync(ctl, 0, offsetof(Ctl, t_start), s));
-  GM_CUDA(cudaMemsetAsync(c.fb[0].get(), 0, (words + 1) * 4, s));
-  GM_CUDA(cudaMemsetAsync(c.fb[1].get(), 0, (words + 1) * 4, s));
   // level stamps of this BFS lie in [lbase, lbase + depth bound]
   const uint64_t depth_bound = std::min<uint64_t>(uint64_t(std::max(max_it, 0)), nv) + 1;
   if (c.lbase == 0 || c.lbase + depth_bound > 0xFFFFFFFFull) {
@@ -1688,10 +1695,11 @@ std::vector<gm_iteration_stats> bfs(Graph& g, uint64_t root, int64_t max_iters, 
   }
   const uint32_t lbase = uint32_t(c.lbase);
   c.lbase += depth_bound;
-  k_bfs_init<<<grid_for(words + 1, 256), 256, 0, s>>>(ctl, c.vis.get(), words + 1, root, perm,
-                                                      c.q[1].get(), c.offs[1].get(), c.qe[1].get(),
-                                                      fw.ptr.get(), g.outdeg.get(), c.level.get(),
-                                                      lbase, n, g.m, nv, max_it);
+  k_bfs_init<<<grid_for(words + 1, 256), 256, 0, s>>>(ctl, c.vis.get(), c.fb[0].get(), c.fb[1].get(),
+                                                      words + 1, root, perm, c.q[1].get(),
+                                                      c.offs[1].get(), c.qe[1].get(), fw.ptr.get(),
+                                                      g.outdeg.get(), c.level.get(), lbase, n, g.m,
+                                                      nv, max_it);
   GM_LAUNCH_CHECK();
   CoopArgs a{};
   a.ctl = ctl;

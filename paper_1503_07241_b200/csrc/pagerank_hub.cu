@@ -97,6 +97,7 @@ struct PrHubCache {
   DevBuf<float> dang;        // [max(grid + n_multi, kInitBlocks)]
   DevBuf<float> dang_chunk;  // per chunk
   DevBuf<float> scalars;
+  DevBuf<unsigned> base_ticket;
   DevBuf<unsigned long long> ctr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   ~PrHubCache() {
@@ -153,10 +154,13 @@ struct HubArgs {
   float* rank_next;
   float* xrow_next;
   float* xhub_next;
-  const float* scalars;
+  float* scalars;  // [0] = this superstep's base (the last CTA writes the next one)
   float damping;
   float* dang_chunk;  // per chunk
   float* dang;        // [grid] per CTA, then [n_multi] split rows
+  unsigned* base_ticket;  // CTAs done this superstep (the last computes the next base)
+  uint32_t n_multi;
+  uint64_t n;
 };
 
 struct Epi {
@@ -212,6 +216,26 @@ __device__ __forceinline__ float piece_sum_of(const uint32_t* __restrict__ col, 
     for (int u = 0; u < kWIPT; ++u) v[u] = vn[u];
   }
   return warp_sum(acc);
+}
+
+// Fixed-order sum of the dangling partials by a CTA of 1024 threads (k_hub_base,
+// or the last CTA of k_pr_hub): thread t sums partials t, t + 1024, ..., then
+// a warp tree and a tree over the 32 warps.
+__device__ __forceinline__ void base_from_partials(const float* partial, uint32_t np, uint64_t n,
+                                                   float damping, float* scalars) {
+  __shared__ float red[32];
+  float s = 0.0f;
+  for (uint32_t i = threadIdx.x; i < np; i += 1024) s += __ldcg(&partial[i]);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = warp_sum(red[threadIdx.x]);
+    if (threadIdx.x == 0) {
+      const float nf = float(n), d = damping;
+      scalars[0] = (1.0f - d) / nf + d * s / nf;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
@@ -356,24 +380,28 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_pr_hub(const HubArgs a) {
     t = warp_sum(t);
     if (lane == 0) a.dang[blockIdx.x] = t;
   }
+  // The last CTA to finish turns the partials into the next superstep's base
+  // (the work of k_hub_base, same fixed-order sum, so the same bits): one
+  // launch per superstep fewer (every CTA captured this superstep's base
+  // when it started, so overwriting it now is safe).
+  __shared__ bool s_last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.base_ticket, 1u) == G - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    base_from_partials(a.dang, G + a.n_multi, a.n, a.damping, a.scalars);
+    if (tid == 0) *a.base_ticket = 0;
+  }
 }
 
-// base = (1-d)/N + d*D/N from fixed-order partials (one CTA).
+// base = (1-d)/N + d*D/N from fixed-order partials (one CTA of 1024 threads).
 __global__ void __launch_bounds__(1024) k_hub_base(const float* partial, uint32_t np, uint64_t n,
                                                    double damping, float* scalars) {
-  __shared__ float red[32];
-  float s = 0.0f;
-  for (uint32_t i = threadIdx.x; i < np; i += 1024) s += partial[i];
-  s = warp_sum(s);
-  if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    s = warp_sum(red[threadIdx.x]);
-    if (threadIdx.x == 0) {
-      const float nf = float(n), d = float(damping);
-      scalars[0] = (1.0f - d) / nf + d * s / nf;
-    }
-  }
+  base_from_partials(partial, np, n, float(damping), scalars);
 }
 
 // Initial state: rank 1/N at every vertex position (0 at pads), x = rank/outdeg,
@@ -685,6 +713,8 @@ PrHubCache& hub_cache(Graph& g) {
   }
   c.dang.alloc(std::max<uint64_t>(kInitBlocks, uint64_t(c.grid) + c.n_multi) + 1, s);
   c.scalars.alloc(4, s);
+  c.base_ticket.alloc(1, s);
+  c.base_ticket.zero(s);
   c.ctr.alloc(4, s);
   GM_CUDA(cudaEventCreate(&c.e0));
   GM_CUDA(cudaEventCreate(&c.e1));
@@ -754,11 +784,12 @@ std::vector<gm_iteration_stats> pagerank_hub(Graph& g, double damping, int64_t i
     a.damping = d;
     a.dang_chunk = c.dang_chunk.get();
     a.dang = c.dang.get();
+    a.base_ticket = c.base_ticket.get();
+    a.n_multi = c.n_multi;
+    a.n = n;
     g.ktimer.begin(s, "k_pr_hub");
     k_pr_hub<<<c.grid, kHubThreads, size_t(c.H) * 4, s>>>(a);
     g.ktimer.end(s);
-    GM_LAUNCH_CHECK();
-    k_hub_base<<<1, 1024, 0, s>>>(c.dang.get(), c.grid + c.n_multi, n, damping, c.scalars.get());
     GM_LAUNCH_CHECK();
     cur ^= 1;
     if (!collect) continue;

@@ -363,7 +363,7 @@ __global__ void k_cf_apply(uint64_t lo, uint64_t n, int kr, const uint32_t* rit,
                            float gamma, float lambda, uint32_t* vbits,
                            unsigned long long* changed) {
   const int k = K > 0 ? K : kr;
-  unsigned long long ch = 0;
+  (void)changed;  // counted by k_cf_count_bits from vbits
   const uint64_t total = n * uint64_t(k);
   const unsigned lane = threadIdx.x & 31u;
   // warp-uniform trip count (the change claim below is warp-collective)
@@ -374,9 +374,10 @@ __global__ void k_cf_apply(uint64_t lo, uint64_t n, int kr, const uint32_t* rit,
     uint64_t v = ~0ull;
     int i = 0;
     if (valid) {
+      constexpr uint32_t KD = K > 0 ? uint32_t(K) : 1u;  // (K == 0 never takes this branch)
       if (K > 0 && t < (1ull << 32)) {
-        v = uint32_t(t) / uint32_t(K);
-        i = int(uint32_t(t) - uint32_t(v) * uint32_t(K));
+        v = uint32_t(t) / KD;
+        i = int(uint32_t(t) - uint32_t(v) * KD);
       } else {
         v = t / uint64_t(k);
         i = int(t % uint64_t(k));
@@ -410,12 +411,20 @@ __global__ void k_cf_apply(uint64_t lo, uint64_t n, int kr, const uint32_t* rit,
     // one atomic per vertex and warp instead of one per changed component.
     const unsigned same = __match_any_sync(0xffffffffu, v);
     const unsigned cm = __ballot_sync(0xffffffffu, changed_here) & same;
-    if (changed_here && lane == unsigned(__ffs(cm) - 1)) {
-      const uint32_t bit = 1u << (v & 31u);
-      ch += !(atomicOr(&vbits[v >> 5], bit) & bit);
-    }
+    if (changed_here && lane == unsigned(__ffs(cm) - 1))
+      atomicOr(&vbits[v >> 5], 1u << (v & 31u));  // no return value: a fire-and-forget RED
   }
-  warp_add_u64(changed, ch);
+}
+
+// vertices_updated of an apply: the set bits of its changed-vertex bitmap
+// (counted here so the apply's claims need no atomic return value -- a round
+// trip per claim in every apply warp step).
+__global__ void k_cf_count_bits(const uint32_t* vbits, uint64_t words, unsigned long long* changed) {
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    c += __popc(vbits[i]);
+  warp_add_u64(changed, c);
 }
 
 // Sum of the per-item squared errors in a fixed order: kSqBlocks contiguous
@@ -583,6 +592,8 @@ void cf_shard_step(Graph& g, uint64_t lo, uint64_t hi, int64_t k, const float* f
                                                     c.rowitem_f.get(), c.part_t.get(), c.part_f.get(),
                                                     f_full, f_block, gamma, lambda, c.vbits.get(),
                                                     upd.get());
+    k_cf_count_bits<<<grid_for((hi - lo + 31) / 32, 256), 256, 0, s>>>(c.vbits.get(), (hi - lo + 31) / 32,
+                                                                          upd.get());
     GM_LAUNCH_CHECK();
   }
   if (c.nit_f) {
@@ -679,6 +690,8 @@ std::vector<gm_iteration_stats> cf(Graph& g, int64_t k, float gamma, float lambd
       (k == 20 ? k_cf_apply<20> : k_cf_apply<0>)<<<grid_for(total, 256), 256, 0, s>>>(0, n, int(k), c.rowitem_t.get(), c.rowitem_f.get(),
                                                       c.part_t.get(), c.part_f.get(), f, fn, gamma,
                                                       lambda, c.vbits.get(), upd.get() + it);
+      k_cf_count_bits<<<grid_for((n + 31) / 32, 256), 256, 0, s>>>(c.vbits.get(), (n + 31) / 32,
+                                                                  upd.get() + it);
     }
     GM_LAUNCH_CHECK();
     GM_CUDA(cudaEventRecord(ev[2 * (it - 1) + 1], s));

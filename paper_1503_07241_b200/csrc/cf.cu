@@ -255,93 +255,6 @@ __global__ void __launch_bounds__(256) k_cf_items_grp(const uint32_t* __restrict
   }
 }
 
-// K = 20, five lanes per group as in k_cf_items_grp, but each group takes five
-// ratings per step and reduces their dot products with a *reduce-scatter*
-// instead of one group tree per rating: lane j holds the partial dots d[u] of
-// its float4 slice for the five ratings u; in rotation r = 1..4 it receives
-// from lane (j + r) mod 5 that lane's partial for rating j, so after four
-// shuffles lane j holds rating j's full dot (summed in a fixed lane rotation:
-// deterministic), computes its error, and five broadcasts hand every lane all
-// five errors for the axpy.  9 shuffles per 30 ratings instead of 4 per 6:
-// the shuffles share the L1TEX data pipe with the factor gathers, which this
-// kernel saturates (§3.4).
-template <typename RT, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_cf_items_rs(const uint32_t* __restrict__ rows,
-                                                     const uint64_t* __restrict__ ibeg,
-                                                     const uint64_t* __restrict__ iend, uint64_t nit,
-                                                     const uint32_t* __restrict__ idx,
-                                                     const uint8_t* __restrict__ val,
-                                                     const float* __restrict__ f,
-                                                     float* __restrict__ part, float* __restrict__ sq) {
-  constexpr int G = 5, NG = 6, U = 5;
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned lane = lane_id();
-  const int grp = int(lane) / G, j = int(lane) % G, base = grp * G;
-  const bool act = grp < NG;
-  const float4* __restrict__ f4 = reinterpret_cast<const float4*>(f);
-  for (uint64_t it = warp; it < nit; it += nwarps) {
-    const uint32_t row = rows[it];
-    const uint64_t b = ibeg[it], e1 = iend[it];
-    const float4 p = act ? f4[uint64_t(row) * G + j] : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float s2 = 0.0f;
-    for (uint64_t e0 = b; e0 < e1; e0 += U * NG) {
-      float4 q[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t e = e0 + uint64_t(u * NG + grp);
-        q[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (act && e < e1) q[u] = f4[uint64_t(__ldg(&idx[e])) * G + j];
-      }
-      const uint64_t eo = e0 + uint64_t(j * NG + grp);  // this lane's own rating (u = j)
-      const bool own = act && eo < e1;
-      const float rv = own ? rating_at<RT>(val, eo) : 0.0f;
-      float d[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) d[u] = p.x * q[u].x + p.y * q[u].y + p.z * q[u].z + p.w * q[u].w;
-      auto pick = [&](int i) {
-        float v = d[0];
-#pragma unroll
-        for (int u = 1; u < U; ++u) v = i == u ? d[u] : v;
-        return v;
-      };
-      float dot = pick(j);
-#pragma unroll
-      for (int r = 1; r < G; ++r) {
-        const int from = j + r < G ? j + r : j + r - G;   // lane whose partial of rating j arrives
-        const int send = j - r >= 0 ? j - r : j - r + G;  // the rating this lane's partial goes to
-        dot += __shfl_sync(0xffffffffu, pick(send), (base + from) & 31);
-      }
-      const float err = own ? rv - dot : 0.0f;
-      s2 += err * err;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float eu = __shfl_sync(0xffffffffu, err, (base + u) & 31);
-        acc.x += eu * q[u].x;
-        acc.y += eu * q[u].y;
-        acc.z += eu * q[u].z;
-        acc.w += eu * q[u].w;
-      }
-    }
-    float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int g2 = 0; g2 < NG; ++g2) {
-      const int src = g2 * G + j;
-      tot.x += __shfl_sync(0xffffffffu, acc.x, src);
-      tot.y += __shfl_sync(0xffffffffu, acc.y, src);
-      tot.z += __shfl_sync(0xffffffffu, acc.z, src);
-      tot.w += __shfl_sync(0xffffffffu, acc.w, src);
-    }
-    if (grp == 0) reinterpret_cast<float4*>(part)[it * G + j] = tot;
-    if (sq) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      if (lane == 0) sq[it] = s2;
-    }
-  }
-}
-
 // Generalised group kernel: G lanes per rating (G = 1, 2, 4 or 8), the row's K/4
 // float4 chunks dealt to the group's lanes round-robin (lane j holds chunks j,
 // j + G, ...), so load instruction c of a warp fetches chunks [cG, cG + G) of
@@ -606,9 +519,6 @@ void pass(const CfCache& c, Graph& g, bool fwd, const float* f, int k, float* sq
                                        csr.val.get(), f, fwd ? c.part_f.get() : c.part_t.get(), sq);
     };
     switch (grp_lanes) {
-      case 50: args(k_cf_items_rs<RT, 1>); break;
-      case 51: args(k_cf_items_rs<RT, 3>); break;
-      case 52: args(k_cf_items_rs<RT, 4>); break;
       case 1: args(k_cf_items_g<20, 1, 2, RT>); break;
       case 2: args(k_cf_items_g<20, 2, 2, RT>); break;
       case 3: args(k_cf_items_g<20, 2, 4, RT>); break;

@@ -187,8 +187,8 @@ __device__ __forceinline__ float group_sum(float v, int base) {
   }
 }
 
-template <int K, typename RT>
-__global__ void __launch_bounds__(256) k_cf_items_grp(const uint32_t* __restrict__ rows,
+template <int K, typename RT, int U = 4, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_cf_items_grp(const uint32_t* __restrict__ rows,
                                                       const uint64_t* __restrict__ ibeg,
                                                       const uint64_t* __restrict__ iend, uint64_t nit,
                                                       const uint32_t* __restrict__ idx,
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(256) k_cf_items_grp(const uint32_t* __restrict
     const float4 p = act ? f4[uint64_t(row) * G + j] : make_float4(0.f, 0.f, 0.f, 0.f);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float s2 = 0.0f;
-    constexpr int U = 4;  // warp steps in flight
+    // U: warp steps in flight
     for (uint64_t e0 = b; e0 < e1; e0 += U * NG) {
       float4 q[U];
       float r[U];
@@ -495,7 +495,11 @@ void launch_items_grp(const CfCache& c, const Csr& csr, bool fwd, const float* f
   const uint64_t nit = fwd ? c.nit_f : c.nit_t;
   if (!nit) return;
   const unsigned grid = grid_for(nit * 32, 256);
-  k_cf_items_grp<K, RT><<<grid, 256, 0, s>>>(fwd ? c.items_f.get() : c.items_t.get(),
+  // three warp steps in flight at <= 48 registers (5 CTAs, 40 warps per SM):
+  // the U x occupancy sweep of DESIGN 3.4 (U = 4 at 63-71 registers: 2.21-2.46 ms
+  // per superstep; this: 2.10)
+  auto kern = k_cf_items_grp<K, RT, 3, 5>;
+  kern<<<grid, 256, 0, s>>>(fwd ? c.items_f.get() : c.items_t.get(),
                                              fwd ? c.ibeg_f.get() : c.ibeg_t.get(),
                                              fwd ? c.iend_f.get() : c.iend_t.get(), nit,
                                              csr.idx.get(), csr.val.get(), f,

@@ -167,7 +167,7 @@ GM_API gm_status gm_kernel_timer_stop(gm_graph_t g, double* total_ms, int64_t* l
 #define GM_OUT_HOST 0
 #define GM_OUT_DEVICE 1
 #define GM_OUT_DEVICE_ASYNC 2
-/*   GM_OUT_HOST_ASYNC   (gm_bfs) host memory, pinned by the caller; returns once
+/*   GM_OUT_HOST_ASYNC   host memory, pinned by the caller; returns once
  *                       the run and the copy into it are enqueued: the copy
  *                       runs on a second stream from a double-buffered device
  *                       staging area, so it overlaps the next call's kernels

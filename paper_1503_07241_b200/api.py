@@ -320,7 +320,10 @@ def pagerank(g: Graph, damping=0.85, iterations=20, *, with_stats=True, out=None
         return None, _stats(st, k.value) if with_stats else []
     if out is None:
         out = np.empty(n, np.float32)
-    _check(L.load().gm_pagerank(g._h, C.byref(cfg), out.ctypes.data, 0,
+    # sync=False with a (pinned) host array: GM_OUT_HOST_ASYNC -- the copy
+    # overlaps the next call; g.synchronize() before reading `out`
+    _check(L.load().gm_pagerank(g._h, C.byref(cfg), out.ctypes.data,
+                                0 if sync else _host_async_mode(with_stats),
                                 st if with_stats else None, iterations,
                                 C.byref(k) if with_stats else None))
     return out, _stats(st, k.value) if with_stats else []
@@ -361,7 +364,7 @@ def sssp(g: Graph, source: int, max_iterations=None, *, with_stats=True, out=Non
     else:
         if out is None:
             out = np.empty(n, np.uint32)
-        ptr, on_dev = out.ctypes.data, 0
+        ptr, on_dev = out.ctypes.data, 0 if sync else _host_async_mode(with_stats)
     _check(L.load().gm_sssp(g._h, source, cap, ptr, on_dev, st if with_stats else None,
                             min(cap, 1 << 16), C.byref(k) if with_stats else None))
     return out, _stats(st, k.value) if with_stats else []

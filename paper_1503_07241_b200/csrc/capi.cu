@@ -340,9 +340,20 @@ GM_API gm_status gm_pagerank(gm_graph_t g, const gm_pagerank_config* cfg, float*
                              int64_t* n_stats) {
   return guarded([&] {
     if (!cfg) gm::fail(GM_EUSAGE, "null config");
-    check_out_mode(out_on_device, stats, n_stats);
-    auto st = gm::pagerank(*handle(g), cfg->damping, cfg->iterations, out_rank, out_on_device != 0,
-                           stats != nullptr || n_stats != nullptr, out_on_device == GM_OUT_DEVICE_ASYNC);
+    check_out_mode(out_on_device, stats, n_stats, /*host_async_ok=*/true);
+    gm::Graph& G = *handle(g);
+    if (out_on_device == GM_OUT_HOST_ASYNC && out_rank && G.n) {
+      // the ranks land in a device staging buffer; its copy to the caller's
+      // pinned memory runs on the copy stream while the next call computes
+      float* stage = static_cast<float*>(G.host_async.stage(G.stream, G.n * 4));
+      gm::pagerank(G, cfg->damping, cfg->iterations, stage, true, false, true);
+      G.host_async.issue(G.stream, out_rank, G.n * 4);
+      return;
+    }
+    auto st = gm::pagerank(G, cfg->damping, cfg->iterations,
+                           out_on_device == GM_OUT_HOST_ASYNC ? nullptr : out_rank,
+                           out_on_device != 0, stats != nullptr || n_stats != nullptr,
+                           out_on_device >= GM_OUT_DEVICE_ASYNC);
     copy_stats(st, stats, cap, n_stats);
   });
 }
@@ -364,9 +375,17 @@ GM_API gm_status gm_sssp(gm_graph_t g, uint64_t source, int64_t max_iters, uint3
                          int32_t out_on_device, gm_iteration_stats* stats, int64_t cap,
                          int64_t* n_stats) {
   return guarded([&] {
-    check_out_mode(out_on_device, stats, n_stats);
-    auto st = gm::sssp(*handle(g), source, max_iters, out_dist, out_on_device != 0,
-                       stats != nullptr || n_stats != nullptr, out_on_device == GM_OUT_DEVICE_ASYNC);
+    check_out_mode(out_on_device, stats, n_stats, /*host_async_ok=*/true);
+    gm::Graph& G = *handle(g);
+    if (out_on_device == GM_OUT_HOST_ASYNC && out_dist && G.n) {
+      uint32_t* stage = static_cast<uint32_t*>(G.host_async.stage(G.stream, G.n * 4));
+      gm::sssp(G, source, max_iters, stage, true, false, true);
+      G.host_async.issue(G.stream, out_dist, G.n * 4);
+      return;
+    }
+    auto st = gm::sssp(G, source, max_iters, out_on_device == GM_OUT_HOST_ASYNC ? nullptr : out_dist,
+                       out_on_device != 0, stats != nullptr || n_stats != nullptr,
+                       out_on_device >= GM_OUT_DEVICE_ASYNC);
     copy_stats(st, stats, cap, n_stats);
   });
 }

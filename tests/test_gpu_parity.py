@@ -1202,6 +1202,36 @@ def test_bfs_host_async_output(gm, orc):
         gm.bfs(g, roots[0], out=bufs[0].numpy(), sync=False)  # stats need the host
 
 
+def test_pagerank_sssp_host_async_output(gm, orc):
+    """GM_OUT_HOST_ASYNC for gm_pagerank and gm_sssp: results reach pinned
+    host memory on the copy stream from alternating staging buffers; after
+    synchronize() every call's output equals the synchronous call's bit for
+    bit (several calls in flight, so a staging buffer is reused)."""
+    import torch
+    g = gm.Graph.rmat(14, 16, seed=7, relabel=True)
+    n = g.num_vertices
+    want, _ = gm.pagerank(g, 0.85, 20)
+    iters = [20, 5, 20, 3]
+    bufs = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in iters]
+    for it, b in zip(iters, bufs):
+        gm.pagerank(g, 0.85, it, with_stats=False, out=b.numpy(), sync=False)
+    g.synchronize()
+    for it, b in zip(iters, bufs):
+        assert np.array_equal(b.numpy().view(np.uint32), gm.pagerank(g, 0.85, it)[0].view(np.uint32))
+    assert np.array_equal(bufs[0].numpy().view(np.uint32), want.view(np.uint32))
+    with pytest.raises(ValueError):
+        gm.pagerank(g, 0.85, 20, out=bufs[0].numpy(), sync=False)  # stats need the host
+
+    gw = gm.Graph.rmat(14, 16, seed=7, relabel=True, weights=True)
+    roots = [gw.pick_source(1), gw.pick_source(2), gw.pick_source(3)]
+    dbufs = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in roots]
+    for r, b in zip(roots, dbufs):
+        gm.sssp(gw, r, with_stats=False, out=b.numpy().view(np.uint32), sync=False)
+    gw.synchronize()
+    for r, b in zip(roots, dbufs):
+        assert np.array_equal(b.numpy().view(np.uint32), gm.sssp(gw, r)[0])
+
+
 @pytest.mark.parametrize("ctas,chunk", [("2", None), ("3", None), ("3", "1"), ("3", "32")])
 def test_bfs_coop_variants(gm, orc, ctas, chunk, monkeypatch):
     """Both k_bfs_coop occupancy variants (2 CTAs x 64 registers, 3 CTAs x 40
